@@ -1,0 +1,151 @@
+/*
+ * mpcg.h — C ABI of the B200-native 2PC secret-shared inference engine (libmpcg.so).
+ *
+ * Drop-in boundary for the MPC-Pipe reference's hot path (arXiv 2209.13643). The
+ * reference is a header-only C++ library with no FFI; each entry point below replaces
+ * the reference interface cited beside it (paths relative to
+ * /root/reference/proj/include/mpcpipe). Plain pointers and sizes only; every call
+ * returns an mpcg status code, with the message in mpcg_last_error().
+ *
+ * Status codes mirror the reference exception classes (errors.hpp:8-45):
+ *   RangeError=1 ShapeError=2 ConfigError=3 ProtocolError=4 TransportError=5
+ *   BudgetError=6 UsageError=7, plus CUDA=8, NCCL=9, internal=10.
+ *
+ * A session holds the party slots living in this process on one GPU:
+ *   n_local = 2: both parties of a 2PC pair on `device` (1-GPU mode)
+ *   n_local = 1: party `party` only; connect the peer with mpcg_session_connect_nccl.
+ * Tensors carry one u64 share per local slot (slot-major, row-major Z_2^64 words, i.e.
+ * the RingTensor layout of ring/tensor.hpp:36-76 repeated per slot).
+ * Every op takes the same tag strings as the reference, so the seeded dealer draws the
+ * exact triples the reference draws (sharing/triple.hpp:138-151) and per-party output
+ * shares are word-identical.
+ */
+#ifndef MPCG_H
+#define MPCG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPCG_OK 0
+#define MPCG_ERR_RANGE 1
+#define MPCG_ERR_SHAPE 2
+#define MPCG_ERR_CONFIG 3
+#define MPCG_ERR_PROTOCOL 4
+#define MPCG_ERR_TRANSPORT 5
+#define MPCG_ERR_BUDGET 6
+#define MPCG_ERR_USAGE 7
+#define MPCG_ERR_CUDA 8
+#define MPCG_ERR_NCCL 9
+#define MPCG_ERR_INTERNAL 10
+
+#define MPCG_REDUCE_SUM 0 /* transport/transport.hpp:12 Reduce::Sum */
+#define MPCG_REDUCE_XOR 1 /* Reduce::Xor */
+
+typedef struct mpcg_session mpcg_session;
+typedef struct mpcg_tensor mpcg_tensor;
+typedef struct mpcg_model mpcg_model;
+typedef struct mpcg_executor mpcg_executor;
+
+/* Thread-local message of the last failing call. */
+const char* mpcg_last_error(void);
+int mpcg_version(void);
+/* Number of visible CUDA devices (0 on a host without a GPU). */
+int mpcg_device_count(int* out);
+
+/* ---- session: replaces SessionConfig + SeededDealer + mask CounterRng + Communicator
+ *      (transport/config.hpp:22-39, sharing/triple.hpp:138-151, engine/bench.hpp:39-40,
+ *       transport/transport.hpp:51-82). mask_seed keys CounterRng(mask_seed, party). */
+int mpcg_session_create(int device, int n_local, int party, uint64_t seed, uint64_t mask_seed, int frac_bits,
+                        mpcg_session** out);
+int mpcg_session_destroy(mpcg_session* s);
+/* ProtoCtx knobs (protocols/context.hpp:17-35): chunks, threshold bytes, merged adder. */
+int mpcg_session_set_pipeline(mpcg_session* s, int chunks, uint64_t threshold_bytes, int merged_adder);
+/* Emulated link (transport/config.hpp:41-43, sim.hpp:90-92): bandwidth<=0 disables. */
+int mpcg_session_set_link(mpcg_session* s, double latency_s, double bandwidth_Bps, double sec_per_message);
+/* Data-parallel shard: this pair holds rows [offset, offset+local) of a global batch. */
+int mpcg_session_set_shard(mpcg_session* s, uint64_t local_batch, uint64_t global_batch, uint64_t batch_offset);
+/* NCCL link for n_local == 1 (the socket mesh of transport/socket.hpp:345-402). */
+int mpcg_nccl_unique_id(uint8_t out[128]);
+int mpcg_session_connect_nccl(mpcg_session* s, const uint8_t id[128], int rank);
+int mpcg_session_sync(mpcg_session* s);
+/* CommStats of one local slot (transport/transport.hpp:39-45): bytes, collectives, p2p. */
+int mpcg_session_stats(mpcg_session* s, int slot, uint64_t out[3]);
+int mpcg_session_n_local(mpcg_session* s, int* out);
+int mpcg_session_trace(mpcg_session* s, int enable);
+
+/* ---- tensors (device RingTensor shares; ring/tensor.hpp:36-76) ---- */
+int mpcg_tensor_create(mpcg_session* s, int ndim, const uint64_t* dims, int scale_bits,
+                       const uint64_t* host /* n_local*numel words or NULL */, mpcg_tensor** out);
+int mpcg_tensor_download(mpcg_tensor* t, uint64_t* host /* n_local*numel words */);
+int mpcg_tensor_shape(const mpcg_tensor* t, int* ndim, uint64_t dims[8], int* scale_bits);
+int mpcg_tensor_destroy(mpcg_tensor* t);
+/* deal_input_share (engine/executor.hpp:70-75): CounterRng(seed, 0x11a9) over the global
+ * input; this session keeps rows [batch_offset, batch_offset + dims[0]). */
+int mpcg_deal_input(mpcg_session* s, const double* x_global, int ndim, const uint64_t* global_dims,
+                    uint64_t batch_offset, uint64_t local_batch, uint64_t seed, mpcg_tensor** out);
+
+/* ---- protocol ops (protocols/*.hpp, nonlinear/*.hpp). Each returns a new tensor. ---- */
+/* Communicator::reveal (transport/transport.hpp:76-79): every slot receives the opening. */
+int mpcg_open(mpcg_session* s, const mpcg_tensor* x, int reduce, const char* tag, mpcg_tensor** out);
+int mpcg_beaver_mul(mpcg_session* s, const mpcg_tensor* x, const mpcg_tensor* y, const char* tag, int chunks,
+                    mpcg_tensor** out);                                        /* beaver.hpp:43 */
+int mpcg_beaver_square(mpcg_session* s, const mpcg_tensor* x, const char* tag, int chunks,
+                       mpcg_tensor** out);                                     /* beaver.hpp:88 */
+int mpcg_beaver_and(mpcg_session* s, const mpcg_tensor* x, const mpcg_tensor* y, const char* tag, int chunks,
+                    mpcg_tensor** out);                                        /* beaver.hpp:129 */
+int mpcg_beaver_matmul(mpcg_session* s, const mpcg_tensor* x, const mpcg_tensor* y, int transpose_b,
+                       const char* tag, int chunks, mpcg_tensor** out);        /* beaver.hpp:186 */
+int mpcg_binary_add(mpcg_session* s, const mpcg_tensor* x, const mpcg_tensor* y, int width, int merged,
+                    int chunks, const char* tag, mpcg_tensor** out);           /* adder.hpp:237 */
+int mpcg_a2b(mpcg_session* s, const mpcg_tensor* x, int chunks, const char* tag, mpcg_tensor** out); /* compare.hpp:24 */
+int mpcg_msb(mpcg_session* s, const mpcg_tensor* x, int chunks, const char* tag, mpcg_tensor** out); /* compare.hpp:57 */
+int mpcg_b2a_bit(mpcg_session* s, const mpcg_tensor* b, const char* tag, int chunks,
+                 mpcg_tensor** out);                                           /* compare.hpp:67 */
+int mpcg_less_than(mpcg_session* s, const mpcg_tensor* x, const mpcg_tensor* y, int chunks, const char* tag,
+                   mpcg_tensor** out);                                         /* compare.hpp:87 */
+int mpcg_truncate(mpcg_session* s, const mpcg_tensor* x, int bits, mpcg_tensor** out); /* trunc.hpp:25 */
+int mpcg_relu(mpcg_session* s, const mpcg_tensor* x, const char* tag, mpcg_tensor** out); /* activations.hpp:39 */
+int mpcg_max_last_dim(mpcg_session* s, const mpcg_tensor* x, uint64_t L, const char* tag,
+                      mpcg_tensor** out);                                      /* activations.hpp:51 */
+int mpcg_exp(mpcg_session* s, const mpcg_tensor* x, const char* tag, mpcg_tensor** out); /* approx.hpp:22 */
+int mpcg_reciprocal(mpcg_session* s, const mpcg_tensor* x, const char* tag, mpcg_tensor** out); /* approx.hpp:43 */
+int mpcg_softmax(mpcg_session* s, const mpcg_tensor* x, uint64_t L, const char* tag,
+                 mpcg_tensor** out);                                           /* activations.hpp:93 */
+int mpcg_maxpool2d(mpcg_session* s, const mpcg_tensor* x, uint64_t N, uint64_t C, uint64_t H, uint64_t W,
+                   uint64_t k, uint64_t stride, const char* tag, mpcg_tensor** out); /* activations.hpp:114 */
+
+/* ---- model + executor (engine/model.hpp, engine/executor.hpp:173-205) ---- */
+#define MPCG_LAYER_DENSE 0
+#define MPCG_LAYER_CONV2D 1
+#define MPCG_LAYER_RELU 2
+#define MPCG_LAYER_MAXPOOL2D 3
+#define MPCG_LAYER_FLATTEN 4
+#define MPCG_LAYER_ATTENTION 5
+#define MPCG_LAYER_SOFTMAX 6
+#define MPCG_LAYER_MEANPOOL 7
+int mpcg_model_create(const char* name, int frac_bits, int ndim, const uint64_t* input_dims, mpcg_model** out);
+int mpcg_model_add_layer(mpcg_model* m, const char* name, int kind, uint64_t out, uint64_t kernel,
+                         uint64_t stride, uint64_t pad, uint64_t heads, int bias);
+int mpcg_model_destroy(mpcg_model* m);
+/* ExecOptions (engine/executor.hpp:28-36). */
+int mpcg_executor_create(mpcg_session* s, const mpcg_model* m, int public_weights, int pipelined, int chunks,
+                         uint64_t chunk_threshold, int merged_adder, mpcg_executor** out);
+/* deal_weight_shares / public_weight_set (engine/executor.hpp:49-68). */
+int mpcg_executor_deal_weights(mpcg_executor* e, int count, const char* const* names,
+                               const double* const* values, uint64_t seed);
+int mpcg_executor_run(mpcg_executor* e, const mpcg_tensor* input, mpcg_tensor** out); /* executor.hpp:193 */
+/* Per-layer device times (ms) of the next runs: enable=1 turns timing on. */
+int mpcg_executor_time_layers(mpcg_executor* e, int enable);
+int mpcg_executor_layer_times(mpcg_executor* e, int max, float* ms, int* count);
+int mpcg_executor_destroy(mpcg_executor* e);
+
+/* FNV-1a over little-endian words (engine/report.hpp:18-23). */
+uint64_t mpcg_fnv1a_words(const uint64_t* words, uint64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPCG_H */

@@ -1,0 +1,277 @@
+"""Python mirror of the reference operator API over the C ABI (include/mpcg.h).
+
+Names and argument meaning follow the reference free functions
+(H/protocols/*.hpp, H/nonlinear/*.hpp, H/engine/executor.hpp); each `Tensor` holds the
+shares of every party slot that lives in this process (2 in 1-GPU mode, 1 otherwise),
+so one call runs the op for all local parties. Exceptions mirror H/errors.hpp.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from .model import LAYER_KINDS, ModelGraph
+
+PHI = 0x9E3779B97F4A7C15
+
+
+def _u64p(a: np.ndarray):
+    return a.ctypes.data_as(N.U64P)
+
+
+def _tag(t: str):
+    return t.encode() if t is not None else None
+
+
+class Session:
+    """Local party slots on one GPU: Communicator + SeededDealer + mask rng + ProtoCtx knobs.
+
+    n_local=2 runs both parties of a pair on `device`; n_local=1 runs `party` only and
+    needs `connect_nccl`. mask_seed defaults to the CLI's seed ^ phi (H/engine/bench.hpp:40).
+    """
+
+    def __init__(self, device=0, n_local=2, party=0, seed=1, mask_seed=None, frac_bits=16):
+        if mask_seed is None:
+            mask_seed = seed ^ PHI
+        h = C.c_void_p()
+        N.call("mpcg_session_create", device, n_local, party, seed, mask_seed & ((1 << 64) - 1), frac_bits,
+               C.byref(h))
+        self._h = h
+        self.n_local = n_local
+        self.party = party
+        self.frac_bits = frac_bits
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib().mpcg_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_pipeline(self, chunks=1, threshold=0, merged=True):
+        N.call("mpcg_session_set_pipeline", self._h, chunks, threshold, int(merged))
+
+    def set_link(self, latency_s=0.0, bandwidth_Bps=0.0, sec_per_message=0.0):
+        N.call("mpcg_session_set_link", self._h, latency_s, bandwidth_Bps, sec_per_message)
+
+    def set_shard(self, local_batch, global_batch, batch_offset):
+        N.call("mpcg_session_set_shard", self._h, local_batch, global_batch, batch_offset)
+
+    def connect_nccl(self, unique_id: bytes, rank: int):
+        N.call("mpcg_session_connect_nccl", self._h, unique_id, rank)
+
+    def sync(self):
+        N.call("mpcg_session_sync", self._h)
+
+    def stats(self, slot=0):
+        out = (C.c_uint64 * 3)()
+        N.call("mpcg_session_stats", self._h, slot, out)
+        return {"bytes_sent": out[0], "collectives": out[1], "p2p_sends": out[2]}
+
+    def tensor(self, shares: np.ndarray, scale=0) -> "Tensor":
+        """shares: array [n_local, *shape] of uint64 (slot-major)."""
+        a = np.ascontiguousarray(shares, dtype=np.uint64)
+        if a.shape[0] != self.n_local:
+            raise N.ShapeError(f"expected {self.n_local} share slots, got {a.shape[0]}")
+        shape = a.shape[1:]
+        dims = np.array(shape, dtype=np.uint64)
+        h = C.c_void_p()
+        N.call("mpcg_tensor_create", self._h, len(shape), _u64p(dims), scale, _u64p(a), C.byref(h))
+        return Tensor(self, h)
+
+    def deal_input(self, x_global: np.ndarray, seed: int, batch_offset=0, local_batch=None) -> "Tensor":
+        """deal_input_share (H/engine/executor.hpp:70-75) of rows [off, off+local)."""
+        x = np.ascontiguousarray(x_global, dtype=np.float64)
+        local_batch = x.shape[0] if local_batch is None else local_batch
+        dims = np.array(x.shape, dtype=np.uint64)
+        h = C.c_void_p()
+        N.call("mpcg_deal_input", self._h, x.ctypes.data_as(C.POINTER(C.c_double)), x.ndim, _u64p(dims),
+               batch_offset, local_batch, seed, C.byref(h))
+        return Tensor(self, h)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    N.call("mpcg_nccl_unique_id", buf)
+    return buf.raw
+
+
+class Tensor:
+    """Device shares of every local slot (RingTensor layout, H/ring/tensor.hpp:36-76)."""
+
+    def __init__(self, sess: Session, h):
+        self.sess = sess
+        self._h = h
+
+    def __del__(self):
+        try:
+            if self._h:
+                N.lib().mpcg_tensor_destroy(self._h)
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def meta(self):
+        nd = C.c_int()
+        dims = (C.c_uint64 * 8)()
+        sc = C.c_int()
+        N.call("mpcg_tensor_shape", self._h, C.byref(nd), dims, C.byref(sc))
+        return tuple(dims[i] for i in range(nd.value)), sc.value
+
+    @property
+    def shape(self):
+        return self.meta()[0]
+
+    @property
+    def scale_bits(self):
+        return self.meta()[1]
+
+    def numpy(self) -> np.ndarray:
+        shape = self.shape
+        out = np.empty((self.sess.n_local,) + tuple(shape), dtype=np.uint64)
+        N.call("mpcg_tensor_download", self._h, _u64p(out))
+        return out
+
+
+def _op(name, sess, *args):
+    h = C.c_void_p()
+    N.call(name, sess.handle, *args, C.byref(h))
+    return Tensor(sess, h)
+
+
+# ---- protocol ops (reference names) -----------------------------------------------
+def open_(s, x, kind="sum", tag=""):
+    return _op("mpcg_open", s, x.handle, 1 if kind == "xor" else 0, _tag(tag))
+
+
+def beaver_mul(s, x, y, tag="mul", chunks=1):
+    return _op("mpcg_beaver_mul", s, x.handle, y.handle, _tag(tag), chunks)
+
+
+def beaver_square(s, x, tag="square", chunks=1):
+    return _op("mpcg_beaver_square", s, x.handle, _tag(tag), chunks)
+
+
+def beaver_and(s, x, y, tag="and", chunks=1):
+    return _op("mpcg_beaver_and", s, x.handle, y.handle, _tag(tag), chunks)
+
+
+def beaver_matmul(s, x, y, transpose_b=False, tag="matmul", chunks=1):
+    return _op("mpcg_beaver_matmul", s, x.handle, y.handle, int(transpose_b), _tag(tag), chunks)
+
+
+def binary_add(s, x, y, width=64, merged=True, chunks=1, tag="badd"):
+    return _op("mpcg_binary_add", s, x.handle, y.handle, width, int(merged), chunks, _tag(tag))
+
+
+def a2b(s, x, chunks=1, tag="a2b"):
+    return _op("mpcg_a2b", s, x.handle, chunks, _tag(tag))
+
+
+def msb(s, x, chunks=1, tag="msb"):
+    return _op("mpcg_msb", s, x.handle, chunks, _tag(tag))
+
+
+def b2a_bit(s, b, tag="b2a", chunks=1):
+    return _op("mpcg_b2a_bit", s, b.handle, _tag(tag), chunks)
+
+
+def less_than(s, x, y, chunks=1, tag="lt"):
+    return _op("mpcg_less_than", s, x.handle, y.handle, chunks, _tag(tag))
+
+
+def truncate_shares(s, x, bits):
+    return _op("mpcg_truncate", s, x.handle, bits)
+
+
+def relu_shares(s, x, tag="relu"):
+    return _op("mpcg_relu", s, x.handle, _tag(tag))
+
+
+def max_last_dim(s, x, L, tag="max"):
+    return _op("mpcg_max_last_dim", s, x.handle, L, _tag(tag))
+
+
+def exp_shares(s, x, tag="exp"):
+    return _op("mpcg_exp", s, x.handle, _tag(tag))
+
+
+def reciprocal_shares(s, x, tag="recip"):
+    return _op("mpcg_reciprocal", s, x.handle, _tag(tag))
+
+
+def softmax_shares(s, x, L, tag="softmax"):
+    return _op("mpcg_softmax", s, x.handle, L, _tag(tag))
+
+
+def maxpool2d_shares(s, x, N_, C_, H, W, k, stride, tag="maxpool"):
+    return _op("mpcg_maxpool2d", s, x.handle, N_, C_, H, W, k, stride, _tag(tag))
+
+
+def fnv1a_words(words: np.ndarray) -> int:
+    a = np.ascontiguousarray(words, dtype=np.uint64).reshape(-1)
+    return int(N.lib().mpcg_fnv1a_words(_u64p(a), a.size))
+
+
+# ---- executor ---------------------------------------------------------------------
+class SecureExecutor:
+    """H/engine/executor.hpp:173-205 on the GPU. ExecOptions: pipelined, chunks, threshold."""
+
+    def __init__(self, sess: Session, g: ModelGraph, public_weights=False, pipelined=False, chunks=4,
+                 chunk_threshold=2 << 20, merged_adder=True):
+        mh = C.c_void_p()
+        dims = np.array(g.input, dtype=np.uint64)
+        N.call("mpcg_model_create", g.name.encode(), g.frac_bits, len(g.input), _u64p(dims), C.byref(mh))
+        try:
+            for l in g.layers:
+                N.call("mpcg_model_add_layer", mh, l.name.encode(), LAYER_KINDS[l.type], l.out, l.kernel,
+                       l.stride, l.pad, l.heads, int(l.bias))
+            eh = C.c_void_p()
+            N.call("mpcg_executor_create", sess.handle, mh, int(public_weights), int(pipelined), chunks,
+                   chunk_threshold, int(merged_adder), C.byref(eh))
+        finally:
+            N.lib().mpcg_model_destroy(mh)
+        self._h = eh
+        self.sess = sess
+        self.graph = g
+
+    def __del__(self):
+        try:
+            if self._h:
+                N.lib().mpcg_executor_destroy(self._h)
+        except Exception:
+            pass
+
+    def deal_weights(self, weights: dict, seed: int):
+        names = sorted(weights)
+        arrs = [np.ascontiguousarray(weights[k], dtype=np.float64).reshape(-1) for k in names]
+        cn = (C.c_char_p * len(names))(*[n.encode() for n in names])
+        cv = (C.POINTER(C.c_double) * len(names))(*[a.ctypes.data_as(C.POINTER(C.c_double)) for a in arrs])
+        N.call("mpcg_executor_deal_weights", self._h, len(names), cn, cv, seed)
+
+    def run(self, x: Tensor) -> Tensor:
+        h = C.c_void_p()
+        N.call("mpcg_executor_run", self._h, x.handle, C.byref(h))
+        return Tensor(self.sess, h)
+
+    def time_layers(self, enable=True):
+        N.call("mpcg_executor_time_layers", self._h, int(enable))
+
+    def layer_times(self):
+        buf = (C.c_float * 256)()
+        n = C.c_int()
+        N.call("mpcg_executor_layer_times", self._h, 256, buf, C.byref(n))
+        return [buf[i] for i in range(min(n.value, 256))]

@@ -1,0 +1,404 @@
+// extern "C" boundary of libmpcg.so (declared in include/mpcg.h).
+#include <cstring>
+#include <memory>
+
+#include "../../include/mpcg.h"
+#include "core.hpp"
+#include "executor.hpp"
+
+using namespace mpcg;
+
+namespace mpcg {
+void nccl_unique_id(void* out128);
+void nccl_connect(Session& s, const void* id128, int rank);
+}  // namespace mpcg
+
+struct mpcg_session {
+  std::unique_ptr<Session> s;
+};
+struct mpcg_tensor {
+  DT t;
+  Session* s;
+};
+struct mpcg_model {
+  ModelGraph g;
+};
+struct mpcg_executor {
+  std::unique_ptr<SecureExecutor> e;
+  Session* s;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return MPCG_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MPCG_ERR_INTERNAL;
+  } catch (...) {
+    g_err = "unknown error";
+    return MPCG_ERR_INTERNAL;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw Error(kUsageError, std::string("null ") + what);
+}
+
+mpcg_tensor* wrap(Session& s, DT t) { return new mpcg_tensor{std::move(t), &s}; }
+const DT& T(const mpcg_tensor* t) {
+  need(t, "tensor");
+  return t->t;
+}
+Session& S(mpcg_session* s) {
+  need(s, "session");
+  return *s->s;
+}
+std::string tagstr(const char* t) { return t ? std::string(t) : std::string(); }
+}  // namespace
+
+extern "C" {
+#pragma GCC visibility push(default)
+
+const char* mpcg_last_error(void) { return g_err.c_str(); }
+int mpcg_version(void) { return 1; }
+
+int mpcg_device_count(int* out) {
+  return guard([&] {
+    need(out, "out");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+    cudaGetLastError();
+    *out = n;
+  });
+}
+
+int mpcg_session_create(int device, int n_local, int party, uint64_t seed, uint64_t mask_seed, int frac_bits,
+                        mpcg_session** out) {
+  return guard([&] {
+    need(out, "out");
+    auto* h = new mpcg_session;
+    try {
+      h->s = std::make_unique<Session>(device, n_local, party, seed, mask_seed, frac_bits);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int mpcg_session_destroy(mpcg_session* s) {
+  return guard([&] { delete s; });
+}
+
+int mpcg_session_set_pipeline(mpcg_session* s, int chunks, uint64_t threshold, int merged) {
+  return guard([&] {
+    Session& ss = S(s);
+    ss.cfg.chunks = chunks;
+    ss.cfg.chunk_threshold = threshold;
+    ss.cfg.merged_adder = merged != 0;
+  });
+}
+
+int mpcg_session_set_link(mpcg_session* s, double latency_s, double bw, double msg) {
+  return guard([&] {
+    Session& ss = S(s);
+    if (latency_s < 0) throw Error(kConfigError, "latency must be >= 0");
+    ss.cfg.link_latency_s = latency_s;
+    ss.cfg.link_bandwidth = bw > 0 ? bw : 0;
+    ss.cfg.sec_per_message = msg;
+  });
+}
+
+int mpcg_session_set_shard(mpcg_session* s, uint64_t local_batch, uint64_t global_batch, uint64_t off) {
+  return guard([&] {
+    Session& ss = S(s);
+    if (local_batch == 0 || global_batch < local_batch || off + local_batch > global_batch)
+      throw Error(kConfigError, "bad shard");
+    ss.shard_local = local_batch;
+    ss.shard_global = global_batch;
+    ss.shard_offset = off;
+  });
+}
+
+int mpcg_nccl_unique_id(uint8_t out[128]) {
+  return guard([&] { nccl_unique_id(out); });
+}
+
+int mpcg_session_connect_nccl(mpcg_session* s, const uint8_t id[128], int rank) {
+  return guard([&] { nccl_connect(S(s), id, rank); });
+}
+
+int mpcg_session_sync(mpcg_session* s) {
+  return guard([&] { S(s).sync(); });
+}
+
+int mpcg_session_stats(mpcg_session* s, int slot, uint64_t out[3]) {
+  return guard([&] {
+    Session& ss = S(s);
+    if (slot < 0 || slot >= ss.n_local) throw Error(kUsageError, "bad slot");
+    out[0] = ss.stats[slot].bytes_sent;
+    out[1] = ss.stats[slot].collectives;
+    out[2] = ss.stats[slot].p2p_sends;
+  });
+}
+
+int mpcg_session_n_local(mpcg_session* s, int* out) {
+  return guard([&] { *out = S(s).n_local; });
+}
+
+int mpcg_session_trace(mpcg_session* s, int enable) {
+  return guard([&] { S(s).trace_on = enable != 0; });
+}
+
+int mpcg_tensor_create(mpcg_session* s, int ndim, const uint64_t* dims, int scale, const uint64_t* host,
+                       mpcg_tensor** out) {
+  return guard([&] {
+    Session& ss = S(s);
+    need(out, "out");
+    if (ndim < 0 || ndim > 8) throw Error(kShapeError, "rank must be in [0, 8]");
+    Shape sh(dims, dims + ndim);
+    DT t = host ? ss.upload(sh, scale, host) : ss.alloc(sh, scale);
+    if (!host && t.numel())
+      MPCG_CUDA(cudaMemsetAsync(t.mem->ptr, 0, t.numel() * ss.n_local * 8, ss.stream));
+    *out = wrap(ss, std::move(t));
+  });
+}
+
+int mpcg_tensor_download(mpcg_tensor* t, uint64_t* host) {
+  return guard([&] {
+    need(t, "tensor");
+    t->s->download(t->t, host);
+  });
+}
+
+int mpcg_tensor_shape(const mpcg_tensor* t, int* ndim, uint64_t dims[8], int* scale) {
+  return guard([&] {
+    const DT& d = T(t);
+    *ndim = int(d.shape.size());
+    for (size_t i = 0; i < d.shape.size() && i < 8; ++i) dims[i] = d.shape[i];
+    if (scale) *scale = d.scale;
+  });
+}
+
+int mpcg_tensor_destroy(mpcg_tensor* t) {
+  return guard([&] { delete t; });
+}
+
+int mpcg_deal_input(mpcg_session* s, const double* x, int ndim, const uint64_t* gdims, uint64_t off,
+                    uint64_t local, uint64_t seed, mpcg_tensor** out) {
+  return guard([&] {
+    Session& ss = S(s);
+    need(x, "input");
+    if (ndim < 1) throw Error(kShapeError, "input needs a batch dim");
+    Shape g(gdims, gdims + ndim);
+    if (off + local > g[0] || local == 0) throw Error(kConfigError, "bad input slice");
+    const size_t per = shape_numel(g) / g[0];
+    const size_t n = per * local, base = per * off;
+    const int f = ss.cfg.frac_bits;
+    const u64 key = seed ^ (u64(0x11a9) * kPhi);
+    std::vector<u64> host(n * ss.n_local);
+    for (size_t i = 0; i < n; ++i) {
+      const u64 r = drw(key, 1 + base + i);
+      const u64 enc = encode_fixed(x[base + i], f);
+      for (int sl = 0; sl < ss.n_local; ++sl) host[sl * n + i] = ss.party_of[sl] == 0 ? enc - r : r;
+    }
+    Shape ls = g;
+    ls[0] = local;
+    *out = wrap(ss, ss.upload(ls, f, host.data()));
+  });
+}
+
+#define OP1(expr)                           \
+  return guard([&] {                        \
+    Session& ss = S(s);                     \
+    need(out, "out");                       \
+    *out = wrap(ss, (expr));                \
+  })
+
+int mpcg_open(mpcg_session* s, const mpcg_tensor* x, int reduce, const char* tag, mpcg_tensor** out) {
+  OP1(open_value(ss, T(x), reduce == MPCG_REDUCE_XOR ? Reduce::Xor : Reduce::Sum, tagstr(tag)));
+}
+int mpcg_beaver_mul(mpcg_session* s, const mpcg_tensor* x, const mpcg_tensor* y, const char* tag, int chunks,
+                    mpcg_tensor** out) {
+  OP1(beaver_mul(ss, T(x), T(y), tagstr(tag), chunks));
+}
+int mpcg_beaver_square(mpcg_session* s, const mpcg_tensor* x, const char* tag, int chunks, mpcg_tensor** out) {
+  OP1(beaver_square(ss, T(x), tagstr(tag), chunks));
+}
+int mpcg_beaver_and(mpcg_session* s, const mpcg_tensor* x, const mpcg_tensor* y, const char* tag, int chunks,
+                    mpcg_tensor** out) {
+  OP1(beaver_and(ss, T(x), T(y), tagstr(tag), chunks));
+}
+int mpcg_beaver_matmul(mpcg_session* s, const mpcg_tensor* x, const mpcg_tensor* y, int tb, const char* tag,
+                       int chunks, mpcg_tensor** out) {
+  OP1(beaver_matmul(ss, T(x), T(y), tb != 0, tagstr(tag), chunks));
+}
+int mpcg_binary_add(mpcg_session* s, const mpcg_tensor* x, const mpcg_tensor* y, int width, int merged, int chunks,
+                    const char* tag, mpcg_tensor** out) {
+  AdderOptions o;
+  o.width = width;
+  o.merged = merged != 0;
+  o.chunks = chunks;
+  OP1(binary_add(ss, T(x), T(y), o, tagstr(tag)));
+}
+int mpcg_a2b(mpcg_session* s, const mpcg_tensor* x, int chunks, const char* tag, mpcg_tensor** out) {
+  AdderOptions o;
+  o.chunks = chunks;
+  OP1(a2b(ss, T(x), o, tagstr(tag)));
+}
+int mpcg_msb(mpcg_session* s, const mpcg_tensor* x, int chunks, const char* tag, mpcg_tensor** out) {
+  AdderOptions o;
+  o.chunks = chunks;
+  OP1(msb(ss, T(x), o, tagstr(tag)));
+}
+int mpcg_b2a_bit(mpcg_session* s, const mpcg_tensor* b, const char* tag, int chunks, mpcg_tensor** out) {
+  OP1(b2a_bit(ss, T(b), tagstr(tag), chunks));
+}
+int mpcg_less_than(mpcg_session* s, const mpcg_tensor* x, const mpcg_tensor* y, int chunks, const char* tag,
+                   mpcg_tensor** out) {
+  AdderOptions o;
+  o.chunks = chunks;
+  OP1(less_than(ss, T(x), T(y), o, tagstr(tag)));
+}
+int mpcg_truncate(mpcg_session* s, const mpcg_tensor* x, int bits, mpcg_tensor** out) {
+  OP1(truncate_shares(ss, T(x), bits));
+}
+int mpcg_relu(mpcg_session* s, const mpcg_tensor* x, const char* tag, mpcg_tensor** out) {
+  OP1(relu_shares(ss, T(x), tagstr(tag)));
+}
+int mpcg_max_last_dim(mpcg_session* s, const mpcg_tensor* x, uint64_t L, const char* tag, mpcg_tensor** out) {
+  OP1(max_last_dim(ss, T(x), L, tagstr(tag)));
+}
+int mpcg_exp(mpcg_session* s, const mpcg_tensor* x, const char* tag, mpcg_tensor** out) {
+  OP1(exp_shares(ss, T(x), tagstr(tag)));
+}
+int mpcg_reciprocal(mpcg_session* s, const mpcg_tensor* x, const char* tag, mpcg_tensor** out) {
+  OP1(reciprocal_shares(ss, T(x), tagstr(tag)));
+}
+int mpcg_softmax(mpcg_session* s, const mpcg_tensor* x, uint64_t L, const char* tag, mpcg_tensor** out) {
+  OP1(softmax_shares(ss, T(x), L, tagstr(tag)));
+}
+int mpcg_maxpool2d(mpcg_session* s, const mpcg_tensor* x, uint64_t N, uint64_t C, uint64_t H, uint64_t W,
+                   uint64_t k, uint64_t stride, const char* tag, mpcg_tensor** out) {
+  OP1(maxpool2d_shares(ss, T(x), N, C, H, W, k, stride, tagstr(tag)));
+}
+
+int mpcg_model_create(const char* name, int frac_bits, int ndim, const uint64_t* dims, mpcg_model** out) {
+  return guard([&] {
+    need(out, "out");
+    if (frac_bits < 1 || frac_bits > 40) throw Error(kConfigError, "frac_bits out of range");
+    auto* m = new mpcg_model;
+    m->g.name = tagstr(name);
+    m->g.frac_bits = frac_bits;
+    m->g.input.assign(dims, dims + ndim);
+    *out = m;
+  });
+}
+
+int mpcg_model_add_layer(mpcg_model* m, const char* name, int kind, uint64_t outc, uint64_t kernel, uint64_t stride,
+                         uint64_t pad, uint64_t heads, int bias) {
+  return guard([&] {
+    need(m, "model");
+    if (kind < 0 || kind > MPCG_LAYER_MEANPOOL) throw Error(kConfigError, "unknown layer kind");
+    LayerSpec l;
+    l.name = tagstr(name);
+    l.kind = static_cast<LayerKind>(kind);
+    l.out = outc;
+    l.kernel = kernel;
+    l.stride = stride;
+    l.pad = pad;
+    l.heads = heads;
+    l.bias = bias != 0;
+    m->g.layers.push_back(l);
+    infer_shapes(m->g);  // validate (H/engine/model.hpp:177)
+  });
+}
+
+int mpcg_model_destroy(mpcg_model* m) {
+  return guard([&] { delete m; });
+}
+
+int mpcg_executor_create(mpcg_session* s, const mpcg_model* m, int pub, int pipelined, int chunks, uint64_t thr,
+                         int merged, mpcg_executor** out) {
+  return guard([&] {
+    Session& ss = S(s);
+    need(m, "model");
+    need(out, "out");
+    ExecOptions o;
+    o.pipelined = pipelined != 0;
+    o.chunks = chunks;
+    o.chunk_threshold = thr;
+    o.merged_adder = merged != 0;
+    auto* e = new mpcg_executor;
+    e->s = &ss;
+    try {
+      e->e = std::make_unique<SecureExecutor>(ss, m->g, pub != 0, o);
+    } catch (...) {
+      delete e;
+      throw;
+    }
+    *out = e;
+  });
+}
+
+int mpcg_executor_deal_weights(mpcg_executor* e, int count, const char* const* names, const double* const* values,
+                               uint64_t seed) {
+  return guard([&] {
+    need(e, "executor");
+    std::vector<std::string> n;
+    std::vector<const double*> v;
+    for (int i = 0; i < count; ++i) {
+      n.emplace_back(names[i]);
+      v.push_back(values[i]);
+    }
+    e->e->deal_weights(n, v, seed);
+  });
+}
+
+int mpcg_executor_run(mpcg_executor* e, const mpcg_tensor* input, mpcg_tensor** out) {
+  return guard([&] {
+    need(e, "executor");
+    need(out, "out");
+    *out = wrap(*e->s, e->e->run(T(input)));
+  });
+}
+
+int mpcg_executor_time_layers(mpcg_executor* e, int enable) {
+  return guard([&] {
+    need(e, "executor");
+    e->e->time_layers = enable != 0;
+  });
+}
+
+int mpcg_executor_layer_times(mpcg_executor* e, int max, float* ms, int* count) {
+  return guard([&] {
+    need(e, "executor");
+    const auto& t = e->e->timings;
+    const int n = int(t.size()) < max ? int(t.size()) : max;
+    for (int i = 0; i < n; ++i) ms[i] = t[i].ms;
+    *count = int(t.size());
+  });
+}
+
+int mpcg_executor_destroy(mpcg_executor* e) {
+  return guard([&] { delete e; });
+}
+
+uint64_t mpcg_fnv1a_words(const uint64_t* w, uint64_t n) {
+  u64 h = 0xcbf29ce484222325ull;
+  for (u64 i = 0; i < n; ++i)
+    for (int b = 0; b < 8; ++b) h = (h ^ ((w[i] >> (8 * b)) & 0xff)) * 0x100000001b3ull;
+  return h;
+}
+
+#pragma GCC visibility pop
+}  // extern "C"

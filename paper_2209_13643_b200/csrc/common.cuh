@@ -1,0 +1,194 @@
+// Shared device/host primitives for the B200 2PC engine (sm_100a).
+//
+// Ring Z_2^64 arithmetic and the counter-mode splitmix64 PRG of the reference
+// (H/ring/ring_ops.hpp:13-25, H/sharing/rng.hpp:10-32), plus the closed-form dealer
+// element functions that regenerate any party's triple share in registers
+// (H/sharing/triple.hpp:85-151, H/sharing/share.hpp:22-50).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace mpcg {
+
+using u64 = std::uint64_t;
+using u32 = std::uint32_t;
+using i64 = std::int64_t;
+
+constexpr u64 kPhi = 0x9E3779B97F4A7C15ull;
+
+// ------------------------------------------------------------------ errors
+// Codes mirror the reference exception hierarchy (H/errors.hpp:8-45).
+enum ErrCode : int {
+  kOk = 0,
+  kRangeError = 1,
+  kShapeError = 2,
+  kConfigError = 3,
+  kProtocolError = 4,
+  kTransportError = 5,
+  kBudgetError = 6,
+  kUsageError = 7,
+  kCudaError = 8,
+  kNcclError = 9,
+  kInternalError = 10,
+};
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess)
+    throw Error(kCudaError, std::string(what) + ": " + cudaGetErrorString(e) + " at " + file + ":" +
+                                std::to_string(line));
+}
+#define MPCG_CUDA(x) ::mpcg::cuda_check((x), #x, __FILE__, __LINE__)
+
+// ------------------------------------------------------------------ ring ops
+__host__ __device__ __forceinline__ u64 sar64(u64 v, int k) {
+  return static_cast<u64>(static_cast<i64>(v) >> k);
+}
+
+__host__ __device__ __forceinline__ u64 mix64(u64 z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+// draw #c (c >= 1) of the stream keyed `key` (already key ^ stream*phi).
+__host__ __device__ __forceinline__ u64 drw(u64 key, u64 c) { return mix64(key + c * kPhi); }
+
+// ------------------------------------------------------------------ dealer
+// One elementwise triple as seen by one party, with the local->global index map that
+// lets a data-parallel shard regenerate exactly its slice of the full-batch triple.
+// A tensor of `half` local elements per stacked half lives at global index
+// s*ghalf + off + i (s = stacked half, 0 for unstacked specs).
+struct EwTriple {
+  u64 key;     // seed ^ (stream * phi)
+  u64 mg;      // global numel of A (== of B, C)
+  u64 ghalf;   // global elements per stacked half (== mg when unstacked)
+  u64 off;     // global offset of this shard inside each half
+  int square;  // B == A as a secret; only A drawn
+  int bin;     // XOR sharing + AND product
+};
+
+__device__ __forceinline__ u64 ew_gidx(const EwTriple& t, int s, u64 i) { return s * t.ghalf + t.off + i; }
+
+// a, b shares of element g (global index) for `party` (0 absorbs the secret).
+__device__ __forceinline__ void ew_ab(const EwTriple& t, int party, u64 g, u64& a, u64& b) {
+  const u64 nbd = t.square ? 0 : t.mg;
+  const u64 baseA = 1 + t.mg + nbd;
+  const u64 baseB = baseA + t.mg;
+  const u64 ra = drw(t.key, baseA + g), rb = drw(t.key, baseB + g);
+  if (party != 0) {
+    a = ra;
+    b = rb;
+    return;
+  }
+  const u64 A = drw(t.key, 1 + g);
+  const u64 B = t.square ? A : drw(t.key, 1 + t.mg + g);
+  if (t.bin) {
+    a = A ^ ra;
+    b = B ^ rb;
+  } else {
+    a = A - ra;
+    b = B - rb;
+  }
+}
+
+__device__ __forceinline__ void ew_abc(const EwTriple& t, int party, u64 g, u64& a, u64& b, u64& c) {
+  const u64 nbd = t.square ? 0 : t.mg;
+  const u64 baseA = 1 + t.mg + nbd;
+  const u64 baseB = baseA + t.mg;
+  const u64 baseC = baseB + t.mg;
+  const u64 ra = drw(t.key, baseA + g), rb = drw(t.key, baseB + g), rc = drw(t.key, baseC + g);
+  if (party != 0) {
+    a = ra;
+    b = rb;
+    c = rc;
+    return;
+  }
+  const u64 A = drw(t.key, 1 + g);
+  const u64 B = t.square ? A : drw(t.key, 1 + t.mg + g);
+  if (t.bin) {
+    a = A ^ ra;
+    b = B ^ rb;
+    c = (A & B) ^ rc;
+  } else {
+    a = A - ra;
+    b = B - rb;
+    c = A * B - rc;
+  }
+}
+
+// Square triples only need a and c (b is never used by the combine).
+__device__ __forceinline__ void sq_ac(const EwTriple& t, int party, u64 g, u64& a, u64& c) {
+  const u64 baseA = 1 + t.mg;
+  const u64 baseC = baseA + 2 * t.mg;
+  const u64 ra = drw(t.key, baseA + g), rc = drw(t.key, baseC + g);
+  if (party != 0) {
+    a = ra;
+    c = rc;
+    return;
+  }
+  const u64 A = drw(t.key, 1 + g);
+  a = A - ra;
+  c = A * A - rc;
+}
+
+__device__ __forceinline__ u64 sq_a(const EwTriple& t, int party, u64 g) {
+  const u64 ra = drw(t.key, 1 + t.mg + g);
+  return party != 0 ? ra : drw(t.key, 1 + g) - ra;
+}
+
+// Matmul triple (H/sharing/triple.hpp:96-114): draws A (na), B (nb), then r_A, r_B, r_C.
+struct MmTriple {
+  u64 key;
+  u64 na, nb, nc;     // global numels
+  u64 offA, offB, offC;
+};
+__device__ __forceinline__ u64 mm_A(const MmTriple& t, u64 i) { return drw(t.key, 1 + t.offA + i); }
+__device__ __forceinline__ u64 mm_B(const MmTriple& t, u64 j) { return drw(t.key, 1 + t.na + t.offB + j); }
+__device__ __forceinline__ u64 mm_rA(const MmTriple& t, u64 i) {
+  return drw(t.key, 1 + t.na + t.nb + t.offA + i);
+}
+__device__ __forceinline__ u64 mm_rB(const MmTriple& t, u64 j) {
+  return drw(t.key, 1 + 2 * t.na + t.nb + t.offB + j);
+}
+__device__ __forceinline__ u64 mm_rC(const MmTriple& t, u64 k) {
+  return drw(t.key, 1 + 2 * t.na + 2 * t.nb + t.offC + k);
+}
+
+// ------------------------------------------------------------------ launch helpers
+constexpr int kSms = 148;
+
+template <class F>
+__global__ void __launch_bounds__(256) ew_kernel(u64 n, F f) {
+  const int slot = blockIdx.y;
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+    f(slot, i);
+}
+
+inline unsigned ew_blocks(u64 n) {
+  u64 b = (n + 255) / 256;
+  const u64 cap = u64(kSms) * 8;  // 8 resident 256-thread CTAs per SM
+  return static_cast<unsigned>(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+// Launch f(slot, i) for i in [0, n) and every local party slot, on `stream`.
+template <class F>
+void launch_ew(cudaStream_t stream, int nslots, u64 n, F f) {
+  if (n == 0) return;
+  dim3 grid(ew_blocks(n), nslots);
+  ew_kernel<<<grid, 256, 0, stream>>>(n, f);
+  MPCG_CUDA(cudaGetLastError());
+}
+
+}  // namespace mpcg

@@ -1,0 +1,315 @@
+// Session runtime: device memory, dealer tag streams, the open/reveal wire.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "core.hpp"
+
+namespace mpcg {
+
+std::string shape_str(const Shape& s) {
+  std::string out = "[";
+  for (size_t i = 0; i < s.size(); ++i) {
+    if (i) out += "x";
+    out += std::to_string(s[i]);
+  }
+  return out + "]";
+}
+
+u64 encode_fixed(double x, int scale_bits) {
+  const long double t = std::floor(static_cast<long double>(x) * std::exp2l(scale_bits) + 0.5L);
+  if (t < -9223372036854775808.0L || t >= 9223372036854775808.0L)
+    throw Error(kRangeError, "encode_fixed: " + std::to_string(x) + " exceeds representable range at scale " +
+                                 std::to_string(scale_bits));
+  return static_cast<u64>(static_cast<i64>(t));
+}
+
+// ------------------------------------------------------------------ memory
+Block::Block(size_t w, cudaStream_t s) : words(w), stream(s) {
+  if (w) MPCG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), w * sizeof(u64), s));
+}
+Block::~Block() {
+  if (ptr) cudaFreeAsync(ptr, stream);  // stream-ordered: safe after every queued reader
+}
+
+std::shared_ptr<Block> Session::raw(size_t words) { return std::make_shared<Block>(words, stream); }
+
+DT Session::alloc(const Shape& shape, int scale) {
+  DT t;
+  t.shape = shape;
+  t.scale = scale;
+  const size_t n = shape_numel(shape);
+  t.mem = raw(n * size_t(n_local) + 1);
+  for (int i = 0; i < n_local; ++i) t.s[i] = t.mem->ptr + size_t(i) * n;
+  return t;
+}
+
+DT Session::upload(const Shape& shape, int scale, const u64* host) {
+  DT t = alloc(shape, scale);
+  const size_t n = shape_numel(shape);
+  if (n)
+    MPCG_CUDA(cudaMemcpyAsync(t.mem->ptr, host, n * n_local * sizeof(u64), cudaMemcpyHostToDevice, stream));
+  return t;
+}
+
+void Session::download(const DT& t, u64* host) {
+  const size_t n = t.numel();
+  if (n)
+    MPCG_CUDA(cudaMemcpyAsync(host, t.mem->ptr, n * n_local * sizeof(u64), cudaMemcpyDeviceToHost, stream));
+  MPCG_CUDA(cudaStreamSynchronize(stream));
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen'd)
+namespace {
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!a.h) throw Error(kNcclError, std::string("cannot load libnccl.so.2: ") + dlerror());
+    auto sym = [&](const char* n) {
+      void* p = dlsym(a.h, n);
+      if (!p) throw Error(kNcclError, std::string("missing NCCL symbol ") + n);
+      return p;
+    };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    return a;
+  }();
+  return api;
+}
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Error(kNcclError, std::string(what) + ": " + nccl_api().GetErrorString(r));
+}
+}  // namespace
+
+void nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  nccl_check(nccl_api().GetUniqueId(&id), "ncclGetUniqueId");
+  std::memcpy(out128, &id, sizeof id);
+}
+
+void nccl_connect(Session& s, const void* id128, int rank) {
+  if (s.n_local != 1) throw Error(kUsageError, "NCCL link needs a single-party session");
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  MPCG_CUDA(cudaSetDevice(s.device));
+  nccl_check(nccl_api().CommInitRank(&s.nccl, 2, id, rank), "ncclCommInitRank");
+}
+
+// ------------------------------------------------------------------ session
+Session::Session(int dev, int nl, int party, u64 sd, u64 mask_seed, int frac_bits)
+    : device(dev), n_local(nl), seed(sd) {
+  if (nl != 1 && nl != 2) throw Error(kConfigError, "n_local must be 1 or 2");
+  if (nl == 1 && (party < 0 || party > 1)) throw Error(kConfigError, "bad party index");
+  if (frac_bits < 1 || frac_bits > 40) throw Error(kConfigError, "frac_bits out of range");
+  cfg.frac_bits = frac_bits;
+  if (nl == 2) {
+    party_of[0] = 0;
+    party_of[1] = 1;
+  } else {
+    party_of[0] = party;
+  }
+  for (int i = 0; i < nl; ++i) mask_key[i] = mask_seed ^ (u64(party_of[i]) * kPhi);
+  MPCG_CUDA(cudaSetDevice(device));
+  MPCG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  MPCG_CUDA(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
+  cudaMemPool_t pool;
+  MPCG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  u64 thr = ~u64(0);
+  MPCG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  MPCG_CUDA(cudaMalloc(&link_state_, 64));
+  MPCG_CUDA(cudaMemset(link_state_, 0, 64));
+  const char* dbg = std::getenv("MPCG_DEBUG_SYNC");
+  debug_sync = dbg && dbg[0] == '1';
+}
+
+Session::~Session() {
+  cudaStreamSynchronize(stream);
+  cudaStreamSynchronize(comm_stream);
+  for (auto e : events_) cudaEventDestroy(e);
+  if (nccl) nccl_api().CommDestroy(nccl);
+  cudaFree(link_state_);
+  cudaStreamDestroy(comm_stream);
+  cudaStreamDestroy(stream);
+}
+
+void Session::sync() {
+  MPCG_CUDA(cudaStreamSynchronize(comm_stream));
+  MPCG_CUDA(cudaStreamSynchronize(stream));
+}
+
+void Session::check() {
+  if (!debug_sync) return;
+  MPCG_CUDA(cudaGetLastError());
+  sync();
+}
+
+// ------------------------------------------------------------------ dealer
+u64 Session::tag_stream(const std::string& tag) {
+  if (tag.empty()) return 0x7452u ^ untagged_index++;
+  u64 h = 0xcbf29ce484222325ull;
+  for (char c : tag) h = (h ^ u64(static_cast<unsigned char>(c))) * 0x100000001b3ull;
+  return mix64(h + 0x51ed270bull * tag_counts[h]++);
+}
+
+Triple Session::fetch(const TripleSpec& spec, const std::string& tag, bool batch_b) {
+  Triple t;
+  t.spec = spec;
+  const u64 stream_id = tag_stream(tag);
+  t.key = seed ^ (stream_id * kPhi);
+  const u64 na = shape_numel(spec.shape_a);
+  if (!spec.matmul) {
+    if (spec.shape_a != spec.shape_b) throw Error(kConfigError, "dealer_gen_triple: elementwise shapes differ");
+    // stacked [2, ...] specs (adder levels) map each half separately
+    const bool stacked = batch_b;
+    const u64 half = stacked ? na / 2 : na;
+    t.ew.key = t.key;
+    t.ew.ghalf = dp_global(half);
+    t.ew.off = dp_offset(half);
+    t.ew.mg = stacked ? 2 * t.ew.ghalf : t.ew.ghalf;
+    t.ew.square = spec.square;
+    t.ew.bin = spec.kind == TripleKind::Bin;
+  } else {
+    const Shape& a = spec.shape_a;
+    const Shape& b = spec.shape_b;
+    if (a.size() < 2 || b.size() < 2) throw Error(kConfigError, "dealer_gen_triple: matmul shapes must have rank >= 2");
+    const size_t k = a.back();
+    const size_t bk = spec.transpose_b ? b.back() : b[b.size() - 2];
+    if (k != bk) throw Error(kConfigError, "dealer_gen_triple: matmul inner dims incompatible");
+    const size_t N = spec.transpose_b ? b[b.size() - 2] : b.back();
+    const u64 nb = shape_numel(b);
+    const u64 nc = na / k * N;
+    const bool bb = b.size() > 2;  // batched rhs is batch-leading (attention)
+    t.mm.key = t.key;
+    t.mm.na = dp_global(na);
+    t.mm.offA = dp_offset(na);
+    t.mm.nb = bb ? dp_global(nb) : nb;
+    t.mm.offB = bb ? dp_offset(nb) : 0;
+    t.mm.nc = dp_global(nc);
+    t.mm.offC = dp_offset(nc);
+  }
+  return t;
+}
+
+u64 Session::take_mask(u64 numel_local) {
+  const u64 base = mask_ctr;
+  mask_ctr += dp_global(numel_local);
+  return base + dp_offset(numel_local);
+}
+
+// ------------------------------------------------------------------ wire
+const u64* Open::peer(int slot) const {
+  return n_local == 2 ? out->ptr + size_t(1 - slot) * n : in->ptr;
+}
+
+cudaEvent_t Session::pool_event() {
+  // Ring of events; an event is re-recorded only 4096 opens later, long after its wait.
+  constexpr size_t kRing = 4096;
+  if (events_.size() < kRing) {
+    cudaEvent_t e;
+    MPCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    events_.push_back(e);
+    return e;
+  }
+  cudaEvent_t e = events_[event_next_];
+  event_next_ = (event_next_ + 1) % kRing;
+  return e;
+}
+
+Open Session::begin_open(size_t nwords, Reduce kind) {
+  Open o;
+  o.n = nwords;
+  o.kind = kind;
+  o.n_local = n_local;
+  o.out = raw(nwords * size_t(n_local) + 1);
+  if (n_local == 1) o.in = raw(nwords + 1);
+  o.seq = next_seq++;
+  return o;
+}
+
+namespace {
+__device__ __forceinline__ u64 globaltimer_ns() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Emulated link (H/transport/sim.hpp:83-166 model): the sender's link is busy for
+// msg + bytes/bw (serialised in issue order), the payload lands `latency` later.
+__global__ void link_delay_kernel(u64* state, u64 busy_ns, u64 latency_ns) {
+  const u64 now = globaltimer_ns();
+  const u64 start = now > state[0] ? now : state[0];
+  const u64 end = start + busy_ns;
+  state[0] = end;
+  const u64 arrive = end + latency_ns;
+  while (globaltimer_ns() < arrive) __nanosleep(500);
+}
+}  // namespace
+
+void Session::throttle(Open& o) {
+  const double busy = cfg.sec_per_message + double(o.n * 8) / cfg.link_bandwidth;
+  link_delay_kernel<<<1, 1, 0, comm_stream>>>(link_state_, u64(busy * 1e9), u64(cfg.link_latency_s * 1e9));
+  MPCG_CUDA(cudaGetLastError());
+}
+
+void Session::post(Open& o, const std::string& tag, bool p2p) {
+  if (o.posted) throw Error(kUsageError, "open posted twice");
+  o.posted = true;
+  for (int i = 0; i < n_local; ++i) {
+    stats[i].bytes_sent += o.n * 8;
+    if (p2p)
+      stats[i].p2p_sends++;
+    else
+      stats[i].collectives++;
+  }
+  if (trace_on) trace.push_back(TraceEvent{o.seq, o.kind, tag, o.n * 8});
+  const bool throttled = cfg.link_bandwidth > 0;
+  if (n_local == 2 && !throttled) {
+    check();
+    return;  // zero-copy: the peer reads our outbox after the stream-ordered kernel boundary
+  }
+  cudaEvent_t built = pool_event();
+  MPCG_CUDA(cudaEventRecord(built, stream));
+  MPCG_CUDA(cudaStreamWaitEvent(comm_stream, built, 0));
+  if (n_local == 1) {
+    if (!nccl) throw Error(kTransportError, "single-party session has no peer link (connect NCCL first)");
+    const int peer = 1 - party_of[0];
+    auto& api = nccl_api();
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    nccl_check(api.Send(o.own(0), o.n, ncclUint64, peer, nccl, comm_stream), "ncclSend");
+    nccl_check(api.Recv(o.in->ptr, o.n, ncclUint64, peer, nccl, comm_stream), "ncclRecv");
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+  }
+  if (throttled) throttle(o);
+  o.ready = pool_event();
+  MPCG_CUDA(cudaEventRecord(o.ready, comm_stream));
+  check();
+}
+
+void Session::wait(Open& o) {
+  if (o.waited) throw Error(kUsageError, "wait() called twice on one handle");
+  if (!o.posted) throw Error(kUsageError, "wait() on an open that was never posted");
+  o.waited = true;
+  if (o.ready) MPCG_CUDA(cudaStreamWaitEvent(stream, o.ready, 0));
+}
+
+}  // namespace mpcg

@@ -1,0 +1,235 @@
+// Host-side runtime of the B200 2PC engine: sessions, device share tensors, the
+// dealer's tag streams and the open/reveal wire.
+//
+// A Session holds the party slots that live in this process on one GPU:
+//   * n_local == 2 — both parties of a 2PC pair on one device (1-GPU mode). Every
+//     kernel runs both parties' slots in one launch (blockIdx.y = slot); a slot only
+//     touches its own party's state plus the peer payload it opened. An open is then a
+//     stream-ordered kernel boundary and the peer reads the poster's outbox in place.
+//   * n_local == 1 — one party per process/GPU (2/4/8-GPU runs); the peer's payload
+//     crosses NVLink with NCCL send/recv on a dedicated comm stream.
+// All protocol code is SPMD over the local slots (H/transport/harness.hpp:23-38 runs
+// one thread per party instead; the values and the collective order are identical).
+#pragma once
+
+#include <map>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+
+typedef struct ncclComm* ncclComm_t;
+
+namespace mpcg {
+
+using Shape = std::vector<size_t>;
+
+inline size_t shape_numel(const Shape& s) {
+  size_t n = 1;
+  for (auto d : s) n *= d;
+  return n;
+}
+std::string shape_str(const Shape& s);
+
+// round(x * 2^scale), ties toward +inf, in long double (H/ring/fixed.hpp:16-22).
+u64 encode_fixed(double x, int scale_bits);
+
+// ------------------------------------------------------------------ device memory
+// Stream-ordered pool allocation (cudaMallocAsync), so allocation inside a CUDA-graph
+// capture becomes graph memory nodes with fixed addresses on replay.
+struct Block {
+  u64* ptr = nullptr;
+  size_t words = 0;
+  cudaStream_t stream = nullptr;
+  Block(size_t words, cudaStream_t s);
+  ~Block();
+  Block(const Block&) = delete;
+  Block& operator=(const Block&) = delete;
+};
+
+// One share per local party slot: slot i at base + i*numel (row-major u64).
+struct DT {
+  std::shared_ptr<Block> mem;
+  u64* s[2] = {nullptr, nullptr};
+  Shape shape;
+  int scale = 0;
+  size_t numel() const { return shape_numel(shape); }
+  explicit operator bool() const { return mem != nullptr; }
+};
+
+enum class Reduce : int { Sum = 0, Xor = 1 };
+
+// Per-party communication counters (H/transport/transport.hpp:25-45).
+struct TraceEvent {
+  u32 seq;
+  Reduce kind;
+  std::string tag;
+  u64 bytes;
+};
+struct CommStats {
+  u64 bytes_sent = 0;
+  u64 collectives = 0;
+  u64 p2p_sends = 0;
+};
+
+// ------------------------------------------------------------------ dealer specs
+enum class TripleKind : int { Arith = 0, Bin = 1 };
+struct TripleSpec {
+  TripleKind kind = TripleKind::Arith;
+  bool matmul = false;
+  bool square = false;
+  bool transpose_b = false;
+  Shape shape_a, shape_b;
+  static TripleSpec elementwise(TripleKind k, Shape s) { return {k, false, false, false, s, s}; }
+  static TripleSpec square_of(Shape s) { return {TripleKind::Arith, false, true, false, s, s}; }
+  static TripleSpec matmul_of(Shape a, Shape b, bool tb = false) {
+    return {TripleKind::Arith, true, false, tb, std::move(a), std::move(b)};
+  }
+};
+
+// A fetched triple: nothing is materialised; kernels regenerate elements from the key.
+struct Triple {
+  TripleSpec spec;
+  u64 key = 0;
+  bool consumed = false;
+  EwTriple ew{};  // elementwise view (global numel / shard offsets filled)
+  MmTriple mm{};  // matmul view
+  void mark_consumed() {
+    if (consumed) throw Error(kProtocolError, "beaver triple reused after consumption");
+    consumed = true;
+  }
+};
+
+// ------------------------------------------------------------------ the wire
+// One collective: each local slot's build kernel writes its payload into own(slot);
+// after wait() the peer's payload for the same slot is readable at peer(slot).
+struct Open {
+  std::shared_ptr<Block> out;    // n_local * n words: own payloads
+  std::shared_ptr<Block> in;     // n words: received peer payload (n_local == 1 only)
+  size_t n = 0;
+  Reduce kind = Reduce::Sum;
+  u32 seq = 0;
+  bool waited = false;
+  bool posted = false;
+  cudaEvent_t ready = nullptr;   // arrival (throttled link or NCCL), or null
+  u64* own(int slot) const { return out->ptr + size_t(slot) * n; }
+  const u64* peer(int slot) const;
+  int n_local = 2;
+};
+
+struct SessionConfig {
+  int frac_bits = 16;
+  int chunks = 1;                 // ProtoCtx::chunks (H/protocols/context.hpp:17-35)
+  u64 chunk_threshold = 0;        // bytes
+  bool merged_adder = true;
+  double link_latency_s = 0;      // optional throttled link (H/transport/config.hpp:41-43)
+  double link_bandwidth = 0;      // bytes/s; 0 = no throttle (NVLink / in-device)
+  double sec_per_message = 0;
+};
+
+class Session {
+ public:
+  Session(int device, int n_local, int party, u64 seed, u64 mask_seed, int frac_bits);
+  ~Session();
+
+  int device = 0;
+  int n_local = 2;
+  int party_of[2] = {0, 1};   // party id of each local slot
+  u64 seed = 1;
+  SessionConfig cfg;
+  cudaStream_t stream = nullptr;       // compute stream (all local slots)
+  cudaStream_t comm_stream = nullptr;  // link emulation / NCCL
+  ncclComm_t nccl = nullptr;
+
+  // data-parallel shard (batch-leading tensors): local rows are a slice of the global batch
+  u64 shard_local = 1, shard_global = 1, shard_offset = 0;
+  u64 dp_global(u64 numel_local) const { return numel_local / shard_local * shard_global; }
+  u64 dp_offset(u64 numel_local) const { return numel_local / shard_local * shard_offset; }
+
+  // ---- tensors
+  DT alloc(const Shape& shape, int scale = 0);
+  DT upload(const Shape& shape, int scale, const u64* host);  // host holds n_local*numel words
+  void download(const DT& t, u64* host);
+  std::shared_ptr<Block> raw(size_t words);
+
+  // ---- dealer (H/sharing/triple.hpp:138-151): stream per tag and fetch count
+  Triple fetch(const TripleSpec& spec, const std::string& tag, bool batch_b = false);
+  u64 tag_stream(const std::string& tag);
+  std::unordered_map<u64, u64> tag_counts;
+  u64 untagged_index = 0;
+
+  // ---- party mask rng (CounterRng(mask_seed, party)): sequential counters per slot
+  u64 mask_key[2] = {0, 0};
+  u64 mask_ctr = 0;  // same count for every party: each a2b draws numel per party
+  u64 take_mask(u64 numel_global);  // returns first counter, advances
+
+  // ---- wire
+  Open begin_open(size_t nwords, Reduce kind);
+  void post(Open& o, const std::string& tag, bool p2p = false);
+  void wait(Open& o);
+  u32 next_seq = 0;
+  CommStats stats[2];
+  std::vector<TraceEvent> trace;
+  bool trace_on = false;
+
+  void sync();
+  void check();  // debug: sync + error check when MPCG_DEBUG_SYNC=1
+  bool debug_sync = false;
+
+ private:
+  void throttle(Open& o);
+  cudaEvent_t pool_event();
+  std::vector<cudaEvent_t> events_;
+  size_t event_next_ = 0;
+  u64* link_state_ = nullptr;  // device: [next free ns]
+};
+
+// ------------------------------------------------------------------ protocol ops
+// Mirrors of the reference free functions; arguments keep their meaning, each DT
+// carries every local party's share (H/protocols/*.hpp, H/nonlinear/*.hpp).
+void require_same_shape(const DT& a, const DT& b, const char* op);
+int clamp_chunks(int chunks, size_t numel);
+inline std::pair<size_t, size_t> chunk_range(size_t total, int chunks, int k) {
+  return {total * size_t(k) / size_t(chunks), total * (size_t(k) + 1) / size_t(chunks)};
+}
+
+struct AdderOptions {
+  int width = 64;
+  bool merged = true;
+  int chunks = 1;
+};
+
+int chunks_for(const Session& s, size_t numel);
+
+DT beaver_mul(Session& s, const DT& x, const DT& y, const std::string& tag = "mul", int chunks = 1);
+DT beaver_square(Session& s, const DT& x, const std::string& tag = "square", int chunks = 1);
+DT beaver_and(Session& s, const DT& x, const DT& y, const std::string& tag = "and", int chunks = 1);
+DT beaver_matmul(Session& s, const DT& x, const DT& y, bool transpose_b, const std::string& tag = "matmul",
+                 int chunks = 1);
+DT binary_add(Session& s, const DT& x, const DT& y, const AdderOptions& opt = {},
+              const std::string& tag = "badd");
+DT a2b(Session& s, const DT& x, const AdderOptions& opt = {}, const std::string& tag = "a2b");
+DT msb(Session& s, const DT& x, const AdderOptions& opt = {}, const std::string& tag = "msb");
+DT b2a_bit(Session& s, const DT& b, const std::string& tag = "b2a", int chunks = 1);
+DT less_than(Session& s, const DT& x, const DT& y, const AdderOptions& opt = {},
+             const std::string& tag = "lt");
+DT truncate_shares(Session& s, const DT& x, int bits);
+DT relu_shares(Session& s, const DT& x, const std::string& tag = "relu");
+DT max_last_dim(Session& s, const DT& x, size_t L, const std::string& tag = "max");
+DT exp_shares(Session& s, const DT& x, const std::string& tag = "exp", int square_iters = 7);
+DT reciprocal_shares(Session& s, const DT& x, const std::string& tag = "recip", int newton_iters = 10);
+DT softmax_shares(Session& s, const DT& x, size_t L, const std::string& tag = "softmax");
+DT maxpool2d_shares(Session& s, const DT& x, size_t N, size_t C, size_t H, size_t W, size_t k,
+                    size_t stride, const std::string& tag = "maxpool");
+DT open_value(Session& s, const DT& x, Reduce kind, const std::string& tag);  // reveal, every slot gets it
+
+// local tensor helpers (fused into producers where it matters)
+DT add_public(Session& s, const DT& x, u64 v);     // party 0 absorbs
+DT scale_public(Session& s, const DT& x, u64 k);
+DT sub_t(Session& s, const DT& a, const DT& b);
+DT add_t(Session& s, const DT& a, const DT& b);
+DT reshape(const DT& a, Shape shape);
+
+}  // namespace mpcg

@@ -1,0 +1,343 @@
+// Fused elementwise round kernels for the Beaver / SPK-adder protocols.
+//
+// Every secure round is "combine the previous open, build the next payload" in ONE
+// pass over the elements, with the dealer's triple shares regenerated in registers
+// (no triple ever touches HBM). A round kernel serves all local party slots in one
+// launch; a slot reads only its own state, its own outbox and the peer payload.
+#pragma once
+
+#include "core.hpp"
+
+namespace mpcg {
+
+struct Pid2 {
+  int v[2];
+};
+struct Ptr2 {
+  u64* p[2];
+};
+struct CPtr2 {
+  const u64* p[2];
+};
+
+inline Pid2 pids(const Session& s) { return Pid2{{s.party_of[0], s.party_of[1]}}; }
+inline Ptr2 ptrs(const DT& t) { return Ptr2{{t.s[0], t.s[1]}}; }
+inline CPtr2 cptrs(const DT& t) { return CPtr2{{t.s[0], t.s[1]}}; }
+inline Ptr2 own_ptrs(const Open& o) {
+  return Ptr2{{o.own(0), o.n_local == 2 ? o.own(1) : nullptr}};
+}
+inline CPtr2 peer_ptrs(const Open& o) {
+  return CPtr2{{o.peer(0), o.n_local == 2 ? o.peer(1) : nullptr}};
+}
+
+// ---------------------------------------------------------------- value sources
+struct SrcMem {  // x[g]
+  CPtr2 x;
+  __device__ u64 operator()(int slot, u64 g) const { return x.p[slot][g]; }
+};
+struct SrcZero {
+  __device__ u64 operator()(int, u64) const { return 0; }
+};
+struct SrcSub {  // x[g] - y[g]
+  CPtr2 x, y;
+  __device__ u64 operator()(int slot, u64 g) const { return x.p[slot][g] - y.p[slot][g]; }
+};
+struct SrcSar {  // sar(x[g], k)
+  CPtr2 x;
+  int k;
+  __device__ u64 operator()(int slot, u64 g) const { return sar64(x.p[slot][g], k); }
+};
+
+// ---------------------------------------------------------------- sinks (post-combine)
+struct SinkStore {  // out[g] = z
+  Ptr2 out;
+  __device__ void operator()(int slot, int, u64 g, u64 z) const { out.p[slot][g] = z; }
+};
+struct SinkTrunc {  // out[g] = sar(z, k)
+  Ptr2 out;
+  int k;
+  __device__ void operator()(int slot, int, u64 g, u64 z) const { out.p[slot][g] = sar64(z, k); }
+};
+
+// ---------------------------------------------------------------- Beaver multiply
+// payload of a chunk of width w: [eps(w) | delta(w)]   (H/protocols/beaver.hpp:53,68-69)
+template <class XF, class YF>
+struct MulBuild {
+  EwTriple T;
+  Pid2 pid;
+  Ptr2 own;
+  u64 lo, w;
+  XF xf;
+  YF yf;
+  __device__ void operator()(int slot, u64 j) const {
+    const u64 g = lo + j;
+    u64 a, b;
+    ew_ab(T, pid.v[slot], T.off + g, a, b);
+    own.p[slot][j] = xf(slot, g) - a;
+    own.p[slot][w + j] = yf(slot, g) - b;
+  }
+};
+
+template <class PF>
+struct MulCombine {
+  EwTriple T;
+  Pid2 pid;
+  CPtr2 own, peer;
+  u64 lo, w;
+  PF pf;
+  __device__ void operator()(int slot, u64 j) const {
+    const int party = pid.v[slot];
+    const u64 g = lo + j;
+    const u64* o = own.p[slot];
+    const u64* q = peer.p[slot];
+    const u64 e = o[j] + q[j];
+    const u64 d = o[w + j] + q[w + j];
+    u64 a, b, c;
+    ew_abc(T, party, T.off + g, a, b, c);
+    u64 z = c + (e * b + d * a);
+    if (party == 0) z += e * d;
+    pf(slot, party, g, z);
+  }
+};
+
+inline CPtr2 as_const(Ptr2 p) { return CPtr2{{p.p[0], p.p[1]}}; }
+
+// z = x*y with sources/sink functors; `chunks` reveals as in beaver_mul.
+template <class XF, class YF, class PF>
+void mul_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::string& tag, XF xf, YF yf,
+            PF pf) {
+  chunks = clamp_chunks(chunks, m);
+  std::vector<Open> opens(static_cast<size_t>(chunks));
+  const Pid2 pid = pids(s);
+  for (int k = 0; k < chunks; ++k) {
+    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
+    opens[k] = s.begin_open(2 * (hi - lo), Reduce::Sum);
+    launch_ew(s.stream, s.n_local, hi - lo, MulBuild<XF, YF>{T, pid, own_ptrs(opens[k]), lo, hi - lo, xf, yf});
+    s.post(opens[k], chunks == 1 ? tag : tag + ".chunk" + std::to_string(k));
+  }
+  for (int k = 0; k < chunks; ++k) {
+    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
+    s.wait(opens[k]);
+    launch_ew(s.stream, s.n_local, hi - lo,
+              MulCombine<PF>{T, pid, as_const(own_ptrs(opens[k])), peer_ptrs(opens[k]), lo, hi - lo, pf});
+    s.check();
+  }
+}
+
+// ---------------------------------------------------------------- Beaver square
+template <class XF>
+struct SqBuild {
+  EwTriple T;
+  Pid2 pid;
+  Ptr2 own;
+  u64 lo;
+  XF xf;
+  __device__ void operator()(int slot, u64 j) const {
+    const u64 g = lo + j;
+    own.p[slot][j] = xf(slot, g) - sq_a(T, pid.v[slot], T.off + g);
+  }
+};
+template <class PF>
+struct SqCombine {
+  EwTriple T;
+  Pid2 pid;
+  CPtr2 own, peer;
+  u64 lo;
+  PF pf;
+  __device__ void operator()(int slot, u64 j) const {
+    const int party = pid.v[slot];
+    const u64 g = lo + j;
+    const u64 e = own.p[slot][j] + peer.p[slot][j];
+    u64 a, c;
+    sq_ac(T, party, T.off + g, a, c);
+    u64 z = c + (e * a) * 2;
+    if (party == 0) z += e * e;
+    pf(slot, party, g, z);
+  }
+};
+
+template <class XF, class PF>
+void square_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::string& tag, XF xf, PF pf) {
+  chunks = clamp_chunks(chunks, m);
+  std::vector<Open> opens(static_cast<size_t>(chunks));
+  const Pid2 pid = pids(s);
+  for (int k = 0; k < chunks; ++k) {
+    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
+    opens[k] = s.begin_open(hi - lo, Reduce::Sum);
+    launch_ew(s.stream, s.n_local, hi - lo, SqBuild<XF>{T, pid, own_ptrs(opens[k]), lo, xf});
+    s.post(opens[k], chunks == 1 ? tag : tag + ".chunk" + std::to_string(k));
+  }
+  for (int k = 0; k < chunks; ++k) {
+    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
+    s.wait(opens[k]);
+    launch_ew(s.stream, s.n_local, hi - lo,
+              SqCombine<PF>{T, pid, as_const(own_ptrs(opens[k])), peer_ptrs(opens[k]), lo, pf});
+    s.check();
+  }
+}
+
+// ---------------------------------------------------------------- SPK adder rounds
+// H/protocols/adder.hpp:122-223. Round 0 is the generate AND on (x, y); rounds 1..L are
+// the prefix levels on the stacked (S, P) pair. One kernel settles round rp and issues
+// round rn for a lane [lo, lo+w); rn == L+1 finalises sum = p_orig ^ (s << 1).
+struct SpkLevel {
+  u64 in, out, mult;
+};
+
+struct SumSink {  // binary share of the sum
+  Ptr2 out;
+  __device__ void operator()(int slot, u64 g, u64 sum) const { out.p[slot][g] = sum; }
+};
+struct MsbSink {  // sign bit in position 0 (H/protocols/compare.hpp:57-62)
+  Ptr2 out;
+  __device__ void operator()(int slot, u64 g, u64 sum) const { out.p[slot][g] = sum >> 63; }
+};
+
+template <class XF, class YF, class FF>
+struct AdderRound {
+  int rp, rn, levels;
+  EwTriple Tp, Tn;
+  SpkLevel lp, ln;
+  Pid2 pid;
+  CPtr2 ownp, peerp;
+  Ptr2 ownn;
+  Ptr2 S, P, P0;
+  u64 lo, w, wmask;
+  XF xf;
+  YF yf;
+  FF ff;
+  __device__ void operator()(int slot, u64 j) const {
+    const int party = pid.v[slot];
+    const u64 g = lo + j;
+    if (rn == 0) {  // issue the generate AND: payload [x^a | y^b]
+      const u64 x = xf(slot, g), y = yf(slot, g);
+      P0.p[slot][g] = x ^ y;
+      u64 a, b;
+      ew_ab(Tn, party, Tn.off + g, a, b);
+      ownn.p[slot][j] = x ^ a;
+      ownn.p[slot][w + j] = y ^ b;
+      return;
+    }
+    const u64* o = ownp.p[slot];
+    const u64* q = peerp.p[slot];
+    u64 s, p;
+    if (rp == 0) {  // settle the generate AND (H/protocols/adder.hpp:209-223)
+      const u64 e = o[j] ^ q[j], d = o[w + j] ^ q[w + j];
+      u64 a, b, c;
+      ew_abc(Tp, party, Tp.off + g, a, b, c);
+      s = c ^ (e & b) ^ (d & a);
+      if (party == 0) s ^= e & d;
+      p = P0.p[slot][g];
+    } else {  // settle a prefix level (H/protocols/adder.hpp:142-165)
+      const u64 e0 = o[j] ^ q[j], e1 = o[w + j] ^ q[w + j];
+      const u64 d0 = o[2 * w + j] ^ q[2 * w + j], d1 = o[3 * w + j] ^ q[3 * w + j];
+      u64 a0, b0, c0, a1, b1, c1;
+      ew_abc(Tp, party, Tp.off + g, a0, b0, c0);
+      ew_abc(Tp, party, Tp.ghalf + Tp.off + g, a1, b1, c1);
+      u64 z0 = c0 ^ (e0 & b0) ^ (d0 & a0);
+      u64 z1 = c1 ^ (e1 & b1) ^ (d1 & a1);
+      if (party == 0) {
+        z0 ^= e0 & d0;
+        z1 ^= e1 & d1;
+      }
+      s = S.p[slot][g] ^ z0;
+      p = (P.p[slot][g] & ~lp.out) ^ z1;
+    }
+    if (rn <= levels) {  // issue level rn-1 (H/protocols/adder.hpp:122-140)
+      const u64 p0 = p & ln.out;
+      u64 a0, b0, a1, b1;
+      ew_ab(Tn, party, Tn.off + g, a0, b0);
+      ew_ab(Tn, party, Tn.ghalf + Tn.off + g, a1, b1);
+      u64* nn = ownn.p[slot];
+      nn[j] = p0 ^ a0;
+      nn[w + j] = p0 ^ a1;
+      nn[2 * w + j] = ((s & ln.in) * ln.mult) ^ b0;
+      nn[3 * w + j] = ((p & ln.in) * ln.mult) ^ b1;
+      S.p[slot][g] = s;
+      P.p[slot][g] = p;
+    } else {
+      ff(slot, g, (P0.p[slot][g] ^ (s << 1)) & wmask);
+    }
+  }
+};
+
+struct SpkConsts {
+  int levels;
+  u64 wmask;
+  SpkLevel lv[6];
+};
+SpkConsts make_spk_constants(int width);
+
+// Secure binary addition of XOR-shared operands given by sources; the sum goes to ff.
+template <class XF, class YF, class FF>
+void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& tag, XF xf, YF yf, FF ff) {
+  const SpkConsts c = make_spk_constants(opt.width);
+  const int chunks = clamp_chunks(opt.chunks, n);
+  const Pid2 pid = pids(s);
+  DT S = s.alloc(Shape{n}), P = s.alloc(Shape{n}), P0 = s.alloc(Shape{n});
+  const int rounds = 1 + c.levels;
+  Triple tr[7];
+  auto fetch_round = [&](int r) {
+    tr[r] = r == 0 ? s.fetch(TripleSpec::elementwise(TripleKind::Bin, Shape{n}), tag + ".g")
+                   : s.fetch(TripleSpec::elementwise(TripleKind::Bin, Shape{2, n}),
+                             tag + ".l" + std::to_string(r - 1), /*stacked=*/true);
+    tr[r].mark_consumed();
+  };
+  auto round_tag = [&](int r, int lane) {
+    std::string t = r == 0 ? tag + ".g" : tag + ".l" + std::to_string(r - 1);
+    return chunks > 1 && !opt.merged ? t + ".chunk" + std::to_string(lane) : t;
+  };
+  std::vector<Open> hs(static_cast<size_t>(chunks));
+  auto kernel = [&](int rp, int rn, int lane, Open* prev, Open* next) {
+    const auto rng_ = chunk_range(n, chunks, lane); const size_t lo = rng_.first, hi = rng_.second;
+    AdderRound<XF, YF, FF> k{};
+    k.rp = rp;
+    k.rn = rn;
+    k.levels = c.levels;
+    if (rp >= 0) k.Tp = tr[rp].ew;
+    if (rn <= c.levels) k.Tn = tr[rn].ew;
+    if (rp >= 1) k.lp = c.lv[rp - 1];
+    if (rn >= 1 && rn <= c.levels) k.ln = c.lv[rn - 1];
+    k.pid = pid;
+    if (prev) {
+      k.ownp = as_const(own_ptrs(*prev));
+      k.peerp = peer_ptrs(*prev);
+    }
+    if (next) k.ownn = own_ptrs(*next);
+    k.S = ptrs(S);
+    k.P = ptrs(P);
+    k.P0 = ptrs(P0);
+    k.lo = lo;
+    k.w = hi - lo;
+    k.wmask = c.wmask;
+    k.xf = xf;
+    k.yf = yf;
+    k.ff = ff;
+    launch_ew(s.stream, s.n_local, hi - lo, k);
+  };
+  fetch_round(0);
+  for (int lane = 0; lane < chunks; ++lane) {
+    const auto rng_ = chunk_range(n, chunks, lane); const size_t lo = rng_.first, hi = rng_.second;
+    hs[lane] = s.begin_open(2 * (hi - lo), Reduce::Xor);
+    kernel(-1, 0, lane, nullptr, &hs[lane]);
+    s.post(hs[lane], round_tag(0, lane));
+  }
+  for (int r = 1; r < rounds; ++r) {
+    fetch_round(r);
+    for (int lane = 0; lane < chunks; ++lane) {
+      const auto rng_ = chunk_range(n, chunks, lane); const size_t lo = rng_.first, hi = rng_.second;
+      Open next = s.begin_open(4 * (hi - lo), Reduce::Xor);
+      s.wait(hs[lane]);
+      kernel(r - 1, r, lane, &hs[lane], &next);
+      hs[lane] = std::move(next);
+      s.post(hs[lane], round_tag(r, lane));
+    }
+  }
+  for (int lane = 0; lane < chunks; ++lane) {
+    s.wait(hs[lane]);
+    kernel(rounds - 1, rounds, lane, &hs[lane], nullptr);
+  }
+  s.check();
+}
+
+}  // namespace mpcg

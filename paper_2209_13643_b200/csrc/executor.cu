@@ -1,0 +1,423 @@
+// Secure executor: per-layer dispatch, Beaver linear layers with the inter-linear-layer
+// delta pipeline, attention. Mirrors H/engine/executor.hpp:173-422 (values, tags and
+// collective order), on device shares.
+#include <algorithm>
+#include <cmath>
+
+#include "ew.cuh"
+#include "executor.hpp"
+#include "gemm.cuh"
+
+namespace mpcg {
+
+std::vector<Shape> infer_shapes(const ModelGraph& g) {
+  // H/engine/model.hpp:69-122
+  std::vector<Shape> out;
+  Shape cur = g.input;
+  for (const LayerSpec& l : g.layers) {
+    switch (l.kind) {
+      case LayerKind::Dense:
+        if (cur.empty()) throw Error(kConfigError, l.name + ": dense needs a trailing feature dim");
+        cur.back() = l.out;
+        break;
+      case LayerKind::Conv2d: {
+        if (cur.size() != 4) throw Error(kConfigError, l.name + ": conv2d expects NCHW input");
+        const size_t h = cur[2], w = cur[3];
+        if (h + 2 * l.pad < l.kernel || w + 2 * l.pad < l.kernel)
+          throw Error(kConfigError, l.name + ": kernel larger than padded input");
+        if (l.stride == 0) throw Error(kConfigError, l.name + ": stride must be >= 1");
+        cur = {cur[0], l.out, (h + 2 * l.pad - l.kernel) / l.stride + 1, (w + 2 * l.pad - l.kernel) / l.stride + 1};
+        break;
+      }
+      case LayerKind::Maxpool2d:
+        if (cur.size() != 4) throw Error(kConfigError, l.name + ": maxpool2d expects NCHW input");
+        if (cur[2] < l.kernel || cur[3] < l.kernel) throw Error(kConfigError, l.name + ": pool window larger than input");
+        if (l.stride == 0) throw Error(kConfigError, l.name + ": stride must be >= 1");
+        cur = {cur[0], cur[1], (cur[2] - l.kernel) / l.stride + 1, (cur[3] - l.kernel) / l.stride + 1};
+        break;
+      case LayerKind::Flatten: {
+        if (cur.empty()) throw Error(kConfigError, l.name + ": flatten on scalar");
+        size_t rest = 1;
+        for (size_t i = 1; i < cur.size(); ++i) rest *= cur[i];
+        cur = {cur[0], rest};
+        break;
+      }
+      case LayerKind::Attention:
+        if (cur.size() != 3) throw Error(kConfigError, l.name + ": attention expects [B, T, d]");
+        if (l.heads == 0 || cur[2] % l.heads != 0)
+          throw Error(kConfigError, l.name + ": head count must divide the model dim");
+        break;
+      case LayerKind::Relu:
+      case LayerKind::Softmax:
+        break;
+      case LayerKind::MeanPool:
+        if (cur.size() != 3) throw Error(kConfigError, l.name + ": mean_pool expects [B, T, d]");
+        cur = {cur[0], cur[2]};
+        break;
+    }
+    out.push_back(cur);
+  }
+  return out;
+}
+
+std::vector<std::pair<std::string, Shape>> model_weight_shapes(const ModelGraph& g) {
+  // H/engine/model.hpp:213-252
+  std::vector<std::pair<std::string, Shape>> out;
+  const auto shapes = infer_shapes(g);
+  Shape cur = g.input;
+  for (size_t i = 0; i < g.layers.size(); ++i) {
+    const LayerSpec& l = g.layers[i];
+    if (l.kind == LayerKind::Dense) {
+      out.push_back({l.name + ".W", Shape{cur.back(), l.out}});
+      if (l.bias) out.push_back({l.name + ".b", Shape{l.out}});
+    } else if (l.kind == LayerKind::Conv2d) {
+      out.push_back({l.name + ".W", Shape{cur[1] * l.kernel * l.kernel, l.out}});
+      if (l.bias) out.push_back({l.name + ".b", Shape{l.out}});
+    } else if (l.kind == LayerKind::Attention) {
+      const size_t d = cur[2];
+      out.push_back({l.name + ".Wqkv", Shape{d, 3 * d}});
+      if (l.bias) out.push_back({l.name + ".bqkv", Shape{3 * d}});
+      out.push_back({l.name + ".Wo", Shape{d, d}});
+      if (l.bias) out.push_back({l.name + ".bo", Shape{d}});
+    }
+    cur = shapes[i];
+  }
+  return out;
+}
+
+SecureExecutor::SecureExecutor(Session& s, ModelGraph g, bool public_weights, ExecOptions opt)
+    : s_(s), g_(std::move(g)), public_(public_weights), opt_(opt) {
+  shapes_ = infer_shapes(g_);
+  s_.cfg.frac_bits = g_.frac_bits;
+  s_.cfg.merged_adder = opt_.merged_adder;
+  if (opt_.pipelined) {
+    s_.cfg.chunks = opt_.chunks;
+    s_.cfg.chunk_threshold = opt_.chunk_threshold;
+  } else {
+    s_.cfg.chunks = 1;
+    s_.cfg.chunk_threshold = 0;
+  }
+  build_weight_ops();
+}
+
+SecureExecutor::~SecureExecutor() {
+  for (auto e : ev_) cudaEventDestroy(e);
+}
+
+void SecureExecutor::add_weight_op(const std::string& tag, const std::string& wkey, const std::string& bkey,
+                                   Shape x_shape) {
+  Shape wshape;
+  for (auto& [k, sh] : model_weight_shapes(g_))
+    if (k == wkey) wshape = sh;
+  WeightOp op;
+  op.tag = tag;
+  op.wkey = wkey;
+  op.bkey = bkey;
+  op.spec = TripleSpec::matmul_of(x_shape, wshape);
+  op.x_shape = std::move(x_shape);
+  wop_index_.emplace(op.tag, wops_.size());
+  wops_.push_back(std::move(op));
+}
+
+void SecureExecutor::build_weight_ops() {
+  // H/engine/executor.hpp:244-273
+  Shape cur = g_.input;
+  for (size_t i = 0; i < g_.layers.size(); ++i) {
+    const LayerSpec& l = g_.layers[i];
+    switch (l.kind) {
+      case LayerKind::Dense: {
+        const size_t in = cur.back();
+        add_weight_op(l.name + ".mm", l.name + ".W", l.bias ? l.name + ".b" : "", Shape{shape_numel(cur) / in, in});
+        break;
+      }
+      case LayerKind::Conv2d: {
+        const size_t rows = cur[0] * ((cur[2] + 2 * l.pad - l.kernel) / l.stride + 1) *
+                            ((cur[3] + 2 * l.pad - l.kernel) / l.stride + 1);
+        add_weight_op(l.name + ".mm", l.name + ".W", l.bias ? l.name + ".b" : "",
+                      Shape{rows, cur[1] * l.kernel * l.kernel});
+        break;
+      }
+      case LayerKind::Attention: {
+        const Shape x2{cur[0] * cur[1], cur[2]};
+        add_weight_op(l.name + ".qkv", l.name + ".Wqkv", l.bias ? l.name + ".bqkv" : "", x2);
+        add_weight_op(l.name + ".proj", l.name + ".Wo", l.bias ? l.name + ".bo" : "", x2);
+        break;
+      }
+      default:
+        break;
+    }
+    cur = shapes_[i];
+  }
+}
+
+void SecureExecutor::deal_weights(const std::vector<std::string>& names, const std::vector<const double*>& values,
+                                  u64 seed) {
+  const auto expected = model_weight_shapes(g_);
+  if (names.size() != expected.size()) throw Error(kConfigError, "weights entry count mismatch for model " + g_.name);
+  std::map<std::string, const double*> byname;
+  for (size_t i = 0; i < names.size(); ++i) byname[names[i]] = values[i];
+  std::map<std::string, Shape> shapes;
+  for (auto& [k, sh] : expected) {
+    if (!byname.count(k)) throw Error(kConfigError, "missing weight tensor: " + k);
+    shapes[k] = sh;
+  }
+  HostRng rng(seed, 0x3e1f);  // one stream over sorted names (H/engine/executor.hpp:49-59)
+  for (auto& [key, vals] : byname) {
+    const Shape& sh = shapes.at(key);
+    const size_t n = shape_numel(sh);
+    std::vector<u64> enc(n), host(n * s_.n_local);
+    for (size_t i = 0; i < n; ++i) enc[i] = encode_fixed(vals[i], g_.frac_bits);
+    if (public_) {
+      for (int sl = 0; sl < s_.n_local; ++sl) std::copy(enc.begin(), enc.end(), host.begin() + sl * n);
+    } else {
+      std::vector<u64> r(n);
+      for (size_t i = 0; i < n; ++i) r[i] = rng();
+      for (int sl = 0; sl < s_.n_local; ++sl)
+        for (size_t i = 0; i < n; ++i) host[sl * n + i] = s_.party_of[sl] == 0 ? enc[i] - r[i] : r[i];
+    }
+    w_[key] = s_.upload(sh, g_.frac_bits, host.data());
+  }
+}
+
+void SecureExecutor::set_weight(const std::string& name, const u64* host_words) {
+  for (auto& [k, sh] : model_weight_shapes(g_))
+    if (k == name) {
+      w_[k] = s_.upload(sh, g_.frac_bits, host_words);
+      return;
+    }
+  throw Error(kConfigError, "unknown weight tensor: " + name);
+}
+
+std::vector<std::string> SecureExecutor::linear_tags() const {
+  std::vector<std::string> t;
+  for (auto& op : wops_) t.push_back(op.tag);
+  return t;
+}
+
+// Fetch the op's triple and put its weight-side opening W - B on the wire
+// (H/engine/executor.hpp:279-286).
+void SecureExecutor::prepare(size_t i) {
+  WeightOp& op = wops_[i];
+  Triple t = s_.fetch(op.spec, op.tag);
+  t.mark_consumed();
+  const DT& W = w_.at(op.wkey);
+  const size_t nb = W.numel();
+  Open d = s_.begin_open(nb, Reduce::Sum);
+  delta_build_mem(s_, t, W.s, nb, d);
+  s_.post(d, op.tag + ".delta");
+  op.triple = t;
+  op.delta = std::move(d);
+}
+
+DT SecureExecutor::weight_matmul(size_t i, const DT& x, const ConvGeom* geom, bool col2im_out, Shape out_shape) {
+  WeightOp& op = wops_[i];
+  const u32 M = u32(op.x_shape[0]), K = u32(op.x_shape[1]);
+  const DT& W = w_.at(op.wkey);
+  const u32 N = u32(W.shape[1]);
+  const int f = g_.frac_bits;
+  Epi ep{};
+  ep.trunc_bits = f;  // finish_linear: truncate then add bias (H/engine/executor.hpp:319-324)
+  if (!op.bkey.empty()) {
+    const DT& b = w_.at(op.bkey);
+    for (int sl = 0; sl < s_.n_local; ++sl)
+      ep.bias[sl] = (!public_ || s_.party_of[sl] == 0) ? b.s[sl] : nullptr;
+  }
+  if (col2im_out) {
+    ep.col2im = 1;
+    ep.OHW = geom->OH * geom->OW;
+  }
+  DT z = s_.alloc(out_shape, g_.frac_bits);
+  if (public_) {  // local product, no triple, no opening (H/engine/executor.hpp:294-298)
+    DT cols = x;
+    if (geom) {
+      cols = s_.alloc(Shape{M, K}, x.scale);
+      const ConvGeom g = *geom;
+      const CPtr2 xp = cptrs(x);
+      const Ptr2 cp = ptrs(cols);
+      launch_ew(s_.stream, s_.n_local, u64(M) * K, [=] __device__(int slot, u64 idx) {
+        const u32 KK = g.C * g.k * g.k;
+        const u32 r = u32(idx / KK), c = u32(idx - u64(r) * KK);
+        const u32 ow = r % g.OW, oh = (r / g.OW) % g.OH, n = r / (g.OW * g.OH);
+        const u32 kj = c % g.k, ki = (c / g.k) % g.k, ci = c / (g.k * g.k);
+        const int ih = int(oh * g.stride + ki) - int(g.pad), iw = int(ow * g.stride + kj) - int(g.pad);
+        u64 v = 0;
+        if (ih >= 0 && iw >= 0 && ih < int(g.H) && iw < int(g.W))
+          v = xp.p[slot][((u64(n) * g.C + ci) * g.H + u32(ih)) * g.W + u32(iw)];
+        cp.p[slot][idx] = v;
+      });
+    }
+    public_gemm(s_, cols.s, W.s[0], z.s, M, N, K, ep);
+    return z;
+  }
+  if (!op.triple) prepare(i);
+  Triple t = *op.triple;
+  Open d = std::move(*op.delta);
+  op.triple.reset();
+  op.delta.reset();
+  const size_t na = size_t(M) * K;
+  Open e = s_.begin_open(na, Reduce::Sum);
+  if (geom)
+    eps_build_im2col(s_, t, x.s, *geom, 0, na, e);
+  else
+    eps_build_mem(s_, t, x.s, 0, na, e);
+  s_.post(e, op.tag + ".eps");
+  if (opt_.pipelined && wops_.size() > 1) {  // next op's delta leaves while this eps travels
+    const size_t next = (i + 1) % wops_.size();
+    if (!wops_[next].triple) prepare(next);
+  }
+  s_.wait(d);
+  s_.wait(e);
+  DT R = prepare_R(s_, t, d, W.numel());
+  DT L = prepare_L(s_, t, e, 0, na);
+  mm_combine(s_, t, L, na, R, W.numel(), z.s, 0, 1, M, N, K, false, false, 0, ep);
+  return z;
+}
+
+DT SecureExecutor::scale_and_rescale(const DT& x, double c) {
+  // H/engine/executor.hpp:326-330: multiply by encode(c), then truncate by f.
+  const u64 k = encode_fixed(c, g_.frac_bits);
+  const int f = g_.frac_bits;
+  DT z = s_.alloc(x.shape, x.scale);
+  const CPtr2 xp = cptrs(x);
+  const Ptr2 zp = ptrs(z);
+  launch_ew(s_.stream, s_.n_local, x.numel(),
+            [=] __device__(int slot, u64 i) { zp.p[slot][i] = sar64(xp.p[slot][i] * k, f); });
+  return z;
+}
+
+DT SecureExecutor::attention(const LayerSpec& l, const DT& x, const Shape& in_shape) {
+  // H/engine/executor.hpp:332-362
+  const size_t B = in_shape[0], T = in_shape[1], d = in_shape[2];
+  const size_t heads = l.heads, dh = d / heads;
+  const size_t qkv_op = wop_index_.at(l.name + ".qkv");
+  const size_t proj_op = wop_index_.at(l.name + ".proj");
+  DT x2 = reshape(x, Shape{B * T, d});
+  DT qkv = weight_matmul(qkv_op, x2, nullptr, false, Shape{B * T, 3 * d});
+  DT qkvh = s_.alloc(Shape{3, B * heads, T, dh}, qkv.scale);  // split_heads x3 in one gather
+  {
+    const CPtr2 src = cptrs(qkv);
+    const Ptr2 dst = ptrs(qkvh);
+    const u32 Tt = u32(T), D = u32(d), H = u32(heads), DH = u32(dh);
+    const u64 per = B * heads * T * dh;
+    launch_ew(s_.stream, s_.n_local, 3 * per, [=] __device__(int slot, u64 i) {
+      const u32 part = u32(i / per);
+      const u64 r = i - part * per;
+      const u32 j = u32(r % DH), t = u32((r / DH) % Tt), h = u32((r / (u64(DH) * Tt)) % H),
+                b = u32(r / (u64(DH) * Tt * H));
+      dst.p[slot][i] = src.p[slot][(u64(b) * Tt + t) * 3 * D + part * D + h * DH + j];
+    });
+  }
+  const size_t per = B * heads * T * dh;
+  DT q, k, v;
+  q = qkvh;
+  q.shape = Shape{B * heads, T, dh};
+  k = q;
+  v = q;
+  k.s[0] = qkvh.s[0] + per;
+  v.s[0] = qkvh.s[0] + 2 * per;
+  if (s_.n_local == 2) {
+    q.s[1] = qkvh.s[1];
+    k.s[1] = qkvh.s[1] + per;
+    v.s[1] = qkvh.s[1] + 2 * per;
+  }
+  DT scores = beaver_matmul(s_, q, k, true, l.name + ".qk", chunks_for(s_, B * heads * T * T));
+  scores = truncate_shares(s_, scores, g_.frac_bits);
+  scores = scale_and_rescale(scores, 1.0 / std::sqrt(static_cast<double>(dh)));
+  DT probs = softmax_shares(s_, scores, T, l.name + ".softmax");
+  DT mixed = beaver_matmul(s_, probs, v, false, l.name + ".av", chunks_for(s_, B * heads * T * dh));
+  mixed = truncate_shares(s_, mixed, g_.frac_bits);
+  DT merged = s_.alloc(Shape{B * T, d}, mixed.scale);  // merge_heads
+  {
+    const CPtr2 src = cptrs(mixed);
+    const Ptr2 dst = ptrs(merged);
+    const u32 Tt = u32(T), D = u32(d), H = u32(heads), DH = u32(dh);
+    launch_ew(s_.stream, s_.n_local, B * T * d, [=] __device__(int slot, u64 i) {
+      const u32 j = u32(i % DH), h = u32((i / DH) % H), t = u32((i / D) % Tt), b = u32(i / (u64(D) * Tt));
+      dst.p[slot][i] = src.p[slot][((u64(b) * H + h) * Tt + t) * DH + j];
+    });
+  }
+  DT out = weight_matmul(proj_op, merged, nullptr, false, Shape{B * T, d});
+  return reshape(out, Shape{B, T, d});
+}
+
+DT SecureExecutor::run_layer(const LayerSpec& l, const DT& x, const Shape& in_shape) {
+  switch (l.kind) {
+    case LayerKind::Dense: {
+      const size_t op = wop_index_.at(l.name + ".mm");
+      Shape out_shape = in_shape;
+      out_shape.back() = l.out;
+      DT x2 = reshape(x, wops_[op].x_shape);
+      return reshape(weight_matmul(op, x2, nullptr, false, Shape{wops_[op].x_shape[0], l.out}), out_shape);
+    }
+    case LayerKind::Conv2d: {
+      const size_t N = in_shape[0], C = in_shape[1], H = in_shape[2], W = in_shape[3];
+      const size_t OH = (H + 2 * l.pad - l.kernel) / l.stride + 1;
+      const size_t OW = (W + 2 * l.pad - l.kernel) / l.stride + 1;
+      const size_t op = wop_index_.at(l.name + ".mm");
+      ConvGeom g{u32(N), u32(C), u32(H), u32(W), u32(l.kernel), u32(l.stride), u32(l.pad), u32(OH), u32(OW)};
+      return weight_matmul(op, x, &g, true, Shape{N, l.out, OH, OW});
+    }
+    case LayerKind::Relu:
+      return relu_shares(s_, x, l.name);
+    case LayerKind::Maxpool2d:
+      return maxpool2d_shares(s_, x, in_shape[0], in_shape[1], in_shape[2], in_shape[3], l.kernel, l.stride, l.name);
+    case LayerKind::Flatten: {
+      size_t rest = 1;
+      for (size_t i = 1; i < in_shape.size(); ++i) rest *= in_shape[i];
+      return reshape(x, Shape{in_shape[0], rest});
+    }
+    case LayerKind::Attention:
+      return attention(l, x, in_shape);
+    case LayerKind::Softmax:
+      return softmax_shares(s_, x, in_shape.back(), l.name);
+    case LayerKind::MeanPool: {
+      const size_t B = in_shape[0], T = in_shape[1], d = in_shape[2];
+      const u64 k = encode_fixed(1.0 / static_cast<double>(T), g_.frac_bits);
+      const int f = g_.frac_bits;
+      DT out = s_.alloc(Shape{B, d}, x.scale);
+      const CPtr2 xp = cptrs(x);
+      const Ptr2 op = ptrs(out);
+      const u64 Tt = T, D = d;
+      launch_ew(s_.stream, s_.n_local, B * d, [=] __device__(int slot, u64 i) {
+        const u64 b = i / D, j = i - b * D;
+        u64 acc = 0;
+        for (u64 t = 0; t < Tt; ++t) acc += xp.p[slot][(b * Tt + t) * D + j];
+        op.p[slot][i] = sar64(acc * k, f);
+      });
+      return out;
+    }
+  }
+  throw Error(kProtocolError, "unhandled layer kind");
+}
+
+DT SecureExecutor::run(const DT& input) {
+  if (input.shape != g_.input) throw Error(kConfigError, "run: input shape mismatch");
+  for (auto& [k, sh] : model_weight_shapes(g_))
+    if (!w_.count(k)) throw Error(kConfigError, "missing weight tensor: " + k);
+  if (opt_.pipelined && !public_ && !wops_.empty() && !wops_[0].triple) prepare(0);
+  if (time_layers && ev_.size() < g_.layers.size() + 1) {
+    for (auto e : ev_) cudaEventDestroy(e);
+    ev_.assign(g_.layers.size() + 1, nullptr);
+    for (auto& e : ev_) MPCG_CUDA(cudaEventCreate(&e));
+  }
+  DT cur = input;
+  Shape cur_shape = g_.input;
+  if (time_layers) MPCG_CUDA(cudaEventRecord(ev_[0], s_.stream));
+  for (size_t i = 0; i < g_.layers.size(); ++i) {
+    cur = run_layer(g_.layers[i], cur, cur_shape);
+    cur_shape = shapes_[i];
+    if (time_layers) MPCG_CUDA(cudaEventRecord(ev_[i + 1], s_.stream));
+  }
+  if (time_layers) {
+    MPCG_CUDA(cudaEventSynchronize(ev_.back()));
+    timings.clear();
+    for (size_t i = 0; i < g_.layers.size(); ++i) {
+      float ms = 0;
+      MPCG_CUDA(cudaEventElapsedTime(&ms, ev_[i], ev_[i + 1]));
+      timings.push_back({g_.layers[i].name, ms});
+    }
+  }
+  return cur;
+}
+
+}  // namespace mpcg

@@ -1,0 +1,96 @@
+// Model graph + secure executor (H/engine/model.hpp, H/engine/executor.hpp).
+#pragma once
+
+#include <optional>
+
+#include "core.hpp"
+
+namespace mpcg {
+
+enum class LayerKind : int { Dense = 0, Conv2d, Relu, Maxpool2d, Flatten, Attention, Softmax, MeanPool };
+
+struct LayerSpec {
+  std::string name;
+  LayerKind kind = LayerKind::Dense;
+  size_t out = 0, kernel = 0, stride = 1, pad = 0, heads = 0;
+  bool bias = true;
+};
+
+struct ModelGraph {
+  std::string name = "model";
+  int frac_bits = 20;
+  Shape input;  // leading dim is the batch
+  std::vector<LayerSpec> layers;
+};
+
+std::vector<Shape> infer_shapes(const ModelGraph& g);
+std::vector<std::pair<std::string, Shape>> model_weight_shapes(const ModelGraph& g);
+
+// Host-side CounterRng (H/sharing/rng.hpp:10-32), used only at setup (dealing).
+struct HostRng {
+  u64 key, ctr = 0;
+  HostRng(u64 k, u64 stream = 0) : key(k ^ (stream * kPhi)) {}
+  u64 operator()() { return drw(key, ++ctr); }
+};
+
+struct ExecOptions {
+  bool pipelined = false;
+  int chunks = 4;
+  u64 chunk_threshold = u64(2) << 20;
+  bool merged_adder = true;
+};
+
+struct LayerTiming {  // per-layer device time of the last timed run (ms)
+  std::string name;
+  float ms = 0;
+};
+
+class SecureExecutor {
+ public:
+  SecureExecutor(Session& s, ModelGraph g, bool public_weights, ExecOptions opt);
+  ~SecureExecutor();
+
+  // Weights: every party derives its share from the session seed, standing in for the
+  // weight owner's dealer (H/engine/executor.hpp:49-68). `values` in sorted-name order.
+  void deal_weights(const std::vector<std::string>& names, const std::vector<const double*>& values,
+                    u64 seed);
+  void set_weight(const std::string& name, const u64* host_words);  // n_local*numel (or numel public)
+
+  DT run(const DT& input);
+
+  std::vector<std::string> linear_tags() const;
+  std::vector<LayerTiming> timings;
+  bool time_layers = false;
+
+  const ModelGraph& graph() const { return g_; }
+  const std::vector<Shape>& shapes() const { return shapes_; }
+
+ public:  // internal (extended __device__ lambdas need public enclosing members)
+  struct WeightOp {
+    std::string tag, wkey, bkey;
+    Shape x_shape;
+    TripleSpec spec;
+    std::optional<Triple> triple;
+    std::optional<Open> delta;
+  };
+  void add_weight_op(const std::string& tag, const std::string& wkey, const std::string& bkey, Shape x_shape);
+  void build_weight_ops();
+  void prepare(size_t i);
+  // x source: plain 2-D shares, or an NCHW tensor gathered by im2col when geom != null
+  DT weight_matmul(size_t i, const DT& x, const struct ConvGeom* geom, bool col2im_out, Shape out_shape);
+  DT attention(const LayerSpec& l, const DT& x, const Shape& in_shape);
+  DT run_layer(const LayerSpec& l, const DT& x, const Shape& in_shape);
+  DT scale_and_rescale(const DT& x, double c);
+
+  Session& s_;
+  ModelGraph g_;
+  std::vector<Shape> shapes_;
+  bool public_;
+  ExecOptions opt_;
+  std::map<std::string, DT> w_;
+  std::vector<WeightOp> wops_;
+  std::map<std::string, size_t> wop_index_;
+  std::vector<cudaEvent_t> ev_;
+};
+
+}  // namespace mpcg

@@ -1,0 +1,341 @@
+// Ring GEMM over Z_2^64 and the Beaver matmul combine.
+//
+// The combine of a matmul triple (H/protocols/beaver.hpp:175-180) is evaluated as ONE
+// multi-segment GEMM per party, exact in Z_2^64 by distributivity:
+//   party 1: z = +r_C + E*r_B + r_A*F
+//   party 0: z = -r_C + A*B + E*(b0 + F) + a0*F        (A*B is the dealer's C = A*B)
+// with E, F the opened eps/delta. The epilogue fuses the 2PC truncation, the bias and
+// the conv col2im scatter (H/engine/executor.hpp:110-136,319-324).
+#include "ew.cuh"
+#include "gemm.cuh"
+
+namespace mpcg {
+
+namespace {
+
+template <int BM, int BN, int TM, int TN>
+__global__ void __launch_bounds__(256) ring_gemm_simt(GemmArgs a) {
+  constexpr int BK = 16, TX = BN / TN, TY = BM / TM;
+  static_assert(TX * TY == 256, "256 threads");
+  __shared__ u64 As[BK][BM + 1];
+  __shared__ u64 Bs[BK][BN + 1];
+  const int slot = blockIdx.z % a.nslots;
+  const u32 b = blockIdx.z / a.nslots;
+  const GemmSlotArgs& S = a.sl[slot];
+  const u32 M = a.M, N = a.N, K = a.K;
+  const u32 m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  u64 acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0;
+
+  for (int sg = 0; sg < S.nseg; ++sg) {
+    const u64* L = S.L[sg] + u64(b) * S.sL[sg];
+    const u64* R = S.R[sg] + u64(b) * S.sR[sg];
+    for (u32 k0 = 0; k0 < K; k0 += BK) {
+      for (int e = threadIdx.x; e < BM * BK; e += 256) {
+        const int kk = e % BK, mm = e / BK;
+        u64 v = 0;
+        if (m0 + mm < M && k0 + kk < K) v = L[u64(m0 + mm) * K + k0 + kk];
+        As[kk][mm] = v;
+      }
+      if (!a.tb) {
+        for (int e = threadIdx.x; e < BN * BK; e += 256) {
+          const int nn = e % BN, kk = e / BN;
+          u64 v = 0;
+          if (k0 + kk < K && n0 + nn < N) v = R[u64(k0 + kk) * N + n0 + nn];
+          Bs[kk][nn] = v;
+        }
+      } else {
+        for (int e = threadIdx.x; e < BN * BK; e += 256) {
+          const int kk = e % BK, nn = e / BK;
+          u64 v = 0;
+          if (k0 + kk < K && n0 + nn < N) v = R[u64(n0 + nn) * K + k0 + kk];
+          Bs[kk][nn] = v;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        u64 ar[TM], br[TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) ar[i] = As[kk][ty + i * TY];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) br[j] = Bs[kk][tx + j * TX];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] += ar[i] * br[j];
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const u32 m = m0 + ty + i * TY;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const u32 n = n0 + tx + j * TX;
+      if (n >= N) continue;
+      gemm_epilogue(a, S, b, m, n, acc[i][j]);
+    }
+  }
+}
+
+template <int BM, int BN, int TM, int TN>
+void launch_simt(const GemmArgs& a, cudaStream_t st) {
+  dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, a.nslots * a.nbatch);
+  ring_gemm_simt<BM, BN, TM, TN><<<grid, 256, 0, st>>>(a);
+  MPCG_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+void ring_gemm_launch(Session& s, const GemmArgs& a) {
+  if (a.M == 0 || a.N == 0 || a.nbatch == 0) return;
+  if (a.M > 65535u * 64u) throw Error(kShapeError, "ring_gemm: M too large");
+  if (ring_gemm_tc_try(s, a)) return;  // tcgen05 int8-limb path when the shape qualifies
+  if (a.N <= 8)
+    launch_simt<128, 8, 4, 1>(a, s.stream);
+  else if (a.N <= 16)
+    launch_simt<128, 16, 8, 1>(a, s.stream);
+  else if (a.N <= 32)
+    launch_simt<64, 32, 4, 2>(a, s.stream);
+  else
+    launch_simt<64, 64, 4, 4>(a, s.stream);
+  s.check();
+}
+
+// ---------------------------------------------------------------- matmul triple operands
+namespace {
+__device__ __forceinline__ u64 mm_a_share(const MmTriple& t, int party, u64 i) {
+  const u64 ra = mm_rA(t, i);
+  return party ? ra : mm_A(t, i) - ra;
+}
+__device__ __forceinline__ u64 mm_b_share(const MmTriple& t, int party, u64 j) {
+  const u64 rb = mm_rB(t, j);
+  return party ? rb : mm_B(t, j) - rb;
+}
+}  // namespace
+
+// own payload = y - b  (delta; H/engine/executor.hpp:283, H/protocols/beaver.hpp:194)
+template <class YF>
+static void delta_build(Session& s, const Triple& t, size_t nb, Open& o, YF yf) {
+  const Pid2 pid = pids(s);
+  const Ptr2 own = own_ptrs(o);
+  const MmTriple mm = t.mm;
+  launch_ew(s.stream, s.n_local, nb, [=] __device__(int slot, u64 j) {
+    own.p[slot][j] = yf(slot, j) - mm_b_share(mm, pid.v[slot], j);
+  });
+}
+
+void delta_build_mem(Session& s, const Triple& t, const u64* const y[2], size_t nb, Open& o) {
+  delta_build(s, t, nb, o, SrcMem{CPtr2{{y[0], y[1]}}});
+}
+
+// own payload = x - a over A elements [a_off, a_off + na)  (eps; beaver.hpp:205,216)
+void eps_build_mem(Session& s, const Triple& t, const u64* const x[2], size_t a_off, size_t na, Open& o) {
+  const Pid2 pid = pids(s);
+  const Ptr2 own = own_ptrs(o);
+  const MmTriple mm = t.mm;
+  const CPtr2 xp{{x[0], x[1]}};
+  launch_ew(s.stream, s.n_local, na, [=] __device__(int slot, u64 j) {
+    own.p[slot][j] = xp.p[slot][a_off + j] - mm_a_share(mm, pid.v[slot], a_off + j);
+  });
+}
+
+// im2col-fused eps build for conv layers (H/engine/executor.hpp:82-108): row=(n,oh,ow),
+// col=(ci,ki,kj), padding taps read zero.
+void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const ConvGeom& gm, size_t a_off,
+                      size_t na, Open& o) {
+  const Pid2 pid = pids(s);
+  const Ptr2 own = own_ptrs(o);
+  const MmTriple mm = t.mm;
+  const CPtr2 xp{{x[0], x[1]}};
+  const ConvGeom g = gm;
+  launch_ew(s.stream, s.n_local, na, [=] __device__(int slot, u64 j) {
+    const u64 idx = a_off + j;
+    const u32 KK = g.C * g.k * g.k;
+    const u32 r = u32(idx / KK), c = u32(idx - u64(r) * KK);
+    const u32 ow = r % g.OW, oh = (r / g.OW) % g.OH, n = r / (g.OW * g.OH);
+    const u32 kj = c % g.k, ki = (c / g.k) % g.k, ci = c / (g.k * g.k);
+    const int ih = int(oh * g.stride + ki) - int(g.pad), iw = int(ow * g.stride + kj) - int(g.pad);
+    u64 v = 0;
+    if (ih >= 0 && iw >= 0 && ih < int(g.H) && iw < int(g.W))
+      v = xp.p[slot][((u64(n) * g.C + ci) * g.H + u32(ih)) * g.W + u32(iw)];
+    own.p[slot][j] = v - mm_a_share(mm, pid.v[slot], idx);
+  });
+}
+
+// R operands per slot (3 x nb words): p0 {B, b0+F, F}, p1 {r_B, F}; F = own + peer delta.
+DT prepare_R(Session& s, const Triple& t, const Open& d, size_t nb) {
+  DT r = s.alloc(Shape{3, nb});
+  const Pid2 pid = pids(s);
+  const CPtr2 ow = as_const(own_ptrs(d)), pe = peer_ptrs(d);
+  const Ptr2 rp = ptrs(r);
+  const MmTriple mm = t.mm;
+  launch_ew(s.stream, s.n_local, nb, [=] __device__(int slot, u64 j) {
+    const u64 F = ow.p[slot][j] + pe.p[slot][j];
+    const u64 rb = mm_rB(mm, j);
+    u64* o = rp.p[slot];
+    if (pid.v[slot] == 0) {
+      const u64 B = mm_B(mm, j);
+      o[j] = B;
+      o[nb + j] = (B - rb) + F;
+      o[2 * nb + j] = F;
+    } else {
+      o[j] = rb;
+      o[nb + j] = F;
+    }
+  });
+  return r;
+}
+
+// L operands per slot (3 x na words) for A elements [a_off, a_off+na):
+// p0 {A, E, a0 = A - r_A}, p1 {E, r_A}; E = own + peer eps.
+DT prepare_L(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na) {
+  DT l = s.alloc(Shape{3, na});
+  const Pid2 pid = pids(s);
+  const CPtr2 ow = as_const(own_ptrs(e)), pe = peer_ptrs(e);
+  const Ptr2 lp = ptrs(l);
+  const MmTriple mm = t.mm;
+  launch_ew(s.stream, s.n_local, na, [=] __device__(int slot, u64 j) {
+    const u64 E = ow.p[slot][j] + pe.p[slot][j];
+    const u64 ra = mm_rA(mm, a_off + j);
+    u64* o = lp.p[slot];
+    if (pid.v[slot] == 0) {
+      const u64 A = mm_A(mm, a_off + j);
+      o[j] = A;
+      o[na + j] = E;
+      o[2 * na + j] = A - ra;
+    } else {
+      o[j] = E;
+      o[na + j] = ra;
+    }
+  });
+  return l;
+}
+
+// z[out_off..] = combine for one chunk. L/R from prepare_L/prepare_R; batched when nbatch>1.
+void mm_combine(Session& s, const Triple& t, const DT& L, size_t na, const DT& R, size_t nb, u64* const out[2],
+                size_t out_off, u32 nbatch, u32 M, u32 N, u32 K, bool tb, bool batched_r, size_t r_batch0,
+                const Epi& ep) {
+  GemmArgs a{};
+  a.nslots = s.n_local;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.tb = tb;
+  a.nbatch = nbatch;
+  a.trunc_bits = ep.trunc_bits;
+  a.col2im = ep.col2im;
+  a.OHW = ep.OHW;
+  const u64 sL = u64(M) * K, sR = batched_r ? u64(K) * N : 0;
+  const u64 rboff = batched_r ? r_batch0 * u64(K) * N : 0;
+  for (int i = 0; i < s.n_local; ++i) {
+    GemmSlotArgs& S = a.sl[i];
+    const u64* Lp = L.s[i];
+    const u64* Rp = R.s[i];
+    S.out = out[i] + out_off;
+    S.bias = ep.bias[i];
+    S.ckey = t.mm.key;
+    S.cbase = 1 + 2 * t.mm.na + 2 * t.mm.nb + t.mm.offC + out_off;
+    if (s.party_of[i] == 0) {
+      S.nseg = 3;
+      S.cterm = -1;
+      for (int g = 0; g < 3; ++g) {
+        S.L[g] = Lp + g * na;
+        S.R[g] = Rp + g * nb + rboff;
+      }
+    } else {
+      S.nseg = 2;
+      S.cterm = +1;
+      S.L[0] = Lp;          // E
+      S.R[0] = Rp + rboff;  // r_B
+      S.L[1] = Lp + na;     // r_A
+      S.R[1] = Rp + nb + rboff;  // F
+    }
+    for (int g = 0; g < 3; ++g) {
+      S.sL[g] = sL;
+      S.sR[g] = sR;
+    }
+  }
+  ring_gemm_launch(s, a);
+}
+
+// Public-weight product x2d * W (H/engine/executor.hpp:294-298): one segment, no triple.
+void public_gemm(Session& s, const u64* const x[2], const u64* W, u64* const out[2], u32 M, u32 N, u32 K,
+                 const Epi& ep) {
+  GemmArgs a{};
+  a.nslots = s.n_local;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.nbatch = 1;
+  a.trunc_bits = ep.trunc_bits;
+  a.col2im = ep.col2im;
+  a.OHW = ep.OHW;
+  for (int i = 0; i < s.n_local; ++i) {
+    GemmSlotArgs& S = a.sl[i];
+    S.nseg = 1;
+    S.L[0] = x[i];
+    S.R[0] = W;
+    S.out = out[i];
+    S.bias = ep.bias[i];
+  }
+  ring_gemm_launch(s, a);
+}
+
+// ---------------------------------------------------------------- beaver_matmul
+DT beaver_matmul(Session& s, const DT& x, const DT& y, bool transpose_b, const std::string& tag, int chunks) {
+  if (x.shape.size() < 2 || y.shape.size() < 2) throw Error(kShapeError, "matmul: operands must have rank >= 2");
+  const bool batched_b = y.shape.size() > 2;
+  Triple t = s.fetch(TripleSpec::matmul_of(x.shape, y.shape, transpose_b), tag, batched_b);
+  t.mark_consumed();
+  const size_t M = x.shape[x.shape.size() - 2], K = x.shape.back();
+  const size_t N = transpose_b ? y.shape[y.shape.size() - 2] : y.shape.back();
+  const size_t nb = y.numel(), na = x.numel();
+  const size_t batch = na / (M * K);
+  if (batched_b && nb / (K * N) != batch) throw Error(kShapeError, "matmul: batch mismatch");
+
+  Open hd = s.begin_open(nb, Reduce::Sum);
+  delta_build_mem(s, t, y.s, nb, hd);
+  s.post(hd, tag + ".delta");
+
+  const size_t rows = batched_b ? batch : na / K;
+  const size_t row_w = batched_b ? M * K : K;
+  chunks = clamp_chunks(chunks, rows);
+  std::vector<Open> he(static_cast<size_t>(chunks));
+  for (int k = 0; k < chunks; ++k) {
+    const auto r = chunk_range(rows, chunks, k);
+    he[k] = s.begin_open((r.second - r.first) * row_w, Reduce::Sum);
+    eps_build_mem(s, t, x.s, r.first * row_w, (r.second - r.first) * row_w, he[k]);
+    s.post(he[k], chunks == 1 ? tag + ".eps" : tag + ".eps.chunk" + std::to_string(k));
+  }
+  s.wait(hd);
+  DT R = prepare_R(s, t, hd, nb);
+  Shape out_shape(x.shape.begin(), x.shape.end() - 1);
+  out_shape.push_back(N);
+  DT z = s.alloc(out_shape, x.scale);
+  const size_t out_row_w = batched_b ? M * N : N;
+  for (int k = 0; k < chunks; ++k) {
+    const auto r = chunk_range(rows, chunks, k);
+    const size_t cnt = r.second - r.first;
+    s.wait(he[k]);
+    DT L = prepare_L(s, t, he[k], r.first * row_w, cnt * row_w);
+    Epi ep{};
+    if (batched_b)
+      mm_combine(s, t, L, cnt * row_w, R, nb, z.s, r.first * out_row_w, u32(cnt), u32(M), u32(N), u32(K),
+                 transpose_b, true, r.first, ep);
+    else
+      mm_combine(s, t, L, cnt * row_w, R, nb, z.s, r.first * out_row_w, 1, u32(cnt), u32(N), u32(K),
+                 transpose_b, false, 0, ep);
+  }
+  s.check();
+  return z;
+}
+
+}  // namespace mpcg

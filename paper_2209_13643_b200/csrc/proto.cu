@@ -1,0 +1,547 @@
+// Secure protocols on device shares: Beaver mul/square/AND, SPK adder, conversions,
+// comparison-based activations and the exp/reciprocal/softmax chain.
+// Reference: H/protocols/{beaver,adder,compare,trunc}.hpp, H/nonlinear/{approx,activations}.hpp.
+#include "ew.cuh"
+
+namespace mpcg {
+
+void require_same_shape(const DT& a, const DT& b, const char* op) {
+  if (a.shape != b.shape)
+    throw Error(kShapeError, std::string(op) + ": shape mismatch " + shape_str(a.shape) + " vs " +
+                                 shape_str(b.shape));
+}
+
+int clamp_chunks(int chunks, size_t numel) {
+  if (chunks < 1) chunks = 1;
+  return int(std::min<size_t>(size_t(chunks), numel ? numel : 1));
+}
+
+int chunks_for(const Session& s, size_t numel) {
+  if (s.cfg.chunks <= 1) return 1;
+  if (s.cfg.chunk_threshold != 0 && numel * sizeof(u64) < s.cfg.chunk_threshold) return 1;
+  return s.cfg.chunks;
+}
+
+static AdderOptions adder_for(const Session& s, size_t numel) {
+  AdderOptions o;
+  o.merged = s.cfg.merged_adder;
+  o.chunks = chunks_for(s, numel);
+  return o;
+}
+
+SpkConsts make_spk_constants(int width) {
+  // H/protocols/adder.hpp:37-57
+  if (width < 2 || width > 64 || (width & (width - 1)))
+    throw Error(kConfigError, "adder width must be a power of two in [2, 64]");
+  SpkConsts c{};
+  int m = 0;
+  while ((1 << m) < width) ++m;
+  c.levels = m;
+  c.wmask = width == 64 ? ~u64(0) : ((u64(1) << width) - 1);
+  for (int i = 0; i < m; ++i) {
+    u64 in = 0, out = 0;
+    const u64 half = u64(1) << i;
+    for (int p = 0; p < width; ++p) {
+      const u64 r = u64(p) & (2 * half - 1);
+      if (r == half - 1) in |= u64(1) << p;
+      if (r >= half) out |= u64(1) << p;
+    }
+    c.lv[i] = SpkLevel{in, out, ((u64(1) << half) - 1) << 1};
+  }
+  return c;
+}
+
+// ---------------------------------------------------------------- local helpers
+DT reshape(const DT& a, Shape shape) {
+  if (shape_numel(shape) != a.numel())
+    throw Error(kShapeError, "reshape: numel mismatch " + shape_str(a.shape) + " -> " + shape_str(shape));
+  DT t = a;
+  t.shape = std::move(shape);
+  return t;
+}
+
+DT add_public(Session& s, const DT& x, u64 v) {
+  DT z = s.alloc(x.shape, x.scale);
+  const Pid2 pid = pids(s);
+  const CPtr2 xp = cptrs(x);
+  const Ptr2 zp = ptrs(z);
+  launch_ew(s.stream, s.n_local, x.numel(), [=] __device__(int slot, u64 i) {
+    zp.p[slot][i] = xp.p[slot][i] + (pid.v[slot] == 0 ? v : 0);
+  });
+  return z;
+}
+
+DT scale_public(Session& s, const DT& x, u64 k) {
+  DT z = s.alloc(x.shape, x.scale);
+  const CPtr2 xp = cptrs(x);
+  const Ptr2 zp = ptrs(z);
+  launch_ew(s.stream, s.n_local, x.numel(), [=] __device__(int slot, u64 i) { zp.p[slot][i] = xp.p[slot][i] * k; });
+  return z;
+}
+
+DT sub_t(Session& s, const DT& a, const DT& b) {
+  require_same_shape(a, b, "sub");
+  DT z = s.alloc(a.shape, a.scale);
+  const CPtr2 ap = cptrs(a), bp = cptrs(b);
+  const Ptr2 zp = ptrs(z);
+  launch_ew(s.stream, s.n_local, a.numel(),
+            [=] __device__(int slot, u64 i) { zp.p[slot][i] = ap.p[slot][i] - bp.p[slot][i]; });
+  return z;
+}
+
+DT add_t(Session& s, const DT& a, const DT& b) {
+  require_same_shape(a, b, "add");
+  DT z = s.alloc(a.shape, a.scale);
+  const CPtr2 ap = cptrs(a), bp = cptrs(b);
+  const Ptr2 zp = ptrs(z);
+  launch_ew(s.stream, s.n_local, a.numel(),
+            [=] __device__(int slot, u64 i) { zp.p[slot][i] = ap.p[slot][i] + bp.p[slot][i]; });
+  return z;
+}
+
+// 2PC truncation: local arithmetic shift of each share (H/protocols/trunc.hpp:25-42).
+DT truncate_shares(Session& s, const DT& x, int bits) {
+  DT z = s.alloc(x.shape, x.scale);
+  const CPtr2 xp = cptrs(x);
+  const Ptr2 zp = ptrs(z);
+  launch_ew(s.stream, s.n_local, x.numel(),
+            [=] __device__(int slot, u64 i) { zp.p[slot][i] = sar64(xp.p[slot][i], bits); });
+  return z;
+}
+
+// Reveal: every slot receives the reconstructed value (Communicator::reveal).
+DT open_value(Session& s, const DT& x, Reduce kind, const std::string& tag) {
+  const size_t n = x.numel();
+  DT z = s.alloc(x.shape, x.scale);
+  Open o = s.begin_open(n, kind);
+  const Ptr2 own = own_ptrs(o);
+  const CPtr2 xp = cptrs(x);
+  launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) { own.p[slot][i] = xp.p[slot][i]; });
+  s.post(o, tag);
+  s.wait(o);
+  const CPtr2 ow = as_const(own_ptrs(o)), pe = peer_ptrs(o);
+  const Ptr2 zp = ptrs(z);
+  const int xr = kind == Reduce::Xor;
+  launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) {
+    const u64 a = ow.p[slot][i], b = pe.p[slot][i];
+    zp.p[slot][i] = xr ? (a ^ b) : (a + b);
+  });
+  s.check();
+  return z;
+}
+
+// ---------------------------------------------------------------- Beaver ops
+DT beaver_mul(Session& s, const DT& x, const DT& y, const std::string& tag, int chunks) {
+  require_same_shape(x, y, "beaver_mul");
+  Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Arith, x.shape), tag);
+  t.mark_consumed();
+  DT z = s.alloc(x.shape, x.scale);
+  mul_op(s, t.ew, x.numel(), chunks, tag, SrcMem{cptrs(x)}, SrcMem{cptrs(y)}, SinkStore{ptrs(z)});
+  return z;
+}
+
+DT beaver_square(Session& s, const DT& x, const std::string& tag, int chunks) {
+  Triple t = s.fetch(TripleSpec::square_of(x.shape), tag);
+  t.mark_consumed();
+  DT z = s.alloc(x.shape, x.scale);
+  square_op(s, t.ew, x.numel(), chunks, tag, SrcMem{cptrs(x)}, SinkStore{ptrs(z)});
+  return z;
+}
+
+namespace {
+template <class XF, class YF>
+struct AndBuild {
+  EwTriple T;
+  Pid2 pid;
+  Ptr2 own;
+  u64 lo, w;
+  XF xf;
+  YF yf;
+  __device__ void operator()(int slot, u64 j) const {
+    const u64 g = lo + j;
+    u64 a, b;
+    ew_ab(T, pid.v[slot], T.off + g, a, b);
+    own.p[slot][j] = xf(slot, g) ^ a;
+    own.p[slot][w + j] = yf(slot, g) ^ b;
+  }
+};
+struct AndCombine {
+  EwTriple T;
+  Pid2 pid;
+  CPtr2 own, peer;
+  Ptr2 out;
+  u64 lo, w;
+  __device__ void operator()(int slot, u64 j) const {
+    const int party = pid.v[slot];
+    const u64 g = lo + j;
+    const u64 e = own.p[slot][j] ^ peer.p[slot][j];
+    const u64 d = own.p[slot][w + j] ^ peer.p[slot][w + j];
+    u64 a, b, c;
+    ew_abc(T, party, T.off + g, a, b, c);
+    u64 z = c ^ (e & b) ^ (d & a);
+    if (party == 0) z ^= e & d;
+    out.p[slot][g] = z;
+  }
+};
+}  // namespace
+
+DT beaver_and(Session& s, const DT& x, const DT& y, const std::string& tag, int chunks) {
+  require_same_shape(x, y, "beaver_and");
+  Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Bin, x.shape), tag);
+  t.mark_consumed();
+  const size_t m = x.numel();
+  chunks = clamp_chunks(chunks, m);
+  DT z = s.alloc(x.shape, x.scale);
+  const Pid2 pid = pids(s);
+  std::vector<Open> opens(static_cast<size_t>(chunks));
+  for (int k = 0; k < chunks; ++k) {
+    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
+    opens[k] = s.begin_open(2 * (hi - lo), Reduce::Xor);
+    launch_ew(s.stream, s.n_local, hi - lo,
+              AndBuild<SrcMem, SrcMem>{t.ew, pid, own_ptrs(opens[k]), lo, hi - lo, SrcMem{cptrs(x)}, SrcMem{cptrs(y)}});
+    s.post(opens[k], chunks == 1 ? tag : tag + ".chunk" + std::to_string(k));
+  }
+  for (int k = 0; k < chunks; ++k) {
+    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
+    s.wait(opens[k]);
+    launch_ew(s.stream, s.n_local, hi - lo,
+              AndCombine{t.ew, pid, as_const(own_ptrs(opens[k])), peer_ptrs(opens[k]), ptrs(z), lo, hi - lo});
+  }
+  s.check();
+  return z;
+}
+
+// ---------------------------------------------------------------- adder / conversions
+DT binary_add(Session& s, const DT& x, const DT& y, const AdderOptions& opt, const std::string& tag) {
+  require_same_shape(x, y, "binary_add");
+  DT z = s.alloc(x.shape, x.scale);
+  adder_op(s, x.numel(), opt, tag, SrcMem{cptrs(x)}, SrcMem{cptrs(y)}, SumSink{ptrs(z)});
+  return z;
+}
+
+namespace {
+// a2b parts in 2PC (H/protocols/compare.hpp:31-53): party 0 adds (keep0, r1), party 1 (r0, keep1).
+struct PartX {
+  Pid2 pid;
+  CPtr2 keep, peer;
+  __device__ u64 operator()(int slot, u64 g) const {
+    return pid.v[slot] == 0 ? keep.p[slot][g] : peer.p[slot][g];
+  }
+};
+struct PartY {
+  Pid2 pid;
+  CPtr2 keep, peer;
+  __device__ u64 operator()(int slot, u64 g) const {
+    return pid.v[slot] == 0 ? peer.p[slot][g] : keep.p[slot][g];
+  }
+};
+
+// Mask draw + p2p send of r, keep = x ^ r. Returns the keep tensor and the open.
+template <class XF>
+DT a2b_mask(Session& s, size_t n, XF xf, Open& o) {
+  DT keep = s.alloc(Shape{n});
+  const u64 base = s.take_mask(n);
+  o = s.begin_open(n, Reduce::Sum);
+  const Ptr2 own = own_ptrs(o), kp = ptrs(keep);
+  const u64 k0 = s.mask_key[0], k1 = s.mask_key[1];
+  launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) {
+    const u64 r = drw(slot == 0 ? k0 : k1, base + 1 + i);
+    own.p[slot][i] = r;
+    kp.p[slot][i] = xf(slot, i) ^ r;
+  });
+  s.post(o, "", /*p2p=*/true);
+  s.wait(o);
+  return keep;
+}
+
+template <class XF, class FF>
+void a2b_op(Session& s, size_t n, const AdderOptions& opt, const std::string& tag, XF xf, FF ff) {
+  Open o;
+  DT keep = a2b_mask(s, n, xf, o);
+  const Pid2 pid = pids(s);
+  adder_op(s, n, opt, tag + ".add1", PartX{pid, cptrs(keep), peer_ptrs(o)},
+           PartY{pid, cptrs(keep), peer_ptrs(o)}, ff);
+}
+
+// b2a_bit (H/protocols/compare.hpp:67-83, n=2): acc = b0 on party 0, bq = b1 on party 1;
+// result acc + bq - 2*acc*bq.
+struct BitAcc {
+  Pid2 pid;
+  CPtr2 b;
+  __device__ u64 operator()(int slot, u64 g) const { return pid.v[slot] == 0 ? (b.p[slot][g] & 1) : 0; }
+};
+struct BitBq {
+  Pid2 pid;
+  CPtr2 b;
+  __device__ u64 operator()(int slot, u64 g) const { return pid.v[slot] == 1 ? (b.p[slot][g] & 1) : 0; }
+};
+struct B2aSink {
+  CPtr2 b;
+  Ptr2 out;
+  __device__ void operator()(int slot, int, u64 g, u64 prod) const {
+    out.p[slot][g] = (b.p[slot][g] & 1) - (prod + prod);
+  }
+};
+}  // namespace
+
+DT a2b(Session& s, const DT& x, const AdderOptions& opt, const std::string& tag) {
+  DT z = s.alloc(x.shape, x.scale);
+  a2b_op(s, x.numel(), opt, tag, SrcMem{cptrs(x)}, SumSink{ptrs(z)});
+  return z;
+}
+
+DT msb(Session& s, const DT& x, const AdderOptions& opt, const std::string& tag) {
+  DT z = s.alloc(x.shape, x.scale);
+  a2b_op(s, x.numel(), opt, tag, SrcMem{cptrs(x)}, MsbSink{ptrs(z)});
+  return z;
+}
+
+DT b2a_bit(Session& s, const DT& b, const std::string& tag, int chunks) {
+  Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Arith, b.shape), tag + ".m1");
+  t.mark_consumed();
+  DT z = s.alloc(b.shape, b.scale);
+  const Pid2 pid = pids(s);
+  mul_op(s, t.ew, b.numel(), chunks, tag + ".m1", BitAcc{pid, cptrs(b)}, BitBq{pid, cptrs(b)},
+         B2aSink{cptrs(b), ptrs(z)});
+  return z;
+}
+
+DT less_than(Session& s, const DT& x, const DT& y, const AdderOptions& opt, const std::string& tag) {
+  require_same_shape(x, y, "less_than");
+  DT m = s.alloc(x.shape, 0);
+  a2b_op(s, x.numel(), opt, tag + ".msb", SrcSub{cptrs(x), cptrs(y)},
+         MsbSink{ptrs(m)});
+  return b2a_bit(s, m, tag + ".b2a", opt.chunks);
+}
+
+// ---------------------------------------------------------------- activations
+namespace {
+struct SinkXMinus {  // out = x - z  (relu gate, H/nonlinear/activations.hpp:46)
+  CPtr2 x;
+  Ptr2 out;
+  __device__ void operator()(int slot, int, u64 g, u64 z) const { out.p[slot][g] = x.p[slot][g] - z; }
+};
+}  // namespace
+
+DT relu_shares(Session& s, const DT& x, const std::string& tag) {
+  const size_t n = x.numel();
+  const int ch = chunks_for(s, n);
+  DT bits = s.alloc(x.shape, 0);
+  a2b_op(s, n, adder_for(s, n), tag + ".msb", SrcMem{cptrs(x)}, MsbSink{ptrs(bits)});
+  DT c = b2a_bit(s, bits, tag + ".b2a", ch);
+  Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Arith, x.shape), tag + ".gate");
+  t.mark_consumed();
+  DT out = s.alloc(x.shape, x.scale);
+  mul_op(s, t.ew, n, ch, tag + ".gate", SrcMem{cptrs(x)}, SrcMem{cptrs(c)}, SinkXMinus{cptrs(x), ptrs(out)});
+  return out;
+}
+
+namespace {
+// cur [outer, len] -> a = cur[:, :h], b = cur[:, h:2h]  (H/nonlinear/activations.hpp:20-33,62-63)
+void take_halves(Session& s, const DT& cur, size_t outer, size_t len, size_t h, DT& a, DT& b) {
+  a = s.alloc(Shape{outer, h}, cur.scale);
+  b = s.alloc(Shape{outer, h}, cur.scale);
+  const CPtr2 cp = cptrs(cur);
+  const Ptr2 ap = ptrs(a), bp = ptrs(b);
+  const u32 H = u32(h), LEN = u32(len);
+  launch_ew(s.stream, s.n_local, outer * h, [=] __device__(int slot, u64 i) {
+    const u32 o = u32(i) / H, j = u32(i) - o * H;
+    const u64 src = u64(o) * LEN + j;
+    ap.p[slot][i] = cp.p[slot][src];
+    bp.p[slot][i] = cp.p[slot][src + H];
+  });
+}
+struct SinkPick {  // m = a + step, written into the next [outer, h(+1)] row layout
+  CPtr2 a;
+  Ptr2 next;
+  u32 h, nw;
+  __device__ void operator()(int slot, int, u64 g, u64 z) const {
+    const u32 o = u32(g) / h, j = u32(g) - o * h;
+    next.p[slot][u64(o) * nw + j] = a.p[slot][g] + z;
+  }
+};
+}  // namespace
+
+DT max_last_dim(Session& s, const DT& x, size_t L, const std::string& tag) {
+  if (L == 0 || x.numel() % L != 0) throw Error(kShapeError, "max_last_dim: bad row length");
+  const size_t outer = x.numel() / L;
+  DT cur = reshape(x, Shape{outer, L});
+  size_t len = L;
+  int round = 0;
+  while (len > 1) {
+    const size_t h = len / 2;
+    const bool odd = len & 1;
+    DT a, b;
+    take_halves(s, cur, outer, len, h, a, b);
+    const std::string rt = tag + ".r" + std::to_string(round++);
+    const size_t n = outer * h;
+    AdderOptions opt = adder_for(s, n);
+    DT gate = less_than(s, a, b, opt, rt);
+    const size_t nw = odd ? h + 1 : h;
+    DT next = s.alloc(Shape{outer, nw}, cur.scale);
+    if (odd) {  // carry the odd tail (H/nonlinear/activations.hpp:71-82)
+      const CPtr2 cp = cptrs(cur);
+      const Ptr2 np = ptrs(next);
+      const u32 LEN = u32(len), NW = u32(nw), HH = u32(h);
+      launch_ew(s.stream, s.n_local, outer, [=] __device__(int slot, u64 o) {
+        np.p[slot][o * NW + HH] = cp.p[slot][o * LEN + LEN - 1];
+      });
+    }
+    Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Arith, Shape{outer, h}), rt + ".pick");
+    t.mark_consumed();
+    mul_op(s, t.ew, n, chunks_for(s, n), rt + ".pick", SrcSub{cptrs(b), cptrs(a)}, SrcMem{cptrs(gate)},
+           SinkPick{cptrs(a), ptrs(next), u32(h), u32(nw)});
+    cur = next;
+    len = nw;
+  }
+  return reshape(cur, Shape{outer, 1});
+}
+
+namespace {
+struct SinkExpInit {  // y = w + trunc(w^2, f+1) + [p0] 2^f   (H/nonlinear/approx.hpp:27-31)
+  CPtr2 x;
+  Ptr2 y;
+  int f, it;
+  __device__ void operator()(int slot, int party, u64 g, u64 z) const {
+    y.p[slot][g] = sar64(x.p[slot][g], it) + sar64(z, f + 1) + (party == 0 ? (u64(1) << f) : 0);
+  }
+};
+}  // namespace
+
+DT exp_shares(Session& s, const DT& x, const std::string& tag, int square_iters) {
+  const int f = s.cfg.frac_bits;
+  const size_t n = x.numel();
+  const int ch = chunks_for(s, n);
+  DT y = s.alloc(x.shape, x.scale);
+  {
+    Triple t = s.fetch(TripleSpec::square_of(x.shape), tag + ".w2");
+    t.mark_consumed();
+    square_op(s, t.ew, n, ch, tag + ".w2", SrcSar{cptrs(x), square_iters},
+              SinkExpInit{cptrs(x), ptrs(y), f, square_iters});
+  }
+  for (int i = 0; i < square_iters; ++i) {
+    Triple t = s.fetch(TripleSpec::square_of(x.shape), tag + ".sq" + std::to_string(i));
+    t.mark_consumed();
+    square_op(s, t.ew, n, ch, tag + ".sq" + std::to_string(i), SrcMem{cptrs(y)}, SinkTrunc{ptrs(y), f});
+  }
+  return y;
+}
+
+namespace {
+struct SinkNewtonU {  // u = [p0] 2^(f+1) - trunc(x*y, f)
+  Ptr2 u;
+  int f;
+  __device__ void operator()(int slot, int party, u64 g, u64 z) const {
+    u.p[slot][g] = (party == 0 ? (u64(2) << f) : 0) - sar64(z, f);
+  }
+};
+}  // namespace
+
+DT reciprocal_shares(Session& s, const DT& x, const std::string& tag, int newton_iters) {
+  const int f = s.cfg.frac_bits;
+  const size_t n = x.numel();
+  const int ch = chunks_for(s, n);
+  // t = 0.5 - x ; y0 = 3 exp(t) + 0.003  (H/nonlinear/approx.hpp:49-51)
+  const u64 half = encode_fixed(0.5, f);
+  const u64 c003 = encode_fixed(0.003, f);
+  DT t0 = s.alloc(x.shape, x.scale);
+  {
+    const Pid2 pid = pids(s);
+    const CPtr2 xp = cptrs(x);
+    const Ptr2 tp = ptrs(t0);
+    launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) {
+      tp.p[slot][i] = (pid.v[slot] == 0 ? half : 0) - xp.p[slot][i];
+    });
+  }
+  DT e = exp_shares(s, t0, tag + ".seed");
+  DT y = s.alloc(x.shape, x.scale);
+  {
+    const Pid2 pid = pids(s);
+    const CPtr2 ep = cptrs(e);
+    const Ptr2 yp = ptrs(y);
+    launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) {
+      yp.p[slot][i] = ep.p[slot][i] * 3 + (pid.v[slot] == 0 ? c003 : 0);
+    });
+  }
+  DT u = s.alloc(x.shape, x.scale);
+  for (int i = 0; i < newton_iters; ++i) {
+    Triple t1 = s.fetch(TripleSpec::elementwise(TripleKind::Arith, x.shape), tag + ".xy" + std::to_string(i));
+    t1.mark_consumed();
+    mul_op(s, t1.ew, n, ch, tag + ".xy" + std::to_string(i), SrcMem{cptrs(x)}, SrcMem{cptrs(y)},
+           SinkNewtonU{ptrs(u), f});
+    Triple t2 = s.fetch(TripleSpec::elementwise(TripleKind::Arith, x.shape), tag + ".yu" + std::to_string(i));
+    t2.mark_consumed();
+    mul_op(s, t2.ew, n, ch, tag + ".yu" + std::to_string(i), SrcMem{cptrs(y)}, SrcMem{cptrs(u)},
+           SinkTrunc{ptrs(y), f});
+  }
+  return y;
+}
+
+namespace {
+struct SrcBcast {  // r[g / L]
+  CPtr2 r;
+  u32 L;
+  __device__ u64 operator()(int slot, u64 g) const { return r.p[slot][u32(g) / L]; }
+};
+}  // namespace
+
+DT softmax_shares(Session& s, const DT& x, size_t L, const std::string& tag) {
+  const size_t outer = x.numel() / L;
+  const size_t n = x.numel();
+  const int ch = chunks_for(s, n);
+  DT mx = max_last_dim(s, x, L, tag + ".max");
+  DT centered = s.alloc(Shape{outer, L}, x.scale);
+  {
+    const CPtr2 xp = cptrs(x), mp = cptrs(mx);
+    const Ptr2 cp = ptrs(centered);
+    const u32 LL = u32(L);
+    launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) {
+      cp.p[slot][i] = xp.p[slot][i] - mp.p[slot][u32(i) / LL];
+    });
+  }
+  DT e = exp_shares(s, centered, tag + ".exp");
+  DT rowsum = s.alloc(Shape{outer, 1}, x.scale);
+  {
+    const CPtr2 ep = cptrs(e);
+    const Ptr2 rp = ptrs(rowsum);
+    const u64 LL = L;
+    launch_ew(s.stream, s.n_local, outer, [=] __device__(int slot, u64 o) {
+      u64 acc = 0;
+      const u64* row = ep.p[slot] + o * LL;
+      for (u64 j = 0; j < LL; ++j) acc += row[j];
+      rp.p[slot][o] = acc;
+    });
+  }
+  DT r = reciprocal_shares(s, rowsum, tag + ".recip");
+  Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Arith, Shape{outer, L}), tag + ".scale");
+  t.mark_consumed();
+  DT out = s.alloc(x.shape, x.scale);
+  mul_op(s, t.ew, n, ch, tag + ".scale", SrcMem{cptrs(e)}, SrcBcast{cptrs(r), u32(L)},
+         SinkTrunc{ptrs(out), s.cfg.frac_bits});
+  return out;
+}
+
+DT maxpool2d_shares(Session& s, const DT& x, size_t N, size_t C, size_t H, size_t W, size_t k,
+                    size_t stride, const std::string& tag) {
+  if (H < k || W < k) throw Error(kShapeError, "maxpool2d: window larger than input");
+  const size_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
+  const size_t rows = N * C * OH * OW;
+  DT win = s.alloc(Shape{rows, k * k}, x.scale);
+  {
+    const CPtr2 xp = cptrs(x);
+    const Ptr2 wp = ptrs(win);
+    const u32 KK = u32(k * k), K = u32(k), S = u32(stride), OWw = u32(OW), OHh = u32(OH), HH = u32(H),
+              WW = u32(W);
+    launch_ew(s.stream, s.n_local, rows * k * k, [=] __device__(int slot, u64 i) {
+      const u32 r = u32(i) / KK, t = u32(i) - r * KK;
+      const u32 ki = t / K, kj = t - ki * K;
+      const u32 ow = r % OWw, oh = (r / OWw) % OHh, nc = r / (OWw * OHh);
+      const u64 src = (u64(nc) * HH + oh * S + ki) * WW + ow * S + kj;
+      wp.p[slot][i] = xp.p[slot][src];
+    });
+  }
+  DT mx = max_last_dim(s, win, k * k, tag);
+  return reshape(mx, Shape{N, C, OH, OW});
+}
+
+}  // namespace mpcg

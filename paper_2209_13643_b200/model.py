@@ -1,0 +1,143 @@
+"""Model configs and deterministic synthetic data (H/engine/model.hpp).
+
+Setup-time host code: JSON model graphs (H/engine/model.hpp:124-191), deterministic
+weight init (H/engine/model.hpp:257-275) and demo input (H/engine/model.hpp:417-424),
+all drawn from the reference's counter-mode splitmix64 so a model run here sees the
+exact weights and inputs the reference sees for the same seed.
+"""
+from __future__ import annotations
+
+import json
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+PHI = 0x9E3779B97F4A7C15
+M64 = (1 << 64) - 1
+CONFIG_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "configs")
+
+LAYER_KINDS = {"dense": 0, "conv2d": 1, "relu": 2, "maxpool2d": 3, "flatten": 4, "attention": 5,
+               "softmax": 6, "mean_pool": 7}
+
+
+def _mix(z: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        z = z.copy()
+        z ^= z >> np.uint64(30)
+        z *= np.uint64(0xBF58476D1CE4E5B9)
+        z ^= z >> np.uint64(27)
+        z *= np.uint64(0x94D049BB133111EB)
+        z ^= z >> np.uint64(31)
+    return z
+
+
+def counter_draws(key: int, stream: int, n: int, first: int = 1) -> np.ndarray:
+    """Draws first..first+n-1 of CounterRng(key, stream) (H/sharing/rng.hpp:10-32)."""
+    k = np.uint64((key ^ ((stream * PHI) & M64)) & M64)
+    with np.errstate(over="ignore"):
+        c = np.arange(first, first + n, dtype=np.uint64)
+        return _mix(k + c * np.uint64(PHI))
+
+
+@dataclass
+class LayerSpec:
+    name: str
+    type: str
+    out: int = 0
+    kernel: int = 0
+    stride: int = 1
+    pad: int = 0
+    heads: int = 0
+    bias: bool = True
+
+
+@dataclass
+class ModelGraph:
+    name: str
+    frac_bits: int
+    input: tuple
+    layers: list = field(default_factory=list)
+
+    @staticmethod
+    def from_json(obj) -> "ModelGraph":
+        """H/engine/model.hpp:159-179 (same keys and defaults)."""
+        if isinstance(obj, str):
+            path = obj if os.path.exists(obj) else os.path.join(CONFIG_DIR, obj + ".json")
+            with open(path) as f:
+                obj = json.load(f)
+        fb = int(obj.get("frac_bits", 20))
+        layers = []
+        for lj in obj["layers"]:
+            t = lj["type"]
+            if t not in LAYER_KINDS:
+                raise ValueError("unknown layer type: " + t)
+            layers.append(LayerSpec(lj.get("name", t), t, int(lj.get("out", 0)), int(lj.get("kernel", 0)),
+                                    int(lj.get("stride", 1)), int(lj.get("pad", 0)), int(lj.get("heads", 0)),
+                                    bool(lj.get("bias", True))))
+        return ModelGraph(obj.get("name", "model"), fb, tuple(int(d) for d in obj["input"]), layers)
+
+    def with_batch(self, batch: int) -> "ModelGraph":
+        return ModelGraph(self.name, self.frac_bits, (batch,) + tuple(self.input[1:]), list(self.layers))
+
+    def shapes(self):
+        """infer_shapes (H/engine/model.hpp:69-122)."""
+        out, cur = [], list(self.input)
+        for l in self.layers:
+            if l.type == "dense":
+                cur[-1] = l.out
+            elif l.type == "conv2d":
+                cur = [cur[0], l.out, (cur[2] + 2 * l.pad - l.kernel) // l.stride + 1,
+                       (cur[3] + 2 * l.pad - l.kernel) // l.stride + 1]
+            elif l.type == "maxpool2d":
+                cur = [cur[0], cur[1], (cur[2] - l.kernel) // l.stride + 1, (cur[3] - l.kernel) // l.stride + 1]
+            elif l.type == "flatten":
+                cur = [cur[0], int(np.prod(cur[1:]))]
+            elif l.type == "mean_pool":
+                cur = [cur[0], cur[2]]
+            out.append(tuple(cur))
+        return out
+
+    def weight_shapes(self):
+        """model_weight_shapes (H/engine/model.hpp:213-252), in layer order."""
+        out, cur = [], self.input
+        for l, nxt in zip(self.layers, self.shapes()):
+            if l.type == "dense":
+                out.append((l.name + ".W", (cur[-1], l.out)))
+                if l.bias:
+                    out.append((l.name + ".b", (l.out,)))
+            elif l.type == "conv2d":
+                out.append((l.name + ".W", (cur[1] * l.kernel * l.kernel, l.out)))
+                if l.bias:
+                    out.append((l.name + ".b", (l.out,)))
+            elif l.type == "attention":
+                d = cur[2]
+                out.append((l.name + ".Wqkv", (d, 3 * d)))
+                if l.bias:
+                    out.append((l.name + ".bqkv", (3 * d,)))
+                out.append((l.name + ".Wo", (d, d)))
+                if l.bias:
+                    out.append((l.name + ".bo", (d,)))
+            cur = nxt
+        return out
+
+
+def _unit(draws: np.ndarray) -> np.ndarray:
+    return (draws >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+
+
+def init_weights(g: ModelGraph, seed: int) -> dict:
+    """H/engine/model.hpp:257-275: one CounterRng(seed, 0x77e1 + idx) per tensor."""
+    w = {}
+    for idx, (key, shape) in enumerate(g.weight_shapes()):
+        span = 1.0 / math.sqrt(float(shape[0])) if len(shape) >= 2 else 0.1
+        u = _unit(counter_draws(seed, 0x77E1 + idx, int(np.prod(shape))))
+        w[key] = ((2.0 * u - 1.0) * span).reshape(shape)
+    return w
+
+
+def demo_input(g: ModelGraph, seed: int) -> np.ndarray:
+    """H/engine/model.hpp:417-424."""
+    u = _unit(counter_draws(seed, 0x1D07, int(np.prod(g.input))))
+    return (2.0 * u - 1.0).reshape(g.input)
