@@ -142,6 +142,23 @@ int mpcg_executor_time_layers(mpcg_executor* e, int enable);
 int mpcg_executor_layer_times(mpcg_executor* e, int max, float* ms, int* count);
 int mpcg_executor_destroy(mpcg_executor* e);
 
+/* ---- measurement hooks (bench.py) ---- */
+/* Kernels launched by this library since load. */
+uint64_t mpcg_launch_count(void);
+/* Time every launch of one kernel class with CUDA events (1 = SPK adder level rounds,
+ * 2 = ring GEMM); stop returns total device ms, launches and algorithmic units
+ * (bytes for elementwise classes, ring MACs for GEMM). */
+int mpcg_probe_start(int kernel_class);
+int mpcg_probe_stop(double* total_ms, uint64_t* launches, double* units);
+/* Page-locked host buffers and async H2D copies into an existing tensor (e2e path). */
+int mpcg_pinned_alloc(uint64_t bytes, void** out);
+int mpcg_pinned_free(void* p);
+int mpcg_tensor_copy_from_host(mpcg_tensor* t, const uint64_t* host /* n_local*numel words */);
+/* Evict L2 between timed steps: memset of a 256 MiB scratch buffer on the session stream. */
+int mpcg_session_flush_l2(mpcg_session* s);
+/* Device timer on the session stream: start/stop pairs accumulate; ms returns the sum. */
+int mpcg_session_timer(mpcg_session* s, int op /* 0 start, 1 stop, 2 reset, 3 read */, double* total_ms);
+
 /* FNV-1a over little-endian words (engine/report.hpp:18-23). */
 uint64_t mpcg_fnv1a_words(const uint64_t* words, uint64_t n);
 

@@ -86,9 +86,17 @@ SIGNATURES = {
     "mpcg_executor_time_layers": [P, I32],
     "mpcg_executor_layer_times": [P, I32, C.POINTER(C.c_float), C.POINTER(I32)],
     "mpcg_executor_destroy": [P],
+    "mpcg_launch_count": [],
+    "mpcg_probe_start": [I32],
+    "mpcg_probe_stop": [C.POINTER(DBL), U64P, C.POINTER(DBL)],
+    "mpcg_pinned_alloc": [U64, PP],
+    "mpcg_pinned_free": [P],
+    "mpcg_tensor_copy_from_host": [P, U64P],
+    "mpcg_session_flush_l2": [P],
+    "mpcg_session_timer": [P, I32, C.POINTER(DBL)],
     "mpcg_fnv1a_words": [U64P, U64],
 }
-_RET = {"mpcg_last_error": C.c_char_p, "mpcg_fnv1a_words": U64}
+_RET = {"mpcg_last_error": C.c_char_p, "mpcg_fnv1a_words": U64, "mpcg_launch_count": U64}
 
 _lib = None
 

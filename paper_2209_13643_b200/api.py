@@ -221,6 +221,61 @@ def maxpool2d_shares(s, x, N_, C_, H, W, k, stride, tag="maxpool"):
     return _op("mpcg_maxpool2d", s, x.handle, N_, C_, H, W, k, stride, _tag(tag))
 
 
+def launch_count() -> int:
+    """Kernels launched by libmpcg.so since load."""
+    return int(N.lib().mpcg_launch_count())
+
+
+KERNEL_CLASS = {"adder_round": 1, "gemm": 2}
+
+
+def probe_start(kernel_class="adder_round"):
+    N.call("mpcg_probe_start", KERNEL_CLASS[kernel_class])
+
+
+def probe_stop():
+    """-> (total device ms, launches, algorithmic units) of the probed kernel class."""
+    ms, n, u = C.c_double(), C.c_uint64(), C.c_double()
+    N.call("mpcg_probe_stop", C.byref(ms), C.byref(n), C.byref(u))
+    return ms.value, n.value, u.value
+
+
+class PinnedBuffer:
+    """Page-locked host buffer of uint64 words (e2e host<->device copies)."""
+
+    def __init__(self, nwords):
+        p = C.c_void_p()
+        N.call("mpcg_pinned_alloc", nwords * 8, C.byref(p))
+        self._p = p
+        self.array = np.ctypeslib.as_array(C.cast(p, N.U64P), shape=(max(nwords, 1),))[:nwords]
+
+    def __del__(self):
+        try:
+            N.lib().mpcg_pinned_free(self._p)
+        except Exception:
+            pass
+
+
+def copy_from_host(t: "Tensor", buf: PinnedBuffer):
+    N.call("mpcg_tensor_copy_from_host", t.handle, buf.array.ctypes.data_as(N.U64P))
+
+
+def download_into(t: "Tensor", buf: PinnedBuffer):
+    N.call("mpcg_tensor_download", t.handle, buf.array.ctypes.data_as(N.U64P))
+
+
+def flush_l2(s: Session):
+    N.call("mpcg_session_flush_l2", s.handle)
+
+
+def timer(s: Session, op: str) -> float:
+    """op in start|stop|reset|read; returns accumulated device ms of completed pairs."""
+    ms = C.c_double()
+    code = {"start": 0, "stop": 1, "reset": 2, "read": 3}[op]
+    N.call("mpcg_session_timer", s.handle, code, C.byref(ms) if op == "read" else None)
+    return ms.value
+
+
 def fnv1a_words(words: np.ndarray) -> int:
     a = np.ascontiguousarray(words, dtype=np.uint64).reshape(-1)
     return int(N.lib().mpcg_fnv1a_words(_u64p(a), a.size))

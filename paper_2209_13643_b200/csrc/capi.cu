@@ -13,19 +13,21 @@ void nccl_unique_id(void* out128);
 void nccl_connect(Session& s, const void* id128, int rank);
 }  // namespace mpcg
 
+// Handles share ownership of the session so device memory is always released on a
+// live stream, whatever order the host language destroys handles in.
 struct mpcg_session {
-  std::unique_ptr<Session> s;
+  std::shared_ptr<Session> s;
 };
 struct mpcg_tensor {
+  std::shared_ptr<Session> s;
   DT t;
-  Session* s;
 };
 struct mpcg_model {
   ModelGraph g;
 };
 struct mpcg_executor {
+  std::shared_ptr<Session> s;
   std::unique_ptr<SecureExecutor> e;
-  Session* s;
 };
 
 namespace {
@@ -52,7 +54,7 @@ void need(const void* p, const char* what) {
   if (!p) throw Error(kUsageError, std::string("null ") + what);
 }
 
-mpcg_tensor* wrap(Session& s, DT t) { return new mpcg_tensor{std::move(t), &s}; }
+mpcg_tensor* wrap(const std::shared_ptr<Session>& s, DT t) { return new mpcg_tensor{s, std::move(t)}; }
 const DT& T(const mpcg_tensor* t) {
   need(t, "tensor");
   return t->t;
@@ -60,6 +62,10 @@ const DT& T(const mpcg_tensor* t) {
 Session& S(mpcg_session* s) {
   need(s, "session");
   return *s->s;
+}
+const std::shared_ptr<Session>& SP(mpcg_session* s) {
+  need(s, "session");
+  return s->s;
 }
 std::string tagstr(const char* t) { return t ? std::string(t) : std::string(); }
 }  // namespace
@@ -86,7 +92,7 @@ int mpcg_session_create(int device, int n_local, int party, uint64_t seed, uint6
     need(out, "out");
     auto* h = new mpcg_session;
     try {
-      h->s = std::make_unique<Session>(device, n_local, party, seed, mask_seed, frac_bits);
+      h->s = std::make_shared<Session>(device, n_local, party, seed, mask_seed, frac_bits);
     } catch (...) {
       delete h;
       throw;
@@ -169,7 +175,7 @@ int mpcg_tensor_create(mpcg_session* s, int ndim, const uint64_t* dims, int scal
     DT t = host ? ss.upload(sh, scale, host) : ss.alloc(sh, scale);
     if (!host && t.numel())
       MPCG_CUDA(cudaMemsetAsync(t.mem->ptr, 0, t.numel() * ss.n_local * 8, ss.stream));
-    *out = wrap(ss, std::move(t));
+    *out = wrap(SP(s), std::move(t));
   });
 }
 
@@ -213,7 +219,7 @@ int mpcg_deal_input(mpcg_session* s, const double* x, int ndim, const uint64_t* 
     }
     Shape ls = g;
     ls[0] = local;
-    *out = wrap(ss, ss.upload(ls, f, host.data()));
+    *out = wrap(SP(s), ss.upload(ls, f, host.data()));
   });
 }
 
@@ -221,7 +227,7 @@ int mpcg_deal_input(mpcg_session* s, const double* x, int ndim, const uint64_t* 
   return guard([&] {                        \
     Session& ss = S(s);                     \
     need(out, "out");                       \
-    *out = wrap(ss, (expr));                \
+    *out = wrap(SP(s), (expr));                \
   })
 
 int mpcg_open(mpcg_session* s, const mpcg_tensor* x, int reduce, const char* tag, mpcg_tensor** out) {
@@ -339,7 +345,7 @@ int mpcg_executor_create(mpcg_session* s, const mpcg_model* m, int pub, int pipe
     o.chunk_threshold = thr;
     o.merged_adder = merged != 0;
     auto* e = new mpcg_executor;
-    e->s = &ss;
+    e->s = SP(s);
     try {
       e->e = std::make_unique<SecureExecutor>(ss, m->g, pub != 0, o);
     } catch (...) {
@@ -368,7 +374,7 @@ int mpcg_executor_run(mpcg_executor* e, const mpcg_tensor* input, mpcg_tensor** 
   return guard([&] {
     need(e, "executor");
     need(out, "out");
-    *out = wrap(*e->s, e->e->run(T(input)));
+    *out = wrap(e->s, e->e->run(T(input)));
   });
 }
 
@@ -391,6 +397,96 @@ int mpcg_executor_layer_times(mpcg_executor* e, int max, float* ms, int* count) 
 
 int mpcg_executor_destroy(mpcg_executor* e) {
   return guard([&] { delete e; });
+}
+
+uint64_t mpcg_launch_count(void) { return g_launches.load(); }
+
+int mpcg_probe_start(int cls) {
+  return guard([&] {
+    for (auto& [a, b] : g_probe.ev) {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+    g_probe = Probe{};
+    g_probe.cls = cls;
+  });
+}
+
+int mpcg_probe_stop(double* total_ms, uint64_t* launches, double* units) {
+  return guard([&] {
+    double ms = 0;
+    for (auto& [a, b] : g_probe.ev) {
+      MPCG_CUDA(cudaEventSynchronize(b));
+      float t = 0;
+      MPCG_CUDA(cudaEventElapsedTime(&t, a, b));
+      ms += t;
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+    *total_ms = ms;
+    *launches = g_probe.launches;
+    *units = g_probe.bytes;
+    g_probe = Probe{};
+  });
+}
+
+int mpcg_pinned_alloc(uint64_t bytes, void** out) {
+  return guard([&] { MPCG_CUDA(cudaHostAlloc(out, bytes ? bytes : 8, cudaHostAllocDefault)); });
+}
+
+int mpcg_pinned_free(void* p) {
+  return guard([&] { MPCG_CUDA(cudaFreeHost(p)); });
+}
+
+int mpcg_tensor_copy_from_host(mpcg_tensor* t, const uint64_t* host) {
+  return guard([&] {
+    need(t, "tensor");
+    const size_t n = t->t.numel() * t->s->n_local;
+    if (n) MPCG_CUDA(cudaMemcpyAsync(t->t.mem->ptr, host, n * 8, cudaMemcpyHostToDevice, t->s->stream));
+  });
+}
+
+int mpcg_session_flush_l2(mpcg_session* s) {
+  return guard([&] {
+    Session& ss = S(s);
+    if (!ss.flush_buf) MPCG_CUDA(cudaMalloc(&ss.flush_buf, kFlushBytes));
+    MPCG_CUDA(cudaMemsetAsync(ss.flush_buf, ss.flush_val++ & 0xff, kFlushBytes, ss.stream));
+  });
+}
+
+int mpcg_session_timer(mpcg_session* s, int op, double* total_ms) {
+  return guard([&] {
+    Session& ss = S(s);
+    if (op == 2) {
+      for (auto& [a, b] : ss.timer_ev) {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+      }
+      ss.timer_ev.clear();
+    } else if (op == 0) {
+      cudaEvent_t a;
+      MPCG_CUDA(cudaEventCreate(&a));
+      MPCG_CUDA(cudaEventRecord(a, ss.stream));
+      ss.timer_ev.push_back({a, nullptr});
+    } else if (op == 1) {
+      if (ss.timer_ev.empty() || ss.timer_ev.back().second) throw Error(kUsageError, "timer stop without start");
+      cudaEvent_t b;
+      MPCG_CUDA(cudaEventCreate(&b));
+      MPCG_CUDA(cudaEventRecord(b, ss.stream));
+      ss.timer_ev.back().second = b;
+    }
+    if (total_ms) {
+      double ms = 0;
+      for (auto& [a, b] : ss.timer_ev) {
+        if (!b) continue;
+        MPCG_CUDA(cudaEventSynchronize(b));
+        float t = 0;
+        MPCG_CUDA(cudaEventElapsedTime(&t, a, b));
+        ms += t;
+      }
+      *total_ms = ms;
+    }
+  });
 }
 
 uint64_t mpcg_fnv1a_words(const uint64_t* w, uint64_t n) {

@@ -8,9 +8,12 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
+#include <vector>
 
 namespace mpcg {
 
@@ -169,6 +172,49 @@ __device__ __forceinline__ u64 mm_rC(const MmTriple& t, u64 k) {
 // ------------------------------------------------------------------ launch helpers
 constexpr int kSms = 148;
 
+// Instrumentation: count of kernels this library launched, and an optional probe that
+// brackets every launch of one kernel class with CUDA events (bench.py's live roofline).
+enum KernelClass : int { kClsOther = 0, kClsAdderRound = 1, kClsGemm = 2, kClsBeaver = 3 };
+struct Probe {
+  int cls = -1;             // class being timed, -1 = off
+  double bytes = 0;         // algorithmic bytes of the probed launches
+  u64 launches = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+};
+inline std::atomic<u64> g_launches{0};
+inline Probe g_probe;
+inline thread_local int t_cls = kClsOther;
+inline thread_local double t_bytes = 0;
+struct ClassScope {  // tags launches issued in this scope: ClassScope cs(kClsAdderRound, bytes)
+  int prev;
+  double pb;
+  ClassScope(int c, double bytes) : prev(t_cls), pb(t_bytes) {
+    t_cls = c;
+    t_bytes = bytes;
+  }
+  ~ClassScope() {
+    t_cls = prev;
+    t_bytes = pb;
+  }
+};
+inline void probe_begin(cudaStream_t st, cudaEvent_t* a) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  *a = nullptr;
+  if (g_probe.cls >= 0 && g_probe.cls == t_cls) {
+    cudaEventCreate(a);
+    cudaEventRecord(*a, st);
+  }
+}
+inline void probe_end(cudaStream_t st, cudaEvent_t a) {
+  if (!a) return;
+  cudaEvent_t b;
+  cudaEventCreate(&b);
+  cudaEventRecord(b, st);
+  g_probe.ev.push_back({a, b});
+  g_probe.bytes += t_bytes;
+  g_probe.launches++;
+}
+
 template <class F>
 __global__ void __launch_bounds__(256) ew_kernel(u64 n, F f) {
   const int slot = blockIdx.y;
@@ -187,8 +233,11 @@ template <class F>
 void launch_ew(cudaStream_t stream, int nslots, u64 n, F f) {
   if (n == 0) return;
   dim3 grid(ew_blocks(n), nslots);
+  cudaEvent_t pe;
+  probe_begin(stream, &pe);
   ew_kernel<<<grid, 256, 0, stream>>>(n, f);
   MPCG_CUDA(cudaGetLastError());
+  probe_end(stream, pe);
 }
 
 }  // namespace mpcg

@@ -147,6 +147,11 @@ Session::~Session() {
   cudaStreamSynchronize(stream);
   cudaStreamSynchronize(comm_stream);
   for (auto e : events_) cudaEventDestroy(e);
+  for (auto& [a, b] : timer_ev) {
+    cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  if (flush_buf) cudaFree(flush_buf);
   if (nccl) nccl_api().CommDestroy(nccl);
   cudaFree(link_state_);
   cudaStreamDestroy(comm_stream);

@@ -129,6 +129,8 @@ struct SessionConfig {
   double sec_per_message = 0;
 };
 
+constexpr size_t kFlushBytes = size_t(256) << 20;  // > 126 MB L2
+
 class Session {
  public:
   Session(int device, int n_local, int party, u64 seed, u64 mask_seed, int frac_bits);
@@ -177,6 +179,11 @@ class Session {
   void sync();
   void check();  // debug: sync + error check when MPCG_DEBUG_SYNC=1
   bool debug_sync = false;
+
+  // measurement helpers (bench.py)
+  void* flush_buf = nullptr;
+  int flush_val = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timer_ev;
 
  private:
   void throttle(Open& o);

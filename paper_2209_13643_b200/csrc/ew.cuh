@@ -313,6 +313,10 @@ void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& 
     k.xf = xf;
     k.yf = yf;
     k.ff = ff;
+    // per element per party: round 0 issue = 2x16 wire + 8x(2 in + 1 out); level = 2x32 wire
+    // + 8x(2 in + 2 out); final = 2x32 wire + 8x(3 in + 1 out)
+    const double per = rn == 0 ? 56.0 : (rn <= c.levels ? 96.0 : 96.0);
+    ClassScope cs(rn >= 1 && rn <= c.levels ? kClsAdderRound : kClsOther, per * double(hi - lo) * s.n_local);
     launch_ew(s.stream, s.n_local, hi - lo, k);
   };
   fetch_round(0);

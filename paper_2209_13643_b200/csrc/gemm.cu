@@ -88,8 +88,11 @@ __global__ void __launch_bounds__(256) ring_gemm_simt(GemmArgs a) {
 template <int BM, int BN, int TM, int TN>
 void launch_simt(const GemmArgs& a, cudaStream_t st) {
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, a.nslots * a.nbatch);
+  cudaEvent_t pe;
+  probe_begin(st, &pe);
   ring_gemm_simt<BM, BN, TM, TN><<<grid, 256, 0, st>>>(a);
   MPCG_CUDA(cudaGetLastError());
+  probe_end(st, pe);
 }
 
 }  // namespace
@@ -97,6 +100,10 @@ void launch_simt(const GemmArgs& a, cudaStream_t st) {
 void ring_gemm_launch(Session& s, const GemmArgs& a) {
   if (a.M == 0 || a.N == 0 || a.nbatch == 0) return;
   if (a.M > 65535u * 64u) throw Error(kShapeError, "ring_gemm: M too large");
+  // algorithmic work: ring MACs of every segment of every slot (8 bytes/MAC-equivalent unused)
+  double macs = 0;
+  for (int i = 0; i < a.nslots; ++i) macs += double(a.sl[i].nseg) * a.M * a.N * a.K * a.nbatch;
+  ClassScope cs(kClsGemm, macs);
   if (ring_gemm_tc_try(s, a)) return;  // tcgen05 int8-limb path when the shape qualifies
   if (a.N <= 8)
     launch_simt<128, 8, 4, 1>(a, s.stream);

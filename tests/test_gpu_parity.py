@@ -157,8 +157,8 @@ def test_shape_mismatch_and_errors(mp):
     b = s.tensor(np.zeros((2, 4, 3), dtype=np.uint64))
     with pytest.raises(mp.ShapeError):
         mp.beaver_mul(s, a, b)
-    with pytest.raises(mp.ShapeError):
-        mp.beaver_matmul(s, a, a)
+    with pytest.raises(mp.ConfigError):  # the dealer rejects first, as in the reference
+        mp.beaver_matmul(s, a, a)  # dealer rejects first, as the reference (triple.hpp:98-100)
     with pytest.raises(mp.ConfigError):
         mp.Session(device=0, n_local=3)
 
