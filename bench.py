@@ -189,9 +189,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    def timed(s, ex, x, steps, warmup):
+    def timed(s, ex, x, steps, warmup, graph):
+        """`graph`: one CUDA-graph replay per step (the production path); else eager run()."""
+        step = ex.replay if graph else (lambda: ex.run(x))
         for _ in range(warmup):
-            ex.run(x)
+            step()
         barrier(s)
         api.timer(s, "reset")
         l0 = api.launch_count()
@@ -199,7 +201,7 @@ def main():
             for _ in range(steps):
                 api.flush_l2(s)           # untimed: evict L2 between timed steps
                 api.timer(s, "start")
-                out = ex.run(x)
+                out = step()
                 api.timer(s, "stop")
             barrier(s)
         launches = api.launch_count() - l0
@@ -208,16 +210,15 @@ def main():
 
     # ---- main arm: the requested mode
     s, ex, x = setup(a.mode)
-    ms_step, launches, clocks, out = timed(s, ex, x, a.steps, a.warmup)
-    z = out.numpy()
-    # per-layer device time of one more step
+    # per-layer device time of one eager step (also the pipelined prologue before capture)
     ex.time_layers(True)
     ex.run(x)
     s.sync()
     layer_ms = ex.layer_times()
     ex.time_layers(False)
+    eager_ms, _, _, _ = timed(s, ex, x, max(3, a.steps // 4), 1, graph=False)
 
-    # ---- roofline probe: device time of every launch of the dominant kernel class (same steps)
+    # ---- roofline probe: device time of every launch of the dominant kernel class (eager steps)
     barrier(s)
     api.probe_start(a.probe)
     for _ in range(a.steps):
@@ -225,21 +226,24 @@ def main():
     s.sync()
     p_ms, p_launches, p_units = api.probe_stop()
 
+    ex.capture(x)
+    ms_step, launches, clocks, out = timed(s, ex, x, a.steps, a.warmup, graph=True)
+    z = out.numpy()
+
     # ---- e2e through the public API: pinned H2D of the input shares, run, D2H of the logits
     nloc = 2 if world == 1 else 1
     xin_host = x.numpy()
     pin_in = api.PinnedBuffer(xin_host.size)
     pin_in.array[:] = xin_host.reshape(-1)
     pin_out = api.PinnedBuffer(z.size)
-    xdev = s.tensor(xin_host, g.frac_bits)
     for _ in range(max(1, a.warmup)):
-        api.copy_from_host(xdev, pin_in)
-        api.download_into(ex.run(xdev), pin_out)
+        api.copy_from_host(x, pin_in)      # the captured graph reads x in place
+        api.download_into(ex.replay(), pin_out)
     barrier(s)
     t0 = time.perf_counter()
     for _ in range(a.steps):
-        api.copy_from_host(xdev, pin_in)
-        api.download_into(ex.run(xdev), pin_out)
+        api.copy_from_host(x, pin_in)
+        api.download_into(ex.replay(), pin_out)
     barrier(s)
     e2e_s = maxall(time.perf_counter() - t0) / a.steps
     h2d = xin_host.size * 8
@@ -249,12 +253,14 @@ def main():
     blocking = None
     if not a.no_blocking and a.mode == "pipelined":
         sb, exb, xb = setup("blocking")
-        b_ms, _, _, _ = timed(sb, exb, xb, a.steps, a.warmup)
         exb.time_layers(True)
         exb.run(xb)
         sb.sync()
         bl = exb.layer_times()
-        blocking = {"ms_per_step": b_ms,
+        exb.time_layers(False)
+        exb.capture(xb)
+        b_ms, _, _, _ = timed(sb, exb, xb, a.steps, a.warmup, graph=True)
+        blocking = {"ms_per_step": b_ms, "note": "same graph-replay timing; per_layer from one eager step",
                     "reduction_pct": (b_ms - ms_step) / b_ms * 100.0,
                     "per_layer": [{"layer": l.name, "blocking_ms": round(bb, 4), "pipelined_ms": round(pp, 4),
                                    "reduction_pct": round((bb - pp) / bb * 100.0, 2) if bb > 0 else 0.0}
@@ -321,6 +327,8 @@ def main():
                    "l2": "flushed between timed steps (256 MiB memset, untimed)",
                    "transport": "in-device zero-copy opens" if world == 1 else "NCCL send/recv over NVLink",
                    "kernels_per_step": launches / a.steps,
+                   "execution": "one CUDA-graph replay per step (whole 2PC inference, both parties)",
+                   "eager_ms_per_step": eager_ms,
                    "logits_hash_slot0": mp.fnv1a_words(dec) if world == 1 else None,
                    "blocking": blocking},
         "roofline": roof,

@@ -137,6 +137,12 @@ int mpcg_executor_create(mpcg_session* s, const mpcg_model* m, int public_weight
 int mpcg_executor_deal_weights(mpcg_executor* e, int count, const char* const* names,
                                const double* const* values, uint64_t seed);
 int mpcg_executor_run(mpcg_executor* e, const mpcg_tensor* input, mpcg_tensor** out); /* executor.hpp:193 */
+/* CUDA-graph form of run(): capture one steady-state inference that reads `input` in place
+ * (pipelined mode needs one mpcg_executor_run first), then each replay performs the next
+ * inference with fresh dealer triples (same values as successive run() calls). The
+ * replay output is valid until the next replay. */
+int mpcg_executor_capture(mpcg_executor* e, const mpcg_tensor* input);
+int mpcg_executor_replay(mpcg_executor* e, mpcg_tensor** out);
 /* Per-layer device times (ms) of the next runs: enable=1 turns timing on. */
 int mpcg_executor_time_layers(mpcg_executor* e, int enable);
 int mpcg_executor_layer_times(mpcg_executor* e, int max, float* ms, int* count);

@@ -83,6 +83,8 @@ SIGNATURES = {
     "mpcg_executor_create": [P, P, I32, I32, I32, U64, I32, PP],
     "mpcg_executor_deal_weights": [P, I32, C.POINTER(C.c_char_p), C.POINTER(C.POINTER(DBL)), U64],
     "mpcg_executor_run": [P, P, PP],
+    "mpcg_executor_capture": [P, P],
+    "mpcg_executor_replay": [P, PP],
     "mpcg_executor_time_layers": [P, I32],
     "mpcg_executor_layer_times": [P, I32, C.POINTER(C.c_float), C.POINTER(I32)],
     "mpcg_executor_destroy": [P],

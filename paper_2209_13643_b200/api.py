@@ -322,6 +322,16 @@ class SecureExecutor:
         N.call("mpcg_executor_run", self._h, x.handle, C.byref(h))
         return Tensor(self.sess, h)
 
+    def capture(self, x: Tensor):
+        """CUDA-graph capture of one inference reading `x` in place (run() once first)."""
+        N.call("mpcg_executor_capture", self._h, x.handle)
+
+    def replay(self) -> Tensor:
+        """Next inference as one graph launch; output valid until the next replay."""
+        h = C.c_void_p()
+        N.call("mpcg_executor_replay", self._h, C.byref(h))
+        return Tensor(self.sess, h)
+
     def time_layers(self, enable=True):
         N.call("mpcg_executor_time_layers", self._h, int(enable))
 

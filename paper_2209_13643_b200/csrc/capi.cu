@@ -378,6 +378,21 @@ int mpcg_executor_run(mpcg_executor* e, const mpcg_tensor* input, mpcg_tensor** 
   });
 }
 
+int mpcg_executor_capture(mpcg_executor* e, const mpcg_tensor* input) {
+  return guard([&] {
+    need(e, "executor");
+    e->e->capture(T(input));
+  });
+}
+
+int mpcg_executor_replay(mpcg_executor* e, mpcg_tensor** out) {
+  return guard([&] {
+    need(e, "executor");
+    DT r = e->e->replay();
+    if (out) *out = wrap(e->s, r);
+  });
+}
+
 int mpcg_executor_time_layers(mpcg_executor* e, int enable) {
   return guard([&] {
     need(e, "executor");

@@ -69,34 +69,41 @@ __host__ __device__ __forceinline__ u64 mix64(u64 z) {
 __host__ __device__ __forceinline__ u64 drw(u64 key, u64 c) { return mix64(key + c * kPhi); }
 
 // ------------------------------------------------------------------ dealer
+// Triple stream keys are either immediates (eager launches) or read from a device key
+// table that a rekey kernel refreshes at the head of every CUDA-graph replay, so a
+// replayed inference draws the next iteration's triples exactly as the reference's
+// per-tag fetch counter does (H/sharing/triple.hpp:146).
+//
 // One elementwise triple as seen by one party, with the local->global index map that
 // lets a data-parallel shard regenerate exactly its slice of the full-batch triple.
 // A tensor of `half` local elements per stacked half lives at global index
 // s*ghalf + off + i (s = stacked half, 0 for unstacked specs).
 struct EwTriple {
-  u64 key;     // seed ^ (stream * phi)
-  u64 mg;      // global numel of A (== of B, C)
-  u64 ghalf;   // global elements per stacked half (== mg when unstacked)
-  u64 off;     // global offset of this shard inside each half
-  int square;  // B == A as a secret; only A drawn
-  int bin;     // XOR sharing + AND product
+  u64 key;        // seed ^ (stream * phi)
+  const u64* kp;  // device key slot (graph replay), or null
+  u64 mg;         // global numel of A (== of B, C)
+  u64 ghalf;      // global elements per stacked half (== mg when unstacked)
+  u64 off;        // global offset of this shard inside each half
+  int square;     // B == A as a secret; only A drawn
+  int bin;        // XOR sharing + AND product
 };
 
-__device__ __forceinline__ u64 ew_gidx(const EwTriple& t, int s, u64 i) { return s * t.ghalf + t.off + i; }
+__device__ __forceinline__ u64 tkey(u64 key, const u64* kp) { return kp ? __ldg(kp) : key; }
 
 // a, b shares of element g (global index) for `party` (0 absorbs the secret).
 __device__ __forceinline__ void ew_ab(const EwTriple& t, int party, u64 g, u64& a, u64& b) {
+  const u64 key = tkey(t.key, t.kp);
   const u64 nbd = t.square ? 0 : t.mg;
   const u64 baseA = 1 + t.mg + nbd;
   const u64 baseB = baseA + t.mg;
-  const u64 ra = drw(t.key, baseA + g), rb = drw(t.key, baseB + g);
+  const u64 ra = drw(key, baseA + g), rb = drw(key, baseB + g);
   if (party != 0) {
     a = ra;
     b = rb;
     return;
   }
-  const u64 A = drw(t.key, 1 + g);
-  const u64 B = t.square ? A : drw(t.key, 1 + t.mg + g);
+  const u64 A = drw(key, 1 + g);
+  const u64 B = t.square ? A : drw(key, 1 + t.mg + g);
   if (t.bin) {
     a = A ^ ra;
     b = B ^ rb;
@@ -107,19 +114,20 @@ __device__ __forceinline__ void ew_ab(const EwTriple& t, int party, u64 g, u64& 
 }
 
 __device__ __forceinline__ void ew_abc(const EwTriple& t, int party, u64 g, u64& a, u64& b, u64& c) {
+  const u64 key = tkey(t.key, t.kp);
   const u64 nbd = t.square ? 0 : t.mg;
   const u64 baseA = 1 + t.mg + nbd;
   const u64 baseB = baseA + t.mg;
   const u64 baseC = baseB + t.mg;
-  const u64 ra = drw(t.key, baseA + g), rb = drw(t.key, baseB + g), rc = drw(t.key, baseC + g);
+  const u64 ra = drw(key, baseA + g), rb = drw(key, baseB + g), rc = drw(key, baseC + g);
   if (party != 0) {
     a = ra;
     b = rb;
     c = rc;
     return;
   }
-  const u64 A = drw(t.key, 1 + g);
-  const u64 B = t.square ? A : drw(t.key, 1 + t.mg + g);
+  const u64 A = drw(key, 1 + g);
+  const u64 B = t.square ? A : drw(key, 1 + t.mg + g);
   if (t.bin) {
     a = A ^ ra;
     b = B ^ rb;
@@ -133,40 +141,45 @@ __device__ __forceinline__ void ew_abc(const EwTriple& t, int party, u64 g, u64&
 
 // Square triples only need a and c (b is never used by the combine).
 __device__ __forceinline__ void sq_ac(const EwTriple& t, int party, u64 g, u64& a, u64& c) {
+  const u64 key = tkey(t.key, t.kp);
   const u64 baseA = 1 + t.mg;
   const u64 baseC = baseA + 2 * t.mg;
-  const u64 ra = drw(t.key, baseA + g), rc = drw(t.key, baseC + g);
+  const u64 ra = drw(key, baseA + g), rc = drw(key, baseC + g);
   if (party != 0) {
     a = ra;
     c = rc;
     return;
   }
-  const u64 A = drw(t.key, 1 + g);
+  const u64 A = drw(key, 1 + g);
   a = A - ra;
   c = A * A - rc;
 }
 
 __device__ __forceinline__ u64 sq_a(const EwTriple& t, int party, u64 g) {
-  const u64 ra = drw(t.key, 1 + t.mg + g);
-  return party != 0 ? ra : drw(t.key, 1 + g) - ra;
+  const u64 key = tkey(t.key, t.kp);
+  const u64 ra = drw(key, 1 + t.mg + g);
+  return party != 0 ? ra : drw(key, 1 + g) - ra;
 }
 
 // Matmul triple (H/sharing/triple.hpp:96-114): draws A (na), B (nb), then r_A, r_B, r_C.
 struct MmTriple {
   u64 key;
+  const u64* kp;
   u64 na, nb, nc;     // global numels
   u64 offA, offB, offC;
 };
-__device__ __forceinline__ u64 mm_A(const MmTriple& t, u64 i) { return drw(t.key, 1 + t.offA + i); }
-__device__ __forceinline__ u64 mm_B(const MmTriple& t, u64 j) { return drw(t.key, 1 + t.na + t.offB + j); }
+__device__ __forceinline__ u64 mm_A(const MmTriple& t, u64 i) { return drw(tkey(t.key, t.kp), 1 + t.offA + i); }
+__device__ __forceinline__ u64 mm_B(const MmTriple& t, u64 j) {
+  return drw(tkey(t.key, t.kp), 1 + t.na + t.offB + j);
+}
 __device__ __forceinline__ u64 mm_rA(const MmTriple& t, u64 i) {
-  return drw(t.key, 1 + t.na + t.nb + t.offA + i);
+  return drw(tkey(t.key, t.kp), 1 + t.na + t.nb + t.offA + i);
 }
 __device__ __forceinline__ u64 mm_rB(const MmTriple& t, u64 j) {
-  return drw(t.key, 1 + 2 * t.na + t.nb + t.offB + j);
+  return drw(tkey(t.key, t.kp), 1 + 2 * t.na + t.nb + t.offB + j);
 }
 __device__ __forceinline__ u64 mm_rC(const MmTriple& t, u64 k) {
-  return drw(t.key, 1 + 2 * t.na + 2 * t.nb + t.offC + k);
+  return drw(tkey(t.key, t.kp), 1 + 2 * t.na + 2 * t.nb + t.offC + k);
 }
 
 // ------------------------------------------------------------------ launch helpers

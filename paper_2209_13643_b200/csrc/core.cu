@@ -32,10 +32,48 @@ Block::Block(size_t w, cudaStream_t s) : words(w), stream(s) {
   if (w) MPCG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), w * sizeof(u64), s));
 }
 Block::~Block() {
-  if (ptr) cudaFreeAsync(ptr, stream);  // stream-ordered: safe after every queued reader
+  if (ptr && owned) {
+    if (sync_free)
+      cudaFree(ptr);
+    else
+      cudaFreeAsync(ptr, stream);  // stream-ordered: safe after every queued reader
+  }
 }
 
-std::shared_ptr<Block> Session::raw(size_t words) { return std::make_shared<Block>(words, stream); }
+std::shared_ptr<Block> Block::persistent(size_t words) {
+  u64* p = nullptr;
+  MPCG_CUDA(cudaMalloc(&p, (words ? words : 1) * sizeof(u64)));
+  auto b = std::make_shared<Block>(p, words);
+  b->owned = true;
+  b->sync_free = true;
+  return b;
+}
+
+std::shared_ptr<Block> Session::raw(size_t words) {
+  if (cap.active) return std::make_shared<Block>(arena_alloc(words), words);
+  return std::make_shared<Block>(words, stream);
+}
+
+u64* Session::arena_alloc(size_t words) {
+  const size_t w = (words + 31) / 32 * 32;  // 256-byte aligned
+  while (true) {
+    if (cap.chunk < cap.chunks.size()) {
+      auto& [p, n] = cap.chunks[cap.chunk];
+      if (cap.off + w <= n) {
+        u64* r = p + cap.off;
+        cap.off += w;
+        return r;
+      }
+      ++cap.chunk;
+      cap.off = 0;
+      continue;
+    }
+    const size_t n = std::max<size_t>(w, size_t(32) << 20);  // >= 256 MiB chunks
+    u64* p = nullptr;
+    MPCG_CUDA(cudaMalloc(&p, n * sizeof(u64)));
+    cap.chunks.push_back({p, n});
+  }
+}
 
 DT Session::alloc(const Shape& shape, int scale) {
   DT t;
@@ -152,6 +190,12 @@ Session::~Session() {
     if (b) cudaEventDestroy(b);
   }
   if (flush_buf) cudaFree(flush_buf);
+  if (cap.exec) cudaGraphExecDestroy(cap.exec);
+  if (cap.graph) cudaGraphDestroy(cap.graph);
+  for (auto& [p, n] : cap.chunks) cudaFree(p);
+  if (cap.tab) cudaFree(cap.tab);
+  if (cap.meta) cudaFree(cap.meta);
+  if (cap.iter) cudaFree(cap.iter);
   if (nccl) nccl_api().CommDestroy(nccl);
   cudaFree(link_state_);
   cudaStreamDestroy(comm_stream);
@@ -180,8 +224,21 @@ u64 Session::tag_stream(const std::string& tag) {
 Triple Session::fetch(const TripleSpec& spec, const std::string& tag, bool batch_b) {
   Triple t;
   t.spec = spec;
+  const u64* kp = nullptr;
+  if (cap.active && !tag.empty()) {  // replayed fetch: key slot refreshed per replay
+    u64 h = 0xcbf29ce484222325ull;
+    for (char c : tag) h = (h ^ u64(static_cast<unsigned char>(c))) * 0x100000001b3ull;
+    if (cap.hs.size() >= kMaxKeys) throw Error(kConfigError, "graph capture: too many triple fetches");
+    kp = cap.tab + cap.hs.size();
+    cap.hs.push_back(h);
+    cap.c0s.push_back(tag_counts[h]);
+  } else if (cap.active) {
+    throw Error(kUsageError, "graph capture needs tagged fetches");
+  }
   const u64 stream_id = tag_stream(tag);
   t.key = seed ^ (stream_id * kPhi);
+  t.ew.kp = kp;
+  t.mm.kp = kp;
   const u64 na = shape_numel(spec.shape_a);
   if (!spec.matmul) {
     if (spec.shape_a != spec.shape_b) throw Error(kConfigError, "dealer_gen_triple: elementwise shapes differ");
@@ -216,10 +273,106 @@ Triple Session::fetch(const TripleSpec& spec, const std::string& tag, bool batch
   return t;
 }
 
-u64 Session::take_mask(u64 numel_local) {
-  const u64 base = mask_ctr;
+Session::MaskRef Session::take_mask(u64 numel_local) {
+  const u64 base = mask_ctr + dp_offset(numel_local);
   mask_ctr += dp_global(numel_local);
-  return base + dp_offset(numel_local);
+  MaskRef r{base, nullptr};
+  if (cap.active) {
+    if (cap.mb0.size() >= kMaxMasks) throw Error(kConfigError, "graph capture: too many a2b calls");
+    r.bp = cap.tab + kMaxKeys + cap.mb0.size();
+    cap.mb0.push_back(base);
+    cap.mask_per_run += dp_global(numel_local);
+  }
+  return r;
+}
+
+// ------------------------------------------------------------------ graph capture
+namespace {
+// Refresh the replay's key table: tag h fetched with count c0 + iter (the reference's
+// per-tag counter, H/sharing/triple.hpp:146), mask bases advanced by whole runs.
+__global__ void rekey_kernel(u64* tab, const u64* meta, u32 nkeys, u32 nmasks, u64* iter, u64 seed,
+                             u64 mask_per_run, u32 kmax) {
+  const u64 it = *iter;
+  for (u32 i = threadIdx.x; i < nkeys; i += blockDim.x)
+    tab[i] = seed ^ (mix64(meta[i] + 0x51ed270bull * (meta[nkeys + i] + it * meta[2 * nkeys + i])) * kPhi);
+  for (u32 j = threadIdx.x; j < nmasks; j += blockDim.x) tab[kmax + j] = meta[3 * nkeys + j] + it * mask_per_run;
+  __syncthreads();
+  if (threadIdx.x == 0) *iter = it + 1;
+}
+}  // namespace
+
+void Session::begin_capture() {
+  if (cap.active) throw Error(kUsageError, "capture already active");
+  sync();
+  if (cap.exec) {
+    cudaGraphExecDestroy(cap.exec);
+    cudaGraphDestroy(cap.graph);
+    cap.exec = nullptr;
+    cap.graph = nullptr;
+  }
+  if (!cap.tab) {
+    MPCG_CUDA(cudaMalloc(&cap.tab, (kMaxKeys + kMaxMasks) * sizeof(u64)));
+    MPCG_CUDA(cudaMalloc(&cap.iter, 64));
+  }
+  MPCG_CUDA(cudaMemset(cap.iter, 0, 64));
+  cap.hs.clear();
+  cap.c0s.clear();
+  cap.mb0.clear();
+  cap.mask_per_run = 0;
+  cap.chunk = 0;
+  cap.off = 0;
+  cap.replays = 0;
+  for (int i = 0; i < 2; ++i) cap.stats_delta[i] = stats[i];
+  cap.seq_delta = next_seq;
+  cap.kernels = g_launches.load();
+  cap.active = true;
+  MPCG_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed));
+}
+
+void Session::end_capture() {
+  cap.active = false;
+  cudaError_t e = cudaStreamEndCapture(stream, &cap.graph);
+  MPCG_CUDA(e);
+  MPCG_CUDA(cudaGraphInstantiate(&cap.exec, cap.graph, 0));
+  cap.kernels = g_launches.load() - cap.kernels;
+  for (int i = 0; i < 2; ++i) {
+    cap.stats_delta[i].bytes_sent = stats[i].bytes_sent - cap.stats_delta[i].bytes_sent;
+    cap.stats_delta[i].collectives = stats[i].collectives - cap.stats_delta[i].collectives;
+    cap.stats_delta[i].p2p_sends = stats[i].p2p_sends - cap.stats_delta[i].p2p_sends;
+  }
+  cap.seq_delta = next_seq - cap.seq_delta;
+  const size_t nk = cap.hs.size(), nm = cap.mb0.size();
+  std::vector<u64> meta(3 * nk + nm + 1);
+  std::unordered_map<u64, u64> per_run;  // fetches of each tag per replay (its count stride)
+  for (u64 h : cap.hs) per_run[h]++;
+  std::copy(cap.hs.begin(), cap.hs.end(), meta.begin());
+  std::copy(cap.c0s.begin(), cap.c0s.end(), meta.begin() + nk);
+  for (size_t i = 0; i < nk; ++i) meta[2 * nk + i] = per_run[cap.hs[i]];
+  std::copy(cap.mb0.begin(), cap.mb0.end(), meta.begin() + 3 * nk);
+  if (cap.meta) cudaFree(cap.meta);
+  MPCG_CUDA(cudaMalloc(&cap.meta, meta.size() * sizeof(u64)));
+  MPCG_CUDA(cudaMemcpy(cap.meta, meta.data(), meta.size() * sizeof(u64), cudaMemcpyHostToDevice));
+}
+
+void Session::replay() {
+  if (!cap.exec) throw Error(kUsageError, "replay without a captured graph");
+  if (cap.replays > 0) {  // keep host dealer state in step with the device's draws
+    for (u64 h : cap.hs) tag_counts[h]++;
+    mask_ctr += cap.mask_per_run;
+    for (int i = 0; i < n_local; ++i) {
+      stats[i].bytes_sent += cap.stats_delta[i].bytes_sent;
+      stats[i].collectives += cap.stats_delta[i].collectives;
+      stats[i].p2p_sends += cap.stats_delta[i].p2p_sends;
+    }
+    next_seq += u32(cap.seq_delta);
+  }
+  cap.replays++;
+  rekey_kernel<<<1, 1024, 0, stream>>>(cap.tab, cap.meta, u32(cap.hs.size()), u32(cap.mb0.size()), cap.iter,
+                                       seed, cap.mask_per_run, u32(kMaxKeys));
+  MPCG_CUDA(cudaGetLastError());
+  MPCG_CUDA(cudaGraphLaunch(cap.exec, stream));
+  g_launches.fetch_add(cap.kernels + 1);
+  check();
 }
 
 // ------------------------------------------------------------------ wire
@@ -241,13 +394,13 @@ cudaEvent_t Session::pool_event() {
   return e;
 }
 
-Open Session::begin_open(size_t nwords, Reduce kind) {
+Open Session::begin_open(size_t nwords, Reduce kind, std::shared_ptr<Block> out, std::shared_ptr<Block> in) {
   Open o;
   o.n = nwords;
   o.kind = kind;
   o.n_local = n_local;
-  o.out = raw(nwords * size_t(n_local) + 1);
-  if (n_local == 1) o.in = raw(nwords + 1);
+  o.out = out ? out : raw(nwords * size_t(n_local) + 1);
+  if (n_local == 1) o.in = in ? in : raw(nwords + 1);
   o.seq = next_seq++;
   return o;
 }

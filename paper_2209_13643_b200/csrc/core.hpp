@@ -37,13 +37,19 @@ std::string shape_str(const Shape& s);
 u64 encode_fixed(double x, int scale_bits);
 
 // ------------------------------------------------------------------ device memory
-// Stream-ordered pool allocation (cudaMallocAsync), so allocation inside a CUDA-graph
-// capture becomes graph memory nodes with fixed addresses on replay.
+// Eager mode: stream-ordered pool allocation (cudaMallocAsync/cudaFreeAsync), safe after
+// every queued reader. Graph capture: a bump arena with fixed addresses and no reuse, so
+// one captured inference replays with every buffer at the same place (the arena is laid
+// out once; 180 GB of HBM3e leaves room for whole-inference arenas).
 struct Block {
   u64* ptr = nullptr;
   size_t words = 0;
   cudaStream_t stream = nullptr;
+  bool owned = true;
+  bool sync_free = false;  // cudaMalloc'd persistent buffer (outlives graph arenas)
   Block(size_t words, cudaStream_t s);
+  Block(u64* arena_ptr, size_t words) : ptr(arena_ptr), words(words), owned(false) {}
+  static std::shared_ptr<Block> persistent(size_t words);
   ~Block();
   Block(const Block&) = delete;
   Block& operator=(const Block&) = delete;
@@ -165,10 +171,38 @@ class Session {
   // ---- party mask rng (CounterRng(mask_seed, party)): sequential counters per slot
   u64 mask_key[2] = {0, 0};
   u64 mask_ctr = 0;  // same count for every party: each a2b draws numel per party
-  u64 take_mask(u64 numel_global);  // returns first counter, advances
+  struct MaskRef {
+    u64 base;
+    const u64* bp;  // device slot (graph replay) or null
+  };
+  MaskRef take_mask(u64 numel_local);  // first counter of this call's draws, advances
+
+  // ---- CUDA-graph capture of a whole inference (executor)
+  static constexpr size_t kMaxKeys = 1 << 15, kMaxMasks = 1 << 13;
+  struct Capture {
+    bool active = false;
+    u64* tab = nullptr;              // device: keys [0,kMaxKeys), mask bases [kMaxKeys, +kMaxMasks)
+    u64* meta = nullptr;             // device: h[], c0[], mbase0[] for the rekey kernel
+    u64* iter = nullptr;             // device replay counter
+    std::vector<u64> hs, c0s, mb0;
+    u64 mask_per_run = 0;
+    CommStats stats_delta[2];
+    u64 seq_delta = 0;
+    std::vector<std::pair<u64*, size_t>> chunks;  // arena (cudaMalloc'd, persistent)
+    size_t chunk = 0, off = 0;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    u64 kernels = 0;                 // kernel nodes in the graph
+    u64 replays = 0;
+  } cap;
+  u64* arena_alloc(size_t words);
+  void begin_capture();
+  void end_capture();
+  void replay();
 
   // ---- wire
-  Open begin_open(size_t nwords, Reduce kind);
+  Open begin_open(size_t nwords, Reduce kind, std::shared_ptr<Block> out = nullptr,
+                  std::shared_ptr<Block> in = nullptr);
   void post(Open& o, const std::string& tag, bool p2p = false);
   void wait(Open& o);
   u32 next_seq = 0;

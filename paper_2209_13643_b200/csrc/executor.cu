@@ -202,7 +202,11 @@ void SecureExecutor::prepare(size_t i) {
   t.mark_consumed();
   const DT& W = w_.at(op.wkey);
   const size_t nb = W.numel();
-  Open d = s_.begin_open(nb, Reduce::Sum);
+  if (!op.dbuf_out) {  // fixed address: the wrap-around prefetch crosses graph replays
+    op.dbuf_out = Block::persistent(nb * s_.n_local + 1);
+    if (s_.n_local == 1) op.dbuf_in = Block::persistent(nb + 1);
+  }
+  Open d = s_.begin_open(nb, Reduce::Sum, op.dbuf_out, op.dbuf_in);
   delta_build_mem(s_, t, W.s, nb, d);
   s_.post(d, op.tag + ".delta");
   op.triple = t;
@@ -388,6 +392,30 @@ DT SecureExecutor::run_layer(const LayerSpec& l, const DT& x, const Shape& in_sh
     }
   }
   throw Error(kProtocolError, "unhandled layer kind");
+}
+
+void SecureExecutor::capture(const DT& input) {
+  if (time_layers) throw Error(kUsageError, "disable layer timing before capture");
+  if (opt_.pipelined && !public_ && !wops_.empty() && !wops_[0].triple)
+    throw Error(kUsageError, "capture needs one eager run first (pipelined prologue)");
+  s_.begin_capture();
+  try {
+    graph_out_ = run(input);
+  } catch (...) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(s_.stream, &g);
+    if (g) cudaGraphDestroy(g);
+    s_.cap.active = false;
+    throw;
+  }
+  s_.end_capture();
+  captured_ = true;
+}
+
+DT SecureExecutor::replay() {
+  if (!captured_) throw Error(kUsageError, "replay before capture");
+  s_.replay();
+  return graph_out_;
 }
 
 DT SecureExecutor::run(const DT& input) {

@@ -58,6 +58,15 @@ class SecureExecutor {
 
   DT run(const DT& input);
 
+  // CUDA-graph capture of one steady-state inference reading `input` in place (refill it
+  // with mpcg_tensor_copy_from_host between replays). replay() returns the arena-backed
+  // logits, valid until the next replay. Values equal the eager run's, iteration by
+  // iteration (device key table refreshed per replay).
+  void capture(const DT& input);
+  DT replay();
+  DT graph_out_;
+  bool captured_ = false;
+
   std::vector<std::string> linear_tags() const;
   std::vector<LayerTiming> timings;
   bool time_layers = false;
@@ -72,6 +81,7 @@ class SecureExecutor {
     TripleSpec spec;
     std::optional<Triple> triple;
     std::optional<Open> delta;
+    std::shared_ptr<Block> dbuf_out, dbuf_in;  // persistent delta payload (fixed address across runs)
   };
   void add_weight_op(const std::string& tag, const std::string& wkey, const std::string& bkey, Shape x_shape);
   void build_weight_ops();

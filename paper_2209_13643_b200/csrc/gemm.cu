@@ -19,8 +19,10 @@ __global__ void __launch_bounds__(256) ring_gemm_simt(GemmArgs a) {
   static_assert(TX * TY == 256, "256 threads");
   __shared__ u64 As[BK][BM + 1];
   __shared__ u64 Bs[BK][BN + 1];
+  // blockIdx.z = (split * nbatch + b) * nslots + slot
   const int slot = blockIdx.z % a.nslots;
-  const u32 b = blockIdx.z / a.nslots;
+  const u32 zb = blockIdx.z / a.nslots;
+  const u32 b = zb % a.nbatch, split = zb / a.nbatch;
   const GemmSlotArgs& S = a.sl[slot];
   const u32 M = a.M, N = a.N, K = a.K;
   const u32 m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
@@ -30,29 +32,35 @@ __global__ void __launch_bounds__(256) ring_gemm_simt(GemmArgs a) {
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = 0;
+  // this block's slice [kb, ke) of the concatenated K' = nseg*K axis
+  const u32 kb = a.ksplit > 1 ? split * a.kchunk : 0;
+  const u32 ke = a.ksplit > 1 ? min(kb + a.kchunk, u32(S.nseg) * K) : u32(S.nseg) * K;
 
   for (int sg = 0; sg < S.nseg; ++sg) {
+    const u32 sb = u32(sg) * K;
+    if (sb + K <= kb || sb >= ke) continue;
+    const u32 lo = kb > sb ? kb - sb : 0, hi = min(K, ke - sb);
     const u64* L = S.L[sg] + u64(b) * S.sL[sg];
     const u64* R = S.R[sg] + u64(b) * S.sR[sg];
-    for (u32 k0 = 0; k0 < K; k0 += BK) {
+    for (u32 k0 = lo; k0 < hi; k0 += BK) {
       for (int e = threadIdx.x; e < BM * BK; e += 256) {
         const int kk = e % BK, mm = e / BK;
         u64 v = 0;
-        if (m0 + mm < M && k0 + kk < K) v = L[u64(m0 + mm) * K + k0 + kk];
+        if (m0 + mm < M && k0 + kk < hi) v = L[u64(m0 + mm) * K + k0 + kk];
         As[kk][mm] = v;
       }
       if (!a.tb) {
         for (int e = threadIdx.x; e < BN * BK; e += 256) {
           const int nn = e % BN, kk = e / BN;
           u64 v = 0;
-          if (k0 + kk < K && n0 + nn < N) v = R[u64(k0 + kk) * N + n0 + nn];
+          if (k0 + kk < hi && n0 + nn < N) v = R[u64(k0 + kk) * N + n0 + nn];
           Bs[kk][nn] = v;
         }
       } else {
         for (int e = threadIdx.x; e < BN * BK; e += 256) {
           const int kk = e % BK, nn = e / BK;
           u64 v = 0;
-          if (k0 + kk < K && n0 + nn < N) v = R[u64(n0 + nn) * K + k0 + kk];
+          if (k0 + kk < hi && n0 + nn < N) v = R[u64(n0 + nn) * K + k0 + kk];
           Bs[kk][nn] = v;
         }
       }
@@ -72,6 +80,7 @@ __global__ void __launch_bounds__(256) ring_gemm_simt(GemmArgs a) {
       __syncthreads();
     }
   }
+  u64* accp = a.ksplit > 1 ? a.acc[slot] : nullptr;
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     const u32 m = m0 + ty + i * TY;
@@ -80,18 +89,60 @@ __global__ void __launch_bounds__(256) ring_gemm_simt(GemmArgs a) {
     for (int j = 0; j < TN; ++j) {
       const u32 n = n0 + tx + j * TX;
       if (n >= N) continue;
-      gemm_epilogue(a, S, b, m, n, acc[i][j]);
+      if (accp)  // partial sum; wrapping u64 add is exact and order-independent
+        atomicAdd(reinterpret_cast<unsigned long long*>(accp + (u64(b) * M + m) * N + n),
+                  static_cast<unsigned long long>(acc[i][j]));
+      else
+        gemm_epilogue(a, S, b, m, n, acc[i][j]);
     }
   }
 }
 
+__global__ void __launch_bounds__(256) gemm_splitk_epilogue(GemmArgs a) {
+  const u64 per = u64(a.nbatch) * a.M * a.N;
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < per * a.nslots; i += u64(gridDim.x) * blockDim.x) {
+    const int slot = int(i / per);
+    const u64 r = i - slot * per;
+    const u32 n = u32(r % a.N), m = u32((r / a.N) % a.M), b = u32(r / (u64(a.N) * a.M));
+    gemm_epilogue(a, a.sl[slot], b, m, n, a.acc[slot][r]);
+  }
+}
+
 template <int BM, int BN, int TM, int TN>
-void launch_simt(const GemmArgs& a, cudaStream_t st) {
-  dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, a.nslots * a.nbatch);
+void launch_simt(Session& s, GemmArgs a) {
+  cudaStream_t st = s.stream;
+  const u64 tiles = u64((a.N + BN - 1) / BN) * ((a.M + BM - 1) / BM) * a.nslots * a.nbatch;
+  int maxseg = 0;
+  for (int i = 0; i < a.nslots; ++i) maxseg = a.sl[i].nseg > maxseg ? a.sl[i].nseg : maxseg;
+  const u32 kp = u32(maxseg) * a.K;
+  // split K' until ~2 waves of CTAs exist, keeping >= 2 k-steps of 16 per split
+  u32 split = 1;
+  if (tiles < 2 * u64(kSms)) {
+    split = u32((2 * u64(kSms) + tiles - 1) / tiles);
+    const u32 maxsplit = (kp + 31) / 32;
+    split = split > maxsplit ? maxsplit : split;
+    split = split < 1 ? 1 : split;
+  }
+  std::shared_ptr<Block> ws;
+  if (split > 1) {
+    a.ksplit = split;
+    a.kchunk = ((kp + split - 1) / split + 15) / 16 * 16;
+    a.ksplit = (kp + a.kchunk - 1) / a.kchunk;
+    const u64 per = u64(a.nbatch) * a.M * a.N;
+    ws = s.raw(per * a.nslots);
+    MPCG_CUDA(cudaMemsetAsync(ws->ptr, 0, per * a.nslots * 8, st));
+    for (int i = 0; i < a.nslots; ++i) a.acc[i] = ws->ptr + i * per;
+  }
+  dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, a.nslots * a.nbatch * a.ksplit);
   cudaEvent_t pe;
   probe_begin(st, &pe);
   ring_gemm_simt<BM, BN, TM, TN><<<grid, 256, 0, st>>>(a);
   MPCG_CUDA(cudaGetLastError());
+  if (a.ksplit > 1) {
+    const u64 n = u64(a.nbatch) * a.M * a.N * a.nslots;
+    gemm_splitk_epilogue<<<ew_blocks(n), 256, 0, st>>>(a);
+    MPCG_CUDA(cudaGetLastError());
+  }
   probe_end(st, pe);
 }
 
@@ -100,19 +151,25 @@ void launch_simt(const GemmArgs& a, cudaStream_t st) {
 void ring_gemm_launch(Session& s, const GemmArgs& a) {
   if (a.M == 0 || a.N == 0 || a.nbatch == 0) return;
   if (a.M > 65535u * 64u) throw Error(kShapeError, "ring_gemm: M too large");
-  // algorithmic work: ring MACs of every segment of every slot (8 bytes/MAC-equivalent unused)
+  // algorithmic work: ring MACs of every segment of every slot
   double macs = 0;
   for (int i = 0; i < a.nslots; ++i) macs += double(a.sl[i].nseg) * a.M * a.N * a.K * a.nbatch;
   ClassScope cs(kClsGemm, macs);
   if (ring_gemm_tc_try(s, a)) return;  // tcgen05 int8-limb path when the shape qualifies
-  if (a.N <= 8)
-    launch_simt<128, 8, 4, 1>(a, s.stream);
-  else if (a.N <= 16)
-    launch_simt<128, 16, 8, 1>(a, s.stream);
-  else if (a.N <= 32)
-    launch_simt<64, 32, 4, 2>(a, s.stream);
-  else
-    launch_simt<64, 64, 4, 4>(a, s.stream);
+  if (a.M <= 16) {
+    if (a.N <= 16)
+      launch_simt<16, 16, 1, 1>(s, a);
+    else
+      launch_simt<16, 64, 1, 4>(s, a);
+  } else if (a.N <= 8) {
+    launch_simt<256, 8, 1, 8>(s, a);
+  } else if (a.N <= 16) {
+    launch_simt<256, 16, 2, 8>(s, a);
+  } else if (a.N <= 32) {
+    launch_simt<64, 32, 4, 2>(s, a);
+  } else {
+    launch_simt<64, 64, 4, 4>(s, a);
+  }
   s.check();
 }
 
@@ -249,6 +306,7 @@ void mm_combine(Session& s, const Triple& t, const DT& L, size_t na, const DT& R
     S.out = out[i] + out_off;
     S.bias = ep.bias[i];
     S.ckey = t.mm.key;
+    S.ckp = t.mm.kp;
     S.cbase = 1 + 2 * t.mm.na + 2 * t.mm.nb + t.mm.offC + out_off;
     if (s.party_of[i] == 0) {
       S.nseg = 3;

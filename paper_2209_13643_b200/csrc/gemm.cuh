@@ -15,6 +15,7 @@ struct GemmSlotArgs {
   const u64* bias = nullptr;  // [N], added after truncation
   int cterm = 0;              // +1 / -1: add / subtract the triple's r_C
   u64 ckey = 0, cbase = 0;    // r_C(idx) = drw(ckey, cbase + idx)
+  const u64* ckp = nullptr;   // device key slot (graph replay)
 };
 
 struct GemmArgs {
@@ -25,6 +26,10 @@ struct GemmArgs {
   int trunc_bits = 0;  // 2PC local truncation (H/protocols/trunc.hpp:41)
   int col2im = 0;      // store NCHW with row = (n, oh, ow)  (H/engine/executor.hpp:110-123)
   u32 OHW = 1;
+  // split-K over the concatenated K' = nseg*K axis: partial sums are added mod 2^64 into
+  // acc[slot] ([nbatch][M][N], zeroed) and a second kernel applies the epilogue.
+  u32 ksplit = 1, kchunk = 0;
+  u64* acc[2] = {nullptr, nullptr};
 };
 
 struct Epi {
@@ -42,7 +47,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& a, const GemmSlotA
                                               u64 v) {
   const u64 lin = (u64(b) * a.M + m) * a.N + n;
   if (S.cterm) {
-    const u64 rc = drw(S.ckey, S.cbase + lin);
+    const u64 rc = drw(tkey(S.ckey, S.ckp), S.cbase + lin);
     v = S.cterm > 0 ? v + rc : v - rc;
   }
   if (a.trunc_bits) v = sar64(v, a.trunc_bits);

@@ -240,12 +240,12 @@ struct PartY {
 template <class XF>
 DT a2b_mask(Session& s, size_t n, XF xf, Open& o) {
   DT keep = s.alloc(Shape{n});
-  const u64 base = s.take_mask(n);
+  const Session::MaskRef mr = s.take_mask(n);
   o = s.begin_open(n, Reduce::Sum);
   const Ptr2 own = own_ptrs(o), kp = ptrs(keep);
   const u64 k0 = s.mask_key[0], k1 = s.mask_key[1];
   launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) {
-    const u64 r = drw(slot == 0 ? k0 : k1, base + 1 + i);
+    const u64 r = drw(slot == 0 ? k0 : k1, tkey(mr.base, mr.bp) + 1 + i);
     own.p[slot][i] = r;
     kp.p[slot][i] = xf(slot, i) ^ r;
   });

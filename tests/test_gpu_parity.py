@@ -102,6 +102,40 @@ def test_model_logit_shares_match_reference(mp, path):
     assert np.abs(dec - ref).max() <= 2.0 ** -6  # P/tools/mpcpipe_bench.cpp:124
 
 
+@pytest.mark.parametrize("name,mode,weights,it", [
+    ("mlp", "pipelined", "private", 2), ("toy_cnn", "blocking", "private", 1),
+    ("toy_transformer", "blocking", "private", 1), ("toy_transformer", "blocking", "public", 1),
+    ("lenet5", "pipelined", "private", 1)])
+def test_graph_replay_matches_reference(mp, name, mode, weights, it):
+    """CUDA-graph replays draw each iteration's triples exactly like eager runs."""
+    g = mp.ModelGraph.from_json(os.path.join(ROOT, "configs", name + ".json"))
+    m = np.load(os.path.join(ROOT, "tests", "golden", f"model_{name}_{mode}_{weights}_it{it}.npz"))
+    s = mp.Session(device=0, n_local=2, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
+    ex = mp.SecureExecutor(s, g, public_weights=weights == "public", pipelined=mode == "pipelined")
+    ex.deal_weights(mp.init_weights(g, 12), 1)
+    x = s.deal_input(mp.demo_input(g, 13), 2)
+    eager = 1 if mode == "pipelined" else 0   # pipelined: run once for the delta prologue
+    for _ in range(eager):
+        z = ex.run(x)
+    ex.capture(x)
+    for _ in range(it - eager):
+        z = ex.replay()
+    z = z.numpy()
+    assert np.array_equal(z[0].reshape(-1), m["z0"].reshape(-1))
+    assert np.array_equal(z[1].reshape(-1), m["z1"].reshape(-1))
+    # more replays keep tracking eager runs iteration by iteration
+    s2 = mp.Session(device=0, n_local=2, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
+    ex2 = mp.SecureExecutor(s2, g, public_weights=weights == "public", pipelined=mode == "pipelined")
+    ex2.deal_weights(mp.init_weights(g, 12), 1)
+    x2 = s2.deal_input(mp.demo_input(g, 13), 2)
+    for _ in range(it + 2):
+        ze = ex2.run(x2)
+    for _ in range(2):
+        zr = ex.replay()
+    assert np.array_equal(zr.numpy(), ze.numpy())
+    assert s.stats(0) == s2.stats(0)
+
+
 def test_blocking_and_pipelined_are_bit_identical(mp):
     g = mp.ModelGraph.from_json(os.path.join(ROOT, "configs", "toy_cnn.json"))
     _, zb = _run_model(mp, g, "blocking", "private", 2)
