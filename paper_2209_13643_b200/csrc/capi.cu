@@ -403,6 +403,7 @@ int mpcg_executor_time_layers(mpcg_executor* e, int enable) {
 int mpcg_executor_layer_times(mpcg_executor* e, int max, float* ms, int* count) {
   return guard([&] {
     need(e, "executor");
+    if (e->e->captured_ && e->e->time_layers) e->e->collect_timings();  // events of the last replay
     const auto& t = e->e->timings;
     const int n = int(t.size()) < max ? int(t.size()) : max;
     for (int i = 0; i < n; ++i) ms[i] = t[i].ms;

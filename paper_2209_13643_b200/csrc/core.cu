@@ -232,8 +232,15 @@ Triple Session::fetch(const TripleSpec& spec, const std::string& tag, bool batch
     kp = cap.tab + cap.hs.size();
     cap.hs.push_back(h);
     cap.c0s.push_back(tag_counts[h]);
+    cap.carried.push_back(0);
   } else if (cap.active) {
     throw Error(kUsageError, "graph capture needs tagged fetches");
+  }
+  if (!tag.empty()) {
+    u64 h = 0xcbf29ce484222325ull;
+    for (char c : tag) h = (h ^ u64(static_cast<unsigned char>(c))) * 0x100000001b3ull;
+    t.tag_hash = h;
+    t.count = tag_counts[h];
   }
   const u64 stream_id = tag_stream(tag);
   t.key = seed ^ (stream_id * kPhi);
@@ -301,6 +308,18 @@ __global__ void rekey_kernel(u64* tab, const u64* meta, u32 nkeys, u32 nmasks, u
 }
 }  // namespace
 
+void Session::capture_adopt(Triple& t) {
+  if (!cap.active) throw Error(kUsageError, "capture_adopt outside a capture");
+  if (t.ew.kp || t.mm.kp) return;
+  if (cap.hs.size() >= kMaxKeys) throw Error(kConfigError, "graph capture: too many triple fetches");
+  const u64* kp = cap.tab + cap.hs.size();
+  cap.hs.push_back(t.tag_hash);
+  cap.c0s.push_back(t.count);
+  cap.carried.push_back(1);
+  t.ew.kp = kp;
+  t.mm.kp = kp;
+}
+
 void Session::begin_capture() {
   if (cap.active) throw Error(kUsageError, "capture already active");
   sync();
@@ -318,6 +337,7 @@ void Session::begin_capture() {
   cap.hs.clear();
   cap.c0s.clear();
   cap.mb0.clear();
+  cap.carried.clear();
   cap.mask_per_run = 0;
   cap.chunk = 0;
   cap.off = 0;
@@ -344,7 +364,8 @@ void Session::end_capture() {
   const size_t nk = cap.hs.size(), nm = cap.mb0.size();
   std::vector<u64> meta(3 * nk + nm + 1);
   std::unordered_map<u64, u64> per_run;  // fetches of each tag per replay (its count stride)
-  for (u64 h : cap.hs) per_run[h]++;
+  for (size_t i = 0; i < nk; ++i)
+    if (!cap.carried[i]) per_run[cap.hs[i]]++;
   std::copy(cap.hs.begin(), cap.hs.end(), meta.begin());
   std::copy(cap.c0s.begin(), cap.c0s.end(), meta.begin() + nk);
   for (size_t i = 0; i < nk; ++i) meta[2 * nk + i] = per_run[cap.hs[i]];
@@ -357,7 +378,8 @@ void Session::end_capture() {
 void Session::replay() {
   if (!cap.exec) throw Error(kUsageError, "replay without a captured graph");
   if (cap.replays > 0) {  // keep host dealer state in step with the device's draws
-    for (u64 h : cap.hs) tag_counts[h]++;
+    for (size_t i = 0; i < cap.hs.size(); ++i)
+      if (!cap.carried[i]) tag_counts[cap.hs[i]]++;
     mask_ctr += cap.mask_per_run;
     for (int i = 0; i < n_local; ++i) {
       stats[i].bytes_sent += cap.stats_delta[i].bytes_sent;

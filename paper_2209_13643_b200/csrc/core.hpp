@@ -99,6 +99,7 @@ struct TripleSpec {
 struct Triple {
   TripleSpec spec;
   u64 key = 0;
+  u64 tag_hash = 0, count = 0;  // FNV-1a of the tag and the fetch count that keyed it
   bool consumed = false;
   EwTriple ew{};  // elementwise view (global numel / shard offsets filled)
   MmTriple mm{};  // matmul view
@@ -185,6 +186,7 @@ class Session {
     u64* meta = nullptr;             // device: h[], c0[], mbase0[] for the rekey kernel
     u64* iter = nullptr;             // device replay counter
     std::vector<u64> hs, c0s, mb0;
+    std::vector<char> carried;  // key slot adopted from a fetch made before the capture
     u64 mask_per_run = 0;
     CommStats stats_delta[2];
     u64 seq_delta = 0;
@@ -196,6 +198,9 @@ class Session {
     u64 replays = 0;
   } cap;
   u64* arena_alloc(size_t words);
+  // A triple fetched before the capture but consumed inside it (the pipelined wrap-around
+  // prefetch): give it a key slot that tracks the previous replay's prefetch.
+  void capture_adopt(Triple& t);
   void begin_capture();
   void end_capture();
   void replay();

@@ -395,11 +395,12 @@ DT SecureExecutor::run_layer(const LayerSpec& l, const DT& x, const Shape& in_sh
 }
 
 void SecureExecutor::capture(const DT& input) {
-  if (time_layers) throw Error(kUsageError, "disable layer timing before capture");
   if (opt_.pipelined && !public_ && !wops_.empty() && !wops_[0].triple)
     throw Error(kUsageError, "capture needs one eager run first (pipelined prologue)");
   s_.begin_capture();
   try {
+    for (auto& op : wops_)  // prefetched before the capture, consumed inside it
+      if (op.triple) s_.capture_adopt(*op.triple);
     graph_out_ = run(input);
   } catch (...) {
     cudaGraph_t g = nullptr;
@@ -436,16 +437,19 @@ DT SecureExecutor::run(const DT& input) {
     cur_shape = shapes_[i];
     if (time_layers) MPCG_CUDA(cudaEventRecord(ev_[i + 1], s_.stream));
   }
-  if (time_layers) {
-    MPCG_CUDA(cudaEventSynchronize(ev_.back()));
-    timings.clear();
-    for (size_t i = 0; i < g_.layers.size(); ++i) {
-      float ms = 0;
-      MPCG_CUDA(cudaEventElapsedTime(&ms, ev_[i], ev_[i + 1]));
-      timings.push_back({g_.layers[i].name, ms});
-    }
-  }
+  if (time_layers && !s_.cap.active) collect_timings();  // captured: event nodes, read after replay
   return cur;
+}
+
+void SecureExecutor::collect_timings() {
+  if (ev_.size() < g_.layers.size() + 1) return;
+  MPCG_CUDA(cudaEventSynchronize(ev_.back()));
+  timings.clear();
+  for (size_t i = 0; i < g_.layers.size(); ++i) {
+    float ms = 0;
+    MPCG_CUDA(cudaEventElapsedTime(&ms, ev_[i], ev_[i + 1]));
+    timings.push_back({g_.layers[i].name, ms});
+  }
 }
 
 }  // namespace mpcg

@@ -69,7 +69,8 @@ class SecureExecutor {
 
   std::vector<std::string> linear_tags() const;
   std::vector<LayerTiming> timings;
-  bool time_layers = false;
+  bool time_layers = false;   // per-layer CUDA events (also captured into the graph)
+  void collect_timings();
 
   const ModelGraph& graph() const { return g_; }
   const std::vector<Shape>& shapes() const { return shapes_; }
