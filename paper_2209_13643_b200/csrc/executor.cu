@@ -431,11 +431,12 @@ DT SecureExecutor::run(const DT& input) {
   }
   DT cur = input;
   Shape cur_shape = g_.input;
-  if (time_layers) MPCG_CUDA(cudaEventRecord(ev_[0], s_.stream));
+  const unsigned rec_flags = s_.cap.active ? cudaEventRecordExternal : cudaEventRecordDefault;  // graph event nodes
+  if (time_layers) MPCG_CUDA(cudaEventRecordWithFlags(ev_[0], s_.stream, rec_flags));
   for (size_t i = 0; i < g_.layers.size(); ++i) {
     cur = run_layer(g_.layers[i], cur, cur_shape);
     cur_shape = shapes_[i];
-    if (time_layers) MPCG_CUDA(cudaEventRecord(ev_[i + 1], s_.stream));
+    if (time_layers) MPCG_CUDA(cudaEventRecordWithFlags(ev_[i + 1], s_.stream, rec_flags));
   }
   if (time_layers && !s_.cap.active) collect_timings();  // captured: event nodes, read after replay
   return cur;
