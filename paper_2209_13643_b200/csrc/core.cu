@@ -423,7 +423,6 @@ Open Session::begin_open(size_t nwords, Reduce kind, std::shared_ptr<Block> out,
   o.n_local = n_local;
   o.out = out ? out : raw(nwords * size_t(n_local) + 1);
   if (n_local == 1) o.in = in ? in : raw(nwords + 1);
-  o.seq = next_seq++;
   return o;
 }
 
@@ -454,6 +453,7 @@ void Session::throttle(Open& o) {
 void Session::post(Open& o, const std::string& tag, bool p2p) {
   if (o.posted) throw Error(kUsageError, "open posted twice");
   o.posted = true;
+  o.seq = next_seq++;  // collective order = post order (what both parties must agree on)
   for (int i = 0; i < n_local; ++i) {
     stats[i].bytes_sent += o.n * 8;
     if (p2p)

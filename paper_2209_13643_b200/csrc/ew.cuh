@@ -184,14 +184,6 @@ struct SpkLevel {
   u64 in, out, mult;
 };
 
-struct SumSink {  // binary share of the sum
-  Ptr2 out;
-  __device__ void operator()(int slot, u64 g, u64 sum) const { out.p[slot][g] = sum; }
-};
-struct MsbSink {  // sign bit in position 0 (H/protocols/compare.hpp:57-62)
-  Ptr2 out;
-  __device__ void operator()(int slot, u64 g, u64 sum) const { out.p[slot][g] = sum >> 63; }
-};
 
 template <class XF, class YF, class FF>
 struct AdderRound {
@@ -218,10 +210,10 @@ struct AdderRound {
       ownn.p[slot][w + j] = y ^ b;
       return;
     }
-    const u64* o = ownp.p[slot];
     const u64* q = peerp.p[slot];
     u64 s, p;
     if (rp == 0) {  // settle the generate AND (H/protocols/adder.hpp:209-223)
+      const u64* o = ownp.p[slot];
       const u64 e = o[j] ^ q[j], d = o[w + j] ^ q[w + j];
       u64 a, b, c;
       ew_abc(Tp, party, Tp.off + g, a, b, c);
@@ -229,19 +221,24 @@ struct AdderRound {
       if (party == 0) s ^= e & d;
       p = P0.p[slot][g];
     } else {  // settle a prefix level (H/protocols/adder.hpp:142-165)
-      const u64 e0 = o[j] ^ q[j], e1 = o[w + j] ^ q[w + j];
-      const u64 d0 = o[2 * w + j] ^ q[2 * w + j], d1 = o[3 * w + j] ^ q[3 * w + j];
+      // Own payload is recomputed from the pre-round state instead of re-read from HBM:
+      // it is a function of (s, p) and the triple, all of which this thread holds.
       u64 a0, b0, c0, a1, b1, c1;
       ew_abc(Tp, party, Tp.off + g, a0, b0, c0);
       ew_abc(Tp, party, Tp.ghalf + Tp.off + g, a1, b1, c1);
+      const u64 s0 = S.p[slot][g], p0s = P.p[slot][g];
+      const u64 po = p0s & lp.out;
+      const u64 e0 = (po ^ a0) ^ q[j], e1 = (po ^ a1) ^ q[w + j];
+      const u64 d0 = (((s0 & lp.in) * lp.mult) ^ b0) ^ q[2 * w + j];
+      const u64 d1 = (((p0s & lp.in) * lp.mult) ^ b1) ^ q[3 * w + j];
       u64 z0 = c0 ^ (e0 & b0) ^ (d0 & a0);
       u64 z1 = c1 ^ (e1 & b1) ^ (d1 & a1);
       if (party == 0) {
         z0 ^= e0 & d0;
         z1 ^= e1 & d1;
       }
-      s = S.p[slot][g] ^ z0;
-      p = (P.p[slot][g] & ~lp.out) ^ z1;
+      s = s0 ^ z0;
+      p = (p0s & ~lp.out) ^ z1;
     }
     if (rn <= levels) {  // issue level rn-1 (H/protocols/adder.hpp:122-140)
       const u64 p0 = p & ln.out;
@@ -256,7 +253,7 @@ struct AdderRound {
       S.p[slot][g] = s;
       P.p[slot][g] = p;
     } else {
-      ff(slot, g, (P0.p[slot][g] ^ (s << 1)) & wmask);
+      ff(slot, party, g, j, (P0.p[slot][g] ^ (s << 1)) & wmask);
     }
   }
 };
@@ -268,9 +265,18 @@ struct SpkConsts {
 };
 SpkConsts make_spk_constants(int width);
 
-// Secure binary addition of XOR-shared operands given by sources; the sum goes to ff.
-template <class XF, class YF, class FF>
-void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& tag, XF xf, YF yf, FF ff) {
+struct NoPost {
+  void operator()(int) const {}
+};
+
+// Secure binary addition of XOR-shared operands given by sources. The last kernel of each
+// lane hands the sum to ff_for_lane(lane, lo, w) — a functor (slot, party, g, j, sum) that
+// may already build the next protocol's payload for the same lane — and post_lane(lane)
+// runs right after it (to post that payload), so a protocol tail costs no extra kernel.
+template <class XF, class YF, class FFL, class POST = NoPost>
+void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& tag, XF xf, YF yf,
+              FFL ff_for_lane, POST post_lane = NoPost{}) {
+  using FF = decltype(ff_for_lane(0, size_t(0), size_t(0)));
   const SpkConsts c = make_spk_constants(opt.width);
   const int chunks = clamp_chunks(opt.chunks, n);
   const Pid2 pid = pids(s);
@@ -289,7 +295,8 @@ void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& 
   };
   std::vector<Open> hs(static_cast<size_t>(chunks));
   auto kernel = [&](int rp, int rn, int lane, Open* prev, Open* next) {
-    const auto rng_ = chunk_range(n, chunks, lane); const size_t lo = rng_.first, hi = rng_.second;
+    const auto rng_ = chunk_range(n, chunks, lane);
+    const size_t lo = rng_.first, hi = rng_.second;
     AdderRound<XF, YF, FF> k{};
     k.rp = rp;
     k.rn = rn;
@@ -312,25 +319,24 @@ void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& 
     k.wmask = c.wmask;
     k.xf = xf;
     k.yf = yf;
-    k.ff = ff;
-    // per element per party: round 0 issue = 2x16 wire + 8x(2 in + 1 out); level = 2x32 wire
-    // + 8x(2 in + 2 out); final = 2x32 wire + 8x(3 in + 1 out)
-    const double per = rn == 0 ? 56.0 : (rn <= c.levels ? 96.0 : 96.0);
-    ClassScope cs(rn >= 1 && rn <= c.levels ? kClsAdderRound : kClsOther, per * double(hi - lo) * s.n_local);
+    if (rn > c.levels) k.ff = ff_for_lane(lane, lo, hi - lo);
+    // algorithmic bytes per element per party (2 x wire + 8 x (in + out)):
+    // level round = 2x32 wire + 8x(2 state in + 2 state out) = 96 B
+    ClassScope cs(rn >= 1 && rn <= c.levels ? kClsAdderRound : kClsOther, 96.0 * double(hi - lo) * s.n_local);
     launch_ew(s.stream, s.n_local, hi - lo, k);
   };
   fetch_round(0);
   for (int lane = 0; lane < chunks; ++lane) {
-    const auto rng_ = chunk_range(n, chunks, lane); const size_t lo = rng_.first, hi = rng_.second;
-    hs[lane] = s.begin_open(2 * (hi - lo), Reduce::Xor);
+    const auto rng_ = chunk_range(n, chunks, lane);
+    hs[lane] = s.begin_open(2 * (rng_.second - rng_.first), Reduce::Xor);
     kernel(-1, 0, lane, nullptr, &hs[lane]);
     s.post(hs[lane], round_tag(0, lane));
   }
   for (int r = 1; r < rounds; ++r) {
     fetch_round(r);
     for (int lane = 0; lane < chunks; ++lane) {
-      const auto rng_ = chunk_range(n, chunks, lane); const size_t lo = rng_.first, hi = rng_.second;
-      Open next = s.begin_open(4 * (hi - lo), Reduce::Xor);
+      const auto rng_ = chunk_range(n, chunks, lane);
+      Open next = s.begin_open(4 * (rng_.second - rng_.first), Reduce::Xor);
       s.wait(hs[lane]);
       kernel(r - 1, r, lane, &hs[lane], &next);
       hs[lane] = std::move(next);
@@ -340,8 +346,28 @@ void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& 
   for (int lane = 0; lane < chunks; ++lane) {
     s.wait(hs[lane]);
     kernel(rounds - 1, rounds, lane, &hs[lane], nullptr);
+    post_lane(lane);
   }
   s.check();
+}
+
+// Plain final sinks for adder_op (same functor for every lane).
+struct SumSink {  // binary share of the sum
+  Ptr2 out;
+  __device__ void operator()(int slot, int, u64 g, u64, u64 sum) const { out.p[slot][g] = sum; }
+};
+struct MsbSink {  // sign bit in position 0 (H/protocols/compare.hpp:57-62)
+  Ptr2 out;
+  __device__ void operator()(int slot, int, u64 g, u64, u64 sum) const { out.p[slot][g] = sum >> 63; }
+};
+template <class FF>
+struct SameFF {
+  FF f;
+  FF operator()(int, size_t, size_t) const { return f; }
+};
+template <class FF>
+SameFF<FF> same(FF f) {
+  return SameFF<FF>{f};
 }
 
 }  // namespace mpcg

@@ -215,7 +215,7 @@ DT beaver_and(Session& s, const DT& x, const DT& y, const std::string& tag, int 
 DT binary_add(Session& s, const DT& x, const DT& y, const AdderOptions& opt, const std::string& tag) {
   require_same_shape(x, y, "binary_add");
   DT z = s.alloc(x.shape, x.scale);
-  adder_op(s, x.numel(), opt, tag, SrcMem{cptrs(x)}, SrcMem{cptrs(y)}, SumSink{ptrs(z)});
+  adder_op(s, x.numel(), opt, tag, SrcMem{cptrs(x)}, SrcMem{cptrs(y)}, same(SumSink{ptrs(z)}));
   return z;
 }
 
@@ -236,7 +236,7 @@ struct PartY {
   }
 };
 
-// Mask draw + p2p send of r, keep = x ^ r. Returns the keep tensor and the open.
+// Mask draw + p2p send of r, keep = x ^ r (H/protocols/compare.hpp:31-46).
 template <class XF>
 DT a2b_mask(Session& s, size_t n, XF xf, Open& o) {
   DT keep = s.alloc(Shape{n});
@@ -254,13 +254,14 @@ DT a2b_mask(Session& s, size_t n, XF xf, Open& o) {
   return keep;
 }
 
-template <class XF, class FF>
-void a2b_op(Session& s, size_t n, const AdderOptions& opt, const std::string& tag, XF xf, FF ff) {
+template <class XF, class FFL, class POST = NoPost>
+void a2b_op(Session& s, size_t n, const AdderOptions& opt, const std::string& tag, XF xf, FFL ffl,
+            POST post = NoPost{}) {
   Open o;
   DT keep = a2b_mask(s, n, xf, o);
   const Pid2 pid = pids(s);
-  adder_op(s, n, opt, tag + ".add1", PartX{pid, cptrs(keep), peer_ptrs(o)},
-           PartY{pid, cptrs(keep), peer_ptrs(o)}, ff);
+  adder_op(s, n, opt, tag + ".add1", PartX{pid, cptrs(keep), peer_ptrs(o)}, PartY{pid, cptrs(keep), peer_ptrs(o)},
+           ffl, post);
 }
 
 // b2a_bit (H/protocols/compare.hpp:67-83, n=2): acc = b0 on party 0, bq = b1 on party 1;
@@ -282,17 +283,105 @@ struct B2aSink {
     out.p[slot][g] = (b.p[slot][g] & 1) - (prod + prod);
   }
 };
+
+// ---- fused comparison tail ----------------------------------------------------------
+// adder final (lane k) -> msb bit -> b2a ".m1" payload of chunk k, in the same kernel.
+struct B2aBuildFF {
+  EwTriple T;
+  Ptr2 own, bits;
+  u64 lo, w;
+  __device__ void operator()(int slot, int party, u64 g, u64 j, u64 sum) const {
+    const u64 bit = sum >> 63;
+    bits.p[slot][g] = bit;
+    u64 a, b;
+    ew_ab(T, party, T.off + g, a, b);
+    own.p[slot][j] = (party == 0 ? bit : 0) - a;      // eps = acc - a
+    own.p[slot][w + j] = (party == 1 ? bit : 0) - b;  // delta = bq - b
+  }
+};
+// b2a combine (c = bit - 2*prod) -> payload of the multiply by c, chunk k, same kernel.
+template <class UF>
+struct MulByBitBuild {
+  EwTriple T;
+  Ptr2 own;
+  CPtr2 bits;
+  u64 lo, w;
+  UF uf;
+  __device__ void operator()(int slot, int party, u64 g, u64 prod) const {
+    const u64 c = (bits.p[slot][g] & 1) - (prod + prod);
+    const u64 j = g - lo;
+    u64 a, b;
+    ew_ab(T, party, T.off + g, a, b);
+    own.p[slot][j] = uf(slot, g) - a;
+    own.p[slot][w + j] = c - b;
+  }
+};
+
+// z = u * b2a(msb(d)) with every round one kernel: the 2PC compare-and-select behind ReLU
+// (H/nonlinear/activations.hpp:39-47) and the tournament pick (activations.hpp:62-70).
+// Tags and collective order are the reference's; chunk lanes must align (they do for every
+// caller in the reference: adder, b2a and the multiply all use chunks_for(numel)).
+template <class DF, class UF, class PF>
+void compare_mul(Session& s, size_t n, const AdderOptions& opt, const std::string& tag_msb,
+                 const std::string& tag_b2a, int chunks_b2a, const std::string& tag_mul, int chunks_mul, DF df,
+                 UF uf, PF pf) {
+  const int ch = clamp_chunks(opt.chunks, n);
+  if (clamp_chunks(chunks_b2a, n) != ch || clamp_chunks(chunks_mul, n) != ch)
+    throw Error(kUsageError, "compare_mul: misaligned chunk lanes");
+  const Pid2 pid = pids(s);
+  DT bits = s.alloc(Shape{n});
+  std::vector<Open> ob(static_cast<size_t>(ch)), og(static_cast<size_t>(ch));
+  for (int k = 0; k < ch; ++k) {
+    const auto r = chunk_range(n, ch, k);
+    ob[k] = s.begin_open(2 * (r.second - r.first), Reduce::Sum);
+    og[k] = s.begin_open(2 * (r.second - r.first), Reduce::Sum);
+  }
+  auto ctag = [&](const std::string& t, int k) { return ch == 1 ? t : t + ".chunk" + std::to_string(k); };
+  Triple t1, t2;
+  bool fetched = false;
+  auto fetch_tail = [&] {  // after the adder's fetches, in reference order
+    if (fetched) return;
+    t1 = s.fetch(TripleSpec::elementwise(TripleKind::Arith, Shape{n}), tag_b2a + ".m1");
+    t1.mark_consumed();
+    t2 = s.fetch(TripleSpec::elementwise(TripleKind::Arith, Shape{n}), tag_mul);
+    t2.mark_consumed();
+    fetched = true;
+  };
+  a2b_op(
+      s, n, opt, tag_msb, df,
+      [&](int lane, size_t lo, size_t w) {
+        fetch_tail();
+        return B2aBuildFF{t1.ew, own_ptrs(ob[lane]), ptrs(bits), lo, w};
+      },
+      [&](int lane) { s.post(ob[lane], ctag(tag_b2a + ".m1", lane)); });
+  for (int k = 0; k < ch; ++k) {
+    const auto r = chunk_range(n, ch, k);
+    const size_t lo = r.first, w = r.second - r.first;
+    s.wait(ob[k]);
+    MulByBitBuild<UF> gb{t2.ew, own_ptrs(og[k]), cptrs(bits), lo, w, uf};
+    launch_ew(s.stream, s.n_local, w,
+              MulCombine<MulByBitBuild<UF>>{t1.ew, pid, as_const(own_ptrs(ob[k])), peer_ptrs(ob[k]), lo, w, gb});
+    s.post(og[k], ctag(tag_mul, k));
+  }
+  for (int k = 0; k < ch; ++k) {
+    const auto r = chunk_range(n, ch, k);
+    s.wait(og[k]);
+    launch_ew(s.stream, s.n_local, r.second - r.first,
+              MulCombine<PF>{t2.ew, pid, as_const(own_ptrs(og[k])), peer_ptrs(og[k]), r.first, r.second - r.first, pf});
+  }
+  s.check();
+}
 }  // namespace
 
 DT a2b(Session& s, const DT& x, const AdderOptions& opt, const std::string& tag) {
   DT z = s.alloc(x.shape, x.scale);
-  a2b_op(s, x.numel(), opt, tag, SrcMem{cptrs(x)}, SumSink{ptrs(z)});
+  a2b_op(s, x.numel(), opt, tag, SrcMem{cptrs(x)}, same(SumSink{ptrs(z)}));
   return z;
 }
 
 DT msb(Session& s, const DT& x, const AdderOptions& opt, const std::string& tag) {
   DT z = s.alloc(x.shape, x.scale);
-  a2b_op(s, x.numel(), opt, tag, SrcMem{cptrs(x)}, MsbSink{ptrs(z)});
+  a2b_op(s, x.numel(), opt, tag, SrcMem{cptrs(x)}, same(MsbSink{ptrs(z)}));
   return z;
 }
 
@@ -309,8 +398,7 @@ DT b2a_bit(Session& s, const DT& b, const std::string& tag, int chunks) {
 DT less_than(Session& s, const DT& x, const DT& y, const AdderOptions& opt, const std::string& tag) {
   require_same_shape(x, y, "less_than");
   DT m = s.alloc(x.shape, 0);
-  a2b_op(s, x.numel(), opt, tag + ".msb", SrcSub{cptrs(x), cptrs(y)},
-         MsbSink{ptrs(m)});
+  a2b_op(s, x.numel(), opt, tag + ".msb", SrcSub{cptrs(x), cptrs(y)}, same(MsbSink{ptrs(m)}));
   return b2a_bit(s, m, tag + ".b2a", opt.chunks);
 }
 
@@ -324,40 +412,35 @@ struct SinkXMinus {  // out = x - z  (relu gate, H/nonlinear/activations.hpp:46)
 }  // namespace
 
 DT relu_shares(Session& s, const DT& x, const std::string& tag) {
+  // x - x*b2a(msb(x)): tags "<l>.msb.add1.*", "<l>.b2a.m1", "<l>.gate" (activations.hpp:39-47)
   const size_t n = x.numel();
   const int ch = chunks_for(s, n);
-  DT bits = s.alloc(x.shape, 0);
-  a2b_op(s, n, adder_for(s, n), tag + ".msb", SrcMem{cptrs(x)}, MsbSink{ptrs(bits)});
-  DT c = b2a_bit(s, bits, tag + ".b2a", ch);
-  Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Arith, x.shape), tag + ".gate");
-  t.mark_consumed();
   DT out = s.alloc(x.shape, x.scale);
-  mul_op(s, t.ew, n, ch, tag + ".gate", SrcMem{cptrs(x)}, SrcMem{cptrs(c)}, SinkXMinus{cptrs(x), ptrs(out)});
+  compare_mul(s, n, adder_for(s, n), tag + ".msb", tag + ".b2a", ch, tag + ".gate", ch, SrcMem{cptrs(x)},
+              SrcMem{cptrs(x)}, SinkXMinus{cptrs(x), ptrs(out)});
   return out;
 }
 
 namespace {
-// cur [outer, len] -> a = cur[:, :h], b = cur[:, h:2h]  (H/nonlinear/activations.hpp:20-33,62-63)
-void take_halves(Session& s, const DT& cur, size_t outer, size_t len, size_t h, DT& a, DT& b) {
-  a = s.alloc(Shape{outer, h}, cur.scale);
-  b = s.alloc(Shape{outer, h}, cur.scale);
-  const CPtr2 cp = cptrs(cur);
-  const Ptr2 ap = ptrs(a), bp = ptrs(b);
-  const u32 H = u32(h), LEN = u32(len);
-  launch_ew(s.stream, s.n_local, outer * h, [=] __device__(int slot, u64 i) {
-    const u32 o = u32(i) / H, j = u32(i) - o * H;
-    const u64 src = u64(o) * LEN + j;
-    ap.p[slot][i] = cp.p[slot][src];
-    bp.p[slot][i] = cp.p[slot][src + H];
-  });
-}
-struct SinkPick {  // m = a + step, written into the next [outer, h(+1)] row layout
-  CPtr2 a;
+// Tournament halves of cur [outer, len]: a = cur[:, :h], b = cur[:, h:2h] read in place
+// (H/nonlinear/activations.hpp:20-33,62-63). sign > 0 gives a - b, else b - a.
+struct SrcHalfDiff {
+  CPtr2 cur;
+  u32 h, len;
+  int sign;
+  __device__ u64 operator()(int slot, u64 g) const {
+    const u32 o = u32(g) / h, j = u32(g) - o * h;
+    const u64* row = cur.p[slot] + u64(o) * len;
+    return sign > 0 ? row[j] - row[h + j] : row[h + j] - row[j];
+  }
+};
+struct SinkPick {  // m = a + step, written into the next [outer, nw] row layout
+  CPtr2 cur;
   Ptr2 next;
-  u32 h, nw;
+  u32 h, len, nw;
   __device__ void operator()(int slot, int, u64 g, u64 z) const {
     const u32 o = u32(g) / h, j = u32(g) - o * h;
-    next.p[slot][u64(o) * nw + j] = a.p[slot][g] + z;
+    next.p[slot][u64(o) * nw + j] = cur.p[slot][u64(o) * len + j] + z;
   }
 };
 }  // namespace
@@ -371,12 +454,9 @@ DT max_last_dim(Session& s, const DT& x, size_t L, const std::string& tag) {
   while (len > 1) {
     const size_t h = len / 2;
     const bool odd = len & 1;
-    DT a, b;
-    take_halves(s, cur, outer, len, h, a, b);
     const std::string rt = tag + ".r" + std::to_string(round++);
     const size_t n = outer * h;
-    AdderOptions opt = adder_for(s, n);
-    DT gate = less_than(s, a, b, opt, rt);
+    const AdderOptions opt = adder_for(s, n);
     const size_t nw = odd ? h + 1 : h;
     DT next = s.alloc(Shape{outer, nw}, cur.scale);
     if (odd) {  // carry the odd tail (H/nonlinear/activations.hpp:71-82)
@@ -387,10 +467,11 @@ DT max_last_dim(Session& s, const DT& x, size_t L, const std::string& tag) {
         np.p[slot][o * NW + HH] = cp.p[slot][o * LEN + LEN - 1];
       });
     }
-    Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Arith, Shape{outer, h}), rt + ".pick");
-    t.mark_consumed();
-    mul_op(s, t.ew, n, chunks_for(s, n), rt + ".pick", SrcSub{cptrs(b), cptrs(a)}, SrcMem{cptrs(gate)},
-           SinkPick{cptrs(a), ptrs(next), u32(h), u32(nw)});
+    // gate = less_than(a, b) (tags rt.msb.add1.*, rt.b2a.m1); pick = (b - a) * gate (rt.pick)
+    const CPtr2 cp = cptrs(cur);
+    compare_mul(s, n, opt, rt + ".msb", rt + ".b2a", opt.chunks, rt + ".pick", chunks_for(s, n),
+                SrcHalfDiff{cp, u32(h), u32(len), +1}, SrcHalfDiff{cp, u32(h), u32(len), -1},
+                SinkPick{cp, ptrs(next), u32(h), u32(len), u32(nw)});
     cur = next;
     len = nw;
   }
