@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-blocking", action="store_true", help="skip the blocking comparison pass")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--probe", default="adder_round", choices=["adder_round", "gemm"])
+    ap.add_argument("--threshold", default="auto",
+                    help="inner-pipeline chunk threshold: auto (calibrate_threshold on this link, like the "
+                         "reference CLI's --threshold auto), ref (the reference default 2 MiB) or bytes")
     return ap.parse_args()
 
 
@@ -168,9 +171,24 @@ def main():
     weights = mp.init_weights(g, seed + 11)
     x_global = mp.demo_input(g_global, seed + 12)
 
+    NEVER = (1 << 63)
+    calib = None
+    if a.threshold == "auto":
+        if world == 1:
+            from paper_2209_13643_b200 import tuning
+            calib = tuning.sweep_threshold("relu", chunks=4)
+            thr = calib["threshold_bytes"] or NEVER
+        else:
+            thr = 2 << 20  # NCCL link: keep the reference default (calibrating needs both ranks)
+    elif a.threshold == "ref":
+        thr = 2 << 20
+    else:
+        thr = int(a.threshold)
+
     def setup(mode):
         s = make_session()
-        ex = mp.SecureExecutor(s, g, public_weights=a.weights == "public", pipelined=mode == "pipelined")
+        ex = mp.SecureExecutor(s, g, public_weights=a.weights == "public", pipelined=mode == "pipelined",
+                               chunk_threshold=thr)
         ex.deal_weights(weights, seed)
         x = s.deal_input(x_global, seed + 1, batch_offset=B * pair, local_batch=B)
         return s, ex, x
@@ -317,7 +335,10 @@ def main():
         "data": "synthetic: the reference's seeded init_weights(seed 12) / demo_input(seed 13), shares dealt on host",
         "config": {"workload": f"{g.name} b{B} 2PC {a.weights} {a.mode}", "model": g.name, "global_batch": B * pairs,
                    "pairs": pairs, "parties_per_gpu": 2 if world == 1 else 1, "mode": a.mode, "weights": a.weights,
-                   "frac_bits": g.frac_bits, "chunks": 4, "chunk_threshold_bytes": 2 << 20,
+                   "frac_bits": g.frac_bits, "chunks": 4,
+                   "chunk_threshold_bytes": None if thr == NEVER else thr,
+                   "chunk_threshold_source": a.threshold,
+                   "calibration": calib,
                    "l2": "flushed between timed steps (256 MiB memset, untimed)",
                    "transport": "in-device zero-copy opens" if world == 1 else "NCCL send/recv over NVLink",
                    "kernels_per_step": launches / a.steps,

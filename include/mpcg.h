@@ -71,6 +71,9 @@ int mpcg_session_set_shard(mpcg_session* s, uint64_t local_batch, uint64_t globa
 int mpcg_nccl_unique_id(uint8_t out[128]);
 int mpcg_session_connect_nccl(mpcg_session* s, const uint8_t id[128], int rank);
 int mpcg_session_sync(mpcg_session* s);
+/* 1-GPU mode: run multi-round chains (ReLU, tournament rounds) as one persistent cooperative
+ * kernel (1, default) or one kernel per exchange round (0). Values are identical. */
+int mpcg_session_set_persistent(mpcg_session* s, int enable);
 /* CommStats of one local slot (transport/transport.hpp:39-45): bytes, collectives, p2p. */
 int mpcg_session_stats(mpcg_session* s, int slot, uint64_t out[3]);
 int mpcg_session_n_local(mpcg_session* s, int* out);

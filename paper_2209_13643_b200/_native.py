@@ -52,6 +52,7 @@ SIGNATURES = {
     "mpcg_nccl_unique_id": [C.c_char_p],
     "mpcg_session_connect_nccl": [P, C.c_char_p, I32],
     "mpcg_session_sync": [P],
+    "mpcg_session_set_persistent": [P, I32],
     "mpcg_session_stats": [P, I32, U64P],
     "mpcg_session_n_local": [P, C.POINTER(I32)],
     "mpcg_session_trace": [P, I32],

@@ -73,6 +73,10 @@ class Session:
     def sync(self):
         N.call("mpcg_session_sync", self._h)
 
+    def set_persistent(self, enable=True):
+        """1-GPU mode: one persistent kernel per compare chain (default) or one per round."""
+        N.call("mpcg_session_set_persistent", self._h, int(enable))
+
     def stats(self, slot=0):
         out = (C.c_uint64 * 3)()
         N.call("mpcg_session_stats", self._h, slot, out)

@@ -143,6 +143,10 @@ int mpcg_session_connect_nccl(mpcg_session* s, const uint8_t id[128], int rank) 
   return guard([&] { nccl_connect(S(s), id, rank); });
 }
 
+int mpcg_session_set_persistent(mpcg_session* s, int enable) {
+  return guard([&] { S(s).no_persistent = enable == 0; });
+}
+
 int mpcg_session_sync(mpcg_session* s) {
   return guard([&] { S(s).sync(); });
 }

@@ -187,7 +187,7 @@ constexpr int kSms = 148;
 
 // Instrumentation: count of kernels this library launched, and an optional probe that
 // brackets every launch of one kernel class with CUDA events (bench.py's live roofline).
-enum KernelClass : int { kClsOther = 0, kClsAdderRound = 1, kClsGemm = 2, kClsBeaver = 3 };
+enum KernelClass : int { kClsOther = 0, kClsAdderRound = 1, kClsGemm = 2, kClsBeaver = 3, kClsChain = 4 };
 struct Probe {
   int cls = -1;             // class being timed, -1 = off
   double bytes = 0;         // algorithmic bytes of the probed launches

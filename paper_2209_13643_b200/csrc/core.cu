@@ -179,6 +179,8 @@ Session::Session(int dev, int nl, int party, u64 sd, u64 mask_seed, int frac_bit
   MPCG_CUDA(cudaMemset(link_state_, 0, 64));
   const char* dbg = std::getenv("MPCG_DEBUG_SYNC");
   debug_sync = dbg && dbg[0] == '1';
+  const char* per = std::getenv("MPCG_PERSISTENT");
+  no_persistent = per && per[0] == '0';
 }
 
 Session::~Session() {
@@ -450,18 +452,27 @@ void Session::throttle(Open& o) {
   MPCG_CUDA(cudaGetLastError());
 }
 
-void Session::post(Open& o, const std::string& tag, bool p2p) {
-  if (o.posted) throw Error(kUsageError, "open posted twice");
-  o.posted = true;
-  o.seq = next_seq++;  // collective order = post order (what both parties must agree on)
+u32 Session::account(size_t nwords, Reduce kind, const std::string& tag, bool p2p) {
+  const u32 seq = next_seq++;  // collective order = post order (what both parties must agree on)
   for (int i = 0; i < n_local; ++i) {
-    stats[i].bytes_sent += o.n * 8;
+    stats[i].bytes_sent += nwords * 8;
     if (p2p)
       stats[i].p2p_sends++;
     else
       stats[i].collectives++;
   }
-  if (trace_on) trace.push_back(TraceEvent{o.seq, o.kind, tag, o.n * 8});
+  if (trace_on) trace.push_back(TraceEvent{seq, kind, tag, nwords * 8});
+  return seq;
+}
+
+bool Session::persistent_ok() const {
+  return n_local == 2 && cfg.link_bandwidth <= 0 && !no_persistent;
+}
+
+void Session::post(Open& o, const std::string& tag, bool p2p) {
+  if (o.posted) throw Error(kUsageError, "open posted twice");
+  o.posted = true;
+  o.seq = account(o.n, o.kind, tag, p2p);
   const bool throttled = cfg.link_bandwidth > 0;
   if (n_local == 2 && !throttled) {
     check();

@@ -210,6 +210,12 @@ class Session {
                   std::shared_ptr<Block> in = nullptr);
   void post(Open& o, const std::string& tag, bool p2p = false);
   void wait(Open& o);
+  // Collective bookkeeping only (stats, trace, order) for opens that a persistent kernel
+  // performs in-device; returns the sequence number.
+  u32 account(size_t nwords, Reduce kind, const std::string& tag, bool p2p = false);
+  // 1-GPU mode without an emulated link: chains of rounds may run as one persistent kernel.
+  bool persistent_ok() const;
+  bool no_persistent = false;  // MPCG_PERSISTENT=0 forces one kernel per round
   u32 next_seq = 0;
   CommStats stats[2];
   std::vector<TraceEvent> trace;

@@ -351,6 +351,53 @@ void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& 
   s.check();
 }
 
+// ---------------------------------------------------------------- persistent round chain
+// In 1-GPU mode an open is only an ordering point between the two party slots, so a whole
+// chain of secure rounds can run as ONE cooperative kernel: each round is a grid-stride
+// pass over the elements, and a grid-wide barrier (release/acquire at gpu scope) takes the
+// place of the kernel boundary. Round logic is the same functors as the multi-kernel path.
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    unsigned v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (v >= target) break;
+      __nanosleep(20);
+    }
+  }
+  __syncthreads();
+}
+
+template <class MR, class AR, class BR, class CR>
+struct ChainParams {
+  MR mask;       // a2b mask + p2p payload
+  AR adder[8];   // round 0 issue, 6 x (settle, issue), final (+ b2a build)
+  int nadder;
+  BR b2a;        // b2a combine + select build
+  CR fin;        // select combine -> output sink
+  u64 n;
+  unsigned* bar;
+};
+
+template <class MR, class AR, class BR, class CR>
+__global__ void __launch_bounds__(256) chain_kernel(const __grid_constant__ ChainParams<MR, AR, BR, CR> p) {
+  const int slot = blockIdx.y;
+  const unsigned nb = gridDim.x * gridDim.y;
+  const u64 t0 = blockIdx.x * u64(blockDim.x) + threadIdx.x, st = u64(gridDim.x) * blockDim.x;
+  unsigned ep = 0;
+  for (u64 g = t0; g < p.n; g += st) p.mask(slot, g);
+  grid_barrier(p.bar, ++ep * nb);
+  for (int r = 0; r < p.nadder; ++r) {
+    for (u64 g = t0; g < p.n; g += st) p.adder[r](slot, g);
+    grid_barrier(p.bar, ++ep * nb);
+  }
+  for (u64 g = t0; g < p.n; g += st) p.b2a(slot, g);
+  grid_barrier(p.bar, ++ep * nb);
+  for (u64 g = t0; g < p.n; g += st) p.fin(slot, g);
+}
+
 // Plain final sinks for adder_op (same functor for every lane).
 struct SumSink {  // binary share of the sum
   Ptr2 out;

@@ -321,6 +321,141 @@ struct MulByBitBuild {
 // (H/nonlinear/activations.hpp:39-47) and the tournament pick (activations.hpp:62-70).
 // Tags and collective order are the reference's; chunk lanes must align (they do for every
 // caller in the reference: adder, b2a and the multiply all use chunks_for(numel)).
+// a2b mask round as a functor (persistent chain form of a2b_mask).
+template <class XF>
+struct MaskRound {
+  u64 k0, k1;
+  Session::MaskRef mr;
+  Ptr2 own, keep;
+  XF xf;
+  __device__ void operator()(int slot, u64 i) const {
+    const u64 r = drw(slot == 0 ? k0 : k1, tkey(mr.base, mr.bp) + 1 + i);
+    own.p[slot][i] = r;
+    keep.p[slot][i] = xf(slot, i) ^ r;
+  }
+};
+
+// One persistent cooperative kernel for the whole compare-and-select chain (1-GPU mode):
+// 10 exchanges become 10 grid barriers. Values, tags and collective accounting are those
+// of the per-round path (chunk lanes only change where an open may start; with in-device
+// opens there is nothing to overlap, so the lanes are accounted but not split).
+template <class DF, class UF, class PF>
+void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const std::string& tag_msb,
+                            const std::string& tag_b2a, const std::string& tag_mul, DF df, UF uf, PF pf) {
+  const int ch = clamp_chunks(opt.chunks, n);
+  const Pid2 pid = pids(s);
+  const SpkConsts c = make_spk_constants(opt.width);
+  const std::string at = tag_msb + ".add1";
+  // dealer fetches in reference order: adder .g, .l0..l5, then b2a .m1, then the select
+  Triple tr[7];
+  for (int r = 0; r < 7; ++r) {
+    tr[r] = r == 0 ? s.fetch(TripleSpec::elementwise(TripleKind::Bin, Shape{n}), at + ".g")
+                   : s.fetch(TripleSpec::elementwise(TripleKind::Bin, Shape{2, n}), at + ".l" + std::to_string(r - 1),
+                             /*stacked=*/true);
+    tr[r].mark_consumed();
+  }
+  Triple t1 = s.fetch(TripleSpec::elementwise(TripleKind::Arith, Shape{n}), tag_b2a + ".m1");
+  t1.mark_consumed();
+  Triple t2 = s.fetch(TripleSpec::elementwise(TripleKind::Arith, Shape{n}), tag_mul);
+  t2.mark_consumed();
+  const Session::MaskRef mr = s.take_mask(n);
+  DT keep = s.alloc(Shape{n}), S = s.alloc(Shape{n}), P = s.alloc(Shape{n}), P0 = s.alloc(Shape{n}),
+     bits = s.alloc(Shape{n});
+  Open om = s.begin_open(n, Reduce::Sum);
+  Open oa[7];
+  for (int r = 0; r < 7; ++r) oa[r] = s.begin_open((r == 0 ? 2 : 4) * n, Reduce::Xor);
+  Open ob = s.begin_open(2 * n, Reduce::Sum), og = s.begin_open(2 * n, Reduce::Sum);
+
+  using XF = PartX;
+  using AR = AdderRound<PartX, PartY, B2aBuildFF>;
+  using BR = MulCombine<MulByBitBuild<UF>>;
+  using CR = MulCombine<PF>;
+  ChainParams<MaskRound<DF>, AR, BR, CR> p{};
+  p.mask = MaskRound<DF>{s.mask_key[0], s.mask_key[1], mr, own_ptrs(om), ptrs(keep), df};
+  const XF xf{pid, cptrs(keep), peer_ptrs(om)};
+  const PartY yf{pid, cptrs(keep), peer_ptrs(om)};
+  for (int r = 0; r <= 7; ++r) {
+    AR& k = p.adder[r];
+    k.rp = r - 1;
+    k.rn = r;
+    k.levels = c.levels;
+    if (r >= 1) k.Tp = tr[r - 1].ew;
+    if (r <= 6) k.Tn = tr[r].ew;
+    if (r >= 2) k.lp = c.lv[r - 2];
+    if (r >= 1 && r <= 6) k.ln = c.lv[r - 1];
+    k.pid = pid;
+    if (r >= 1) {
+      k.ownp = as_const(own_ptrs(oa[r - 1]));
+      k.peerp = peer_ptrs(oa[r - 1]);
+    }
+    if (r <= 6) k.ownn = own_ptrs(oa[r]);
+    k.S = ptrs(S);
+    k.P = ptrs(P);
+    k.P0 = ptrs(P0);
+    k.lo = 0;
+    k.w = n;
+    k.wmask = c.wmask;
+    k.xf = xf;
+    k.yf = yf;
+    if (r == 7) k.ff = B2aBuildFF{t1.ew, own_ptrs(ob), ptrs(bits), 0, n};
+  }
+  p.nadder = 8;
+  p.b2a = BR{t1.ew, pid, as_const(own_ptrs(ob)), peer_ptrs(ob), 0, n,
+             MulByBitBuild<UF>{t2.ew, own_ptrs(og), cptrs(bits), 0, n, uf}};
+  p.fin = CR{t2.ew, pid, as_const(own_ptrs(og)), peer_ptrs(og), 0, n, pf};
+  DT bar = s.alloc(Shape{1});
+  MPCG_CUDA(cudaMemsetAsync(bar.s[0], 0, 8, s.stream));
+  p.n = n;
+  p.bar = reinterpret_cast<unsigned*>(bar.s[0]);
+
+  auto kern = chain_kernel<MaskRound<DF>, AR, BR, CR>;
+  static int per_sm = -1;  // resident 256-thread CTAs per SM for this instantiation
+  if (per_sm < 0) {
+    MPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    if (per_sm < 1) throw Error(kInternalError, "chain kernel cannot be resident");
+  }
+  const u64 cap = u64(per_sm) * kSms / u64(s.n_local);
+  u64 blocks = (n + 1023) / 1024;  // ~4 elements per thread per round
+  blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(unsigned(blocks), unsigned(s.n_local));
+  lc.blockDim = dim3(256);
+  lc.stream = s.stream;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barrier)
+  attr.val.cooperative = 1;
+  lc.attrs = &attr;
+  lc.numAttrs = 1;
+  {
+    // ReLU / compared pair = 2 x 248 B wire + 8 x (in + out) ~ 512 B/elem/party
+    ClassScope cs(kClsChain, 512.0 * double(n) * s.n_local);
+    cudaEvent_t pe;
+    probe_begin(s.stream, &pe);
+    MPCG_CUDA(cudaLaunchKernelEx(&lc, kern, p));
+    probe_end(s.stream, pe);
+  }
+  // bookkeeping in the reference's collective order (H/protocols/compare.hpp:37-52,
+  // adder.hpp:312-322, beaver.hpp:63-71)
+  auto ctag = [&](const std::string& t, int k) { return ch == 1 ? t : t + ".chunk" + std::to_string(k); };
+  s.account(n, Reduce::Sum, "", /*p2p=*/true);
+  for (int r = 0; r < 7; ++r)
+    for (int k = 0; k < ch; ++k) {
+      const auto rg = chunk_range(n, ch, k);
+      const std::string t = r == 0 ? at + ".g" : at + ".l" + std::to_string(r - 1);
+      s.account((r == 0 ? 2 : 4) * (rg.second - rg.first), Reduce::Xor,
+                ch > 1 && !opt.merged ? t + ".chunk" + std::to_string(k) : t);
+    }
+  for (int k = 0; k < ch; ++k) {
+    const auto rg = chunk_range(n, ch, k);
+    s.account(2 * (rg.second - rg.first), Reduce::Sum, ctag(tag_b2a + ".m1", k));
+  }
+  for (int k = 0; k < ch; ++k) {
+    const auto rg = chunk_range(n, ch, k);
+    s.account(2 * (rg.second - rg.first), Reduce::Sum, ctag(tag_mul, k));
+  }
+  s.check();
+}
+
 template <class DF, class UF, class PF>
 void compare_mul(Session& s, size_t n, const AdderOptions& opt, const std::string& tag_msb,
                  const std::string& tag_b2a, int chunks_b2a, const std::string& tag_mul, int chunks_mul, DF df,
@@ -328,6 +463,10 @@ void compare_mul(Session& s, size_t n, const AdderOptions& opt, const std::strin
   const int ch = clamp_chunks(opt.chunks, n);
   if (clamp_chunks(chunks_b2a, n) != ch || clamp_chunks(chunks_mul, n) != ch)
     throw Error(kUsageError, "compare_mul: misaligned chunk lanes");
+  if (s.persistent_ok() && n > 0) {
+    compare_mul_persistent(s, n, opt, tag_msb, tag_b2a, tag_mul, df, uf, pf);
+    return;
+  }
   const Pid2 pid = pids(s);
   DT bits = s.alloc(Shape{n});
   std::vector<Open> ob(static_cast<size_t>(ch)), og(static_cast<size_t>(ch));

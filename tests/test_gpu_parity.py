@@ -24,9 +24,10 @@ def mp():
     return mp
 
 
-def _sess(mp, seed, f, mask_seed, chunks=1, threshold=0):
+def _sess(mp, seed, f, mask_seed, chunks=1, threshold=0, persistent=True):
     s = mp.Session(device=0, n_local=2, seed=seed, mask_seed=mask_seed, frac_bits=f)
     s.set_pipeline(chunks, threshold, True)
+    s.set_persistent(persistent)
     return s
 
 
@@ -59,10 +60,11 @@ GOLDEN_OPS = [
 ]
 
 
+@pytest.mark.parametrize("persistent", [True, False], ids=["persistent", "per-round"])
 @pytest.mark.parametrize("name,seed,f,chunks,fn", GOLDEN_OPS, ids=[o[0] for o in GOLDEN_OPS])
-def test_op_matches_reference_shares(mp, golden_ops, name, seed, f, chunks, fn):
+def test_op_matches_reference_shares(mp, golden_ops, name, seed, f, chunks, fn, persistent):
     G = golden_ops
-    s = _sess(mp, seed + 1, f, seed + 2, chunks)
+    s = _sess(mp, seed + 1, f, seed + 2, chunks, persistent=persistent)
     X = s.tensor(np.stack([G[name + "/x0"], G[name + "/x1"]]), f)
     Y = s.tensor(np.stack([G[name + "/y0"], G[name + "/y1"]]), f)
     Z = fn(mp, s, X, Y).numpy()
@@ -76,8 +78,9 @@ def test_op_matches_reference_shares(mp, golden_ops, name, seed, f, chunks, fn):
 MODEL_FIXTURES = sorted(glob.glob(os.path.join(ROOT, "tests", "golden", "model_*.npz")))
 
 
-def _run_model(mp, g, mode, weights, iters, seed=1):
+def _run_model(mp, g, mode, weights, iters, seed=1, persistent=True):
     s = mp.Session(device=0, n_local=2, seed=seed, mask_seed=seed ^ PHI, frac_bits=g.frac_bits)
+    s.set_persistent(persistent)
     ex = mp.SecureExecutor(s, g, public_weights=weights == "public", pipelined=mode == "pipelined")
     ex.deal_weights(mp.init_weights(g, seed + 11), seed)
     x = s.deal_input(mp.demo_input(g, seed + 12), seed + 1)
@@ -87,12 +90,13 @@ def _run_model(mp, g, mode, weights, iters, seed=1):
     return s, out.numpy()
 
 
+@pytest.mark.parametrize("persistent", [True, False], ids=["persistent", "per-round"])
 @pytest.mark.parametrize("path", MODEL_FIXTURES, ids=[os.path.basename(p)[6:-4] for p in MODEL_FIXTURES])
-def test_model_logit_shares_match_reference(mp, path):
+def test_model_logit_shares_match_reference(mp, path, persistent):
     name, mode, weights, it = os.path.basename(path)[6:-4].rsplit("_", 3)
     m = np.load(path)
     g = mp.ModelGraph.from_json(os.path.join(ROOT, "configs", name + ".json"))
-    s, z = _run_model(mp, g, mode, weights, int(it[2:]))
+    s, z = _run_model(mp, g, mode, weights, int(it[2:]), persistent=persistent)
     assert np.array_equal(z[0].reshape(-1), m["z0"].reshape(-1))
     assert np.array_equal(z[1].reshape(-1), m["z1"].reshape(-1))
     opened = (z[0] + z[1]).reshape(-1)
@@ -134,6 +138,30 @@ def test_graph_replay_matches_reference(mp, name, mode, weights, it):
         zr = ex.replay()
     assert np.array_equal(zr.numpy(), ze.numpy())
     assert s.stats(0) == s2.stats(0)
+
+
+@pytest.mark.parametrize("name,pairs", [("lenet5", 2), ("toy_transformer", 2), ("lenet5", 4)])
+def test_dp_shards_match_full_batch(mp, name, pairs):
+    """Data-parallel pairs: each pair regenerates its slice of the full-batch
+    triples and masks, so the concatenated logits equal the single-pair full-batch run."""
+    mode = "pipelined" if name == "lenet5" else "blocking"
+    m = np.load(os.path.join(ROOT, "tests", "golden", f"model_{name}_{mode}_private_it1.npz"))
+    g = mp.ModelGraph.from_json(os.path.join(ROOT, "configs", name + ".json"))
+    B = g.input[0]
+    local = B // pairs
+    gl = g.with_batch(local)
+    xg = mp.demo_input(g, 13)
+    outs = []
+    for p in range(pairs):
+        s = mp.Session(device=0, n_local=2, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
+        s.set_shard(local, B, p * local)
+        ex = mp.SecureExecutor(s, gl, pipelined=mode == "pipelined")
+        ex.deal_weights(mp.init_weights(g, 12), 1)
+        x = s.deal_input(xg, 2, batch_offset=p * local, local_batch=local)
+        outs.append(ex.run(x).numpy())
+    z = np.concatenate(outs, axis=1)
+    assert np.array_equal(z[0].reshape(-1), m["z0"].reshape(-1))
+    assert np.array_equal(z[1].reshape(-1), m["z1"].reshape(-1))
 
 
 def test_blocking_and_pipelined_are_bit_identical(mp):
