@@ -228,8 +228,42 @@ inline void probe_end(cudaStream_t st, cudaEvent_t a) {
   g_probe.launches++;
 }
 
+// Programmatic dependent launch: every kernel lets the next one in the stream be scheduled
+// as soon as its own CTAs are all resident, and waits (griddepcontrol.wait) for the
+// previous grid's completion + memory flush before touching data. In a CUDA graph this
+// overlaps the ~µs launch latency of each dependent round kernel with its predecessor.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+inline bool& pdl_enabled() {
+  static bool on = [] {
+    const char* e = std::getenv("MPCG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// cudaLaunchKernelEx with the PDL attribute (when enabled).
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = &attr;
+  lc.numAttrs = pdl_enabled() ? 1 : 0;
+  MPCG_CUDA(cudaLaunchKernelEx(&lc, kern, std::forward<Args>(args)...));
+}
+
 template <class F>
 __global__ void __launch_bounds__(256) ew_kernel(u64 n, F f) {
+  pdl_enter();
   const int slot = blockIdx.y;
   for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
     f(slot, i);
@@ -248,8 +282,7 @@ void launch_ew(cudaStream_t stream, int nslots, u64 n, F f) {
   dim3 grid(ew_blocks(n), nslots);
   cudaEvent_t pe;
   probe_begin(stream, &pe);
-  ew_kernel<<<grid, 256, 0, stream>>>(n, f);
-  MPCG_CUDA(cudaGetLastError());
+  launch_pdl(ew_kernel<F>, grid, dim3(256), 0, stream, n, f);
   probe_end(stream, pe);
 }
 

@@ -180,7 +180,7 @@ Session::Session(int dev, int nl, int party, u64 sd, u64 mask_seed, int frac_bit
   const char* dbg = std::getenv("MPCG_DEBUG_SYNC");
   debug_sync = dbg && dbg[0] == '1';
   const char* per = std::getenv("MPCG_PERSISTENT");
-  no_persistent = per && per[0] == '0';
+  no_persistent = !(per && per[0] == '1');  // opt-in until it beats one kernel per round
 }
 
 Session::~Session() {

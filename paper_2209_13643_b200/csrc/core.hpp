@@ -215,7 +215,7 @@ class Session {
   u32 account(size_t nwords, Reduce kind, const std::string& tag, bool p2p = false);
   // 1-GPU mode without an emulated link: chains of rounds may run as one persistent kernel.
   bool persistent_ok() const;
-  bool no_persistent = false;  // MPCG_PERSISTENT=0 forces one kernel per round
+  bool no_persistent = true;  // MPCG_PERSISTENT=1 / set_persistent(1) selects the persistent chain
   u32 next_seq = 0;
   CommStats stats[2];
   std::vector<TraceEvent> trace;

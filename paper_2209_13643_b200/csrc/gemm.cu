@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(256) ring_gemm_simt(GemmArgs a) {
   static_assert(TX * TY == 256, "256 threads");
   __shared__ u64 As[BK][BM + 1];
   __shared__ u64 Bs[BK][BN + 1];
+  pdl_enter();
   // blockIdx.z = (split * nbatch + b) * nslots + slot
   const int slot = blockIdx.z % a.nslots;
   const u32 zb = blockIdx.z / a.nslots;
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(256) ring_gemm_simt(GemmArgs a) {
 }
 
 __global__ void __launch_bounds__(256) gemm_splitk_epilogue(GemmArgs a) {
+  pdl_enter();
   const u64 per = u64(a.nbatch) * a.M * a.N;
   for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < per * a.nslots; i += u64(gridDim.x) * blockDim.x) {
     const int slot = int(i / per);
@@ -136,12 +138,10 @@ void launch_simt(Session& s, GemmArgs a) {
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, a.nslots * a.nbatch * a.ksplit);
   cudaEvent_t pe;
   probe_begin(st, &pe);
-  ring_gemm_simt<BM, BN, TM, TN><<<grid, 256, 0, st>>>(a);
-  MPCG_CUDA(cudaGetLastError());
+  launch_pdl(ring_gemm_simt<BM, BN, TM, TN>, grid, dim3(256), 0, st, a);
   if (a.ksplit > 1) {
     const u64 n = u64(a.nbatch) * a.M * a.N * a.nslots;
-    gemm_splitk_epilogue<<<ew_blocks(n), 256, 0, st>>>(a);
-    MPCG_CUDA(cudaGetLastError());
+    launch_pdl(gemm_splitk_epilogue, dim3(ew_blocks(n)), dim3(256), 0, st, a);
   }
   probe_end(st, pe);
 }

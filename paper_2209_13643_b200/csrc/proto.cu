@@ -415,7 +415,7 @@ void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const
     if (per_sm < 1) throw Error(kInternalError, "chain kernel cannot be resident");
   }
   const u64 cap = u64(per_sm) * kSms / u64(s.n_local);
-  u64 blocks = (n + 1023) / 1024;  // ~4 elements per thread per round
+  u64 blocks = (n + 255) / 256;  // one element per thread per round (the rounds are PRG-latency bound)
   blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(unsigned(blocks), unsigned(s.n_local));

@@ -39,8 +39,12 @@ def _time_op(op, elems, chunks, link, seed, reps, device=0):
     return ms
 
 
-def sweep_threshold(op="relu", sizes=DEFAULT_SIZES, chunks=4, link=None, seed=7, reps=5, device=0):
-    """Blocking vs chunked per operand size (bench.hpp:175-193). link=(latency_s, bytes/s, msg_s)."""
+def sweep_threshold(op="relu", sizes=DEFAULT_SIZES, chunks=4, link=None, seed=7, reps=5, device=0,
+                    margin=0.05):
+    """Blocking vs chunked per operand size (bench.hpp:175-193). link=(latency_s, bytes/s, msg_s).
+
+    The reference compares deterministic simulated clocks with a strict `<`; measured device
+    times carry run-to-run noise, so chunking must win by `margin` (default 5%) to count."""
     if len(sizes) < 2:
         raise ValueError("insufficient sweep: need at least two operand sizes")
     if chunks < 2:
@@ -49,9 +53,10 @@ def sweep_threshold(op="relu", sizes=DEFAULT_SIZES, chunks=4, link=None, seed=7,
     for elems in sizes:
         b = _time_op(op, elems, 1, link, seed, reps, device)
         c = _time_op(op, elems, chunks, link, seed, reps, device)
+        wins = c < b * (1.0 - margin)
         points.append({"elems": elems, "bytes": elems * 8, "blocking_ms": b, "chunked_ms": c,
-                       "chunked_wins": c < b})
-        if c < b and thr is None:
+                       "chunked_wins": wins})
+        if wins and thr is None:
             thr = elems * 8
     return {"op": op, "chunks": chunks, "points": points, "threshold_bytes": thr}
 
