@@ -72,7 +72,8 @@ int mpcg_nccl_unique_id(uint8_t out[128]);
 int mpcg_session_connect_nccl(mpcg_session* s, const uint8_t id[128], int rank);
 int mpcg_session_sync(mpcg_session* s);
 /* 1-GPU mode: run multi-round chains (ReLU, tournament rounds) as one persistent cooperative
- * kernel (1, default) or one kernel per exchange round (0). Values are identical. */
+ * kernel (1), one kernel per exchange round (0), or auto by size (2, default). Values are
+ * identical in every mode. */
 int mpcg_session_set_persistent(mpcg_session* s, int enable);
 /* CommStats of one local slot (transport/transport.hpp:39-45): bytes, collectives, p2p. */
 int mpcg_session_stats(mpcg_session* s, int slot, uint64_t out[3]);
@@ -150,6 +151,10 @@ int mpcg_executor_replay(mpcg_executor* e, mpcg_tensor** out);
 int mpcg_executor_time_layers(mpcg_executor* e, int enable);
 int mpcg_executor_layer_times(mpcg_executor* e, int max, float* ms, int* count);
 int mpcg_executor_destroy(mpcg_executor* e);
+
+/* Ring-GEMM engine: 0 = SIMT only, 1 = tcgen05 int8-limb path for every shape within its
+ * exact-accumulation budget (K' <= 16384), 2 = auto (tcgen05 for large shapes; default). */
+int mpcg_set_gemm_mode(int mode);
 
 /* ---- measurement hooks (bench.py) ---- */
 /* Kernels launched by this library since load. */

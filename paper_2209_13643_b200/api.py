@@ -73,9 +73,10 @@ class Session:
     def sync(self):
         N.call("mpcg_session_sync", self._h)
 
-    def set_persistent(self, enable=True):
-        """1-GPU mode: one persistent kernel per compare chain (default) or one per round."""
-        N.call("mpcg_session_set_persistent", self._h, int(enable))
+    def set_persistent(self, mode=True):
+        """1-GPU mode: persistent compare chains (True/1), one kernel per round (False/0) or
+        auto by size (2, the session default)."""
+        N.call("mpcg_session_set_persistent", self._h, int(mode))
 
     def stats(self, slot=0):
         out = (C.c_uint64 * 3)()
@@ -223,6 +224,11 @@ def softmax_shares(s, x, L, tag="softmax"):
 
 def maxpool2d_shares(s, x, N_, C_, H, W, k, stride, tag="maxpool"):
     return _op("mpcg_maxpool2d", s, x.handle, N_, C_, H, W, k, stride, _tag(tag))
+
+
+def set_gemm_mode(mode: str = "auto"):
+    """Ring-GEMM engine: "simt", "tc" (tcgen05 int8 limbs wherever exact) or "auto"."""
+    N.call("mpcg_set_gemm_mode", {"simt": 0, "tc": 1, "auto": 2}[mode])
 
 
 def launch_count() -> int:

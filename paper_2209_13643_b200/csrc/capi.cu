@@ -11,6 +11,7 @@ using namespace mpcg;
 namespace mpcg {
 void nccl_unique_id(void* out128);
 void nccl_connect(Session& s, const void* id128, int rank);
+int& tc_gemm_mode();
 }  // namespace mpcg
 
 // Handles share ownership of the session so device memory is always released on a
@@ -144,7 +145,7 @@ int mpcg_session_connect_nccl(mpcg_session* s, const uint8_t id[128], int rank) 
 }
 
 int mpcg_session_set_persistent(mpcg_session* s, int enable) {
-  return guard([&] { S(s).no_persistent = enable == 0; });
+  return guard([&] { S(s).persistent_mode = enable; });
 }
 
 int mpcg_session_sync(mpcg_session* s) {
@@ -417,6 +418,13 @@ int mpcg_executor_layer_times(mpcg_executor* e, int max, float* ms, int* count) 
 
 int mpcg_executor_destroy(mpcg_executor* e) {
   return guard([&] { delete e; });
+}
+
+int mpcg_set_gemm_mode(int mode) {
+  return guard([&] {
+    if (mode < 0 || mode > 2) throw Error(kConfigError, "gemm mode must be 0, 1 or 2");
+    tc_gemm_mode() = mode;
+  });
 }
 
 uint64_t mpcg_launch_count(void) { return g_launches.load(); }

@@ -180,7 +180,7 @@ Session::Session(int dev, int nl, int party, u64 sd, u64 mask_seed, int frac_bit
   const char* dbg = std::getenv("MPCG_DEBUG_SYNC");
   debug_sync = dbg && dbg[0] == '1';
   const char* per = std::getenv("MPCG_PERSISTENT");
-  no_persistent = !(per && per[0] == '1');  // opt-in until it beats one kernel per round
+  if (per && (per[0] == '0' || per[0] == '1')) persistent_mode = per[0] - '0';
 }
 
 Session::~Session() {
@@ -465,8 +465,9 @@ u32 Session::account(size_t nwords, Reduce kind, const std::string& tag, bool p2
   return seq;
 }
 
-bool Session::persistent_ok() const {
-  return n_local == 2 && cfg.link_bandwidth <= 0 && !no_persistent;
+bool Session::persistent_ok(size_t n) const {
+  if (n_local != 2 || cfg.link_bandwidth > 0 || persistent_mode == 0) return false;
+  return persistent_mode == 1 || n <= kPersistentMaxElems;
 }
 
 void Session::post(Open& o, const std::string& tag, bool p2p) {

@@ -214,8 +214,11 @@ class Session {
   // performs in-device; returns the sequence number.
   u32 account(size_t nwords, Reduce kind, const std::string& tag, bool p2p = false);
   // 1-GPU mode without an emulated link: chains of rounds may run as one persistent kernel.
-  bool persistent_ok() const;
-  bool no_persistent = true;  // MPCG_PERSISTENT=1 / set_persistent(1) selects the persistent chain
+  // Auto (2): small chains are launch-latency bound and run persistent; large ones run one
+  // kernel per round at full occupancy. 0 = never, 1 = always (MPCG_PERSISTENT / set_persistent).
+  bool persistent_ok(size_t n) const;
+  int persistent_mode = 2;
+  static constexpr size_t kPersistentMaxElems = 32768;
   u32 next_seq = 0;
   CommStats stats[2];
   std::vector<TraceEvent> trace;

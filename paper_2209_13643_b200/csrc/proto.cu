@@ -463,7 +463,7 @@ void compare_mul(Session& s, size_t n, const AdderOptions& opt, const std::strin
   const int ch = clamp_chunks(opt.chunks, n);
   if (clamp_chunks(chunks_b2a, n) != ch || clamp_chunks(chunks_mul, n) != ch)
     throw Error(kUsageError, "compare_mul: misaligned chunk lanes");
-  if (s.persistent_ok() && n > 0) {
+  if (n > 0 && s.persistent_ok(n)) {
     compare_mul_persistent(s, n, opt, tag_msb, tag_b2a, tag_mul, df, uf, pf);
     return;
   }
