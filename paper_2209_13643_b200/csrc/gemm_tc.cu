@@ -22,7 +22,7 @@ namespace {
 
 constexpr int kTM = 128;        // tile rows (UMMA M)
 constexpr int kKB = 64;         // K elements (= bytes per limb row) per pipeline stage
-constexpr int kThreads = 128;   // 4 warps: producers, MMA issuer (thread 0), epilogue
+constexpr int kThreads = 512;   // 16 warps: producers (1 A unit each), MMA issuer (thread 0), epilogue
 constexpr u32 kMaxKPrime = 16384;
 
 __device__ __forceinline__ u32 smem_u32(const void* p) {
@@ -114,7 +114,9 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc_kernel(const __grid_
   constexpr u32 kBPlane = BN * kKB;        // bytes per B limb plane per stage
   constexpr u32 kStage = 8 * (kAPlane + kBPlane);
   constexpr u32 kCols = 8 * BN;            // TMEM columns: one s32 accumulator per diagonal
+  constexpr int kBUnits = BN * (kKB / 16);
   static_assert(kCols <= 512, "TMEM budget");
+  static_assert(kTM * (kKB / 16) == kThreads, "one A unit per thread per stage");
   extern __shared__ __align__(1024) char smem[];
   __shared__ u64 bar_empty[2];
   __shared__ u64 bar_done;
@@ -150,97 +152,106 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc_kernel(const __grid_
   constexpr u32 idesc = idesc_i8(kTM, BN);
   u32 phase[2] = {0, 0};
 
-  for (u32 st = 0; st < steps; ++st) {
-    const u32 stage = st & 1;
+  // this thread's units: A (row ra, k-chunk ka) always; B (row rb, k-chunk kb) if tid < kBUnits
+  const int ra = tid % kTM, ka = tid / kTM;
+  const bool hasB = tid < kBUnits;
+  const int rb = tid % BN, kbc = tid / BN;
+  u64 va[16], vb[16];
+  // Register prefetch of step `st`'s operands (issued while earlier MMAs run).
+  auto load_step = [&](u32 st) {
     const int sg = int(st / kb_per_seg);
     const u32 k0 = (st - u32(sg) * kb_per_seg) * kKB;
+    const u64* L = S.L[sg] + u64(b) * S.sL[sg];
+    const u64* R = S.R[sg] + u64(b) * S.sR[sg];
+    const u32 m = m0 + ra;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const u32 k = k0 + ka * 16 + i;
+      va[i] = (m < M && k < K) ? __ldg(L + u64(m) * K + k) : 0;
+    }
+    if (hasB) {
+      const u32 n = n0 + rb;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const u32 k = k0 + kbc * 16 + i;
+        u64 x = 0;
+        if (n < N && k < K) x = a.tb ? __ldg(R + u64(n) * K + k) : __ldg(R + u64(k) * N + n);
+        vb[i] = x;
+      }
+    }
+  };
+
+  if (steps > 0) load_step(0);
+  for (u32 st = 0; st < steps; ++st) {
+    const u32 stage = st & 1;
     char* sA = smem + stage * kStage;
     char* sB = sA + 8 * kAPlane;
     if (st >= 2) {  // the MMAs that read this stage two steps ago must be done
       mbar_wait(&bar_empty[stage], phase[stage]);
       phase[stage] ^= 1;
     }
-    const u64* L = S.L[sg] + u64(b) * S.sL[sg];
-    const u64* R = S.R[sg] + u64(b) * S.sR[sg];
-    // ---- A: 128 rows x 64 k -> 512 units of (row, 16-k chunk)
-    for (int u = tid; u < kTM * (kKB / 16); u += kThreads) {
-      const int r = u % kTM, kc = u / kTM;
-      u64 v[16];
-      const u32 m = m0 + r;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const u32 k = k0 + kc * 16 + i;
-        v[i] = (m < M && k < K) ? __ldg(L + u64(m) * K + k) : 0;
-      }
-      // core matrix (row group r/8, k chunk kc): offset (kc*(128/8) + r/8)*128 + (r%8)*16
-      transpose_store(v, sA, kAPlane, (kc * (kTM / 8) + r / 8) * 128 + (r % 8) * 16);
-    }
-    // ---- B: BN rows (n) x 64 k
-    for (int u = tid; u < BN * (kKB / 16); u += kThreads) {
-      const int r = u % BN, kc = u / BN;
-      u64 v[16];
-      const u32 n = n0 + r;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const u32 k = k0 + kc * 16 + i;
-        u64 x = 0;
-        if (n < N && k < K) x = a.tb ? __ldg(R + u64(n) * K + k) : __ldg(R + u64(k) * N + n);
-        v[i] = x;
-      }
-      transpose_store(v, sB, kBPlane, (kc * (BN / 8) + r / 8) * 128 + (r % 8) * 16);
-    }
+    // core matrix (row group r/8, k chunk kc) at (kc*(rows/8) + r/8)*128, row r%8 at +16*(r%8)
+    transpose_store(va, sA, kAPlane, (ka * (kTM / 8) + ra / 8) * 128 + (ra % 8) * 16);
+    if (hasB) transpose_store(vb, sB, kBPlane, (kbc * (BN / 8) + rb / 8) * 128 + (rb % 8) * 16);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> tensor core
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const u32 aBase = smem_u32(sA), bBase = smem_u32(sB);
 #pragma unroll
-      for (int j = 0; j < kKB / 32; ++j) {  // two MMA K-slabs of 32 bytes per stage
+      for (int j = 0; j < kKB / 32; ++j) {  // MMA K-slabs of 32 bytes per stage
 #pragma unroll
         for (int l = 0; l < 8; ++l) {
           const u64 ad = smem_desc(aBase + l * kAPlane + 2 * j * (kTM / 8) * 128, (kTM / 8) * 128, 128);
 #pragma unroll
           for (int mm = 0; mm + l < 8; ++mm) {
             const u64 bd = smem_desc(bBase + mm * kBPlane + 2 * j * (BN / 8) * 128, (BN / 8) * 128, 128);
-            const u32 acc = (st > 0 || j > 0 || l > 0) ? 1u : 0u;  // first MMA of diagonal initialises
+            const u32 acc = (st > 0 || j > 0 || l > 0) ? 1u : 0u;  // first MMA of a diagonal initialises
             mma_i8(tmem + u32(l + mm) * BN, ad, bd, idesc, acc);
           }
         }
       }
       mma_commit(&bar_empty[stage]);
     }
+    if (st + 1 < steps) load_step(st + 1);
   }
   if (tid == 0) mma_commit(&bar_done);
   mbar_wait(&bar_done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-  // ---- epilogue: warp w owns TMEM lanes (rows) 32w..32w+31; recombine the diagonals
-  const u32 row = u32(warp) * 32 + (tid & 31);
+  // ---- epilogue: warp w reads TMEM lanes 32*(w%4).. (its rows) and column group w/4;
+  // recombine the diagonals z = sum_d D_d << 8d (mod 2^64) and apply the Beaver epilogue.
+  constexpr int kCW = BN / 4;  // columns per warp
+  const int q = warp & 3, cg = warp >> 2;
+  const u32 row = u32(q) * 32 + (tid & 31);
   const u32 m = m0 + row;
-  const u32 lane_addr = tmem + ((u32(warp) * 32) << 16);
-#pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    u64 acc[16];
+  const u32 lane_addr = tmem + ((u32(q) * 32) << 16) + u32(cg * kCW);
+  u64 acc[kCW];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) acc[c] = 0;
+  for (int c = 0; c < kCW; ++c) acc[c] = 0;
 #pragma unroll
-    for (int d = 0; d < 8; ++d) {
-      u32 r[16];
+  for (int d = 0; d < 8; ++d) {
+    u32 r[kCW];
+    if constexpr (kCW == 16) {
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
           : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
             "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-          : "r"(lane_addr + u32(d) * BN + u32(c0)));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-      for (int c = 0; c < 16; ++c) acc[c] += u64(r[c]) << (8 * d);
+          : "r"(lane_addr + u32(d) * BN));
+    } else {
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                   : "r"(lane_addr + u32(d) * BN));
     }
-    if (m < M) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const u32 n = n0 + u32(c0 + c);
-        if (n < N) gemm_epilogue(a, S, b, m, n, acc[c]);
-      }
+    for (int c = 0; c < kCW; ++c) acc[c] += u64(r[c]) << (8 * d);
+  }
+  if (m < M) {
+#pragma unroll
+    for (int c = 0; c < kCW; ++c) {
+      const u32 n = n0 + u32(cg * kCW + c);
+      if (n < N) gemm_epilogue(a, S, b, m, n, acc[c]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
