@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-blocking", action="store_true", help="skip the blocking comparison pass")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--probe", default="adder_round", choices=["adder_round", "gemm"])
+    ap.add_argument("--link", default="",
+                    help="emulate a LAN/WAN link between the parties, e.g. 10gbps (1.25e9 B/s, 0.1 ms) or "
+                         "'<latency_s>,<bytes_per_s>'; default: the real in-device / NVLink transport")
     ap.add_argument("--threshold", default="auto",
                     help="inner-pipeline chunk threshold: auto (calibrate_threshold on this link, like the "
                          "reference CLI's --threshold auto), ref (the reference default 2 MiB) or bytes")
@@ -171,12 +174,22 @@ def main():
     weights = mp.init_weights(g, seed + 11)
     x_global = mp.demo_input(g_global, seed + 12)
 
+    link = None
+    if a.link:
+        if a.link.lower() in ("10gbps", "10g"):
+            link = (1e-4, 1.25e9, 0.0)      # the paper's 10 Gb/s LAN
+        elif a.link.lower() in ("1gbps", "1g"):
+            link = (1e-3, 1.25e8, 0.0)
+        else:
+            lat, bw = (float(v) for v in a.link.split(","))
+            link = (lat, bw, 0.0)
+
     NEVER = (1 << 63)
     calib = None
     if a.threshold == "auto":
         if world == 1:
             from paper_2209_13643_b200 import tuning
-            calib = tuning.sweep_threshold("relu", chunks=4)
+            calib = tuning.sweep_threshold("relu", chunks=4, link=link)
             thr = calib["threshold_bytes"] or NEVER
         else:
             thr = 2 << 20  # NCCL link: keep the reference default (calibrating needs both ranks)
@@ -187,6 +200,8 @@ def main():
 
     def setup(mode):
         s = make_session()
+        if link:
+            s.set_link(*link)
         ex = mp.SecureExecutor(s, g, public_weights=a.weights == "public", pipelined=mode == "pipelined",
                                chunk_threshold=thr)
         ex.deal_weights(weights, seed)
@@ -340,7 +355,8 @@ def main():
                    "chunk_threshold_source": a.threshold,
                    "calibration": calib,
                    "l2": "flushed between timed steps (256 MiB memset, untimed)",
-                   "transport": "in-device zero-copy opens" if world == 1 else "NCCL send/recv over NVLink",
+                   "transport": ("in-device zero-copy opens" if world == 1 else "NCCL send/recv over NVLink")
+                   + (f" + emulated link latency {link[0]} s, {link[1]:.3g} B/s" if link else ""),
                    "kernels_per_step": launches / a.steps,
                    "execution": "one CUDA-graph replay per step (whole 2PC inference, both parties)",
                    "eager_ms_per_step": eager_ms,

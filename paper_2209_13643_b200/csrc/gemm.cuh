@@ -30,6 +30,7 @@ struct GemmArgs {
   // acc[slot] ([nbatch][M][N], zeroed) and a second kernel applies the epilogue.
   u32 ksplit = 1, kchunk = 0;
   u64* acc[2] = {nullptr, nullptr};
+  int vec16 = 0;  // every L (and transposed R) row start is 16-byte aligned (K even, bases aligned)
 };
 
 struct Epi {

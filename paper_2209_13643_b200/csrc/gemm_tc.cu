@@ -164,19 +164,41 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc_kernel(const __grid_
     const u64* L = S.L[sg] + u64(b) * S.sL[sg];
     const u64* R = S.R[sg] + u64(b) * S.sR[sg];
     const u32 m = m0 + ra;
+    const u32 ka0 = k0 + ka * 16;
+    if (a.vec16 && m < M && ka0 + 16 <= K) {  // 16-byte vector loads of a full K-chunk
+      const uint4* p = reinterpret_cast<const uint4*>(L + u64(m) * K + ka0);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const u32 k = k0 + ka * 16 + i;
-      va[i] = (m < M && k < K) ? __ldg(L + u64(m) * K + k) : 0;
+      for (int i = 0; i < 8; ++i) {
+        const uint4 w = __ldg(p + i);
+        va[2 * i] = (u64(w.y) << 32) | w.x;
+        va[2 * i + 1] = (u64(w.w) << 32) | w.z;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const u32 k = ka0 + i;
+        va[i] = (m < M && k < K) ? __ldg(L + u64(m) * K + k) : 0;
+      }
     }
     if (hasB) {
       const u32 n = n0 + rb;
+      const u32 kb0 = k0 + kbc * 16;
+      if (a.tb && a.vec16 && n < N && kb0 + 16 <= K) {
+        const uint4* p = reinterpret_cast<const uint4*>(R + u64(n) * K + kb0);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const u32 k = k0 + kbc * 16 + i;
-        u64 x = 0;
-        if (n < N && k < K) x = a.tb ? __ldg(R + u64(n) * K + k) : __ldg(R + u64(k) * N + n);
-        vb[i] = x;
+        for (int i = 0; i < 8; ++i) {
+          const uint4 w = __ldg(p + i);
+          vb[2 * i] = (u64(w.y) << 32) | w.x;
+          vb[2 * i + 1] = (u64(w.w) << 32) | w.z;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const u32 k = kb0 + i;
+          u64 x = 0;
+          if (n < N && k < K) x = a.tb ? __ldg(R + u64(n) * K + k) : __ldg(R + u64(k) * N + n);
+          vb[i] = x;
+        }
       }
     }
   };
@@ -299,10 +321,18 @@ bool ring_gemm_tc_try(Session& s, const GemmArgs& a) {
   if (a.ksplit > 1) return false;
   const double work = double(a.M) * a.N * a.K * maxseg * a.nbatch * a.nslots;
   if (!forced && (a.M < 128 || a.N < 32 || work < 2e8)) return false;
+  GemmArgs v = a;
+  bool al = (a.K % 2) == 0;
+  for (int i = 0; i < a.nslots && al; ++i)
+    for (int g = 0; g < a.sl[i].nseg; ++g) {
+      al = al && (reinterpret_cast<uintptr_t>(a.sl[i].L[g]) % 16 == 0) && (a.sl[i].sL[g] % 2 == 0);
+      if (a.tb) al = al && (reinterpret_cast<uintptr_t>(a.sl[i].R[g]) % 16 == 0) && (a.sl[i].sR[g] % 2 == 0);
+    }
+  v.vec16 = al ? 1 : 0;
   if (a.N > 32)
-    launch_tc<64>(s, a);
+    launch_tc<64>(s, v);
   else
-    launch_tc<32>(s, a);
+    launch_tc<32>(s, v);
   s.check();
   return true;
 }
