@@ -344,6 +344,7 @@ void Session::begin_capture() {
   cap.chunk = 0;
   cap.off = 0;
   cap.replays = 0;
+  cap.comm_used = false;
   for (int i = 0; i < 2; ++i) cap.stats_delta[i] = stats[i];
   cap.seq_delta = next_seq;
   cap.kernels = g_launches.load();
@@ -352,6 +353,11 @@ void Session::begin_capture() {
 }
 
 void Session::end_capture() {
+  if (cap.comm_used) {  // rejoin the comm stream (opens still in flight at the end of the run)
+    cudaEvent_t j = pool_event();
+    MPCG_CUDA(cudaEventRecord(j, comm_stream));
+    MPCG_CUDA(cudaStreamWaitEvent(stream, j, 0));
+  }
   cap.active = false;
   cudaError_t e = cudaStreamEndCapture(stream, &cap.graph);
   MPCG_CUDA(e);
@@ -482,6 +488,7 @@ void Session::post(Open& o, const std::string& tag, bool p2p) {
   cudaEvent_t built = pool_event();
   MPCG_CUDA(cudaEventRecord(built, stream));
   MPCG_CUDA(cudaStreamWaitEvent(comm_stream, built, 0));
+  if (cap.active) cap.comm_used = true;
   if (n_local == 1) {
     if (!nccl) throw Error(kTransportError, "single-party session has no peer link (connect NCCL first)");
     const int peer = 1 - party_of[0];

@@ -187,6 +187,7 @@ class Session {
     u64* iter = nullptr;             // device replay counter
     std::vector<u64> hs, c0s, mb0;
     std::vector<char> carried;  // key slot adopted from a fetch made before the capture
+    bool comm_used = false;     // the comm stream was forked into the capture
     u64 mask_per_run = 0;
     CommStats stats_delta[2];
     u64 seq_delta = 0;

@@ -397,6 +397,14 @@ DT SecureExecutor::run_layer(const LayerSpec& l, const DT& x, const Shape& in_sh
 void SecureExecutor::capture(const DT& input) {
   if (opt_.pipelined && !public_ && !wops_.empty() && !wops_[0].triple)
     throw Error(kUsageError, "capture needs one eager run first (pipelined prologue)");
+  // An open posted before the capture (the wrap-around delta on an emulated link / NCCL) must
+  // be waited outside it; inside the graph its data is then already in place, and each replay
+  // joins its own comm-stream work before it ends (Session::end_capture).
+  for (auto& op : wops_)
+    if (op.delta && op.delta->ready) {
+      MPCG_CUDA(cudaStreamWaitEvent(s_.stream, op.delta->ready, 0));
+      op.delta->ready = nullptr;
+    }
   s_.begin_capture();
   try {
     for (auto& op : wops_)  // prefetched before the capture, consumed inside it
