@@ -55,6 +55,19 @@ def parse():
     return ap.parse_args()
 
 
+def pair_layout(rank, world, local_batch):
+    """Rank -> 2PC pair placement: N=1 runs both parties on one GPU; N>=2 puts
+    party 0/1 of pair k on ranks 2k/2k+1, each pair on its own shard of the global batch."""
+    if world == 1:
+        return {"pair": 0, "party": 0, "pairs": 1, "batch_offset": 0, "global_batch": local_batch, "peer": None}
+    if world % 2:
+        raise ValueError("--gpus must be 1 or even (one party per GPU)")
+    pairs = world // 2
+    pair = rank // 2
+    return {"pair": pair, "party": rank % 2, "pairs": pairs, "batch_offset": pair * local_batch,
+            "global_batch": pairs * local_batch, "peer": rank ^ 1}
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
@@ -146,16 +159,17 @@ def main():
             run_reference(a, g, model_path)
         return
 
+    B = g.input[0]
+    try:
+        lay = pair_layout(rank, world, B)
+    except ValueError as e:
+        raise SystemExit(str(e))
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
-        if world % 2:
-            raise SystemExit("--gpus must be 1 or even (one party per GPU)")
-    pairs = max(1, world // 2)
-    pair, party = (rank // 2, rank % 2) if world > 1 else (0, 0)
-    B = g.input[0]
-    g_global = g.with_batch(B * pairs)
+    pairs, pair, party = lay["pairs"], lay["pair"], lay["party"]
+    g_global = g.with_batch(lay["global_batch"])
     seed = 1
 
     def make_session():
