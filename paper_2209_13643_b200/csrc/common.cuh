@@ -240,7 +240,7 @@ __device__ __forceinline__ void pdl_enter() {
 inline bool& pdl_enabled() {
   static bool on = [] {
     const char* e = std::getenv("MPCG_PDL");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';  // measured neutral-to-negative inside graphs: opt-in (MPCG_PDL=1)
   }();
   return on;
 }

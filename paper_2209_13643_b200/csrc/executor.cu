@@ -271,9 +271,8 @@ DT SecureExecutor::weight_matmul(size_t i, const DT& x, const ConvGeom* geom, bo
   }
   s_.wait(d);
   s_.wait(e);
-  DT R = prepare_R(s_, t, d, W.numel());
-  DT L = prepare_L(s_, t, e, 0, na);
-  mm_combine(s_, t, L, na, R, W.numel(), z.s, 0, 1, M, N, K, false, false, 0, ep);
+  DT rcache;
+  beaver_combine(s_, t, e, 0, na, d, W.numel(), &rcache, z.s, 0, 1, M, N, K, false, false, 0, ep);
   return z;
 }
 

@@ -41,27 +41,26 @@ __global__ void __launch_bounds__(256) ring_gemm_simt(GemmArgs a) {
     const u32 sb = u32(sg) * K;
     if (sb + K <= kb || sb >= ke) continue;
     const u32 lo = kb > sb ? kb - sb : 0, hi = min(K, ke - sb);
-    const u64* L = S.L[sg] + u64(b) * S.sL[sg];
-    const u64* R = S.R[sg] + u64(b) * S.sR[sg];
+    const u64 lb = u64(b) * S.sL[sg], rbb = u64(b) * S.sR[sg];
     for (u32 k0 = lo; k0 < hi; k0 += BK) {
       for (int e = threadIdx.x; e < BM * BK; e += 256) {
         const int kk = e % BK, mm = e / BK;
         u64 v = 0;
-        if (m0 + mm < M && k0 + kk < hi) v = L[u64(m0 + mm) * K + k0 + kk];
+        if (m0 + mm < M && k0 + kk < hi) v = load_l(S, sg, lb + u64(m0 + mm) * K + k0 + kk);
         As[kk][mm] = v;
       }
       if (!a.tb) {
         for (int e = threadIdx.x; e < BN * BK; e += 256) {
           const int nn = e % BN, kk = e / BN;
           u64 v = 0;
-          if (k0 + kk < hi && n0 + nn < N) v = R[u64(k0 + kk) * N + n0 + nn];
+          if (k0 + kk < hi && n0 + nn < N) v = load_r(S, sg, rbb + u64(k0 + kk) * N + n0 + nn);
           Bs[kk][nn] = v;
         }
       } else {
         for (int e = threadIdx.x; e < BN * BK; e += 256) {
           const int kk = e % BK, nn = e / BK;
           u64 v = 0;
-          if (k0 + kk < hi && n0 + nn < N) v = R[u64(n0 + nn) * K + k0 + kk];
+          if (k0 + kk < hi && n0 + nn < N) v = load_r(S, sg, rbb + u64(n0 + nn) * K + k0 + kk);
           Bs[kk][nn] = v;
         }
       }
@@ -90,9 +89,8 @@ __global__ void __launch_bounds__(256) ring_gemm_simt(GemmArgs a) {
     for (int j = 0; j < TN; ++j) {
       const u32 n = n0 + tx + j * TX;
       if (n >= N) continue;
-      if (accp)  // partial sum; wrapping u64 add is exact and order-independent
-        atomicAdd(reinterpret_cast<unsigned long long*>(accp + (u64(b) * M + m) * N + n),
-                  static_cast<unsigned long long>(acc[i][j]));
+      if (accp)  // this split's partial sum (summed mod 2^64 by the epilogue kernel)
+        accp[u64(split) * a.nbatch * M * N + (u64(b) * M + m) * N + n] = acc[i][j];
       else
         gemm_epilogue(a, S, b, m, n, acc[i][j]);
     }
@@ -106,7 +104,9 @@ __global__ void __launch_bounds__(256) gemm_splitk_epilogue(GemmArgs a) {
     const int slot = int(i / per);
     const u64 r = i - slot * per;
     const u32 n = u32(r % a.N), m = u32((r / a.N) % a.M), b = u32(r / (u64(a.N) * a.M));
-    gemm_epilogue(a, a.sl[slot], b, m, n, a.acc[slot][r]);
+    u64 v = 0;
+    for (u32 sp = 0; sp < a.ksplit; ++sp) v += a.acc[slot][u64(sp) * per + r];
+    gemm_epilogue(a, a.sl[slot], b, m, n, v);
   }
 }
 
@@ -130,10 +130,9 @@ void launch_simt(Session& s, GemmArgs a) {
     a.ksplit = split;
     a.kchunk = ((kp + split - 1) / split + 15) / 16 * 16;
     a.ksplit = (kp + a.kchunk - 1) / a.kchunk;
-    const u64 per = u64(a.nbatch) * a.M * a.N;
-    ws = s.raw(per * a.nslots);
-    MPCG_CUDA(cudaMemsetAsync(ws->ptr, 0, per * a.nslots * 8, st));
-    for (int i = 0; i < a.nslots; ++i) a.acc[i] = ws->ptr + i * per;
+    const u64 per = u64(a.nbatch) * a.M * a.N;  // one partial tile set per split, no zeroing pass
+    ws = s.raw(per * a.ksplit * a.nslots);
+    for (int i = 0; i < a.nslots; ++i) a.acc[i] = ws->ptr + i * per * a.ksplit;
   }
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, a.nslots * a.nbatch * a.ksplit);
   cudaEvent_t pe;
@@ -331,6 +330,68 @@ void mm_combine(Session& s, const Triple& t, const DT& L, size_t na, const DT& R
   ring_gemm_launch(s, a);
 }
 
+// The Beaver combine of one chunk straight from the opened payloads (see the file header):
+// operands are generated in the SIMT tile loaders; only a tcgen05-bound GEMM materialises
+// them (prepare_L / prepare_R, R cached across chunks in *rcache).
+void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na, const Open& d, size_t nb,
+                    DT* rcache, u64* const out[2], size_t out_off, u32 nbatch, u32 M, u32 N, u32 K, bool tb,
+                    bool batched_r, size_t r_batch0, const Epi& ep) {
+  GemmArgs a{};
+  a.nslots = s.n_local;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.tb = tb;
+  a.nbatch = nbatch;
+  a.trunc_bits = ep.trunc_bits;
+  a.col2im = ep.col2im;
+  a.OHW = ep.OHW;
+  for (int i = 0; i < s.n_local; ++i) a.sl[i].nseg = s.party_of[i] == 0 ? 3 : 2;
+  if (ring_gemm_tc_wants(a)) {
+    DT L = prepare_L(s, t, e, a_off, na);
+    if (!*rcache) *rcache = prepare_R(s, t, d, nb);
+    mm_combine(s, t, L, na, *rcache, nb, out, out_off, nbatch, M, N, K, tb, batched_r, r_batch0, ep);
+    return;
+  }
+  const u64 sL = u64(M) * K, sR = batched_r ? u64(K) * N : 0;
+  const u64 rboff = batched_r ? r_batch0 * u64(K) * N : 0;
+  for (int i = 0; i < s.n_local; ++i) {
+    GemmSlotArgs& S = a.sl[i];
+    const u64* E0 = e.own(i);
+    const u64* E1 = e.peer(i);
+    const u64* F0 = d.own(i) + rboff;
+    const u64* F1 = d.peer(i) + rboff;
+    S.out = out[i] + out_off;
+    S.bias = ep.bias[i];
+    S.ckey = t.mm.key;
+    S.ckp = t.mm.kp;
+    S.cbase = 1 + 2 * t.mm.na + 2 * t.mm.nb + t.mm.offC + out_off;
+    S.mm = t.mm;
+    S.aoff = a_off;
+    S.boff = rboff;
+    if (s.party_of[i] == 0) {  // -r_C + A*B + E*(b0 + F) + a0*F
+      S.cterm = -1;
+      S.lk[0] = kOpA;
+      S.rk[0] = kOpB;
+      S.lk[1] = kOpSum, S.L[1] = E0, S.L2[1] = E1;
+      S.rk[2 - 1] = kOpB0F, S.R[1] = F0, S.R2[1] = F1;
+      S.lk[2] = kOpA0;
+      S.rk[2] = kOpSum, S.R[2] = F0, S.R2[2] = F1;
+    } else {  // +r_C + E*r_B + r_A*F
+      S.cterm = +1;
+      S.lk[0] = kOpSum, S.L[0] = E0, S.L2[0] = E1;
+      S.rk[0] = kOpRB;
+      S.lk[1] = kOpRA;
+      S.rk[1] = kOpSum, S.R[1] = F0, S.R2[1] = F1;
+    }
+    for (int g = 0; g < 3; ++g) {
+      S.sL[g] = sL;
+      S.sR[g] = sR;
+    }
+  }
+  ring_gemm_launch(s, a);
+}
+
 // Public-weight product x2d * W (H/engine/executor.hpp:294-298): one segment, no triple.
 void public_gemm(Session& s, const u64* const x[2], const u64* W, u64* const out[2], u32 M, u32 N, u32 K,
                  const Epi& ep) {
@@ -381,7 +442,7 @@ DT beaver_matmul(Session& s, const DT& x, const DT& y, bool transpose_b, const s
     s.post(he[k], chunks == 1 ? tag + ".eps" : tag + ".eps.chunk" + std::to_string(k));
   }
   s.wait(hd);
-  DT R = prepare_R(s, t, hd, nb);
+  DT rcache;
   Shape out_shape(x.shape.begin(), x.shape.end() - 1);
   out_shape.push_back(N);
   DT z = s.alloc(out_shape, x.scale);
@@ -390,14 +451,13 @@ DT beaver_matmul(Session& s, const DT& x, const DT& y, bool transpose_b, const s
     const auto r = chunk_range(rows, chunks, k);
     const size_t cnt = r.second - r.first;
     s.wait(he[k]);
-    DT L = prepare_L(s, t, he[k], r.first * row_w, cnt * row_w);
     Epi ep{};
     if (batched_b)
-      mm_combine(s, t, L, cnt * row_w, R, nb, z.s, r.first * out_row_w, u32(cnt), u32(M), u32(N), u32(K),
-                 transpose_b, true, r.first, ep);
+      beaver_combine(s, t, he[k], r.first * row_w, cnt * row_w, hd, nb, &rcache, z.s, r.first * out_row_w,
+                     u32(cnt), u32(M), u32(N), u32(K), transpose_b, true, r.first, ep);
     else
-      mm_combine(s, t, L, cnt * row_w, R, nb, z.s, r.first * out_row_w, 1, u32(cnt), u32(N), u32(K),
-                 transpose_b, false, 0, ep);
+      beaver_combine(s, t, he[k], r.first * row_w, cnt * row_w, hd, nb, &rcache, z.s, r.first * out_row_w, 1,
+                     u32(cnt), u32(N), u32(K), transpose_b, false, 0, ep);
   }
   s.check();
   return z;

@@ -5,12 +5,31 @@
 
 namespace mpcg {
 
+// Operand kinds of a GEMM segment. Plain loads, or generated on the fly in the SIMT tile
+// loader from the dealer's stream / the two halves of an opened payload, so the Beaver
+// combine needs no operand-materialisation pass (matmul triple draws: H/sharing/triple.hpp:96-114).
+enum OpKind : int {
+  kOpMem = 0,   // p[idx]
+  kOpSum = 1,   // p[idx] + q[idx]               (opened E or F = own + peer payload)
+  kOpA = 2,     // dealer A                       (party 0)
+  kOpA0 = 3,    // a0 = A - r_A                   (party 0 share of A)
+  kOpRA = 4,    // r_A                            (party 1 share of A)
+  kOpB = 5,     // dealer B                       (party 0)
+  kOpB0F = 6,   // (B - r_B) + p[idx] + q[idx]    (party 0: b0 + F)
+  kOpRB = 7,    // r_B                            (party 1 share of B)
+};
+
 // One party slot of a multi-segment ring GEMM: out = epi( sum_g L_g * R_g ).
 struct GemmSlotArgs {
   int nseg = 0;
   const u64* L[3] = {};   // [batch][M][K], batch stride sL (0 = shared)
   const u64* R[3] = {};   // [batch][K][N] or, transposed, [batch][N][K]; stride sR
   u64 sL[3] = {}, sR[3] = {};
+  int lk[3] = {0, 0, 0}, rk[3] = {0, 0, 0};   // OpKind per segment (kOpMem = plain)
+  const u64* L2[3] = {};  // second addend of kOpSum
+  const u64* R2[3] = {};  // second addend of kOpSum / kOpB0F
+  MmTriple mm{};          // dealer view for generated operands
+  u64 aoff = 0, boff = 0; // element offset of this call inside A / B (PRG index base)
   u64* out = nullptr;
   const u64* bias = nullptr;  // [N], added after truncation
   int cterm = 0;              // +1 / -1: add / subtract the triple's r_C
@@ -44,6 +63,27 @@ struct ConvGeom {
   u32 N, C, H, W, k, stride, pad, OH, OW;
 };
 
+// Element idx (call-local linear index in the segment's stored layout) of a segment.
+__device__ __forceinline__ u64 load_l(const GemmSlotArgs& S, int sg, u64 idx) {
+  switch (S.lk[sg]) {
+    case kOpMem: return S.L[sg][idx];
+    case kOpSum: return S.L[sg][idx] + S.L2[sg][idx];
+    case kOpA: return mm_A(S.mm, S.aoff + idx);
+    case kOpA0: return mm_A(S.mm, S.aoff + idx) - mm_rA(S.mm, S.aoff + idx);
+    default: return mm_rA(S.mm, S.aoff + idx);
+  }
+}
+__device__ __forceinline__ u64 load_r(const GemmSlotArgs& S, int sg, u64 idx) {
+  switch (S.rk[sg]) {
+    case kOpMem: return S.R[sg][idx];
+    case kOpSum: return S.R[sg][idx] + S.R2[sg][idx];
+    case kOpB: return mm_B(S.mm, S.boff + idx);
+    case kOpB0F:
+      return (mm_B(S.mm, S.boff + idx) - mm_rB(S.mm, S.boff + idx)) + (S.R[sg][idx] + S.R2[sg][idx]);
+    default: return mm_rB(S.mm, S.boff + idx);
+  }
+}
+
 __device__ __forceinline__ void gemm_epilogue(const GemmArgs& a, const GemmSlotArgs& S, u32 b, u32 m, u32 n,
                                               u64 v) {
   const u64 lin = (u64(b) * a.M + m) * a.N + n;
@@ -63,6 +103,10 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& a, const GemmSlotA
 
 void ring_gemm_launch(Session& s, const GemmArgs& a);
 bool ring_gemm_tc_try(Session& s, const GemmArgs& a);
+bool ring_gemm_tc_wants(const GemmArgs& a);  // shape/budget test only (operands not inspected)
+void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na, const Open& d, size_t nb,
+                    DT* rcache, u64* const out[2], size_t out_off, u32 nbatch, u32 M, u32 N, u32 K, bool tb,
+                    bool batched_r, size_t r_batch0, const Epi& ep);
 
 void delta_build_mem(Session& s, const Triple& t, const u64* const y[2], size_t nb, Open& o);
 void eps_build_mem(Session& s, const Triple& t, const u64* const x[2], size_t a_off, size_t na, Open& o);

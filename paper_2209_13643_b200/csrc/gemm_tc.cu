@@ -311,16 +311,22 @@ int& tc_gemm_mode() {
 }
 
 // Shapes worth the tensor cores: full 128-row tiles, N >= 32, exact-accumulation budget.
-bool ring_gemm_tc_try(Session& s, const GemmArgs& a) {
+bool ring_gemm_tc_wants(const GemmArgs& a) {
   const int mode = tc_gemm_mode();
-  const bool forced = mode == 1;
   if (mode == 0) return false;
   int maxseg = 0;
   for (int i = 0; i < a.nslots; ++i) maxseg = a.sl[i].nseg > maxseg ? a.sl[i].nseg : maxseg;
   if (u64(maxseg) * a.K > kMaxKPrime) return false;  // needs the multi-pass drain (not yet)
   if (a.ksplit > 1) return false;
   const double work = double(a.M) * a.N * a.K * maxseg * a.nbatch * a.nslots;
-  if (!forced && (a.M < 128 || a.N < 32 || work < 2e8)) return false;
+  return mode == 1 || (a.M >= 128 && a.N >= 32 && work >= 2e8);
+}
+
+bool ring_gemm_tc_try(Session& s, const GemmArgs& a) {
+  if (!ring_gemm_tc_wants(a)) return false;
+  for (int i = 0; i < a.nslots; ++i)  // the tensor-core producer reads materialised operands
+    for (int g = 0; g < a.sl[i].nseg; ++g)
+      if (a.sl[i].lk[g] != kOpMem || a.sl[i].rk[g] != kOpMem) return false;
   GemmArgs v = a;
   bool al = (a.K % 2) == 0;
   for (int i = 0; i < a.nslots && al; ++i)

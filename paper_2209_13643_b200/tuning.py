@@ -49,15 +49,20 @@ def sweep_threshold(op="relu", sizes=DEFAULT_SIZES, chunks=4, link=None, seed=7,
         raise ValueError("insufficient sweep: need at least two operand sizes")
     if chunks < 2:
         raise ValueError("sweep needs chunks >= 2")
-    points, thr = [], None
+    points = []
     for elems in sizes:
         b = _time_op(op, elems, 1, link, seed, reps, device)
         c = _time_op(op, elems, chunks, link, seed, reps, device)
         wins = c < b * (1.0 - margin)
         points.append({"elems": elems, "bytes": elems * 8, "blocking_ms": b, "chunked_ms": c,
                        "chunked_wins": wins})
-        if wins and thr is None:
-            thr = elems * 8
+    # A crossover: chunking wins at this size and at every larger swept size (an isolated
+    # noisy "win" below a loss does not gate chunking on).
+    thr = None
+    for i in range(len(points) - 1, -1, -1):
+        if not points[i]["chunked_wins"]:
+            break
+        thr = points[i]["bytes"]
     return {"op": op, "chunks": chunks, "points": points, "threshold_bytes": thr}
 
 
