@@ -260,10 +260,12 @@ DT SecureExecutor::weight_matmul(size_t i, const DT& x, const ConvGeom* geom, bo
   op.delta.reset();
   const size_t na = size_t(M) * K;
   Open e = s_.begin_open(na, Reduce::Sum);
+  DT aops;  // A-side combine operands from the eps draws (SIMT combine only)
+  if (!beaver_combine_uses_tc(s_, 1, M, N, K)) aops = s_.alloc(Shape{2, na});
   if (geom)
-    eps_build_im2col(s_, t, x.s, *geom, 0, na, e);
+    eps_build_im2col(s_, t, x.s, *geom, 0, na, e, aops ? &aops : nullptr);
   else
-    eps_build_mem(s_, t, x.s, 0, na, e);
+    eps_build_mem(s_, t, x.s, 0, na, e, aops ? &aops : nullptr);
   s_.post(e, op.tag + ".eps");
   if (opt_.pipelined && wops_.size() > 1) {  // next op's delta leaves while this eps travels
     const size_t next = (i + 1) % wops_.size();
@@ -272,7 +274,8 @@ DT SecureExecutor::weight_matmul(size_t i, const DT& x, const ConvGeom* geom, bo
   s_.wait(d);
   s_.wait(e);
   DT rcache;
-  beaver_combine(s_, t, e, 0, na, d, W.numel(), &rcache, z.s, 0, 1, M, N, K, false, false, 0, ep);
+  beaver_combine(s_, t, e, 0, na, d, W.numel(), &rcache, z.s, 0, 1, M, N, K, false, false, 0, ep,
+                 aops ? &aops : nullptr);
   return z;
 }
 

@@ -200,36 +200,56 @@ void delta_build_mem(Session& s, const Triple& t, const u64* const y[2], size_t 
 }
 
 // own payload = x - a over A elements [a_off, a_off + na)  (eps; beaver.hpp:205,216)
-void eps_build_mem(Session& s, const Triple& t, const u64* const x[2], size_t a_off, size_t na, Open& o) {
+// a-share of A element i; also emits the party's A-side GEMM operands into aop (if given):
+// party 0 {A, a0 = A - r_A} at [j] and [na + j], party 1 {r_A} at [j]. The draws are the ones
+// the eps payload needs anyway, so the combine GEMM reads them instead of redrawing.
+__device__ __forceinline__ u64 a_share_out(const MmTriple& t, int party, u64 i, u64* aop, u64 j, u64 na) {
+  const u64 ra = mm_rA(t, i);
+  if (party) {
+    if (aop) aop[j] = ra;
+    return ra;
+  }
+  const u64 A = mm_A(t, i), a0 = A - ra;
+  if (aop) {
+    aop[j] = A;
+    aop[na + j] = a0;
+  }
+  return a0;
+}
+
+void eps_build_mem(Session& s, const Triple& t, const u64* const x[2], size_t a_off, size_t na, Open& o,
+                   const DT* aops) {
   const Pid2 pid = pids(s);
   const Ptr2 own = own_ptrs(o);
   const MmTriple mm = t.mm;
   const CPtr2 xp{{x[0], x[1]}};
+  const Ptr2 ap{{aops ? aops->s[0] : nullptr, aops ? aops->s[1] : nullptr}};
   launch_ew(s.stream, s.n_local, na, [=] __device__(int slot, u64 j) {
-    own.p[slot][j] = xp.p[slot][a_off + j] - mm_a_share(mm, pid.v[slot], a_off + j);
+    own.p[slot][j] = xp.p[slot][a_off + j] - a_share_out(mm, pid.v[slot], a_off + j, ap.p[slot], j, na);
   });
 }
 
 // im2col-fused eps build for conv layers (H/engine/executor.hpp:82-108): row=(n,oh,ow),
 // col=(ci,ki,kj), padding taps read zero.
 void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const ConvGeom& gm, size_t a_off,
-                      size_t na, Open& o) {
+                      size_t na, Open& o, const DT* aops) {
   const Pid2 pid = pids(s);
   const Ptr2 own = own_ptrs(o);
   const MmTriple mm = t.mm;
   const CPtr2 xp{{x[0], x[1]}};
   const ConvGeom g = gm;
+  const Ptr2 ap{{aops ? aops->s[0] : nullptr, aops ? aops->s[1] : nullptr}};
   launch_ew(s.stream, s.n_local, na, [=] __device__(int slot, u64 j) {
     const u64 idx = a_off + j;
     const u32 KK = g.C * g.k * g.k;
-    const u32 r = u32(idx / KK), c = u32(idx - u64(r) * KK);
+    const u32 r = u32(idx) / KK, c = u32(idx) - r * KK;
     const u32 ow = r % g.OW, oh = (r / g.OW) % g.OH, n = r / (g.OW * g.OH);
     const u32 kj = c % g.k, ki = (c / g.k) % g.k, ci = c / (g.k * g.k);
     const int ih = int(oh * g.stride + ki) - int(g.pad), iw = int(ow * g.stride + kj) - int(g.pad);
     u64 v = 0;
     if (ih >= 0 && iw >= 0 && ih < int(g.H) && iw < int(g.W))
       v = xp.p[slot][((u64(n) * g.C + ci) * g.H + u32(ih)) * g.W + u32(iw)];
-    own.p[slot][j] = v - mm_a_share(mm, pid.v[slot], idx);
+    own.p[slot][j] = v - a_share_out(mm, pid.v[slot], idx, ap.p[slot], j, na);
   });
 }
 
@@ -333,9 +353,20 @@ void mm_combine(Session& s, const Triple& t, const DT& L, size_t na, const DT& R
 // The Beaver combine of one chunk straight from the opened payloads (see the file header):
 // operands are generated in the SIMT tile loaders; only a tcgen05-bound GEMM materialises
 // them (prepare_L / prepare_R, R cached across chunks in *rcache).
+bool beaver_combine_uses_tc(const Session& s, u32 nbatch, u32 M, u32 N, u32 K) {
+  GemmArgs a{};
+  a.nslots = s.n_local;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.nbatch = nbatch;
+  for (int i = 0; i < s.n_local; ++i) a.sl[i].nseg = s.party_of[i] == 0 ? 3 : 2;
+  return ring_gemm_tc_wants(a);
+}
+
 void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na, const Open& d, size_t nb,
                     DT* rcache, u64* const out[2], size_t out_off, u32 nbatch, u32 M, u32 N, u32 K, bool tb,
-                    bool batched_r, size_t r_batch0, const Epi& ep) {
+                    bool batched_r, size_t r_batch0, const Epi& ep, const DT* aops) {
   GemmArgs a{};
   a.nslots = s.n_local;
   a.M = M;
@@ -369,19 +400,23 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
     S.mm = t.mm;
     S.aoff = a_off;
     S.boff = rboff;
+    const u64* ao = aops ? aops->s[i] : nullptr;  // A-side operands emitted by the eps build
     if (s.party_of[i] == 0) {  // -r_C + A*B + E*(b0 + F) + a0*F
       S.cterm = -1;
-      S.lk[0] = kOpA;
+      if (ao) S.lk[0] = kOpMem, S.L[0] = ao;
+      else S.lk[0] = kOpA;
       S.rk[0] = kOpB;
       S.lk[1] = kOpSum, S.L[1] = E0, S.L2[1] = E1;
-      S.rk[2 - 1] = kOpB0F, S.R[1] = F0, S.R2[1] = F1;
-      S.lk[2] = kOpA0;
+      S.rk[1] = kOpB0F, S.R[1] = F0, S.R2[1] = F1;
+      if (ao) S.lk[2] = kOpMem, S.L[2] = ao + na;
+      else S.lk[2] = kOpA0;
       S.rk[2] = kOpSum, S.R[2] = F0, S.R2[2] = F1;
     } else {  // +r_C + E*r_B + r_A*F
       S.cterm = +1;
       S.lk[0] = kOpSum, S.L[0] = E0, S.L2[0] = E1;
       S.rk[0] = kOpRB;
-      S.lk[1] = kOpRA;
+      if (ao) S.lk[1] = kOpMem, S.L[1] = ao;
+      else S.lk[1] = kOpRA;
       S.rk[1] = kOpSum, S.R[1] = F0, S.R2[1] = F1;
     }
     for (int g = 0; g < 3; ++g) {
@@ -435,10 +470,15 @@ DT beaver_matmul(Session& s, const DT& x, const DT& y, bool transpose_b, const s
   const size_t row_w = batched_b ? M * K : K;
   chunks = clamp_chunks(chunks, rows);
   std::vector<Open> he(static_cast<size_t>(chunks));
+  std::vector<DT> aops(static_cast<size_t>(chunks));
   for (int k = 0; k < chunks; ++k) {
     const auto r = chunk_range(rows, chunks, k);
-    he[k] = s.begin_open((r.second - r.first) * row_w, Reduce::Sum);
-    eps_build_mem(s, t, x.s, r.first * row_w, (r.second - r.first) * row_w, he[k]);
+    const size_t cnt = r.second - r.first;
+    he[k] = s.begin_open(cnt * row_w, Reduce::Sum);
+    const bool tc = batched_b ? beaver_combine_uses_tc(s, u32(cnt), u32(M), u32(N), u32(K))
+                              : beaver_combine_uses_tc(s, 1, u32(cnt), u32(N), u32(K));
+    if (!tc) aops[k] = s.alloc(Shape{2, cnt * row_w});
+    eps_build_mem(s, t, x.s, r.first * row_w, cnt * row_w, he[k], tc ? nullptr : &aops[k]);
     s.post(he[k], chunks == 1 ? tag + ".eps" : tag + ".eps.chunk" + std::to_string(k));
   }
   s.wait(hd);
@@ -454,10 +494,10 @@ DT beaver_matmul(Session& s, const DT& x, const DT& y, bool transpose_b, const s
     Epi ep{};
     if (batched_b)
       beaver_combine(s, t, he[k], r.first * row_w, cnt * row_w, hd, nb, &rcache, z.s, r.first * out_row_w,
-                     u32(cnt), u32(M), u32(N), u32(K), transpose_b, true, r.first, ep);
+                     u32(cnt), u32(M), u32(N), u32(K), transpose_b, true, r.first, ep, aops[k] ? &aops[k] : nullptr);
     else
       beaver_combine(s, t, he[k], r.first * row_w, cnt * row_w, hd, nb, &rcache, z.s, r.first * out_row_w, 1,
-                     u32(cnt), u32(N), u32(K), transpose_b, false, 0, ep);
+                     u32(cnt), u32(N), u32(K), transpose_b, false, 0, ep, aops[k] ? &aops[k] : nullptr);
   }
   s.check();
   return z;

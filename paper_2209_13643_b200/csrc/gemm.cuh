@@ -106,12 +106,17 @@ bool ring_gemm_tc_try(Session& s, const GemmArgs& a);
 bool ring_gemm_tc_wants(const GemmArgs& a);  // shape/budget test only (operands not inspected)
 void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na, const Open& d, size_t nb,
                     DT* rcache, u64* const out[2], size_t out_off, u32 nbatch, u32 M, u32 N, u32 K, bool tb,
-                    bool batched_r, size_t r_batch0, const Epi& ep);
+                    bool batched_r, size_t r_batch0, const Epi& ep, const DT* aops = nullptr);
+// Whether the combine of this shape runs on the tensor cores (materialised operands) —
+// callers then skip emitting the A-side operands in the eps build.
+bool beaver_combine_uses_tc(const Session& s, u32 nbatch, u32 M, u32 N, u32 K);
 
 void delta_build_mem(Session& s, const Triple& t, const u64* const y[2], size_t nb, Open& o);
-void eps_build_mem(Session& s, const Triple& t, const u64* const x[2], size_t a_off, size_t na, Open& o);
+// eps = x - a payload; with `aops` ([2, na] per slot) also the A-side combine operands.
+void eps_build_mem(Session& s, const Triple& t, const u64* const x[2], size_t a_off, size_t na, Open& o,
+                   const DT* aops = nullptr);
 void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const ConvGeom& g, size_t a_off,
-                      size_t na, Open& o);
+                      size_t na, Open& o, const DT* aops = nullptr);
 DT prepare_R(Session& s, const Triple& t, const Open& d, size_t nb);
 DT prepare_L(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na);
 void mm_combine(Session& s, const Triple& t, const DT& L, size_t na, const DT& R, size_t nb, u64* const out[2],
