@@ -147,8 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc_kernel(const __grid_
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const u32 tmem = tmem_base_slot;
 
-  const u32 kb_per_seg = (K + kKB - 1) / kKB;
-  const u32 steps = u32(S.nseg) * kb_per_seg;
+  const u32 steps = (u32(S.nseg) * K + kKB - 1) / kKB;
   constexpr u32 idesc = idesc_i8(kTM, BN);
   u32 phase[2] = {0, 0};
 
@@ -157,50 +156,40 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc_kernel(const __grid_
   const bool hasB = tid < kBUnits;
   const int rb = tid % BN, kbc = tid / BN;
   u64 va[16], vb[16];
-  // Register prefetch of step `st`'s operands (issued while earlier MMAs run).
-  auto load_step = [&](u32 st) {
-    const int sg = int(st / kb_per_seg);
-    const u32 k0 = (st - u32(sg) * kb_per_seg) * kKB;
-    const u64* L = S.L[sg] + u64(b) * S.sL[sg];
-    const u64* R = S.R[sg] + u64(b) * S.sR[sg];
-    const u32 m = m0 + ra;
-    const u32 ka0 = k0 + ka * 16;
-    if (a.vec16 && m < M && ka0 + 16 <= K) {  // 16-byte vector loads of a full K-chunk
-      const uint4* p = reinterpret_cast<const uint4*>(L + u64(m) * K + ka0);
+  // Register prefetch of step `st`'s operands (issued while earlier MMAs run). The segments
+  // are packed back to back along K' = nseg*K, so small K (e.g. 25) is not padded per segment.
+  const u32 KP = u32(S.nseg) * K;
+  auto load16 = [&](const u64* const* base, const u64* stride, bool trans, u32 row, u32 rows, u32 kp, u64 (&v)[16]) {
+    // 16 K'-consecutive values of `row` starting at packed index kp
+    const u32 sg0 = kp / K;
+    if (row < rows && kp + 16 <= KP && sg0 == (kp + 15) / K && a.vec16 && (trans || base == S.L)) {
+      const u32 k = kp - sg0 * K;
+      const u64* P = base[sg0] + u64(b) * stride[sg0] + u64(row) * K + k;
+      const uint4* p4 = reinterpret_cast<const uint4*>(P);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const uint4 w = __ldg(p + i);
-        va[2 * i] = (u64(w.y) << 32) | w.x;
-        va[2 * i + 1] = (u64(w.w) << 32) | w.z;
+        const uint4 w = __ldg(p4 + i);
+        v[2 * i] = (u64(w.y) << 32) | w.x;
+        v[2 * i + 1] = (u64(w.w) << 32) | w.z;
       }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const u32 k = ka0 + i;
-        va[i] = (m < M && k < K) ? __ldg(L + u64(m) * K + k) : 0;
-      }
+      return;
     }
-    if (hasB) {
-      const u32 n = n0 + rb;
-      const u32 kb0 = k0 + kbc * 16;
-      if (a.tb && a.vec16 && n < N && kb0 + 16 <= K) {
-        const uint4* p = reinterpret_cast<const uint4*>(R + u64(n) * K + kb0);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint4 w = __ldg(p + i);
-          vb[2 * i] = (u64(w.y) << 32) | w.x;
-          vb[2 * i + 1] = (u64(w.w) << 32) | w.z;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const u32 k = kb0 + i;
-          u64 x = 0;
-          if (n < N && k < K) x = a.tb ? __ldg(R + u64(n) * K + k) : __ldg(R + u64(k) * N + n);
-          vb[i] = x;
-        }
+    for (int i = 0; i < 16; ++i) {
+      u64 x = 0;
+      const u32 q = kp + i;
+      if (row < rows && q < KP) {
+        const u32 sg = q / K, k = q - sg * K;
+        const u64* P = base[sg] + u64(b) * stride[sg];
+        x = trans ? __ldg(P + u64(row) * K + k) : __ldg(P + u64(k) * N + row);
       }
+      v[i] = x;
     }
+  };
+  auto load_step = [&](u32 st) {
+    const u32 k0 = st * kKB;
+    load16(S.L, S.sL, true, m0 + ra, M, k0 + ka * 16, va);          // A rows are K-contiguous
+    if (hasB) load16(S.R, S.sR, a.tb != 0, n0 + rb, N, k0 + kbc * 16, vb);
   };
 
   if (steps > 0) load_step(0);
@@ -260,9 +249,13 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc_kernel(const __grid_
           : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
             "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
           : "r"(lane_addr + u32(d) * BN));
-    } else {
+    } else if constexpr (kCW == 8) {
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                   : "r"(lane_addr + u32(d) * BN));
+    } else {
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                    : "r"(lane_addr + u32(d) * BN));
     }
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -319,7 +312,10 @@ bool ring_gemm_tc_wants(const GemmArgs& a) {
   if (u64(maxseg) * a.K > kMaxKPrime) return false;  // needs the multi-pass drain (not yet)
   if (a.ksplit > 1) return false;
   const double work = double(a.M) * a.N * a.K * maxseg * a.nbatch * a.nslots;
-  return mode == 1 || (a.M >= 128 && a.N >= 32 && work >= 2e8);
+  // Full 128-row tiles and enough work to amortise the operand materialisation; the SIMT
+  // path is issue-bound at ~9 instructions per ring MAC, so even N=6 convs win on the
+  // tensor cores (N padded to 16).
+  return mode == 1 || (a.M >= 128 && work >= 3e7);
 }
 
 bool ring_gemm_tc_try(Session& s, const GemmArgs& a) {
@@ -337,8 +333,10 @@ bool ring_gemm_tc_try(Session& s, const GemmArgs& a) {
   v.vec16 = al ? 1 : 0;
   if (a.N > 32)
     launch_tc<64>(s, v);
-  else
+  else if (a.N > 16)
     launch_tc<32>(s, v);
+  else
+    launch_tc<16>(s, v);
   s.check();
   return true;
 }
