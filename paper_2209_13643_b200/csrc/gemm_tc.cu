@@ -315,7 +315,7 @@ bool ring_gemm_tc_wants(const GemmArgs& a) {
   // Full 128-row tiles and enough work to amortise the operand materialisation; the SIMT
   // path is issue-bound at ~9 instructions per ring MAC, so even N=6 convs win on the
   // tensor cores (N padded to 16).
-  return mode == 1 || (a.M >= 128 && work >= 3e7);
+  return mode == 1 || (a.M >= 128 && a.N >= 16 && work >= 3e7);
 }
 
 bool ring_gemm_tc_try(Session& s, const GemmArgs& a) {
