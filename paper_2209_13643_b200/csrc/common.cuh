@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -90,53 +91,58 @@ struct EwTriple {
 
 __device__ __forceinline__ u64 tkey(u64 key, const u64* kp) { return kp ? __ldg(kp) : key; }
 
-// a, b shares of element g (global index) for `party` (0 absorbs the secret).
-__device__ __forceinline__ void ew_ab(const EwTriple& t, int party, u64 g, u64& a, u64& b) {
+// Raw dealer draws of elementwise triple element g (H/sharing/triple.hpp:62-94): the masks
+// rA, rB (, rC) that party 1 receives and, when `p0` is asked for, the secrets A, B that
+// party 0's shares absorb. Splitting draws from shares lets a thread that evaluates BOTH
+// co-located party slots (1-GPU mode) run the dealer once per element, as the dealer does.
+struct Dw {
+  u64 A, B, ra, rb, rc;
+};
+template <bool WithC>
+__device__ __forceinline__ Dw ew_draw(const EwTriple& t, u64 g, bool p0) {
   const u64 key = tkey(t.key, t.kp);
   const u64 nbd = t.square ? 0 : t.mg;
   const u64 baseA = 1 + t.mg + nbd;
   const u64 baseB = baseA + t.mg;
-  const u64 ra = drw(key, baseA + g), rb = drw(key, baseB + g);
+  Dw d;
+  d.ra = drw(key, baseA + g);
+  d.rb = drw(key, baseB + g);
+  d.rc = WithC ? drw(key, baseB + t.mg + g) : 0;
+  d.A = d.B = 0;
+  if (p0) {
+    d.A = drw(key, 1 + g);
+    d.B = t.square ? d.A : drw(key, 1 + t.mg + g);
+  }
+  return d;
+}
+// `party`'s shares of a drawn element (0 absorbs the secret).
+template <bool WithC>
+__device__ __forceinline__ void ew_share(const EwTriple& t, int party, const Dw& d, u64& a, u64& b, u64& c) {
   if (party != 0) {
-    a = ra;
-    b = rb;
+    a = d.ra;
+    b = d.rb;
+    if (WithC) c = d.rc;
     return;
   }
-  const u64 A = drw(key, 1 + g);
-  const u64 B = t.square ? A : drw(key, 1 + t.mg + g);
   if (t.bin) {
-    a = A ^ ra;
-    b = B ^ rb;
+    a = d.A ^ d.ra;
+    b = d.B ^ d.rb;
+    if (WithC) c = (d.A & d.B) ^ d.rc;
   } else {
-    a = A - ra;
-    b = B - rb;
+    a = d.A - d.ra;
+    b = d.B - d.rb;
+    if (WithC) c = d.A * d.B - d.rc;
   }
 }
 
+// a, b shares of element g (global index) for `party` (0 absorbs the secret).
+__device__ __forceinline__ void ew_ab(const EwTriple& t, int party, u64 g, u64& a, u64& b) {
+  u64 c;
+  ew_share<false>(t, party, ew_draw<false>(t, g, party == 0), a, b, c);
+}
+
 __device__ __forceinline__ void ew_abc(const EwTriple& t, int party, u64 g, u64& a, u64& b, u64& c) {
-  const u64 key = tkey(t.key, t.kp);
-  const u64 nbd = t.square ? 0 : t.mg;
-  const u64 baseA = 1 + t.mg + nbd;
-  const u64 baseB = baseA + t.mg;
-  const u64 baseC = baseB + t.mg;
-  const u64 ra = drw(key, baseA + g), rb = drw(key, baseB + g), rc = drw(key, baseC + g);
-  if (party != 0) {
-    a = ra;
-    b = rb;
-    c = rc;
-    return;
-  }
-  const u64 A = drw(key, 1 + g);
-  const u64 B = t.square ? A : drw(key, 1 + t.mg + g);
-  if (t.bin) {
-    a = A ^ ra;
-    b = B ^ rb;
-    c = (A & B) ^ rc;
-  } else {
-    a = A - ra;
-    b = B - rb;
-    c = A * B - rc;
-  }
+  ew_share<true>(t, party, ew_draw<true>(t, g, party == 0), a, b, c);
 }
 
 // Square triples only need a and c (b is never used by the combine).
@@ -275,14 +281,56 @@ inline unsigned ew_blocks(u64 n) {
   return static_cast<unsigned>(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
+// Pair evaluation (1-GPU mode, both party slots local): a functor that defines both(i)
+// evaluates element i for slot 0 and slot 1 in one thread, running the dealer's draws for
+// that element once. Each slot still writes its own outbox and reads the peer's payload
+// from memory, exactly as in per-slot evaluation. MPCG_PAIR_EVAL=0 turns it off.
+template <class F, class = void>
+struct has_both : std::false_type {};
+template <class F>
+struct has_both<F, std::void_t<decltype(std::declval<const F&>().both(u64(0)))>> : std::true_type {};
+
+inline bool& pair_eval_enabled() {
+  static bool on = [] {
+    const char* e = std::getenv("MPCG_PAIR_EVAL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// f for slot `slot`, or for both slots when `pair`.
+template <class F>
+__device__ __forceinline__ void eval_slots(const F& f, bool pair, int slot, u64 i) {
+  if (!pair) {
+    f(slot, i);
+  } else if constexpr (has_both<F>::value) {
+    f.both(i);
+  } else {
+    f(0, i);
+    f(1, i);
+  }
+}
+
+template <class F>
+__global__ void __launch_bounds__(256) ew_pair_kernel(u64 n, F f) {
+  pdl_enter();
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) f.both(i);
+}
+
 // Launch f(slot, i) for i in [0, n) and every local party slot, on `stream`.
 template <class F>
 void launch_ew(cudaStream_t stream, int nslots, u64 n, F f) {
   if (n == 0) return;
-  dim3 grid(ew_blocks(n), nslots);
   cudaEvent_t pe;
   probe_begin(stream, &pe);
-  launch_pdl(ew_kernel<F>, grid, dim3(256), 0, stream, n, f);
+  if constexpr (has_both<F>::value) {
+    if (nslots == 2 && pair_eval_enabled()) {
+      launch_pdl(ew_pair_kernel<F>, dim3(ew_blocks(n)), dim3(256), 0, stream, n, f);
+      probe_end(stream, pe);
+      return;
+    }
+  }
+  launch_pdl(ew_kernel<F>, dim3(ew_blocks(n), nslots), dim3(256), 0, stream, n, f);
   probe_end(stream, pe);
 }
 

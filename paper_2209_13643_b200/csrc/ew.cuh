@@ -69,12 +69,20 @@ struct MulBuild {
   u64 lo, w;
   XF xf;
   YF yf;
-  __device__ void operator()(int slot, u64 j) const {
+  __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
+  __device__ void both(u64 j) const { step<2>(0, j); }
+  template <int NS>
+  __device__ __forceinline__ void step(int slot0, u64 j) const {
     const u64 g = lo + j;
-    u64 a, b;
-    ew_ab(T, pid.v[slot], T.off + g, a, b);
-    own.p[slot][j] = xf(slot, g) - a;
-    own.p[slot][w + j] = yf(slot, g) - b;
+    const Dw d = ew_draw<false>(T, T.off + g, NS == 2 || pid.v[slot0] == 0);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const int slot = slot0 + k;
+      u64 a, b, c;
+      ew_share<false>(T, pid.v[slot], d, a, b, c);
+      own.p[slot][j] = xf(slot, g) - a;
+      own.p[slot][w + j] = yf(slot, g) - b;
+    }
   }
 };
 
@@ -85,18 +93,25 @@ struct MulCombine {
   CPtr2 own, peer;
   u64 lo, w;
   PF pf;
-  __device__ void operator()(int slot, u64 j) const {
-    const int party = pid.v[slot];
+  __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
+  __device__ void both(u64 j) const { step<2>(0, j); }
+  template <int NS>
+  __device__ __forceinline__ void step(int slot0, u64 j) const {
     const u64 g = lo + j;
-    const u64* o = own.p[slot];
-    const u64* q = peer.p[slot];
-    const u64 e = o[j] + q[j];
-    const u64 d = o[w + j] + q[w + j];
-    u64 a, b, c;
-    ew_abc(T, party, T.off + g, a, b, c);
-    u64 z = c + (e * b + d * a);
-    if (party == 0) z += e * d;
-    pf(slot, party, g, z);
+    const Dw dr = ew_draw<true>(T, T.off + g, NS == 2 || pid.v[slot0] == 0);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const int slot = slot0 + k, party = pid.v[slot];
+      const u64* o = own.p[slot];
+      const u64* q = peer.p[slot];
+      const u64 e = o[j] + q[j];
+      const u64 d = o[w + j] + q[w + j];
+      u64 a, b, c;
+      ew_share<true>(T, party, dr, a, b, c);
+      u64 z = c + (e * b + d * a);
+      if (party == 0) z += e * d;
+      pf(slot, party, g, z);
+    }
   }
 };
 
@@ -198,62 +213,93 @@ struct AdderRound {
   XF xf;
   YF yf;
   FF ff;
-  __device__ void operator()(int slot, u64 j) const {
-    const int party = pid.v[slot];
+  __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
+  __device__ void both(u64 j) const { step<2>(0, j); }
+
+  // NS party slots (slot0, slot0+1, ...) of element j; dealer draws are shared by the slots.
+  template <int NS>
+  __device__ __forceinline__ void step(int slot0, u64 j) const {
     const u64 g = lo + j;
+    const bool p0 = NS == 2 || pid.v[slot0] == 0;  // does any evaluated slot play party 0
+    u64 dummy;
     if (rn == 0) {  // issue the generate AND: payload [x^a | y^b]
-      const u64 x = xf(slot, g), y = yf(slot, g);
-      P0.p[slot][g] = x ^ y;
-      u64 a, b;
-      ew_ab(Tn, party, Tn.off + g, a, b);
-      ownn.p[slot][j] = x ^ a;
-      ownn.p[slot][w + j] = y ^ b;
+      const Dw dn = ew_draw<false>(Tn, Tn.off + g, p0);
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const int slot = slot0 + k;
+        const u64 x = xf(slot, g), y = yf(slot, g);
+        P0.p[slot][g] = x ^ y;
+        u64 a, b;
+        ew_share<false>(Tn, pid.v[slot], dn, a, b, dummy);
+        ownn.p[slot][j] = x ^ a;
+        ownn.p[slot][w + j] = y ^ b;
+      }
       return;
     }
-    const u64* q = peerp.p[slot];
-    u64 s, p;
+    u64 s[NS], p[NS];
     if (rp == 0) {  // settle the generate AND (H/protocols/adder.hpp:209-223)
-      const u64* o = ownp.p[slot];
-      const u64 e = o[j] ^ q[j], d = o[w + j] ^ q[w + j];
-      u64 a, b, c;
-      ew_abc(Tp, party, Tp.off + g, a, b, c);
-      s = c ^ (e & b) ^ (d & a);
-      if (party == 0) s ^= e & d;
-      p = P0.p[slot][g];
+      const Dw dp = ew_draw<true>(Tp, Tp.off + g, p0);
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const int slot = slot0 + k, party = pid.v[slot];
+        const u64* o = ownp.p[slot];
+        const u64* q = peerp.p[slot];
+        const u64 e = o[j] ^ q[j], d = o[w + j] ^ q[w + j];
+        u64 a, b, c;
+        ew_share<true>(Tp, party, dp, a, b, c);
+        s[k] = c ^ (e & b) ^ (d & a);
+        if (party == 0) s[k] ^= e & d;
+        p[k] = P0.p[slot][g];
+      }
     } else {  // settle a prefix level (H/protocols/adder.hpp:142-165)
       // Own payload is recomputed from the pre-round state instead of re-read from HBM:
       // it is a function of (s, p) and the triple, all of which this thread holds.
-      u64 a0, b0, c0, a1, b1, c1;
-      ew_abc(Tp, party, Tp.off + g, a0, b0, c0);
-      ew_abc(Tp, party, Tp.ghalf + Tp.off + g, a1, b1, c1);
-      const u64 s0 = S.p[slot][g], p0s = P.p[slot][g];
-      const u64 po = p0s & lp.out;
-      const u64 e0 = (po ^ a0) ^ q[j], e1 = (po ^ a1) ^ q[w + j];
-      const u64 d0 = (((s0 & lp.in) * lp.mult) ^ b0) ^ q[2 * w + j];
-      const u64 d1 = (((p0s & lp.in) * lp.mult) ^ b1) ^ q[3 * w + j];
-      u64 z0 = c0 ^ (e0 & b0) ^ (d0 & a0);
-      u64 z1 = c1 ^ (e1 & b1) ^ (d1 & a1);
-      if (party == 0) {
-        z0 ^= e0 & d0;
-        z1 ^= e1 & d1;
+      const Dw d0 = ew_draw<true>(Tp, Tp.off + g, p0), d1 = ew_draw<true>(Tp, Tp.ghalf + Tp.off + g, p0);
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const int slot = slot0 + k, party = pid.v[slot];
+        const u64* q = peerp.p[slot];
+        u64 a0, b0, c0, a1, b1, c1;
+        ew_share<true>(Tp, party, d0, a0, b0, c0);
+        ew_share<true>(Tp, party, d1, a1, b1, c1);
+        const u64 s0 = S.p[slot][g], p0s = P.p[slot][g];
+        const u64 po = p0s & lp.out;
+        const u64 e0 = (po ^ a0) ^ q[j], e1 = (po ^ a1) ^ q[w + j];
+        const u64 dd0 = (((s0 & lp.in) * lp.mult) ^ b0) ^ q[2 * w + j];
+        const u64 dd1 = (((p0s & lp.in) * lp.mult) ^ b1) ^ q[3 * w + j];
+        u64 z0 = c0 ^ (e0 & b0) ^ (dd0 & a0);
+        u64 z1 = c1 ^ (e1 & b1) ^ (dd1 & a1);
+        if (party == 0) {
+          z0 ^= e0 & dd0;
+          z1 ^= e1 & dd1;
+        }
+        s[k] = s0 ^ z0;
+        p[k] = (p0s & ~lp.out) ^ z1;
       }
-      s = s0 ^ z0;
-      p = (p0s & ~lp.out) ^ z1;
     }
     if (rn <= levels) {  // issue level rn-1 (H/protocols/adder.hpp:122-140)
-      const u64 p0 = p & ln.out;
-      u64 a0, b0, a1, b1;
-      ew_ab(Tn, party, Tn.off + g, a0, b0);
-      ew_ab(Tn, party, Tn.ghalf + Tn.off + g, a1, b1);
-      u64* nn = ownn.p[slot];
-      nn[j] = p0 ^ a0;
-      nn[w + j] = p0 ^ a1;
-      nn[2 * w + j] = ((s & ln.in) * ln.mult) ^ b0;
-      nn[3 * w + j] = ((p & ln.in) * ln.mult) ^ b1;
-      S.p[slot][g] = s;
-      P.p[slot][g] = p;
+      const Dw d0 = ew_draw<false>(Tn, Tn.off + g, p0), d1 = ew_draw<false>(Tn, Tn.ghalf + Tn.off + g, p0);
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const int slot = slot0 + k, party = pid.v[slot];
+        u64 a0, b0, a1, b1;
+        ew_share<false>(Tn, party, d0, a0, b0, dummy);
+        ew_share<false>(Tn, party, d1, a1, b1, dummy);
+        const u64 po = p[k] & ln.out;
+        u64* nn = ownn.p[slot];
+        nn[j] = po ^ a0;
+        nn[w + j] = po ^ a1;
+        nn[2 * w + j] = ((s[k] & ln.in) * ln.mult) ^ b0;
+        nn[3 * w + j] = ((p[k] & ln.in) * ln.mult) ^ b1;
+        S.p[slot][g] = s[k];
+        P.p[slot][g] = p[k];
+      }
     } else {
-      ff(slot, party, g, j, (P0.p[slot][g] ^ (s << 1)) & wmask);
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const int slot = slot0 + k;
+        ff(slot, pid.v[slot], g, j, (P0.p[slot][g] ^ (s[k] << 1)) & wmask);
+      }
     }
   }
 };
@@ -379,23 +425,25 @@ struct ChainParams {
   CR fin;        // select combine -> output sink
   u64 n;
   unsigned* bar;
+  int pair;      // one thread evaluates both local slots (grid y == 1)
 };
 
 template <class MR, class AR, class BR, class CR>
 __global__ void __launch_bounds__(256) chain_kernel(const __grid_constant__ ChainParams<MR, AR, BR, CR> p) {
   const int slot = blockIdx.y;
+  const bool pr = p.pair != 0;
   const unsigned nb = gridDim.x * gridDim.y;
   const u64 t0 = blockIdx.x * u64(blockDim.x) + threadIdx.x, st = u64(gridDim.x) * blockDim.x;
   unsigned ep = 0;
-  for (u64 g = t0; g < p.n; g += st) p.mask(slot, g);
+  for (u64 g = t0; g < p.n; g += st) eval_slots(p.mask, pr, slot, g);
   grid_barrier(p.bar, ++ep * nb);
   for (int r = 0; r < p.nadder; ++r) {
-    for (u64 g = t0; g < p.n; g += st) p.adder[r](slot, g);
+    for (u64 g = t0; g < p.n; g += st) eval_slots(p.adder[r], pr, slot, g);
     grid_barrier(p.bar, ++ep * nb);
   }
-  for (u64 g = t0; g < p.n; g += st) p.b2a(slot, g);
+  for (u64 g = t0; g < p.n; g += st) eval_slots(p.b2a, pr, slot, g);
   grid_barrier(p.bar, ++ep * nb);
-  for (u64 g = t0; g < p.n; g += st) p.fin(slot, g);
+  for (u64 g = t0; g < p.n; g += st) eval_slots(p.fin, pr, slot, g);
 }
 
 // Plain final sinks for adder_op (same functor for every lane).

@@ -407,6 +407,8 @@ void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const
   MPCG_CUDA(cudaMemsetAsync(bar.s[0], 0, 8, s.stream));
   p.n = n;
   p.bar = reinterpret_cast<unsigned*>(bar.s[0]);
+  p.pair = s.n_local == 2 && pair_eval_enabled();
+  const unsigned gy = p.pair ? 1u : unsigned(s.n_local);
 
   auto kern = chain_kernel<MaskRound<DF>, AR, BR, CR>;
   static int per_sm = -1;  // resident 256-thread CTAs per SM for this instantiation
@@ -414,11 +416,11 @@ void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const
     MPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
     if (per_sm < 1) throw Error(kInternalError, "chain kernel cannot be resident");
   }
-  const u64 cap = u64(per_sm) * kSms / u64(s.n_local);
+  const u64 cap = u64(per_sm) * kSms / gy;
   u64 blocks = (n + 255) / 256;  // one element per thread per round (the rounds are PRG-latency bound)
   blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);
   cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(unsigned(blocks), unsigned(s.n_local));
+  lc.gridDim = dim3(unsigned(blocks), gy);
   lc.blockDim = dim3(256);
   lc.stream = s.stream;
   cudaLaunchAttribute attr{};
