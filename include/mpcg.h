@@ -120,6 +120,14 @@ int mpcg_softmax(mpcg_session* s, const mpcg_tensor* x, uint64_t L, const char* 
                  mpcg_tensor** out);                                           /* activations.hpp:93 */
 int mpcg_maxpool2d(mpcg_session* s, const mpcg_tensor* x, uint64_t N, uint64_t C, uint64_t H, uint64_t W,
                    uint64_t k, uint64_t stride, const char* tag, mpcg_tensor** out); /* activations.hpp:114 */
+/* Extensions (not in the reference, built from its blocks; oracle/mpc_oracle.py restates them). */
+int mpcg_sigmoid(mpcg_session* s, const mpcg_tensor* x, const char* tag, mpcg_tensor** out);
+int mpcg_gelu(mpcg_session* s, const mpcg_tensor* x, const char* tag, mpcg_tensor** out);
+int mpcg_inv_sqrt(mpcg_session* s, const mpcg_tensor* v, const char* tag, int newton_iters, mpcg_tensor** out);
+int mpcg_layernorm(mpcg_session* s, const mpcg_tensor* x, uint64_t d, const mpcg_tensor* gamma,
+                   const mpcg_tensor* beta, int public_weights, const char* tag, mpcg_tensor** out);
+int mpcg_global_avg_pool(mpcg_session* s, const mpcg_tensor* x, uint64_t N, uint64_t C, uint64_t HW,
+                         mpcg_tensor** out);
 
 /* ---- model + executor (engine/model.hpp, engine/executor.hpp:173-205) ---- */
 #define MPCG_LAYER_DENSE 0
@@ -130,9 +138,20 @@ int mpcg_maxpool2d(mpcg_session* s, const mpcg_tensor* x, uint64_t N, uint64_t C
 #define MPCG_LAYER_ATTENTION 5
 #define MPCG_LAYER_SOFTMAX 6
 #define MPCG_LAYER_MEANPOOL 7
+/* Extensions (not in the reference; needed by the ResNet-18 / BERT-base configs). */
+#define MPCG_LAYER_ADD 8
+#define MPCG_LAYER_GLOBAL_AVG_POOL 9
+#define MPCG_LAYER_GELU 10
+#define MPCG_LAYER_LAYERNORM 11
 int mpcg_model_create(const char* name, int frac_bits, int ndim, const uint64_t* input_dims, mpcg_model** out);
 int mpcg_model_add_layer(mpcg_model* m, const char* name, int kind, uint64_t out, uint64_t kernel,
                          uint64_t stride, uint64_t pad, uint64_t heads, int bias);
+/* Extension: add_layer with wiring — `from` = the layer whose output it reads (NULL/"" = the
+ * previous layer, "input" = the model input), `with_` = an ADD's second operand. (The
+ * reference's models are chains, engine/model.hpp:18-20; add_layer == add_layer_ex(.., 0, 0).) */
+int mpcg_model_add_layer_ex(mpcg_model* m, const char* name, int kind, uint64_t out, uint64_t kernel,
+                            uint64_t stride, uint64_t pad, uint64_t heads, int bias, const char* from,
+                            const char* with_);
 int mpcg_model_destroy(mpcg_model* m);
 /* ExecOptions (engine/executor.hpp:28-36). */
 int mpcg_executor_create(mpcg_session* s, const mpcg_model* m, int public_weights, int pipelined, int chunks,

@@ -581,10 +581,109 @@ def maxpool2d_shares(X, N, C, H, W, k, s, ctx: Ctx, tag="maxpool"):
     return [m.reshape(N, C, OH, OW) for m in mx]
 
 
+# ---------------------------------------------------------------- extensions (NOT in the reference)
+# Layers the BASELINE configs need that the reference lacks (SURVEY §0, §8(a*), §8f row 1):
+# GeLU and LayerNorm (BERT-base), residual add and global average pooling (ResNet-18; BatchNorm
+# is folded into the conv weights/bias by the weight owner). They are composed only from the
+# reference's own building blocks — beaver_mul/square, msb/b2a_bit (compare.hpp), exp_shares /
+# reciprocal_shares (approx.hpp), local truncation — with tags "<layer>.<step>" in the style of
+# relu_shares/softmax_shares. PARITY UNPINNED by the reference (it has no such layers): the GPU
+# path is held bit-exact to THIS restatement, and decoded values to the float64 forward below.
+
+GELU_K = 1.702        # GeLU(x) ~= x * sigmoid(1.702 x)  (the sigmoid form of Hendrycks & Gimpel)
+LN_EPS = 1e-5
+ISQRT_ITERS = 3
+
+
+def scale_rescale(X, c, f):
+    """H/engine/executor.hpp:326-330 (scale_and_rescale) as a free function."""
+    k = encode_fixed(c, f)
+    return truncate_shares([x * k for x in X], f)
+
+
+def sigmoid_shares(X, ctx: Ctx, tag="sigmoid"):
+    """sigma(x) = b ? 1 - sigma(|x|) : sigma(|x|), b = [x < 0], sigma(|x|) = 1/(1 + exp(-|x|)).
+    exp only ever sees -|x| <= 0 (exp_shares' accurate side, H/nonlinear/approx.hpp:22-39) and the
+    reciprocal only (1, 2] (inside reciprocal_shares' convergence range, approx.hpp:43-62)."""
+    f = ctx.frac_bits
+    ch = ctx.chunks_for(X[0].size)
+    s = msb(X, ctx, tag + ".msb", ch)
+    b = b2a_bit(s, ctx, tag + ".b2a", ch)
+    xb = beaver_mul(X, b, ctx, tag + ".abs", ch)
+    nabs = [(xb[p] + xb[p]) - X[p] for p in range(2)]                 # -|x|
+    e = exp_shares(nabs, ctx, tag + ".exp")
+    r = reciprocal_shares(add_public(e, 1 << f), ctx, tag + ".recip")  # sigma(|x|)
+    t = add_public([U64(0) - (r[p] + r[p]) for p in range(2)], 1 << f)  # 1 - 2 sigma(|x|)
+    sel = beaver_mul(b, t, ctx, tag + ".sel", ch)                      # b has scale 0: no truncation
+    return [r[p] + sel[p] for p in range(2)]
+
+
+def gelu_shares(X, ctx: Ctx, tag="gelu"):
+    f = ctx.frac_bits
+    ch = ctx.chunks_for(X[0].size)
+    z = scale_rescale(X, GELU_K, f)
+    sg = sigmoid_shares(z, ctx, tag + ".sig")
+    return truncate_shares(beaver_mul(X, sg, ctx, tag + ".out", ch), f)
+
+
+def inv_sqrt_shares(V, ctx: Ctx, tag="isqrt", newton_iters=ISQRT_ITERS):
+    """1/sqrt(v): seed y0 = 2.2 exp(-(v/2 + 0.2)) + 0.2 - v/1024, then Newton
+    y <- y (3 - v y^2) / 2 (CrypTen's inv_sqrt recipe; accurate for v in ~[0.1, 200])."""
+    f = ctx.frac_bits
+    ch = ctx.chunks_for(V[0].size)
+    t = add_public([U64(0) - sar(V[p], 1) for p in range(2)], -int(encode_fixed(0.2, f)))
+    e = exp_shares(t, ctx, tag + ".seed")
+    y = scale_rescale(e, 2.2, f)
+    y = add_public([y[p] - sar(V[p], 10) for p in range(2)], int(encode_fixed(0.2, f)))
+    three = int(encode_fixed(3.0, f))
+    for i in range(newton_iters):
+        y2 = truncate_shares(beaver_square(y, ctx, f"{tag}.y2{i}", ch), f)
+        vy2 = truncate_shares(beaver_mul(V, y2, ctx, f"{tag}.vy{i}", ch), f)
+        u = add_public([U64(0) - vy2[p] for p in range(2)], three)
+        y = truncate_shares(beaver_mul(y, u, ctx, f"{tag}.yu{i}", ch), f + 1)   # /2 folded in
+    return y
+
+
+def layernorm_shares(X, d, gamma, beta, ctx: Ctx, tag="ln", public=False):
+    """LayerNorm over the last dim: (x - mean) * inv_sqrt(var + eps) * gamma + beta.
+    gamma/beta: [share0, share1] of [d] (private) or encoded plaintext [d] (public)."""
+    f = ctx.frac_bits
+    shape = X[0].shape
+    rows = X[0].size // d
+    ch = ctx.chunks_for(X[0].size)
+    x = [v.reshape(rows, d) for v in X]
+    mu = scale_rescale([v.sum(axis=1, keepdims=True, dtype=U64) for v in x], 1.0 / d, f)
+    c = [x[p] - mu[p] for p in range(2)]
+    sq = truncate_shares(beaver_square(c, ctx, tag + ".sq", ch), f)
+    var = scale_rescale([v.sum(axis=1, keepdims=True, dtype=U64) for v in sq], 1.0 / d, f)
+    var = add_public(var, int(encode_fixed(LN_EPS, f)))
+    y = inv_sqrt_shares(var, ctx, tag + ".isqrt")
+    yb = [np.broadcast_to(y[p], (rows, d)).copy() for p in range(2)]
+    n = truncate_shares(beaver_mul(c, yb, ctx, tag + ".norm", ch), f)
+    if public:
+        out = truncate_shares([v * gamma[None, :] for v in n], f)
+        out = [out[0] + beta[None, :], out[1]]
+    else:
+        gb = [np.broadcast_to(gamma[p][None, :], (rows, d)).copy() for p in range(2)]
+        out = truncate_shares(beaver_mul(n, gb, ctx, tag + ".gamma", ch), f)
+        out = [out[p] + beta[p][None, :] for p in range(2)]
+    return [o.reshape(shape) for o in out]
+
+
+def global_avg_pool(X, in_shape, f):
+    """NCHW -> [N, C]: sum over H*W then scale_and_rescale(1/(H*W)) (as MeanPool,
+    H/engine/executor.hpp:399-410)."""
+    N, C, H, W = in_shape
+    s = [x.reshape(N, C, H * W).sum(axis=2, dtype=U64) for x in X]
+    return scale_rescale(s, 1.0 / (H * W), f)
+
+
 # ---------------------------------------------------------------- engine
 # H/engine/model.hpp, H/engine/executor.hpp.
 
-LAYER_KINDS = ("dense", "conv2d", "relu", "maxpool2d", "flatten", "attention", "softmax", "mean_pool")
+LAYER_KINDS = ("dense", "conv2d", "relu", "maxpool2d", "flatten", "attention", "softmax", "mean_pool",
+               # extensions for the ResNet-18 / BERT-base configs (absent from the reference)
+               "add", "global_avg_pool", "gelu", "layernorm")
 
 
 @dataclass
@@ -597,6 +696,8 @@ class Layer:
     pad: int = 0
     heads: int = 0
     bias: bool = True
+    src: str = ""      # extension: "from" — input is this earlier layer's output ("input" = model input)
+    other: str = ""    # extension: "with" — second operand of an "add"
 
 
 @dataclass
@@ -617,18 +718,50 @@ def model_from_json(j: dict) -> Model:
             raise ValueError("unknown layer type: " + t)
         layers.append(Layer(lj.get("name", t), t, int(lj.get("out", 0)), int(lj.get("kernel", 0)),
                             int(lj.get("stride", 1)), int(lj.get("pad", 0)), int(lj.get("heads", 0)),
-                            bool(lj.get("bias", True))))
+                            bool(lj.get("bias", True)), str(lj.get("from", "")), str(lj.get("with", ""))))
     m = Model(j.get("name", "model"), fb, tuple(int(d) for d in j["input"]), layers)
     infer_shapes(m)
     return m
 
 
+def layer_inputs(g: Model):
+    """Extension (non-chain graphs): index of each layer's input producer (-1 = model input)
+    and of an "add"'s second operand. The reference only has chains (H/engine/model.hpp:18-20)."""
+    names = {}
+    src, oth = [], []
+    for i, l in enumerate(g.layers):
+        def look(n):
+            if n == "input":
+                return -1
+            if n not in names:
+                raise ValueError(f"{l.name}: unknown or later layer '{n}'")
+            return names[n]
+        src.append(look(l.src) if l.src else i - 1)
+        if l.type == "add":
+            if not l.other:
+                raise ValueError(f"{l.name}: add needs 'with'")
+            oth.append(look(l.other))
+        else:
+            oth.append(None)
+        if l.name in names:
+            raise ValueError("duplicate layer name: " + l.name)
+        names[l.name] = i
+    return src, oth
+
+
 def infer_shapes(g: Model):
-    """H/engine/model.hpp:69-122."""
+    """H/engine/model.hpp:69-122 (+ the extension layers)."""
     out = []
-    cur = list(g.input)
-    for l in g.layers:
-        if l.type == "dense":
+    src, oth = layer_inputs(g)
+    for i, l in enumerate(g.layers):
+        cur = list(g.input if src[i] < 0 else out[src[i]])
+        if l.type == "add":
+            other = list(g.input if oth[i] < 0 else out[oth[i]])
+            if other != cur:
+                raise ValueError(f"{l.name}: add operand shapes differ {cur} vs {other}")
+        elif l.type == "global_avg_pool":
+            cur = [cur[0], cur[1]]
+        elif l.type == "dense":
             cur[-1] = l.out
         elif l.type == "conv2d":
             h, w = cur[2], cur[3]
@@ -665,16 +798,17 @@ def layer_weight_shapes(l: Layer, in_shape):
         if l.bias:
             r.append((l.name + ".bo", (d,)))
         return r
+    if l.type == "layernorm":  # extension: affine LayerNorm over the last dim
+        return [(l.name + ".gamma", (in_shape[-1],)), (l.name + ".beta", (in_shape[-1],))]
     return []
 
 
 def model_weight_shapes(g: Model):
     shapes = infer_shapes(g)
+    src, _ = layer_inputs(g)
     out = []
-    cur = g.input
     for i, l in enumerate(g.layers):
-        out += layer_weight_shapes(l, cur)
-        cur = shapes[i]
+        out += layer_weight_shapes(l, g.input if src[i] < 0 else shapes[src[i]])
     return out
 
 
@@ -690,6 +824,8 @@ def init_weights(g: Model, seed: int) -> dict:
         span = 1.0 / math.sqrt(float(shape[0])) if len(shape) >= 2 else 0.1
         u = _unit_doubles(rng, int(np.prod(shape)))
         w[key] = ((2.0 * u - 1.0) * span).reshape(shape)
+        if key.endswith(".gamma"):  # extension: LayerNorm scale centred on 1
+            w[key] = w[key] + 1.0
     return w
 
 
@@ -831,15 +967,30 @@ class SecureExecutor:
             B, T, d = in_shape
             s = [x.reshape(B, T, d).sum(axis=1, dtype=U64) for x in X]
             return self.scale_and_rescale(s, 1.0 / T)
+        if l.type == "global_avg_pool":
+            return global_avg_pool(X, in_shape, self.g.frac_bits)
+        if l.type == "gelu":
+            return gelu_shares(X, self.ctx, l.name)
+        if l.type == "layernorm":
+            return layernorm_shares(X, in_shape[-1], self.w[l.name + ".gamma"], self.w[l.name + ".beta"],
+                                    self.ctx, l.name, self.public)
         raise ValueError(l.type)
 
     def run(self, X):
-        cur = X
-        shape = self.g.input
+        """Chain order as the reference (H/engine/executor.hpp:193-205); the extension's
+        "from"/"with" read earlier outputs (an "add" is a local share addition)."""
+        src, oth = layer_inputs(self.g)
+        outs = []
         for i, l in enumerate(self.g.layers):
-            cur = self.run_layer(l, cur, shape)
-            shape = self.shapes[i]
-        return cur
+            x = X if src[i] < 0 else outs[src[i]]
+            shape = self.g.input if src[i] < 0 else self.shapes[src[i]]
+            if l.type == "add":
+                y = X if oth[i] < 0 else outs[oth[i]]
+                cur = [x[p] + y[p] for p in range(2)]
+            else:
+                cur = self.run_layer(l, x, shape)
+            outs.append(cur)
+        return outs[-1]
 
 
 def bench_party_values(g: Model, seed: int = 1, iterations: int = 1, public: bool = False,
@@ -864,11 +1015,25 @@ def bench_party_values(g: Model, seed: int = 1, iterations: int = 1, public: boo
 # ---------------------------------------------------------------- plaintext reference
 def reference_forward(g: Model, w: dict, x: np.ndarray) -> np.ndarray:
     """Double-precision forward of H/engine/reference.hpp:128-200."""
-    cur = np.asarray(x, dtype=np.float64)
-    shape = g.input
+    x0 = np.asarray(x, dtype=np.float64)
     shapes = infer_shapes(g)
+    src, oth = layer_inputs(g)
+    outs = []
     for i, l in enumerate(g.layers):
-        if l.type == "dense":
+        cur = x0 if src[i] < 0 else outs[src[i]]
+        shape = g.input if src[i] < 0 else shapes[src[i]]
+        if l.type == "add":
+            cur = cur + (x0 if oth[i] < 0 else outs[oth[i]])
+        elif l.type == "global_avg_pool":
+            cur = cur.reshape(shape).mean(axis=(2, 3))
+        elif l.type == "gelu":
+            cur = cur / (1.0 + np.exp(-GELU_K * cur))
+        elif l.type == "layernorm":
+            v = cur.reshape(-1, shape[-1])
+            mu = v.mean(axis=1, keepdims=True)
+            var = ((v - mu) ** 2).mean(axis=1, keepdims=True)
+            cur = (v - mu) / np.sqrt(var + LN_EPS) * w[l.name + ".gamma"] + w[l.name + ".beta"]
+        elif l.type == "dense":
             cur = cur.reshape(-1, shape[-1]) @ w[l.name + ".W"]
             if l.bias:
                 cur = cur + w[l.name + ".b"]
@@ -906,6 +1071,6 @@ def reference_forward(g: Model, w: dict, x: np.ndarray) -> np.ndarray:
             if l.bias:
                 o = o + w[l.name + ".bo"]
             cur = o
-        shape = shapes[i]
-        cur = cur.reshape(shape)
-    return cur
+        cur = cur.reshape(shapes[i])
+        outs.append(cur)
+    return outs[-1]

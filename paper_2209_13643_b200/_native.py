@@ -80,6 +80,12 @@ SIGNATURES = {
     "mpcg_maxpool2d": [P, P, U64, U64, U64, U64, U64, U64, STR, PP],
     "mpcg_model_create": [STR, I32, I32, U64P, PP],
     "mpcg_model_add_layer": [P, STR, I32, U64, U64, U64, U64, U64, I32],
+    "mpcg_model_add_layer_ex": [P, STR, I32, U64, U64, U64, U64, U64, I32, STR, STR],
+    "mpcg_sigmoid": [P, P, STR, PP],
+    "mpcg_gelu": [P, P, STR, PP],
+    "mpcg_inv_sqrt": [P, P, STR, I32, PP],
+    "mpcg_layernorm": [P, P, U64, P, P, I32, STR, PP],
+    "mpcg_global_avg_pool": [P, P, U64, U64, U64, PP],
     "mpcg_model_destroy": [P],
     "mpcg_executor_create": [P, P, I32, I32, I32, U64, I32, PP],
     "mpcg_executor_deal_weights": [P, I32, C.POINTER(C.c_char_p), C.POINTER(C.POINTER(DBL)), U64],

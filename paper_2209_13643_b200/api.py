@@ -226,6 +226,27 @@ def maxpool2d_shares(s, x, N_, C_, H, W, k, stride, tag="maxpool"):
     return _op("mpcg_maxpool2d", s, x.handle, N_, C_, H, W, k, stride, _tag(tag))
 
 
+# ---- extensions (not in the reference; restated in oracle/mpc_oracle.py) ----
+def sigmoid_shares(s, x, tag="sigmoid"):
+    return _op("mpcg_sigmoid", s, x.handle, _tag(tag))
+
+
+def gelu_shares(s, x, tag="gelu"):
+    return _op("mpcg_gelu", s, x.handle, _tag(tag))
+
+
+def inv_sqrt_shares(s, v, tag="isqrt", newton_iters=3):
+    return _op("mpcg_inv_sqrt", s, v.handle, _tag(tag), newton_iters)
+
+
+def layernorm_shares(s, x, d, gamma, beta, public=False, tag="ln"):
+    return _op("mpcg_layernorm", s, x.handle, d, gamma.handle, beta.handle, int(public), _tag(tag))
+
+
+def global_avg_pool(s, x, N_, C_, HW):
+    return _op("mpcg_global_avg_pool", s, x.handle, N_, C_, HW)
+
+
 def set_gemm_mode(mode: str = "auto"):
     """Ring-GEMM engine: "simt", "tc" (tcgen05 int8 limbs wherever exact) or "auto"."""
     N.call("mpcg_set_gemm_mode", {"simt": 0, "tc": 1, "auto": 2}[mode])
@@ -302,8 +323,8 @@ class SecureExecutor:
         N.call("mpcg_model_create", g.name.encode(), g.frac_bits, len(g.input), _u64p(dims), C.byref(mh))
         try:
             for l in g.layers:
-                N.call("mpcg_model_add_layer", mh, l.name.encode(), LAYER_KINDS[l.type], l.out, l.kernel,
-                       l.stride, l.pad, l.heads, int(l.bias))
+                N.call("mpcg_model_add_layer_ex", mh, l.name.encode(), LAYER_KINDS[l.type], l.out, l.kernel,
+                       l.stride, l.pad, l.heads, int(l.bias), l.src.encode(), l.other.encode())
             eh = C.c_void_p()
             N.call("mpcg_executor_create", sess.handle, mh, int(public_weights), int(pipelined), chunks,
                    chunk_threshold, int(merged_adder), C.byref(eh))

@@ -303,6 +303,24 @@ int mpcg_maxpool2d(mpcg_session* s, const mpcg_tensor* x, uint64_t N, uint64_t C
   OP1(maxpool2d_shares(ss, T(x), N, C, H, W, k, stride, tagstr(tag)));
 }
 
+int mpcg_sigmoid(mpcg_session* s, const mpcg_tensor* x, const char* tag, mpcg_tensor** out) {
+  OP1(sigmoid_shares(ss, T(x), tagstr(tag)));
+}
+int mpcg_gelu(mpcg_session* s, const mpcg_tensor* x, const char* tag, mpcg_tensor** out) {
+  OP1(gelu_shares(ss, T(x), tagstr(tag)));
+}
+int mpcg_inv_sqrt(mpcg_session* s, const mpcg_tensor* v, const char* tag, int newton_iters, mpcg_tensor** out) {
+  OP1(inv_sqrt_shares(ss, T(v), tagstr(tag), newton_iters));
+}
+int mpcg_layernorm(mpcg_session* s, const mpcg_tensor* x, uint64_t d, const mpcg_tensor* gamma,
+                   const mpcg_tensor* beta, int public_weights, const char* tag, mpcg_tensor** out) {
+  OP1(layernorm_shares(ss, T(x), d, T(gamma), T(beta), public_weights != 0, tagstr(tag)));
+}
+int mpcg_global_avg_pool(mpcg_session* s, const mpcg_tensor* x, uint64_t N, uint64_t C, uint64_t HW,
+                         mpcg_tensor** out) {
+  OP1(global_avg_pool(ss, T(x), N, C, HW));
+}
+
 int mpcg_model_create(const char* name, int frac_bits, int ndim, const uint64_t* dims, mpcg_model** out) {
   return guard([&] {
     need(out, "out");
@@ -315,11 +333,12 @@ int mpcg_model_create(const char* name, int frac_bits, int ndim, const uint64_t*
   });
 }
 
-int mpcg_model_add_layer(mpcg_model* m, const char* name, int kind, uint64_t outc, uint64_t kernel, uint64_t stride,
-                         uint64_t pad, uint64_t heads, int bias) {
+int mpcg_model_add_layer_ex(mpcg_model* m, const char* name, int kind, uint64_t outc, uint64_t kernel,
+                            uint64_t stride, uint64_t pad, uint64_t heads, int bias, const char* from,
+                            const char* with_) {
   return guard([&] {
     need(m, "model");
-    if (kind < 0 || kind > MPCG_LAYER_MEANPOOL) throw Error(kConfigError, "unknown layer kind");
+    if (kind < 0 || kind > MPCG_LAYER_LAYERNORM) throw Error(kConfigError, "unknown layer kind");
     LayerSpec l;
     l.name = tagstr(name);
     l.kind = static_cast<LayerKind>(kind);
@@ -329,9 +348,21 @@ int mpcg_model_add_layer(mpcg_model* m, const char* name, int kind, uint64_t out
     l.pad = pad;
     l.heads = heads;
     l.bias = bias != 0;
+    l.from = from ? from : "";
+    l.with = with_ ? with_ : "";
     m->g.layers.push_back(l);
-    infer_shapes(m->g);  // validate (H/engine/model.hpp:177)
+    try {
+      infer_shapes(m->g);  // validate (H/engine/model.hpp:177)
+    } catch (...) {
+      m->g.layers.pop_back();
+      throw;
+    }
   });
+}
+
+int mpcg_model_add_layer(mpcg_model* m, const char* name, int kind, uint64_t outc, uint64_t kernel, uint64_t stride,
+                         uint64_t pad, uint64_t heads, int bias) {
+  return mpcg_model_add_layer_ex(m, name, kind, outc, kernel, stride, pad, heads, bias, nullptr, nullptr);
 }
 
 int mpcg_model_destroy(mpcg_model* m) {

@@ -281,6 +281,17 @@ DT maxpool2d_shares(Session& s, const DT& x, size_t N, size_t C, size_t H, size_
                     size_t stride, const std::string& tag = "maxpool");
 DT open_value(Session& s, const DT& x, Reduce kind, const std::string& tag);  // reveal, every slot gets it
 
+// Extensions the ResNet-18 / BERT-base configs need and the reference lacks (ext.cu;
+// restated in oracle/mpc_oracle.py, parity unpinned by the reference).
+constexpr double kLnEps = 1e-5;
+constexpr int kIsqrtIters = 3;
+DT sigmoid_shares(Session& s, const DT& x, const std::string& tag = "sigmoid");
+DT gelu_shares(Session& s, const DT& x, const std::string& tag = "gelu");
+DT inv_sqrt_shares(Session& s, const DT& v, const std::string& tag = "isqrt", int newton_iters = kIsqrtIters);
+DT layernorm_shares(Session& s, const DT& x, size_t d, const DT& gamma, const DT& beta, bool public_weights,
+                    const std::string& tag = "ln");
+DT global_avg_pool(Session& s, const DT& x, size_t N, size_t C, size_t HW);
+
 // local tensor helpers (fused into producers where it matters)
 DT add_public(Session& s, const DT& x, u64 v);     // party 0 absorbs
 DT scale_public(Session& s, const DT& x, u64 k);

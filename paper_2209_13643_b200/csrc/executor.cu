@@ -10,12 +10,53 @@
 
 namespace mpcg {
 
+LayerWiring layer_wiring(const ModelGraph& g) {
+  // The reference's graphs are chains (H/engine/model.hpp:18-20); the extension lets a layer
+  // read an earlier output ("from") and an Add combine two ("with").
+  LayerWiring w;
+  std::map<std::string, long> names;
+  for (size_t i = 0; i < g.layers.size(); ++i) {
+    const LayerSpec& l = g.layers[i];
+    auto look = [&](const std::string& n) -> long {
+      if (n == "input") return -1;
+      auto it = names.find(n);
+      if (it == names.end()) throw Error(kConfigError, l.name + ": unknown or later layer '" + n + "'");
+      return it->second;
+    };
+    w.src.push_back(l.from.empty() ? long(i) - 1 : look(l.from));
+    if (l.kind == LayerKind::Add) {
+      if (l.with.empty()) throw Error(kConfigError, l.name + ": add needs 'with'");
+      w.other.push_back(look(l.with));
+    } else {
+      w.other.push_back(-2);
+    }
+    if (!names.emplace(l.name, long(i)).second) throw Error(kConfigError, "duplicate layer name: " + l.name);
+  }
+  return w;
+}
+
 std::vector<Shape> infer_shapes(const ModelGraph& g) {
-  // H/engine/model.hpp:69-122
+  // H/engine/model.hpp:69-122 (+ the extension layers)
   std::vector<Shape> out;
-  Shape cur = g.input;
-  for (const LayerSpec& l : g.layers) {
+  const LayerWiring wr = layer_wiring(g);
+  for (size_t li = 0; li < g.layers.size(); ++li) {
+    const LayerSpec& l = g.layers[li];
+    Shape cur = wr.src[li] < 0 ? g.input : out[size_t(wr.src[li])];
     switch (l.kind) {
+      case LayerKind::Add: {
+        const Shape& o = wr.other[li] < 0 ? g.input : out[size_t(wr.other[li])];
+        if (o != cur) throw Error(kConfigError, l.name + ": add operand shapes differ");
+        break;
+      }
+      case LayerKind::GlobalAvgPool:
+        if (cur.size() != 4) throw Error(kConfigError, l.name + ": global_avg_pool expects NCHW input");
+        cur = {cur[0], cur[1]};
+        break;
+      case LayerKind::Gelu:
+        break;
+      case LayerKind::LayerNorm:
+        if (cur.empty()) throw Error(kConfigError, l.name + ": layernorm needs a trailing feature dim");
+        break;
       case LayerKind::Dense:
         if (cur.empty()) throw Error(kConfigError, l.name + ": dense needs a trailing feature dim");
         cur.back() = l.out;
@@ -64,10 +105,14 @@ std::vector<std::pair<std::string, Shape>> model_weight_shapes(const ModelGraph&
   // H/engine/model.hpp:213-252
   std::vector<std::pair<std::string, Shape>> out;
   const auto shapes = infer_shapes(g);
-  Shape cur = g.input;
+  const LayerWiring wr = layer_wiring(g);
   for (size_t i = 0; i < g.layers.size(); ++i) {
     const LayerSpec& l = g.layers[i];
-    if (l.kind == LayerKind::Dense) {
+    const Shape& cur = wr.src[i] < 0 ? g.input : shapes[size_t(wr.src[i])];
+    if (l.kind == LayerKind::LayerNorm) {  // extension
+      out.push_back({l.name + ".gamma", Shape{cur.back()}});
+      out.push_back({l.name + ".beta", Shape{cur.back()}});
+    } else if (l.kind == LayerKind::Dense) {
       out.push_back({l.name + ".W", Shape{cur.back(), l.out}});
       if (l.bias) out.push_back({l.name + ".b", Shape{l.out}});
     } else if (l.kind == LayerKind::Conv2d) {
@@ -80,7 +125,6 @@ std::vector<std::pair<std::string, Shape>> model_weight_shapes(const ModelGraph&
       out.push_back({l.name + ".Wo", Shape{d, d}});
       if (l.bias) out.push_back({l.name + ".bo", Shape{d}});
     }
-    cur = shapes[i];
   }
   return out;
 }
@@ -121,9 +165,10 @@ void SecureExecutor::add_weight_op(const std::string& tag, const std::string& wk
 
 void SecureExecutor::build_weight_ops() {
   // H/engine/executor.hpp:244-273
-  Shape cur = g_.input;
+  const LayerWiring wr = layer_wiring(g_);
   for (size_t i = 0; i < g_.layers.size(); ++i) {
     const LayerSpec& l = g_.layers[i];
+    const Shape& cur = wr.src[i] < 0 ? g_.input : shapes_[size_t(wr.src[i])];
     switch (l.kind) {
       case LayerKind::Dense: {
         const size_t in = cur.back();
@@ -146,7 +191,6 @@ void SecureExecutor::build_weight_ops() {
       default:
         break;
     }
-    cur = shapes_[i];
   }
 }
 
@@ -392,6 +436,15 @@ DT SecureExecutor::run_layer(const LayerSpec& l, const DT& x, const Shape& in_sh
       });
       return out;
     }
+    case LayerKind::GlobalAvgPool:
+      return global_avg_pool(s_, x, in_shape[0], in_shape[1], in_shape[2] * in_shape[3]);
+    case LayerKind::Gelu:
+      return gelu_shares(s_, x, l.name);
+    case LayerKind::LayerNorm:
+      return layernorm_shares(s_, x, in_shape.back(), w_.at(l.name + ".gamma"), w_.at(l.name + ".beta"), public_,
+                              l.name);
+    case LayerKind::Add:
+      break;  // needs both operands: handled in run()
   }
   throw Error(kProtocolError, "unhandled layer kind");
 }
@@ -439,17 +492,34 @@ DT SecureExecutor::run(const DT& input) {
     ev_.assign(g_.layers.size() + 1, nullptr);
     for (auto& e : ev_) MPCG_CUDA(cudaEventCreate(&e));
   }
-  DT cur = input;
-  Shape cur_shape = g_.input;
   const unsigned rec_flags = s_.cap.active ? cudaEventRecordExternal : cudaEventRecordDefault;  // graph event nodes
   if (time_layers) MPCG_CUDA(cudaEventRecordWithFlags(ev_[0], s_.stream, rec_flags));
-  for (size_t i = 0; i < g_.layers.size(); ++i) {
-    cur = run_layer(g_.layers[i], cur, cur_shape);
-    cur_shape = shapes_[i];
+  // Layers run in list order (the reference's chain order, executor.hpp:193-205); an output
+  // is kept only until its last reader ("from"/"with" of a later layer) has run.
+  const LayerWiring wr = layer_wiring(g_);
+  const size_t nl = g_.layers.size();
+  std::vector<size_t> last(nl, 0);
+  for (size_t i = 0; i < nl; ++i) {
+    last[i] = i + 1 < nl ? i + 1 : i;
+    if (wr.src[i] >= 0) last[size_t(wr.src[i])] = std::max(last[size_t(wr.src[i])], i);
+    if (wr.other[i] >= 0) last[size_t(wr.other[i])] = std::max(last[size_t(wr.other[i])], i);
+  }
+  std::vector<DT> outs(nl);
+  for (size_t i = 0; i < nl; ++i) {
+    const LayerSpec& l = g_.layers[i];
+    const DT& x = wr.src[i] < 0 ? input : outs[size_t(wr.src[i])];
+    const Shape& xs = wr.src[i] < 0 ? g_.input : shapes_[size_t(wr.src[i])];
+    if (l.kind == LayerKind::Add) {  // residual: local share addition
+      outs[i] = add_t(s_, x, wr.other[i] < 0 ? input : outs[size_t(wr.other[i])]);
+    } else {
+      outs[i] = run_layer(l, x, xs);
+    }
     if (time_layers) MPCG_CUDA(cudaEventRecordWithFlags(ev_[i + 1], s_.stream, rec_flags));
+    for (size_t j = 0; j < i; ++j)
+      if (outs[j] && last[j] <= i) outs[j] = DT{};
   }
   if (time_layers && !s_.cap.active) collect_timings();  // captured: event nodes, read after replay
-  return cur;
+  return outs[nl - 1];
 }
 
 void SecureExecutor::collect_timings() {

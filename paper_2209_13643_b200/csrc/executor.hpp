@@ -7,13 +7,20 @@
 
 namespace mpcg {
 
-enum class LayerKind : int { Dense = 0, Conv2d, Relu, Maxpool2d, Flatten, Attention, Softmax, MeanPool };
+// Dense..MeanPool are the reference's kinds (H/engine/model.hpp:21); Add..LayerNorm are the
+// extensions the ResNet-18 / BERT-base configs need (not in the reference, see ext.cu).
+enum class LayerKind : int {
+  Dense = 0, Conv2d, Relu, Maxpool2d, Flatten, Attention, Softmax, MeanPool,
+  Add, GlobalAvgPool, Gelu, LayerNorm
+};
 
 struct LayerSpec {
   std::string name;
   LayerKind kind = LayerKind::Dense;
   size_t out = 0, kernel = 0, stride = 1, pad = 0, heads = 0;
   bool bias = true;
+  std::string from;  // extension: input = this earlier layer's output ("input" = model input)
+  std::string with;  // extension: second operand of Add
 };
 
 struct ModelGraph {
@@ -22,6 +29,13 @@ struct ModelGraph {
   Shape input;  // leading dim is the batch
   std::vector<LayerSpec> layers;
 };
+
+// Producer index of each layer's input (-1 = model input) and of an Add's second operand.
+struct LayerWiring {
+  std::vector<long> src, other;
+};
+LayerWiring layer_wiring(const ModelGraph& g);
+
 
 std::vector<Shape> infer_shapes(const ModelGraph& g);
 std::vector<std::pair<std::string, Shape>> model_weight_shapes(const ModelGraph& g);

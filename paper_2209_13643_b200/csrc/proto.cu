@@ -307,8 +307,10 @@ struct MulByBitBuild {
   CPtr2 bits;
   u64 lo, w;
   UF uf;
+  Ptr2 cout;  // optional: keep the arithmetic bit c (sigmoid's select reuses it)
   __device__ void operator()(int slot, int party, u64 g, u64 prod) const {
     const u64 c = (bits.p[slot][g] & 1) - (prod + prod);
+    if (cout.p[slot]) cout.p[slot][g] = c;
     const u64 j = g - lo;
     u64 a, b;
     ew_ab(T, party, T.off + g, a, b);
@@ -341,7 +343,8 @@ struct MaskRound {
 // opens there is nothing to overlap, so the lanes are accounted but not split).
 template <class DF, class UF, class PF>
 void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const std::string& tag_msb,
-                            const std::string& tag_b2a, const std::string& tag_mul, DF df, UF uf, PF pf) {
+                            const std::string& tag_b2a, const std::string& tag_mul, DF df, UF uf, PF pf,
+                            Ptr2 cout) {
   const int ch = clamp_chunks(opt.chunks, n);
   const Pid2 pid = pids(s);
   const SpkConsts c = make_spk_constants(opt.width);
@@ -401,7 +404,7 @@ void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const
   }
   p.nadder = 8;
   p.b2a = BR{t1.ew, pid, as_const(own_ptrs(ob)), peer_ptrs(ob), 0, n,
-             MulByBitBuild<UF>{t2.ew, own_ptrs(og), cptrs(bits), 0, n, uf}};
+             MulByBitBuild<UF>{t2.ew, own_ptrs(og), cptrs(bits), 0, n, uf, cout}};
   p.fin = CR{t2.ew, pid, as_const(own_ptrs(og)), peer_ptrs(og), 0, n, pf};
   DT bar = s.alloc(Shape{1});
   MPCG_CUDA(cudaMemsetAsync(bar.s[0], 0, 8, s.stream));
@@ -461,12 +464,12 @@ void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const
 template <class DF, class UF, class PF>
 void compare_mul(Session& s, size_t n, const AdderOptions& opt, const std::string& tag_msb,
                  const std::string& tag_b2a, int chunks_b2a, const std::string& tag_mul, int chunks_mul, DF df,
-                 UF uf, PF pf) {
+                 UF uf, PF pf, Ptr2 cout = Ptr2{{nullptr, nullptr}}) {
   const int ch = clamp_chunks(opt.chunks, n);
   if (clamp_chunks(chunks_b2a, n) != ch || clamp_chunks(chunks_mul, n) != ch)
     throw Error(kUsageError, "compare_mul: misaligned chunk lanes");
   if (n > 0 && s.persistent_ok(n)) {
-    compare_mul_persistent(s, n, opt, tag_msb, tag_b2a, tag_mul, df, uf, pf);
+    compare_mul_persistent(s, n, opt, tag_msb, tag_b2a, tag_mul, df, uf, pf, cout);
     return;
   }
   const Pid2 pid = pids(s);
@@ -499,7 +502,7 @@ void compare_mul(Session& s, size_t n, const AdderOptions& opt, const std::strin
     const auto r = chunk_range(n, ch, k);
     const size_t lo = r.first, w = r.second - r.first;
     s.wait(ob[k]);
-    MulByBitBuild<UF> gb{t2.ew, own_ptrs(og[k]), cptrs(bits), lo, w, uf};
+    MulByBitBuild<UF> gb{t2.ew, own_ptrs(og[k]), cptrs(bits), lo, w, uf, cout};
     launch_ew(s.stream, s.n_local, w,
               MulCombine<MulByBitBuild<UF>>{t1.ew, pid, as_const(own_ptrs(ob[k])), peer_ptrs(ob[k]), lo, w, gb});
     s.post(og[k], ctag(tag_mul, k));
@@ -764,6 +767,50 @@ DT maxpool2d_shares(Session& s, const DT& x, size_t N, size_t C, size_t H, size_
   }
   DT mx = max_last_dim(s, win, k * k, tag);
   return reshape(mx, Shape{N, C, OH, OW});
+}
+
+// ---------------------------------------------------------------- extension: sigmoid
+// NOT in the reference (needed by GeLU for BERT-base; SURVEY 8(a*)). Built only from the
+// reference's blocks in its tag style; restated in oracle/mpc_oracle.py:sigmoid_shares.
+//   b = b2a(msb(x)), -|x| = 2 x b - x  (one fused compare-and-multiply chain, as relu_shares)
+//   r = 1 / (1 + exp(-|x|))  (exp sees only x <= 0, the reciprocal only (1, 2])
+//   sigma(x) = r + b (1 - 2 r)
+namespace {
+struct SinkNegAbs {  // -|x| = 2 x b - x
+  CPtr2 x;
+  Ptr2 out;
+  __device__ void operator()(int slot, int, u64 g, u64 z) const { out.p[slot][g] = (z + z) - x.p[slot][g]; }
+};
+struct SrcOneMinus2 {  // [p0] 2^f - 2 r
+  Pid2 pid;
+  CPtr2 r;
+  u64 one;
+  __device__ u64 operator()(int slot, u64 g) const {
+    return (pid.v[slot] == 0 ? one : 0) - (r.p[slot][g] + r.p[slot][g]);
+  }
+};
+struct SinkAddTo {  // out = r + z
+  CPtr2 r;
+  Ptr2 out;
+  __device__ void operator()(int slot, int, u64 g, u64 z) const { out.p[slot][g] = r.p[slot][g] + z; }
+};
+}  // namespace
+
+DT sigmoid_shares(Session& s, const DT& x, const std::string& tag) {
+  const int f = s.cfg.frac_bits;
+  const size_t n = x.numel();
+  const int ch = chunks_for(s, n);
+  DT b = s.alloc(x.shape, 0), nabs = s.alloc(x.shape, x.scale);
+  compare_mul(s, n, adder_for(s, n), tag + ".msb", tag + ".b2a", ch, tag + ".abs", ch, SrcMem{cptrs(x)},
+              SrcMem{cptrs(x)}, SinkNegAbs{cptrs(x), ptrs(nabs)}, ptrs(b));
+  DT e = exp_shares(s, nabs, tag + ".exp");
+  DT r = reciprocal_shares(s, add_public(s, e, u64(1) << f), tag + ".recip");
+  Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Arith, x.shape), tag + ".sel");
+  t.mark_consumed();
+  DT out = s.alloc(x.shape, x.scale);
+  mul_op(s, t.ew, n, ch, tag + ".sel", SrcMem{cptrs(b)}, SrcOneMinus2{pids(s), cptrs(r), u64(1) << f},
+         SinkAddTo{cptrs(r), ptrs(out)});
+  return out;
 }
 
 }  // namespace mpcg

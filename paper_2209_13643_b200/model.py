@@ -19,7 +19,9 @@ M64 = (1 << 64) - 1
 CONFIG_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "configs")
 
 LAYER_KINDS = {"dense": 0, "conv2d": 1, "relu": 2, "maxpool2d": 3, "flatten": 4, "attention": 5,
-               "softmax": 6, "mean_pool": 7}
+               "softmax": 6, "mean_pool": 7,
+               # extensions for the ResNet-18 / BERT-base configs (absent from the reference)
+               "add": 8, "global_avg_pool": 9, "gelu": 10, "layernorm": 11}
 
 
 def _mix(z: np.ndarray) -> np.ndarray:
@@ -51,6 +53,8 @@ class LayerSpec:
     pad: int = 0
     heads: int = 0
     bias: bool = True
+    src: str = ""     # extension "from": input = this earlier layer's output ("input" = model input)
+    other: str = ""   # extension "with": second operand of an "add"
 
 
 @dataclass
@@ -75,16 +79,34 @@ class ModelGraph:
                 raise ValueError("unknown layer type: " + t)
             layers.append(LayerSpec(lj.get("name", t), t, int(lj.get("out", 0)), int(lj.get("kernel", 0)),
                                     int(lj.get("stride", 1)), int(lj.get("pad", 0)), int(lj.get("heads", 0)),
-                                    bool(lj.get("bias", True))))
+                                    bool(lj.get("bias", True)), str(lj.get("from", "")), str(lj.get("with", ""))))
         return ModelGraph(obj.get("name", "model"), fb, tuple(int(d) for d in obj["input"]), layers)
 
     def with_batch(self, batch: int) -> "ModelGraph":
         return ModelGraph(self.name, self.frac_bits, (batch,) + tuple(self.input[1:]), list(self.layers))
 
+    def wiring(self):
+        """Producer index of each layer's input (-1 = model input) and of an add's second
+        operand (extension; the reference's graphs are chains, H/engine/model.hpp:18-20)."""
+        names, src, oth = {}, [], []
+        for i, l in enumerate(self.layers):
+            def look(n):
+                if n == "input":
+                    return -1
+                if n not in names:
+                    raise ValueError(f"{l.name}: unknown or later layer '{n}'")
+                return names[n]
+            src.append(look(l.src) if l.src else i - 1)
+            oth.append(look(l.other) if l.type == "add" else None)
+            names[l.name] = i
+        return src, oth
+
     def shapes(self):
-        """infer_shapes (H/engine/model.hpp:69-122)."""
-        out, cur = [], list(self.input)
-        for l in self.layers:
+        """infer_shapes (H/engine/model.hpp:69-122, + the extension layers)."""
+        out = []
+        src, oth = self.wiring()
+        for i, l in enumerate(self.layers):
+            cur = list(self.input if src[i] < 0 else out[src[i]])
             if l.type == "dense":
                 cur[-1] = l.out
             elif l.type == "conv2d":
@@ -96,13 +118,18 @@ class ModelGraph:
                 cur = [cur[0], int(np.prod(cur[1:]))]
             elif l.type == "mean_pool":
                 cur = [cur[0], cur[2]]
+            elif l.type == "global_avg_pool":
+                cur = [cur[0], cur[1]]
             out.append(tuple(cur))
         return out
 
     def weight_shapes(self):
         """model_weight_shapes (H/engine/model.hpp:213-252), in layer order."""
-        out, cur = [], self.input
-        for l, nxt in zip(self.layers, self.shapes()):
+        out = []
+        shapes = self.shapes()
+        src, _ = self.wiring()
+        for i, l in enumerate(self.layers):
+            cur = self.input if src[i] < 0 else shapes[src[i]]
             if l.type == "dense":
                 out.append((l.name + ".W", (cur[-1], l.out)))
                 if l.bias:
@@ -119,7 +146,9 @@ class ModelGraph:
                 out.append((l.name + ".Wo", (d, d)))
                 if l.bias:
                     out.append((l.name + ".bo", (d,)))
-            cur = nxt
+            elif l.type == "layernorm":  # extension
+                out.append((l.name + ".gamma", (cur[-1],)))
+                out.append((l.name + ".beta", (cur[-1],)))
         return out
 
 
@@ -134,6 +163,8 @@ def init_weights(g: ModelGraph, seed: int) -> dict:
         span = 1.0 / math.sqrt(float(shape[0])) if len(shape) >= 2 else 0.1
         u = _unit(counter_draws(seed, 0x77E1 + idx, int(np.prod(shape))))
         w[key] = ((2.0 * u - 1.0) * span).reshape(shape)
+        if key.endswith(".gamma"):  # extension: LayerNorm scale centred on 1
+            w[key] = w[key] + 1.0
     return w
 
 

@@ -42,11 +42,13 @@ def test_model_helpers_match_oracle():
     import paper_2209_13643_b200 as mp
     from oracle import mpc_oracle as O
     import json
-    for name in ("mlp", "lenet5", "toy_cnn", "toy_transformer", "vgg16"):
+    for name in ("mlp", "lenet5", "toy_cnn", "toy_transformer", "vgg16", "toy_resnet", "toy_bert", "resnet18",
+                 "bert_base"):
         g = mp.ModelGraph.from_json(name)
         go = O.model_from_json(json.load(open(os.path.join(ROOT, "configs", name + ".json"))))
         assert [tuple(s) for s in g.shapes()] == [tuple(s) for s in O.infer_shapes(go)]
-        if name != "vgg16":
+        assert g.weight_shapes() == [(k, tuple(v)) for k, v in O.model_weight_shapes(go)]
+        if name not in ("vgg16", "resnet18", "bert_base"):
             w1, w2 = mp.init_weights(g, 12), O.init_weights(go, 12)
             assert sorted(w1) == sorted(w2)
             assert all(np.array_equal(w1[k], w2[k]) for k in w1)

@@ -26,6 +26,7 @@ ap.add_argument("--threshold", type=int, default=2 << 20)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--batch", type=int, default=0)
 ap.add_argument("--check", action="store_true", help="decode and compare with the numpy plaintext forward")
+ap.add_argument("--no-graph", action="store_true", help="eager runs only (no CUDA-graph capture)")
 a = ap.parse_args()
 
 g = mp.ModelGraph.from_json(a.model)
@@ -56,13 +57,18 @@ for mode in (["blocking", "pipelined"] if a.mode == "both" else [a.mode]):
         api.timer(s, "stop")
     eager_ms = api.timer(s, "read") / a.iters
     ex.time_layers(True)
-    ex.capture(xin)
-    api.timer(s, "reset")
-    for _ in range(a.iters):
-        api.timer(s, "start")
-        z = ex.replay()
-        api.timer(s, "stop")
-    graph_ms = api.timer(s, "read") / a.iters
+    if a.no_graph:
+        z = ex.run(xin)
+        s.sync()
+        graph_ms = None
+    else:
+        ex.capture(xin)
+        api.timer(s, "reset")
+        for _ in range(a.iters):
+            api.timer(s, "start")
+            z = ex.replay()
+            api.timer(s, "stop")
+        graph_ms = api.timer(s, "read") / a.iters
     layers = ex.layer_times()
     st = s.stats(0)
     res = {"first_run_s": first_s, "eager_ms": eager_ms, "graph_ms": graph_ms,
@@ -83,6 +89,7 @@ for mode in (["blocking", "pipelined"] if a.mode == "both" else [a.mode]):
     del ex
     s.close()
 if "blocking" in out and "pipelined" in out:
-    b, p = out["blocking"]["graph_ms"], out["pipelined"]["graph_ms"]
+    key = "eager_ms" if a.no_graph else "graph_ms"
+    b, p = out["blocking"][key], out["pipelined"][key]
     out["pipelined_vs_blocking_reduction_pct"] = (b - p) / b * 100
 print(json.dumps(out))
