@@ -174,6 +174,12 @@ int mpcg_executor_destroy(mpcg_executor* e);
 /* Ring-GEMM engine: 0 = SIMT only, 1 = tcgen05 int8-limb path for every shape within its
  * exact-accumulation budget (K' <= 16384), 2 = auto (tcgen05 for large shapes; default). */
 int mpcg_set_gemm_mode(int mode);
+/* Small-M combines (M <= 16, unbatched): fused-segment streaming kernel (1, default) or the
+ * tiled SIMT/tcgen05 paths (0). */
+int mpcg_set_gemv(int on);
+/* tcgen05 generation: 1 = warp-specialised pipeline (operands generated in producer warps or
+ * packed once, bulk-copied; default), 0 = first-generation kernel (materialised operands). */
+int mpcg_set_tc2(int on);
 
 /* ---- measurement hooks (bench.py) ---- */
 /* Kernels launched by this library since load. */

@@ -96,6 +96,8 @@ SIGNATURES = {
     "mpcg_executor_layer_times": [P, I32, C.POINTER(C.c_float), C.POINTER(I32)],
     "mpcg_executor_destroy": [P],
     "mpcg_set_gemm_mode": [I32],
+    "mpcg_set_gemv": [I32],
+    "mpcg_set_tc2": [I32],
     "mpcg_launch_count": [],
     "mpcg_probe_start": [I32],
     "mpcg_probe_stop": [C.POINTER(DBL), U64P, C.POINTER(DBL)],

@@ -247,6 +247,16 @@ def global_avg_pool(s, x, N_, C_, HW):
     return _op("mpcg_global_avg_pool", s, x.handle, N_, C_, HW)
 
 
+def set_gemv(on: bool = True):
+    """Small-M combines: fused-segment streaming kernel (True) or the tiled GEMM paths."""
+    N.call("mpcg_set_gemv", int(on))
+
+
+def set_tc2(on: bool = True):
+    """tcgen05 kernel generation: warp-specialised pipeline (True) or the first-generation one."""
+    N.call("mpcg_set_tc2", int(on))
+
+
 def set_gemm_mode(mode: str = "auto"):
     """Ring-GEMM engine: "simt", "tc" (tcgen05 int8 limbs wherever exact) or "auto"."""
     N.call("mpcg_set_gemm_mode", {"simt": 0, "tc": 1, "auto": 2}[mode])

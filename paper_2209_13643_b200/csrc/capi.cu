@@ -4,6 +4,7 @@
 
 #include "../../include/mpcg.h"
 #include "core.hpp"
+#include "gemm.cuh"
 #include "executor.hpp"
 
 using namespace mpcg;
@@ -449,6 +450,14 @@ int mpcg_executor_layer_times(mpcg_executor* e, int max, float* ms, int* count) 
 
 int mpcg_executor_destroy(mpcg_executor* e) {
   return guard([&] { delete e; });
+}
+
+int mpcg_set_tc2(int on) {
+  return guard([&] { tc2_mode() = on ? 1 : 0; });
+}
+
+int mpcg_set_gemv(int on) {
+  return guard([&] { gemv_mode() = on ? 1 : 0; });
 }
 
 int mpcg_set_gemm_mode(int mode) {

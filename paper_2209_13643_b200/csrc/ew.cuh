@@ -191,6 +191,199 @@ void square_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::s
   }
 }
 
+// ---------------------------------------------------------------- fused Beaver chains
+// A chain of dependent Beaver rounds (exp's repeated squaring, the reciprocal's Newton
+// steps) runs as "combine round r, build round r+1" in ONE pass per element, exactly like
+// the SPK adder rounds: the intermediate value never round-trips through HBM and the kernel
+// count halves. Posts keep the reference's collective order: every lane of round r is
+// posted before any lane of round r+1 (lane k of r+1 is posted right after lane k of r is
+// combined), and the sequence numbers are assigned at post time.
+
+// Square-triple draws of element g: A (party 0 only), r_A, r_C (H/sharing/triple.hpp:96-114).
+struct Sw {
+  u64 A, ra, rc;
+};
+__device__ __forceinline__ Sw sq_draw(const EwTriple& t, u64 g, bool p0, bool with_c) {
+  const u64 key = tkey(t.key, t.kp);
+  const u64 baseA = 1 + t.mg;
+  Sw d;
+  d.ra = drw(key, baseA + g);
+  d.rc = with_c ? drw(key, baseA + 2 * t.mg + g) : 0;
+  d.A = p0 ? drw(key, 1 + g) : 0;
+  return d;
+}
+__device__ __forceinline__ u64 sq_share_a(int party, const Sw& d) { return party ? d.ra : d.A - d.ra; }
+__device__ __forceinline__ u64 sq_share_c(int party, const Sw& d) { return party ? d.rc : d.A * d.A - d.rc; }
+
+// Build of the first square of a chain: payload eps = x - a (pair-evaluated).
+template <class XF>
+struct SqBuild2 {
+  EwTriple T;
+  Pid2 pid;
+  Ptr2 own;
+  u64 lo;
+  XF xf;
+  __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
+  __device__ void both(u64 j) const { step<2>(0, j); }
+  template <int NS>
+  __device__ __forceinline__ void step(int slot0, u64 j) const {
+    const u64 g = lo + j;
+    const Sw d = sq_draw(T, T.off + g, NS == 2 || pid.v[slot0] == 0, false);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const int slot = slot0 + k;
+      own.p[slot][j] = xf(slot, g) - sq_share_a(pid.v[slot], d);
+    }
+  }
+};
+
+// Combine square Tp, y = yf(slot, party, g, z); unless last, build square Tn on y.
+template <class YF>
+struct SqChainStep {
+  EwTriple Tp, Tn;
+  Pid2 pid;
+  CPtr2 ownp, peerp;
+  Ptr2 ownn;
+  u64 lo;
+  int last;
+  YF yf;
+  __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
+  __device__ void both(u64 j) const { step<2>(0, j); }
+  template <int NS>
+  __device__ __forceinline__ void step(int slot0, u64 j) const {
+    const u64 g = lo + j;
+    const bool p0 = NS == 2 || pid.v[slot0] == 0;
+    const Sw dp = sq_draw(Tp, Tp.off + g, p0, true);
+    Sw dn{0, 0, 0};
+    if (!last) dn = sq_draw(Tn, Tn.off + g, p0, false);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const int slot = slot0 + k, party = pid.v[slot];
+      const u64 e = ownp.p[slot][j] + peerp.p[slot][j];
+      u64 z = sq_share_c(party, dp) + (e * sq_share_a(party, dp)) * 2;
+      if (party == 0) z += e * e;
+      const u64 y = yf(slot, party, g, z);
+      if (!last) ownn.p[slot][j] = y - sq_share_a(party, dn);
+    }
+  }
+};
+
+// Rounds tr[0..R) of squares: round 0 squares x0(slot, g); round r squares the value
+// yf_for(r-1) produced from round r-1's product; yf_for(R-1) sees the chain's last product.
+template <class XF, class YFF>
+void square_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr,
+                  const std::vector<std::string>& tags, XF x0, YFF yf_for) {
+  chunks = clamp_chunks(chunks, n);
+  const int R = int(tr.size());
+  const Pid2 pid = pids(s);
+  auto ctag = [&](int r, int k) { return chunks == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
+  std::vector<Open> hs(static_cast<size_t>(chunks));
+  for (int k = 0; k < chunks; ++k) {
+    const auto rg = chunk_range(n, chunks, k);
+    hs[k] = s.begin_open(rg.second - rg.first, Reduce::Sum);
+    launch_ew(s.stream, s.n_local, rg.second - rg.first, SqBuild2<XF>{tr[0].ew, pid, own_ptrs(hs[k]), rg.first, x0});
+    s.post(hs[k], ctag(0, k));
+  }
+  using YF = decltype(yf_for(0));
+  for (int r = 1; r <= R; ++r) {
+    for (int k = 0; k < chunks; ++k) {
+      const auto rg = chunk_range(n, chunks, k);
+      const size_t w = rg.second - rg.first;
+      Open next;
+      if (r < R) next = s.begin_open(w, Reduce::Sum);
+      s.wait(hs[k]);
+      SqChainStep<YF> st{tr[r - 1].ew, r < R ? tr[r].ew : tr[r - 1].ew, pid, as_const(own_ptrs(hs[k])),
+                         peer_ptrs(hs[k]), r < R ? own_ptrs(next) : Ptr2{{nullptr, nullptr}}, rg.first,
+                         r == R ? 1 : 0, yf_for(r - 1)};
+      launch_ew(s.stream, s.n_local, w, st);
+      if (r < R) {
+        hs[k] = std::move(next);
+        s.post(hs[k], ctag(r, k));
+      }
+    }
+  }
+  s.check();
+}
+
+// Combine mul Tp, v = P.val(slot, party, g, z); unless last, build mul Tn with
+// eps = P.nx(slot, g, v), delta = P.ny(slot, g, v). Payload of a lane: [eps(w) | delta(w)].
+template <class PV>
+struct MulChainStep {
+  EwTriple Tp, Tn;
+  Pid2 pid;
+  CPtr2 ownp, peerp;
+  Ptr2 ownn;
+  u64 lo, w;
+  int last;
+  PV pv;
+  __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
+  __device__ void both(u64 j) const { step<2>(0, j); }
+  template <int NS>
+  __device__ __forceinline__ void step(int slot0, u64 j) const {
+    const u64 g = lo + j;
+    const bool p0 = NS == 2 || pid.v[slot0] == 0;
+    const Dw dp = ew_draw<true>(Tp, Tp.off + g, p0);
+    Dw dn{0, 0, 0, 0, 0};
+    if (!last) dn = ew_draw<false>(Tn, Tn.off + g, p0);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const int slot = slot0 + k, party = pid.v[slot];
+      const u64* o = ownp.p[slot];
+      const u64* q = peerp.p[slot];
+      const u64 e = o[j] + q[j], d = o[w + j] + q[w + j];
+      u64 a, b, c;
+      ew_share<true>(Tp, party, dp, a, b, c);
+      u64 z = c + (e * b + d * a);
+      if (party == 0) z += e * d;
+      const u64 v = pv.val(slot, party, g, z);
+      if (!last) {
+        u64 an, bn, cn;
+        ew_share<false>(Tn, party, dn, an, bn, cn);
+        ownn.p[slot][j] = pv.nx(slot, g, v) - an;
+        ownn.p[slot][w + j] = pv.ny(slot, g, v) - bn;
+      }
+    }
+  }
+};
+
+// Rounds tr[0..R) of multiplies: round 0 multiplies x0 * y0; round r's operands come from
+// pv_for(r-1) (applied to round r-1's product); pv_for(R-1).val sees the last product.
+template <class XF, class YF, class PVF>
+void mul_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, const std::vector<std::string>& tags,
+               XF x0, YF y0, PVF pv_for) {
+  chunks = clamp_chunks(chunks, n);
+  const int R = int(tr.size());
+  const Pid2 pid = pids(s);
+  auto ctag = [&](int r, int k) { return chunks == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
+  std::vector<Open> hs(static_cast<size_t>(chunks));
+  for (int k = 0; k < chunks; ++k) {
+    const auto rg = chunk_range(n, chunks, k);
+    const size_t w = rg.second - rg.first;
+    hs[k] = s.begin_open(2 * w, Reduce::Sum);
+    launch_ew(s.stream, s.n_local, w, MulBuild<XF, YF>{tr[0].ew, pid, own_ptrs(hs[k]), rg.first, w, x0, y0});
+    s.post(hs[k], ctag(0, k));
+  }
+  using PV = decltype(pv_for(0));
+  for (int r = 1; r <= R; ++r) {
+    for (int k = 0; k < chunks; ++k) {
+      const auto rg = chunk_range(n, chunks, k);
+      const size_t w = rg.second - rg.first;
+      Open next;
+      if (r < R) next = s.begin_open(2 * w, Reduce::Sum);
+      s.wait(hs[k]);
+      MulChainStep<PV> st{tr[r - 1].ew, r < R ? tr[r].ew : tr[r - 1].ew, pid, as_const(own_ptrs(hs[k])),
+                          peer_ptrs(hs[k]), r < R ? own_ptrs(next) : Ptr2{{nullptr, nullptr}}, rg.first, w,
+                          r == R ? 1 : 0, pv_for(r - 1)};
+      launch_ew(s.stream, s.n_local, w, st);
+      if (r < R) {
+        hs[k] = std::move(next);
+        s.post(hs[k], ctag(r, k));
+      }
+    }
+  }
+  s.check();
+}
+
 // ---------------------------------------------------------------- SPK adder rounds
 // H/protocols/adder.hpp:122-223. Round 0 is the generate AND on (x, y); rounds 1..L are
 // the prefix levels on the stacked (S, P) pair. One kernel settles round rp and issues

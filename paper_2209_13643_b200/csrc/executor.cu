@@ -304,8 +304,8 @@ DT SecureExecutor::weight_matmul(size_t i, const DT& x, const ConvGeom* geom, bo
   op.delta.reset();
   const size_t na = size_t(M) * K;
   Open e = s_.begin_open(na, Reduce::Sum);
-  DT aops;  // A-side combine operands from the eps draws (SIMT combine only)
-  if (!beaver_combine_uses_tc(s_, 1, M, N, K)) aops = s_.alloc(Shape{2, na});
+  DT aops;  // A-side combine operands from the eps draws (memory-operand combines only)
+  if (beaver_combine_wants_aops(s_, 1, M, N, K)) aops = s_.alloc(Shape{2, na});
   if (geom)
     eps_build_im2col(s_, t, x.s, *geom, 0, na, e, aops ? &aops : nullptr);
   else

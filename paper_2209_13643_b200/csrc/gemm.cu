@@ -145,6 +145,97 @@ void launch_simt(Session& s, GemmArgs a) {
   probe_end(st, pe);
 }
 
+// ---------------------------------------------------------------- small-M (GEMV-shaped) path
+// Dense heads at batch 1..16 (MLP, VGG fc6/fc7/fc8, LeNet fc): the combine streams the
+// weight-side operands R_g[k][n] (dealer B / r_B draws and the opened F = own + peer delta)
+// exactly once per (k, n) for ALL segments of a slot — party 0's three segments share one
+// B / r_B draw and one F load — while the few L rows of a K-chunk are staged in shared
+// memory. Bound by reading F (2 x 8 B per (k, n) per party) and the dealer draws.
+constexpr int kGvM = 16;    // max rows
+constexpr int kGvKC = 64;   // K chunk staged in smem
+
+template <int MR>
+__global__ void __launch_bounds__(256) ring_gemv(GemmArgs a) {
+  __shared__ u64 Ls[3][MR][kGvKC];
+  pdl_enter();
+  const int slot = blockIdx.z;
+  const GemmSlotArgs& S = a.sl[slot];
+  const u32 M = a.M, N = a.N, K = a.K;
+  const u32 n = blockIdx.x * 256 + threadIdx.x;
+  const u32 kb = blockIdx.y * a.kchunk, ke = min(K, kb + a.kchunk);
+  bool needB = false, needRB = false, needF = false;
+  for (int g = 0; g < S.nseg; ++g) {
+    const int rk = S.rk[g];
+    needB |= rk == kOpB || rk == kOpB0F;
+    needRB |= rk == kOpRB || rk == kOpB0F;
+    needF |= rk == kOpSum || rk == kOpB0F;
+  }
+  const u64* Fo = nullptr;
+  const u64* Fp = nullptr;
+  for (int g = 0; g < S.nseg; ++g)
+    if (S.rk[g] == kOpSum || S.rk[g] == kOpB0F) Fo = S.R[g], Fp = S.R2[g];
+  u64 acc[MR];
+#pragma unroll
+  for (int m = 0; m < MR; ++m) acc[m] = 0;
+  for (u32 k0 = kb; k0 < ke; k0 += kGvKC) {
+    const u32 kc = min(u32(kGvKC), ke - k0);
+    __syncthreads();
+    for (u32 e = threadIdx.x; e < u32(S.nseg) * MR * kGvKC; e += 256) {
+      const u32 kk = e % kGvKC, m = (e / kGvKC) % MR, g = e / (kGvKC * MR);
+      Ls[g][m][kk] = (m < M && kk < kc) ? load_l(S, int(g), u64(m) * K + k0 + kk) : 0;
+    }
+    __syncthreads();
+    if (n >= N) continue;
+    for (u32 kk = 0; kk < kc; ++kk) {
+      const u64 idx = u64(k0 + kk) * N + n;
+      const u64 B = needB ? mm_B(S.mm, S.boff + idx) : 0;
+      const u64 rB = needRB ? mm_rB(S.mm, S.boff + idx) : 0;
+      const u64 F = needF ? __ldg(Fo + idx) + __ldg(Fp + idx) : 0;
+#pragma unroll
+      for (int g = 0; g < 3; ++g) {
+        if (g >= S.nseg) break;
+        u64 r;
+        switch (S.rk[g]) {
+          case kOpMem: r = __ldg(S.R[g] + idx); break;
+          case kOpSum: r = F; break;
+          case kOpB: r = B; break;
+          case kOpB0F: r = (B - rB) + F; break;
+          default: r = rB; break;
+        }
+#pragma unroll
+        for (int m = 0; m < MR; ++m) acc[m] += Ls[g][m][kk] * r;
+      }
+    }
+  }
+  if (n >= N) return;
+  const u64 per = u64(M) * N;
+#pragma unroll
+  for (int m = 0; m < MR; ++m)
+    if (u32(m) < M) a.acc[slot][u64(blockIdx.y) * per + u64(m) * N + n] = acc[m];
+}
+
+template <int MR>
+void launch_gemv(Session& s, GemmArgs a) {
+  cudaStream_t st = s.stream;
+  const u32 nblk = (a.N + 255) / 256;
+  // split K until ~3 waves of 256-thread CTAs (8 resident per SM), chunks of >= 4 smem stages
+  u32 split = u32((3 * 8 * u64(kSms) / a.nslots + nblk - 1) / nblk);
+  const u32 maxsplit = (a.K + 4 * kGvKC - 1) / (4 * kGvKC);
+  split = split > maxsplit ? maxsplit : (split < 1 ? 1 : split);
+  a.kchunk = (a.K + split - 1) / split;
+  a.ksplit = (a.K + a.kchunk - 1) / a.kchunk;
+  const u64 per = u64(a.M) * a.N;
+  std::shared_ptr<Block> ws = s.raw(per * a.ksplit * a.nslots);
+  for (int i = 0; i < a.nslots; ++i) a.acc[i] = ws->ptr + i * per * a.ksplit;
+  cudaEvent_t pe;
+  probe_begin(st, &pe);
+  launch_pdl(ring_gemv<MR>, dim3(nblk, a.ksplit, a.nslots), dim3(256), 0, st, a);
+  launch_pdl(gemm_splitk_epilogue, dim3(ew_blocks(per * a.nslots)), dim3(256), 0, st, a);
+  probe_end(st, pe);
+}
+
+bool gemv_eligible(const GemmArgs& a) { return a.M <= u32(kGvM) && a.nbatch == 1 && !a.tb && !a.col2im; }
+
 }  // namespace
 
 void ring_gemm_launch(Session& s, const GemmArgs& a) {
@@ -154,7 +245,15 @@ void ring_gemm_launch(Session& s, const GemmArgs& a) {
   double macs = 0;
   for (int i = 0; i < a.nslots; ++i) macs += double(a.sl[i].nseg) * a.M * a.N * a.K * a.nbatch;
   ClassScope cs(kClsGemm, macs);
-  if (ring_gemm_tc_try(s, a)) return;  // tcgen05 int8-limb path when the shape qualifies
+  if (gemv_eligible(a) && gemv_mode() != 0) {
+    if (a.M <= 1) launch_gemv<1>(s, a);
+    else if (a.M <= 4) launch_gemv<4>(s, a);
+    else launch_gemv<16>(s, a);
+    s.check();
+    return;
+  }
+  if (ring_gemm_tc2_try(s, a)) return;  // warp-specialised tcgen05 int8-limb path
+  if (ring_gemm_tc_try(s, a)) return;   // first-generation tcgen05 path (materialised operands)
   if (a.M <= 16) {
     if (a.N <= 16)
       launch_simt<16, 16, 1, 1>(s, a);
@@ -364,6 +463,21 @@ bool beaver_combine_uses_tc(const Session& s, u32 nbatch, u32 M, u32 N, u32 K) {
   return ring_gemm_tc_wants(a);
 }
 
+// The eps build also emits the A-side operands (A, a0 / r_A) only for combines that read them
+// from memory (tiled SIMT and first-generation tcgen05); the small-M path and the
+// warp-specialised tcgen05 path draw them in place.
+bool beaver_combine_wants_aops(const Session& s, u32 nbatch, u32 M, u32 N, u32 K) {
+  GemmArgs a{};
+  a.nslots = s.n_local;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.nbatch = nbatch;
+  for (int i = 0; i < s.n_local; ++i) a.sl[i].nseg = s.party_of[i] == 0 ? 3 : 2;
+  if (M <= 16 && nbatch == 1 && gemv_mode() != 0) return false;
+  return !ring_gemm_tc2_wants(a);
+}
+
 void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na, const Open& d, size_t nb,
                     DT* rcache, u64* const out[2], size_t out_off, u32 nbatch, u32 M, u32 N, u32 K, bool tb,
                     bool batched_r, size_t r_batch0, const Epi& ep, const DT* aops) {
@@ -378,10 +492,45 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
   a.col2im = ep.col2im;
   a.OHW = ep.OHW;
   for (int i = 0; i < s.n_local; ++i) a.sl[i].nseg = s.party_of[i] == 0 ? 3 : 2;
-  if (ring_gemm_tc_wants(a)) {
-    DT L = prepare_L(s, t, e, a_off, na);
+  if (!ring_gemm_tc2_wants(a) && ring_gemm_tc_wants(a)) {
     if (!*rcache) *rcache = prepare_R(s, t, d, nb);
-    mm_combine(s, t, L, na, *rcache, nb, out, out_off, nbatch, M, N, K, tb, batched_r, r_batch0, ep);
+    if (!aops) {  // no A-side operands from the eps build: materialise L
+      DT L = prepare_L(s, t, e, a_off, na);
+      mm_combine(s, t, L, na, *rcache, nb, out, out_off, nbatch, M, N, K, tb, batched_r, r_batch0, ep);
+      return;
+    }
+    // L straight from the eps build's A-side operands and the two opened eps halves (E = own +
+    // peer, summed in the tcgen05 producer); R (weight side, small) materialised once per layer.
+    const u64 sL = u64(M) * K, sR = batched_r ? u64(K) * N : 0;
+    const u64 rboff = batched_r ? r_batch0 * u64(K) * N : 0;
+    for (int i = 0; i < s.n_local; ++i) {
+      GemmSlotArgs& S = a.sl[i];
+      const u64* Rp = rcache->s[i];
+      const u64* ao = aops->s[i];
+      S.out = out[i] + out_off;
+      S.bias = ep.bias[i];
+      S.ckey = t.mm.key;
+      S.ckp = t.mm.kp;
+      S.cbase = 1 + 2 * t.mm.na + 2 * t.mm.nb + t.mm.offC + out_off;
+      if (s.party_of[i] == 0) {  // -r_C + A*B + E*(b0 + F) + a0*F ; R = {B, b0+F, F}
+        S.cterm = -1;
+        S.L[0] = ao;
+        S.lk[1] = kOpSum, S.L[1] = e.own(i), S.L2[1] = e.peer(i);
+        S.L[2] = ao + na;
+        for (int g = 0; g < 3; ++g) S.R[g] = Rp + g * nb + rboff;
+      } else {  // +r_C + E*r_B + r_A*F ; R = {r_B, F}
+        S.cterm = +1;
+        S.lk[0] = kOpSum, S.L[0] = e.own(i), S.L2[0] = e.peer(i);
+        S.L[1] = ao;
+        S.R[0] = Rp + rboff;
+        S.R[1] = Rp + nb + rboff;
+      }
+      for (int g = 0; g < 3; ++g) {
+        S.sL[g] = sL;
+        S.sR[g] = sR;
+      }
+    }
+    ring_gemm_launch(s, a);
     return;
   }
   const u64 sL = u64(M) * K, sR = batched_r ? u64(K) * N : 0;
@@ -475,10 +624,10 @@ DT beaver_matmul(Session& s, const DT& x, const DT& y, bool transpose_b, const s
     const auto r = chunk_range(rows, chunks, k);
     const size_t cnt = r.second - r.first;
     he[k] = s.begin_open(cnt * row_w, Reduce::Sum);
-    const bool tc = batched_b ? beaver_combine_uses_tc(s, u32(cnt), u32(M), u32(N), u32(K))
-                              : beaver_combine_uses_tc(s, 1, u32(cnt), u32(N), u32(K));
-    if (!tc) aops[k] = s.alloc(Shape{2, cnt * row_w});
-    eps_build_mem(s, t, x.s, r.first * row_w, cnt * row_w, he[k], tc ? nullptr : &aops[k]);
+    const bool want = batched_b ? beaver_combine_wants_aops(s, u32(cnt), u32(M), u32(N), u32(K))
+                                : beaver_combine_wants_aops(s, 1, u32(cnt), u32(N), u32(K));
+    if (want) aops[k] = s.alloc(Shape{2, cnt * row_w});  // A-side combine operands from the eps draws
+    eps_build_mem(s, t, x.s, r.first * row_w, cnt * row_w, he[k], want ? &aops[k] : nullptr);
     s.post(he[k], chunks == 1 ? tag + ".eps" : tag + ".eps.chunk" + std::to_string(k));
   }
   s.wait(hd);

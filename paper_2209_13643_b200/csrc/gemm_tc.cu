@@ -159,18 +159,29 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc_kernel(const __grid_
   // Register prefetch of step `st`'s operands (issued while earlier MMAs run). The segments
   // are packed back to back along K' = nseg*K, so small K (e.g. 25) is not padded per segment.
   const u32 KP = u32(S.nseg) * K;
-  auto load16 = [&](const u64* const* base, const u64* stride, bool trans, u32 row, u32 rows, u32 kp, u64 (&v)[16]) {
+  // base2: second addend of kOpSum segments (the opened E = own + peer eps), L side only.
+  auto load16 = [&](const u64* const* base, const u64* const* base2, const int* kind, const u64* stride, bool trans,
+                    u32 row, u32 rows, u32 kp, u64 (&v)[16]) {
     // 16 K'-consecutive values of `row` starting at packed index kp
     const u32 sg0 = kp / K;
     if (row < rows && kp + 16 <= KP && sg0 == (kp + 15) / K && a.vec16 && (trans || base == S.L)) {
       const u32 k = kp - sg0 * K;
-      const u64* P = base[sg0] + u64(b) * stride[sg0] + u64(row) * K + k;
-      const uint4* p4 = reinterpret_cast<const uint4*>(P);
+      const u64 off = u64(b) * stride[sg0] + u64(row) * K + k;
+      const uint4* p4 = reinterpret_cast<const uint4*>(base[sg0] + off);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const uint4 w = __ldg(p4 + i);
         v[2 * i] = (u64(w.y) << 32) | w.x;
         v[2 * i + 1] = (u64(w.w) << 32) | w.z;
+      }
+      if (kind && kind[sg0] == kOpSum) {
+        const uint4* q4 = reinterpret_cast<const uint4*>(base2[sg0] + off);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint4 w = __ldg(q4 + i);
+          v[2 * i] += (u64(w.y) << 32) | w.x;
+          v[2 * i + 1] += (u64(w.w) << 32) | w.z;
+        }
       }
       return;
     }
@@ -180,16 +191,17 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc_kernel(const __grid_
       const u32 q = kp + i;
       if (row < rows && q < KP) {
         const u32 sg = q / K, k = q - sg * K;
-        const u64* P = base[sg] + u64(b) * stride[sg];
-        x = trans ? __ldg(P + u64(row) * K + k) : __ldg(P + u64(k) * N + row);
+        const u64 off = u64(b) * stride[sg] + (trans ? u64(row) * K + k : u64(k) * N + row);
+        x = __ldg(base[sg] + off);
+        if (kind && kind[sg] == kOpSum) x += __ldg(base2[sg] + off);
       }
       v[i] = x;
     }
   };
   auto load_step = [&](u32 st) {
     const u32 k0 = st * kKB;
-    load16(S.L, S.sL, true, m0 + ra, M, k0 + ka * 16, va);          // A rows are K-contiguous
-    if (hasB) load16(S.R, S.sR, a.tb != 0, n0 + rb, N, k0 + kbc * 16, vb);
+    load16(S.L, S.L2, S.lk, S.sL, true, m0 + ra, M, k0 + ka * 16, va);  // A rows are K-contiguous
+    if (hasB) load16(S.R, nullptr, nullptr, S.sR, a.tb != 0, n0 + rb, N, k0 + kbc * 16, vb);
   };
 
   if (steps > 0) load_step(0);
@@ -320,14 +332,15 @@ bool ring_gemm_tc_wants(const GemmArgs& a) {
 
 bool ring_gemm_tc_try(Session& s, const GemmArgs& a) {
   if (!ring_gemm_tc_wants(a)) return false;
-  for (int i = 0; i < a.nslots; ++i)  // the tensor-core producer reads materialised operands
+  for (int i = 0; i < a.nslots; ++i)  // the producer reads memory operands (L: plain or own + peer)
     for (int g = 0; g < a.sl[i].nseg; ++g)
-      if (a.sl[i].lk[g] != kOpMem || a.sl[i].rk[g] != kOpMem) return false;
+      if ((a.sl[i].lk[g] != kOpMem && a.sl[i].lk[g] != kOpSum) || a.sl[i].rk[g] != kOpMem) return false;
   GemmArgs v = a;
   bool al = (a.K % 2) == 0;
   for (int i = 0; i < a.nslots && al; ++i)
     for (int g = 0; g < a.sl[i].nseg; ++g) {
       al = al && (reinterpret_cast<uintptr_t>(a.sl[i].L[g]) % 16 == 0) && (a.sl[i].sL[g] % 2 == 0);
+      if (a.sl[i].lk[g] == kOpSum) al = al && (reinterpret_cast<uintptr_t>(a.sl[i].L2[g]) % 16 == 0);
       if (a.tb) al = al && (reinterpret_cast<uintptr_t>(a.sl[i].R[g]) % 16 == 0) && (a.sl[i].sR[g] % 2 == 0);
     }
   v.vec16 = al ? 1 : 0;

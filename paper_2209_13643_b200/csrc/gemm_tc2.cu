@@ -1,0 +1,496 @@
+// tcgen05 int8-limb ring GEMM over Z_2^64, warp-specialised (sm_100a).
+//
+// Same arithmetic as gemm_tc.cu (u64 operands split into 8 u8 limbs; the 36 limb pairs with
+// l+m <= 7 run as tcgen05.mma.kind::i8 into 8 s32 TMEM accumulators, one per diagonal
+// d = l+m; the epilogue recombines z = sum_d D_d << 8d mod 2^64 — the int8 form of
+// LimbPlan/limb_matmul, H/ring/limb.hpp:15-99), restructured as a Blackwell pipeline:
+//
+//   warps 0-7  L producers: generate the left operand of every segment straight from its
+//              source — the opened E = own + peer eps (two vector loads) or the dealer's
+//              A / r_A draws (counter PRG, H/sharing/triple.hpp:96-114) — byte-transpose it
+//              into K-major limb planes and publish the stage with an mbarrier arrive;
+//   warp 8     bulk loader: the right operands (weight side, packed once per layer into the
+//              exact shared-memory image of a stage) arrive by cp.async.bulk (TMA engine)
+//              on the same mbarrier with expect_tx;
+//   warp 9     MMA issuer (one thread): 36 tcgen05.mma per stage, tcgen05.commit frees the
+//              stage;
+//   warps 0-7  epilogue: tcgen05.ld of the 8 diagonals, recombination, Beaver epilogue.
+//
+// A 4-stage ring of 32-byte K slabs keeps HBM loads, PRG work and MMAs in flight together.
+// When N spans several BN tiles the left operand is also packed once (pack kernel) and both
+// sides arrive by cp.async.bulk, so the generation is not repeated per N tile.
+// Exactness: per-diagonal sums over K' = nseg*K <= 16384 (see gemm_tc.cu).
+#include "gemm.cuh"
+
+namespace mpcg {
+
+namespace {
+
+constexpr int kM = 128;        // tile rows (UMMA M)
+constexpr int kKB = 32;        // K values (= limb bytes) per stage: one UMMA K slab
+constexpr int kStages = 4;
+constexpr int kProd = 256;     // L producer threads (warps 0-7)
+constexpr int kThreads = 320;  // + warp 8 (bulk loader) + warp 9 (MMA issuer, TMEM owner)
+constexpr u32 kMaxKPrime = 16384;
+
+__device__ __forceinline__ u32 smem_u32(const void* p) { return static_cast<u32>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// K-major SWIZZLE_NONE descriptor (version 1): LBO between the two 16-B K chunks, SBO between
+// 8-row groups.
+__device__ __forceinline__ u64 smem_desc(u32 addr, u32 lbo, u32 sbo) {
+  return u64((addr >> 4) & 0x3FFF) | (u64((lbo >> 4) & 0x3FFF) << 16) | (u64((sbo >> 4) & 0x3FFF) << 32) |
+         (u64(1) << 46);
+}
+// kind::i8, D = s32, A/B unsigned 8-bit, both K-major.
+__host__ __device__ constexpr u32 idesc_i8(u32 M, u32 N) { return (2u << 4) | ((N >> 3) << 17) | ((M >> 4) << 24); }
+
+__device__ __forceinline__ void mma_i8(u32 d_tmem, u64 adesc, u64 bdesc, u32 idesc, u32 acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(u64* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ u32 gather4(u32 a, u32 b, u32 c, u32 d, u32 l) {
+  const u32 sel = l | ((l + 4) << 4);
+  return __byte_perm(__byte_perm(a, b, sel), __byte_perm(c, d, sel), 0x5410);
+}
+// 16 K-consecutive u64 -> one 16-byte row in each of the 8 limb planes (base + p*plane + off).
+__device__ __forceinline__ void transpose_store(const u64 (&v)[16], char* base, u32 plane, u32 off) {
+#pragma unroll
+  for (int l = 0; l < 8; ++l) {
+    const int sh = (l & 3), hi = l >> 2;
+    u32 w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = hi ? u32(v[i] >> 32) : u32(v[i]);
+    uint4 o;
+    o.x = gather4(w[0], w[1], w[2], w[3], sh);
+    o.y = gather4(w[4], w[5], w[6], w[7], sh);
+    o.z = gather4(w[8], w[9], w[10], w[11], sh);
+    o.w = gather4(w[12], w[13], w[14], w[15], sh);
+    *reinterpret_cast<uint4*>(base + l * plane + off) = o;
+  }
+}
+
+// 16 dealer draws c0, c0+1, ... of one stream, incrementally (key + c*phi advances by phi).
+__device__ __forceinline__ void draws16(u64 key, u64 c0, u64 (&v)[16]) {
+  u64 z = key + c0 * kPhi;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    v[i] = mix64(z);
+    z += kPhi;
+  }
+}
+
+__device__ __forceinline__ void load16v(const u64* p, u64 (&v)[16]) {
+  const uint4* p4 = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint4 w = __ldg(p4 + i);
+    v[2 * i] = (u64(w.y) << 32) | w.x;
+    v[2 * i + 1] = (u64(w.w) << 32) | w.z;
+  }
+}
+
+}  // namespace
+
+struct Tc2Args {
+  GemmArgs g;
+  const char* Rpk[2] = {nullptr, nullptr};  // packed right operand per slot
+  u64 Rpk_b = 0;                            // bytes per batch (0 = shared across the batch)
+  const char* Lpk[2] = {nullptr, nullptr};  // packed left operand (multi-N-tile shapes) or null
+  u64 Lpk_b = 0;
+  u32 nkb = 0;                              // K blocks of 32
+  int vec = 0;                              // L rows 16-byte aligned (vector loads)
+};
+
+namespace {
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_constant__ Tc2Args P) {
+  constexpr u32 kA = kM * kKB;  // bytes per A limb plane per stage
+  constexpr u32 kB = BN * kKB;  // bytes per B limb plane per stage
+  constexpr u32 kStage = 8 * (kA + kB);
+  constexpr u32 kCols = 8 * BN;
+  static_assert(kCols <= 512, "TMEM budget");
+  extern __shared__ __align__(1024) char smem[];
+  __shared__ __align__(8) u64 full[kStages], empty[kStages], done;
+  __shared__ u32 tmem_slot;
+
+  pdl_enter();
+  const GemmArgs& a = P.g;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int slot = blockIdx.z % a.nslots;
+  const u32 b = blockIdx.z / a.nslots;
+  const GemmSlotArgs& S = a.sl[slot];
+  const u32 M = a.M, N = a.N, K = a.K;
+  const u32 m0 = blockIdx.y * kM, n0 = blockIdx.x * BN;
+  const int nseg = S.nseg;
+  const u32 nst = P.nkb * u32(nseg);
+  const bool packedL = P.Lpk[slot] != nullptr;
+
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], packedL ? 1 : 9);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                 "r"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const u32 tmem = tmem_slot;
+
+  if (warp < 8) {
+    if (!packedL) {
+      // ---- L producers: unit = (row r, K chunk kc) of 16 values per stage
+      const int r = tid & (kM - 1), kc = tid >> 7;
+      const u32 m = m0 + u32(r);
+      const bool rowok = m < M;
+      const u64 rowoff = u64(b) * S.sL[0] + u64(m) * K;  // same stride for every segment
+      const u64 key = tkey(S.mm.key, S.mm.kp);
+      const u64 iA = 1 + S.mm.offA + S.aoff;                   // draw index of A[0]
+      const u64 iRA = 1 + S.mm.na + S.mm.nb + S.mm.offA + S.aoff;  // of r_A[0]
+      const u32 off = (u32(kc) * (kM / 8) + u32(r) / 8) * 128 + (u32(r) % 8) * 16;
+      u64 cA[16];
+      u32 it = 0;
+      for (u32 kb = 0; kb < P.nkb; ++kb) {
+        const u32 k0 = kb * kKB + u32(kc) * 16;
+        const bool full16 = rowok && k0 + 16 <= K;
+        bool haveA = false;
+        for (int g = 0; g < nseg; ++g, ++it) {
+          const int stg = int(it % kStages);
+          u64 v[16];
+          const int kind = S.lk[g];
+          if (!rowok || k0 >= K) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = 0;
+          } else if (kind == kOpMem || kind == kOpSum) {
+            const u64* p = S.L[g] + rowoff + k0;
+            if (full16 && P.vec) {
+              load16v(p, v);
+              if (kind == kOpSum) {
+                u64 w[16];
+                load16v(S.L2[g] + rowoff + k0, w);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] += w[i];
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                u64 x = 0;
+                if (k0 + i < K) {
+                  x = __ldg(p + i);
+                  if (kind == kOpSum) x += __ldg(S.L2[g] + rowoff + k0 + i);
+                }
+                v[i] = x;
+              }
+            }
+          } else {  // dealer draws: A, a0 = A - r_A (party 0), r_A (party 1)
+            const u64 e0 = rowoff + k0;
+            if (kind == kOpRA) {
+              draws16(key, iRA + e0, v);
+            } else {
+              if (!haveA) {
+                draws16(key, iA + e0, cA);
+                haveA = true;
+              }
+              if (kind == kOpA) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = cA[i];
+              } else {
+                draws16(key, iRA + e0, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = cA[i] - v[i];
+              }
+            }
+            if (!full16) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (k0 + i >= K) v[i] = 0;
+            }
+          }
+          if (it >= kStages) mbar_wait(&empty[stg], ((it / kStages) & 1) ^ 1);
+          transpose_store(v, smem + stg * kStage, kA, off);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[stg]);
+        }
+      }
+    }
+  } else if (warp == 8) {
+    if (lane == 0) {  // ---- bulk loader
+      const char* Rb = P.Rpk[slot] + u64(b) * P.Rpk_b + u64(blockIdx.x) * P.nkb * u64(nseg) * 8 * kB;
+      const char* Lb = packedL ? P.Lpk[slot] + u64(b) * P.Lpk_b + u64(blockIdx.y) * P.nkb * u64(nseg) * 8 * kA
+                               : nullptr;
+      for (u32 it = 0; it < nst; ++it) {
+        const int stg = int(it % kStages);
+        if (it >= kStages) mbar_wait(&empty[stg], ((it / kStages) & 1) ^ 1);
+        char* sA = smem + stg * kStage;
+        mbar_arrive_tx(&full[stg], 8 * kB + (packedL ? 8 * kA : 0));
+        bulk_g2s(sA + 8 * kA, Rb + u64(it) * 8 * kB, 8 * kB, &full[stg]);
+        if (packedL) bulk_g2s(sA, Lb + u64(it) * 8 * kA, 8 * kA, &full[stg]);
+      }
+    }
+  } else {
+    if (lane == 0) {  // ---- MMA issuer
+      constexpr u32 idesc = idesc_i8(kM, BN);
+      for (u32 it = 0; it < nst; ++it) {
+        const int stg = int(it % kStages);
+        mbar_wait(&full[stg], (it / kStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const u32 aBase = smem_u32(smem + stg * kStage), bBase = aBase + 8 * kA;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+          const u64 ad = smem_desc(aBase + l * kA, (kM / 8) * 128, 128);
+#pragma unroll
+          for (int mm = 0; mm + l < 8; ++mm) {
+            const u64 bd = smem_desc(bBase + mm * kB, (BN / 8) * 128, 128);
+            mma_i8(tmem + u32(l + mm) * BN, ad, bd, idesc, (it > 0 || l > 0) ? 1u : 0u);
+          }
+        }
+        mma_commit(&empty[stg]);
+      }
+      mma_commit(&done);
+    }
+  }
+
+  // ---- epilogue (warps 0-7): warp w reads TMEM lanes 32*(w%4).. and column half w/4
+  if (warp < 8) {
+    mbar_wait(&done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    constexpr int kHalf = BN / 2;
+    constexpr int kCW = kHalf < 16 ? kHalf : 16;
+    const int q = warp & 3, ch = warp >> 2;
+    const u32 row = u32(q) * 32 + u32(lane);
+    const u32 m = m0 + row;
+    const u32 lane_addr = tmem + ((u32(q) * 32) << 16) + u32(ch * kHalf);
+#pragma unroll
+    for (int c0 = 0; c0 < kHalf; c0 += kCW) {
+      u64 acc[kCW];
+#pragma unroll
+      for (int c = 0; c < kCW; ++c) acc[c] = 0;
+#pragma unroll
+      for (int d = 0; d < 8; ++d) {
+        u32 rr[kCW];
+        const u32 ad = lane_addr + u32(d) * BN + u32(c0);
+        if constexpr (kCW == 16) {
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3]), "=r"(rr[4]), "=r"(rr[5]), "=r"(rr[6]),
+                "=r"(rr[7]), "=r"(rr[8]), "=r"(rr[9]), "=r"(rr[10]), "=r"(rr[11]), "=r"(rr[12]), "=r"(rr[13]),
+                "=r"(rr[14]), "=r"(rr[15])
+              : "r"(ad));
+        } else {
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3]), "=r"(rr[4]), "=r"(rr[5]), "=r"(rr[6]),
+                         "=r"(rr[7])
+                       : "r"(ad));
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < kCW; ++c) acc[c] += u64(rr[c]) << (8 * d);
+      }
+      if (m < M) {
+#pragma unroll
+        for (int c = 0; c < kCW; ++c) {
+          const u32 n = n0 + u32(ch * kHalf + c0 + c);
+          if (n < N) gemm_epilogue(a, S, b, m, n, acc[c]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 9)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols) : "memory");
+}
+
+// Packs one operand into the shared-memory image of every stage it feeds:
+// [batch][row tile][K block][segment][limb plane][BR rows x 32 B], core matrices K-major
+// (row group r/8, K chunk kc) at (kc*(BR/8) + r/8)*128, row r%8 at +16*(r%8).
+// left: value = load_l(S, g, b*sL + row*K + k); right: load_r at (b*sR + k*N + row) or,
+// transposed, (b*sR + row*K + k).
+template <int BR>
+__global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int slot, int left, u32 rows, u32 nbatch, u32 nkb,
+                                                  char* out) {
+  pdl_enter();
+  const GemmSlotArgs& S = a.sl[slot];
+  const u32 K = a.K, N = a.N, nseg = u32(S.nseg);
+  const u32 tiles = (rows + BR - 1) / BR;
+  const u64 units = u64(nbatch) * tiles * nkb * nseg * BR * 2;
+  constexpr u32 plane = BR * kKB;
+  for (u64 uid = blockIdx.x * u64(blockDim.x) + threadIdx.x; uid < units; uid += u64(gridDim.x) * blockDim.x) {
+    u64 t = uid;
+    const u32 r = u32(t % BR);
+    t /= BR;
+    const u32 kc = u32(t % 2);
+    t /= 2;
+    const u32 g = u32(t % nseg);
+    t /= nseg;
+    const u32 kb = u32(t % nkb);
+    t /= nkb;
+    const u32 tile = u32(t % tiles);
+    const u32 bb = u32(t / tiles);
+    const u32 row = tile * BR + r;
+    const u32 k0 = kb * kKB + kc * 16;
+    u64 v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const u32 k = k0 + u32(i);
+      u64 x = 0;
+      if (row < rows && k < K) {
+        if (left)
+          x = load_l(S, int(g), u64(bb) * S.sL[g] + u64(row) * K + k);
+        else
+          x = load_r(S, int(g), u64(bb) * S.sR[g] + (a.tb ? u64(row) * K + k : u64(k) * N + row));
+      }
+      v[i] = x;
+    }
+    char* base = out + ((((u64(bb) * tiles + tile) * nkb + kb) * nseg + g) * 8) * plane;
+    transpose_store(v, base, plane, (kc * (BR / 8) + r / 8) * 128 + (r % 8) * 16);
+  }
+}
+
+template <int BR>
+void launch_pack(Session& s, const GemmArgs& a, int slot, bool left, u32 rows, u32 nbatch, u32 nkb, char* out) {
+  const u32 tiles = (rows + BR - 1) / BR;
+  const u64 units = u64(nbatch) * tiles * nkb * a.sl[slot].nseg * BR * 2;
+  cudaEvent_t pe;
+  probe_begin(s.stream, &pe);
+  launch_pdl(pack_limbs<BR>, dim3(ew_blocks(units)), dim3(256), 0, s.stream, a, slot, left ? 1 : 0, rows, nbatch,
+             nkb, out);
+  probe_end(s.stream, pe);
+}
+
+template <int BN>
+void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
+  constexpr u32 kStage = 8 * (kM * kKB + BN * kKB);
+  const size_t smem = kStages * kStage;
+  static bool attr = false;
+  if (!attr) {
+    MPCG_CUDA(cudaFuncSetAttribute(ring_gemm_tc2<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  Tc2Args P{};
+  P.g = a;
+  P.nkb = (a.K + kKB - 1) / kKB;
+  const u32 ntiles = (a.N + BN - 1) / BN, mtiles = (a.M + kM - 1) / kM;
+  // right operand: batched only when some segment's R has a batch stride
+  bool rbatched = false;
+  for (int i = 0; i < a.nslots; ++i)
+    for (int g = 0; g < a.sl[i].nseg; ++g) rbatched |= a.sl[i].sR[g] != 0;
+  const u32 rb = rbatched ? a.nbatch : 1;
+  std::vector<std::shared_ptr<Block>> keep;
+  for (int i = 0; i < a.nslots; ++i) {
+    const u64 rbytes = u64(ntiles) * P.nkb * a.sl[i].nseg * 8 * BN * kKB;
+    auto blk = s.raw((rbytes * rb + 7) / 8);
+    keep.push_back(blk);
+    launch_pack<BN>(s, a, i, false, a.N, rb, P.nkb, reinterpret_cast<char*>(blk->ptr));
+    P.Rpk[i] = reinterpret_cast<const char*>(blk->ptr);
+    P.Rpk_b = rbatched ? rbytes : 0;
+    if (packL) {
+      const u64 lbytes = u64(mtiles) * P.nkb * a.sl[i].nseg * 8 * kM * kKB;
+      auto lb = s.raw((lbytes * a.nbatch + 7) / 8);
+      keep.push_back(lb);
+      launch_pack<kM>(s, a, i, true, a.M, a.nbatch, P.nkb, reinterpret_cast<char*>(lb->ptr));
+      P.Lpk[i] = reinterpret_cast<const char*>(lb->ptr);
+      P.Lpk_b = lbytes;
+    }
+  }
+  bool vec = (a.K % 2) == 0;
+  for (int i = 0; i < a.nslots && vec; ++i)
+    for (int g = 0; g < a.sl[i].nseg; ++g) {
+      const GemmSlotArgs& S = a.sl[i];
+      if (S.lk[g] == kOpMem || S.lk[g] == kOpSum)
+        vec = vec && reinterpret_cast<uintptr_t>(S.L[g]) % 16 == 0 && S.sL[g] % 2 == 0;
+      if (S.lk[g] == kOpSum) vec = vec && reinterpret_cast<uintptr_t>(S.L2[g]) % 16 == 0;
+    }
+  P.vec = vec ? 1 : 0;
+  dim3 grid(ntiles, mtiles, a.nslots * a.nbatch);
+  cudaEvent_t pe;
+  probe_begin(s.stream, &pe);
+  launch_pdl(ring_gemm_tc2<BN>, grid, dim3(kThreads), smem, s.stream, P);
+  probe_end(s.stream, pe);
+  // the packed buffers are stream-ordered pool blocks (or graph-arena blocks): released
+  // after the GEMM's queued reads by the Block destructor
+}
+
+}  // namespace
+
+int& tc2_mode() {  // 1 = warp-specialised tcgen05 path enabled (default), 0 = off (MPCG_TC2=0)
+  static int mode = [] {
+    const char* e = std::getenv("MPCG_TC2");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return mode;
+}
+
+bool ring_gemm_tc2_wants(const GemmArgs& a) {
+  if (tc2_mode() == 0 || tc_gemm_mode() == 0) return false;
+  int maxseg = 0;
+  for (int i = 0; i < a.nslots; ++i) maxseg = a.sl[i].nseg > maxseg ? a.sl[i].nseg : maxseg;
+  if (u64(maxseg) * a.K > kMaxKPrime) return false;
+  if (a.ksplit > 1) return false;
+  const double work = double(a.M) * a.N * a.K * maxseg * a.nbatch * a.nslots;
+  return tc_gemm_mode() == 1 || (a.M >= 128 && a.N >= 16 && work >= 3e7);
+}
+
+bool ring_gemm_tc2_try(Session& s, const GemmArgs& a) {
+  if (!ring_gemm_tc2_wants(a)) return false;
+  for (int i = 0; i < a.nslots; ++i)
+    for (int g = 0; g < a.sl[i].nseg; ++g) {
+      const GemmSlotArgs& S = a.sl[i];
+      if (S.sL[g] != S.sL[0]) return false;  // the producer uses one row stride for every segment
+    }
+  const bool multiN = a.N > 64;
+  if (a.N > 32)
+    launch_tc2<64>(s, a, multiN);
+  else if (a.N > 16)
+    launch_tc2<32>(s, a, false);
+  else
+    launch_tc2<16>(s, a, false);
+  s.check();
+  return true;
+}
+
+}  // namespace mpcg

@@ -623,86 +623,118 @@ DT max_last_dim(Session& s, const DT& x, size_t L, const std::string& tag) {
 }
 
 namespace {
-struct SinkExpInit {  // y = w + trunc(w^2, f+1) + [p0] 2^f   (H/nonlinear/approx.hpp:27-31)
-  CPtr2 x;
-  Ptr2 y;
-  int f, it;
-  __device__ void operator()(int slot, int party, u64 g, u64 z) const {
-    y.p[slot][g] = sar64(x.p[slot][g], it) + sar64(z, f + 1) + (party == 0 ? (u64(1) << f) : 0);
+// exp chain (H/nonlinear/approx.hpp:22-39) as ONE fused square chain: round 0 squares
+// w = trunc(x, it) and forms y = w + trunc(w^2, f+1) + [p0] 2^f; rounds 1..it square y with
+// truncation by f; the last y goes to of(slot, party, g, y).
+template <class XF, class OF>
+struct ExpY {
+  XF xsrc;
+  OF of;
+  int it, f, first, last;
+  __device__ u64 operator()(int slot, int party, u64 g, u64 z) const {
+    const u64 y = first ? sar64(xsrc(slot, g), it) + sar64(z, f + 1) + (party == 0 ? (u64(1) << f) : 0)
+                        : sar64(z, f);
+    if (last) of(slot, party, g, y);
+    return y;
   }
 };
+template <class XF>
+struct SarOf {  // w = trunc(x, it), the first squared value
+  XF x;
+  int it;
+  __device__ u64 operator()(int slot, u64 g) const { return sar64(x(slot, g), it); }
+};
+struct OutStore {  // out[g] = y
+  Ptr2 out;
+  __device__ void operator()(int slot, int, u64 g, u64 y) const { out.p[slot][g] = y; }
+};
+struct OutAffine {  // out[g] = k*y + [p0] c   (reciprocal seed 3 exp + 0.003; sigmoid's 1 + exp)
+  Ptr2 out;
+  u64 k, c;
+  __device__ void operator()(int slot, int party, u64 g, u64 y) const {
+    out.p[slot][g] = y * k + (party == 0 ? c : 0);
+  }
+};
+struct SrcConstMinus {  // [p0] c - x[g]   (reciprocal seed argument 0.5 - x)
+  Pid2 pid;
+  CPtr2 x;
+  u64 c;
+  __device__ u64 operator()(int slot, u64 g) const { return (pid.v[slot] == 0 ? c : 0) - x.p[slot][g]; }
+};
+
+template <class XF, class OF>
+void exp_chain(Session& s, const Shape& shape, const std::string& tag, int square_iters, XF xsrc, OF of) {
+  const int f = s.cfg.frac_bits;
+  const size_t n = shape_numel(shape);
+  std::vector<Triple> tr;
+  std::vector<std::string> tags;
+  tags.push_back(tag + ".w2");
+  for (int i = 0; i < square_iters; ++i) tags.push_back(tag + ".sq" + std::to_string(i));
+  for (auto& t : tags) {
+    tr.push_back(s.fetch(TripleSpec::square_of(shape), t));
+    tr.back().mark_consumed();
+  }
+  const int R = int(tr.size());
+  square_chain(s, n, chunks_for(s, n), tr, tags, SarOf<XF>{xsrc, square_iters}, [&](int r) {
+    return ExpY<XF, OF>{xsrc, of, square_iters, f, r == 0 ? 1 : 0, r == R - 1 ? 1 : 0};
+  });
+}
 }  // namespace
 
 DT exp_shares(Session& s, const DT& x, const std::string& tag, int square_iters) {
-  const int f = s.cfg.frac_bits;
-  const size_t n = x.numel();
-  const int ch = chunks_for(s, n);
   DT y = s.alloc(x.shape, x.scale);
-  {
-    Triple t = s.fetch(TripleSpec::square_of(x.shape), tag + ".w2");
-    t.mark_consumed();
-    square_op(s, t.ew, n, ch, tag + ".w2", SrcSar{cptrs(x), square_iters},
-              SinkExpInit{cptrs(x), ptrs(y), f, square_iters});
-  }
-  for (int i = 0; i < square_iters; ++i) {
-    Triple t = s.fetch(TripleSpec::square_of(x.shape), tag + ".sq" + std::to_string(i));
-    t.mark_consumed();
-    square_op(s, t.ew, n, ch, tag + ".sq" + std::to_string(i), SrcMem{cptrs(y)}, SinkTrunc{ptrs(y), f});
-  }
+  exp_chain(s, x.shape, tag, square_iters, SrcMem{cptrs(x)}, OutStore{ptrs(y)});
   return y;
 }
 
 namespace {
-struct SinkNewtonU {  // u = [p0] 2^(f+1) - trunc(x*y, f)
-  Ptr2 u;
-  int f;
-  __device__ void operator()(int slot, int party, u64 g, u64 z) const {
-    u.p[slot][g] = (party == 0 ? (u64(2) << f) : 0) - sar64(z, f);
+// Newton steps of reciprocal_shares (H/nonlinear/approx.hpp:52-60) as one fused mul chain:
+// after xy_i: u = [p0] 2^(f+1) - trunc(x*y, f), next eps/delta = (y, u);
+// after yu_i: y = trunc(y*u, f) (stored), next eps/delta = (x, y).
+struct RecipPV {
+  CPtr2 x;
+  Ptr2 y;
+  int f, odd;
+  __device__ u64 val(int slot, int party, u64 g, u64 z) const {
+    if (!odd) return (party == 0 ? (u64(2) << f) : 0) - sar64(z, f);
+    const u64 v = sar64(z, f);
+    y.p[slot][g] = v;
+    return v;
   }
+  __device__ u64 nx(int slot, u64 g, u64) const { return odd ? x.p[slot][g] : y.p[slot][g]; }
+  __device__ u64 ny(int, u64, u64 v) const { return v; }
 };
 }  // namespace
 
 DT reciprocal_shares(Session& s, const DT& x, const std::string& tag, int newton_iters) {
   const int f = s.cfg.frac_bits;
   const size_t n = x.numel();
-  const int ch = chunks_for(s, n);
-  // t = 0.5 - x ; y0 = 3 exp(t) + 0.003  (H/nonlinear/approx.hpp:49-51)
-  const u64 half = encode_fixed(0.5, f);
-  const u64 c003 = encode_fixed(0.003, f);
-  DT t0 = s.alloc(x.shape, x.scale);
-  {
-    const Pid2 pid = pids(s);
-    const CPtr2 xp = cptrs(x);
-    const Ptr2 tp = ptrs(t0);
-    launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) {
-      tp.p[slot][i] = (pid.v[slot] == 0 ? half : 0) - xp.p[slot][i];
-    });
-  }
-  DT e = exp_shares(s, t0, tag + ".seed");
+  // y0 = 3 exp(0.5 - x) + 0.003  (H/nonlinear/approx.hpp:49-51), the seed exp fused in
   DT y = s.alloc(x.shape, x.scale);
-  {
-    const Pid2 pid = pids(s);
-    const CPtr2 ep = cptrs(e);
-    const Ptr2 yp = ptrs(y);
-    launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) {
-      yp.p[slot][i] = ep.p[slot][i] * 3 + (pid.v[slot] == 0 ? c003 : 0);
-    });
-  }
-  DT u = s.alloc(x.shape, x.scale);
+  exp_chain(s, x.shape, tag + ".seed", 7, SrcConstMinus{pids(s), cptrs(x), encode_fixed(0.5, f)},
+            OutAffine{ptrs(y), 3, encode_fixed(0.003, f)});
+  if (newton_iters <= 0) return y;
+  std::vector<Triple> tr;
+  std::vector<std::string> tags;
   for (int i = 0; i < newton_iters; ++i) {
-    Triple t1 = s.fetch(TripleSpec::elementwise(TripleKind::Arith, x.shape), tag + ".xy" + std::to_string(i));
-    t1.mark_consumed();
-    mul_op(s, t1.ew, n, ch, tag + ".xy" + std::to_string(i), SrcMem{cptrs(x)}, SrcMem{cptrs(y)},
-           SinkNewtonU{ptrs(u), f});
-    Triple t2 = s.fetch(TripleSpec::elementwise(TripleKind::Arith, x.shape), tag + ".yu" + std::to_string(i));
-    t2.mark_consumed();
-    mul_op(s, t2.ew, n, ch, tag + ".yu" + std::to_string(i), SrcMem{cptrs(y)}, SrcMem{cptrs(u)},
-           SinkTrunc{ptrs(y), f});
+    tags.push_back(tag + ".xy" + std::to_string(i));
+    tags.push_back(tag + ".yu" + std::to_string(i));
   }
+  for (auto& t : tags) {
+    tr.push_back(s.fetch(TripleSpec::elementwise(TripleKind::Arith, x.shape), t));
+    tr.back().mark_consumed();
+  }
+  mul_chain(s, n, chunks_for(s, n), tr, tags, SrcMem{cptrs(x)}, SrcMem{cptrs(y)},
+            [&](int r) { return RecipPV{cptrs(x), ptrs(y), f, r & 1}; });
   return y;
 }
 
 namespace {
+struct SrcSubRowMax {  // x[g] - m[g / L]
+  CPtr2 x, m;
+  u32 L;
+  __device__ u64 operator()(int slot, u64 g) const { return x.p[slot][g] - m.p[slot][u32(g) / L]; }
+};
 struct SrcBcast {  // r[g / L]
   CPtr2 r;
   u32 L;
@@ -715,16 +747,8 @@ DT softmax_shares(Session& s, const DT& x, size_t L, const std::string& tag) {
   const size_t n = x.numel();
   const int ch = chunks_for(s, n);
   DT mx = max_last_dim(s, x, L, tag + ".max");
-  DT centered = s.alloc(Shape{outer, L}, x.scale);
-  {
-    const CPtr2 xp = cptrs(x), mp = cptrs(mx);
-    const Ptr2 cp = ptrs(centered);
-    const u32 LL = u32(L);
-    launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) {
-      cp.p[slot][i] = xp.p[slot][i] - mp.p[slot][u32(i) / LL];
-    });
-  }
-  DT e = exp_shares(s, centered, tag + ".exp");
+  DT e = s.alloc(Shape{outer, L}, x.scale);  // exp(x - max), the centring fused into the exp chain
+  exp_chain(s, Shape{outer, L}, tag + ".exp", 7, SrcSubRowMax{cptrs(x), cptrs(mx), u32(L)}, OutStore{ptrs(e)});
   DT rowsum = s.alloc(Shape{outer, 1}, x.scale);
   {
     const CPtr2 ep = cptrs(e);
@@ -803,8 +827,9 @@ DT sigmoid_shares(Session& s, const DT& x, const std::string& tag) {
   DT b = s.alloc(x.shape, 0), nabs = s.alloc(x.shape, x.scale);
   compare_mul(s, n, adder_for(s, n), tag + ".msb", tag + ".b2a", ch, tag + ".abs", ch, SrcMem{cptrs(x)},
               SrcMem{cptrs(x)}, SinkNegAbs{cptrs(x), ptrs(nabs)}, ptrs(b));
-  DT e = exp_shares(s, nabs, tag + ".exp");
-  DT r = reciprocal_shares(s, add_public(s, e, u64(1) << f), tag + ".recip");
+  DT d = s.alloc(x.shape, x.scale);  // 1 + exp(-|x|), the +1 fused into the exp chain's last round
+  exp_chain(s, x.shape, tag + ".exp", 7, SrcMem{cptrs(nabs)}, OutAffine{ptrs(d), 1, u64(1) << f});
+  DT r = reciprocal_shares(s, d, tag + ".recip");
   Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Arith, x.shape), tag + ".sel");
   t.mark_consumed();
   DT out = s.alloc(x.shape, x.scale);

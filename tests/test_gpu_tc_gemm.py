@@ -11,13 +11,16 @@ pytestmark = pytest.mark.gpu
 PHI = 0x9E3779B97F4A7C15
 
 
-@pytest.fixture
-def tc():
+@pytest.fixture(params=["tc2", "tc1"])
+def tc(request):
+    """Tensor cores forced on; tc2 = warp-specialised pipeline, tc1 = first-generation kernel."""
     import paper_2209_13643_b200 as mp
     from paper_2209_13643_b200 import api
     api.set_gemm_mode("tc")
+    api.set_tc2(request.param == "tc2")
     yield mp
     api.set_gemm_mode("auto")
+    api.set_tc2(True)
 
 
 def _run(mp, X, Y, tb, tag, chunks=1):
@@ -33,7 +36,8 @@ def _run(mp, X, Y, tb, tag, chunks=1):
 
 @pytest.mark.parametrize("M,K,N", [(128, 32, 32), (256, 64, 64), (300, 100, 48), (128, 576, 64),
                                    (1000, 150, 16), (257, 1000, 130), (300, 25, 6), (129, 33, 7),
-                                   (6400, 150, 16), (4000, 25, 6)])
+                                   (6400, 150, 16), (4000, 25, 6), (640, 96, 256), (512, 1152, 128),
+                                   (384, 64, 200)])
 def test_tc_gemm_random(tc, M, K, N):
     from oracle import mpc_oracle as O
     r = O.CounterRng(M * 7 + K * 3 + N)
@@ -73,3 +77,19 @@ def test_tc_gemm_model_parity(tc):
     z = ex.run(s.deal_input(tc.demo_input(g, 13), 2)).numpy()
     assert np.array_equal(z[0].reshape(-1), m["z0"].reshape(-1))
     assert np.array_equal(z[1].reshape(-1), m["z1"].reshape(-1))
+
+
+def test_tc_public_gemm_model_path(tc):
+    """Public-weight products (one memory segment) through the tensor-core kernels."""
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for name in ("toy_cnn", "toy_transformer"):
+        m = np.load(os.path.join(root, "tests", "golden", f"model_{name}_" +
+                                 ("pipelined_public_it1.npz" if name == "toy_cnn" else "blocking_public_it1.npz")))
+        g = tc.ModelGraph.from_json(os.path.join(root, "configs", name + ".json"))
+        s = tc.Session(device=0, n_local=2, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
+        ex = tc.SecureExecutor(s, g, public_weights=True, pipelined=name == "toy_cnn")
+        ex.deal_weights(tc.init_weights(g, 12), 1)
+        z = ex.run(s.deal_input(tc.demo_input(g, 13), 2)).numpy()
+        assert np.array_equal(z[0].reshape(-1), m["z0"].reshape(-1))
+        assert np.array_equal(z[1].reshape(-1), m["z1"].reshape(-1))

@@ -66,5 +66,8 @@ def dump(cfg):
 if __name__ == "__main__":
     dump(resnet("resnet18", [128, 3, 32, 32], [64, 128, 256, 512], [2, 2, 2, 2], 10))
     dump(resnet("toy_resnet", [2, 3, 8, 8], [4, 8], [1, 1], 10))
-    dump(bert("bert_base", [8, 128, 768], 12, 12, 3072))
+    # frac 16 (CrypTen's default, the reference MLP's): the reference's 2PC truncation (local sar,
+    # H/protocols/trunc.hpp:25-42) fails with probability ~|x|/2^64 per element, and BERT-base
+    # truncates ~1.7e9 values per inference — at frac 20 that is tens of 2^(64-f) errors.
+    dump(bert("bert_base", [8, 128, 768], 12, 12, 3072, frac_bits=16))
     dump(bert("toy_bert", [2, 8, 16], 2, 2, 32))

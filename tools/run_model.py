@@ -83,7 +83,10 @@ for mode in (["blocking", "pipelined"] if a.mode == "both" else [a.mode]):
         ref = O.reference_forward(go, w, x)
         zz = z.numpy()
         dec = (zz[0] + zz[1]).view(np.int64).astype(np.float64) * 2.0 ** -g.frac_bits
-        res["max_abs_err_vs_plaintext"] = float(np.abs(dec.reshape(-1) - ref.reshape(-1)).max())
+        err = np.abs(dec.reshape(-1) - ref.reshape(-1))
+        res["max_abs_err_vs_plaintext"] = float(err.max())
+        res["frac_within_2^-6"] = float((err <= 2.0 ** -6).mean())
+        res["median_abs_err"] = float(np.median(err))
     out[mode] = res
     print(json.dumps({mode: {k: v for k, v in res.items() if k != "per_layer_ms"}}), flush=True)
     del ex
