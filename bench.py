@@ -45,7 +45,6 @@ def parse():
     ap.add_argument("--weights", default="private", choices=["private", "public"])
     ap.add_argument("--no-blocking", action="store_true", help="skip the blocking comparison pass")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
-    ap.add_argument("--probe", default="adder_round", choices=["adder_round", "gemm"])
     ap.add_argument("--link", default="",
                     help="emulate a LAN/WAN link between the parties, e.g. 10gbps (1.25e9 B/s, 0.1 ms) or "
                          "'<latency_s>,<bytes_per_s>'; default: the real in-device / NVLink transport")
@@ -108,6 +107,31 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
                 "reasons": reasons, "samples": len(rows)}
+
+
+def measure_int8_peak():
+    """Dense int8 tensor throughput of this GPU: cuBLASLt IMMA via torch._int_mm on 8192^3,
+    best of 5 (burst), CUDA events. Falls back to the 4.5 POPS datasheet figure."""
+    try:
+        import torch
+        n = 8192
+        a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+        b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+        for _ in range(3):
+            torch._int_mm(a, b)
+        best = None
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            e1.synchronize()
+            t = e0.elapsed_time(e1) / 1e3
+            best = t if best is None else min(best, t)
+        del a, b
+        return 2.0 * n ** 3 / best / 1e12, "measured: torch._int_mm 8192^3 best of 5"
+    except Exception as e:  # noqa: BLE001
+        return 4500.0, "fallback: 4.5 POPS dense int8 datasheet (" + repr(e)[:60] + ")"
 
 
 # ----------------------------------------------------------------------------- reference
@@ -259,13 +283,16 @@ def main():
     s, ex, x = setup(a.mode)
     eager_ms, _, _, _ = timed(s, ex, x, max(3, a.steps // 4), 2, graph=False)
 
-    # ---- roofline probe: device time of every launch of the dominant kernel class (eager steps)
-    barrier(s)
-    api.probe_start(a.probe)
-    for _ in range(a.steps):
-        ex.run(x)
-    s.sync()
-    p_ms, p_launches, p_units = api.probe_stop()
+    # ---- roofline probes: device time of every launch of each kernel class (eager steps, CUDA
+    # events on the session stream around each launch of the class)
+    probes = {}
+    for cls in ("adder_round", "beaver", "chain", "gemm"):
+        barrier(s)
+        api.probe_start(cls)
+        for _ in range(a.steps):
+            ex.run(x)
+        s.sync()
+        probes[cls] = api.probe_stop()
 
     ex.time_layers(True)   # per-layer CUDA events recorded inside the graph
     ex.capture(x)
@@ -332,27 +359,40 @@ def main():
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except OSError:
         pass
-    traffic = None
+    traffic = {}
     try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        traffic = prof.get(a.probe, {}).get("dram_bytes_per_launch")
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
     except (OSError, ValueError):
         pass
-    if a.probe == "adder_round":
-        hbm = peaks.get("hbm_gbs")
-        achieved = (p_units / 1e9) / (p_ms / 1e3) if p_ms > 0 else 0.0
-        roof = {"bound": "hbm", "kernel": "ew_kernel<AdderRound> (SPK level round: settle r, issue r+1)",
-                "achieved": achieved, "peak": hbm or 6650.0, "unit": "GB/s",
-                "frac": achieved / (hbm or 6650.0), "traffic": traffic,
-                "peak_source": "measured" if hbm else "fallback",
-                "launches": p_launches, "avg_launch_us": p_ms * 1e3 / max(1, p_launches),
-                "algorithmic_bytes_per_launch": p_units / max(1, p_launches),
-                "note": "96 B/element/party per level round (2x32 B wire + 8x(2 in + 2 out)); separate probed pass"}
-    else:
-        macs = p_units
-        achieved = macs / (p_ms / 1e3) / 1e12 if p_ms > 0 else 0.0
-        roof = {"bound": "tensor", "kernel": "ring GEMM", "achieved": achieved, "peak": None, "unit": "T ring-MAC/s",
-                "frac": None, "traffic": traffic, "launches": p_launches}
+    hbm = peaks.get("hbm_gbs")
+    hbm_peak = hbm or 6650.0
+    int8_peak, int8_src = measure_int8_peak()
+    # algorithmic units per class: bytes for the HBM-bound protocol rounds, ring MACs
+    # for the GEMM (x36 int8 MACs = 72 int8 ops each, the limb-pair products of the tcgen05 path)
+    notes = {"adder_round": "SPK level round (settle r, issue r+1): 96 B/elem/party = 2x32 B wire + 8x(2 in + 2 out)",
+             "beaver": "Beaver mul/square rounds incl. fused exp/Newton chains: 56 / 32 B/elem/party per op",
+             "chain": "persistent compare-and-select chain (ReLU/tournament): 512 B/elem/party",
+             "gemm": "ring GEMM main kernel: 72 int8 ops per ring MAC (36 limb-pair MACs), packing excluded"}
+    rooflines = []
+    for cls, (p_ms, p_launches, p_units) in probes.items():
+        if p_launches == 0 or p_ms <= 0:
+            continue
+        if cls == "gemm":
+            ach = 72.0 * p_units / (p_ms / 1e3) / 1e12
+            r = {"kernel": cls, "bound": "tensor", "achieved": ach, "peak": int8_peak, "unit": "TOP/s (int8)",
+                 "frac": ach / int8_peak, "peak_source": int8_src}
+        else:
+            ach = (p_units / 1e9) / (p_ms / 1e3)
+            r = {"kernel": cls, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                 "frac": ach / hbm_peak, "peak_source": "measured" if hbm else "fallback"}
+        r.update({"launches": p_launches, "device_ms_per_step": p_ms / a.steps,
+                  "avg_launch_us": p_ms * 1e3 / p_launches, "units_per_launch": p_units / p_launches,
+                  "traffic": (traffic.get(cls) or {}).get("dram_bytes_per_launch"), "note": notes[cls]})
+        rooflines.append(r)
+    rooflines.sort(key=lambda r: -r["device_ms_per_step"])
+    roof = dict(rooflines[0]) if rooflines else None  # the dominant class of the step
+    if roof:
+        roof["share_of_probed_ms"] = roof["device_ms_per_step"] / sum(r["device_ms_per_step"] for r in rooflines)
 
     pipelined_ms = ms_step
     value = B * pairs / (ms_step / 1e3)
@@ -377,6 +417,7 @@ def main():
                    "logits_hash_slot0": mp.fnv1a_words(dec) if world == 1 else None,
                    "blocking": blocking},
         "roofline": roof,
+        "rooflines": rooflines,
         "cpu_baseline": cpu,
         "e2e": {"value": B * pairs / e2e_s, "unit": "inferences/s", "ms_per_step": e2e_s * 1e3,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -267,7 +267,7 @@ def launch_count() -> int:
     return int(N.lib().mpcg_launch_count())
 
 
-KERNEL_CLASS = {"adder_round": 1, "gemm": 2}
+KERNEL_CLASS = {"adder_round": 1, "gemm": 2, "beaver": 3, "chain": 4}
 
 
 def probe_start(kernel_class="adder_round"):

@@ -87,6 +87,19 @@ struct EwTriple {
   u64 off;        // global offset of this shard inside each half
   int square;     // B == A as a secret; only A drawn
   int bin;        // XOR sharing + AND product
+  // draw c of element g is mix(key + (base + g)*phi) = mix((key + base*phi) + g*phi): the
+  // base*phi terms of the five streams are host constants (set_phis), so a thread pays one
+  // 64-bit multiply (g*phi) per element instead of one per draw.
+  u64 pA, pB, pra, prb, prc;
+  __host__ void set_phis() {
+    const u64 nbd = square ? 0 : mg;
+    const u64 baseA = 1 + mg + nbd, baseB = baseA + mg;
+    pA = kPhi;
+    pB = square ? kPhi : (1 + mg) * kPhi;
+    pra = baseA * kPhi;
+    prb = baseB * kPhi;
+    prc = (baseB + mg) * kPhi;
+  }
 };
 
 __device__ __forceinline__ u64 tkey(u64 key, const u64* kp) { return kp ? __ldg(kp) : key; }
@@ -101,17 +114,15 @@ struct Dw {
 template <bool WithC>
 __device__ __forceinline__ Dw ew_draw(const EwTriple& t, u64 g, bool p0) {
   const u64 key = tkey(t.key, t.kp);
-  const u64 nbd = t.square ? 0 : t.mg;
-  const u64 baseA = 1 + t.mg + nbd;
-  const u64 baseB = baseA + t.mg;
+  const u64 gp = g * kPhi;
   Dw d;
-  d.ra = drw(key, baseA + g);
-  d.rb = drw(key, baseB + g);
-  d.rc = WithC ? drw(key, baseB + t.mg + g) : 0;
+  d.ra = mix64(key + t.pra + gp);
+  d.rb = mix64(key + t.prb + gp);
+  d.rc = WithC ? mix64(key + t.prc + gp) : 0;
   d.A = d.B = 0;
   if (p0) {
-    d.A = drw(key, 1 + g);
-    d.B = t.square ? d.A : drw(key, 1 + t.mg + g);
+    d.A = mix64(key + t.pA + gp);
+    d.B = t.square ? d.A : mix64(key + t.pB + gp);
   }
   return d;
 }
@@ -148,23 +159,23 @@ __device__ __forceinline__ void ew_abc(const EwTriple& t, int party, u64 g, u64&
 // Square triples only need a and c (b is never used by the combine).
 __device__ __forceinline__ void sq_ac(const EwTriple& t, int party, u64 g, u64& a, u64& c) {
   const u64 key = tkey(t.key, t.kp);
-  const u64 baseA = 1 + t.mg;
-  const u64 baseC = baseA + 2 * t.mg;
-  const u64 ra = drw(key, baseA + g), rc = drw(key, baseC + g);
+  const u64 gp = g * kPhi;
+  const u64 ra = mix64(key + t.pra + gp), rc = mix64(key + t.prc + gp);
   if (party != 0) {
     a = ra;
     c = rc;
     return;
   }
-  const u64 A = drw(key, 1 + g);
+  const u64 A = mix64(key + t.pA + gp);
   a = A - ra;
   c = A * A - rc;
 }
 
 __device__ __forceinline__ u64 sq_a(const EwTriple& t, int party, u64 g) {
   const u64 key = tkey(t.key, t.kp);
-  const u64 ra = drw(key, 1 + t.mg + g);
-  return party != 0 ? ra : drw(key, 1 + g) - ra;
+  const u64 gp = g * kPhi;
+  const u64 ra = mix64(key + t.pra + gp);
+  return party != 0 ? ra : mix64(key + t.pA + gp) - ra;
 }
 
 // Matmul triple (H/sharing/triple.hpp:96-114): draws A (na), B (nb), then r_A, r_B, r_C.
@@ -173,19 +184,25 @@ struct MmTriple {
   const u64* kp;
   u64 na, nb, nc;     // global numels
   u64 offA, offB, offC;
+  u64 pA, pB, prA, prB, prC;  // (stream base + shard offset) * phi, see EwTriple::set_phis
+  __host__ void set_phis() {
+    pA = (1 + offA) * kPhi;
+    pB = (1 + na + offB) * kPhi;
+    prA = (1 + na + nb + offA) * kPhi;
+    prB = (1 + 2 * na + nb + offB) * kPhi;
+    prC = (1 + 2 * na + 2 * nb + offC) * kPhi;
+  }
 };
-__device__ __forceinline__ u64 mm_A(const MmTriple& t, u64 i) { return drw(tkey(t.key, t.kp), 1 + t.offA + i); }
-__device__ __forceinline__ u64 mm_B(const MmTriple& t, u64 j) {
-  return drw(tkey(t.key, t.kp), 1 + t.na + t.offB + j);
-}
+__device__ __forceinline__ u64 mm_A(const MmTriple& t, u64 i) { return mix64(tkey(t.key, t.kp) + t.pA + i * kPhi); }
+__device__ __forceinline__ u64 mm_B(const MmTriple& t, u64 j) { return mix64(tkey(t.key, t.kp) + t.pB + j * kPhi); }
 __device__ __forceinline__ u64 mm_rA(const MmTriple& t, u64 i) {
-  return drw(tkey(t.key, t.kp), 1 + t.na + t.nb + t.offA + i);
+  return mix64(tkey(t.key, t.kp) + t.prA + i * kPhi);
 }
 __device__ __forceinline__ u64 mm_rB(const MmTriple& t, u64 j) {
-  return drw(tkey(t.key, t.kp), 1 + 2 * t.na + t.nb + t.offB + j);
+  return mix64(tkey(t.key, t.kp) + t.prB + j * kPhi);
 }
 __device__ __forceinline__ u64 mm_rC(const MmTriple& t, u64 k) {
-  return drw(tkey(t.key, t.kp), 1 + 2 * t.na + 2 * t.nb + t.offC + k);
+  return mix64(tkey(t.key, t.kp) + t.prC + k * kPhi);
 }
 
 // ------------------------------------------------------------------ launch helpers

@@ -260,6 +260,7 @@ Triple Session::fetch(const TripleSpec& spec, const std::string& tag, bool batch
     t.ew.mg = stacked ? 2 * t.ew.ghalf : t.ew.ghalf;
     t.ew.square = spec.square;
     t.ew.bin = spec.kind == TripleKind::Bin;
+    t.ew.set_phis();
   } else {
     const Shape& a = spec.shape_a;
     const Shape& b = spec.shape_b;
@@ -278,6 +279,7 @@ Triple Session::fetch(const TripleSpec& spec, const std::string& tag, bool batch
     t.mm.offB = bb ? dp_offset(nb) : 0;
     t.mm.nc = dp_global(nc);
     t.mm.offC = dp_offset(nc);
+    t.mm.set_phis();
   }
   return t;
 }

@@ -124,6 +124,8 @@ void mul_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::stri
   chunks = clamp_chunks(chunks, m);
   std::vector<Open> opens(static_cast<size_t>(chunks));
   const Pid2 pid = pids(s);
+  // beaver_mul = 2 x 16 B wire + 8 x (2 in + 1 out) = 56 B/elem/party over build + combine
+  ClassScope cs(kClsBeaver, 28.0 * double(m / chunks) * s.n_local);
   for (int k = 0; k < chunks; ++k) {
     const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
     opens[k] = s.begin_open(2 * (hi - lo), Reduce::Sum);
@@ -176,6 +178,8 @@ void square_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::s
   chunks = clamp_chunks(chunks, m);
   std::vector<Open> opens(static_cast<size_t>(chunks));
   const Pid2 pid = pids(s);
+  // beaver_square = 2 x 8 B wire + 8 x (1 in + 1 out) = 32 B/elem/party over build + combine
+  ClassScope cs(kClsBeaver, 16.0 * double(m / chunks) * s.n_local);
   for (int k = 0; k < chunks; ++k) {
     const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
     opens[k] = s.begin_open(hi - lo, Reduce::Sum);
@@ -205,11 +209,11 @@ struct Sw {
 };
 __device__ __forceinline__ Sw sq_draw(const EwTriple& t, u64 g, bool p0, bool with_c) {
   const u64 key = tkey(t.key, t.kp);
-  const u64 baseA = 1 + t.mg;
+  const u64 gp = g * kPhi;
   Sw d;
-  d.ra = drw(key, baseA + g);
-  d.rc = with_c ? drw(key, baseA + 2 * t.mg + g) : 0;
-  d.A = p0 ? drw(key, 1 + g) : 0;
+  d.ra = mix64(key + t.pra + gp);
+  d.rc = with_c ? mix64(key + t.prc + gp) : 0;
+  d.A = p0 ? mix64(key + t.pA + gp) : 0;
   return d;
 }
 __device__ __forceinline__ u64 sq_share_a(int party, const Sw& d) { return party ? d.ra : d.A - d.ra; }
@@ -278,6 +282,8 @@ void square_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& t
   const Pid2 pid = pids(s);
   auto ctag = [&](int r, int k) { return chunks == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
   std::vector<Open> hs(static_cast<size_t>(chunks));
+  // R squares x 32 B/elem/party spread over the R+1 fused launches of a lane
+  ClassScope cs(kClsBeaver, 32.0 * R / (R + 1) * double(n / chunks) * s.n_local);
   for (int k = 0; k < chunks; ++k) {
     const auto rg = chunk_range(n, chunks, k);
     hs[k] = s.begin_open(rg.second - rg.first, Reduce::Sum);
@@ -356,6 +362,8 @@ void mul_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, 
   const Pid2 pid = pids(s);
   auto ctag = [&](int r, int k) { return chunks == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
   std::vector<Open> hs(static_cast<size_t>(chunks));
+  // R multiplies x 56 B/elem/party spread over the R+1 fused launches of a lane
+  ClassScope cs(kClsBeaver, 56.0 * R / (R + 1) * double(n / chunks) * s.n_local);
   for (int k = 0; k < chunks; ++k) {
     const auto rg = chunk_range(n, chunks, k);
     const size_t w = rg.second - rg.first;

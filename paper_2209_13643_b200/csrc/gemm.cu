@@ -166,14 +166,15 @@ __global__ void __launch_bounds__(256) ring_gemv(GemmArgs a) {
   bool needB = false, needRB = false, needF = false;
   for (int g = 0; g < S.nseg; ++g) {
     const int rk = S.rk[g];
-    needB |= rk == kOpB || rk == kOpB0F;
+    needB |= rk == kOpB || rk == kOpB0F || rk == kOpBF;
     needRB |= rk == kOpRB || rk == kOpB0F;
-    needF |= rk == kOpSum || rk == kOpB0F;
+    needF |= rk == kOpSum || rk == kOpB0F || rk == kOpBF || rk == kOpNegSum;
   }
   const u64* Fo = nullptr;
   const u64* Fp = nullptr;
   for (int g = 0; g < S.nseg; ++g)
-    if (S.rk[g] == kOpSum || S.rk[g] == kOpB0F) Fo = S.R[g], Fp = S.R2[g];
+    if (S.rk[g] == kOpSum || S.rk[g] == kOpB0F || S.rk[g] == kOpBF || S.rk[g] == kOpNegSum)
+      Fo = S.R[g], Fp = S.R2[g];
   u64 acc[MR];
 #pragma unroll
   for (int m = 0; m < MR; ++m) acc[m] = 0;
@@ -200,6 +201,8 @@ __global__ void __launch_bounds__(256) ring_gemv(GemmArgs a) {
           case kOpSum: r = F; break;
           case kOpB: r = B; break;
           case kOpB0F: r = (B - rB) + F; break;
+          case kOpBF: r = B + F; break;
+          case kOpNegSum: r = u64(0) - F; break;
           default: r = rB; break;
         }
 #pragma unroll
@@ -234,9 +237,12 @@ void launch_gemv(Session& s, GemmArgs a) {
   probe_end(st, pe);
 }
 
-bool gemv_eligible(const GemmArgs& a) { return a.M <= u32(kGvM) && a.nbatch == 1 && !a.tb && !a.col2im; }
-
 }  // namespace
+
+bool gemv_eligible_shape(u32 M, u32 nbatch, bool tb, int col2im) {
+  return M <= u32(kGvM) && nbatch == 1 && !tb && !col2im;
+}
+static bool gemv_eligible(const GemmArgs& a) { return gemv_eligible_shape(a.M, a.nbatch, a.tb, a.col2im); }
 
 void ring_gemm_launch(Session& s, const GemmArgs& a) {
   if (a.M == 0 || a.N == 0 || a.nbatch == 0) return;
@@ -273,10 +279,6 @@ void ring_gemm_launch(Session& s, const GemmArgs& a) {
 
 // ---------------------------------------------------------------- matmul triple operands
 namespace {
-__device__ __forceinline__ u64 mm_a_share(const MmTriple& t, int party, u64 i) {
-  const u64 ra = mm_rA(t, i);
-  return party ? ra : mm_A(t, i) - ra;
-}
 __device__ __forceinline__ u64 mm_b_share(const MmTriple& t, int party, u64 j) {
   const u64 rb = mm_rB(t, j);
   return party ? rb : mm_B(t, j) - rb;
@@ -303,12 +305,13 @@ void delta_build_mem(Session& s, const Triple& t, const u64* const y[2], size_t 
 // party 0 {A, a0 = A - r_A} at [j] and [na + j], party 1 {r_A} at [j]. The draws are the ones
 // the eps payload needs anyway, so the combine GEMM reads them instead of redrawing.
 __device__ __forceinline__ u64 a_share_out(const MmTriple& t, int party, u64 i, u64* aop, u64 j, u64 na) {
-  const u64 ra = mm_rA(t, i);
+  const u64 key = tkey(t.key, t.kp), ip = i * kPhi;
+  const u64 ra = mix64(key + t.prA + ip);
   if (party) {
     if (aop) aop[j] = ra;
     return ra;
   }
-  const u64 A = mm_A(t, i), a0 = A - ra;
+  const u64 A = mix64(key + t.pA + ip), a0 = A - ra;
   if (aop) {
     aop[j] = A;
     aop[na + j] = a0;
@@ -474,7 +477,7 @@ bool beaver_combine_wants_aops(const Session& s, u32 nbatch, u32 M, u32 N, u32 K
   a.K = K;
   a.nbatch = nbatch;
   for (int i = 0; i < s.n_local; ++i) a.sl[i].nseg = s.party_of[i] == 0 ? 3 : 2;
-  if (M <= 16 && nbatch == 1 && gemv_mode() != 0) return false;
+  if (gemv_eligible_shape(M, nbatch, false, 0) && gemv_mode() != 0) return false;
   return !ring_gemm_tc2_wants(a);
 }
 
@@ -535,6 +538,7 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
   }
   const u64 sL = u64(M) * K, sR = batched_r ? u64(K) * N : 0;
   const u64 rboff = batched_r ? r_batch0 * u64(K) * N : 0;
+  const bool tc2 = !(gemv_eligible_shape(M, nbatch, tb, ep.col2im) && gemv_mode() != 0) && ring_gemm_tc2_wants(a);
   for (int i = 0; i < s.n_local; ++i) {
     GemmSlotArgs& S = a.sl[i];
     const u64* E0 = e.own(i);
@@ -550,7 +554,15 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
     S.aoff = a_off;
     S.boff = rboff;
     const u64* ao = aops ? aops->s[i] : nullptr;  // A-side operands emitted by the eps build
-    if (s.party_of[i] == 0) {  // -r_C + A*B + E*(b0 + F) + a0*F
+    if (s.party_of[i] == 0 && !ao && tc2) {  // -r_C + A*(B + F) + E*(b0 + F) - r_A*F  (= a0*F split)
+      S.cterm = -1;
+      S.lk[0] = kOpA;
+      S.rk[0] = kOpBF, S.R[0] = F0, S.R2[0] = F1;
+      S.lk[1] = kOpSum, S.L[1] = E0, S.L2[1] = E1;
+      S.rk[1] = kOpB0F, S.R[1] = F0, S.R2[1] = F1;
+      S.lk[2] = kOpRA;
+      S.rk[2] = kOpNegSum, S.R[2] = F0, S.R2[2] = F1;
+    } else if (s.party_of[i] == 0) {  // -r_C + A*B + E*(b0 + F) + a0*F
       S.cterm = -1;
       if (ao) S.lk[0] = kOpMem, S.L[0] = ao;
       else S.lk[0] = kOpA;

@@ -17,6 +17,8 @@ enum OpKind : int {
   kOpB = 5,     // dealer B                       (party 0)
   kOpB0F = 6,   // (B - r_B) + p[idx] + q[idx]    (party 0: b0 + F)
   kOpRB = 7,    // r_B                            (party 1 share of B)
+  kOpBF = 8,    // B + p[idx] + q[idx]            (party 0, tensor-core split: A*(B + F))
+  kOpNegSum = 9,  // -(p[idx] + q[idx])           (party 0, tensor-core split: -r_A*F)
 };
 
 // One party slot of a multi-segment ring GEMM: out = epi( sum_g L_g * R_g ).
@@ -80,6 +82,8 @@ __device__ __forceinline__ u64 load_r(const GemmSlotArgs& S, int sg, u64 idx) {
     case kOpB: return mm_B(S.mm, S.boff + idx);
     case kOpB0F:
       return (mm_B(S.mm, S.boff + idx) - mm_rB(S.mm, S.boff + idx)) + (S.R[sg][idx] + S.R2[sg][idx]);
+    case kOpBF: return mm_B(S.mm, S.boff + idx) + (S.R[sg][idx] + S.R2[sg][idx]);
+    case kOpNegSum: return u64(0) - (S.R[sg][idx] + S.R2[sg][idx]);
     default: return mm_rB(S.mm, S.boff + idx);
   }
 }
@@ -102,6 +106,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& a, const GemmSlotA
 }
 
 void ring_gemm_launch(Session& s, const GemmArgs& a);
+bool gemv_eligible_shape(u32 M, u32 nbatch, bool tb, int col2im);  // the small-M path takes it
 // Small-M fused-segment path (ring_gemv): 1 = on (default), 0 = off (MPCG_GEMV=0).
 inline int& gemv_mode() {
   static int m = [] {

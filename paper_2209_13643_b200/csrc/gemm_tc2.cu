@@ -129,9 +129,9 @@ __device__ __forceinline__ void load16v(const u64* p, u64 (&v)[16]) {
 struct Tc2Args {
   GemmArgs g;
   const char* Rpk[2] = {nullptr, nullptr};  // packed right operand per slot
-  u64 Rpk_b = 0;                            // bytes per batch (0 = shared across the batch)
+  u64 Rpk_b[2] = {0, 0};                    // bytes per batch (0 = shared across the batch)
   const char* Lpk[2] = {nullptr, nullptr};  // packed left operand (multi-N-tile shapes) or null
-  u64 Lpk_b = 0;
+  u64 Lpk_b[2] = {0, 0};
   u32 nkb = 0;                              // K blocks of 32
   int vec = 0;                              // L rows 16-byte aligned (vector loads)
 };
@@ -191,57 +191,69 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
       const u64 iA = 1 + S.mm.offA + S.aoff;                   // draw index of A[0]
       const u64 iRA = 1 + S.mm.na + S.mm.nb + S.mm.offA + S.aoff;  // of r_A[0]
       const u32 off = (u32(kc) * (kM / 8) + u32(r) / 8) * 128 + (u32(r) % 8) * 16;
-      u64 cA[16];
+      // The first memory segment (the opened E = own + peer, or a plain operand) is software-
+      // pipelined one K block ahead: its loads for block kb+1 are issued as soon as block kb's
+      // values are consumed, so they fly behind the next block's dealer draws and transposes.
+      int pf = -1;
+      for (int g = 0; g < nseg && pf < 0; ++g)
+        if (S.lk[g] == kOpMem || S.lk[g] == kOpSum) pf = g;
+      u64 pr[16], pr2[16];
+      auto fetch = [&](u32 kb) {
+        const u32 k0 = kb * kKB + u32(kc) * 16;
+        const bool sum = S.lk[pf] == kOpSum;
+        if (!rowok || kb >= P.nkb || k0 >= K) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pr[i] = pr2[i] = 0;
+        } else if (k0 + 16 <= K && P.vec) {
+          load16v(S.L[pf] + rowoff + k0, pr);
+          if (sum) load16v(S.L2[pf] + rowoff + k0, pr2);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const bool in = k0 + i < K;
+            pr[i] = in ? __ldg(S.L[pf] + rowoff + k0 + i) : 0;
+            pr2[i] = (in && sum) ? __ldg(S.L2[pf] + rowoff + k0 + i) : 0;
+          }
+        }
+        if (!sum) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pr2[i] = 0;
+        }
+      };
+      if (pf >= 0) fetch(0);
       u32 it = 0;
       for (u32 kb = 0; kb < P.nkb; ++kb) {
         const u32 k0 = kb * kKB + u32(kc) * 16;
         const bool full16 = rowok && k0 + 16 <= K;
-        bool haveA = false;
         for (int g = 0; g < nseg; ++g, ++it) {
           const int stg = int(it % kStages);
           u64 v[16];
           const int kind = S.lk[g];
-          if (!rowok || k0 >= K) {
+          if (g == pf) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = pr[i] + pr2[i];
+            fetch(kb + 1);
+          } else if (!rowok || k0 >= K) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = 0;
           } else if (kind == kOpMem || kind == kOpSum) {
-            const u64* p = S.L[g] + rowoff + k0;
-            if (full16 && P.vec) {
-              load16v(p, v);
-              if (kind == kOpSum) {
-                u64 w[16];
-                load16v(S.L2[g] + rowoff + k0, w);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] += w[i];
+            for (int i = 0; i < 16; ++i) {
+              u64 x = 0;
+              if (k0 + i < K) {
+                x = __ldg(S.L[g] + rowoff + k0 + i);
+                if (kind == kOpSum) x += __ldg(S.L2[g] + rowoff + k0 + i);
               }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                u64 x = 0;
-                if (k0 + i < K) {
-                  x = __ldg(p + i);
-                  if (kind == kOpSum) x += __ldg(S.L2[g] + rowoff + k0 + i);
-                }
-                v[i] = x;
-              }
+              v[i] = x;
             }
-          } else {  // dealer draws: A, a0 = A - r_A (party 0), r_A (party 1)
+          } else {  // dealer draws: A, r_A (party 0 splits a0*F as A*F - r_A*F), or a0 = A - r_A
             const u64 e0 = rowoff + k0;
-            if (kind == kOpRA) {
-              draws16(key, iRA + e0, v);
-            } else {
-              if (!haveA) {
-                draws16(key, iA + e0, cA);
-                haveA = true;
-              }
-              if (kind == kOpA) {
+            draws16(key, (kind == kOpRA ? iRA : iA) + e0, v);
+            if (kind == kOpA0) {
+              u64 w[16];
+              draws16(key, iRA + e0, w);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = cA[i];
-              } else {
-                draws16(key, iRA + e0, v);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = cA[i] - v[i];
-              }
+              for (int i = 0; i < 16; ++i) v[i] -= w[i];
             }
             if (!full16) {
 #pragma unroll
@@ -259,8 +271,8 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
     }
   } else if (warp == 8) {
     if (lane == 0) {  // ---- bulk loader
-      const char* Rb = P.Rpk[slot] + u64(b) * P.Rpk_b + u64(blockIdx.x) * P.nkb * u64(nseg) * 8 * kB;
-      const char* Lb = packedL ? P.Lpk[slot] + u64(b) * P.Lpk_b + u64(blockIdx.y) * P.nkb * u64(nseg) * 8 * kA
+      const char* Rb = P.Rpk[slot] + u64(b) * P.Rpk_b[slot] + u64(blockIdx.x) * P.nkb * u64(nseg) * 8 * kB;
+      const char* Lb = packedL ? P.Lpk[slot] + u64(b) * P.Lpk_b[slot] + u64(blockIdx.y) * P.nkb * u64(nseg) * 8 * kA
                                : nullptr;
       for (u32 it = 0; it < nst; ++it) {
         const int stg = int(it % kStages);
@@ -422,19 +434,20 @@ void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
   const u32 rb = rbatched ? a.nbatch : 1;
   std::vector<std::shared_ptr<Block>> keep;
   for (int i = 0; i < a.nslots; ++i) {
+    ClassScope pack_scope(kClsOther, 0);  // the roofline probe times the GEMM kernel itself
     const u64 rbytes = u64(ntiles) * P.nkb * a.sl[i].nseg * 8 * BN * kKB;
     auto blk = s.raw((rbytes * rb + 7) / 8);
     keep.push_back(blk);
     launch_pack<BN>(s, a, i, false, a.N, rb, P.nkb, reinterpret_cast<char*>(blk->ptr));
     P.Rpk[i] = reinterpret_cast<const char*>(blk->ptr);
-    P.Rpk_b = rbatched ? rbytes : 0;
+    P.Rpk_b[i] = rbatched ? rbytes : 0;
     if (packL) {
       const u64 lbytes = u64(mtiles) * P.nkb * a.sl[i].nseg * 8 * kM * kKB;
       auto lb = s.raw((lbytes * a.nbatch + 7) / 8);
       keep.push_back(lb);
       launch_pack<kM>(s, a, i, true, a.M, a.nbatch, P.nkb, reinterpret_cast<char*>(lb->ptr));
       P.Lpk[i] = reinterpret_cast<const char*>(lb->ptr);
-      P.Lpk_b = lbytes;
+      P.Lpk_b[i] = lbytes;
     }
   }
   bool vec = (a.K % 2) == 0;

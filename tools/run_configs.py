@@ -1,0 +1,145 @@
+"""Every BASELINE config on one B200 (both parties of the 2PC pair on cuda:0), blocking vs
+pipelined, plus the chunk-count / link-bandwidth sweep of config 5 — one JSON document.
+
+  python tools/run_configs.py [--out gpurun_out/configs.json] [--quick]
+
+Per config: latency per inference (ms, CUDA-graph replay where the whole inference is
+captured, else eager), inferences/s, the pipelined-vs-blocking reduction per layer, bytes
+sent per party per inference and the decoded error vs the float64 plaintext forward
+(tolerance 2^-6, P/tools/mpcpipe_bench.cpp:124). Links: "device" = in-device zero-copy opens;
+"nvlink" = an emulated 900 GB/s, 2 us link (the comm-stream token bucket, so opens overlap
+compute as they would between two GPUs); "10gbps" = the paper's LAN (1.25e9 B/s, 0.1 ms).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+
+import paper_2209_13643_b200 as mp  # noqa: E402
+from paper_2209_13643_b200 import api  # noqa: E402
+
+PHI = 0x9E3779B97F4A7C15
+LINKS = {"device": None, "nvlink": (2e-6, 9.0e11, 0.0), "10gbps": (1e-4, 1.25e9, 0.0)}
+
+
+def run_one(g, mode, weights, link, chunks=4, threshold=2 << 20, iters=3, graph=True, check_ref=None):
+    s = mp.Session(device=0, n_local=2, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
+    if LINKS[link]:
+        s.set_link(*LINKS[link])
+    ex = mp.SecureExecutor(s, g, public_weights=weights == "public", pipelined=mode == "pipelined", chunks=chunks,
+                           chunk_threshold=threshold)
+    ex.deal_weights(mp.init_weights(g, 12), 1)
+    x = s.deal_input(mp.demo_input(g, 13), 2)
+    z = ex.run(x)
+    s.sync()
+    st0 = s.stats(0)
+    z = ex.run(x)
+    s.sync()
+    st1 = s.stats(0)
+    ex.time_layers(True)
+    api.timer(s, "reset")
+    if graph:
+        ex.capture(x)
+        for _ in range(iters):
+            api.timer(s, "start")
+            z = ex.replay()
+            api.timer(s, "stop")
+    else:
+        for _ in range(iters):
+            api.timer(s, "start")
+            z = ex.run(x)
+            api.timer(s, "stop")
+    ms = api.timer(s, "read") / iters
+    layers = ex.layer_times()
+    res = {"ms": ms, "inferences_per_s": g.input[0] / (ms / 1e3), "exec": "graph" if graph else "eager",
+           "bytes_sent_per_party": st1["bytes_sent"] - st0["bytes_sent"],
+           "collectives": st1["collectives"] - st0["collectives"],
+           "per_layer_ms": {l.name: round(t, 4) for l, t in zip(g.layers, layers)}}
+    if check_ref is not None:
+        zz = z.numpy()
+        dec = (zz[0] + zz[1]).view(np.int64).astype(np.float64) * 2.0 ** -g.frac_bits
+        err = np.abs(dec.reshape(-1) - check_ref.reshape(-1))
+        res["max_abs_err"] = float(err.max())
+        res["frac_within_2^-6"] = float((err <= 2.0 ** -6).mean())
+    del ex
+    s.close()
+    return res
+
+
+def reduction(b, p):
+    out = {"blocking_ms": b["ms"], "pipelined_ms": p["ms"], "reduction_pct": (b["ms"] - p["ms"]) / b["ms"] * 100}
+    out["per_layer"] = {k: {"blocking_ms": b["per_layer_ms"][k], "pipelined_ms": p["per_layer_ms"][k],
+                            "reduction_pct": round((b["per_layer_ms"][k] - p["per_layer_ms"][k]) /
+                                                   b["per_layer_ms"][k] * 100, 2) if b["per_layer_ms"][k] > 0 else 0}
+                        for k in b["per_layer_ms"]}
+    return out
+
+
+def plaintext(g):
+    from oracle import mpc_oracle as O
+    go = O.model_from_json(json.load(open(os.path.join(ROOT, "configs", g.name + ".json"))))
+    return O.reference_forward(go, O.init_weights(go, 12), O.demo_input(go, 13))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.json"))
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", default="")
+    a = ap.parse_args()
+    doc = {"device": "1x B200, both parties on cuda:0", "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
+           "configs": {}, "sweep": []}
+    plan = [  # (config, weights, links, graph)
+        ("mlp", "private", ["device", "nvlink"], True),
+        ("lenet5", "private", ["device", "nvlink"], True),
+        ("lenet5", "public", ["device"], True),
+        ("resnet18", "private", ["device", "nvlink"], False),
+        ("bert_base", "private", ["device", "nvlink"], False),
+        ("bert_base", "public", ["device"], False),
+        ("vgg16", "private", ["device", "nvlink"], True),
+    ]
+    for name, weights, links, graph in plan:
+        if a.only and name not in a.only.split(","):
+            continue
+        g = mp.ModelGraph.from_json(name)
+        ref = plaintext(g)
+        for link in links:
+            key = f"{name}/{weights}/{link}"
+            t0 = time.time()
+            try:
+                b = run_one(g, "blocking", weights, link, graph=graph, check_ref=ref, iters=2 if a.quick else 3)
+                p = run_one(g, "pipelined", weights, link, graph=graph, check_ref=ref, iters=2 if a.quick else 3)
+                doc["configs"][key] = {"batch": g.input[0], "blocking": {k: v for k, v in b.items() if k != "per_layer_ms"},
+                                       "pipelined": {k: v for k, v in p.items() if k != "per_layer_ms"},
+                                       "pipelining": reduction(b, p), "wall_s": time.time() - t0}
+            except Exception as e:  # recorded, the sweep goes on
+                doc["configs"][key] = {"error": repr(e)[:300]}
+            print(key, json.dumps({k: v for k, v in doc["configs"][key].items() if k != "pipelining"})[:400],
+                  flush=True)
+    if not a.only or "sweep" in a.only:
+        g = mp.ModelGraph.from_json("vgg16")
+        for link in ["nvlink", "10gbps"]:
+            for n in ([1, 4, 16] if a.quick else [1, 2, 4, 8, 16]):
+                for mode in ["blocking", "pipelined"]:
+                    if mode == "blocking" and n > 1:
+                        continue  # blocking never chunks (chunking belongs to the pipelined mode)
+                    try:
+                        r = run_one(g, mode, "private", link, chunks=n, threshold=0, graph=(link != "10gbps"),
+                                    iters=1 if link == "10gbps" else 2)
+                        doc["sweep"].append({"model": "vgg16", "link": link, "chunks": n, "mode": mode, "ms": r["ms"],
+                                             "bytes_sent_per_party": r["bytes_sent_per_party"]})
+                    except Exception as e:
+                        doc["sweep"].append({"link": link, "chunks": n, "mode": mode, "error": repr(e)[:200]})
+                    print(json.dumps(doc["sweep"][-1]), flush=True)
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    with open(a.out, "w") as f:
+        json.dump(doc, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
