@@ -401,6 +401,29 @@ struct SpkLevel {
 };
 
 
+// Issue-to-settle draw cache (L2-sized rounds): the issue of round r draws A, B, r_A, r_B of
+// triple r for the payload; the settle of round r (next kernel) needs them again plus r_C.
+// When the cache is on, the issue kernel keeps the four draws of each half in a small
+// SoA buffer ([half][4][n], coalesced) that stays L2-resident, and the settle draws only
+// r_C: 10 instead of 18 splitmix64 per element and level round. Values are unchanged.
+__device__ __forceinline__ void dw_store(u64* c, u64 n, u64 g, int half, const Dw& d) {
+  u64* b = c + u64(half) * 4 * n + g;
+  b[0] = d.A;
+  b[n] = d.B;
+  b[2 * n] = d.ra;
+  b[3 * n] = d.rb;
+}
+__device__ __forceinline__ Dw dw_load(const u64* c, u64 n, u64 g, int half, const EwTriple& t, u64 gidx) {
+  const u64* b = c + u64(half) * 4 * n + g;
+  Dw d;
+  d.A = b[0];
+  d.B = b[n];
+  d.ra = b[2 * n];
+  d.rb = b[3 * n];
+  d.rc = mix64(tkey(t.key, t.kp) + t.prc + gidx * kPhi);
+  return d;
+}
+
 template <class XF, class YF, class FF>
 struct AdderRound {
   int rp, rn, levels;
@@ -414,6 +437,9 @@ struct AdderRound {
   XF xf;
   YF yf;
   FF ff;
+  const u64* cwp = nullptr;  // draw cache written by the previous round's issue (or null)
+  u64* cwn = nullptr;        // draw cache for the next round's settle (or null)
+  u64 cwN = 0;               // elements per cache plane
   __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
   __device__ void both(u64 j) const { step<2>(0, j); }
 
@@ -425,6 +451,7 @@ struct AdderRound {
     u64 dummy;
     if (rn == 0) {  // issue the generate AND: payload [x^a | y^b]
       const Dw dn = ew_draw<false>(Tn, Tn.off + g, p0);
+      if (cwn) dw_store(cwn, cwN, g, 0, dn);
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
         const int slot = slot0 + k;
@@ -439,7 +466,7 @@ struct AdderRound {
     }
     u64 s[NS], p[NS];
     if (rp == 0) {  // settle the generate AND (H/protocols/adder.hpp:209-223)
-      const Dw dp = ew_draw<true>(Tp, Tp.off + g, p0);
+      const Dw dp = cwp ? dw_load(cwp, cwN, g, 0, Tp, Tp.off + g) : ew_draw<true>(Tp, Tp.off + g, p0);
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
         const int slot = slot0 + k, party = pid.v[slot];
@@ -455,7 +482,9 @@ struct AdderRound {
     } else {  // settle a prefix level (H/protocols/adder.hpp:142-165)
       // Own payload is recomputed from the pre-round state instead of re-read from HBM:
       // it is a function of (s, p) and the triple, all of which this thread holds.
-      const Dw d0 = ew_draw<true>(Tp, Tp.off + g, p0), d1 = ew_draw<true>(Tp, Tp.ghalf + Tp.off + g, p0);
+      const Dw d0 = cwp ? dw_load(cwp, cwN, g, 0, Tp, Tp.off + g) : ew_draw<true>(Tp, Tp.off + g, p0);
+      const Dw d1 = cwp ? dw_load(cwp, cwN, g, 1, Tp, Tp.ghalf + Tp.off + g)
+                        : ew_draw<true>(Tp, Tp.ghalf + Tp.off + g, p0);
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
         const int slot = slot0 + k, party = pid.v[slot];
@@ -480,6 +509,10 @@ struct AdderRound {
     }
     if (rn <= levels) {  // issue level rn-1 (H/protocols/adder.hpp:122-140)
       const Dw d0 = ew_draw<false>(Tn, Tn.off + g, p0), d1 = ew_draw<false>(Tn, Tn.ghalf + Tn.off + g, p0);
+      if (cwn) {
+        dw_store(cwn, cwN, g, 0, d0);
+        dw_store(cwn, cwN, g, 1, d1);
+      }
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
         const int slot = slot0 + k, party = pid.v[slot];
@@ -516,6 +549,17 @@ struct NoPost {
   void operator()(int) const {}
 };
 
+// The issue-to-settle draw cache is used when one thread evaluates every local slot of an
+// element (pair evaluation, or one party per process) and the two buffers stay L2-resident.
+inline bool adder_draw_cache_ok(const Session& s, size_t n) {
+  static const bool on = [] {
+    const char* e = std::getenv("MPCG_DRAW_CACHE");
+    return !(e && e[0] == '0');
+  }();
+  const bool one_thread = s.n_local == 1 || pair_eval_enabled();
+  return on && one_thread && n > 0 && n * 2 * 64 <= (size_t(48) << 20);
+}
+
 // Secure binary addition of XOR-shared operands given by sources. The last kernel of each
 // lane hands the sum to ff_for_lane(lane, lo, w) — a functor (slot, party, g, j, sum) that
 // may already build the next protocol's payload for the same lane — and post_lane(lane)
@@ -529,6 +573,9 @@ void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& 
   const Pid2 pid = pids(s);
   DT S = s.alloc(Shape{n}), P = s.alloc(Shape{n}), P0 = s.alloc(Shape{n});
   const int rounds = 1 + c.levels;
+  DT cw[2];
+  if (adder_draw_cache_ok(s, n))
+    for (auto& b : cw) b = s.alloc(Shape{8 * n});
   Triple tr[7];
   auto fetch_round = [&](int r) {
     tr[r] = r == 0 ? s.fetch(TripleSpec::elementwise(TripleKind::Bin, Shape{n}), tag + ".g")
@@ -566,6 +613,11 @@ void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& 
     k.wmask = c.wmask;
     k.xf = xf;
     k.yf = yf;
+    if (cw[0]) {
+      k.cwN = n;
+      if (rp >= 0) k.cwp = cw[rp & 1].s[0];
+      if (rn <= c.levels) k.cwn = cw[rn & 1].s[0];
+    }
     if (rn > c.levels) k.ff = ff_for_lane(lane, lo, hi - lo);
     // algorithmic bytes per element per party (2 x wire + 8 x (in + out)):
     // level round = 2x32 wire + 8x(2 state in + 2 state out) = 96 B

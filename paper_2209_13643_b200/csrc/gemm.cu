@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(256) ring_gemm_simt(GemmArgs a) {
   }
 }
 
+}  // namespace
 __global__ void __launch_bounds__(256) gemm_splitk_epilogue(GemmArgs a) {
   pdl_enter();
   const u64 per = u64(a.nbatch) * a.M * a.N;
@@ -109,6 +110,8 @@ __global__ void __launch_bounds__(256) gemm_splitk_epilogue(GemmArgs a) {
     gemm_epilogue(a, a.sl[slot], b, m, n, v);
   }
 }
+splitk_epilogue_t gemm_splitk_epilogue_fn() { return gemm_splitk_epilogue; }
+namespace {
 
 template <int BM, int BN, int TM, int TN>
 void launch_simt(Session& s, GemmArgs a) {
@@ -121,6 +124,7 @@ void launch_simt(Session& s, GemmArgs a) {
   u32 split = 1;
   if (tiles < 2 * u64(kSms)) {
     split = u32((2 * u64(kSms) + tiles - 1) / tiles);
+    split = split > 16 ? 16 : split;  // the epilogue kernel sums the partials serially
     const u32 maxsplit = (kp + 31) / 32;
     split = split > maxsplit ? maxsplit : split;
     split = split < 1 ? 1 : split;
@@ -237,7 +241,52 @@ void launch_gemv(Session& s, GemmArgs a) {
   probe_end(st, pe);
 }
 
+// ---------------------------------------------------------------- skinny-N (row) path
+// Convolutions with few output channels (LeNet conv0: M=50176, K=25, N=6): one thread owns
+// one output row of one slot and streams its left-operand rows (every segment), while the
+// right operand of a K chunk (nseg x KC x N words) is staged in shared memory. The tiled SIMT
+// kernel wastes its BN-wide tile and syncs every 16 K; this one is bound by reading L.
+constexpr int kRowN = 8;    // max N
+constexpr int kRowKC = 64;  // K chunk of R staged in smem
+
+template <int NR>
+__global__ void __launch_bounds__(256) ring_gemm_rows(GemmArgs a) {
+  __shared__ u64 Rs[3][kRowKC][NR];
+  pdl_enter();
+  const int slot = blockIdx.y;
+  const GemmSlotArgs& S = a.sl[slot];
+  const u32 M = a.M, N = a.N, K = a.K;
+  const u32 m = blockIdx.x * 256 + threadIdx.x;
+  u64 acc[NR];
+#pragma unroll
+  for (int n = 0; n < NR; ++n) acc[n] = 0;
+  for (u32 k0 = 0; k0 < K; k0 += kRowKC) {
+    const u32 kc = min(u32(kRowKC), K - k0);
+    __syncthreads();
+    for (u32 e = threadIdx.x; e < u32(S.nseg) * kRowKC * NR; e += 256) {
+      const u32 n = e % NR, kk = (e / NR) % kRowKC, g = e / (NR * kRowKC);
+      Rs[g][kk][n] = (n < N && kk < kc) ? load_r(S, int(g), u64(k0 + kk) * N + n) : 0;
+    }
+    __syncthreads();
+    if (m >= M) continue;
+    for (int g = 0; g < S.nseg; ++g) {
+      const u64 rowbase = u64(m) * K + k0;
+      for (u32 kk = 0; kk < kc; ++kk) {
+        const u64 v = load_l(S, g, rowbase + kk);
+#pragma unroll
+        for (int n = 0; n < NR; ++n) acc[n] += v * Rs[g][kk][n];
+      }
+    }
+  }
+  if (m >= M) return;
+#pragma unroll
+  for (int n = 0; n < NR; ++n)
+    if (u32(n) < N) gemm_epilogue(a, S, 0, m, u32(n), acc[n]);
+}
+
 }  // namespace
+
+static bool rows_eligible(const GemmArgs& a) { return a.N <= u32(kRowN) && a.M >= 1024 && a.nbatch == 1 && !a.tb; }
 
 bool gemv_eligible_shape(u32 M, u32 nbatch, bool tb, int col2im) {
   return M <= u32(kGvM) && nbatch == 1 && !tb && !col2im;
@@ -255,6 +304,14 @@ void ring_gemm_launch(Session& s, const GemmArgs& a) {
     if (a.M <= 1) launch_gemv<1>(s, a);
     else if (a.M <= 4) launch_gemv<4>(s, a);
     else launch_gemv<16>(s, a);
+    s.check();
+    return;
+  }
+  if (rows_eligible(a) && gemv_mode() != 0) {  // skinny N: one thread per output row
+    cudaEvent_t pe;
+    probe_begin(s.stream, &pe);
+    launch_pdl(ring_gemm_rows<kRowN>, dim3((a.M + 255) / 256, a.nslots), dim3(256), 0, s.stream, a);
+    probe_end(s.stream, pe);
     s.check();
     return;
   }

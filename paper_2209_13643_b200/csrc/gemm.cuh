@@ -106,6 +106,10 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& a, const GemmSlotA
 }
 
 void ring_gemm_launch(Session& s, const GemmArgs& a);
+// Split-K epilogue: sums a.ksplit partial tiles from a.acc[slot] mod 2^64, then the Beaver epilogue.
+__global__ void gemm_splitk_epilogue(GemmArgs a);
+using splitk_epilogue_t = void (*)(GemmArgs);
+splitk_epilogue_t gemm_splitk_epilogue_fn();
 bool gemv_eligible_shape(u32 M, u32 nbatch, bool tb, int col2im);  // the small-M path takes it
 // Small-M fused-segment path (ring_gemv): 1 = on (default), 0 = off (MPCG_GEMV=0).
 inline int& gemv_mode() {

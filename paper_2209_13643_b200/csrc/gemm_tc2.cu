@@ -29,8 +29,11 @@ namespace {
 constexpr int kM = 128;        // tile rows (UMMA M)
 constexpr int kKB = 32;        // K values (= limb bytes) per stage: one UMMA K slab
 constexpr int kStages = 4;
-constexpr int kProd = 256;     // L producer threads (warps 0-7)
-constexpr int kThreads = 320;  // + warp 8 (bulk loader) + warp 9 (MMA issuer, TMEM owner)
+constexpr int kProdWarps = 16;                 // L producers (and epilogue): warps 0-15
+constexpr int kVW = 8;                         // K values per producer unit (= 8-byte limb row segment)
+constexpr int kLoadWarp = kProdWarps;          // bulk loader
+constexpr int kMmaWarp = kProdWarps + 1;       // MMA issuer, TMEM owner
+constexpr int kThreads = (kProdWarps + 2) * 32;
 constexpr u32 kMaxKPrime = 16384;
 
 __device__ __forceinline__ u32 smem_u32(const void* p) { return static_cast<u32>(__cvta_generic_to_shared(p)); }
@@ -87,42 +90,62 @@ __device__ __forceinline__ u32 gather4(u32 a, u32 b, u32 c, u32 d, u32 l) {
   const u32 sel = l | ((l + 4) << 4);
   return __byte_perm(__byte_perm(a, b, sel), __byte_perm(c, d, sel), 0x5410);
 }
-// 16 K-consecutive u64 -> one 16-byte row in each of the 8 limb planes (base + p*plane + off).
-__device__ __forceinline__ void transpose_store(const u64 (&v)[16], char* base, u32 plane, u32 off) {
-#pragma unroll
-  for (int l = 0; l < 8; ++l) {
-    const int sh = (l & 3), hi = l >> 2;
-    u32 w[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) w[i] = hi ? u32(v[i] >> 32) : u32(v[i]);
-    uint4 o;
-    o.x = gather4(w[0], w[1], w[2], w[3], sh);
-    o.y = gather4(w[4], w[5], w[6], w[7], sh);
-    o.z = gather4(w[8], w[9], w[10], w[11], sh);
-    o.w = gather4(w[12], w[13], w[14], w[15], sh);
-    *reinterpret_cast<uint4*>(base + l * plane + off) = o;
-  }
-}
 
-// 16 dealer draws c0, c0+1, ... of one stream, incrementally (key + c*phi advances by phi).
-__device__ __forceinline__ void draws16(u64 key, u64 c0, u64 (&v)[16]) {
+
+// kVW dealer draws c0, c0+1, ... of one stream (key + c*phi advances by phi).
+__device__ __forceinline__ void draws_vec(u64 key, u64 c0, u64 (&v)[kVW]) {
   u64 z = key + c0 * kPhi;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
+  for (int i = 0; i < kVW; ++i) {
     v[i] = mix64(z);
     z += kPhi;
   }
 }
-
-__device__ __forceinline__ void load16v(const u64* p, u64 (&v)[16]) {
+__device__ __forceinline__ void load_vec(const u64* p, u64 (&v)[kVW]) {
   const uint4* p4 = reinterpret_cast<const uint4*>(p);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < kVW / 2; ++i) {
     const uint4 w = __ldg(p4 + i);
     v[2 * i] = (u64(w.y) << 32) | w.x;
     v[2 * i + 1] = (u64(w.w) << 32) | w.z;
   }
 }
+// 8 K-consecutive u64 -> one 8-byte row segment in each of the 8 limb planes.
+__device__ __forceinline__ void transpose8_store(const u64 (&v)[kVW], char* base, u32 plane, u32 off) {
+#pragma unroll
+  for (int l = 0; l < 8; ++l) {
+    const int sh = (l & 3), hi = l >> 2;
+    u32 w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = hi ? u32(v[i] >> 32) : u32(v[i]);
+    uint2 o;
+    o.x = gather4(w[0], w[1], w[2], w[3], sh);
+    o.y = gather4(w[4], w[5], w[6], w[7], sh);
+    *reinterpret_cast<uint2*>(base + l * plane + off) = o;
+  }
+}
+// tcgen05.ld of W consecutive 32-bit TMEM columns of this warp's 32 lanes.
+template <int W>
+__device__ __forceinline__ void tmem_ld(u32 addr, u32 (&r)[W]) {
+  if constexpr (W == 16) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+  } else if constexpr (W == 8) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(addr));
+  } else {
+    static_assert(W == 4, "tmem_ld width");
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+  }
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 
 }  // namespace
 
@@ -134,6 +157,7 @@ struct Tc2Args {
   u64 Lpk_b[2] = {0, 0};
   u32 nkb = 0;                              // K blocks of 32
   int vec = 0;                              // L rows 16-byte aligned (vector loads)
+  u32 ksplit = 1, kbper = 0;                // split-K over K blocks (partials summed by the epilogue kernel)
 };
 
 namespace {
@@ -153,23 +177,25 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
   const GemmArgs& a = P.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int slot = blockIdx.z % a.nslots;
-  const u32 b = blockIdx.z / a.nslots;
+  const u32 b = (blockIdx.z / a.nslots) % a.nbatch;
+  const u32 split = blockIdx.z / (a.nslots * a.nbatch);
   const GemmSlotArgs& S = a.sl[slot];
   const u32 M = a.M, N = a.N, K = a.K;
   const u32 m0 = blockIdx.y * kM, n0 = blockIdx.x * BN;
   const int nseg = S.nseg;
-  const u32 nst = P.nkb * u32(nseg);
+  const u32 kb0 = split * P.kbper, kb1 = min(P.nkb, kb0 + P.kbper);  // this CTA's K blocks
+  const u32 nst = (kb1 - kb0) * u32(nseg);
   const bool packedL = P.Lpk[slot] != nullptr;
 
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) {
-      mbar_init(&full[i], packedL ? 1 : 9);
+      mbar_init(&full[i], packedL ? 1 : kProdWarps + 1);
       mbar_init(&empty[i], 1);
     }
     mbar_init(&done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 9) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
                  "r"(kCols)
                  : "memory");
@@ -180,36 +206,37 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const u32 tmem = tmem_slot;
 
-  if (warp < 8) {
+  if (warp < kProdWarps) {
     if (!packedL) {
-      // ---- L producers: unit = (row r, K chunk kc) of 16 values per stage
-      const int r = tid & (kM - 1), kc = tid >> 7;
+      // ---- L producers: unit = (row r, quarter q) = 8 K-consecutive values of one row per
+      // stage; each becomes one 8-byte row segment in every limb plane.
+      const int r = tid & (kM - 1), q = tid >> 7;
       const u32 m = m0 + u32(r);
       const bool rowok = m < M;
       const u64 rowoff = u64(b) * S.sL[0] + u64(m) * K;  // same stride for every segment
       const u64 key = tkey(S.mm.key, S.mm.kp);
-      const u64 iA = 1 + S.mm.offA + S.aoff;                   // draw index of A[0]
+      const u64 iA = 1 + S.mm.offA + S.aoff;                       // draw index of A[0]
       const u64 iRA = 1 + S.mm.na + S.mm.nb + S.mm.offA + S.aoff;  // of r_A[0]
-      const u32 off = (u32(kc) * (kM / 8) + u32(r) / 8) * 128 + (u32(r) % 8) * 16;
+      const u32 off = (u32(q >> 1) * (kM / 8) + u32(r) / 8) * 128 + (u32(r) % 8) * 16 + u32(q & 1) * 8;
       // The first memory segment (the opened E = own + peer, or a plain operand) is software-
       // pipelined one K block ahead: its loads for block kb+1 are issued as soon as block kb's
       // values are consumed, so they fly behind the next block's dealer draws and transposes.
       int pf = -1;
       for (int g = 0; g < nseg && pf < 0; ++g)
         if (S.lk[g] == kOpMem || S.lk[g] == kOpSum) pf = g;
-      u64 pr[16], pr2[16];
+      u64 pr[kVW], pr2[kVW];
       auto fetch = [&](u32 kb) {
-        const u32 k0 = kb * kKB + u32(kc) * 16;
+        const u32 k0 = kb * kKB + u32(q) * kVW;
         const bool sum = S.lk[pf] == kOpSum;
-        if (!rowok || kb >= P.nkb || k0 >= K) {
+        if (!rowok || kb >= kb1 || k0 >= K) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) pr[i] = pr2[i] = 0;
-        } else if (k0 + 16 <= K && P.vec) {
-          load16v(S.L[pf] + rowoff + k0, pr);
-          if (sum) load16v(S.L2[pf] + rowoff + k0, pr2);
+          for (int i = 0; i < kVW; ++i) pr[i] = pr2[i] = 0;
+        } else if (k0 + kVW <= K && P.vec) {
+          load_vec(S.L[pf] + rowoff + k0, pr);
+          if (sum) load_vec(S.L2[pf] + rowoff + k0, pr2);
         } else {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
+          for (int i = 0; i < kVW; ++i) {
             const bool in = k0 + i < K;
             pr[i] = in ? __ldg(S.L[pf] + rowoff + k0 + i) : 0;
             pr2[i] = (in && sum) ? __ldg(S.L2[pf] + rowoff + k0 + i) : 0;
@@ -217,28 +244,28 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
         }
         if (!sum) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) pr2[i] = 0;
+          for (int i = 0; i < kVW; ++i) pr2[i] = 0;
         }
       };
-      if (pf >= 0) fetch(0);
+      if (pf >= 0) fetch(kb0);
       u32 it = 0;
-      for (u32 kb = 0; kb < P.nkb; ++kb) {
-        const u32 k0 = kb * kKB + u32(kc) * 16;
-        const bool full16 = rowok && k0 + 16 <= K;
+      for (u32 kb = kb0; kb < kb1; ++kb) {
+        const u32 k0 = kb * kKB + u32(q) * kVW;
+        const bool fullv = rowok && k0 + kVW <= K;
         for (int g = 0; g < nseg; ++g, ++it) {
           const int stg = int(it % kStages);
-          u64 v[16];
+          u64 v[kVW];
           const int kind = S.lk[g];
           if (g == pf) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = pr[i] + pr2[i];
+            for (int i = 0; i < kVW; ++i) v[i] = pr[i] + pr2[i];
             fetch(kb + 1);
           } else if (!rowok || k0 >= K) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = 0;
+            for (int i = 0; i < kVW; ++i) v[i] = 0;
           } else if (kind == kOpMem || kind == kOpSum) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
+            for (int i = 0; i < kVW; ++i) {
               u64 x = 0;
               if (k0 + i < K) {
                 x = __ldg(S.L[g] + rowoff + k0 + i);
@@ -248,31 +275,33 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
             }
           } else {  // dealer draws: A, r_A (party 0 splits a0*F as A*F - r_A*F), or a0 = A - r_A
             const u64 e0 = rowoff + k0;
-            draws16(key, (kind == kOpRA ? iRA : iA) + e0, v);
+            draws_vec(key, (kind == kOpRA ? iRA : iA) + e0, v);
             if (kind == kOpA0) {
-              u64 w[16];
-              draws16(key, iRA + e0, w);
+              u64 w[kVW];
+              draws_vec(key, iRA + e0, w);
 #pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] -= w[i];
+              for (int i = 0; i < kVW; ++i) v[i] -= w[i];
             }
-            if (!full16) {
+            if (!fullv) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i)
+              for (int i = 0; i < kVW; ++i)
                 if (k0 + i >= K) v[i] = 0;
             }
           }
           if (it >= kStages) mbar_wait(&empty[stg], ((it / kStages) & 1) ^ 1);
-          transpose_store(v, smem + stg * kStage, kA, off);
+          transpose8_store(v, smem + stg * kStage, kA, off);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
           __syncwarp();
           if (lane == 0) mbar_arrive(&full[stg]);
         }
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == kLoadWarp) {
     if (lane == 0) {  // ---- bulk loader
-      const char* Rb = P.Rpk[slot] + u64(b) * P.Rpk_b[slot] + u64(blockIdx.x) * P.nkb * u64(nseg) * 8 * kB;
-      const char* Lb = packedL ? P.Lpk[slot] + u64(b) * P.Lpk_b[slot] + u64(blockIdx.y) * P.nkb * u64(nseg) * 8 * kA
+      const char* Rb = P.Rpk[slot] + u64(b) * P.Rpk_b[slot] +
+                       (u64(blockIdx.x) * P.nkb + kb0) * u64(nseg) * 8 * kB;
+      const char* Lb = packedL ? P.Lpk[slot] + u64(b) * P.Lpk_b[slot] +
+                                     (u64(blockIdx.y) * P.nkb + kb0) * u64(nseg) * 8 * kA
                                : nullptr;
       for (u32 it = 0; it < nst; ++it) {
         const int stg = int(it % kStages);
@@ -306,54 +335,43 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
     }
   }
 
-  // ---- epilogue (warps 0-7): warp w reads TMEM lanes 32*(w%4).. and column half w/4
-  if (warp < 8) {
+  // ---- epilogue (producer warps): warp w reads TMEM lanes 32*(w%4).. and column group w/4
+  if (warp < kProdWarps) {
     mbar_wait(&done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    constexpr int kHalf = BN / 2;
-    constexpr int kCW = kHalf < 16 ? kHalf : 16;
-    const int q = warp & 3, ch = warp >> 2;
-    const u32 row = u32(q) * 32 + u32(lane);
+    constexpr int kGrp = kProdWarps / 4;
+    constexpr int kCW = BN / kGrp;  // columns per warp: 16 / 8 / 4 for BN = 64 / 32 / 16
+    const int qd = warp & 3, cg = warp >> 2;
+    const u32 row = u32(qd) * 32 + u32(lane);
     const u32 m = m0 + row;
-    const u32 lane_addr = tmem + ((u32(q) * 32) << 16) + u32(ch * kHalf);
+    const u32 lane_addr = tmem + ((u32(qd) * 32) << 16) + u32(cg * kCW);
+    u64 acc[kCW];
 #pragma unroll
-    for (int c0 = 0; c0 < kHalf; c0 += kCW) {
-      u64 acc[kCW];
+    for (int c = 0; c < kCW; ++c) acc[c] = 0;
 #pragma unroll
-      for (int c = 0; c < kCW; ++c) acc[c] = 0;
+    for (int d = 0; d < 8; ++d) {
+      u32 rr[kCW];
+      tmem_ld<kCW>(lane_addr + u32(d) * BN, rr);
 #pragma unroll
-      for (int d = 0; d < 8; ++d) {
-        u32 rr[kCW];
-        const u32 ad = lane_addr + u32(d) * BN + u32(c0);
-        if constexpr (kCW == 16) {
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-              : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3]), "=r"(rr[4]), "=r"(rr[5]), "=r"(rr[6]),
-                "=r"(rr[7]), "=r"(rr[8]), "=r"(rr[9]), "=r"(rr[10]), "=r"(rr[11]), "=r"(rr[12]), "=r"(rr[13]),
-                "=r"(rr[14]), "=r"(rr[15])
-              : "r"(ad));
-        } else {
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                       : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3]), "=r"(rr[4]), "=r"(rr[5]), "=r"(rr[6]),
-                         "=r"(rr[7])
-                       : "r"(ad));
-        }
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int c = 0; c < kCW; ++c) acc[c] += u64(rr[c]) << (8 * d);
+    }
+    if (m < M) {
+      u64* part = P.ksplit > 1 ? a.acc[slot] + u64(split) * a.nbatch * M * N : nullptr;
 #pragma unroll
-        for (int c = 0; c < kCW; ++c) acc[c] += u64(rr[c]) << (8 * d);
-      }
-      if (m < M) {
-#pragma unroll
-        for (int c = 0; c < kCW; ++c) {
-          const u32 n = n0 + u32(ch * kHalf + c0 + c);
-          if (n < N) gemm_epilogue(a, S, b, m, n, acc[c]);
+      for (int c = 0; c < kCW; ++c) {
+        const u32 n = n0 + u32(cg * kCW + c);
+        if (n < N) {
+          if (part)
+            part[(u64(b) * M + m) * N + n] = acc[c];
+          else
+            gemm_epilogue(a, S, b, m, n, acc[c]);
         }
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 9)
+  if (warp == kMmaWarp)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols) : "memory");
 }
 
@@ -363,20 +381,23 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
 // left: value = load_l(S, g, b*sL + row*K + k); right: load_r at (b*sR + k*N + row) or,
 // transposed, (b*sR + row*K + k).
 template <int BR>
-__global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int slot, int left, u32 rows, u32 nbatch, u32 nkb,
-                                                  char* out) {
+__global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows, u32 nbatch, u32 nkb, char* out0,
+                                                  char* out1) {
   pdl_enter();
+  const int slot = blockIdx.y;  // every local slot in one launch
+  char* out = slot ? out1 : out0;
   const GemmSlotArgs& S = a.sl[slot];
   const u32 K = a.K, N = a.N, nseg = u32(S.nseg);
   const u32 tiles = (rows + BR - 1) / BR;
-  const u64 units = u64(nbatch) * tiles * nkb * nseg * BR * 2;
+  // unit = 4 K-consecutive values of one row: one 4-byte word in each of the 8 limb planes
+  const u64 units = u64(nbatch) * tiles * nkb * nseg * BR * 8;
   constexpr u32 plane = BR * kKB;
   for (u64 uid = blockIdx.x * u64(blockDim.x) + threadIdx.x; uid < units; uid += u64(gridDim.x) * blockDim.x) {
     u64 t = uid;
     const u32 r = u32(t % BR);
     t /= BR;
-    const u32 kc = u32(t % 2);
-    t /= 2;
+    const u32 kq = u32(t % 8);  // 4-value quarter of the 32-value K block
+    t /= 8;
     const u32 g = u32(t % nseg);
     t /= nseg;
     const u32 kb = u32(t % nkb);
@@ -384,10 +405,10 @@ __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int slot, int left
     const u32 tile = u32(t % tiles);
     const u32 bb = u32(t / tiles);
     const u32 row = tile * BR + r;
-    const u32 k0 = kb * kKB + kc * 16;
-    u64 v[16];
+    const u32 k0 = kb * kKB + kq * 4;
+    u32 lo[4], hi[4];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < 4; ++i) {
       const u32 k = k0 + u32(i);
       u64 x = 0;
       if (row < rows && k < K) {
@@ -396,21 +417,30 @@ __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int slot, int left
         else
           x = load_r(S, int(g), u64(bb) * S.sR[g] + (a.tb ? u64(row) * K + k : u64(k) * N + row));
       }
-      v[i] = x;
+      lo[i] = u32(x);
+      hi[i] = u32(x >> 32);
     }
     char* base = out + ((((u64(bb) * tiles + tile) * nkb + kb) * nseg + g) * 8) * plane;
-    transpose_store(v, base, plane, (kc * (BR / 8) + r / 8) * 128 + (r % 8) * 16);
+    const u32 kc = kq / 4;  // which 16-byte K chunk of the core matrix
+    const u32 off = (kc * (BR / 8) + r / 8) * 128 + (r % 8) * 16 + (kq % 4) * 4;
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+      const u32* w = l < 4 ? lo : hi;
+      *reinterpret_cast<u32*>(base + l * plane + off) = gather4(w[0], w[1], w[2], w[3], u32(l & 3));
+    }
   }
 }
 
 template <int BR>
-void launch_pack(Session& s, const GemmArgs& a, int slot, bool left, u32 rows, u32 nbatch, u32 nkb, char* out) {
+void launch_pack(Session& s, const GemmArgs& a, bool left, u32 rows, u32 nbatch, u32 nkb, char* out0, char* out1) {
   const u32 tiles = (rows + BR - 1) / BR;
-  const u64 units = u64(nbatch) * tiles * nkb * a.sl[slot].nseg * BR * 2;
+  int maxseg = 0;
+  for (int i = 0; i < a.nslots; ++i) maxseg = a.sl[i].nseg > maxseg ? a.sl[i].nseg : maxseg;
+  const u64 units = u64(nbatch) * tiles * nkb * maxseg * BR * 8;
   cudaEvent_t pe;
   probe_begin(s.stream, &pe);
-  launch_pdl(pack_limbs<BR>, dim3(ew_blocks(units)), dim3(256), 0, s.stream, a, slot, left ? 1 : 0, rows, nbatch,
-             nkb, out);
+  launch_pdl(pack_limbs<BR>, dim3(ew_blocks(units), a.nslots), dim3(256), 0, s.stream, a, left ? 1 : 0, rows, nbatch,
+             nkb, out0, out1);
   probe_end(s.stream, pe);
 }
 
@@ -433,22 +463,28 @@ void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
     for (int g = 0; g < a.sl[i].nseg; ++g) rbatched |= a.sl[i].sR[g] != 0;
   const u32 rb = rbatched ? a.nbatch : 1;
   std::vector<std::shared_ptr<Block>> keep;
-  for (int i = 0; i < a.nslots; ++i) {
+  {
     ClassScope pack_scope(kClsOther, 0);  // the roofline probe times the GEMM kernel itself
-    const u64 rbytes = u64(ntiles) * P.nkb * a.sl[i].nseg * 8 * BN * kKB;
-    auto blk = s.raw((rbytes * rb + 7) / 8);
-    keep.push_back(blk);
-    launch_pack<BN>(s, a, i, false, a.N, rb, P.nkb, reinterpret_cast<char*>(blk->ptr));
-    P.Rpk[i] = reinterpret_cast<const char*>(blk->ptr);
-    P.Rpk_b[i] = rbatched ? rbytes : 0;
-    if (packL) {
-      const u64 lbytes = u64(mtiles) * P.nkb * a.sl[i].nseg * 8 * kM * kKB;
-      auto lb = s.raw((lbytes * a.nbatch + 7) / 8);
-      keep.push_back(lb);
-      launch_pack<kM>(s, a, i, true, a.M, a.nbatch, P.nkb, reinterpret_cast<char*>(lb->ptr));
-      P.Lpk[i] = reinterpret_cast<const char*>(lb->ptr);
-      P.Lpk_b[i] = lbytes;
+    char* rp[2] = {nullptr, nullptr};
+    char* lp[2] = {nullptr, nullptr};
+    for (int i = 0; i < a.nslots; ++i) {
+      const u64 rbytes = u64(ntiles) * P.nkb * a.sl[i].nseg * 8 * BN * kKB;
+      auto blk = s.raw((rbytes * rb + 7) / 8);
+      keep.push_back(blk);
+      rp[i] = reinterpret_cast<char*>(blk->ptr);
+      P.Rpk[i] = rp[i];
+      P.Rpk_b[i] = rbatched ? rbytes : 0;
+      if (packL) {
+        const u64 lbytes = u64(mtiles) * P.nkb * a.sl[i].nseg * 8 * kM * kKB;
+        auto lb = s.raw((lbytes * a.nbatch + 7) / 8);
+        keep.push_back(lb);
+        lp[i] = reinterpret_cast<char*>(lb->ptr);
+        P.Lpk[i] = lp[i];
+        P.Lpk_b[i] = lbytes;
+      }
     }
+    launch_pack<BN>(s, a, false, a.N, rb, P.nkb, rp[0], rp[1]);
+    if (packL) launch_pack<kM>(s, a, true, a.M, a.nbatch, P.nkb, lp[0], lp[1]);
   }
   bool vec = (a.K % 2) == 0;
   for (int i = 0; i < a.nslots && vec; ++i)
@@ -459,11 +495,34 @@ void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
       if (S.lk[g] == kOpSum) vec = vec && reinterpret_cast<uintptr_t>(S.L2[g]) % 16 == 0;
     }
   P.vec = vec ? 1 : 0;
-  dim3 grid(ntiles, mtiles, a.nslots * a.nbatch);
+  // split K when the tile grid cannot fill the SMs (small-M layers): >= 2 K blocks per split
+  const u64 ctas = u64(ntiles) * mtiles * a.nslots * a.nbatch;
+  u32 split = 1;
+  if (ctas < u64(kSms)) {
+    split = u32((kSms + ctas - 1) / ctas);
+    split = split > 16 ? 16 : split;
+    const u32 maxs = P.nkb / 2 > 0 ? P.nkb / 2 : 1;
+    split = split > maxs ? maxs : split;
+  }
+  P.kbper = (P.nkb + split - 1) / split;
+  P.ksplit = (P.nkb + P.kbper - 1) / P.kbper;
+  std::shared_ptr<Block> ws;
+  if (P.ksplit > 1) {
+    const u64 per = u64(a.nbatch) * a.M * a.N;
+    ws = s.raw(per * P.ksplit * a.nslots);
+    for (int i = 0; i < a.nslots; ++i) P.g.acc[i] = ws->ptr + i * per * P.ksplit;
+    P.g.ksplit = P.ksplit;
+  }
+  dim3 grid(ntiles, mtiles, a.nslots * a.nbatch * P.ksplit);
   cudaEvent_t pe;
   probe_begin(s.stream, &pe);
   launch_pdl(ring_gemm_tc2<BN>, grid, dim3(kThreads), smem, s.stream, P);
   probe_end(s.stream, pe);
+  if (P.ksplit > 1) {
+    ClassScope ep_scope(kClsOther, 0);
+    const u64 n = u64(a.nbatch) * a.M * a.N * a.nslots;
+    launch_pdl(gemm_splitk_epilogue_fn(), dim3(ew_blocks(n)), dim3(256), 0, s.stream, P.g);
+  }
   // the packed buffers are stream-ordered pool blocks (or graph-arena blocks): released
   // after the GEMM's queued reads by the Block destructor
 }

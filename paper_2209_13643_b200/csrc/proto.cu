@@ -364,6 +364,9 @@ void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const
   const Session::MaskRef mr = s.take_mask(n);
   DT keep = s.alloc(Shape{n}), S = s.alloc(Shape{n}), P = s.alloc(Shape{n}), P0 = s.alloc(Shape{n}),
      bits = s.alloc(Shape{n});
+  DT cw[2];  // issue-to-settle draw cache (ew.cuh)
+  if (adder_draw_cache_ok(s, n) && (s.n_local == 1 || pair_eval_enabled()))
+    for (auto& b : cw) b = s.alloc(Shape{8 * n});
   Open om = s.begin_open(n, Reduce::Sum);
   Open oa[7];
   for (int r = 0; r < 7; ++r) oa[r] = s.begin_open((r == 0 ? 2 : 4) * n, Reduce::Xor);
@@ -400,6 +403,11 @@ void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const
     k.wmask = c.wmask;
     k.xf = xf;
     k.yf = yf;
+    if (cw[0]) {
+      k.cwN = n;
+      if (r >= 1) k.cwp = cw[(r - 1) & 1].s[0];
+      if (r <= 6) k.cwn = cw[r & 1].s[0];
+    }
     if (r == 7) k.ff = B2aBuildFF{t1.ew, own_ptrs(ob), ptrs(bits), 0, n};
   }
   p.nadder = 8;
