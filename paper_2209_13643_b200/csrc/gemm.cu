@@ -271,7 +271,26 @@ __global__ void __launch_bounds__(256) ring_gemm_rows(GemmArgs a) {
     if (m >= M) continue;
     for (int g = 0; g < S.nseg; ++g) {
       const u64 rowbase = u64(m) * K + k0;
-      for (u32 kk = 0; kk < kc; ++kk) {
+      const int kind = S.lk[g];
+      u32 kk = 0;
+      if (kind == kOpMem || kind == kOpSum) {  // 8 independent loads in flight per thread
+        const u64* p = S.L[g] + rowbase;
+        const u64* p2 = S.L2[g] + rowbase;
+        for (; kk + 8 <= kc; kk += 8) {
+          u64 v[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = __ldg(p + kk + i);
+          if (kind == kOpSum) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] += __ldg(p2 + kk + i);
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int n = 0; n < NR; ++n) acc[n] += v[i] * Rs[g][kk + i][n];
+        }
+      }
+      for (; kk < kc; ++kk) {
         const u64 v = load_l(S, g, rowbase + kk);
 #pragma unroll
         for (int n = 0; n < NR; ++n) acc[n] += v * Rs[g][kk][n];
@@ -390,8 +409,90 @@ void eps_build_mem(Session& s, const Triple& t, const u64* const x[2], size_t a_
 
 // im2col-fused eps build for conv layers (H/engine/executor.hpp:82-108): row=(n,oh,ow),
 // col=(ci,ki,kj), padding taps read zero.
+// Row-strip form: one thread owns a strip of kStrip im2col columns of one row (n,oh,ow), walks
+// (ci,ki,kj) incrementally (no per-element divisions) and, when both party slots are local,
+// evaluates both with one draw of r_A per element (party 0 also draws A), as the dealer does.
+namespace {
+constexpr u32 kStrip = 8;
+struct EpsIm2colPair {
+  MmTriple mm;
+  Pid2 pid;
+  Ptr2 own, ap;
+  CPtr2 xp;
+  ConvGeom g;
+  u64 a_off, na;
+  int nslots;
+  __device__ void operator()(u64 t) const {
+    const u32 KK = g.C * g.k * g.k;
+    const u32 strips = (KK + kStrip - 1) / kStrip;
+    const u32 r = u32(t / strips), c0 = u32(t % strips) * kStrip;
+    const u32 ow = r % g.OW, oh = (r / g.OW) % g.OH, n = r / (g.OW * g.OH);
+    u32 kj = c0 % g.k, ki = (c0 / g.k) % g.k, ci = c0 / (g.k * g.k);
+    const u64 key = tkey(mm.key, mm.kp);
+    const u64 rowoff = u64(r) * KK;
+    const int ih0 = int(oh * g.stride) - int(g.pad), iw0 = int(ow * g.stride) - int(g.pad);
+    for (u32 c = c0; c < c0 + kStrip && c < KK; ++c) {
+      const u64 j = rowoff + c;  // call-local element
+      const u64 idx = a_off + j;
+      const u64 ip = idx * kPhi;
+      const u64 ra = mix64(key + mm.prA + ip);
+      const int ih = ih0 + int(ki), iw = iw0 + int(kj);
+      const bool in = ih >= 0 && iw >= 0 && ih < int(g.H) && iw < int(g.W);
+      const u64 src = ((u64(n) * g.C + ci) * g.H + u32(ih)) * g.W + u32(iw);
+      u64 A = 0;
+      bool haveA = false;
+#pragma unroll
+      for (int sl = 0; sl < 2; ++sl) {
+        if (sl >= nslots) break;
+        const u64 v = in ? xp.p[sl][src] : 0;
+        u64 a;
+        if (pid.v[sl] == 0) {
+          if (!haveA) {
+            A = mix64(key + mm.pA + ip);
+            haveA = true;
+          }
+          a = A - ra;
+          if (ap.p[sl]) {
+            ap.p[sl][j] = A;
+            ap.p[sl][na + j] = a;
+          }
+        } else {
+          a = ra;
+          if (ap.p[sl]) ap.p[sl][j] = ra;
+        }
+        own.p[sl][j] = v - a;
+      }
+      if (++kj == g.k) {
+        kj = 0;
+        if (++ki == g.k) {
+          ki = 0;
+          ++ci;
+        }
+      }
+    }
+  }
+};
+template <class F>
+__global__ void __launch_bounds__(256) strip_kernel(u64 n, F f) {
+  pdl_enter();
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) f(i);
+}
+}  // namespace
+
 void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const ConvGeom& gm, size_t a_off,
                       size_t na, Open& o, const DT* aops) {
+  if (a_off == 0 && na % (u64(gm.C) * gm.k * gm.k) == 0) {  // whole rows: the strip kernel
+    const u32 KK = gm.C * gm.k * gm.k;
+    const u64 rows = na / KK, units = rows * ((KK + kStrip - 1) / kStrip);
+    EpsIm2colPair f{t.mm, pids(s), own_ptrs(o),
+                    Ptr2{{aops ? aops->s[0] : nullptr, aops && s.n_local == 2 ? aops->s[1] : nullptr}},
+                    CPtr2{{x[0], s.n_local == 2 ? x[1] : nullptr}}, gm, a_off, na, s.n_local};
+    cudaEvent_t pe;
+    probe_begin(s.stream, &pe);
+    launch_pdl(strip_kernel<EpsIm2colPair>, dim3(ew_blocks(units)), dim3(256), 0, s.stream, units, f);
+    probe_end(s.stream, pe);
+    return;
+  }
   const Pid2 pid = pids(s);
   const Ptr2 own = own_ptrs(o);
   const MmTriple mm = t.mm;

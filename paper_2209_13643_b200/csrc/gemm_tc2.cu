@@ -31,6 +31,7 @@ constexpr int kKB = 32;        // K values (= limb bytes) per stage: one UMMA K 
 constexpr int kStages = 4;
 constexpr int kProdWarps = 16;                 // L producers (and epilogue): warps 0-15
 constexpr int kVW = 8;                         // K values per producer unit (= 8-byte limb row segment)
+constexpr u32 kL2Ahead = 3;                    // K blocks of L2 prefetch ahead of the register loads
 constexpr int kLoadWarp = kProdWarps;          // bulk loader
 constexpr int kMmaWarp = kProdWarps + 1;       // MMA issuer, TMEM owner
 constexpr int kThreads = (kProdWarps + 2) * 32;
@@ -245,6 +246,13 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
         if (!sum) {
 #pragma unroll
           for (int i = 0; i < kVW; ++i) pr2[i] = 0;
+        }
+        // deeper, register-free prefetch: pull block kb+kL2Ahead into L2 so that the register
+        // load issued one block ahead finds it there (HBM latency > one block of producer work)
+        const u32 kp = (kb + kL2Ahead) * kKB + u32(q) * kVW;
+        if (rowok && kb + kL2Ahead < kb1 && kp < K) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(S.L[pf] + rowoff + kp));
+          if (sum) asm volatile("prefetch.global.L2 [%0];" ::"l"(S.L2[pf] + rowoff + kp));
         }
       };
       if (pf >= 0) fetch(kb0);
@@ -554,7 +562,13 @@ bool ring_gemm_tc2_try(Session& s, const GemmArgs& a) {
       const GemmSlotArgs& S = a.sl[i];
       if (S.sL[g] != S.sL[0]) return false;  // the producer uses one row stride for every segment
     }
-  const bool multiN = a.N > 64;
+  // several N tiles: pack the left operand once (bulk-copied per tile) or regenerate it per
+  // tile in the producers (CTAs of one M tile run side by side, so E re-reads hit L2).
+  static const int packl = [] {
+    const char* e = std::getenv("MPCG_TC2_PACKL");
+    return e ? e[0] - '0' : 0;
+  }();
+  const bool multiN = a.N > 64 && packl == 1;
   if (a.N > 32)
     launch_tc2<64>(s, a, multiN);
   else if (a.N > 16)
