@@ -601,10 +601,28 @@ def scale_rescale(X, c, f):
     return truncate_shares([x * k for x in X], f)
 
 
+RECIP_UNIT_ITERS = 3
+
+
+def recip_unit_shares(D, ctx: Ctx, tag="recip", iters=RECIP_UNIT_ITERS):
+    """1/d for d in [1, 2]: linear seed y0 = 24/17 - 8/17 d (relative error <= 1/17), then the
+    reference's Newton step y <- trunc(y (2 - trunc(d y))) (H/nonlinear/approx.hpp:52-60);
+    three steps take the error below 2^-30, so the reference's exp seed and ten steps are not
+    needed on this interval."""
+    f = ctx.frac_bits
+    ch = ctx.chunks_for(D[0].size)
+    y = add_public([U64(0) - v for v in scale_rescale(D, 8.0 / 17.0, f)], int(encode_fixed(24.0 / 17.0, f)))
+    for i in range(iters):
+        xy = truncate_shares(beaver_mul(D, y, ctx, f"{tag}.xy{i}", ch), f)
+        u = add_public([U64(0) - xy[0], U64(0) - xy[1]], 2 << f)
+        y = truncate_shares(beaver_mul(y, u, ctx, f"{tag}.yu{i}", ch), f)
+    return y
+
+
 def sigmoid_shares(X, ctx: Ctx, tag="sigmoid"):
     """sigma(x) = b ? 1 - sigma(|x|) : sigma(|x|), b = [x < 0], sigma(|x|) = 1/(1 + exp(-|x|)).
     exp only ever sees -|x| <= 0 (exp_shares' accurate side, H/nonlinear/approx.hpp:22-39) and the
-    reciprocal only (1, 2] (inside reciprocal_shares' convergence range, approx.hpp:43-62)."""
+    reciprocal only (1, 2] (recip_unit_shares)."""
     f = ctx.frac_bits
     ch = ctx.chunks_for(X[0].size)
     s = msb(X, ctx, tag + ".msb", ch)
@@ -612,7 +630,7 @@ def sigmoid_shares(X, ctx: Ctx, tag="sigmoid"):
     xb = beaver_mul(X, b, ctx, tag + ".abs", ch)
     nabs = [(xb[p] + xb[p]) - X[p] for p in range(2)]                 # -|x|
     e = exp_shares(nabs, ctx, tag + ".exp")
-    r = reciprocal_shares(add_public(e, 1 << f), ctx, tag + ".recip")  # sigma(|x|)
+    r = recip_unit_shares(add_public(e, 1 << f), ctx, tag + ".recip")  # sigma(|x|)
     t = add_public([U64(0) - (r[p] + r[p]) for p in range(2)], 1 << f)  # 1 - 2 sigma(|x|)
     sel = beaver_mul(b, t, ctx, tag + ".sel", ch)                      # b has scale 0: no truncation
     return [r[p] + sel[p] for p in range(2)]

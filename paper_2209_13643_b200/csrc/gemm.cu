@@ -409,66 +409,65 @@ void eps_build_mem(Session& s, const Triple& t, const u64* const x[2], size_t a_
 
 // im2col-fused eps build for conv layers (H/engine/executor.hpp:82-108): row=(n,oh,ow),
 // col=(ci,ki,kj), padding taps read zero.
-// Row-strip form: one thread owns a strip of kStrip im2col columns of one row (n,oh,ow), walks
-// (ci,ki,kj) incrementally (no per-element divisions) and, when both party slots are local,
-// evaluates both with one draw of r_A per element (party 0 also draws A), as the dealer does.
+// One thread per im2col element (consecutive threads write consecutive words: fully
+// coalesced payload stores), index decomposition by invariant-divisor multiplication instead of
+// hardware-less 32-bit division, and, when both party slots are local, one r_A draw per element
+// for both slots (party 0 also draws A), as the dealer does.
 namespace {
-constexpr u32 kStrip = 8;
+struct FastDiv {  // q = n / d for any 32-bit n (Granlund-Montgomery, round-up multiplier)
+  u32 d, m, l;
+  FastDiv() = default;
+  explicit FastDiv(u32 dv) : d(dv) {
+    l = 0;
+    while ((u64(1) << l) < dv) ++l;
+    m = u32(((u64(1) << 32) * ((u64(1) << l) - dv)) / dv + 1);
+  }
+  __device__ __forceinline__ u32 div(u32 n) const { return u32((u64(__umulhi(m, n)) + n) >> l); }
+};
 struct EpsIm2colPair {
   MmTriple mm;
   Pid2 pid;
   Ptr2 own, ap;
   CPtr2 xp;
   ConvGeom g;
+  FastDiv fKK, fk, fOW, fOH;
   u64 a_off, na;
   int nslots;
-  __device__ void operator()(u64 t) const {
-    const u32 KK = g.C * g.k * g.k;
-    const u32 strips = (KK + kStrip - 1) / kStrip;
-    const u32 r = u32(t / strips), c0 = u32(t % strips) * kStrip;
-    const u32 ow = r % g.OW, oh = (r / g.OW) % g.OH, n = r / (g.OW * g.OH);
-    u32 kj = c0 % g.k, ki = (c0 / g.k) % g.k, ci = c0 / (g.k * g.k);
+  __device__ void operator()(u64 j) const {
+    const u32 jj = u32(j);
+    const u32 r = fKK.div(jj), c = jj - r * fKK.d;
+    const u32 rq = fOW.div(r), ow = r - rq * g.OW;
+    const u32 n = fOH.div(rq), oh = rq - n * g.OH;
+    const u32 c1 = fk.div(c), kj = c - c1 * g.k;
+    const u32 ci = fk.div(c1), ki = c1 - ci * g.k;
+    const int ih = int(oh * g.stride + ki) - int(g.pad), iw = int(ow * g.stride + kj) - int(g.pad);
+    const bool in = ih >= 0 && iw >= 0 && ih < int(g.H) && iw < int(g.W);
+    const u64 src = ((u64(n) * g.C + ci) * g.H + u32(ih)) * g.W + u32(iw);
     const u64 key = tkey(mm.key, mm.kp);
-    const u64 rowoff = u64(r) * KK;
-    const int ih0 = int(oh * g.stride) - int(g.pad), iw0 = int(ow * g.stride) - int(g.pad);
-    for (u32 c = c0; c < c0 + kStrip && c < KK; ++c) {
-      const u64 j = rowoff + c;  // call-local element
-      const u64 idx = a_off + j;
-      const u64 ip = idx * kPhi;
-      const u64 ra = mix64(key + mm.prA + ip);
-      const int ih = ih0 + int(ki), iw = iw0 + int(kj);
-      const bool in = ih >= 0 && iw >= 0 && ih < int(g.H) && iw < int(g.W);
-      const u64 src = ((u64(n) * g.C + ci) * g.H + u32(ih)) * g.W + u32(iw);
-      u64 A = 0;
-      bool haveA = false;
+    const u64 ip = (a_off + j) * kPhi;
+    const u64 ra = mix64(key + mm.prA + ip);
+    u64 A = 0;
+    bool haveA = false;
 #pragma unroll
-      for (int sl = 0; sl < 2; ++sl) {
-        if (sl >= nslots) break;
-        const u64 v = in ? xp.p[sl][src] : 0;
-        u64 a;
-        if (pid.v[sl] == 0) {
-          if (!haveA) {
-            A = mix64(key + mm.pA + ip);
-            haveA = true;
-          }
-          a = A - ra;
-          if (ap.p[sl]) {
-            ap.p[sl][j] = A;
-            ap.p[sl][na + j] = a;
-          }
-        } else {
-          a = ra;
-          if (ap.p[sl]) ap.p[sl][j] = ra;
+    for (int sl = 0; sl < 2; ++sl) {
+      if (sl >= nslots) break;
+      const u64 v = in ? xp.p[sl][src] : 0;
+      u64 a;
+      if (pid.v[sl] == 0) {
+        if (!haveA) {
+          A = mix64(key + mm.pA + ip);
+          haveA = true;
         }
-        own.p[sl][j] = v - a;
-      }
-      if (++kj == g.k) {
-        kj = 0;
-        if (++ki == g.k) {
-          ki = 0;
-          ++ci;
+        a = A - ra;
+        if (ap.p[sl]) {
+          ap.p[sl][j] = A;
+          ap.p[sl][na + j] = a;
         }
+      } else {
+        a = ra;
+        if (ap.p[sl]) ap.p[sl][j] = ra;
       }
+      own.p[sl][j] = v - a;
     }
   }
 };
@@ -481,15 +480,14 @@ __global__ void __launch_bounds__(256) strip_kernel(u64 n, F f) {
 
 void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const ConvGeom& gm, size_t a_off,
                       size_t na, Open& o, const DT* aops) {
-  if (a_off == 0 && na % (u64(gm.C) * gm.k * gm.k) == 0) {  // whole rows: the strip kernel
-    const u32 KK = gm.C * gm.k * gm.k;
-    const u64 rows = na / KK, units = rows * ((KK + kStrip - 1) / kStrip);
+  if (a_off == 0 && na < (u64(1) << 32)) {  // call-local indices fit the 32-bit fast division
     EpsIm2colPair f{t.mm, pids(s), own_ptrs(o),
                     Ptr2{{aops ? aops->s[0] : nullptr, aops && s.n_local == 2 ? aops->s[1] : nullptr}},
-                    CPtr2{{x[0], s.n_local == 2 ? x[1] : nullptr}}, gm, a_off, na, s.n_local};
+                    CPtr2{{x[0], s.n_local == 2 ? x[1] : nullptr}}, gm, FastDiv(gm.C * gm.k * gm.k), FastDiv(gm.k),
+                    FastDiv(gm.OW), FastDiv(gm.OH), a_off, na, s.n_local};
     cudaEvent_t pe;
     probe_begin(s.stream, &pe);
-    launch_pdl(strip_kernel<EpsIm2colPair>, dim3(ew_blocks(units)), dim3(256), 0, s.stream, units, f);
+    launch_pdl(strip_kernel<EpsIm2colPair>, dim3(ew_blocks(na)), dim3(256), 0, s.stream, u64(na), f);
     probe_end(s.stream, pe);
     return;
   }

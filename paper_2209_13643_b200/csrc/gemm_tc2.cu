@@ -564,11 +564,13 @@ bool ring_gemm_tc2_try(Session& s, const GemmArgs& a) {
     }
   // several N tiles: pack the left operand once (bulk-copied per tile) or regenerate it per
   // tile in the producers (CTAs of one M tile run side by side, so E re-reads hit L2).
+  // Measured: regenerating wins up to 8 tiles (ResNet-18 / VGG-16 convs), packing beyond
+  // (BERT's 768..3072-wide projections, where the dealer draws would repeat 12..48 times).
   static const int packl = [] {
-    const char* e = std::getenv("MPCG_TC2_PACKL");
-    return e ? e[0] - '0' : 0;
+    const char* e = std::getenv("MPCG_TC2_PACKL");  // 0 = never, 1 = whenever N > 64, else auto
+    return e ? e[0] - '0' : 2;
   }();
-  const bool multiN = a.N > 64 && packl == 1;
+  const bool multiN = a.N > 64 && (packl == 1 || (packl == 2 && a.N > 512));
   if (a.N > 32)
     launch_tc2<64>(s, a, multiN);
   else if (a.N > 16)

@@ -663,6 +663,16 @@ struct OutAffine {  // out[g] = k*y + [p0] c   (reciprocal seed 3 exp + 0.003; s
     out.p[slot][g] = y * k + (party == 0 ? c : 0);
   }
 };
+struct OutRecipSeed {  // d = y + [p0] 1; seed = [p0] c0 - trunc(d * c1, f)
+  Ptr2 d, seed;
+  u64 one, c1, c0;
+  int f;
+  __device__ void operator()(int slot, int party, u64 g, u64 y) const {
+    const u64 dv = y + (party == 0 ? one : 0);
+    d.p[slot][g] = dv;
+    seed.p[slot][g] = (party == 0 ? c0 : 0) - sar64(dv * c1, f);
+  }
+};
 struct SrcConstMinus {  // [p0] c - x[g]   (reciprocal seed argument 0.5 - x)
   Pid2 pid;
   CPtr2 x;
@@ -714,14 +724,11 @@ struct RecipPV {
 };
 }  // namespace
 
-DT reciprocal_shares(Session& s, const DT& x, const std::string& tag, int newton_iters) {
+// Newton steps y <- trunc(y (2 - trunc(x y))) on y in place (approx.hpp:52-60), one fused chain.
+static void recip_newton(Session& s, const DT& x, DT& y, const std::string& tag, int newton_iters) {
   const int f = s.cfg.frac_bits;
   const size_t n = x.numel();
-  // y0 = 3 exp(0.5 - x) + 0.003  (H/nonlinear/approx.hpp:49-51), the seed exp fused in
-  DT y = s.alloc(x.shape, x.scale);
-  exp_chain(s, x.shape, tag + ".seed", 7, SrcConstMinus{pids(s), cptrs(x), encode_fixed(0.5, f)},
-            OutAffine{ptrs(y), 3, encode_fixed(0.003, f)});
-  if (newton_iters <= 0) return y;
+  if (newton_iters <= 0) return;
   std::vector<Triple> tr;
   std::vector<std::string> tags;
   for (int i = 0; i < newton_iters; ++i) {
@@ -734,6 +741,15 @@ DT reciprocal_shares(Session& s, const DT& x, const std::string& tag, int newton
   }
   mul_chain(s, n, chunks_for(s, n), tr, tags, SrcMem{cptrs(x)}, SrcMem{cptrs(y)},
             [&](int r) { return RecipPV{cptrs(x), ptrs(y), f, r & 1}; });
+}
+
+DT reciprocal_shares(Session& s, const DT& x, const std::string& tag, int newton_iters) {
+  const int f = s.cfg.frac_bits;
+  // y0 = 3 exp(0.5 - x) + 0.003  (H/nonlinear/approx.hpp:49-51), the seed exp fused in
+  DT y = s.alloc(x.shape, x.scale);
+  exp_chain(s, x.shape, tag + ".seed", 7, SrcConstMinus{pids(s), cptrs(x), encode_fixed(0.5, f)},
+            OutAffine{ptrs(y), 3, encode_fixed(0.003, f)});
+  recip_newton(s, x, y, tag, newton_iters);
   return y;
 }
 
@@ -835,9 +851,12 @@ DT sigmoid_shares(Session& s, const DT& x, const std::string& tag) {
   DT b = s.alloc(x.shape, 0), nabs = s.alloc(x.shape, x.scale);
   compare_mul(s, n, adder_for(s, n), tag + ".msb", tag + ".b2a", ch, tag + ".abs", ch, SrcMem{cptrs(x)},
               SrcMem{cptrs(x)}, SinkNegAbs{cptrs(x), ptrs(nabs)}, ptrs(b));
-  DT d = s.alloc(x.shape, x.scale);  // 1 + exp(-|x|), the +1 fused into the exp chain's last round
-  exp_chain(s, x.shape, tag + ".exp", 7, SrcMem{cptrs(nabs)}, OutAffine{ptrs(d), 1, u64(1) << f});
-  DT r = reciprocal_shares(s, d, tag + ".recip");
+  // d = 1 + exp(-|x|) in (1, 2] and the reciprocal's linear seed y0 = 24/17 - 8/17 d, both
+  // formed in the exp chain's last round; then three Newton steps (oracle recip_unit_shares)
+  DT d = s.alloc(x.shape, x.scale), r = s.alloc(x.shape, x.scale);
+  exp_chain(s, x.shape, tag + ".exp", 7, SrcMem{cptrs(nabs)},
+            OutRecipSeed{ptrs(d), ptrs(r), u64(1) << f, encode_fixed(8.0 / 17.0, f), encode_fixed(24.0 / 17.0, f), f});
+  recip_newton(s, d, r, tag + ".recip", kRecipUnitIters);
   Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Arith, x.shape), tag + ".sel");
   t.mark_consumed();
   DT out = s.alloc(x.shape, x.scale);
