@@ -253,10 +253,10 @@ template <int NR>
 __global__ void __launch_bounds__(256) ring_gemm_rows(GemmArgs a) {
   __shared__ u64 Rs[3][kRowKC][NR];
   pdl_enter();
-  const int slot = blockIdx.y;
+  const int slot = int(blockIdx.x % a.nslots);  // both slots of a row block co-scheduled (shared E in L2)
   const GemmSlotArgs& S = a.sl[slot];
   const u32 M = a.M, N = a.N, K = a.K;
-  const u32 m = blockIdx.x * 256 + threadIdx.x;
+  const u32 m = (blockIdx.x / a.nslots) * 256 + threadIdx.x;
   u64 acc[NR];
 #pragma unroll
   for (int n = 0; n < NR; ++n) acc[n] = 0;
@@ -329,7 +329,7 @@ void ring_gemm_launch(Session& s, const GemmArgs& a) {
   if (rows_eligible(a) && gemv_mode() != 0) {  // skinny N: one thread per output row
     cudaEvent_t pe;
     probe_begin(s.stream, &pe);
-    launch_pdl(ring_gemm_rows<kRowN>, dim3((a.M + 255) / 256, a.nslots), dim3(256), 0, s.stream, a);
+    launch_pdl(ring_gemm_rows<kRowN>, dim3((a.M + 255) / 256 * a.nslots), dim3(256), 0, s.stream, a);
     probe_end(s.stream, pe);
     s.check();
     return;

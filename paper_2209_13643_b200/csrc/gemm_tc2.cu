@@ -177,12 +177,15 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
   pdl_enter();
   const GemmArgs& a = P.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int slot = blockIdx.z % a.nslots;
-  const u32 b = (blockIdx.z / a.nslots) % a.nbatch;
-  const u32 split = blockIdx.z / (a.nslots * a.nbatch);
+  // grid.x = (N tile, slot) with the slot fastest: the CTAs that read the same opened-E rows
+  // (both party slots of an M tile, every N tile) are co-scheduled, so the rows come from L2.
+  const int slot = int(blockIdx.x % a.nslots);
+  const u32 ntile = blockIdx.x / a.nslots;
+  const u32 b = blockIdx.z % a.nbatch;
+  const u32 split = blockIdx.z / a.nbatch;
   const GemmSlotArgs& S = a.sl[slot];
   const u32 M = a.M, N = a.N, K = a.K;
-  const u32 m0 = blockIdx.y * kM, n0 = blockIdx.x * BN;
+  const u32 m0 = blockIdx.y * kM, n0 = ntile * BN;
   const int nseg = S.nseg;
   const u32 kb0 = split * P.kbper, kb1 = min(P.nkb, kb0 + P.kbper);  // this CTA's K blocks
   const u32 nst = (kb1 - kb0) * u32(nseg);
@@ -307,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
   } else if (warp == kLoadWarp) {
     if (lane == 0) {  // ---- bulk loader
       const char* Rb = P.Rpk[slot] + u64(b) * P.Rpk_b[slot] +
-                       (u64(blockIdx.x) * P.nkb + kb0) * u64(nseg) * 8 * kB;
+                       (u64(ntile) * P.nkb + kb0) * u64(nseg) * 8 * kB;
       const char* Lb = packedL ? P.Lpk[slot] + u64(b) * P.Lpk_b[slot] +
                                      (u64(blockIdx.y) * P.nkb + kb0) * u64(nseg) * 8 * kA
                                : nullptr;
@@ -521,7 +524,7 @@ void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
     for (int i = 0; i < a.nslots; ++i) P.g.acc[i] = ws->ptr + i * per * P.ksplit;
     P.g.ksplit = P.ksplit;
   }
-  dim3 grid(ntiles, mtiles, a.nslots * a.nbatch * P.ksplit);
+  dim3 grid(ntiles * a.nslots, mtiles, a.nbatch * P.ksplit);
   cudaEvent_t pe;
   probe_begin(s.stream, &pe);
   launch_pdl(ring_gemm_tc2<BN>, grid, dim3(kThreads), smem, s.stream, P);
