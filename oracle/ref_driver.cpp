@@ -9,6 +9,10 @@
 //       inputs and per-party output shares. tests/golden/make_golden.py turns the
 //       dump into tests/golden/*.npz fixtures.
 //
+//   ref_driver mpcw <model.json> <seed> <out.mpcw> [<in.mpcw>]
+//       The reference's init_weights written with its save_weights, or a file read back by
+//       its load_weights/check_weights and re-saved (MPCW interchange pin).
+//
 //   ref_driver bench <model.json> <blocking|pipelined> <iters> <private|public> <seed>
 //                    [<chunks> <threshold_bytes>]
 //       Times bench_party (H/engine/bench.hpp:36-79) with the two parties as threads
@@ -319,6 +323,23 @@ int cmd_bench(int argc, char** argv) {
   return 0;
 }
 
+// MPCW interchange check: the reference's own init_weights(model, seed) written by its
+// save_weights (H/engine/model.hpp:257-275,277-313), and a file read back by its
+// load_weights + check_weights (:315-376) and re-saved, so the package's MPCW reader/writer
+// can be compared byte for byte.
+int cmd_mpcw(const char* model_path, unsigned long long seed, const char* out_path, const char* in_path) {
+  using namespace mpcpipe;
+  const ModelGraph g = load_model(model_path);
+  if (in_path) {
+    WeightMap w = load_weights(in_path);
+    check_weights(g, w);
+    save_weights(w, out_path);
+  } else {
+    save_weights(init_weights(g, seed), out_path);
+  }
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -328,6 +349,8 @@ int main(int argc, char** argv) {
       return cmd_model_golden(argv[2], argv[3], std::atoi(argv[4]), argv[5],
                               std::strtoull(argv[6], nullptr, 10), argv[7]);
     if (argc >= 7 && std::string(argv[1]) == "bench") return cmd_bench(argc, argv);
+    if (argc >= 5 && std::string(argv[1]) == "mpcw")
+      return cmd_mpcw(argv[2], std::strtoull(argv[3], nullptr, 10), argv[4], argc >= 6 ? argv[5] : nullptr);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "ref_driver: %s\n", e.what());
     return 1;
@@ -335,6 +358,7 @@ int main(int argc, char** argv) {
   std::fprintf(stderr,
                "usage: ref_driver golden <out.bin>\n"
                "       ref_driver model <model.json> <mode> <iters> <private|public> <seed> <out.bin>\n"
-               "       ref_driver bench <model.json> <mode> <iters> <private|public> <seed> [chunks thr]\n");
+               "       ref_driver bench <model.json> <mode> <iters> <private|public> <seed> [chunks thr]\n"
+               "       ref_driver mpcw <model.json> <seed> <out.mpcw> [<in.mpcw>]\n");
   return 2;
 }

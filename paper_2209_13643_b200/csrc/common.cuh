@@ -329,7 +329,7 @@ __device__ __forceinline__ void eval_slots(const F& f, bool pair, int slot, u64 
 }
 
 template <class F>
-__global__ void __launch_bounds__(256) ew_pair_kernel(u64 n, F f) {
+__global__ void __launch_bounds__(256, 4) ew_pair_kernel(u64 n, F f) {
   pdl_enter();
   for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) f.both(i);
 }

@@ -403,12 +403,25 @@ __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows
   // unit = 4 K-consecutive values of one row: one 4-byte word in each of the 8 limb planes
   const u64 units = u64(nbatch) * tiles * nkb * nseg * BR * 8;
   constexpr u32 plane = BR * kKB;
+  // Unit order: when the source rows are K-contiguous (left operand, transposed right operand)
+  // the 8 K-quarters of a row are the fastest index, so a warp reads 4 rows x 256 contiguous
+  // bytes and writes whole 16-byte core-matrix rows; otherwise (right operand [K][N]) the row
+  // index is fastest, so a warp reads 32 consecutive N columns of each K.
+  const bool kfast = left || a.tb;
   for (u64 uid = blockIdx.x * u64(blockDim.x) + threadIdx.x; uid < units; uid += u64(gridDim.x) * blockDim.x) {
     u64 t = uid;
-    const u32 r = u32(t % BR);
-    t /= BR;
-    const u32 kq = u32(t % 8);  // 4-value quarter of the 32-value K block
-    t /= 8;
+    u32 r, kq;
+    if (kfast) {
+      kq = u32(t % 8);
+      t /= 8;
+      r = u32(t % BR);
+      t /= BR;
+    } else {
+      r = u32(t % BR);
+      t /= BR;
+      kq = u32(t % 8);  // 4-value quarter of the 32-value K block
+      t /= 8;
+    }
     const u32 g = u32(t % nseg);
     t /= nseg;
     const u32 kb = u32(t % nkb);

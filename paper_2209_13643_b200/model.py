@@ -172,3 +172,148 @@ def demo_input(g: ModelGraph, seed: int) -> np.ndarray:
     """H/engine/model.hpp:417-424."""
     u = _unit(counter_draws(seed, 0x1D07, int(np.prod(g.input))))
     return (2.0 * u - 1.0).reshape(g.input)
+
+
+# ---------------------------------------------------------------- MPCW weights file
+# H/engine/model.hpp:277-364: magic "MPCW", u32 version 1, u32 count, then per entry
+# u32 name length, name, u32 rank, u64 dims, raw little-endian doubles.
+def save_weights(w: dict, path: str) -> None:
+    import struct
+    with open(path, "wb") as f:
+        f.write(b"MPCW")
+        f.write(struct.pack("<II", 1, len(w)))
+        for name in sorted(w):  # std::map order
+            t = np.ascontiguousarray(w[name], dtype="<f8")
+            nb = name.encode()
+            f.write(struct.pack("<I", len(nb)))
+            f.write(nb)
+            f.write(struct.pack("<I", t.ndim))
+            f.write(struct.pack("<%dQ" % t.ndim, *t.shape))
+            f.write(t.tobytes())
+
+
+def load_weights(path: str) -> dict:
+    import struct
+    with open(path, "rb") as f:
+        data = f.read()
+    if data[:4] != b"MPCW":
+        raise ValueError("not a weights file: " + path)
+    off = 4
+    version, count = struct.unpack_from("<II", data, off)
+    off += 8
+    if version != 1:
+        raise ValueError("unsupported weights version")
+    w = {}
+    for _ in range(count):
+        (nl,) = struct.unpack_from("<I", data, off)
+        off += 4
+        name = data[off:off + nl].decode()
+        off += nl
+        (rank,) = struct.unpack_from("<I", data, off)
+        off += 4
+        shape = struct.unpack_from("<%dQ" % rank, data, off)
+        off += 8 * rank
+        n = int(np.prod(shape)) if rank else 1
+        if off + 8 * n > len(data):
+            raise ValueError("weights file truncated")
+        w[name] = np.frombuffer(data, dtype="<f8", count=n, offset=off).reshape(shape).copy()
+        off += 8 * n
+    return w
+
+
+def check_weights(g: ModelGraph, w: dict) -> None:
+    """H/engine/model.hpp:366-376: exactly the declared tensors, with their shapes."""
+    expected = g.weight_shapes()
+    if len(expected) != len(w):
+        raise ValueError("weights entry count mismatch for model " + g.name)
+    for key, shape in expected:
+        if key not in w:
+            raise ValueError("missing weight tensor: " + key)
+        if tuple(w[key].shape) != tuple(shape):
+            raise ValueError("wrong shape for weight tensor: " + key)
+
+
+# ---------------------------------------------------------------- plaintext forward
+# H/engine/reference.hpp:128-200: the double-precision replica the CLI's verify/replica
+# check compares the decoded MPC logits against (+ the extension layers, with the same
+# definitions as the secure ones: GeLU = x sigmoid(1.702 x), LayerNorm eps 1e-5).
+def _im2col(x, k, stride, pad):
+    N, C, H, W = x.shape
+    OH, OW = (H + 2 * pad - k) // stride + 1, (W + 2 * pad - k) // stride + 1
+    xp = np.zeros((N, C, H + 2 * pad, W + 2 * pad), dtype=x.dtype)
+    xp[:, :, pad:pad + H, pad:pad + W] = x
+    cols = np.empty((N, OH, OW, C, k, k), dtype=x.dtype)
+    for ki in range(k):
+        for kj in range(k):
+            cols[:, :, :, :, ki, kj] = xp[:, :, ki:ki + stride * (OH - 1) + 1:stride,
+                                          kj:kj + stride * (OW - 1) + 1:stride].transpose(0, 2, 3, 1)
+    return cols.reshape(N * OH * OW, C * k * k)
+
+
+def plaintext_forward(g: ModelGraph, w: dict, x: np.ndarray) -> np.ndarray:
+    shapes = g.shapes()
+    src, oth = g.wiring()
+    x0 = np.asarray(x, dtype=np.float64)
+    outs = []
+    for i, l in enumerate(g.layers):
+        cur = x0 if src[i] < 0 else outs[src[i]]
+        shape = g.input if src[i] < 0 else shapes[src[i]]
+        if l.type == "add":
+            cur = cur + (x0 if oth[i] < 0 else outs[oth[i]])
+        elif l.type == "dense":
+            cur = cur.reshape(-1, shape[-1]) @ w[l.name + ".W"]
+            if l.bias:
+                cur = cur + w[l.name + ".b"]
+        elif l.type == "conv2d":
+            y = _im2col(cur.reshape(shape), l.kernel, l.stride, l.pad) @ w[l.name + ".W"]
+            if l.bias:
+                y = y + w[l.name + ".b"]
+            N, _, OH, OW = shapes[i]
+            cur = y.reshape(N, OH, OW, l.out).transpose(0, 3, 1, 2)
+        elif l.type == "relu":
+            cur = np.maximum(cur, 0.0)
+        elif l.type == "maxpool2d":
+            N, C, H, W = shape
+            v = cur.reshape(shape)
+            OH, OW = (H - l.kernel) // l.stride + 1, (W - l.kernel) // l.stride + 1
+            m = np.full((N, C, OH, OW), -np.inf)
+            for ki in range(l.kernel):
+                for kj in range(l.kernel):
+                    m = np.maximum(m, v[:, :, ki:ki + l.stride * (OH - 1) + 1:l.stride,
+                                        kj:kj + l.stride * (OW - 1) + 1:l.stride])
+            cur = m
+        elif l.type in ("softmax",):
+            v = cur.reshape(-1, shape[-1])
+            e = np.exp(v - v.max(axis=1, keepdims=True))
+            cur = e / e.sum(axis=1, keepdims=True)
+        elif l.type == "mean_pool":
+            cur = cur.reshape(shape).mean(axis=1)
+        elif l.type == "global_avg_pool":
+            cur = cur.reshape(shape).mean(axis=(2, 3))
+        elif l.type == "gelu":
+            cur = cur / (1.0 + np.exp(-1.702 * cur))
+        elif l.type == "layernorm":
+            v = cur.reshape(-1, shape[-1])
+            mu = v.mean(axis=1, keepdims=True)
+            var = ((v - mu) ** 2).mean(axis=1, keepdims=True)
+            cur = (v - mu) / np.sqrt(var + 1e-5) * w[l.name + ".gamma"] + w[l.name + ".beta"]
+        elif l.type == "attention":
+            B, T, d = shape
+            H = l.heads
+            dh = d // H
+            qkv = cur.reshape(B * T, d) @ w[l.name + ".Wqkv"]
+            if l.bias:
+                qkv = qkv + w[l.name + ".bqkv"]
+            q, k, v = (qkv.reshape(B, T, 3, H, dh)[:, :, j].transpose(0, 2, 1, 3) for j in range(3))
+            s = np.matmul(q, np.swapaxes(k, -1, -2)) / np.sqrt(dh)
+            e = np.exp(s - s.max(axis=-1, keepdims=True))
+            o = np.matmul(e / e.sum(axis=-1, keepdims=True), v)
+            o = o.transpose(0, 2, 1, 3).reshape(B * T, d) @ w[l.name + ".Wo"]
+            if l.bias:
+                o = o + w[l.name + ".bo"]
+            cur = o
+        elif l.type == "flatten":
+            pass
+        cur = cur.reshape(shapes[i])
+        outs.append(cur)
+    return outs[-1]
