@@ -155,14 +155,16 @@ void launch_simt(Session& s, GemmArgs a) {
 // exactly once per (k, n) for ALL segments of a slot — party 0's three segments share one
 // B / r_B draw and one F load — while the few L rows of a K-chunk are staged in shared
 // memory. Bound by reading F (2 x 8 B per (k, n) per party) and the dealer draws.
-constexpr int kGvM = 16;    // max rows
+constexpr int kGvM = 16;    // rows per block (row groups above that)
+constexpr int kGvMax = 64;  // the small-M path takes M <= kGvMax
 constexpr int kGvKC = 64;   // K chunk staged in smem
 
 template <int MR>
 __global__ void __launch_bounds__(256) ring_gemv(GemmArgs a) {
   __shared__ u64 Ls[3][MR][kGvKC];
   pdl_enter();
-  const int slot = blockIdx.z;
+  const int slot = int(blockIdx.z % a.nslots);
+  const u32 m0 = (blockIdx.z / a.nslots) * MR;  // row group (M > MR: the R stream is re-read per group)
   const GemmSlotArgs& S = a.sl[slot];
   const u32 M = a.M, N = a.N, K = a.K;
   const u32 n = blockIdx.x * 256 + threadIdx.x;
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(256) ring_gemv(GemmArgs a) {
     __syncthreads();
     for (u32 e = threadIdx.x; e < u32(S.nseg) * MR * kGvKC; e += 256) {
       const u32 kk = e % kGvKC, m = (e / kGvKC) % MR, g = e / (kGvKC * MR);
-      Ls[g][m][kk] = (m < M && kk < kc) ? load_l(S, int(g), u64(m) * K + k0 + kk) : 0;
+      Ls[g][m][kk] = (m0 + m < M && kk < kc) ? load_l(S, int(g), u64(m0 + m) * K + k0 + kk) : 0;
     }
     __syncthreads();
     if (n >= N) continue;
@@ -218,15 +220,16 @@ __global__ void __launch_bounds__(256) ring_gemv(GemmArgs a) {
   const u64 per = u64(M) * N;
 #pragma unroll
   for (int m = 0; m < MR; ++m)
-    if (u32(m) < M) a.acc[slot][u64(blockIdx.y) * per + u64(m) * N + n] = acc[m];
+    if (m0 + u32(m) < M) a.acc[slot][u64(blockIdx.y) * per + u64(m0 + m) * N + n] = acc[m];
 }
 
 template <int MR>
 void launch_gemv(Session& s, GemmArgs a) {
   cudaStream_t st = s.stream;
   const u32 nblk = (a.N + 255) / 256;
+  const u32 mgrp = (a.M + MR - 1) / MR;
   // split K until ~3 waves of 256-thread CTAs (8 resident per SM), chunks of >= 4 smem stages
-  u32 split = u32((3 * 8 * u64(kSms) / a.nslots + nblk - 1) / nblk);
+  u32 split = u32((3 * 8 * u64(kSms) / (a.nslots * mgrp) + nblk - 1) / nblk);
   const u32 maxsplit = (a.K + 4 * kGvKC - 1) / (4 * kGvKC);
   split = split > maxsplit ? maxsplit : (split < 1 ? 1 : split);
   a.kchunk = (a.K + split - 1) / split;
@@ -236,7 +239,7 @@ void launch_gemv(Session& s, GemmArgs a) {
   for (int i = 0; i < a.nslots; ++i) a.acc[i] = ws->ptr + i * per * a.ksplit;
   cudaEvent_t pe;
   probe_begin(st, &pe);
-  launch_pdl(ring_gemv<MR>, dim3(nblk, a.ksplit, a.nslots), dim3(256), 0, st, a);
+  launch_pdl(ring_gemv<MR>, dim3(nblk, a.ksplit, a.nslots * mgrp), dim3(256), 0, st, a);
   launch_pdl(gemm_splitk_epilogue, dim3(ew_blocks(per * a.nslots)), dim3(256), 0, st, a);
   probe_end(st, pe);
 }
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(256) ring_gemm_rows(GemmArgs a) {
 static bool rows_eligible(const GemmArgs& a) { return a.N <= u32(kRowN) && a.M >= 1024 && a.nbatch == 1 && !a.tb; }
 
 bool gemv_eligible_shape(u32 M, u32 nbatch, bool tb, int col2im) {
-  return M <= u32(kGvM) && nbatch == 1 && !tb && !col2im;
+  return M <= u32(kGvMax) && nbatch == 1 && !tb && !col2im;
 }
 static bool gemv_eligible(const GemmArgs& a) { return gemv_eligible_shape(a.M, a.nbatch, a.tb, a.col2im); }
 
