@@ -156,7 +156,7 @@ void launch_simt(Session& s, GemmArgs a) {
 // B / r_B draw and one F load — while the few L rows of a K-chunk are staged in shared
 // memory. Bound by reading F (2 x 8 B per (k, n) per party) and the dealer draws.
 constexpr int kGvM = 16;    // rows per block (row groups above that)
-constexpr int kGvMax = 64;  // the small-M path takes M <= kGvMax
+constexpr int kGvMax = 16;  // the small-M path takes M <= kGvMax (M=64 x N=120 measured 6x slower than SIMT)
 constexpr int kGvKC = 64;   // K chunk staged in smem
 
 template <int MR>

@@ -31,7 +31,6 @@ constexpr int kKB = 32;        // K values (= limb bytes) per stage: one UMMA K 
 constexpr int kStages = 4;
 constexpr int kProdWarps = 16;                 // L producers (and epilogue): warps 0-15
 constexpr int kVW = 8;                         // K values per producer unit (= 8-byte limb row segment)
-constexpr u32 kL2Ahead = 3;                    // K blocks of L2 prefetch ahead of the register loads
 constexpr int kLoadWarp = kProdWarps;          // bulk loader
 constexpr int kMmaWarp = kProdWarps + 1;       // MMA issuer, TMEM owner
 constexpr int kThreads = (kProdWarps + 2) * 32;
@@ -159,6 +158,7 @@ struct Tc2Args {
   u32 nkb = 0;                              // K blocks of 32
   int vec = 0;                              // L rows 16-byte aligned (vector loads)
   u32 ksplit = 1, kbper = 0;                // split-K over K blocks (partials summed by the epilogue kernel)
+  u32 l2ahead = 3;                          // K blocks of L2 prefetch ahead of the register loads (0 = off)
 };
 
 namespace {
@@ -252,8 +252,8 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
         }
         // deeper, register-free prefetch: pull block kb+kL2Ahead into L2 so that the register
         // load issued one block ahead finds it there (HBM latency > one block of producer work)
-        const u32 kp = (kb + kL2Ahead) * kKB + u32(q) * kVW;
-        if (rowok && kb + kL2Ahead < kb1 && kp < K) {
+        const u32 kp = (kb + P.l2ahead) * kKB + u32(q) * kVW;
+        if (P.l2ahead && rowok && kb + P.l2ahead < kb1 && kp < K) {
           asm volatile("prefetch.global.L2 [%0];" ::"l"(S.L[pf] + rowoff + kp));
           if (sum) asm volatile("prefetch.global.L2 [%0];" ::"l"(S.L2[pf] + rowoff + kp));
         }
@@ -480,6 +480,11 @@ void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
   Tc2Args P{};
   P.g = a;
   P.nkb = (a.K + kKB - 1) / kKB;
+  static const u32 l2ahead = [] {
+    const char* e = std::getenv("MPCG_TC2_L2AHEAD");
+    return e ? u32(std::atoi(e)) : 3u;
+  }();
+  P.l2ahead = l2ahead;
   const u32 ntiles = (a.N + BN - 1) / BN, mtiles = (a.M + kM - 1) / kM;
   // right operand: batched only when some segment's R has a batch stride
   bool rbatched = false;
