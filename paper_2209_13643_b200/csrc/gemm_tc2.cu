@@ -92,6 +92,40 @@ __device__ __forceinline__ u32 gather4(u32 a, u32 b, u32 c, u32 d, u32 l) {
 }
 
 
+__device__ __forceinline__ void draws16(u64 key, u64 c0, u64 (&v)[16]) {
+  u64 z = key + c0 * kPhi;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    v[i] = mix64(z);
+    z += kPhi;
+  }
+}
+__device__ __forceinline__ void load16(const u64* p, u64 (&v)[16]) {
+  const uint4* p4 = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint4 w = __ldg(p4 + i);
+    v[2 * i] = (u64(w.y) << 32) | w.x;
+    v[2 * i + 1] = (u64(w.w) << 32) | w.z;
+  }
+}
+// 16 K-consecutive u64 -> one 16-byte row in each of the 8 limb planes.
+__device__ __forceinline__ void transpose16_store(const u64 (&v)[16], char* base, u32 plane, u32 off) {
+#pragma unroll
+  for (int l = 0; l < 8; ++l) {
+    const int sh = (l & 3), hi = l >> 2;
+    u32 w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = hi ? u32(v[i] >> 32) : u32(v[i]);
+    uint4 o;
+    o.x = gather4(w[0], w[1], w[2], w[3], sh);
+    o.y = gather4(w[4], w[5], w[6], w[7], sh);
+    o.z = gather4(w[8], w[9], w[10], w[11], sh);
+    o.w = gather4(w[12], w[13], w[14], w[15], sh);
+    *reinterpret_cast<uint4*>(base + l * plane + off) = o;
+  }
+}
+
 // kVW dealer draws c0, c0+1, ... of one stream (key + c*phi advances by phi).
 __device__ __forceinline__ void draws_vec(u64 key, u64 c0, u64 (&v)[kVW]) {
   u64 z = key + c0 * kPhi;
@@ -163,7 +197,7 @@ struct Tc2Args {
 
 namespace {
 
-template <int BN>
+template <int BN, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_constant__ Tc2Args P) {
   constexpr u32 kA = kM * kKB;  // bytes per A limb plane per stage
   constexpr u32 kB = BN * kKB;  // bytes per B limb plane per stage
@@ -193,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
 
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) {
-      mbar_init(&full[i], packedL ? 1 : kProdWarps + 1);
+      mbar_init(&full[i], packedL ? 1 : (SPLIT ? kProdWarps / 2 : kProdWarps) + 1);
       mbar_init(&empty[i], 1);
     }
     mbar_init(&done, 1);
@@ -210,7 +244,104 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const u32 tmem = tmem_slot;
 
-  if (warp < kProdWarps) {
+  if (SPLIT && warp < kProdWarps && !packedL) {
+    // ---- split producers: warps 0-7 own the generated segments (dealer draws), warps 8-15
+    // the memory segments (opened E); each unit is 16 K-consecutive values of one row, so a
+    // stage is written by one group of 8 warps and the E loads of block kb+1 stay in flight
+    // while the other group generates — the E group has nothing else to wait on.
+    const int gt = tid & 255;             // thread within the group
+    const bool egroup = warp >= kProdWarps / 2;
+    const int r = gt & (kM - 1), hf = gt >> 7;
+    const u32 m = m0 + u32(r);
+    const bool rowok = m < M;
+    const u64 rowoff = u64(b) * S.sL[0] + u64(m) * K;
+    const u64 key = tkey(S.mm.key, S.mm.kp);
+    const u64 iA = 1 + S.mm.offA + S.aoff;
+    const u64 iRA = 1 + S.mm.na + S.mm.nb + S.mm.offA + S.aoff;
+    const u32 off = (u32(hf) * (kM / 8) + u32(r) / 8) * 128 + (u32(r) % 8) * 16;
+    u64 pr[16], pr2[16];
+    // issue the loads of memory segment g for K block kb into pr/pr2 (E = own + peer)
+    auto fetch = [&](int g, u32 kb) {
+      const u32 k0 = kb * kKB + u32(hf) * 16;
+      const bool sum = S.lk[g] == kOpSum;
+      if (!rowok || k0 >= K) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pr[i] = pr2[i] = 0;
+      } else if (k0 + 16 <= K && P.vec) {
+        load16(S.L[g] + rowoff + k0, pr);
+        if (sum) load16(S.L2[g] + rowoff + k0, pr2);
+        else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pr2[i] = 0;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const bool in = k0 + i < K;
+          pr[i] = in ? __ldg(S.L[g] + rowoff + k0 + i) : 0;
+          pr2[i] = (in && sum) ? __ldg(S.L2[g] + rowoff + k0 + i) : 0;
+        }
+      }
+    };
+    // the memory segments this group serves, in stage order
+    auto is_mem = [&](int g) { return S.lk[g] == kOpMem || S.lk[g] == kOpSum; };
+    int firstmem = -1;
+    for (int g = 0; g < nseg && firstmem < 0; ++g)
+      if (is_mem(g)) firstmem = g;
+    auto publish = [&](const u64 (&v)[16], u32 it) {
+      const int stg = int(it % kStages);
+      if (it >= kStages) mbar_wait(&empty[stg], ((it / kStages) & 1) ^ 1);
+      transpose16_store(v, smem + stg * kStage, kA, off);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[stg]);
+    };
+    if (egroup) {  // memory segments: loads of the next one in flight while this one is published
+      if (firstmem >= 0) fetch(firstmem, kb0);
+      u32 it = 0;
+      for (u32 kb = kb0; kb < kb1; ++kb)
+        for (int g = 0; g < nseg; ++g, ++it) {
+          if (!is_mem(g)) continue;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pr[i] += pr2[i];  // in place: E = own + peer
+          publish(pr, it);
+          int ng = -1;
+          for (int h = g + 1; h < nseg && ng < 0; ++h)
+            if (is_mem(h)) ng = h;
+          if (ng >= 0) fetch(ng, kb);
+          else if (kb + 1 < kb1) fetch(firstmem, kb + 1);
+        }
+    } else {  // generated segments: the dealer's A / r_A draws
+      u32 it = 0;
+      for (u32 kb = kb0; kb < kb1; ++kb) {
+        const u32 k0 = kb * kKB + u32(hf) * 16;
+        for (int g = 0; g < nseg; ++g, ++it) {
+          if (is_mem(g)) continue;
+          const int kind = S.lk[g];
+          const u64 e0 = rowoff + k0;
+          u64 v[16];
+          if (!rowok || k0 >= K) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = 0;
+          } else {
+            draws16(key, (kind == kOpRA ? iRA : iA) + e0, v);
+            if (kind == kOpA0) {
+              u64 w[16];
+              draws16(key, iRA + e0, w);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] -= w[i];
+            }
+            if (k0 + 16 > K) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (k0 + i >= K) v[i] = 0;
+            }
+          }
+          publish(v, it);
+        }
+      }
+    }
+  } else if (warp < kProdWarps) {
     if (!packedL) {
       // ---- L producers: unit = (row r, quarter q) = 8 K-consecutive values of one row per
       // stage; each becomes one 8-byte row segment in every limb plane.
@@ -474,7 +605,8 @@ void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
   const size_t smem = kStages * kStage;
   static bool attr = false;
   if (!attr) {
-    MPCG_CUDA(cudaFuncSetAttribute(ring_gemm_tc2<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    MPCG_CUDA(cudaFuncSetAttribute(ring_gemm_tc2<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    MPCG_CUDA(cudaFuncSetAttribute(ring_gemm_tc2<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr = true;
   }
   Tc2Args P{};
@@ -545,7 +677,14 @@ void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
   dim3 grid(ntiles * a.nslots, mtiles, a.nbatch * P.ksplit);
   cudaEvent_t pe;
   probe_begin(s.stream, &pe);
-  launch_pdl(ring_gemm_tc2<BN>, grid, dim3(kThreads), smem, s.stream, P);
+  static const bool split_groups = [] {
+    const char* e = std::getenv("MPCG_TC2_SPLIT");
+    return e && e[0] == '1';
+  }();
+  if (split_groups)
+    launch_pdl(ring_gemm_tc2<BN, true>, grid, dim3(kThreads), smem, s.stream, P);
+  else
+    launch_pdl(ring_gemm_tc2<BN, false>, grid, dim3(kThreads), smem, s.stream, P);
   probe_end(s.stream, pe);
   if (P.ksplit > 1) {
     ClassScope ep_scope(kClsOther, 0);
