@@ -67,6 +67,11 @@ class Session:
     def set_shard(self, local_batch, global_batch, batch_offset):
         N.call("mpcg_session_set_shard", self._h, local_batch, global_batch, batch_offset)
 
+    def connect_loopback(self, peer: "Session"):
+        """Link this single-party session with `peer` (the other party) on the same GPU: the
+        2-GPU code path with device copies instead of NCCL (each party on its own thread)."""
+        N.call("mpcg_session_connect_loopback", self._h, peer._h)
+
     def connect_nccl(self, unique_id: bytes, rank: int):
         N.call("mpcg_session_connect_nccl", self._h, unique_id, rank)
 

@@ -452,6 +452,19 @@ int mpcg_executor_destroy(mpcg_executor* e) {
   return guard([&] { delete e; });
 }
 
+int mpcg_session_connect_loopback(mpcg_session* a, mpcg_session* b) {
+  return guard([&] {
+    Session& x = S(a);
+    Session& y = S(b);
+    if (x.n_local != 1 || y.n_local != 1) throw Error(kUsageError, "loopback link needs two single-party sessions");
+    if (x.party_of[0] == y.party_of[0]) throw Error(kUsageError, "loopback link needs party 0 and party 1");
+    if (x.device != y.device) throw Error(kUsageError, "loopback link: sessions on different devices (use NCCL)");
+    auto link = std::make_shared<LoopLink>();
+    x.loop = link;
+    y.loop = link;
+  });
+}
+
 int mpcg_set_tc2(int on) {
   return guard([&] { tc2_mode() = on ? 1 : 0; });
 }

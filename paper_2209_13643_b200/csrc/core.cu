@@ -491,7 +491,30 @@ void Session::post(Open& o, const std::string& tag, bool p2p) {
   MPCG_CUDA(cudaEventRecord(built, stream));
   MPCG_CUDA(cudaStreamWaitEvent(comm_stream, built, 0));
   if (cap.active) cap.comm_used = true;
-  if (n_local == 1) {
+  if (n_local == 1 && loop) {
+    if (cap.active) throw Error(kUsageError, "loopback link: graph capture is not supported");
+    const int me = party_of[0];
+    std::unique_lock<std::mutex> lk(loop->mu);
+    LoopLink::Slot& sl = loop->slots[u64(o.seq)];
+    sl.own[me] = o.own(0);
+    sl.in[me] = o.in->ptr;
+    sl.built[me] = built;
+    if (sl.arrived == 1 && sl.n != o.n) throw Error(kProtocolError, "loopback link: collective size mismatch");
+    sl.n = o.n;
+    if (++sl.arrived == 2) {
+      MPCG_CUDA(cudaStreamWaitEvent(comm_stream, sl.built[1 - me], 0));
+      MPCG_CUDA(cudaMemcpyAsync(sl.in[me], sl.own[1 - me], o.n * sizeof(u64), cudaMemcpyDeviceToDevice, comm_stream));
+      MPCG_CUDA(cudaMemcpyAsync(sl.in[1 - me], sl.own[me], o.n * sizeof(u64), cudaMemcpyDeviceToDevice, comm_stream));
+      sl.done = pool_event();
+      MPCG_CUDA(cudaEventRecord(sl.done, comm_stream));
+      sl.completed = true;
+      loop->cv.notify_all();
+    } else {
+      loop->cv.wait(lk, [&] { return sl.completed; });
+      MPCG_CUDA(cudaStreamWaitEvent(comm_stream, sl.done, 0));
+      loop->slots.erase(u64(o.seq));
+    }
+  } else if (n_local == 1) {
     if (!nccl) throw Error(kTransportError, "single-party session has no peer link (connect NCCL first)");
     const int peer = 1 - party_of[0];
     auto& api = nccl_api();

@@ -12,8 +12,10 @@
 // one thread per party instead; the values and the collective order are identical).
 #pragma once
 
+#include <condition_variable>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -138,6 +140,25 @@ struct SessionConfig {
 
 constexpr size_t kFlushBytes = size_t(256) << 20;  // > 126 MB L2
 
+// In-process link between two single-party sessions on one GPU (party 0 and party 1 driven
+// by two host threads): the same one-party-per-session code path a 2-GPU pair runs, with the
+// NCCL send/recv replaced by device copies, so it can be exercised on one device. The second
+// party to post a collective enqueues both directions on its comm stream; both wait on it.
+struct LoopLink {
+  struct Slot {
+    const u64* own[2] = {nullptr, nullptr};
+    u64* in[2] = {nullptr, nullptr};
+    cudaEvent_t built[2] = {nullptr, nullptr};
+    cudaEvent_t done = nullptr;
+    size_t n = 0;
+    int arrived = 0;
+    bool completed = false;
+  };
+  std::mutex mu;
+  std::condition_variable cv;
+  std::map<u64, Slot> slots;
+};
+
 class Session {
  public:
   Session(int device, int n_local, int party, u64 seed, u64 mask_seed, int frac_bits);
@@ -151,6 +172,7 @@ class Session {
   cudaStream_t stream = nullptr;       // compute stream (all local slots)
   cudaStream_t comm_stream = nullptr;  // link emulation / NCCL
   ncclComm_t nccl = nullptr;
+  std::shared_ptr<LoopLink> loop;      // in-process peer (tests of the one-party path on one GPU)
 
   // data-parallel shard (batch-leading tensors): local rows are a slice of the global batch
   u64 shard_local = 1, shard_global = 1, shard_offset = 0;
