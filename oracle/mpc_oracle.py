@@ -601,15 +601,23 @@ def scale_rescale(X, c, f):
     return truncate_shares([x * k for x in X], f)
 
 
-RECIP_UNIT_ITERS = 3
+def recip_unit_iters(f: int) -> int:
+    """Newton steps for 1/d on [1, 2] from the 1/17-accurate linear seed: the relative error
+    after k steps is (1/17)^(2^k), below 2^-f once 2^k * log2(17) > f (f=16: 2, f=20: 3)."""
+    k = 1
+    while (2 ** k) * math.log2(17.0) <= f:
+        k += 1
+    return k
 
 
-def recip_unit_shares(D, ctx: Ctx, tag="recip", iters=RECIP_UNIT_ITERS):
+def recip_unit_shares(D, ctx: Ctx, tag="recip", iters=None):
     """1/d for d in [1, 2]: linear seed y0 = 24/17 - 8/17 d (relative error <= 1/17), then the
     reference's Newton step y <- trunc(y (2 - trunc(d y))) (H/nonlinear/approx.hpp:52-60);
-    three steps take the error below 2^-30, so the reference's exp seed and ten steps are not
-    needed on this interval."""
+    recip_unit_iters(f) steps take the error below the fixed-point resolution, so the
+    reference's exp seed and ten steps are not needed on this interval."""
     f = ctx.frac_bits
+    if iters is None:
+        iters = recip_unit_iters(f)
     ch = ctx.chunks_for(D[0].size)
     y = add_public([U64(0) - v for v in scale_rescale(D, 8.0 / 17.0, f)], int(encode_fixed(24.0 / 17.0, f)))
     for i in range(iters):

@@ -307,7 +307,7 @@ DT open_value(Session& s, const DT& x, Reduce kind, const std::string& tag);  //
 // restated in oracle/mpc_oracle.py, parity unpinned by the reference).
 constexpr double kLnEps = 1e-5;
 constexpr int kIsqrtIters = 3;
-constexpr int kRecipUnitIters = 3;  // 1/d on [1, 2] from a linear seed (sigmoid)
+int recip_unit_iters(int frac_bits);  // Newton steps for 1/d on [1, 2] from a linear seed (sigmoid)
 DT sigmoid_shares(Session& s, const DT& x, const std::string& tag = "sigmoid");
 DT gelu_shares(Session& s, const DT& x, const std::string& tag = "gelu");
 DT inv_sqrt_shares(Session& s, const DT& v, const std::string& tag = "isqrt", int newton_iters = kIsqrtIters);

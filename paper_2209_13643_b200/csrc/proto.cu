@@ -1,6 +1,8 @@
 // Secure protocols on device shares: Beaver mul/square/AND, SPK adder, conversions,
 // comparison-based activations and the exp/reciprocal/softmax chain.
 // Reference: H/protocols/{beaver,adder,compare,trunc}.hpp, H/nonlinear/{approx,activations}.hpp.
+#include <cmath>
+
 #include "ew.cuh"
 
 namespace mpcg {
@@ -724,6 +726,14 @@ struct RecipPV {
 };
 }  // namespace
 
+// Newton steps for 1/d on [1, 2] from the 1/17-accurate linear seed: error (1/17)^(2^k) drops
+// below 2^-f once 2^k log2(17) > f (oracle recip_unit_iters).
+int recip_unit_iters(int f) {
+  int k = 1;
+  while (double(1 << k) * std::log2(17.0) <= double(f)) ++k;
+  return k;
+}
+
 // Newton steps y <- trunc(y (2 - trunc(x y))) on y in place (approx.hpp:52-60), one fused chain.
 static void recip_newton(Session& s, const DT& x, DT& y, const std::string& tag, int newton_iters) {
   const int f = s.cfg.frac_bits;
@@ -856,7 +866,7 @@ DT sigmoid_shares(Session& s, const DT& x, const std::string& tag) {
   DT d = s.alloc(x.shape, x.scale), r = s.alloc(x.shape, x.scale);
   exp_chain(s, x.shape, tag + ".exp", 7, SrcMem{cptrs(nabs)},
             OutRecipSeed{ptrs(d), ptrs(r), u64(1) << f, encode_fixed(8.0 / 17.0, f), encode_fixed(24.0 / 17.0, f), f});
-  recip_newton(s, d, r, tag + ".recip", kRecipUnitIters);
+  recip_newton(s, d, r, tag + ".recip", recip_unit_iters(f));
   Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Arith, x.shape), tag + ".sel");
   t.mark_consumed();
   DT out = s.alloc(x.shape, x.scale);
