@@ -161,13 +161,18 @@ constexpr int kGvKC = 64;   // K chunk staged in smem
 
 template <int MR>
 __global__ void __launch_bounds__(256) ring_gemv(GemmArgs a) {
+  // block = 32 columns x 8 warps: lane = column (coalesced R reads), warp = K slice of every
+  // staged chunk; the 8 warp partials are summed in shared memory at the end.
   __shared__ u64 Ls[3][MR][kGvKC];
+  constexpr int kRG = MR < 4 ? MR : 4;  // rows reduced per pass
+  __shared__ u64 red[8][kRG][32];
   pdl_enter();
   const int slot = int(blockIdx.z % a.nslots);
   const u32 m0 = (blockIdx.z / a.nslots) * MR;  // row group (M > MR: the R stream is re-read per group)
   const GemmSlotArgs& S = a.sl[slot];
   const u32 M = a.M, N = a.N, K = a.K;
-  const u32 n = blockIdx.x * 256 + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u32 n = blockIdx.x * 32 + lane;
   const u32 kb = blockIdx.y * a.kchunk, ke = min(K, kb + a.kchunk);
   bool needB = false, needRB = false, needF = false;
   for (int g = 0; g < S.nseg; ++g) {
@@ -193,7 +198,7 @@ __global__ void __launch_bounds__(256) ring_gemv(GemmArgs a) {
     }
     __syncthreads();
     if (n >= N) continue;
-    for (u32 kk = 0; kk < kc; ++kk) {
+    for (u32 kk = u32(warp); kk < kc; kk += 8) {
       const u64 idx = u64(k0 + kk) * N + n;
       const u64 B = needB ? mm_B(S.mm, S.boff + idx) : 0;
       const u64 rB = needRB ? mm_rB(S.mm, S.boff + idx) : 0;
@@ -216,30 +221,43 @@ __global__ void __launch_bounds__(256) ring_gemv(GemmArgs a) {
       }
     }
   }
-  if (n >= N) return;
   const u64 per = u64(M) * N;
 #pragma unroll
-  for (int m = 0; m < MR; ++m)
-    if (m0 + u32(m) < M) a.acc[slot][u64(blockIdx.y) * per + u64(m0 + m) * N + n] = acc[m];
+  for (int mb = 0; mb < MR; mb += kRG) {
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kRG; ++j) red[warp][j][lane] = acc[mb + j];
+    __syncthreads();
+    if (warp == 0 && n < N) {
+#pragma unroll
+      for (int j = 0; j < kRG; ++j) {
+        u64 v = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v += red[w][j][lane];
+        if (m0 + u32(mb + j) < M) a.acc[slot][u64(blockIdx.y) * per + u64(m0 + mb + j) * N + n] = v;
+      }
+    }
+  }
 }
 
 template <int MR>
 void launch_gemv(Session& s, GemmArgs a) {
   cudaStream_t st = s.stream;
-  const u32 nblk = (a.N + 255) / 256;
+  const u32 ncol = (a.N + 31) / 32;
   const u32 mgrp = (a.M + MR - 1) / MR;
-  // split K until ~3 waves of 256-thread CTAs (8 resident per SM), chunks of >= 4 smem stages
-  u32 split = u32((3 * 8 * u64(kSms) / (a.nslots * mgrp) + nblk - 1) / nblk);
-  const u32 maxsplit = (a.K + 4 * kGvKC - 1) / (4 * kGvKC);
+  // split K until ~3 blocks per SM, >= one staged chunk per split
+  const u64 base = u64(ncol) * a.nslots * mgrp;
+  u32 split = u32((3 * u64(kSms) + base - 1) / base);
+  const u32 maxsplit = (a.K + kGvKC - 1) / kGvKC;
   split = split > maxsplit ? maxsplit : (split < 1 ? 1 : split);
-  a.kchunk = (a.K + split - 1) / split;
+  a.kchunk = ((a.K + split - 1) / split + kGvKC - 1) / kGvKC * kGvKC;
   a.ksplit = (a.K + a.kchunk - 1) / a.kchunk;
   const u64 per = u64(a.M) * a.N;
   std::shared_ptr<Block> ws = s.raw(per * a.ksplit * a.nslots);
   for (int i = 0; i < a.nslots; ++i) a.acc[i] = ws->ptr + i * per * a.ksplit;
   cudaEvent_t pe;
   probe_begin(st, &pe);
-  launch_pdl(ring_gemv<MR>, dim3(nblk, a.ksplit, a.nslots * mgrp), dim3(256), 0, st, a);
+  launch_pdl(ring_gemv<MR>, dim3(ncol, a.ksplit, a.nslots * mgrp), dim3(256), 0, st, a);
   launch_pdl(gemm_splitk_epilogue, dim3(ew_blocks(per * a.nslots)), dim3(256), 0, st, a);
   probe_end(st, pe);
 }
