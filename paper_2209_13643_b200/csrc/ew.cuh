@@ -272,6 +272,11 @@ struct SqChainStep {
   }
 };
 
+// Small chains in 1-GPU mode run as ONE cooperative kernel (grid barriers instead of kernel
+// boundaries, as the compare chains do); defined after grid_barrier below.
+template <class B0, class ST>
+void persistent_beaver_chain(Session& s, u64 n, const B0& build, const std::vector<ST>& steps);
+
 // Rounds tr[0..R) of squares: round 0 squares x0(slot, g); round r squares the value
 // yf_for(r-1) produced from round r-1's product; yf_for(R-1) sees the chain's last product.
 template <class XF, class YFF>
@@ -281,6 +286,20 @@ void square_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& t
   const int R = int(tr.size());
   const Pid2 pid = pids(s);
   auto ctag = [&](int r, int k) { return chunks == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
+  using YF0 = decltype(yf_for(0));
+  if (chunks == 1 && R <= 24 && n > 0 && s.persistent_ok(n)) {
+    std::vector<Open> op(static_cast<size_t>(R));
+    for (int r = 0; r < R; ++r) op[r] = s.begin_open(n, Reduce::Sum);
+    std::vector<SqChainStep<YF0>> st;
+    for (int r = 1; r <= R; ++r)
+      st.push_back(SqChainStep<YF0>{tr[r - 1].ew, r < R ? tr[r].ew : tr[r - 1].ew, pid, as_const(own_ptrs(op[r - 1])),
+                                    peer_ptrs(op[r - 1]), r < R ? own_ptrs(op[r]) : Ptr2{{nullptr, nullptr}}, 0,
+                                    r == R ? 1 : 0, yf_for(r - 1)});
+    persistent_beaver_chain(s, n, SqBuild2<XF>{tr[0].ew, pid, own_ptrs(op[0]), 0, x0}, st);
+    for (int r = 0; r < R; ++r) s.account(n, Reduce::Sum, tags[r]);  // the reference's collective order
+    s.check();
+    return;
+  }
   std::vector<Open> hs(static_cast<size_t>(chunks));
   // R squares x 32 B/elem/party spread over the R+1 fused launches of a lane
   ClassScope cs(kClsBeaver, 32.0 * R / (R + 1) * double(n / chunks) * s.n_local);
@@ -361,6 +380,21 @@ void mul_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, 
   const int R = int(tr.size());
   const Pid2 pid = pids(s);
   auto ctag = [&](int r, int k) { return chunks == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
+  using PV0 = decltype(pv_for(0));
+  if (chunks == 1 && R <= 24 && n > 0 && s.persistent_ok(n)) {
+    std::vector<Open> op(static_cast<size_t>(R));
+    for (int r = 0; r < R; ++r) op[r] = s.begin_open(2 * n, Reduce::Sum);
+    std::vector<MulChainStep<PV0>> st;
+    for (int r = 1; r <= R; ++r)
+      st.push_back(MulChainStep<PV0>{tr[r - 1].ew, r < R ? tr[r].ew : tr[r - 1].ew, pid,
+                                     as_const(own_ptrs(op[r - 1])), peer_ptrs(op[r - 1]),
+                                     r < R ? own_ptrs(op[r]) : Ptr2{{nullptr, nullptr}}, 0, n, r == R ? 1 : 0,
+                                     pv_for(r - 1)});
+    persistent_beaver_chain(s, n, MulBuild<XF, YF>{tr[0].ew, pid, own_ptrs(op[0]), 0, n, x0, y0}, st);
+    for (int r = 0; r < R; ++r) s.account(2 * n, Reduce::Sum, tags[r]);
+    s.check();
+    return;
+  }
   std::vector<Open> hs(static_cast<size_t>(chunks));
   // R multiplies x 56 B/elem/party spread over the R+1 fused launches of a lane
   ClassScope cs(kClsBeaver, 56.0 * R / (R + 1) * double(n / chunks) * s.n_local);
@@ -697,6 +731,68 @@ __global__ void __launch_bounds__(256) chain_kernel(const __grid_constant__ Chai
   for (u64 g = t0; g < p.n; g += st) eval_slots(p.b2a, pr, slot, g);
   grid_barrier(p.bar, ++ep * nb);
   for (u64 g = t0; g < p.n; g += st) eval_slots(p.fin, pr, slot, g);
+}
+
+constexpr int kMaxChainSteps = 24;
+template <class B0, class ST>
+struct BeaverChainParams {
+  B0 build;
+  ST steps[kMaxChainSteps];
+  int nsteps;
+  u64 n;
+  unsigned* bar;
+  int pair;
+};
+
+template <class B0, class ST>
+__global__ void __launch_bounds__(256) beaver_chain_kernel(const __grid_constant__ BeaverChainParams<B0, ST> p) {
+  const int slot = blockIdx.y;
+  const bool pr = p.pair != 0;
+  const unsigned nb = gridDim.x * gridDim.y;
+  const u64 t0 = blockIdx.x * u64(blockDim.x) + threadIdx.x, stride = u64(gridDim.x) * blockDim.x;
+  unsigned ep = 0;
+  for (u64 g = t0; g < p.n; g += stride) eval_slots(p.build, pr, slot, g);
+  for (int r = 0; r < p.nsteps; ++r) {
+    grid_barrier(p.bar, ++ep * nb);
+    for (u64 g = t0; g < p.n; g += stride) eval_slots(p.steps[r], pr, slot, g);
+  }
+}
+
+template <class B0, class ST>
+void persistent_beaver_chain(Session& s, u64 n, const B0& build, const std::vector<ST>& steps) {
+  if (steps.size() > size_t(kMaxChainSteps)) throw Error(kInternalError, "beaver chain too long");
+  BeaverChainParams<B0, ST> p{};
+  p.build = build;
+  for (size_t i = 0; i < steps.size(); ++i) p.steps[i] = steps[i];
+  p.nsteps = int(steps.size());
+  p.n = n;
+  p.pair = s.n_local == 2 && pair_eval_enabled();
+  DT bar = s.alloc(Shape{1});
+  MPCG_CUDA(cudaMemsetAsync(bar.s[0], 0, 8, s.stream));
+  p.bar = reinterpret_cast<unsigned*>(bar.s[0]);
+  const unsigned gy = p.pair ? 1u : unsigned(s.n_local);
+  auto kern = beaver_chain_kernel<B0, ST>;
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    MPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    if (per_sm < 1) throw Error(kInternalError, "beaver chain kernel cannot be resident");
+  }
+  const u64 cap = u64(per_sm) * kSms / gy;
+  u64 blocks = (n + 255) / 256;
+  blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(unsigned(blocks), gy);
+  lc.blockDim = dim3(256);
+  lc.stream = s.stream;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeCooperative;
+  attr.val.cooperative = 1;
+  lc.attrs = &attr;
+  lc.numAttrs = 1;
+  cudaEvent_t pe;
+  probe_begin(s.stream, &pe);
+  MPCG_CUDA(cudaLaunchKernelEx(&lc, kern, p));
+  probe_end(s.stream, pe);
 }
 
 // Plain final sinks for adder_op (same functor for every lane).
