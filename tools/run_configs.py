@@ -9,6 +9,8 @@ sent per party per inference and the decoded error vs the float64 plaintext forw
 (tolerance 2^-6, P/tools/mpcpipe_bench.cpp:124). Links: "device" = in-device zero-copy opens;
 "nvlink" = an emulated 900 GB/s, 2 us link (the comm-stream token bucket, so opens overlap
 compute as they would between two GPUs); "10gbps" = the paper's LAN (1.25e9 B/s, 0.1 ms).
+The pipelined mode's chunk threshold is calibrated per link (the reference's --threshold auto):
+off for in-device opens, the ReLU-probe crossover for the emulated link; the sweep forces chunking.
 """
 import argparse
 import json
@@ -103,6 +105,14 @@ def main():
         ("bert_base", "public", ["device"], False),
         ("vgg16", "private", ["device", "nvlink"], True),
     ]
+    # inner-pipeline threshold per link, as the reference CLI's --threshold auto (bench.hpp:200-205):
+    # in-device opens never gain from chunking; an emulated link is calibrated with the ReLU probe
+    from paper_2209_13643_b200 import tuning
+    thr = {"device": 1 << 62}
+    for link in ("nvlink",):
+        t = tuning.calibrate_threshold(4, LINKS[link])
+        thr[link] = (1 << 62) if t is None else t
+    doc["thresholds"] = {k: (None if v == 1 << 62 else v) for k, v in thr.items()}
     for name, weights, links, graph in plan:
         if a.only and name not in a.only.split(","):
             continue
@@ -113,7 +123,8 @@ def main():
             t0 = time.time()
             try:
                 b = run_one(g, "blocking", weights, link, graph=graph, check_ref=ref, iters=2 if a.quick else 3)
-                p = run_one(g, "pipelined", weights, link, graph=graph, check_ref=ref, iters=2 if a.quick else 3)
+                p = run_one(g, "pipelined", weights, link, threshold=thr[link], graph=graph, check_ref=ref,
+                            iters=2 if a.quick else 3)
                 doc["configs"][key] = {"batch": g.input[0], "blocking": {k: v for k, v in b.items() if k != "per_layer_ms"},
                                        "pipelined": {k: v for k, v in p.items() if k != "per_layer_ms"},
                                        "pipelining": reduction(b, p), "wall_s": time.time() - t0}
