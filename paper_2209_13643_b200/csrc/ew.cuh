@@ -426,6 +426,127 @@ void mul_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, 
   s.check();
 }
 
+// Mixed chain: any sequence of Beaver squares and multiplies, each "combine round r, build
+// round r+1" in one pass (LayerNorm's inverse-sqrt Newton step is square, mul, mul). The
+// policy PV maps round r's product to the value v (val) and the next round's operands
+// (nx, ny; a square uses nx only). Payload of a lane: square [eps(w)], multiply [eps(w) | delta(w)].
+template <class PV>
+struct MixedChainStep {
+  EwTriple Tp, Tn;
+  int psq, nsq;  // round r / r+1 is a square
+  Pid2 pid;
+  CPtr2 ownp, peerp;
+  Ptr2 ownn;
+  u64 lo, w;
+  int last;
+  PV pv;
+  __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
+  __device__ void both(u64 j) const { step<2>(0, j); }
+  template <int NS>
+  __device__ __forceinline__ void step(int slot0, u64 j) const {
+    const u64 g = lo + j;
+    const bool p0 = NS == 2 || pid.v[slot0] == 0;
+    Sw sp{0, 0, 0}, sn{0, 0, 0};
+    Dw dp{0, 0, 0, 0, 0}, dn{0, 0, 0, 0, 0};
+    if (psq) sp = sq_draw(Tp, Tp.off + g, p0, true);
+    else dp = ew_draw<true>(Tp, Tp.off + g, p0);
+    if (!last) {
+      if (nsq) sn = sq_draw(Tn, Tn.off + g, p0, false);
+      else dn = ew_draw<false>(Tn, Tn.off + g, p0);
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const int slot = slot0 + k, party = pid.v[slot];
+      const u64* o = ownp.p[slot];
+      const u64* q = peerp.p[slot];
+      u64 z;
+      if (psq) {
+        const u64 e = o[j] + q[j];
+        z = sq_share_c(party, sp) + (e * sq_share_a(party, sp)) * 2;
+        if (party == 0) z += e * e;
+      } else {
+        const u64 e = o[j] + q[j], d = o[w + j] + q[w + j];
+        u64 a, b, c;
+        ew_share<true>(Tp, party, dp, a, b, c);
+        z = c + (e * b + d * a);
+        if (party == 0) z += e * d;
+      }
+      const u64 v = pv.val(slot, party, g, z);
+      if (!last) {
+        if (nsq) {
+          ownn.p[slot][j] = pv.nx(slot, g, v) - sq_share_a(party, sn);
+        } else {
+          u64 an, bn, cn;
+          ew_share<false>(Tn, party, dn, an, bn, cn);
+          ownn.p[slot][j] = pv.nx(slot, g, v) - an;
+          ownn.p[slot][w + j] = pv.ny(slot, g, v) - bn;
+        }
+      }
+    }
+  }
+};
+
+// Rounds tr[0..R) (sq[r] says square or multiply): round 0 on (x0, y0) (square: x0 only),
+// round r on pv_for(r-1)'s operands; pv_for(R-1).val sees the last product.
+template <class XF, class YF, class PVF>
+void mixed_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, const std::vector<int>& sq,
+                 const std::vector<std::string>& tags, XF x0, YF y0, PVF pv_for) {
+  chunks = clamp_chunks(chunks, n);
+  const int R = int(tr.size());
+  const Pid2 pid = pids(s);
+  auto ctag = [&](int r, int k) { return chunks == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
+  auto words = [&](int r, size_t w) { return sq[r] ? w : 2 * w; };
+  using PV0 = decltype(pv_for(0));
+  if (chunks == 1 && R <= 24 && n > 0 && s.persistent_ok(n)) {  // one cooperative kernel
+    std::vector<Open> op(static_cast<size_t>(R));
+    for (int r = 0; r < R; ++r) op[r] = s.begin_open(words(r, n), Reduce::Sum);
+    std::vector<MixedChainStep<PV0>> st;
+    for (int r = 1; r <= R; ++r)
+      st.push_back(MixedChainStep<PV0>{tr[r - 1].ew, r < R ? tr[r].ew : tr[r - 1].ew, sq[r - 1], r < R ? sq[r] : 0,
+                                       pid, as_const(own_ptrs(op[r - 1])), peer_ptrs(op[r - 1]),
+                                       r < R ? own_ptrs(op[r]) : Ptr2{{nullptr, nullptr}}, 0, n, r == R ? 1 : 0,
+                                       pv_for(r - 1)});
+    if (sq[0])
+      persistent_beaver_chain(s, n, SqBuild2<XF>{tr[0].ew, pid, own_ptrs(op[0]), 0, x0}, st);
+    else
+      persistent_beaver_chain(s, n, MulBuild<XF, YF>{tr[0].ew, pid, own_ptrs(op[0]), 0, n, x0, y0}, st);
+    for (int r = 0; r < R; ++r) s.account(words(r, n), Reduce::Sum, tags[r]);
+    s.check();
+    return;
+  }
+  std::vector<Open> hs(static_cast<size_t>(chunks));
+  for (int k = 0; k < chunks; ++k) {
+    const auto rg = chunk_range(n, chunks, k);
+    const size_t w = rg.second - rg.first;
+    hs[k] = s.begin_open(words(0, w), Reduce::Sum);
+    if (sq[0])
+      launch_ew(s.stream, s.n_local, w, SqBuild2<XF>{tr[0].ew, pid, own_ptrs(hs[k]), rg.first, x0});
+    else
+      launch_ew(s.stream, s.n_local, w, MulBuild<XF, YF>{tr[0].ew, pid, own_ptrs(hs[k]), rg.first, w, x0, y0});
+    s.post(hs[k], ctag(0, k));
+  }
+  using PV = decltype(pv_for(0));
+  for (int r = 1; r <= R; ++r) {
+    for (int k = 0; k < chunks; ++k) {
+      const auto rg = chunk_range(n, chunks, k);
+      const size_t w = rg.second - rg.first;
+      Open next;
+      if (r < R) next = s.begin_open(words(r, w), Reduce::Sum);
+      s.wait(hs[k]);
+      MixedChainStep<PV> st{tr[r - 1].ew, r < R ? tr[r].ew : tr[r - 1].ew, sq[r - 1], r < R ? sq[r] : 0, pid,
+                            as_const(own_ptrs(hs[k])), peer_ptrs(hs[k]),
+                            r < R ? own_ptrs(next) : Ptr2{{nullptr, nullptr}}, rg.first, w, r == R ? 1 : 0,
+                            pv_for(r - 1)};
+      launch_ew(s.stream, s.n_local, w, st);
+      if (r < R) {
+        hs[k] = std::move(next);
+        s.post(hs[k], ctag(r, k));
+      }
+    }
+  }
+  s.check();
+}
+
 // ---------------------------------------------------------------- SPK adder rounds
 // H/protocols/adder.hpp:122-223. Round 0 is the generate AND on (x, y); rounds 1..L are
 // the prefix levels on the stacked (S, P) pair. One kernel settles round rp and issues

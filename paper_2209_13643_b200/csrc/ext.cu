@@ -67,13 +67,28 @@ struct OutScaleRescale {  // out[r] = sar(acc * k, f) (+ [p0] add)
     out.p[slot][r] = sar64(acc * k, f) + (pid.v[slot] == 0 ? add : 0);
   }
 };
-struct SinkNewtonU3 {  // u = [p0] 3 - trunc(v y^2, f)
-  Ptr2 u;
+// Round policy of the fused inverse-sqrt Newton chain (oracle inv_sqrt_shares):
+//   after square y2_i: y2 = trunc(z, f)            -> next mul (v, y2)
+//   after mul vy_i:    u = [p0] 3 - trunc(z, f)    -> next mul (y, u)
+//   after mul yu_i:    y = trunc(z, f+1), stored   -> next square (y)
+struct IsqrtPV {
+  Pid2 pid;
+  CPtr2 v;
+  Ptr2 y;
   int f;
   u64 three;
-  __device__ void operator()(int slot, int party, u64 g, u64 z) const {
-    u.p[slot][g] = (party == 0 ? three : 0) - sar64(z, f);
+  int phase;
+  __device__ u64 val(int slot, int party, u64 g, u64 z) const {
+    if (phase == 0) return sar64(z, f);
+    if (phase == 1) return (party == 0 ? three : 0) - sar64(z, f);
+    const u64 yy = sar64(z, f + 1);
+    y.p[slot][g] = yy;
+    return yy;
   }
+  __device__ u64 nx(int slot, u64 g, u64 val) const {
+    return phase == 0 ? v.p[slot][g] : (phase == 1 ? y.p[slot][g] : val);
+  }
+  __device__ u64 ny(int, u64, u64 val) const { return val; }
 };
 struct SinkTruncAddCol {  // out = sar(z, f) + beta[g % d]
   Ptr2 out;
@@ -131,19 +146,26 @@ DT inv_sqrt_shares(Session& s, const DT& v, const std::string& tag, int newton_i
       yp.p[slot][i] = (sar64(ep.p[slot][i] * c22, f) - sar64(vp.p[slot][i], 10)) + (pid.v[slot] == 0 ? c02 : 0);
     });
   }
-  DT y2 = s.alloc(v.shape, v.scale), u = s.alloc(v.shape, v.scale);
+  if (newton_iters <= 0) return y;
+  // Newton steps as ONE fused chain of 3*iters rounds: square y -> y2, mul v*y2 -> u, mul y*u -> y
+  std::vector<Triple> tr;
+  std::vector<int> sq;
+  std::vector<std::string> tags;
   for (int i = 0; i < newton_iters; ++i) {
     const std::string it = std::to_string(i);
-    Triple ts = s.fetch(TripleSpec::square_of(v.shape), tag + ".y2" + it);
-    ts.mark_consumed();
-    square_op(s, ts.ew, n, ch, tag + ".y2" + it, SrcMem{cptrs(y)}, SinkTrunc{ptrs(y2), f});
-    Triple tv = s.fetch(TripleSpec::elementwise(TripleKind::Arith, v.shape), tag + ".vy" + it);
-    tv.mark_consumed();
-    mul_op(s, tv.ew, n, ch, tag + ".vy" + it, SrcMem{cptrs(v)}, SrcMem{cptrs(y2)}, SinkNewtonU3{ptrs(u), f, three});
-    Triple ty = s.fetch(TripleSpec::elementwise(TripleKind::Arith, v.shape), tag + ".yu" + it);
-    ty.mark_consumed();
-    mul_op(s, ty.ew, n, ch, tag + ".yu" + it, SrcMem{cptrs(y)}, SrcMem{cptrs(u)}, SinkTrunc{ptrs(y), f + 1});
+    tags.push_back(tag + ".y2" + it);
+    tr.push_back(s.fetch(TripleSpec::square_of(v.shape), tags.back()));
+    sq.push_back(1);
+    tags.push_back(tag + ".vy" + it);
+    tr.push_back(s.fetch(TripleSpec::elementwise(TripleKind::Arith, v.shape), tags.back()));
+    sq.push_back(0);
+    tags.push_back(tag + ".yu" + it);
+    tr.push_back(s.fetch(TripleSpec::elementwise(TripleKind::Arith, v.shape), tags.back()));
+    sq.push_back(0);
   }
+  for (auto& t : tr) t.mark_consumed();
+  mixed_chain(s, n, ch, tr, sq, tags, SrcMem{cptrs(y)}, SrcZero{},
+              [&](int r) { return IsqrtPV{pids(s), cptrs(v), ptrs(y), f, three, r % 3}; });
   return y;
 }
 

@@ -155,7 +155,6 @@ void launch_simt(Session& s, GemmArgs a) {
 // exactly once per (k, n) for ALL segments of a slot — party 0's three segments share one
 // B / r_B draw and one F load — while the few L rows of a K-chunk are staged in shared
 // memory. Bound by reading F (2 x 8 B per (k, n) per party) and the dealer draws.
-constexpr int kGvM = 16;    // rows per block (row groups above that)
 constexpr int kGvMax = 16;  // the small-M path takes M <= kGvMax (M=64 x N=120 measured 6x slower than SIMT)
 constexpr int kGvKC = 64;   // K chunk staged in smem
 
