@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libmpcg.so")
+# MPCG_LIB selects another build of the same ABI (e.g. lib/libmpcg_nodealer.so, the online-only
+# timing build of tools/dealer_split.py); there is no CPU fallback either way.
+LIB_PATH = os.environ.get("MPCG_LIB") or os.path.join(_HERE, "lib", "libmpcg.so")
 
 
 class Error(RuntimeError):

@@ -58,6 +58,12 @@ __host__ __device__ __forceinline__ u64 sar64(u64 v, int k) {
 }
 
 __host__ __device__ __forceinline__ u64 mix64(u64 z) {
+#if defined(MPCG_NO_DEALER) && defined(__CUDA_ARCH__)
+  // Measurement build (make dealerless): device-side dealer/mask draws cost nothing, so timing
+  // it beside the real build separates the online protocol from the dealer's work (SURVEY
+  // 8f row 4). Its shares are NOT the reference's; it is never used for parity.
+  return z;
+#endif
   z ^= z >> 30;
   z *= 0xBF58476D1CE4E5B9ull;
   z ^= z >> 27;
