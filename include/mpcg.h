@@ -180,6 +180,10 @@ int mpcg_set_gemv(int on);
 /* tcgen05 generation: 1 = warp-specialised pipeline (operands generated in producer warps or
  * packed once, bulk-copied; default), 0 = first-generation kernel (materialised operands). */
 int mpcg_set_tc2(int on);
+/* Debug: stage timestamps (clock64) of the last tcgen05 GEMM's first CTA when MPCG_TC2_TRACE=1;
+ * [stage][10] = MMA wait start/end/issue end, generated-producer and memory-producer
+ * empty-wait start/end/arrive. */
+int mpcg_debug_tc2_trace(uint64_t* out, int n);
 /* Link two single-party sessions (party 0, party 1) of this process on the same GPU: the
  * one-party-per-GPU code path with device copies in place of NCCL send/recv. Each party
  * must be driven by its own host thread (a collective waits for the peer's matching post). */

@@ -465,6 +465,10 @@ int mpcg_session_connect_loopback(mpcg_session* a, mpcg_session* b) {
   });
 }
 
+int mpcg_debug_tc2_trace(uint64_t* out, int n) {
+  return guard([&] { tc2_trace_read(reinterpret_cast<unsigned long long*>(out), n); });
+}
+
 int mpcg_set_tc2(int on) {
   return guard([&] { tc2_mode() = on ? 1 : 0; });
 }

@@ -126,6 +126,7 @@ int& tc_gemm_mode();  // 0 = never tensor cores, 1 = whenever exact, 2 = auto by
 int& tc2_mode();
 bool ring_gemm_tc2_wants(const GemmArgs& a);
 bool ring_gemm_tc2_try(Session& s, const GemmArgs& a);
+void tc2_trace_read(unsigned long long* out, int n);  // debug: stage timestamps (MPCG_TC2_TRACE=1)
 bool ring_gemm_tc_wants(const GemmArgs& a);  // shape/budget test only (operands not inspected)
 void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na, const Open& d, size_t nb,
                     DT* rcache, u64* const out[2], size_t out_off, u32 nbatch, u32 M, u32 N, u32 K, bool tb,

@@ -183,6 +183,12 @@ __device__ __forceinline__ void tmem_ld(u32 addr, u32 (&r)[W]) {
 
 }  // namespace
 
+// Debug trace (MPCG_TC2_TRACE=1): stage timestamps of CTA (0,0,0) — MMA thread wait-for-full
+// start/end + issue end, producer warps 0 (generated) and 8 (memory) empty-wait start/end and
+// arrive — read back with mpcg_debug_tc2_trace. Off by default; no effect on values.
+constexpr int kTraceStages = 256;
+__device__ unsigned long long g_tc2_trace[kTraceStages][10];
+
 struct Tc2Args {
   GemmArgs g;
   const char* Rpk[2] = {nullptr, nullptr};  // packed right operand per slot
@@ -193,6 +199,7 @@ struct Tc2Args {
   int vec = 0;                              // L rows 16-byte aligned (vector loads)
   u32 ksplit = 1, kbper = 0;                // split-K over K blocks (partials summed by the epilogue kernel)
   u32 l2ahead = 3;                          // K blocks of L2 prefetch ahead of the register loads (0 = off)
+  int trace = 0;
 };
 
 namespace {
@@ -288,13 +295,19 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
     int firstmem = -1;
     for (int g = 0; g < nseg && firstmem < 0; ++g)
       if (is_mem(g)) firstmem = g;
+    const bool tr = P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 &&
+                    (warp == 0 || warp == kProdWarps / 2);
+    const int tcol = warp == 0 ? 3 : 6;
     auto publish = [&](const u64 (&v)[16], u32 it) {
       const int stg = int(it % kStages);
+      if (tr && it < kTraceStages) g_tc2_trace[it][tcol] = clock64();
       if (it >= kStages) mbar_wait(&empty[stg], ((it / kStages) & 1) ^ 1);
+      if (tr && it < kTraceStages) g_tc2_trace[it][tcol + 1] = clock64();
       transpose16_store(v, smem + stg * kStage, kA, off);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[stg]);
+      if (tr && it < kTraceStages) g_tc2_trace[it][tcol + 2] = clock64();
     };
     if (egroup) {  // memory segments: loads of the next one in flight while this one is published
       if (firstmem >= 0) fetch(firstmem, kb0);
@@ -459,7 +472,10 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
       constexpr u32 idesc = idesc_i8(kM, BN);
       for (u32 it = 0; it < nst; ++it) {
         const int stg = int(it % kStages);
+        const bool tr = P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && it < kTraceStages;
+        if (tr) g_tc2_trace[it][0] = clock64();
         mbar_wait(&full[stg], (it / kStages) & 1);
+        if (tr) g_tc2_trace[it][1] = clock64();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const u32 aBase = smem_u32(smem + stg * kStage), bBase = aBase + 8 * kA;
 #pragma unroll
@@ -472,6 +488,8 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
           }
         }
         mma_commit(&empty[stg]);
+        if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && it < kTraceStages)
+          g_tc2_trace[it][2] = clock64();
       }
       mma_commit(&done);
     }
@@ -617,6 +635,11 @@ void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
     return e ? u32(std::atoi(e)) : 3u;
   }();
   P.l2ahead = l2ahead;
+  static const int trace = [] {
+    const char* e = std::getenv("MPCG_TC2_TRACE");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  P.trace = trace;
   const u32 ntiles = (a.N + BN - 1) / BN, mtiles = (a.M + kM - 1) / kM;
   // right operand: batched only when some segment's R has a batch stride
   bool rbatched = false;
@@ -739,6 +762,11 @@ bool ring_gemm_tc2_try(Session& s, const GemmArgs& a) {
     launch_tc2<16>(s, a, false);
   s.check();
   return true;
+}
+
+void tc2_trace_read(unsigned long long* out, int n) {
+  const int m = n < kTraceStages * 10 ? n : kTraceStages * 10;
+  MPCG_CUDA(cudaMemcpyFromSymbol(out, g_tc2_trace, sizeof(unsigned long long) * size_t(m)));
 }
 
 }  // namespace mpcg
