@@ -5,16 +5,18 @@
 // d = l+m; the epilogue recombines z = sum_d D_d << 8d mod 2^64 — the int8 form of
 // LimbPlan/limb_matmul, H/ring/limb.hpp:15-99), restructured as a Blackwell pipeline:
 //
-//   warps 0-7  L producers: generate the left operand of every segment straight from its
+//   warps 0-15 L producers: generate the left operand of every segment straight from its
 //              source — the opened E = own + peer eps (two vector loads) or the dealer's
 //              A / r_A draws (counter PRG, H/sharing/triple.hpp:96-114) — byte-transpose it
 //              into K-major limb planes and publish the stage with an mbarrier arrive;
-//   warp 8     bulk loader: the right operands (weight side, packed once per layer into the
+//   warp 16    bulk loader: the right operands (weight side, packed once per layer into the
 //              exact shared-memory image of a stage) arrive by cp.async.bulk (TMA engine)
 //              on the same mbarrier with expect_tx;
-//   warp 9     MMA issuer (one thread): 36 tcgen05.mma per stage, tcgen05.commit frees the
-//              stage;
-//   warps 0-7  epilogue: tcgen05.ld of the 8 diagonals, recombination, Beaver epilogue.
+//   warp 17    MMA issuer (one thread): per stage, A plane l against the B planes 0..7-l
+//              stacked along N (the packed B image interleaves the planes per K chunk) — 8
+//              MMAs of N = (8-l)*BN (split at 256), 12 for BN = 64 instead of 36 per-pair
+//              MMAs, since the issue cost is per instruction; tcgen05.commit frees the stage;
+//   warps 0-15 epilogue: tcgen05.ld of the 8 diagonals, recombination, Beaver epilogue.
 //
 // A 4-stage ring of 32-byte K slabs keeps HBM loads, PRG work and MMAs in flight together.
 // When N spans several BN tiles the left operand is also packed once (pack kernel) and both
@@ -28,7 +30,10 @@ namespace {
 
 constexpr int kM = 128;        // tile rows (UMMA M)
 constexpr int kKB = 32;        // K values (= limb bytes) per stage: one UMMA K slab
-constexpr int kStages = 4;
+#ifndef MPCG_TC2_STAGES
+#define MPCG_TC2_STAGES 4
+#endif
+constexpr int kStages = MPCG_TC2_STAGES;
 constexpr int kProdWarps = 16;                 // L producers (and epilogue): warps 0-15
 constexpr int kVW = 8;                         // K values per producer unit (= 8-byte limb row segment)
 constexpr int kLoadWarp = kProdWarps;          // bulk loader
@@ -81,6 +86,15 @@ __device__ __forceinline__ void mma_i8(u32 d_tmem, u64 adesc, u64 bdesc, u32 ide
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
+// A operand from TMEM (lanes = rows, 4 K bytes per 32-bit column), B from shared memory.
+__device__ __forceinline__ void mma_i8_ts(u32 d_tmem, u32 a_tmem, u64 bdesc, u32 idesc, u32 acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(u64* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -126,6 +140,23 @@ __device__ __forceinline__ void transpose16_store(const u64 (&v)[16], char* base
   }
 }
 
+// The same 16-value unit stored into a TMEM A stage instead: this thread's lane, columns
+// plane*8 + base (+0..3) — 8 tcgen05.st of 4 columns.
+__device__ __forceinline__ void transpose16_tmem(const u64 (&v)[16], u32 taddr) {
+#pragma unroll
+  for (int l = 0; l < 8; ++l) {
+    const int sh = (l & 3), hi = l >> 2;
+    u32 w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = hi ? u32(v[i] >> 32) : u32(v[i]);
+    const u32 x = gather4(w[0], w[1], w[2], w[3], sh), y = gather4(w[4], w[5], w[6], w[7], sh),
+              z = gather4(w[8], w[9], w[10], w[11], sh), t = gather4(w[12], w[13], w[14], w[15], sh);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr + u32(l) * 8), "r"(x),
+                 "r"(y), "r"(z), "r"(t)
+                 : "memory");
+  }
+}
+
 // kVW dealer draws c0, c0+1, ... of one stream (key + c*phi advances by phi).
 __device__ __forceinline__ void draws_vec(u64 key, u64 c0, u64 (&v)[kVW]) {
   u64 z = key + c0 * kPhi;
@@ -142,6 +173,18 @@ __device__ __forceinline__ void load_vec(const u64* p, u64 (&v)[kVW]) {
     const uint4 w = __ldg(p4 + i);
     v[2 * i] = (u64(w.y) << 32) | w.x;
     v[2 * i + 1] = (u64(w.w) << 32) | w.z;
+  }
+}
+__device__ __forceinline__ void transpose8_tmem(const u64 (&v)[kVW], u32 taddr) {
+#pragma unroll
+  for (int l = 0; l < 8; ++l) {
+    const int sh = (l & 3), hi = l >> 2;
+    u32 w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = hi ? u32(v[i] >> 32) : u32(v[i]);
+    const u32 x = gather4(w[0], w[1], w[2], w[3], sh), y = gather4(w[4], w[5], w[6], w[7], sh);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr + u32(l) * 8), "r"(x), "r"(y)
+                 : "memory");
   }
 }
 // 8 K-consecutive u64 -> one 8-byte row segment in each of the 8 limb planes.
@@ -204,12 +247,19 @@ struct Tc2Args {
 
 namespace {
 
-template <int BN, bool SPLIT>
+// AT: the left operand's limb planes live in TMEM (4 stages x 8 planes x 8 columns after the
+// 8*BN accumulator columns), written by the producers with tcgen05.st; each MMA then reads
+// only its B plane from shared memory. Without it every MMA re-reads a 4 KB A plane and the
+// 36-MMA stage is shared-memory-bandwidth bound (~51-70 cycles per M128xN64 MMA, measured)
+// rather than tensor bound (32). Needs 8*BN + 256 <= 512 columns, i.e. BN = 32.
+template <int BN, bool SPLIT, bool AT>
 __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_constant__ Tc2Args P) {
-  constexpr u32 kA = kM * kKB;  // bytes per A limb plane per stage
-  constexpr u32 kB = BN * kKB;  // bytes per B limb plane per stage
+  constexpr u32 kA = AT ? 0 : kM * kKB;  // bytes per A limb plane per shared-memory stage
+  constexpr u32 kB = BN * kKB;           // bytes per B limb plane per stage
   constexpr u32 kStage = 8 * (kA + kB);
-  constexpr u32 kCols = 8 * BN;
+  constexpr u32 kAcols = 8 * BN;
+  constexpr u32 kCols = AT ? 512 : kAcols;
+  static_assert(!AT || kAcols + kStages * 64 <= 512, "TMEM budget (A stages)");
   static_assert(kCols <= 512, "TMEM budget");
   extern __shared__ __align__(1024) char smem[];
   __shared__ __align__(8) u64 full[kStages], empty[kStages], done;
@@ -303,8 +353,15 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
       if (tr && it < kTraceStages) g_tc2_trace[it][tcol] = clock64();
       if (it >= kStages) mbar_wait(&empty[stg], ((it / kStages) & 1) ^ 1);
       if (tr && it < kTraceStages) g_tc2_trace[it][tcol + 1] = clock64();
-      transpose16_store(v, smem + stg * kStage, kA, off);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if constexpr (AT) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        transpose16_tmem(v, tmem + ((u32(r) & ~31u) << 16) + kAcols + u32(stg) * 64 + u32(hf) * 4);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      } else {
+        transpose16_store(v, smem + stg * kStage, kA, off);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[stg]);
       if (tr && it < kTraceStages) g_tc2_trace[it][tcol + 2] = clock64();
@@ -444,8 +501,15 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
             }
           }
           if (it >= kStages) mbar_wait(&empty[stg], ((it / kStages) & 1) ^ 1);
-          transpose8_store(v, smem + stg * kStage, kA, off);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+          if constexpr (AT) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            transpose8_tmem(v, tmem + ((u32(r) & ~31u) << 16) + kAcols + u32(stg) * 64 + u32(q) * 2);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          } else {
+            transpose8_store(v, smem + stg * kStage, kA, off);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+          }
           __syncwarp();
           if (lane == 0) mbar_arrive(&full[stg]);
         }
@@ -469,7 +533,6 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
     }
   } else {
     if (lane == 0) {  // ---- MMA issuer
-      constexpr u32 idesc = idesc_i8(kM, BN);
       for (u32 it = 0; it < nst; ++it) {
         const int stg = int(it % kStages);
         const bool tr = P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && it < kTraceStages;
@@ -478,13 +541,22 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
         if (tr) g_tc2_trace[it][1] = clock64();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const u32 aBase = smem_u32(smem + stg * kStage), bBase = aBase + 8 * kA;
+        // A plane l times B planes 0..7-l (stacked along N) -> diagonals l..7 (adjacent TMEM
+        // column blocks): one MMA of N = (8-l)*BN, split at the 256-column MMA limit. Issue
+        // cost is per instruction (~50 cycles measured for any N <= 64), so 12 wide MMAs
+        // instead of 36 narrow ones leave the stage tensor-bound.
 #pragma unroll
         for (int l = 0; l < 8; ++l) {
-          const u64 ad = smem_desc(aBase + l * kA, (kM / 8) * 128, 128);
+          const u32 acc = (it > 0 || l > 0) ? 1u : 0u;
 #pragma unroll
-          for (int mm = 0; mm + l < 8; ++mm) {
-            const u64 bd = smem_desc(bBase + mm * kB, (BN / 8) * 128, 128);
-            mma_i8(tmem + u32(l + mm) * BN, ad, bd, idesc, (it > 0 || l > 0) ? 1u : 0u);
+          for (u32 c0 = 0; c0 < u32(8 - l) * BN; c0 += 256) {
+            const u32 nn = min(256u, u32(8 - l) * BN - c0);
+            const u64 bd = smem_desc(bBase + (c0 / 8) * 128, BN * 128, 128);
+            const u32 dcol = tmem + u32(l) * BN + c0;
+            if constexpr (AT)
+              mma_i8_ts(dcol, tmem + kAcols + u32(stg) * 64 + u32(l) * 8, bd, idesc_i8(kM, nn), acc);
+            else
+              mma_i8(dcol, smem_desc(aBase + l * kA, (kM / 8) * 128, 128), bd, idesc_i8(kM, nn), acc);
           }
         }
         mma_commit(&empty[stg]);
@@ -595,11 +667,15 @@ __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows
     }
     char* base = out + ((((u64(bb) * tiles + tile) * nkb + kb) * nseg + g) * 8) * plane;
     const u32 kc = kq / 4;  // which 16-byte K chunk of the core matrix
-    const u32 off = (kc * (BR / 8) + r / 8) * 128 + (r % 8) * 16 + (kq % 4) * 4;
+    // left: plane-major (one MMA A operand per plane); right: the 8 planes stacked along N
+    // inside each K chunk, so planes 0..7-l form one B operand of N = (8-l)*BR rows
+    const u32 off = left ? (kc * (BR / 8) + r / 8) * 128 + (r % 8) * 16 + (kq % 4) * 4
+                         : kc * (BR * 128) + (r / 8) * 128 + (r % 8) * 16 + (kq % 4) * 4;
+    const u32 pstride = left ? plane : BR * 16;
 #pragma unroll
     for (int l = 0; l < 8; ++l) {
       const u32* w = l < 4 ? lo : hi;
-      *reinterpret_cast<u32*>(base + l * plane + off) = gather4(w[0], w[1], w[2], w[3], u32(l & 3));
+      *reinterpret_cast<u32*>(base + l * pstride + off) = gather4(w[0], w[1], w[2], w[3], u32(l & 3));
     }
   }
 }
@@ -617,14 +693,16 @@ void launch_pack(Session& s, const GemmArgs& a, bool left, u32 rows, u32 nbatch,
   probe_end(s.stream, pe);
 }
 
-template <int BN>
+template <int BN, bool AT = false>
 void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
-  constexpr u32 kStage = 8 * (kM * kKB + BN * kKB);
+  constexpr u32 kStage = 8 * ((AT ? 0 : kM * kKB) + BN * kKB);
   const size_t smem = kStages * kStage;
   static bool attr = false;
   if (!attr) {
-    MPCG_CUDA(cudaFuncSetAttribute(ring_gemm_tc2<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    MPCG_CUDA(cudaFuncSetAttribute(ring_gemm_tc2<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    MPCG_CUDA(
+        cudaFuncSetAttribute(ring_gemm_tc2<BN, false, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    MPCG_CUDA(
+        cudaFuncSetAttribute(ring_gemm_tc2<BN, true, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr = true;
   }
   Tc2Args P{};
@@ -705,9 +783,9 @@ void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
     return !(e && e[0] == '0');
   }();
   if (split_groups)
-    launch_pdl(ring_gemm_tc2<BN, true>, grid, dim3(kThreads), smem, s.stream, P);
+    launch_pdl(ring_gemm_tc2<BN, true, AT>, grid, dim3(kThreads), smem, s.stream, P);
   else
-    launch_pdl(ring_gemm_tc2<BN, false>, grid, dim3(kThreads), smem, s.stream, P);
+    launch_pdl(ring_gemm_tc2<BN, false, AT>, grid, dim3(kThreads), smem, s.stream, P);
   probe_end(s.stream, pe);
   if (P.ksplit > 1) {
     ClassScope ep_scope(kClsOther, 0);
@@ -754,7 +832,16 @@ bool ring_gemm_tc2_try(Session& s, const GemmArgs& a) {
     return e ? e[0] - '0' : 2;
   }();
   const bool multiN = a.N > 64 && (packl == 1 || (packl == 2 && a.N > 512));
-  if (a.N > 32)
+  // left operand in TMEM (BN = 32 tiles) for the regenerated-L shapes: opt-in only — with the
+  // wide MMAs the stage is no longer shared-memory bound, and halving BN doubles the L
+  // regeneration (measured ResNet-18 51.4 vs 43.3 ms)
+  static const int at = [] {
+    const char* e = std::getenv("MPCG_TC2_AT");  // 1 = on, 0 = off
+    return e ? e[0] - '0' : 0;
+  }();
+  if (at == 1 && !multiN && a.N > 16)
+    launch_tc2<32, true>(s, a, false);
+  else if (a.N > 32)
     launch_tc2<64>(s, a, multiN);
   else if (a.N > 16)
     launch_tc2<32>(s, a, false);
