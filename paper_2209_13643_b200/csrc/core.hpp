@@ -123,6 +123,10 @@ struct Open {
   bool waited = false;
   bool posted = false;
   cudaEvent_t ready = nullptr;   // arrival (throttled link or NCCL), or null
+  // n_local == 2 only, set by the caller before the build: the build writes the opened value
+  // (own0 + own1 — what both parties read after the zero-copy open) once into own(0) instead
+  // of the two payloads; consumers read it as one operand (beaver_combine).
+  bool summed = false;
   u64* own(int slot) const { return out->ptr + size_t(slot) * n; }
   const u64* peer(int slot) const;
   int n_local = 2;

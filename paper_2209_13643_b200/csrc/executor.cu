@@ -306,6 +306,7 @@ DT SecureExecutor::weight_matmul(size_t i, const DT& x, const ConvGeom* geom, bo
   Open e = s_.begin_open(na, Reduce::Sum);
   DT aops;  // A-side combine operands from the eps draws (memory-operand combines only)
   if (beaver_combine_wants_aops(s_, 1, M, N, K)) aops = s_.alloc(Shape{2, na});
+  else if (!geom || na < (size_t(1) << 32)) e.summed = beaver_combine_fuses_eps(s_, 1, M, N, K);
   if (geom)
     eps_build_im2col(s_, t, x.s, *geom, 0, na, e, aops ? &aops : nullptr);
   else

@@ -422,6 +422,15 @@ void eps_build_mem(Session& s, const Triple& t, const u64* const x[2], size_t a_
   const MmTriple mm = t.mm;
   const CPtr2 xp{{x[0], x[1]}};
   const Ptr2 ap{{aops ? aops->s[0] : nullptr, aops ? aops->s[1] : nullptr}};
+  if (o.summed) {  // fused in-device open: both payloads, summed in registers
+    if (s.n_local != 2 || aops) throw Error(kUsageError, "summed eps open needs both slots and no A operands");
+    launch_ew(s.stream, 1, na, [=] __device__(int, u64 j) {
+      const u64 e0 = xp.p[0][a_off + j] - a_share_out(mm, pid.v[0], a_off + j, nullptr, j, na);
+      const u64 e1 = xp.p[1][a_off + j] - a_share_out(mm, pid.v[1], a_off + j, nullptr, j, na);
+      own.p[0][j] = e0 + e1;
+    });
+    return;
+  }
   launch_ew(s.stream, s.n_local, na, [=] __device__(int slot, u64 j) {
     own.p[slot][j] = xp.p[slot][a_off + j] - a_share_out(mm, pid.v[slot], a_off + j, ap.p[slot], j, na);
   });
@@ -453,6 +462,7 @@ struct EpsIm2colPair {
   FastDiv fKK, fk, fOW, fOH;
   u64 a_off, na;
   int nslots;
+  int summed;  // fused in-device open: write own0 + own1 into own.p[0] only
   __device__ void operator()(u64 j) const {
     const u32 jj = u32(j);
     const u32 r = fKK.div(jj), c = jj - r * fKK.d;
@@ -468,6 +478,7 @@ struct EpsIm2colPair {
     const u64 ra = mix64(key + mm.prA + ip);
     u64 A = 0;
     bool haveA = false;
+    u64 esum = 0;
 #pragma unroll
     for (int sl = 0; sl < 2; ++sl) {
       if (sl >= nslots) break;
@@ -487,8 +498,10 @@ struct EpsIm2colPair {
         a = ra;
         if (ap.p[sl]) ap.p[sl][j] = ra;
       }
-      own.p[sl][j] = v - a;
+      if (summed) esum += v - a;  // this party's payload, reconstructed with the peer's below
+      else own.p[sl][j] = v - a;
     }
+    if (summed) own.p[0][j] = esum;
   }
 };
 template <class F>
@@ -504,7 +517,9 @@ void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const 
     EpsIm2colPair f{t.mm, pids(s), own_ptrs(o),
                     Ptr2{{aops ? aops->s[0] : nullptr, aops && s.n_local == 2 ? aops->s[1] : nullptr}},
                     CPtr2{{x[0], s.n_local == 2 ? x[1] : nullptr}}, gm, FastDiv(gm.C * gm.k * gm.k), FastDiv(gm.k),
-                    FastDiv(gm.OW), FastDiv(gm.OH), a_off, na, s.n_local};
+                    FastDiv(gm.OW), FastDiv(gm.OH), a_off, na, s.n_local, o.summed ? 1 : 0};
+    if (o.summed && (s.n_local != 2 || aops))
+      throw Error(kUsageError, "summed eps open needs both slots and no A operands");
     cudaEvent_t pe;
     probe_begin(s.stream, &pe);
     launch_pdl(strip_kernel<EpsIm2colPair>, dim3(ew_blocks(na)), dim3(256), 0, s.stream, u64(na), f);
@@ -517,6 +532,7 @@ void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const 
   const CPtr2 xp{{x[0], x[1]}};
   const ConvGeom g = gm;
   const Ptr2 ap{{aops ? aops->s[0] : nullptr, aops ? aops->s[1] : nullptr}};
+  if (o.summed) throw Error(kUsageError, "summed eps open: call-local im2col indices must fit 32 bits");
   launch_ew(s.stream, s.n_local, na, [=] __device__(int slot, u64 j) {
     const u64 idx = a_off + j;
     const u32 KK = g.C * g.k * g.k;
@@ -657,6 +673,24 @@ bool beaver_combine_wants_aops(const Session& s, u32 nbatch, u32 M, u32 N, u32 K
   return !ring_gemm_tc2_wants(a);
 }
 
+// The eps open can be fused into its build (Open::summed) when both slots are local and the
+// combine reads E as a GEMM operand (not through prepare_L / the A-operand path).
+bool beaver_combine_fuses_eps(const Session& s, u32 nbatch, u32 M, u32 N, u32 K) {
+  static const bool enabled = [] {  // MPCG_EPS_FUSE=0: always materialise both payloads
+    const char* e = std::getenv("MPCG_EPS_FUSE");
+    return !(e && e[0] == '0');
+  }();
+  if (!enabled || s.n_local != 2 || beaver_combine_wants_aops(s, nbatch, M, N, K)) return false;
+  GemmArgs a{};
+  a.nslots = s.n_local;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.nbatch = nbatch;
+  for (int i = 0; i < s.n_local; ++i) a.sl[i].nseg = s.party_of[i] == 0 ? 3 : 2;
+  return ring_gemm_tc2_wants(a) || !ring_gemm_tc_wants(a);
+}
+
 void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na, const Open& d, size_t nb,
                     DT* rcache, u64* const out[2], size_t out_off, u32 nbatch, u32 M, u32 N, u32 K, bool tb,
                     bool batched_r, size_t r_batch0, const Epi& ep, const DT* aops) {
@@ -672,6 +706,7 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
   a.OHW = ep.OHW;
   for (int i = 0; i < s.n_local; ++i) a.sl[i].nseg = s.party_of[i] == 0 ? 3 : 2;
   if (!ring_gemm_tc2_wants(a) && ring_gemm_tc_wants(a)) {
+    if (e.summed) throw Error(kUsageError, "beaver_combine: summed eps on the prepare_L path");
     if (!*rcache) *rcache = prepare_R(s, t, d, nb);
     if (!aops) {  // no A-side operands from the eps build: materialise L
       DT L = prepare_L(s, t, e, a_off, na);
@@ -717,8 +752,9 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
   const bool tc2 = !(gemv_eligible_shape(M, nbatch, tb, ep.col2im) && gemv_mode() != 0) && ring_gemm_tc2_wants(a);
   for (int i = 0; i < s.n_local; ++i) {
     GemmSlotArgs& S = a.sl[i];
-    const u64* E0 = e.own(i);
-    const u64* E1 = e.peer(i);
+    const u64* E0 = e.summed ? e.own(0) : e.own(i);
+    const u64* E1 = e.summed ? nullptr : e.peer(i);
+    const int ek = e.summed ? kOpMem : kOpSum;  // E = own + peer, or already summed
     const u64* F0 = d.own(i) + rboff;
     const u64* F1 = d.peer(i) + rboff;
     S.out = out[i] + out_off;
@@ -734,7 +770,7 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
       S.cterm = -1;
       S.lk[0] = kOpA;
       S.rk[0] = kOpBF, S.R[0] = F0, S.R2[0] = F1;
-      S.lk[1] = kOpSum, S.L[1] = E0, S.L2[1] = E1;
+      S.lk[1] = ek, S.L[1] = E0, S.L2[1] = E1;
       S.rk[1] = kOpB0F, S.R[1] = F0, S.R2[1] = F1;
       S.lk[2] = kOpRA;
       S.rk[2] = kOpNegSum, S.R[2] = F0, S.R2[2] = F1;
@@ -743,14 +779,14 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
       if (ao) S.lk[0] = kOpMem, S.L[0] = ao;
       else S.lk[0] = kOpA;
       S.rk[0] = kOpB;
-      S.lk[1] = kOpSum, S.L[1] = E0, S.L2[1] = E1;
+      S.lk[1] = ek, S.L[1] = E0, S.L2[1] = E1;
       S.rk[1] = kOpB0F, S.R[1] = F0, S.R2[1] = F1;
       if (ao) S.lk[2] = kOpMem, S.L[2] = ao + na;
       else S.lk[2] = kOpA0;
       S.rk[2] = kOpSum, S.R[2] = F0, S.R2[2] = F1;
     } else {  // +r_C + E*r_B + r_A*F
       S.cterm = +1;
-      S.lk[0] = kOpSum, S.L[0] = E0, S.L2[0] = E1;
+      S.lk[0] = ek, S.L[0] = E0, S.L2[0] = E1;
       S.rk[0] = kOpRB;
       if (ao) S.lk[1] = kOpMem, S.L[1] = ao;
       else S.lk[1] = kOpRA;
@@ -815,6 +851,9 @@ DT beaver_matmul(Session& s, const DT& x, const DT& y, bool transpose_b, const s
     const bool want = batched_b ? beaver_combine_wants_aops(s, u32(cnt), u32(M), u32(N), u32(K))
                                 : beaver_combine_wants_aops(s, 1, u32(cnt), u32(N), u32(K));
     if (want) aops[k] = s.alloc(Shape{2, cnt * row_w});  // A-side combine operands from the eps draws
+    else
+      he[k].summed = batched_b ? beaver_combine_fuses_eps(s, u32(cnt), u32(M), u32(N), u32(K))
+                               : beaver_combine_fuses_eps(s, 1, u32(cnt), u32(N), u32(K));
     eps_build_mem(s, t, x.s, r.first * row_w, cnt * row_w, he[k], want ? &aops[k] : nullptr);
     s.post(he[k], chunks == 1 ? tag + ".eps" : tag + ".eps.chunk" + std::to_string(k));
   }

@@ -134,6 +134,7 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
 // Whether the combine of this shape runs on the tensor cores (materialised operands) —
 // callers then skip emitting the A-side operands in the eps build.
 bool beaver_combine_uses_tc(const Session& s, u32 nbatch, u32 M, u32 N, u32 K);
+bool beaver_combine_fuses_eps(const Session& s, u32 nbatch, u32 M, u32 N, u32 K);
 bool beaver_combine_wants_aops(const Session& s, u32 nbatch, u32 M, u32 N, u32 K);
 
 void delta_build_mem(Session& s, const Triple& t, const u64* const y[2], size_t nb, Open& o);

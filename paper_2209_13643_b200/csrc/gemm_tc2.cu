@@ -123,6 +123,13 @@ __device__ __forceinline__ void load16(const u64* p, u64 (&v)[16]) {
     v[2 * i + 1] = (u64(w.w) << 32) | w.z;
   }
 }
+__device__ __forceinline__ void load16w(const u64* p, u64 (&v)[16]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+        : "=l"(v[4 * i]), "=l"(v[4 * i + 1]), "=l"(v[4 * i + 2]), "=l"(v[4 * i + 3])
+        : "l"(p + 4 * i));
+}
 // 16 K-consecutive u64 -> one 16-byte row in each of the 8 limb planes.
 __device__ __forceinline__ void transpose16_store(const u64 (&v)[16], char* base, u32 plane, u32 off) {
 #pragma unroll
@@ -174,6 +181,13 @@ __device__ __forceinline__ void load_vec(const u64* p, u64 (&v)[kVW]) {
     v[2 * i] = (u64(w.y) << 32) | w.x;
     v[2 * i + 1] = (u64(w.w) << 32) | w.z;
   }
+}
+__device__ __forceinline__ void load_vecw(const u64* p, u64 (&v)[kVW]) {
+#pragma unroll
+  for (int i = 0; i < kVW / 4; ++i)
+    asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+        : "=l"(v[4 * i]), "=l"(v[4 * i + 1]), "=l"(v[4 * i + 2]), "=l"(v[4 * i + 3])
+        : "l"(p + 4 * i));
 }
 __device__ __forceinline__ void transpose8_tmem(const u64 (&v)[kVW], u32 taddr) {
 #pragma unroll
@@ -239,7 +253,7 @@ struct Tc2Args {
   const char* Lpk[2] = {nullptr, nullptr};  // packed left operand (multi-N-tile shapes) or null
   u64 Lpk_b[2] = {0, 0};
   u32 nkb = 0;                              // K blocks of 32
-  int vec = 0;                              // L rows 16-byte aligned (vector loads)
+  int vec = 0;                              // L row loads: 2 = 32-byte, 1 = 16-byte, 0 = scalar
   u32 ksplit = 1, kbper = 0;                // split-K over K blocks (partials summed by the epilogue kernel)
   u32 l2ahead = 3;                          // K blocks of L2 prefetch ahead of the register loads (0 = off)
   int trace = 0;
@@ -325,11 +339,16 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
 #pragma unroll
         for (int i = 0; i < 16; ++i) pr[i] = pr2[i] = 0;
       } else if (k0 + 16 <= K && P.vec) {
-        load16(S.L[g] + rowoff + k0, pr);
-        if (sum) load16(S.L2[g] + rowoff + k0, pr2);
-        else {
+        // 256-bit loads where aligned: one L1 wavefront per 32-byte sector, not two
+        if (P.vec == 2) load16w(S.L[g] + rowoff + k0, pr);
+        else load16(S.L[g] + rowoff + k0, pr);
+        if (!sum) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) pr2[i] = 0;
+        } else if (P.vec == 2) {
+          load16w(S.L2[g] + rowoff + k0, pr2);
+        } else {
+          load16(S.L2[g] + rowoff + k0, pr2);
         }
       } else {
 #pragma unroll
@@ -437,8 +456,13 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
 #pragma unroll
           for (int i = 0; i < kVW; ++i) pr[i] = pr2[i] = 0;
         } else if (k0 + kVW <= K && P.vec) {
-          load_vec(S.L[pf] + rowoff + k0, pr);
-          if (sum) load_vec(S.L2[pf] + rowoff + k0, pr2);
+          if (P.vec == 2) {
+            load_vecw(S.L[pf] + rowoff + k0, pr);
+            if (sum) load_vecw(S.L2[pf] + rowoff + k0, pr2);
+          } else {
+            load_vec(S.L[pf] + rowoff + k0, pr);
+            if (sum) load_vec(S.L2[pf] + rowoff + k0, pr2);
+          }
         } else {
 #pragma unroll
           for (int i = 0; i < kVW; ++i) {
@@ -748,15 +772,19 @@ void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
     launch_pack<BN>(s, a, false, a.N, rb, P.nkb, rp[0], rp[1]);
     if (packL) launch_pack<kM>(s, a, true, a.M, a.nbatch, P.nkb, lp[0], lp[1]);
   }
-  bool vec = (a.K % 2) == 0;
-  for (int i = 0; i < a.nslots && vec; ++i)
-    for (int g = 0; g < a.sl[i].nseg; ++g) {
-      const GemmSlotArgs& S = a.sl[i];
-      if (S.lk[g] == kOpMem || S.lk[g] == kOpSum)
-        vec = vec && reinterpret_cast<uintptr_t>(S.L[g]) % 16 == 0 && S.sL[g] % 2 == 0;
-      if (S.lk[g] == kOpSum) vec = vec && reinterpret_cast<uintptr_t>(S.L2[g]) % 16 == 0;
-    }
-  P.vec = vec ? 1 : 0;
+  // vector width of the L row loads: 2 = 32-byte (LDG.256), 1 = 16-byte, 0 = scalar
+  auto aligned = [&](u32 vals) {
+    bool ok = (a.K % vals) == 0;
+    for (int i = 0; i < a.nslots && ok; ++i)
+      for (int g = 0; g < a.sl[i].nseg; ++g) {
+        const GemmSlotArgs& S = a.sl[i];
+        if (S.lk[g] == kOpMem || S.lk[g] == kOpSum)
+          ok = ok && reinterpret_cast<uintptr_t>(S.L[g]) % (8 * vals) == 0 && S.sL[g] % vals == 0;
+        if (S.lk[g] == kOpSum) ok = ok && reinterpret_cast<uintptr_t>(S.L2[g]) % (8 * vals) == 0;
+      }
+    return ok;
+  };
+  P.vec = aligned(4) ? 2 : aligned(2) ? 1 : 0;
   // split K when the tile grid cannot fill the SMs (small-M layers): >= 2 K blocks per split
   const u64 ctas = u64(ntiles) * mtiles * a.nslots * a.nbatch;
   u32 split = 1;
