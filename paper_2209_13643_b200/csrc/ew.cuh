@@ -604,9 +604,15 @@ struct AdderRound {
     const u64 g = lo + j;
     const bool p0 = NS == 2 || pid.v[slot0] == 0;  // does any evaluated slot play party 0
     u64 dummy;
+    // Pair evaluation (NS == 2; the launchers use it for every round of an adder or none): the
+    // wire holds the opened value (payload0 ^ payload1, what the XOR open reveals to both
+    // parties) once, in slot 0's outbox, instead of the two payloads — a settle reads 32 B per
+    // element instead of 2 x 32, an issue writes 32 instead of 2 x 32.
+    constexpr bool op = NS == 2;
     if (rn == 0) {  // issue the generate AND: payload [x^a | y^b]
       const Dw dn = ew_draw<false>(Tn, Tn.off + g, p0);
       if (cwn) dw_store(cwn, cwN, g, 0, dn);
+      u64 o0 = 0, o1 = 0;
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
         const int slot = slot0 + k;
@@ -614,8 +620,17 @@ struct AdderRound {
         P0.p[slot][g] = x ^ y;
         u64 a, b;
         ew_share<false>(Tn, pid.v[slot], dn, a, b, dummy);
-        ownn.p[slot][j] = x ^ a;
-        ownn.p[slot][w + j] = y ^ b;
+        if (op) {
+          o0 ^= x ^ a;
+          o1 ^= y ^ b;
+        } else {
+          ownn.p[slot][j] = x ^ a;
+          ownn.p[slot][w + j] = y ^ b;
+        }
+      }
+      if (op) {
+        ownn.p[0][j] = o0;
+        ownn.p[0][w + j] = o1;
       }
       return;
     }
@@ -625,9 +640,9 @@ struct AdderRound {
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
         const int slot = slot0 + k, party = pid.v[slot];
-        const u64* o = ownp.p[slot];
+        const u64* o = ownp.p[op ? 0 : slot];
         const u64* q = peerp.p[slot];
-        const u64 e = o[j] ^ q[j], d = o[w + j] ^ q[w + j];
+        const u64 e = op ? o[j] : o[j] ^ q[j], d = op ? o[w + j] : o[w + j] ^ q[w + j];
         u64 a, b, c;
         ew_share<true>(Tp, party, dp, a, b, c);
         s[k] = c ^ (e & b) ^ (d & a);
@@ -640,6 +655,11 @@ struct AdderRound {
       const Dw d0 = cwp ? dw_load(cwp, cwN, g, 0, Tp, Tp.off + g) : ew_draw<true>(Tp, Tp.off + g, p0);
       const Dw d1 = cwp ? dw_load(cwp, cwN, g, 1, Tp, Tp.ghalf + Tp.off + g)
                         : ew_draw<true>(Tp, Tp.ghalf + Tp.off + g, p0);
+      u64 oe0 = 0, oe1 = 0, od0 = 0, od1 = 0;  // the opened wire (pair evaluation)
+      if (op) {
+        const u64* o = ownp.p[0];
+        oe0 = o[j], oe1 = o[w + j], od0 = o[2 * w + j], od1 = o[3 * w + j];
+      }
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
         const int slot = slot0 + k, party = pid.v[slot];
@@ -649,9 +669,9 @@ struct AdderRound {
         ew_share<true>(Tp, party, d1, a1, b1, c1);
         const u64 s0 = S.p[slot][g], p0s = P.p[slot][g];
         const u64 po = p0s & lp.out;
-        const u64 e0 = (po ^ a0) ^ q[j], e1 = (po ^ a1) ^ q[w + j];
-        const u64 dd0 = (((s0 & lp.in) * lp.mult) ^ b0) ^ q[2 * w + j];
-        const u64 dd1 = (((p0s & lp.in) * lp.mult) ^ b1) ^ q[3 * w + j];
+        const u64 e0 = op ? oe0 : (po ^ a0) ^ q[j], e1 = op ? oe1 : (po ^ a1) ^ q[w + j];
+        const u64 dd0 = op ? od0 : (((s0 & lp.in) * lp.mult) ^ b0) ^ q[2 * w + j];
+        const u64 dd1 = op ? od1 : (((p0s & lp.in) * lp.mult) ^ b1) ^ q[3 * w + j];
         u64 z0 = c0 ^ (e0 & b0) ^ (dd0 & a0);
         u64 z1 = c1 ^ (e1 & b1) ^ (dd1 & a1);
         if (party == 0) {
@@ -668,6 +688,7 @@ struct AdderRound {
         dw_store(cwn, cwN, g, 0, d0);
         dw_store(cwn, cwN, g, 1, d1);
       }
+      u64 o[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
         const int slot = slot0 + k, party = pid.v[slot];
@@ -675,13 +696,26 @@ struct AdderRound {
         ew_share<false>(Tn, party, d0, a0, b0, dummy);
         ew_share<false>(Tn, party, d1, a1, b1, dummy);
         const u64 po = p[k] & ln.out;
-        u64* nn = ownn.p[slot];
-        nn[j] = po ^ a0;
-        nn[w + j] = po ^ a1;
-        nn[2 * w + j] = ((s[k] & ln.in) * ln.mult) ^ b0;
-        nn[3 * w + j] = ((p[k] & ln.in) * ln.mult) ^ b1;
+        const u64 v0 = po ^ a0, v1 = po ^ a1, v2 = ((s[k] & ln.in) * ln.mult) ^ b0,
+                  v3 = ((p[k] & ln.in) * ln.mult) ^ b1;
+        if (op) {
+          o[0] ^= v0, o[1] ^= v1, o[2] ^= v2, o[3] ^= v3;
+        } else {
+          u64* nn = ownn.p[slot];
+          nn[j] = v0;
+          nn[w + j] = v1;
+          nn[2 * w + j] = v2;
+          nn[3 * w + j] = v3;
+        }
         S.p[slot][g] = s[k];
         P.p[slot][g] = p[k];
+      }
+      if (op) {
+        u64* nn = ownn.p[0];
+        nn[j] = o[0];
+        nn[w + j] = o[1];
+        nn[2 * w + j] = o[2];
+        nn[3 * w + j] = o[3];
       }
     } else {
 #pragma unroll
@@ -714,6 +748,10 @@ inline bool adder_draw_cache_ok(const Session& s, size_t n) {
   const bool one_thread = s.n_local == 1 || pair_eval_enabled();
   return on && one_thread && n > 0 && n * 2 * 64 <= (size_t(48) << 20);
 }
+
+// Opened-wire adder rounds (see AdderRound::step): exactly when the pair kernel evaluates
+// every round (both slots local, pair evaluation on; MPCG_PAIR_EVAL=0 = two payloads).
+inline bool adder_opened_wire(const Session& s) { return s.n_local == 2 && pair_eval_enabled(); }
 
 // Secure binary addition of XOR-shared operands given by sources. The last kernel of each
 // lane hands the sum to ff_for_lane(lane, lo, w) — a functor (slot, party, g, j, sum) that
@@ -775,8 +813,11 @@ void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& 
     }
     if (rn > c.levels) k.ff = ff_for_lane(lane, lo, hi - lo);
     // algorithmic bytes per element per party (2 x wire + 8 x (in + out)):
-    // level round = 2x32 wire + 8x(2 state in + 2 state out) = 96 B
-    ClassScope cs(rn >= 1 && rn <= c.levels ? kClsAdderRound : kClsOther, 96.0 * double(hi - lo) * s.n_local);
+    // level round = 2x32 wire + 8x(2 state in + 2 state out) = 96 B; with the opened wire
+    // (pair evaluation) the 32-byte opened value is written once and read once per element
+    // pair: 32 + 32 state = 64 B per element per party
+    ClassScope cs(rn >= 1 && rn <= c.levels ? kClsAdderRound : kClsOther,
+                  (adder_opened_wire(s) ? 64.0 : 96.0) * double(hi - lo) * s.n_local);
     launch_ew(s.stream, s.n_local, hi - lo, k);
   };
   fetch_round(0);

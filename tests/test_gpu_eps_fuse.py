@@ -1,6 +1,8 @@
-"""The fused in-device eps open (Open::summed: the eps build writes own0 + own1 once, the
-combine GEMM reads it as one operand) must leave every output share word-identical to the
-two-payload form (MPCG_EPS_FUSE=0). Runs both forms in subprocesses (the knob is read once)."""
+"""The fused in-device opens must leave every output share word-identical to the two-payload
+forms: the eps open summed at build time (Open::summed, off with MPCG_EPS_FUSE=0) and the
+opened-value wire of pair-evaluated adder rounds (off with MPCG_PAIR_EVAL=0, which evaluates
+each party slot separately with its own payload). Runs each form in a subprocess (the knobs
+are read once)."""
 import json
 import os
 import subprocess
@@ -31,18 +33,22 @@ for (M, K, N) in [(1024, 576, 64), (8, 300, 40), (4, 64, 64)]:
     X = s.tensor(rng.integers(0, 2**63, size=(2, M, K), dtype=np.uint64))
     Y = s.tensor(rng.integers(0, 2**63, size=(2, K, N), dtype=np.uint64))
     out[f"mm{M}x{K}x{N}"] = hashlib.sha1(mp.beaver_matmul(s, X, Y, False, "t").numpy().tobytes()).hexdigest()
+for n in (1000, 300000):
+    X = s.tensor(rng.integers(0, 2**63, size=(2, n), dtype=np.uint64))
+    out[f"relu{n}"] = hashlib.sha1(mp.relu_shares(s, X).numpy().tobytes()).hexdigest()
 print(json.dumps(out))
 ''' % ROOT
 
 
-def run(fuse):
-    env = dict(os.environ, MPCG_EPS_FUSE=fuse)
+def run(fuse, pair="1"):
+    env = dict(os.environ, MPCG_EPS_FUSE=fuse, MPCG_PAIR_EVAL=pair)
     r = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     return json.loads(r.stdout.strip().splitlines()[-1])
 
 
 @pytest.mark.gpu
-def test_fused_eps_open_matches_two_payloads():
-    a, b = run("1"), run("0")
+def test_fused_opens_match_two_payloads():
+    a, b, c = run("1"), run("0"), run("0", pair="0")
     assert a == b
+    assert a == c
