@@ -13,6 +13,21 @@ namespace mpcg {
 struct Pid2 {
   int v[2];
 };
+
+// Slot and party at position k of a step<NS>(slot0, ...) loop. Pair evaluation (NS == 2, both
+// parties local, so the two slots play parties 0 and 1): position k is PARTY k, which makes
+// every party-dependent branch of the share algebra a compile-time constant.
+template <int NS>
+__device__ __forceinline__ int pair_slot(const Pid2& pid, int slot0, int k) {
+  if constexpr (NS == 2) return pid.v[0] == k ? 0 : 1;
+  else return slot0 + k;
+}
+template <int NS>
+__device__ __forceinline__ int pair_party(const Pid2& pid, int slot, int k) {
+  if constexpr (NS == 2) return k;
+  else return pid.v[slot];
+}
+
 struct Ptr2 {
   u64* p[2];
 };
@@ -77,7 +92,7 @@ struct MulBuild {
     const Dw d = ew_draw<false>(T, T.off + g, NS == 2 || pid.v[slot0] == 0);
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      const int slot = slot0 + k;
+      const int slot = pair_slot<NS>(pid, slot0, k);
       u64 a, b, c;
       ew_share<false>(T, pid.v[slot], d, a, b, c);
       own.p[slot][j] = xf(slot, g) - a;
@@ -101,7 +116,7 @@ struct MulCombine {
     const Dw dr = ew_draw<true>(T, T.off + g, NS == 2 || pid.v[slot0] == 0);
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      const int slot = slot0 + k, party = pid.v[slot];
+      const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
       const u64* o = own.p[slot];
       const u64* q = peer.p[slot];
       const u64 e = o[j] + q[j];
@@ -235,7 +250,7 @@ struct SqBuild2 {
     const Sw d = sq_draw(T, T.off + g, NS == 2 || pid.v[slot0] == 0, false);
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      const int slot = slot0 + k;
+      const int slot = pair_slot<NS>(pid, slot0, k);
       own.p[slot][j] = xf(slot, g) - sq_share_a(pid.v[slot], d);
     }
   }
@@ -262,7 +277,7 @@ struct SqChainStep {
     if (!last) dn = sq_draw(Tn, Tn.off + g, p0, false);
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      const int slot = slot0 + k, party = pid.v[slot];
+      const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
       const u64 e = ownp.p[slot][j] + peerp.p[slot][j];
       u64 z = sq_share_c(party, dp) + (e * sq_share_a(party, dp)) * 2;
       if (party == 0) z += e * e;
@@ -352,7 +367,7 @@ struct MulChainStep {
     if (!last) dn = ew_draw<false>(Tn, Tn.off + g, p0);
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      const int slot = slot0 + k, party = pid.v[slot];
+      const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
       const u64* o = ownp.p[slot];
       const u64* q = peerp.p[slot];
       const u64 e = o[j] + q[j], d = o[w + j] + q[w + j];
@@ -456,7 +471,7 @@ struct MixedChainStep {
     }
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      const int slot = slot0 + k, party = pid.v[slot];
+      const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
       const u64* o = ownp.p[slot];
       const u64* q = peerp.p[slot];
       u64 z;
@@ -615,7 +630,7 @@ struct AdderRound {
       u64 o0 = 0, o1 = 0;
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
-        const int slot = slot0 + k;
+        const int slot = pair_slot<NS>(pid, slot0, k);
         const u64 x = xf(slot, g), y = yf(slot, g);
         P0.p[slot][g] = x ^ y;
         u64 a, b;
@@ -639,7 +654,7 @@ struct AdderRound {
       const Dw dp = cwp ? dw_load(cwp, cwN, g, 0, Tp, Tp.off + g) : ew_draw<true>(Tp, Tp.off + g, p0);
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
-        const int slot = slot0 + k, party = pid.v[slot];
+        const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
         const u64* o = ownp.p[op ? 0 : slot];
         const u64* q = peerp.p[slot];
         const u64 e = op ? o[j] : o[j] ^ q[j], d = op ? o[w + j] : o[w + j] ^ q[w + j];
@@ -662,7 +677,7 @@ struct AdderRound {
       }
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
-        const int slot = slot0 + k, party = pid.v[slot];
+        const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
         const u64* q = peerp.p[slot];
         u64 a0, b0, c0, a1, b1, c1;
         ew_share<true>(Tp, party, d0, a0, b0, c0);
@@ -691,7 +706,7 @@ struct AdderRound {
       u64 o[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
-        const int slot = slot0 + k, party = pid.v[slot];
+        const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
         u64 a0, b0, a1, b1;
         ew_share<false>(Tn, party, d0, a0, b0, dummy);
         ew_share<false>(Tn, party, d1, a1, b1, dummy);
@@ -720,7 +735,7 @@ struct AdderRound {
     } else {
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
-        const int slot = slot0 + k;
+        const int slot = pair_slot<NS>(pid, slot0, k);
         ff(slot, pid.v[slot], g, j, (P0.p[slot][g] ^ (s[k] << 1)) & wmask);
       }
     }
