@@ -132,6 +132,17 @@ __device__ __forceinline__ Dw ew_draw(const EwTriple& t, u64 g, bool p0) {
   }
   return d;
 }
+// Only the dealer's secrets A, B of element g: what the two parties' shares reconstruct to
+// (a0 ^ a1 or a0 + a1), all an opened-wire issue needs — the masks cancel in the open.
+__device__ __forceinline__ Dw ew_secrets(const EwTriple& t, u64 g) {
+  const u64 key = tkey(t.key, t.kp);
+  const u64 gp = g * kPhi;
+  Dw d;
+  d.ra = d.rb = d.rc = 0;
+  d.A = mix64(key + t.pA + gp);
+  d.B = t.square ? d.A : mix64(key + t.pB + gp);
+  return d;
+}
 // `party`'s shares of a drawn element (0 absorbs the secret).
 template <bool WithC>
 __device__ __forceinline__ void ew_share(const EwTriple& t, int party, const Dw& d, u64& a, u64& b, u64& c) {

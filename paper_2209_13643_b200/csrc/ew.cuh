@@ -625,7 +625,9 @@ struct AdderRound {
     // element instead of 2 x 32, an issue writes 32 instead of 2 x 32.
     constexpr bool op = NS == 2;
     if (rn == 0) {  // issue the generate AND: payload [x^a | y^b]
-      const Dw dn = ew_draw<false>(Tn, Tn.off + g, p0);
+      // opened wire: payload0 ^ payload1 = (x0 ^ x1) ^ (a0 ^ a1) with a0 ^ a1 = A (the masks
+      // r_A cancel), so only the dealer's A, B are drawn
+      const Dw dn = op && !cwn ? ew_secrets(Tn, Tn.off + g) : ew_draw<false>(Tn, Tn.off + g, p0);
       if (cwn) dw_store(cwn, cwN, g, 0, dn);
       u64 o0 = 0, o1 = 0;
 #pragma unroll
@@ -636,16 +638,16 @@ struct AdderRound {
         u64 a, b;
         ew_share<false>(Tn, pid.v[slot], dn, a, b, dummy);
         if (op) {
-          o0 ^= x ^ a;
-          o1 ^= y ^ b;
+          o0 ^= x;
+          o1 ^= y;
         } else {
           ownn.p[slot][j] = x ^ a;
           ownn.p[slot][w + j] = y ^ b;
         }
       }
       if (op) {
-        ownn.p[0][j] = o0;
-        ownn.p[0][w + j] = o1;
+        ownn.p[0][j] = o0 ^ dn.A;
+        ownn.p[0][w + j] = o1 ^ dn.B;
       }
       return;
     }
@@ -698,24 +700,26 @@ struct AdderRound {
       }
     }
     if (rn <= levels) {  // issue level rn-1 (H/protocols/adder.hpp:122-140)
-      const Dw d0 = ew_draw<false>(Tn, Tn.off + g, p0), d1 = ew_draw<false>(Tn, Tn.ghalf + Tn.off + g, p0);
+      // opened wire: the masks r_A, r_B cancel between the two payloads (see rn == 0)
+      const bool sec = op && !cwn;
+      const Dw d0 = sec ? ew_secrets(Tn, Tn.off + g) : ew_draw<false>(Tn, Tn.off + g, p0);
+      const Dw d1 = sec ? ew_secrets(Tn, Tn.ghalf + Tn.off + g) : ew_draw<false>(Tn, Tn.ghalf + Tn.off + g, p0);
       if (cwn) {
         dw_store(cwn, cwN, g, 0, d0);
         dw_store(cwn, cwN, g, 1, d1);
       }
-      u64 o[4] = {0, 0, 0, 0};
+      u64 o[4] = {0, 0, 0, 0};  // o[1] unused: words 0 and 1 share the unmasked half po
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
         const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
         u64 a0, b0, a1, b1;
         ew_share<false>(Tn, party, d0, a0, b0, dummy);
         ew_share<false>(Tn, party, d1, a1, b1, dummy);
-        const u64 po = p[k] & ln.out;
-        const u64 v0 = po ^ a0, v1 = po ^ a1, v2 = ((s[k] & ln.in) * ln.mult) ^ b0,
-                  v3 = ((p[k] & ln.in) * ln.mult) ^ b1;
-        if (op) {
-          o[0] ^= v0, o[1] ^= v1, o[2] ^= v2, o[3] ^= v3;
+        const u64 po = p[k] & ln.out, ms = (s[k] & ln.in) * ln.mult, mp = (p[k] & ln.in) * ln.mult;
+        if (op) {  // the unmasked halves; the XOR of the two parties' masks is added below
+          o[0] ^= po, o[2] ^= ms, o[3] ^= mp;
         } else {
+          const u64 v0 = po ^ a0, v1 = po ^ a1, v2 = ms ^ b0, v3 = mp ^ b1;
           u64* nn = ownn.p[slot];
           nn[j] = v0;
           nn[w + j] = v1;
@@ -725,12 +729,12 @@ struct AdderRound {
         S.p[slot][g] = s[k];
         P.p[slot][g] = p[k];
       }
-      if (op) {
+      if (op) {  // a0 ^ a1 = A, b0 ^ b1 = B for each of the two triples
         u64* nn = ownn.p[0];
-        nn[j] = o[0];
-        nn[w + j] = o[1];
-        nn[2 * w + j] = o[2];
-        nn[3 * w + j] = o[3];
+        nn[j] = o[0] ^ d0.A;
+        nn[w + j] = o[0] ^ d1.A;
+        nn[2 * w + j] = o[2] ^ d0.B;
+        nn[3 * w + j] = o[3] ^ d1.B;
       }
     } else {
 #pragma unroll

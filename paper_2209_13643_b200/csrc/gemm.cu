@@ -424,10 +424,9 @@ void eps_build_mem(Session& s, const Triple& t, const u64* const x[2], size_t a_
   const Ptr2 ap{{aops ? aops->s[0] : nullptr, aops ? aops->s[1] : nullptr}};
   if (o.summed) {  // fused in-device open: both payloads, summed in registers
     if (s.n_local != 2 || aops) throw Error(kUsageError, "summed eps open needs both slots and no A operands");
-    launch_ew(s.stream, 1, na, [=] __device__(int, u64 j) {
-      const u64 e0 = xp.p[0][a_off + j] - a_share_out(mm, pid.v[0], a_off + j, nullptr, j, na);
-      const u64 e1 = xp.p[1][a_off + j] - a_share_out(mm, pid.v[1], a_off + j, nullptr, j, na);
-      own.p[0][j] = e0 + e1;
+    launch_ew(s.stream, 1, na, [=] __device__(int, u64 j) {  // eps0 + eps1 = x0 + x1 - A
+      const u64 key = tkey(mm.key, mm.kp);
+      own.p[0][j] = xp.p[0][a_off + j] + xp.p[1][a_off + j] - mix64(key + mm.pA + (a_off + j) * kPhi);
     });
     return;
   }
@@ -475,10 +474,14 @@ struct EpsIm2colPair {
     const u64 src = ((u64(n) * g.C + ci) * g.H + u32(ih)) * g.W + u32(iw);
     const u64 key = tkey(mm.key, mm.kp);
     const u64 ip = (a_off + j) * kPhi;
+    if (summed) {  // eps0 + eps1 = (x0 + x1) - (a0 + a1), a0 + a1 = A: the r_A masks cancel
+      const u64 v = in ? xp.p[0][src] + xp.p[1][src] : 0;
+      own.p[0][j] = v - mix64(key + mm.pA + ip);
+      return;
+    }
     const u64 ra = mix64(key + mm.prA + ip);
     u64 A = 0;
     bool haveA = false;
-    u64 esum = 0;
 #pragma unroll
     for (int sl = 0; sl < 2; ++sl) {
       if (sl >= nslots) break;
@@ -498,10 +501,8 @@ struct EpsIm2colPair {
         a = ra;
         if (ap.p[sl]) ap.p[sl][j] = ra;
       }
-      if (summed) esum += v - a;  // this party's payload, reconstructed with the peer's below
-      else own.p[sl][j] = v - a;
+      own.p[sl][j] = v - a;
     }
-    if (summed) own.p[0][j] = esum;
   }
 };
 template <class F>
