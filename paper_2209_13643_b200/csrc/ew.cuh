@@ -36,6 +36,10 @@ struct CPtr2 {
 };
 
 inline Pid2 pids(const Session& s) { return Pid2{{s.party_of[0], s.party_of[1]}}; }
+// Opened wire (AdderRound, MulBuild/MulCombine, the compare chain's b2a and multiply): exactly
+// when the pair kernel evaluates every kernel of the exchange (both slots local, pair
+// evaluation on); MPCG_PAIR_EVAL=0 = per-slot evaluation with two payloads.
+inline bool adder_opened_wire(const Session& s) { return s.n_local == 2 && pair_eval_enabled(); }
 inline Ptr2 ptrs(const DT& t) { return Ptr2{{t.s[0], t.s[1]}}; }
 inline CPtr2 cptrs(const DT& t) { return CPtr2{{t.s[0], t.s[1]}}; }
 inline Ptr2 own_ptrs(const Open& o) {
@@ -84,11 +88,18 @@ struct MulBuild {
   u64 lo, w;
   XF xf;
   YF yf;
+  bool opened = false;  // pair evaluation: write the opened (eps, delta) once (see MulCombine)
   __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
   __device__ void both(u64 j) const { step<2>(0, j); }
   template <int NS>
   __device__ __forceinline__ void step(int slot0, u64 j) const {
     const u64 g = lo + j;
+    if (NS == 2 && opened) {  // eps0 + eps1 = x0 + x1 - (a0 + a1), a0 + a1 = A: masks cancel
+      const Dw d = ew_secrets(T, T.off + g);
+      own.p[0][j] = xf(0, g) + xf(1, g) - d.A;
+      own.p[0][w + j] = yf(0, g) + yf(1, g) - d.B;
+      return;
+    }
     const Dw d = ew_draw<false>(T, T.off + g, NS == 2 || pid.v[slot0] == 0);
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
@@ -101,6 +112,19 @@ struct MulBuild {
   }
 };
 
+// Functors that can take both party slots' values at once (pair evaluation): FF::pair(q0, g,
+// j, v0, v1) / PF::pair(q0, g, z0, z1), v_k / z_k being party k's, q0 the slot of party 0.
+template <class F, class = void>
+struct has_pair_pf : std::false_type {};
+template <class F>
+struct has_pair_pf<F, std::void_t<decltype(std::declval<const F&>().pair(0, u64(0), u64(0), u64(0)))>>
+    : std::true_type {};
+template <class F, class = void>
+struct has_pair_ff : std::false_type {};
+template <class F>
+struct has_pair_ff<F, std::void_t<decltype(std::declval<const F&>().pair(0, u64(0), u64(0), u64(0), u64(0)))>>
+    : std::true_type {};
+
 template <class PF>
 struct MulCombine {
   EwTriple T;
@@ -108,25 +132,38 @@ struct MulCombine {
   CPtr2 own, peer;
   u64 lo, w;
   PF pf;
+  // Pair evaluation only, and only if the payload's builder wrote it the same way: the opened
+  // (eps, delta) = own0 + own1 sits once in slot 0's outbox (8 B each per element pair
+  // instead of both payloads read by both slots).
+  bool opened = false;
   __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
   __device__ void both(u64 j) const { step<2>(0, j); }
   template <int NS>
   __device__ __forceinline__ void step(int slot0, u64 j) const {
     const u64 g = lo + j;
     const Dw dr = ew_draw<true>(T, T.off + g, NS == 2 || pid.v[slot0] == 0);
+    const bool op = NS == 2 && opened;
+    u64 oe = 0, od = 0;
+    if (op) oe = own.p[0][j], od = own.p[0][w + j];
+    u64 zs[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
-      const u64* o = own.p[slot];
-      const u64* q = peer.p[slot];
-      const u64 e = o[j] + q[j];
-      const u64 d = o[w + j] + q[w + j];
+      u64 e = oe, d = od;
+      if (!op) {
+        const u64* o = own.p[slot];
+        const u64* q = peer.p[slot];
+        e = o[j] + q[j];
+        d = o[w + j] + q[w + j];
+      }
       u64 a, b, c;
       ew_share<true>(T, party, dr, a, b, c);
       u64 z = c + (e * b + d * a);
       if (party == 0) z += e * d;
-      pf(slot, party, g, z);
+      zs[k] = z;
+      if constexpr (!(NS == 2 && has_pair_pf<PF>::value)) pf(slot, party, g, z);
     }
+    if constexpr (NS == 2 && has_pair_pf<PF>::value) pf.pair(pair_slot<2>(pid, 0, 0), g, zs[0], zs[1]);
   }
 };
 
@@ -139,19 +176,25 @@ void mul_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::stri
   chunks = clamp_chunks(chunks, m);
   std::vector<Open> opens(static_cast<size_t>(chunks));
   const Pid2 pid = pids(s);
-  // beaver_mul = 2 x 16 B wire + 8 x (2 in + 1 out) = 56 B/elem/party over build + combine
-  ClassScope cs(kClsBeaver, 28.0 * double(m / chunks) * s.n_local);
+  // beaver_mul = 2 x 16 B wire + 8 x (2 in + 1 out) = 56 B/elem/party over build +
+  // combine; with the opened wire (pair evaluation) the 16 B opened pair is written and read once
+  // per element pair: 8 x 3 + 16 = 40 B/elem/party
+  const bool opened = adder_opened_wire(s);
+  ClassScope cs(kClsBeaver, (opened ? 20.0 : 28.0) * double(m / chunks) * s.n_local);
   for (int k = 0; k < chunks; ++k) {
     const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
     opens[k] = s.begin_open(2 * (hi - lo), Reduce::Sum);
-    launch_ew(s.stream, s.n_local, hi - lo, MulBuild<XF, YF>{T, pid, own_ptrs(opens[k]), lo, hi - lo, xf, yf});
+    MulBuild<XF, YF> mb{T, pid, own_ptrs(opens[k]), lo, hi - lo, xf, yf};
+    mb.opened = opened;
+    launch_ew(s.stream, s.n_local, hi - lo, mb);
     s.post(opens[k], chunks == 1 ? tag : tag + ".chunk" + std::to_string(k));
   }
   for (int k = 0; k < chunks; ++k) {
     const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
     s.wait(opens[k]);
-    launch_ew(s.stream, s.n_local, hi - lo,
-              MulCombine<PF>{T, pid, as_const(own_ptrs(opens[k])), peer_ptrs(opens[k]), lo, hi - lo, pf});
+    MulCombine<PF> mc{T, pid, as_const(own_ptrs(opens[k])), peer_ptrs(opens[k]), lo, hi - lo, pf};
+    mc.opened = opened;
+    launch_ew(s.stream, s.n_local, hi - lo, mc);
     s.check();
   }
 }
@@ -736,6 +779,9 @@ struct AdderRound {
         nn[2 * w + j] = o[2] ^ d0.B;
         nn[3 * w + j] = o[3] ^ d1.B;
       }
+    } else if constexpr (NS == 2 && has_pair_ff<FF>::value) {
+      const int q0 = pair_slot<2>(pid, 0, 0);
+      ff.pair(q0, g, j, (P0.p[q0][g] ^ (s[0] << 1)) & wmask, (P0.p[1 - q0][g] ^ (s[1] << 1)) & wmask);
     } else {
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
@@ -768,9 +814,6 @@ inline bool adder_draw_cache_ok(const Session& s, size_t n) {
   return on && one_thread && n > 0 && n * 2 * 64 <= (size_t(48) << 20);
 }
 
-// Opened-wire adder rounds (see AdderRound::step): exactly when the pair kernel evaluates
-// every round (both slots local, pair evaluation on; MPCG_PAIR_EVAL=0 = two payloads).
-inline bool adder_opened_wire(const Session& s) { return s.n_local == 2 && pair_eval_enabled(); }
 
 // Secure binary addition of XOR-shared operands given by sources. The last kernel of each
 // lane hands the sum to ff_for_lane(lane, lo, w) — a functor (slot, party, g, j, sum) that

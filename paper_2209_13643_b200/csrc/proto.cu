@@ -292,6 +292,7 @@ struct B2aBuildFF {
   EwTriple T;
   Ptr2 own, bits;
   u64 lo, w;
+  bool opened = false;  // pair evaluation: the opened (eps, delta) once in slot 0's outbox
   __device__ void operator()(int slot, int party, u64 g, u64 j, u64 sum) const {
     const u64 bit = sum >> 63;
     bits.p[slot][g] = bit;
@@ -299,6 +300,20 @@ struct B2aBuildFF {
     ew_ab(T, party, T.off + g, a, b);
     own.p[slot][j] = (party == 0 ? bit : 0) - a;      // eps = acc - a
     own.p[slot][w + j] = (party == 1 ? bit : 0) - b;  // delta = bq - b
+  }
+  // both parties (sum_k = party k's, q0 = slot of party 0)
+  __device__ void pair(int q0, u64 g, u64 j, u64 sum0, u64 sum1) const {
+    if (!opened) {
+      (*this)(q0, 0, g, j, sum0);
+      (*this)(1 - q0, 1, g, j, sum1);
+      return;
+    }
+    const u64 bit0 = sum0 >> 63, bit1 = sum1 >> 63;
+    bits.p[q0][g] = bit0;
+    bits.p[1 - q0][g] = bit1;
+    const Dw d = ew_secrets(T, T.off + g);  // eps0 + eps1 = bit0 - A, delta0 + delta1 = bit1 - B
+    own.p[0][j] = bit0 - d.A;
+    own.p[0][w + j] = bit1 - d.B;
   }
 };
 // b2a combine (c = bit - 2*prod) -> payload of the multiply by c, chunk k, same kernel.
@@ -310,6 +325,7 @@ struct MulByBitBuild {
   u64 lo, w;
   UF uf;
   Ptr2 cout;  // optional: keep the arithmetic bit c (sigmoid's select reuses it)
+  bool opened = false;  // pair evaluation: the opened (eps, delta) once in slot 0's outbox
   __device__ void operator()(int slot, int party, u64 g, u64 prod) const {
     const u64 c = (bits.p[slot][g] & 1) - (prod + prod);
     if (cout.p[slot]) cout.p[slot][g] = c;
@@ -318,6 +334,21 @@ struct MulByBitBuild {
     ew_ab(T, party, T.off + g, a, b);
     own.p[slot][j] = uf(slot, g) - a;
     own.p[slot][w + j] = c - b;
+  }
+  __device__ void pair(int q0, u64 g, u64 prod0, u64 prod1) const {
+    if (!opened) {
+      (*this)(q0, 0, g, prod0);
+      (*this)(1 - q0, 1, g, prod1);
+      return;
+    }
+    const int q1 = 1 - q0;
+    const u64 c0 = (bits.p[q0][g] & 1) - (prod0 + prod0), c1 = (bits.p[q1][g] & 1) - (prod1 + prod1);
+    if (cout.p[q0]) cout.p[q0][g] = c0;
+    if (cout.p[q1]) cout.p[q1][g] = c1;
+    const u64 j = g - lo;
+    const Dw d = ew_secrets(T, T.off + g);  // the masks cancel in the open
+    own.p[0][j] = uf(q0, g) + uf(q1, g) - d.A;
+    own.p[0][w + j] = c0 + c1 - d.B;
   }
 };
 
@@ -347,6 +378,7 @@ template <class DF, class UF, class PF>
 void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const std::string& tag_msb,
                             const std::string& tag_b2a, const std::string& tag_mul, DF df, UF uf, PF pf,
                             Ptr2 cout) {
+  const bool opened = adder_opened_wire(s);  // pair evaluation: opened wire for b2a and the multiply
   const int ch = clamp_chunks(opt.chunks, n);
   const Pid2 pid = pids(s);
   const SpkConsts c = make_spk_constants(opt.width);
@@ -410,12 +442,17 @@ void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const
       if (r >= 1) k.cwp = cw[(r - 1) & 1].s[0];
       if (r <= 6) k.cwn = cw[r & 1].s[0];
     }
-    if (r == 7) k.ff = B2aBuildFF{t1.ew, own_ptrs(ob), ptrs(bits), 0, n};
+    if (r == 7) {
+      k.ff = B2aBuildFF{t1.ew, own_ptrs(ob), ptrs(bits), 0, n};
+      k.ff.opened = opened;
+    }
   }
   p.nadder = 8;
   p.b2a = BR{t1.ew, pid, as_const(own_ptrs(ob)), peer_ptrs(ob), 0, n,
              MulByBitBuild<UF>{t2.ew, own_ptrs(og), cptrs(bits), 0, n, uf, cout}};
+  p.b2a.opened = p.b2a.pf.opened = opened;
   p.fin = CR{t2.ew, pid, as_const(own_ptrs(og)), peer_ptrs(og), 0, n, pf};
+  p.fin.opened = opened;
   DT bar = s.alloc(Shape{1});
   MPCG_CUDA(cudaMemsetAsync(bar.s[0], 0, 8, s.stream));
   p.n = n;
@@ -475,6 +512,7 @@ template <class DF, class UF, class PF>
 void compare_mul(Session& s, size_t n, const AdderOptions& opt, const std::string& tag_msb,
                  const std::string& tag_b2a, int chunks_b2a, const std::string& tag_mul, int chunks_mul, DF df,
                  UF uf, PF pf, Ptr2 cout = Ptr2{{nullptr, nullptr}}) {
+  const bool opened = adder_opened_wire(s);  // pair evaluation: opened wire for b2a and the multiply
   const int ch = clamp_chunks(opt.chunks, n);
   if (clamp_chunks(chunks_b2a, n) != ch || clamp_chunks(chunks_mul, n) != ch)
     throw Error(kUsageError, "compare_mul: misaligned chunk lanes");
@@ -505,7 +543,9 @@ void compare_mul(Session& s, size_t n, const AdderOptions& opt, const std::strin
       s, n, opt, tag_msb, df,
       [&](int lane, size_t lo, size_t w) {
         fetch_tail();
-        return B2aBuildFF{t1.ew, own_ptrs(ob[lane]), ptrs(bits), lo, w};
+        B2aBuildFF f{t1.ew, own_ptrs(ob[lane]), ptrs(bits), lo, w};
+        f.opened = opened;
+        return f;
       },
       [&](int lane) { s.post(ob[lane], ctag(tag_b2a + ".m1", lane)); });
   for (int k = 0; k < ch; ++k) {
@@ -513,15 +553,18 @@ void compare_mul(Session& s, size_t n, const AdderOptions& opt, const std::strin
     const size_t lo = r.first, w = r.second - r.first;
     s.wait(ob[k]);
     MulByBitBuild<UF> gb{t2.ew, own_ptrs(og[k]), cptrs(bits), lo, w, uf, cout};
-    launch_ew(s.stream, s.n_local, w,
-              MulCombine<MulByBitBuild<UF>>{t1.ew, pid, as_const(own_ptrs(ob[k])), peer_ptrs(ob[k]), lo, w, gb});
+    gb.opened = opened;
+    MulCombine<MulByBitBuild<UF>> bc{t1.ew, pid, as_const(own_ptrs(ob[k])), peer_ptrs(ob[k]), lo, w, gb};
+    bc.opened = opened;
+    launch_ew(s.stream, s.n_local, w, bc);
     s.post(og[k], ctag(tag_mul, k));
   }
   for (int k = 0; k < ch; ++k) {
     const auto r = chunk_range(n, ch, k);
     s.wait(og[k]);
-    launch_ew(s.stream, s.n_local, r.second - r.first,
-              MulCombine<PF>{t2.ew, pid, as_const(own_ptrs(og[k])), peer_ptrs(og[k]), r.first, r.second - r.first, pf});
+    MulCombine<PF> fc{t2.ew, pid, as_const(own_ptrs(og[k])), peer_ptrs(og[k]), r.first, r.second - r.first, pf};
+    fc.opened = opened;
+    launch_ew(s.stream, s.n_local, r.second - r.first, fc);
   }
   s.check();
 }
