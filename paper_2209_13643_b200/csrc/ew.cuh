@@ -275,6 +275,10 @@ __device__ __forceinline__ Sw sq_draw(const EwTriple& t, u64 g, bool p0, bool wi
   return d;
 }
 __device__ __forceinline__ u64 sq_share_a(int party, const Sw& d) { return party ? d.ra : d.A - d.ra; }
+// the square triple's secret A alone (a0 + a1 = A: all an opened-wire build needs)
+__device__ __forceinline__ u64 sq_secret(const EwTriple& t, u64 g) {
+  return mix64(tkey(t.key, t.kp) + t.pA + g * kPhi);
+}
 __device__ __forceinline__ u64 sq_share_c(int party, const Sw& d) { return party ? d.rc : d.A * d.A - d.rc; }
 
 // Build of the first square of a chain: payload eps = x - a (pair-evaluated).
@@ -285,11 +289,16 @@ struct SqBuild2 {
   Ptr2 own;
   u64 lo;
   XF xf;
+  bool opened = false;  // pair evaluation: write the opened eps once (slot 0's outbox)
   __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
   __device__ void both(u64 j) const { step<2>(0, j); }
   template <int NS>
   __device__ __forceinline__ void step(int slot0, u64 j) const {
     const u64 g = lo + j;
+    if (NS == 2 && opened) {  // eps0 + eps1 = x0 + x1 - A
+      own.p[0][j] = xf(0, g) + xf(1, g) - sq_secret(T, T.off + g);
+      return;
+    }
     const Sw d = sq_draw(T, T.off + g, NS == 2 || pid.v[slot0] == 0, false);
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
@@ -309,24 +318,30 @@ struct SqChainStep {
   u64 lo;
   int last;
   YF yf;
+  bool opened = false;  // pair evaluation: read / write the opened eps once (slot 0's outbox)
   __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
   __device__ void both(u64 j) const { step<2>(0, j); }
   template <int NS>
   __device__ __forceinline__ void step(int slot0, u64 j) const {
     const u64 g = lo + j;
     const bool p0 = NS == 2 || pid.v[slot0] == 0;
+    const bool op = NS == 2 && opened;
     const Sw dp = sq_draw(Tp, Tp.off + g, p0, true);
     Sw dn{0, 0, 0};
-    if (!last) dn = sq_draw(Tn, Tn.off + g, p0, false);
+    if (!last && !op) dn = sq_draw(Tn, Tn.off + g, p0, false);
+    const u64 oe = op ? ownp.p[0][j] : 0;
+    u64 ysum = 0;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
-      const u64 e = ownp.p[slot][j] + peerp.p[slot][j];
+      const u64 e = op ? oe : ownp.p[slot][j] + peerp.p[slot][j];
       u64 z = sq_share_c(party, dp) + (e * sq_share_a(party, dp)) * 2;
       if (party == 0) z += e * e;
       const u64 y = yf(slot, party, g, z);
-      if (!last) ownn.p[slot][j] = y - sq_share_a(party, dn);
+      if (op) ysum += y;
+      else if (!last) ownn.p[slot][j] = y - sq_share_a(party, dn);
     }
+    if (op && !last) ownn.p[0][j] = ysum - sq_secret(Tn, Tn.off + g);  // masks cancel in the open
   }
 };
 
@@ -340,6 +355,7 @@ void persistent_beaver_chain(Session& s, u64 n, const B0& build, const std::vect
 template <class XF, class YFF>
 void square_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr,
                   const std::vector<std::string>& tags, XF x0, YFF yf_for) {
+  const bool opened = adder_opened_wire(s);  // pair evaluation: opened wire between the rounds
   chunks = clamp_chunks(chunks, n);
   const int R = int(tr.size());
   const Pid2 pid = pids(s);
@@ -353,7 +369,10 @@ void square_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& t
       st.push_back(SqChainStep<YF0>{tr[r - 1].ew, r < R ? tr[r].ew : tr[r - 1].ew, pid, as_const(own_ptrs(op[r - 1])),
                                     peer_ptrs(op[r - 1]), r < R ? own_ptrs(op[r]) : Ptr2{{nullptr, nullptr}}, 0,
                                     r == R ? 1 : 0, yf_for(r - 1)});
-    persistent_beaver_chain(s, n, SqBuild2<XF>{tr[0].ew, pid, own_ptrs(op[0]), 0, x0}, st);
+    SqBuild2<XF> b0{tr[0].ew, pid, own_ptrs(op[0]), 0, x0};
+    b0.opened = opened;
+    for (auto& x : st) x.opened = opened;
+    persistent_beaver_chain(s, n, b0, st);
     for (int r = 0; r < R; ++r) s.account(n, Reduce::Sum, tags[r]);  // the reference's collective order
     s.check();
     return;
@@ -364,7 +383,9 @@ void square_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& t
   for (int k = 0; k < chunks; ++k) {
     const auto rg = chunk_range(n, chunks, k);
     hs[k] = s.begin_open(rg.second - rg.first, Reduce::Sum);
-    launch_ew(s.stream, s.n_local, rg.second - rg.first, SqBuild2<XF>{tr[0].ew, pid, own_ptrs(hs[k]), rg.first, x0});
+    SqBuild2<XF> b0{tr[0].ew, pid, own_ptrs(hs[k]), rg.first, x0};
+    b0.opened = opened;
+    launch_ew(s.stream, s.n_local, rg.second - rg.first, b0);
     s.post(hs[k], ctag(0, k));
   }
   using YF = decltype(yf_for(0));
@@ -378,6 +399,7 @@ void square_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& t
       SqChainStep<YF> st{tr[r - 1].ew, r < R ? tr[r].ew : tr[r - 1].ew, pid, as_const(own_ptrs(hs[k])),
                          peer_ptrs(hs[k]), r < R ? own_ptrs(next) : Ptr2{{nullptr, nullptr}}, rg.first,
                          r == R ? 1 : 0, yf_for(r - 1)};
+      st.opened = opened;
       launch_ew(s.stream, s.n_local, w, st);
       if (r < R) {
         hs[k] = std::move(next);
@@ -399,32 +421,47 @@ struct MulChainStep {
   u64 lo, w;
   int last;
   PV pv;
+  bool opened = false;  // pair evaluation: read / write the opened (eps, delta) once
   __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
   __device__ void both(u64 j) const { step<2>(0, j); }
   template <int NS>
   __device__ __forceinline__ void step(int slot0, u64 j) const {
     const u64 g = lo + j;
     const bool p0 = NS == 2 || pid.v[slot0] == 0;
+    const bool op = NS == 2 && opened;
     const Dw dp = ew_draw<true>(Tp, Tp.off + g, p0);
     Dw dn{0, 0, 0, 0, 0};
-    if (!last) dn = ew_draw<false>(Tn, Tn.off + g, p0);
+    if (!last) dn = op ? ew_secrets(Tn, Tn.off + g) : ew_draw<false>(Tn, Tn.off + g, p0);
+    u64 oe = 0, od = 0, sx = 0, sy = 0;
+    if (op) oe = ownp.p[0][j], od = ownp.p[0][w + j];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
-      const u64* o = ownp.p[slot];
-      const u64* q = peerp.p[slot];
-      const u64 e = o[j] + q[j], d = o[w + j] + q[w + j];
+      u64 e = oe, d = od;
+      if (!op) {
+        const u64* o = ownp.p[slot];
+        const u64* q = peerp.p[slot];
+        e = o[j] + q[j], d = o[w + j] + q[w + j];
+      }
       u64 a, b, c;
       ew_share<true>(Tp, party, dp, a, b, c);
       u64 z = c + (e * b + d * a);
       if (party == 0) z += e * d;
       const u64 v = pv.val(slot, party, g, z);
       if (!last) {
-        u64 an, bn, cn;
-        ew_share<false>(Tn, party, dn, an, bn, cn);
-        ownn.p[slot][j] = pv.nx(slot, g, v) - an;
-        ownn.p[slot][w + j] = pv.ny(slot, g, v) - bn;
+        if (op) {
+          sx += pv.nx(slot, g, v), sy += pv.ny(slot, g, v);
+        } else {
+          u64 an, bn, cn;
+          ew_share<false>(Tn, party, dn, an, bn, cn);
+          ownn.p[slot][j] = pv.nx(slot, g, v) - an;
+          ownn.p[slot][w + j] = pv.ny(slot, g, v) - bn;
+        }
       }
+    }
+    if (op && !last) {  // a0 + a1 = A, b0 + b1 = B
+      ownn.p[0][j] = sx - dn.A;
+      ownn.p[0][w + j] = sy - dn.B;
     }
   }
 };
@@ -434,6 +471,7 @@ struct MulChainStep {
 template <class XF, class YF, class PVF>
 void mul_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, const std::vector<std::string>& tags,
                XF x0, YF y0, PVF pv_for) {
+  const bool opened = adder_opened_wire(s);  // pair evaluation: opened wire between the rounds
   chunks = clamp_chunks(chunks, n);
   const int R = int(tr.size());
   const Pid2 pid = pids(s);
@@ -448,7 +486,10 @@ void mul_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, 
                                      as_const(own_ptrs(op[r - 1])), peer_ptrs(op[r - 1]),
                                      r < R ? own_ptrs(op[r]) : Ptr2{{nullptr, nullptr}}, 0, n, r == R ? 1 : 0,
                                      pv_for(r - 1)});
-    persistent_beaver_chain(s, n, MulBuild<XF, YF>{tr[0].ew, pid, own_ptrs(op[0]), 0, n, x0, y0}, st);
+    MulBuild<XF, YF> b0{tr[0].ew, pid, own_ptrs(op[0]), 0, n, x0, y0};
+    b0.opened = opened;
+    for (auto& x : st) x.opened = opened;
+    persistent_beaver_chain(s, n, b0, st);
     for (int r = 0; r < R; ++r) s.account(2 * n, Reduce::Sum, tags[r]);
     s.check();
     return;
@@ -460,7 +501,9 @@ void mul_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, 
     const auto rg = chunk_range(n, chunks, k);
     const size_t w = rg.second - rg.first;
     hs[k] = s.begin_open(2 * w, Reduce::Sum);
-    launch_ew(s.stream, s.n_local, w, MulBuild<XF, YF>{tr[0].ew, pid, own_ptrs(hs[k]), rg.first, w, x0, y0});
+    MulBuild<XF, YF> b0{tr[0].ew, pid, own_ptrs(hs[k]), rg.first, w, x0, y0};
+    b0.opened = opened;
+    launch_ew(s.stream, s.n_local, w, b0);
     s.post(hs[k], ctag(0, k));
   }
   using PV = decltype(pv_for(0));
@@ -474,6 +517,7 @@ void mul_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, 
       MulChainStep<PV> st{tr[r - 1].ew, r < R ? tr[r].ew : tr[r - 1].ew, pid, as_const(own_ptrs(hs[k])),
                           peer_ptrs(hs[k]), r < R ? own_ptrs(next) : Ptr2{{nullptr, nullptr}}, rg.first, w,
                           r == R ? 1 : 0, pv_for(r - 1)};
+      st.opened = opened;
       launch_ew(s.stream, s.n_local, w, st);
       if (r < R) {
         hs[k] = std::move(next);
@@ -498,19 +542,32 @@ struct MixedChainStep {
   u64 lo, w;
   int last;
   PV pv;
+  bool opened = false;  // pair evaluation: read / write the opened payload once
   __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
   __device__ void both(u64 j) const { step<2>(0, j); }
   template <int NS>
   __device__ __forceinline__ void step(int slot0, u64 j) const {
     const u64 g = lo + j;
     const bool p0 = NS == 2 || pid.v[slot0] == 0;
+    const bool op = NS == 2 && opened;
     Sw sp{0, 0, 0}, sn{0, 0, 0};
     Dw dp{0, 0, 0, 0, 0}, dn{0, 0, 0, 0, 0};
     if (psq) sp = sq_draw(Tp, Tp.off + g, p0, true);
     else dp = ew_draw<true>(Tp, Tp.off + g, p0);
     if (!last) {
-      if (nsq) sn = sq_draw(Tn, Tn.off + g, p0, false);
-      else dn = ew_draw<false>(Tn, Tn.off + g, p0);
+      if (op) {  // the secrets only: the masks cancel in the open
+        if (nsq) sn.A = sq_secret(Tn, Tn.off + g);
+        else dn = ew_secrets(Tn, Tn.off + g);
+      } else if (nsq) {
+        sn = sq_draw(Tn, Tn.off + g, p0, false);
+      } else {
+        dn = ew_draw<false>(Tn, Tn.off + g, p0);
+      }
+    }
+    u64 oe = 0, od = 0, sx = 0, sy = 0;
+    if (op) {
+      oe = ownp.p[0][j];
+      if (!psq) od = ownp.p[0][w + j];
     }
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
@@ -519,11 +576,11 @@ struct MixedChainStep {
       const u64* q = peerp.p[slot];
       u64 z;
       if (psq) {
-        const u64 e = o[j] + q[j];
+        const u64 e = op ? oe : o[j] + q[j];
         z = sq_share_c(party, sp) + (e * sq_share_a(party, sp)) * 2;
         if (party == 0) z += e * e;
       } else {
-        const u64 e = o[j] + q[j], d = o[w + j] + q[w + j];
+        const u64 e = op ? oe : o[j] + q[j], d = op ? od : o[w + j] + q[w + j];
         u64 a, b, c;
         ew_share<true>(Tp, party, dp, a, b, c);
         z = c + (e * b + d * a);
@@ -531,7 +588,10 @@ struct MixedChainStep {
       }
       const u64 v = pv.val(slot, party, g, z);
       if (!last) {
-        if (nsq) {
+        if (op) {
+          sx += pv.nx(slot, g, v);
+          if (!nsq) sy += pv.ny(slot, g, v);
+        } else if (nsq) {
           ownn.p[slot][j] = pv.nx(slot, g, v) - sq_share_a(party, sn);
         } else {
           u64 an, bn, cn;
@@ -539,6 +599,14 @@ struct MixedChainStep {
           ownn.p[slot][j] = pv.nx(slot, g, v) - an;
           ownn.p[slot][w + j] = pv.ny(slot, g, v) - bn;
         }
+      }
+    }
+    if (op && !last) {
+      if (nsq) {
+        ownn.p[0][j] = sx - sn.A;
+      } else {
+        ownn.p[0][j] = sx - dn.A;
+        ownn.p[0][w + j] = sy - dn.B;
       }
     }
   }
@@ -549,6 +617,7 @@ struct MixedChainStep {
 template <class XF, class YF, class PVF>
 void mixed_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, const std::vector<int>& sq,
                  const std::vector<std::string>& tags, XF x0, YF y0, PVF pv_for) {
+  const bool opened = adder_opened_wire(s);  // pair evaluation: opened wire between the rounds
   chunks = clamp_chunks(chunks, n);
   const int R = int(tr.size());
   const Pid2 pid = pids(s);
@@ -564,10 +633,16 @@ void mixed_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr
                                        pid, as_const(own_ptrs(op[r - 1])), peer_ptrs(op[r - 1]),
                                        r < R ? own_ptrs(op[r]) : Ptr2{{nullptr, nullptr}}, 0, n, r == R ? 1 : 0,
                                        pv_for(r - 1)});
-    if (sq[0])
-      persistent_beaver_chain(s, n, SqBuild2<XF>{tr[0].ew, pid, own_ptrs(op[0]), 0, x0}, st);
-    else
-      persistent_beaver_chain(s, n, MulBuild<XF, YF>{tr[0].ew, pid, own_ptrs(op[0]), 0, n, x0, y0}, st);
+    for (auto& x : st) x.opened = opened;
+    if (sq[0]) {
+      SqBuild2<XF> b0{tr[0].ew, pid, own_ptrs(op[0]), 0, x0};
+      b0.opened = opened;
+      persistent_beaver_chain(s, n, b0, st);
+    } else {
+      MulBuild<XF, YF> b0{tr[0].ew, pid, own_ptrs(op[0]), 0, n, x0, y0};
+      b0.opened = opened;
+      persistent_beaver_chain(s, n, b0, st);
+    }
     for (int r = 0; r < R; ++r) s.account(words(r, n), Reduce::Sum, tags[r]);
     s.check();
     return;
@@ -577,10 +652,15 @@ void mixed_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr
     const auto rg = chunk_range(n, chunks, k);
     const size_t w = rg.second - rg.first;
     hs[k] = s.begin_open(words(0, w), Reduce::Sum);
-    if (sq[0])
-      launch_ew(s.stream, s.n_local, w, SqBuild2<XF>{tr[0].ew, pid, own_ptrs(hs[k]), rg.first, x0});
-    else
-      launch_ew(s.stream, s.n_local, w, MulBuild<XF, YF>{tr[0].ew, pid, own_ptrs(hs[k]), rg.first, w, x0, y0});
+    if (sq[0]) {
+      SqBuild2<XF> b0{tr[0].ew, pid, own_ptrs(hs[k]), rg.first, x0};
+      b0.opened = opened;
+      launch_ew(s.stream, s.n_local, w, b0);
+    } else {
+      MulBuild<XF, YF> b0{tr[0].ew, pid, own_ptrs(hs[k]), rg.first, w, x0, y0};
+      b0.opened = opened;
+      launch_ew(s.stream, s.n_local, w, b0);
+    }
     s.post(hs[k], ctag(0, k));
   }
   using PV = decltype(pv_for(0));
@@ -595,6 +675,7 @@ void mixed_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr
                             as_const(own_ptrs(hs[k])), peer_ptrs(hs[k]),
                             r < R ? own_ptrs(next) : Ptr2{{nullptr, nullptr}}, rg.first, w, r == R ? 1 : 0,
                             pv_for(r - 1)};
+      st.opened = opened;
       launch_ew(s.stream, s.n_local, w, st);
       if (r < R) {
         hs[k] = std::move(next);

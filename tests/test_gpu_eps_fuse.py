@@ -19,7 +19,7 @@ import numpy as np
 import paper_2209_13643_b200 as mp
 PHI = 0x9E3779B97F4A7C15
 out = {}
-for name in ["mlp", "lenet5", "toy_resnet"]:
+for name in ["mlp", "lenet5", "toy_resnet", "toy_bert"]:
     g = mp.ModelGraph.from_json(name)
     s = mp.Session(device=0, n_local=2, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
     ex = mp.SecureExecutor(s, g, public_weights=False, pipelined=True, chunks=2)
