@@ -505,6 +505,45 @@ struct EpsIm2colPair {
     }
   }
 };
+// Fused in-device open of the im2col eps (Open::summed): E[r][c] = x0[src] + x1[src] - A[r][c].
+// A warp owns an im2col row r = (n, oh, ow) and walks its K = C*k*k columns 32 at a time; the
+// column decomposition c -> (x offset, ki, kj) comes from a per-block shared table built once,
+// so an element costs one table read, two gathers, one dealer draw (the counter advances by
+// 32*phi per step) and a coalesced store — instead of five divisions per element.
+__global__ void __launch_bounds__(256) eps_im2col_summed_kernel(MmTriple mm, ConvGeom g, const u64* __restrict__ x0,
+                                                               const u64* __restrict__ x1, u64* __restrict__ out,
+                                                               u32 rows, u64 a_off) {
+  extern __shared__ int2 tab[];  // per column: {ci*H*W + ki*W + kj, ki | kj << 16}
+  pdl_enter();
+  const u32 K = g.C * g.k * g.k, kk = g.k * g.k;
+  for (u32 c = threadIdx.x; c < K; c += blockDim.x) {
+    const u32 ci = c / kk, rem = c - ci * kk, ki = rem / g.k, kj = rem - ki * g.k;
+    tab[c] = make_int2(int(ci * g.H * g.W + ki * g.W + kj), int(ki | (kj << 16)));
+  }
+  __syncthreads();
+  const u64 key = tkey(mm.key, mm.kp) + mm.pA;
+  const u32 lane = threadIdx.x & 31;
+  const u32 wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const u64 chw = u64(g.C) * g.H * g.W;
+  for (u32 r = wg; r < rows; r += nw) {
+    const u32 ow = r % g.OW, t = r / g.OW, oh = t % g.OH, n = t / g.OH;
+    const int ih0 = int(oh * g.stride) - int(g.pad), iw0 = int(ow * g.stride) - int(g.pad);
+    const long long xb = (long long)(u64(n) * chw) + (long long)ih0 * g.W + iw0;
+    const u64 j0 = u64(r) * K;
+    u64 z = key + (a_off + j0 + lane) * kPhi;
+    for (u32 c = lane; c < K; c += 32, z += 32 * kPhi) {
+      const int2 e = tab[c];
+      const int ih = ih0 + (e.y & 0xFFFF), iw = iw0 + (e.y >> 16);
+      u64 v = 0;
+      if (unsigned(ih) < g.H && unsigned(iw) < g.W) {
+        const long long src = xb + e.x;
+        v = x0[src] + x1[src];
+      }
+      out[j0 + c] = v - mix64(z);  // eps0 + eps1 = x0 + x1 - (a0 + a1), a0 + a1 = A
+    }
+  }
+}
+
 template <class F>
 __global__ void __launch_bounds__(256) strip_kernel(u64 n, F f) {
   pdl_enter();
@@ -514,6 +553,25 @@ __global__ void __launch_bounds__(256) strip_kernel(u64 n, F f) {
 
 void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const ConvGeom& gm, size_t a_off,
                       size_t na, Open& o, const DT* aops) {
+  const u32 Kc = gm.C * gm.k * gm.k;
+  if (o.summed && s.n_local == 2 && !aops && a_off % Kc == 0 && na % Kc == 0 && Kc * sizeof(int2) <= 96 * 1024) {
+    const u32 rows = u32(na / Kc);
+    const size_t smem = Kc * sizeof(int2);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+      MPCG_CUDA(cudaFuncSetAttribute(eps_im2col_summed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      attr = smem;
+    }
+    u64 blocks = (u64(rows) + 7) / 8;
+    const u64 cap = u64(kSms) * 8;
+    blocks = blocks > cap ? cap : (blocks < 1 ? 1 : blocks);
+    cudaEvent_t pe;
+    probe_begin(s.stream, &pe);
+    launch_pdl(eps_im2col_summed_kernel, dim3(unsigned(blocks)), dim3(256), smem, s.stream, t.mm, gm, x[0], x[1],
+               o.own(0), rows, u64(a_off));
+    probe_end(s.stream, pe);
+    return;
+  }
   if (a_off == 0 && na < (u64(1) << 32)) {  // call-local indices fit the 32-bit fast division
     EpsIm2colPair f{t.mm, pids(s), own_ptrs(o),
                     Ptr2{{aops ? aops->s[0] : nullptr, aops && s.n_local == 2 ? aops->s[1] : nullptr}},
