@@ -251,6 +251,9 @@ void SecureExecutor::prepare(size_t i) {
     if (s_.n_local == 1) op.dbuf_in = Block::persistent(nb + 1);
   }
   Open d = s_.begin_open(nb, Reduce::Sum, op.dbuf_out, op.dbuf_in);
+  // fused in-device open of delta, on the same condition as eps's (weight_matmul)
+  const size_t M = op.x_shape[0], K = op.x_shape[1];
+  d.summed = beaver_combine_fuses_eps(s_, 1, u32(M), u32(nb / K), u32(K));
   delta_build_mem(s_, t, W.s, nb, d);
   s_.post(d, op.tag + ".delta");
   op.triple = t;

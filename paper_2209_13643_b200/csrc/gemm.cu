@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(256) ring_gemv(GemmArgs a) {
       const u64 idx = u64(k0 + kk) * N + n;
       const u64 B = needB ? mm_B(S.mm, S.boff + idx) : 0;
       const u64 rB = needRB ? mm_rB(S.mm, S.boff + idx) : 0;
-      const u64 F = needF ? __ldg(Fo + idx) + __ldg(Fp + idx) : 0;
+      const u64 F = needF ? (Fp ? __ldg(Fo + idx) + __ldg(Fp + idx) : __ldg(Fo + idx)) : 0;
 #pragma unroll
       for (int g = 0; g < 3; ++g) {
         if (g >= S.nseg) break;
@@ -387,6 +387,11 @@ static void delta_build(Session& s, const Triple& t, size_t nb, Open& o, YF yf) 
   const Pid2 pid = pids(s);
   const Ptr2 own = own_ptrs(o);
   const MmTriple mm = t.mm;
+  if (o.summed) {  // fused in-device open: delta0 + delta1 = y0 + y1 - B (the r_B masks cancel)
+    if (s.n_local != 2) throw Error(kUsageError, "summed delta open needs both slots");
+    launch_ew(s.stream, 1, nb, [=] __device__(int, u64 j) { own.p[0][j] = yf(0, j) + yf(1, j) - mm_B(mm, j); });
+    return;
+  }
   launch_ew(s.stream, s.n_local, nb, [=] __device__(int slot, u64 j) {
     own.p[slot][j] = yf(slot, j) - mm_b_share(mm, pid.v[slot], j);
   });
@@ -608,6 +613,7 @@ void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const 
 
 // R operands per slot (3 x nb words): p0 {B, b0+F, F}, p1 {r_B, F}; F = own + peer delta.
 DT prepare_R(Session& s, const Triple& t, const Open& d, size_t nb) {
+  if (d.summed) throw Error(kUsageError, "prepare_R: summed delta");
   DT r = s.alloc(Shape{3, nb});
   const Pid2 pid = pids(s);
   const CPtr2 ow = as_const(own_ptrs(d)), pe = peer_ptrs(d);
@@ -814,8 +820,8 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
     const u64* E0 = e.summed ? e.own(0) : e.own(i);
     const u64* E1 = e.summed ? nullptr : e.peer(i);
     const int ek = e.summed ? kOpMem : kOpSum;  // E = own + peer, or already summed
-    const u64* F0 = d.own(i) + rboff;
-    const u64* F1 = d.peer(i) + rboff;
+    const u64* F0 = (d.summed ? d.own(0) : d.own(i)) + rboff;
+    const u64* F1 = d.summed ? nullptr : d.peer(i) + rboff;  // null: F summed at build time
     S.out = out[i] + out_off;
     S.bias = ep.bias[i];
     S.ckey = t.mm.key;

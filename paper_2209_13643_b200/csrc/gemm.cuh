@@ -75,15 +75,18 @@ __device__ __forceinline__ u64 load_l(const GemmSlotArgs& S, int sg, u64 idx) {
     default: return mm_rA(S.mm, S.aoff + idx);
   }
 }
+// The opened F = own + peer delta, or (R2 null: the open summed at build time) R alone.
+__device__ __forceinline__ u64 load_f(const GemmSlotArgs& S, int sg, u64 idx) {
+  return S.R2[sg] ? S.R[sg][idx] + S.R2[sg][idx] : S.R[sg][idx];
+}
 __device__ __forceinline__ u64 load_r(const GemmSlotArgs& S, int sg, u64 idx) {
   switch (S.rk[sg]) {
     case kOpMem: return S.R[sg][idx];
-    case kOpSum: return S.R[sg][idx] + S.R2[sg][idx];
+    case kOpSum: return load_f(S, sg, idx);
     case kOpB: return mm_B(S.mm, S.boff + idx);
-    case kOpB0F:
-      return (mm_B(S.mm, S.boff + idx) - mm_rB(S.mm, S.boff + idx)) + (S.R[sg][idx] + S.R2[sg][idx]);
-    case kOpBF: return mm_B(S.mm, S.boff + idx) + (S.R[sg][idx] + S.R2[sg][idx]);
-    case kOpNegSum: return u64(0) - (S.R[sg][idx] + S.R2[sg][idx]);
+    case kOpB0F: return (mm_B(S.mm, S.boff + idx) - mm_rB(S.mm, S.boff + idx)) + load_f(S, sg, idx);
+    case kOpBF: return mm_B(S.mm, S.boff + idx) + load_f(S, sg, idx);
+    case kOpNegSum: return u64(0) - load_f(S, sg, idx);
     default: return mm_rB(S.mm, S.boff + idx);
   }
 }
