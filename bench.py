@@ -369,8 +369,11 @@ def main():
     int8_peak, int8_src = measure_int8_peak()
     # algorithmic units per class: bytes for the HBM-bound protocol rounds, ring MACs
     # for the GEMM (x36 int8 MACs = 72 int8 ops each, the limb-pair products of the tcgen05 path)
-    notes = {"adder_round": "SPK level round (settle r, issue r+1): 96 B/elem/party = 2x32 B wire + 8x(2 in + 2 out)",
-             "beaver": "Beaver mul/square rounds incl. fused exp/Newton chains: 56 / 32 B/elem/party per op",
+    notes = {"adder_round": "SPK level round (settle r, issue r+1), opened wire (pair evaluation): 64 B/elem/party = "
+                            "32 B opened value written + read once per element pair + 8x(2 in + 2 out) state "
+                            "(per-slot form: 96 B = 2x32 B wire + state)",
+             "beaver": "Beaver mul/square rounds incl. fused exp/Newton chains: 40 (opened wire) or 56 / 32 B/elem/party "
+                       "per op",
              "chain": "persistent compare-and-select chain (ReLU/tournament): 512 B/elem/party",
              "gemm": "ring GEMM main kernel: 72 int8 ops per ring MAC (36 limb-pair MACs), packing excluded"}
     rooflines = []
