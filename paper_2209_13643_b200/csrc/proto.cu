@@ -256,12 +256,39 @@ DT a2b_mask(Session& s, size_t n, XF xf, Open& o) {
   return keep;
 }
 
+// The a2b mask folded into the adder's generate round (pair evaluation): the adder operands
+// PartX / PartY computed from x and the two parties' mask draws directly instead of read back
+// from keep = x ^ r and the peer's mask outbox. Operand y = 0 (X): party 0 holds x ^ r and
+// party 1 the peer's r; y = 1 (Y): the other way round.
+template <class XF>
+struct MaskedPart {
+  Pid2 pid;
+  u64 k0, k1;
+  Session::MaskRef mr;
+  XF xf;
+  int y;
+  __device__ u64 operator()(int slot, u64 g) const {
+    const u64 c = tkey(mr.base, mr.bp) + 1 + g;
+    if ((pid.v[slot] == 0) == (y == 0)) return xf(slot, g) ^ drw(slot == 0 ? k0 : k1, c);  // keep
+    return drw(slot == 0 ? k1 : k0, c);  // the peer slot's mask r
+  }
+};
+
 template <class XF, class FFL, class POST = NoPost>
 void a2b_op(Session& s, size_t n, const AdderOptions& opt, const std::string& tag, XF xf, FFL ffl,
             POST post = NoPost{}) {
+  const Pid2 pid = pids(s);
+  if (adder_opened_wire(s)) {  // one thread plays both parties: no mask kernel, no keep tensor
+    const Session::MaskRef mr = s.take_mask(n);
+    Open o = s.begin_open(n, Reduce::Sum);
+    s.post(o, "", /*p2p=*/true);  // the mask exchange, accounted as the reference sends it
+    s.wait(o);
+    adder_op(s, n, opt, tag + ".add1", MaskedPart<XF>{pid, s.mask_key[0], s.mask_key[1], mr, xf, 0},
+             MaskedPart<XF>{pid, s.mask_key[0], s.mask_key[1], mr, xf, 1}, ffl, post);
+    return;
+  }
   Open o;
   DT keep = a2b_mask(s, n, xf, o);
-  const Pid2 pid = pids(s);
   adder_op(s, n, opt, tag + ".add1", PartX{pid, cptrs(keep), peer_ptrs(o)}, PartY{pid, cptrs(keep), peer_ptrs(o)},
            ffl, post);
 }
