@@ -199,6 +199,37 @@ void mul_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::stri
   }
 }
 
+// One warp per row: of(slot, row, sum_j vf(slot, row*L + j)) with wrapping u64 adds (exact
+// and order-independent mod 2^64). Rows are contiguous, so lanes read coalesced 256 B runs.
+template <class VF, class OF>
+__global__ void __launch_bounds__(256) row_reduce_kernel(u64 rows, u32 L, VF vf, OF of) {
+  pdl_enter();
+  const int slot = blockIdx.y;
+  const unsigned lane = threadIdx.x & 31;
+  const u64 nw = u64(gridDim.x) * (blockDim.x / 32);
+  for (u64 r = (blockIdx.x * u64(blockDim.x) + threadIdx.x) / 32; r < rows; r += nw) {
+    u64 acc = 0;
+    for (u32 j = lane; j < L; j += 32) acc += vf(slot, r * L + j);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) of(slot, r, acc);
+  }
+}
+
+template <class VF, class OF>
+void row_reduce(Session& s, u64 rows, u32 L, VF vf, OF of) {
+  if (rows == 0) return;
+  u64 blocks = (rows * 32 + 255) / 256;
+  const u64 cap = u64(kSms) * 8;
+  blocks = blocks > cap ? cap : blocks;
+  cudaEvent_t pe;
+  probe_begin(s.stream, &pe);
+  launch_pdl(row_reduce_kernel<VF, OF>, dim3(unsigned(blocks), s.n_local), dim3(256), 0, s.stream, rows, L, vf, of);
+  probe_end(s.stream, pe);
+  s.check();
+}
+
+
 // ---------------------------------------------------------------- Beaver square
 template <class XF>
 struct SqBuild {

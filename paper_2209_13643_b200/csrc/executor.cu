@@ -353,11 +353,11 @@ DT SecureExecutor::attention(const LayerSpec& l, const DT& x, const Shape& in_sh
     const Ptr2 dst = ptrs(qkvh);
     const u32 Tt = u32(T), D = u32(d), H = u32(heads), DH = u32(dh);
     const u64 per = B * heads * T * dh;
-    launch_ew(s_.stream, s_.n_local, 3 * per, [=] __device__(int slot, u64 i) {
-      const u32 part = u32(i / per);
-      const u64 r = i - part * per;
-      const u32 j = u32(r % DH), t = u32((r / DH) % Tt), h = u32((r / (u64(DH) * Tt)) % H),
-                b = u32(r / (u64(DH) * Tt * H));
+    if (3 * per >= (u64(1) << 32)) throw Error(kShapeError, "attention: activation too large");
+    const u32 per32 = u32(per);
+    launch_ew(s_.stream, s_.n_local, 3 * per, [=] __device__(int slot, u64 i64) {  // 32-bit index math
+      const u32 i = u32(i64), part = i / per32, r = i - part * per32;
+      const u32 rj = r / DH, j = r - rj * DH, rt = rj / Tt, t = rj - rt * Tt, b = rt / H, h = rt - b * H;
       dst.p[slot][i] = src.p[slot][(u64(b) * Tt + t) * 3 * D + part * D + h * DH + j];
     });
   }
@@ -375,19 +375,28 @@ DT SecureExecutor::attention(const LayerSpec& l, const DT& x, const Shape& in_sh
     v.s[1] = qkvh.s[1] + 2 * per;
   }
   DT scores = beaver_matmul(s_, q, k, true, l.name + ".qk", chunks_for(s_, B * heads * T * T));
-  scores = truncate_shares(s_, scores, g_.frac_bits);
-  scores = scale_and_rescale(scores, 1.0 / std::sqrt(static_cast<double>(dh)));
+  {  // truncate, then scale_and_rescale by 1/sqrt(dh), in one local pass (same values as two)
+    const u64 kc = encode_fixed(1.0 / std::sqrt(static_cast<double>(dh)), g_.frac_bits);
+    const int f = g_.frac_bits;
+    DT z = s_.alloc(scores.shape, scores.scale);
+    const CPtr2 xp = cptrs(scores);
+    const Ptr2 zp = ptrs(z);
+    launch_ew(s_.stream, s_.n_local, scores.numel(),
+              [=] __device__(int slot, u64 i) { zp.p[slot][i] = sar64(sar64(xp.p[slot][i], f) * kc, f); });
+    scores = z;
+  }
   DT probs = softmax_shares(s_, scores, T, l.name + ".softmax");
   DT mixed = beaver_matmul(s_, probs, v, false, l.name + ".av", chunks_for(s_, B * heads * T * dh));
-  mixed = truncate_shares(s_, mixed, g_.frac_bits);
-  DT merged = s_.alloc(Shape{B * T, d}, mixed.scale);  // merge_heads
+  DT merged = s_.alloc(Shape{B * T, d}, mixed.scale);  // truncate + merge_heads in one local pass
   {
     const CPtr2 src = cptrs(mixed);
     const Ptr2 dst = ptrs(merged);
     const u32 Tt = u32(T), D = u32(d), H = u32(heads), DH = u32(dh);
-    launch_ew(s_.stream, s_.n_local, B * T * d, [=] __device__(int slot, u64 i) {
-      const u32 j = u32(i % DH), h = u32((i / DH) % H), t = u32((i / D) % Tt), b = u32(i / (u64(D) * Tt));
-      dst.p[slot][i] = src.p[slot][((u64(b) * H + h) * Tt + t) * DH + j];
+    const int f = g_.frac_bits;
+    if (B * T * d >= (u64(1) << 32)) throw Error(kShapeError, "attention: activation too large");
+    launch_ew(s_.stream, s_.n_local, B * T * d, [=] __device__(int slot, u64 i64) {
+      const u32 i = u32(i64), q1 = i / DH, j = i - q1 * DH, q2 = q1 / H, h = q1 - q2 * H, b = q2 / Tt, t = q2 - b * Tt;
+      dst.p[slot][i] = sar64(src.p[slot][((u64(b) * H + h) * Tt + t) * DH + j], f);
     });
   }
   DT out = weight_matmul(proj_op, merged, nullptr, false, Shape{B * T, d});

@@ -846,6 +846,11 @@ struct SrcBcast {  // r[g / L]
 };
 }  // namespace
 
+struct OutRowStore {  // out[r] = acc
+  Ptr2 out;
+  __device__ void operator()(int slot, u64 r, u64 acc) const { out.p[slot][r] = acc; }
+};
+
 DT softmax_shares(Session& s, const DT& x, size_t L, const std::string& tag) {
   const size_t outer = x.numel() / L;
   const size_t n = x.numel();
@@ -854,17 +859,7 @@ DT softmax_shares(Session& s, const DT& x, size_t L, const std::string& tag) {
   DT e = s.alloc(Shape{outer, L}, x.scale);  // exp(x - max), the centring fused into the exp chain
   exp_chain(s, Shape{outer, L}, tag + ".exp", 7, SrcSubRowMax{cptrs(x), cptrs(mx), u32(L)}, OutStore{ptrs(e)});
   DT rowsum = s.alloc(Shape{outer, 1}, x.scale);
-  {
-    const CPtr2 ep = cptrs(e);
-    const Ptr2 rp = ptrs(rowsum);
-    const u64 LL = L;
-    launch_ew(s.stream, s.n_local, outer, [=] __device__(int slot, u64 o) {
-      u64 acc = 0;
-      const u64* row = ep.p[slot] + o * LL;
-      for (u64 j = 0; j < LL; ++j) acc += row[j];
-      rp.p[slot][o] = acc;
-    });
-  }
+  row_reduce(s, outer, u32(L), SrcMem{cptrs(e)}, OutRowStore{ptrs(rowsum)});  // warp per row
   DT r = reciprocal_shares(s, rowsum, tag + ".recip");
   Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Arith, Shape{outer, L}), tag + ".scale");
   t.mark_consumed();
