@@ -230,68 +230,6 @@ void row_reduce(Session& s, u64 rows, u32 L, VF vf, OF of) {
 }
 
 
-// ---------------------------------------------------------------- Beaver square
-template <class XF>
-struct SqBuild {
-  EwTriple T;
-  Pid2 pid;
-  Ptr2 own;
-  u64 lo;
-  XF xf;
-  __device__ void operator()(int slot, u64 j) const {
-    const u64 g = lo + j;
-    own.p[slot][j] = xf(slot, g) - sq_a(T, pid.v[slot], T.off + g);
-  }
-};
-template <class PF>
-struct SqCombine {
-  EwTriple T;
-  Pid2 pid;
-  CPtr2 own, peer;
-  u64 lo;
-  PF pf;
-  __device__ void operator()(int slot, u64 j) const {
-    const int party = pid.v[slot];
-    const u64 g = lo + j;
-    const u64 e = own.p[slot][j] + peer.p[slot][j];
-    u64 a, c;
-    sq_ac(T, party, T.off + g, a, c);
-    u64 z = c + (e * a) * 2;
-    if (party == 0) z += e * e;
-    pf(slot, party, g, z);
-  }
-};
-
-template <class XF, class PF>
-void square_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::string& tag, XF xf, PF pf) {
-  chunks = clamp_chunks(chunks, m);
-  std::vector<Open> opens(static_cast<size_t>(chunks));
-  const Pid2 pid = pids(s);
-  // beaver_square = 2 x 8 B wire + 8 x (1 in + 1 out) = 32 B/elem/party over build + combine
-  ClassScope cs(kClsBeaver, 16.0 * double(m / chunks) * s.n_local);
-  for (int k = 0; k < chunks; ++k) {
-    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
-    opens[k] = s.begin_open(hi - lo, Reduce::Sum);
-    launch_ew(s.stream, s.n_local, hi - lo, SqBuild<XF>{T, pid, own_ptrs(opens[k]), lo, xf});
-    s.post(opens[k], chunks == 1 ? tag : tag + ".chunk" + std::to_string(k));
-  }
-  for (int k = 0; k < chunks; ++k) {
-    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
-    s.wait(opens[k]);
-    launch_ew(s.stream, s.n_local, hi - lo,
-              SqCombine<PF>{T, pid, as_const(own_ptrs(opens[k])), peer_ptrs(opens[k]), lo, pf});
-    s.check();
-  }
-}
-
-// ---------------------------------------------------------------- fused Beaver chains
-// A chain of dependent Beaver rounds (exp's repeated squaring, the reciprocal's Newton
-// steps) runs as "combine round r, build round r+1" in ONE pass per element, exactly like
-// the SPK adder rounds: the intermediate value never round-trips through HBM and the kernel
-// count halves. Posts keep the reference's collective order: every lane of round r is
-// posted before any lane of round r+1 (lane k of r+1 is posted right after lane k of r is
-// combined), and the sequence numbers are assigned at post time.
-
 // Square-triple draws of element g: A (party 0 only), r_A, r_C (H/sharing/triple.hpp:96-114).
 struct Sw {
   u64 A, ra, rc;
@@ -311,6 +249,101 @@ __device__ __forceinline__ u64 sq_secret(const EwTriple& t, u64 g) {
   return mix64(tkey(t.key, t.kp) + t.pA + g * kPhi);
 }
 __device__ __forceinline__ u64 sq_share_c(int party, const Sw& d) { return party ? d.rc : d.A * d.A - d.rc; }
+
+// ---------------------------------------------------------------- Beaver square
+template <class XF>
+struct SqBuild {
+  EwTriple T;
+  Pid2 pid;
+  Ptr2 own;
+  u64 lo;
+  XF xf;
+  bool opened = false;  // pair evaluation: the opened eps once (slot 0's outbox)
+  __device__ void operator()(int slot, u64 j) const {
+    const u64 g = lo + j;
+    own.p[slot][j] = xf(slot, g) - sq_a(T, pid.v[slot], T.off + g);
+  }
+  __device__ void both(u64 j) const {
+    const u64 g = lo + j;
+    if (opened) {  // eps0 + eps1 = x0 + x1 - A
+      own.p[0][j] = xf(0, g) + xf(1, g) - mix64(tkey(T.key, T.kp) + T.pA + (T.off + g) * kPhi);
+      return;
+    }
+    (*this)(0, j);
+    (*this)(1, j);
+  }
+};
+template <class PF>
+struct SqCombine {
+  EwTriple T;
+  Pid2 pid;
+  CPtr2 own, peer;
+  u64 lo;
+  PF pf;
+  bool opened = false;  // pair evaluation: read the opened eps once
+  __device__ void operator()(int slot, u64 j) const {
+    const int party = pid.v[slot];
+    const u64 g = lo + j;
+    const u64 e = own.p[slot][j] + peer.p[slot][j];
+    u64 a, c;
+    sq_ac(T, party, T.off + g, a, c);
+    u64 z = c + (e * a) * 2;
+    if (party == 0) z += e * e;
+    pf(slot, party, g, z);
+  }
+  __device__ void both(u64 j) const {
+    if (!opened) {
+      (*this)(0, j);
+      (*this)(1, j);
+      return;
+    }
+    const u64 g = lo + j;
+    const u64 e = own.p[0][j];
+    const Sw d = sq_draw(T, T.off + g, true, true);  // one draw set for both parties
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int slot = pair_slot<2>(pid, 0, k);
+      u64 z = sq_share_c(k, d) + (e * sq_share_a(k, d)) * 2;
+      if (k == 0) z += e * e;
+      pf(slot, k, g, z);
+    }
+  }
+};
+
+template <class XF, class PF>
+void square_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::string& tag, XF xf, PF pf) {
+  chunks = clamp_chunks(chunks, m);
+  std::vector<Open> opens(static_cast<size_t>(chunks));
+  const Pid2 pid = pids(s);
+  // beaver_square = 2 x 8 B wire + 8 x (1 in + 1 out) = 32 B/elem/party over build + combine
+  // (opened wire: 8 B written + read once per element pair = 24 B/elem/party)
+  const bool opened = adder_opened_wire(s);
+  ClassScope cs(kClsBeaver, (opened ? 12.0 : 16.0) * double(m / chunks) * s.n_local);
+  for (int k = 0; k < chunks; ++k) {
+    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
+    opens[k] = s.begin_open(hi - lo, Reduce::Sum);
+    SqBuild<XF> b{T, pid, own_ptrs(opens[k]), lo, xf};
+    b.opened = opened;
+    launch_ew(s.stream, s.n_local, hi - lo, b);
+    s.post(opens[k], chunks == 1 ? tag : tag + ".chunk" + std::to_string(k));
+  }
+  for (int k = 0; k < chunks; ++k) {
+    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
+    s.wait(opens[k]);
+    SqCombine<PF> c{T, pid, as_const(own_ptrs(opens[k])), peer_ptrs(opens[k]), lo, pf};
+    c.opened = opened;
+    launch_ew(s.stream, s.n_local, hi - lo, c);
+    s.check();
+  }
+}
+
+// ---------------------------------------------------------------- fused Beaver chains
+// A chain of dependent Beaver rounds (exp's repeated squaring, the reciprocal's Newton
+// steps) runs as "combine round r, build round r+1" in ONE pass per element, exactly like
+// the SPK adder rounds: the intermediate value never round-trips through HBM and the kernel
+// count halves. Posts keep the reference's collective order: every lane of round r is
+// posted before any lane of round r+1 (lane k of r+1 is posted right after lane k of r is
+// combined), and the sequence numbers are assigned at post time.
 
 // Build of the first square of a chain: payload eps = x - a (pair-evaluated).
 template <class XF>
