@@ -252,6 +252,7 @@ struct Tc2Args {
   u64 Rpk_b[2] = {0, 0};                    // bytes per batch (0 = shared across the batch)
   const char* Lpk[2] = {nullptr, nullptr};  // packed left operand (multi-N-tile shapes) or null
   u64 Lpk_b[2] = {0, 0};
+  u32 lmask[2] = {0, 0};  // segments whose left operand is in Lpk (all: fully packed; else hybrid)
   u32 nkb = 0;                              // K blocks of 32
   int vec = 0;                              // L row loads: 2 = 32-byte, 1 = 16-byte, 0 = scalar
   u32 ksplit = 1, kbper = 0;                // split-K over K blocks (partials summed by the epilogue kernel)
@@ -294,7 +295,11 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
   const int nseg = S.nseg;
   const u32 kb0 = split * P.kbper, kb1 = min(P.nkb, kb0 + P.kbper);  // this CTA's K blocks
   const u32 nst = (kb1 - kb0) * u32(nseg);
-  const bool packedL = P.Lpk[slot] != nullptr;
+  // left operand: fully packed (every segment bulk-copied), hybrid (the dealer-drawn segments
+  // packed once per layer, the memory segments loaded by the producers), or generated
+  const u32 lm = P.Lpk[slot] ? P.lmask[slot] : 0u;
+  const bool packedL = lm != 0 && lm == (1u << nseg) - 1;
+  const u32 npk = __popc(lm);
 
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) {
@@ -406,6 +411,13 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
         const u32 k0 = kb * kKB + u32(hf) * 16;
         for (int g = 0; g < nseg; ++g, ++it) {
           if (is_mem(g)) continue;
+          if ((lm >> g) & 1u) {  // hybrid: this stage's left operand is bulk-copied by the loader
+            const int stg = int(it % kStages);
+            if (it >= kStages) mbar_wait(&empty[stg], ((it / kStages) & 1) ^ 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[stg]);
+            continue;
+          }
           const int kind = S.lk[g];
           const u64 e0 = rowoff + k0;
           u64 v[16];
@@ -490,6 +502,12 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
         const bool fullv = rowok && k0 + kVW <= K;
         for (int g = 0; g < nseg; ++g, ++it) {
           const int stg = int(it % kStages);
+          if ((lm >> g) & 1u) {  // hybrid: bulk-copied by the loader
+            if (it >= kStages) mbar_wait(&empty[stg], ((it / kStages) & 1) ^ 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[stg]);
+            continue;
+          }
           u64 v[kVW];
           const int kind = S.lk[g];
           if (g == pf) {
@@ -543,16 +561,17 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
     if (lane == 0) {  // ---- bulk loader
       const char* Rb = P.Rpk[slot] + u64(b) * P.Rpk_b[slot] +
                        (u64(ntile) * P.nkb + kb0) * u64(nseg) * 8 * kB;
-      const char* Lb = packedL ? P.Lpk[slot] + u64(b) * P.Lpk_b[slot] +
-                                     (u64(blockIdx.y) * P.nkb + kb0) * u64(nseg) * 8 * kA
-                               : nullptr;
+      const char* Lb =
+          lm ? P.Lpk[slot] + u64(b) * P.Lpk_b[slot] + (u64(blockIdx.y) * P.nkb + kb0) * u64(npk) * 8 * kA : nullptr;
       for (u32 it = 0; it < nst; ++it) {
         const int stg = int(it % kStages);
         if (it >= kStages) mbar_wait(&empty[stg], ((it / kStages) & 1) ^ 1);
         char* sA = smem + stg * kStage;
-        mbar_arrive_tx(&full[stg], 8 * kB + (packedL ? 8 * kA : 0));
+        const u32 g = it % u32(nseg), kr = it / u32(nseg);
+        const bool pl = (lm >> g) & 1u;
+        mbar_arrive_tx(&full[stg], 8 * kB + (pl ? 8 * kA : 0));
         bulk_g2s(sA + 8 * kA, Rb + u64(it) * 8 * kB, 8 * kB, &full[stg]);
-        if (packedL) bulk_g2s(sA, Lb + u64(it) * 8 * kA, 8 * kA, &full[stg]);
+        if (pl) bulk_g2s(sA, Lb + (u64(kr) * npk + __popc(lm & ((1u << g) - 1))) * 8 * kA, 8 * kA, &full[stg]);
       }
     }
   } else {
@@ -638,12 +657,14 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
 // transposed, (b*sR + row*K + k).
 template <int BR>
 __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows, u32 nbatch, u32 nkb, char* out0,
-                                                  char* out1) {
+                                                  char* out1, u32 mask0, u32 mask1) {
   pdl_enter();
   const int slot = blockIdx.y;  // every local slot in one launch
   char* out = slot ? out1 : out0;
   const GemmSlotArgs& S = a.sl[slot];
-  const u32 K = a.K, N = a.N, nseg = u32(S.nseg);
+  // packed segments: all (right operand, full left pack) or the masked ones (hybrid left)
+  const u32 smask = (slot ? mask1 : mask0) & ((1u << S.nseg) - 1);
+  const u32 K = a.K, N = a.N, nseg = u32(__popc(smask));
   const u32 tiles = (rows + BR - 1) / BR;
   // unit = 4 K-consecutive values of one row: one 4-byte word in each of the 8 limb planes
   const u64 units = u64(nbatch) * tiles * nkb * nseg * BR * 8;
@@ -667,8 +688,14 @@ __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows
       kq = u32(t % 8);  // 4-value quarter of the 32-value K block
       t /= 8;
     }
-    const u32 g = u32(t % nseg);
+    const u32 gp = u32(t % nseg);  // packed index; g = the gp-th segment of the mask
     t /= nseg;
+    u32 g = 0;
+    for (u32 c = 0, m = smask;; m &= m - 1, ++c)
+      if (c == gp) {
+        g = u32(__ffs(m) - 1);
+        break;
+      }
     const u32 kb = u32(t % nkb);
     t /= nkb;
     const u32 tile = u32(t % tiles);
@@ -689,7 +716,7 @@ __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows
       lo[i] = u32(x);
       hi[i] = u32(x >> 32);
     }
-    char* base = out + ((((u64(bb) * tiles + tile) * nkb + kb) * nseg + g) * 8) * plane;
+    char* base = out + ((((u64(bb) * tiles + tile) * nkb + kb) * nseg + gp) * 8) * plane;
     const u32 kc = kq / 4;  // which 16-byte K chunk of the core matrix
     // left: plane-major (one MMA A operand per plane); right: the 8 planes stacked along N
     // inside each K chunk, so planes 0..7-l form one B operand of N = (8-l)*BR rows
@@ -705,20 +732,26 @@ __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows
 }
 
 template <int BR>
-void launch_pack(Session& s, const GemmArgs& a, bool left, u32 rows, u32 nbatch, u32 nkb, char* out0, char* out1) {
+void launch_pack(Session& s, const GemmArgs& a, bool left, u32 rows, u32 nbatch, u32 nkb, char* out0, char* out1,
+                 u32 mask0 = ~0u, u32 mask1 = ~0u) {
   const u32 tiles = (rows + BR - 1) / BR;
   int maxseg = 0;
-  for (int i = 0; i < a.nslots; ++i) maxseg = a.sl[i].nseg > maxseg ? a.sl[i].nseg : maxseg;
+  for (int i = 0; i < a.nslots; ++i) {
+    const int np = __builtin_popcount((i ? mask1 : mask0) & ((1u << a.sl[i].nseg) - 1));
+    maxseg = np > maxseg ? np : maxseg;
+  }
   const u64 units = u64(nbatch) * tiles * nkb * maxseg * BR * 8;
   cudaEvent_t pe;
   probe_begin(s.stream, &pe);
   launch_pdl(pack_limbs<BR>, dim3(ew_blocks(units), a.nslots), dim3(256), 0, s.stream, a, left ? 1 : 0, rows, nbatch,
-             nkb, out0, out1);
+             nkb, out0, out1, mask0, mask1);
   probe_end(s.stream, pe);
 }
 
+// packL: 0 = left operand generated by the producers, 1 = fully packed, 2 = hybrid (the
+// dealer-drawn segments packed once, the memory segments loaded by the producers)
 template <int BN, bool AT = false>
-void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
+void launch_tc2(Session& s, const GemmArgs& a, int packL) {
   constexpr u32 kStage = 8 * ((AT ? 0 : kM * kKB) + BN * kKB);
   const size_t smem = kStages * kStage;
   static bool attr = false;
@@ -760,8 +793,14 @@ void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
       rp[i] = reinterpret_cast<char*>(blk->ptr);
       P.Rpk[i] = rp[i];
       P.Rpk_b[i] = rbatched ? rbytes : 0;
-      if (packL) {
-        const u64 lbytes = u64(mtiles) * P.nkb * a.sl[i].nseg * 8 * kM * kKB;
+      u32 lmask = 0;
+      for (int g = 0; g < a.sl[i].nseg; ++g) {
+        const int k = a.sl[i].lk[g];
+        if (packL == 1 || (packL == 2 && k != kOpMem && k != kOpSum)) lmask |= 1u << g;
+      }
+      P.lmask[i] = lmask;
+      if (lmask) {
+        const u64 lbytes = u64(mtiles) * P.nkb * __builtin_popcount(lmask) * 8 * kM * kKB;
         auto lb = s.raw((lbytes * a.nbatch + 7) / 8);
         keep.push_back(lb);
         lp[i] = reinterpret_cast<char*>(lb->ptr);
@@ -770,7 +809,8 @@ void launch_tc2(Session& s, const GemmArgs& a, bool packL) {
       }
     }
     launch_pack<BN>(s, a, false, a.N, rb, P.nkb, rp[0], rp[1]);
-    if (packL) launch_pack<kM>(s, a, true, a.M, a.nbatch, P.nkb, lp[0], lp[1]);
+    if (P.lmask[0] | P.lmask[1])
+      launch_pack<kM>(s, a, true, a.M, a.nbatch, P.nkb, lp[0], lp[1], P.lmask[0], P.lmask[1]);
   }
   // vector width of the L row loads: 2 = 32-byte (LDG.256), 1 = 16-byte, 0 = scalar
   auto aligned = [&](u32 vals) {
@@ -867,14 +907,23 @@ bool ring_gemm_tc2_try(Session& s, const GemmArgs& a) {
     const char* e = std::getenv("MPCG_TC2_AT");  // 1 = on, 0 = off
     return e ? e[0] - '0' : 0;
   }();
+  // five or more N tiles but not fully packed: pack only the dealer-drawn segments (their draws
+  // would repeat per N tile) and let the producers load E (MPCG_TC2_HYBRID=0: regenerate
+  // everything). Measured per layer: a win at 8 tiles (ResNet-18 layer4 / VGG-16 conv4-5, up to
+  // -15%), a loss at 2-4 (the packed planes' HBM round trip outweighs 2-4 regenerations).
+  static const bool hybrid = [] {
+    const char* e = std::getenv("MPCG_TC2_HYBRID");
+    return !(e && e[0] == '0');
+  }();
+  const int lmode = multiN ? 1 : (hybrid && a.N > 4 * 64 ? 2 : 0);
   if (at == 1 && !multiN && a.N > 16)
-    launch_tc2<32, true>(s, a, false);
+    launch_tc2<32, true>(s, a, 0);
   else if (a.N > 32)
-    launch_tc2<64>(s, a, multiN);
+    launch_tc2<64>(s, a, lmode);
   else if (a.N > 16)
-    launch_tc2<32>(s, a, false);
+    launch_tc2<32>(s, a, 0);
   else
-    launch_tc2<16>(s, a, false);
+    launch_tc2<16>(s, a, 0);
   s.check();
   return true;
 }
