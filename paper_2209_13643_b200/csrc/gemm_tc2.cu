@@ -881,7 +881,9 @@ bool ring_gemm_tc2_wants(const GemmArgs& a) {
   if (u64(maxseg) * a.K > kMaxKPrime) return false;
   if (a.ksplit > 1) return false;
   const double work = double(a.M) * a.N * a.K * maxseg * a.nbatch * a.nslots;
-  return tc_gemm_mode() == 1 || (a.M >= 128 && a.N >= 16 && work >= 3e7);
+  // partial-row tiles pay off on short, wide linear layers too (LeNet fc0 64x256x120: SIMT
+  // split-K 50.5 us -> 36.2 us measured); below ~5e6 ring MACs the SIMT kernel's latency wins
+  return tc_gemm_mode() == 1 || (a.M >= 128 && a.N >= 16 && work >= 3e7) || (a.M < 128 && a.N >= 16 && work >= 5e6);
 }
 
 bool ring_gemm_tc2_try(Session& s, const GemmArgs& a) {
