@@ -310,6 +310,17 @@ __global__ void __launch_bounds__(256) ring_gemm_rows(GemmArgs a) {
             for (int n = 0; n < NR; ++n) acc[n] += v[i] * Rs[g][kk + i][n];
         }
       }
+      if (kind == kOpA || kind == kOpRA || kind == kOpA0) {  // dealer draws: counters advance by phi
+        const u64 key = tkey(S.mm.key, S.mm.kp);
+        const u64 e0 = S.aoff + rowbase + kk;
+        u64 z = key + (kind == kOpRA ? S.mm.prA : S.mm.pA) + e0 * kPhi, z2 = key + S.mm.prA + e0 * kPhi;
+        for (; kk < kc; ++kk, z += kPhi, z2 += kPhi) {
+          u64 v = mix64(z);
+          if (kind == kOpA0) v -= mix64(z2);
+#pragma unroll
+          for (int n = 0; n < NR; ++n) acc[n] += v * Rs[g][kk][n];
+        }
+      }
       for (; kk < kc; ++kk) {
         const u64 v = load_l(S, g, rowbase + kk);
 #pragma unroll
@@ -349,7 +360,15 @@ void ring_gemm_launch(Session& s, const GemmArgs& a) {
   if (rows_eligible(a) && gemv_mode() != 0) {  // skinny N: one thread per output row
     cudaEvent_t pe;
     probe_begin(s.stream, &pe);
-    launch_pdl(ring_gemm_rows<kRowN>, dim3((a.M + 255) / 256 * a.nslots), dim3(256), 0, s.stream, a);
+    const dim3 grid((a.M + 255) / 256 * a.nslots);  // accumulators sized to N (no padded columns)
+    if (a.N <= 2)
+      launch_pdl(ring_gemm_rows<2>, grid, dim3(256), 0, s.stream, a);
+    else if (a.N <= 4)
+      launch_pdl(ring_gemm_rows<4>, grid, dim3(256), 0, s.stream, a);
+    else if (a.N <= 6)
+      launch_pdl(ring_gemm_rows<6>, grid, dim3(256), 0, s.stream, a);
+    else
+      launch_pdl(ring_gemm_rows<kRowN>, grid, dim3(256), 0, s.stream, a);
     probe_end(s.stream, pe);
     s.check();
     return;
