@@ -1081,7 +1081,8 @@ struct ChainParams {
   CR fin;        // select combine -> output sink
   u64 n;
   unsigned* bar;
-  int pair;      // one thread evaluates both local slots (grid y == 1)
+  int pair;       // one thread evaluates both local slots (grid y == 1)
+  int skip_mask;  // the mask is folded into the adder's generate round (pair evaluation)
 };
 
 template <class MR, class AR, class BR, class CR>
@@ -1091,8 +1092,10 @@ __global__ void __launch_bounds__(256) chain_kernel(const __grid_constant__ Chai
   const unsigned nb = gridDim.x * gridDim.y;
   const u64 t0 = blockIdx.x * u64(blockDim.x) + threadIdx.x, st = u64(gridDim.x) * blockDim.x;
   unsigned ep = 0;
-  for (u64 g = t0; g < p.n; g += st) eval_slots(p.mask, pr, slot, g);
-  grid_barrier(p.bar, ++ep * nb);
+  if (!p.skip_mask) {
+    for (u64 g = t0; g < p.n; g += st) eval_slots(p.mask, pr, slot, g);
+    grid_barrier(p.bar, ++ep * nb);
+  }
   for (int r = 0; r < p.nadder; ++r) {
     for (u64 g = t0; g < p.n; g += st) eval_slots(p.adder[r], pr, slot, g);
     grid_barrier(p.bar, ++ep * nb);

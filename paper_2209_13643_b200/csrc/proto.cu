@@ -274,6 +274,23 @@ struct MaskedPart {
   }
 };
 
+// Adder operand of the a2b: from keep = x ^ r and the peer's mask outbox (PartX / PartY), or,
+// when `fused` (pair evaluation), straight from x and the two mask draws (MaskedPart).
+template <class XF>
+struct A2bPart {
+  Pid2 pid;
+  CPtr2 keep, peer;
+  u64 k0, k1;
+  Session::MaskRef mr;
+  XF xf;
+  int y;  // 0 = X operand, 1 = Y operand
+  int fused;
+  __device__ u64 operator()(int slot, u64 g) const {
+    if (fused) return MaskedPart<XF>{pid, k0, k1, mr, xf, y}(slot, g);
+    return (pid.v[slot] == 0) == (y == 0) ? keep.p[slot][g] : peer.p[slot][g];
+  }
+};
+
 template <class XF, class FFL, class POST = NoPost>
 void a2b_op(Session& s, size_t n, const AdderOptions& opt, const std::string& tag, XF xf, FFL ffl,
             POST post = NoPost{}) {
@@ -433,14 +450,14 @@ void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const
   for (int r = 0; r < 7; ++r) oa[r] = s.begin_open((r == 0 ? 2 : 4) * n, Reduce::Xor);
   Open ob = s.begin_open(2 * n, Reduce::Sum), og = s.begin_open(2 * n, Reduce::Sum);
 
-  using XF = PartX;
-  using AR = AdderRound<PartX, PartY, B2aBuildFF>;
+  using XF = A2bPart<DF>;
+  using AR = AdderRound<XF, XF, B2aBuildFF>;
   using BR = MulCombine<MulByBitBuild<UF>>;
   using CR = MulCombine<PF>;
   ChainParams<MaskRound<DF>, AR, BR, CR> p{};
   p.mask = MaskRound<DF>{s.mask_key[0], s.mask_key[1], mr, own_ptrs(om), ptrs(keep), df};
-  const XF xf{pid, cptrs(keep), peer_ptrs(om)};
-  const PartY yf{pid, cptrs(keep), peer_ptrs(om)};
+  const XF xf{pid, cptrs(keep), peer_ptrs(om), s.mask_key[0], s.mask_key[1], mr, df, 0, opened ? 1 : 0};
+  const XF yf{pid, cptrs(keep), peer_ptrs(om), s.mask_key[0], s.mask_key[1], mr, df, 1, opened ? 1 : 0};
   for (int r = 0; r <= 7; ++r) {
     AR& k = p.adder[r];
     k.rp = r - 1;
@@ -485,6 +502,7 @@ void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const
   p.n = n;
   p.bar = reinterpret_cast<unsigned*>(bar.s[0]);
   p.pair = s.n_local == 2 && pair_eval_enabled();
+  p.skip_mask = opened ? 1 : 0;
   const unsigned gy = p.pair ? 1u : unsigned(s.n_local);
 
   auto kern = chain_kernel<MaskRound<DF>, AR, BR, CR>;
