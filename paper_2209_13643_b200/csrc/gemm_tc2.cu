@@ -46,13 +46,16 @@ __device__ __forceinline__ u32 smem_u32(const void* p) { return static_cast<u32>
 __device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+// The waiting thread is suspended in try_wait (time hint 10 ms, i.e. until the phase completes)
+// instead of re-issuing the test: spinning waiters (producers ahead of the MMA, the loader)
+// otherwise take issue slots from the producer warps that share their SM sub-partition.
 __device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)
       : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(u64* bar) {
