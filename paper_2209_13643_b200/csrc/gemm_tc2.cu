@@ -670,28 +670,30 @@ __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows
   const u32 K = a.K, N = a.N, nseg = u32(__popc(smask));
   const u32 tiles = (rows + BR - 1) / BR;
   // unit = 4 K-consecutive values of one row: one 4-byte word in each of the 8 limb planes
-  const u64 units = u64(nbatch) * tiles * nkb * nseg * BR * 8;
+  const u32 units = nbatch * tiles * nkb * nseg * BR * 8;
   constexpr u32 plane = BR * kKB;
   // Unit order: when the source rows are K-contiguous (left operand, transposed right operand)
   // the 8 K-quarters of a row are the fastest index, so a warp reads 4 rows x 256 contiguous
   // bytes and writes whole 16-byte core-matrix rows; otherwise (right operand [K][N]) the row
   // index is fastest, so a warp reads 32 consecutive N columns of each K.
   const bool kfast = left || a.tb;
-  for (u64 uid = blockIdx.x * u64(blockDim.x) + threadIdx.x; uid < units; uid += u64(gridDim.x) * blockDim.x) {
-    u64 t = uid;
+  // unit index math in 32 bits (the launcher guarantees units < 2^32): runtime divisors
+  // (segments, K blocks, tiles) cost a 32-bit division each instead of a 64-bit one
+  for (u32 uid = blockIdx.x * blockDim.x + threadIdx.x; uid < units; uid += gridDim.x * blockDim.x) {
+    u32 t = uid;
     u32 r, kq;
     if (kfast) {
-      kq = u32(t % 8);
+      kq = t % 8;
       t /= 8;
-      r = u32(t % BR);
+      r = t % BR;
       t /= BR;
     } else {
-      r = u32(t % BR);
+      r = t % BR;
       t /= BR;
-      kq = u32(t % 8);  // 4-value quarter of the 32-value K block
+      kq = t % 8;  // 4-value quarter of the 32-value K block
       t /= 8;
     }
-    const u32 gp = u32(t % nseg);  // packed index; g = the gp-th segment of the mask
+    const u32 gp = t % nseg;  // packed index; g = the gp-th segment of the mask
     t /= nseg;
     u32 g = 0;
     for (u32 c = 0, m = smask;; m &= m - 1, ++c)
@@ -744,6 +746,7 @@ void launch_pack(Session& s, const GemmArgs& a, bool left, u32 rows, u32 nbatch,
     maxseg = np > maxseg ? np : maxseg;
   }
   const u64 units = u64(nbatch) * tiles * nkb * maxseg * BR * 8;
+  if (units >= (u64(1) << 32)) throw Error(kShapeError, "tcgen05 pack: operand too large");
   cudaEvent_t pe;
   probe_begin(s.stream, &pe);
   launch_pdl(pack_limbs<BR>, dim3(ew_blocks(units), a.nslots), dim3(256), 0, s.stream, a, left ? 1 : 0, rows, nbatch,
