@@ -669,16 +669,32 @@ __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows
   const u32 smask = (slot ? mask1 : mask0) & ((1u << S.nseg) - 1);
   const u32 K = a.K, N = a.N, nseg = u32(__popc(smask));
   const u32 tiles = (rows + BR - 1) / BR;
-  // unit = 4 K-consecutive values of one row: one 4-byte word in each of the 8 limb planes
-  const u32 units = nbatch * tiles * nkb * nseg * BR * 8;
+  // unit = 4 K-consecutive values of one row for EVERY packed segment of the slot: one 4-byte
+  // word in each limb plane of each segment. The dealer draws (A, r_A / B, r_B) and the
+  // opened F of a value are produced once and shared by the segments that use them
+  // (the launcher guarantees one stride and one F for all segments).
+  const u32 units = nbatch * tiles * nkb * BR * 8;
   constexpr u32 plane = BR * kKB;
+  bool dA = false, dRA = false, dB = false, dRB = false, dF = false;
+  int fseg = 0;
+  for (u32 g = 0; g < u32(S.nseg); ++g) {
+    if (!((smask >> g) & 1u)) continue;
+    const int k = left ? S.lk[g] : S.rk[g];
+    if (left) {
+      dA |= k == kOpA || k == kOpA0;
+      dRA |= k == kOpRA || k == kOpA0;
+    } else {
+      dB |= k == kOpB || k == kOpB0F || k == kOpBF;
+      dRB |= k == kOpRB || k == kOpB0F;
+      if (k == kOpSum || k == kOpB0F || k == kOpBF || k == kOpNegSum) dF = true, fseg = int(g);
+    }
+  }
   // Unit order: when the source rows are K-contiguous (left operand, transposed right operand)
   // the 8 K-quarters of a row are the fastest index, so a warp reads 4 rows x 256 contiguous
   // bytes and writes whole 16-byte core-matrix rows; otherwise (right operand [K][N]) the row
   // index is fastest, so a warp reads 32 consecutive N columns of each K.
   const bool kfast = left || a.tb;
-  // unit index math in 32 bits (the launcher guarantees units < 2^32): runtime divisors
-  // (segments, K blocks, tiles) cost a 32-bit division each instead of a 64-bit one
+  // unit index math in 32 bits (the launcher guarantees units < 2^32)
   for (u32 uid = blockIdx.x * blockDim.x + threadIdx.x; uid < units; uid += gridDim.x * blockDim.x) {
     u32 t = uid;
     u32 r, kq;
@@ -693,45 +709,79 @@ __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows
       kq = t % 8;  // 4-value quarter of the 32-value K block
       t /= 8;
     }
-    const u32 gp = t % nseg;  // packed index; g = the gp-th segment of the mask
-    t /= nseg;
-    u32 g = 0;
-    for (u32 c = 0, m = smask;; m &= m - 1, ++c)
-      if (c == gp) {
-        g = u32(__ffs(m) - 1);
-        break;
-      }
-    const u32 kb = u32(t % nkb);
+    const u32 kb = t % nkb;
     t /= nkb;
-    const u32 tile = u32(t % tiles);
-    const u32 bb = u32(t / tiles);
+    const u32 tile = t % tiles;
+    const u32 bb = t / tiles;
     const u32 row = tile * BR + r;
     const u32 k0 = kb * kKB + kq * 4;
-    u32 lo[4], hi[4];
+    u64 A[4], RA[4], F[4];  // per value: the shared draws (left: A, r_A; right: B, r_B) and F
+    u64 idx[4];
+    bool in[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const u32 k = k0 + u32(i);
-      u64 x = 0;
-      if (row < rows && k < K) {
-        if (left)
-          x = load_l(S, int(g), u64(bb) * S.sL[g] + u64(row) * K + k);
-        else
-          x = load_r(S, int(g), u64(bb) * S.sR[g] + (a.tb ? u64(row) * K + k : u64(k) * N + row));
+      in[i] = row < rows && k < K;
+      idx[i] = left ? u64(bb) * S.sL[0] + u64(row) * K + k
+                    : u64(bb) * S.sR[0] + (a.tb ? u64(row) * K + k : u64(k) * N + row);
+      A[i] = RA[i] = F[i] = 0;
+      if (in[i]) {
+        if (left) {
+          if (dA) A[i] = mm_A(S.mm, S.aoff + idx[i]);
+          if (dRA) RA[i] = mm_rA(S.mm, S.aoff + idx[i]);
+        } else {
+          if (dB) A[i] = mm_B(S.mm, S.boff + idx[i]);
+          if (dRB) RA[i] = mm_rB(S.mm, S.boff + idx[i]);
+          if (dF) F[i] = load_f(S, fseg, idx[i]);
+        }
       }
-      lo[i] = u32(x);
-      hi[i] = u32(x >> 32);
     }
-    char* base = out + ((((u64(bb) * tiles + tile) * nkb + kb) * nseg + gp) * 8) * plane;
+    const u64 img = (((u64(bb) * tiles + tile) * nkb + kb) * nseg) * 8 * plane;
     const u32 kc = kq / 4;  // which 16-byte K chunk of the core matrix
     // left: plane-major (one MMA A operand per plane); right: the 8 planes stacked along N
     // inside each K chunk, so planes 0..7-l form one B operand of N = (8-l)*BR rows
     const u32 off = left ? (kc * (BR / 8) + r / 8) * 128 + (r % 8) * 16 + (kq % 4) * 4
                          : kc * (BR * 128) + (r / 8) * 128 + (r % 8) * 16 + (kq % 4) * 4;
     const u32 pstride = left ? plane : BR * 16;
+    u32 gp = 0;
+    for (int g = 0; g < S.nseg; ++g) {
+      if (!((smask >> g) & 1u)) continue;
+      const int kind = left ? S.lk[g] : S.rk[g];
+      u32 lo[4], hi[4];
 #pragma unroll
-    for (int l = 0; l < 8; ++l) {
-      const u32* w = l < 4 ? lo : hi;
-      *reinterpret_cast<u32*>(base + l * pstride + off) = gather4(w[0], w[1], w[2], w[3], u32(l & 3));
+      for (int i = 0; i < 4; ++i) {
+        u64 x = 0;
+        if (in[i]) {
+          if (left) {
+            switch (kind) {
+              case kOpMem: x = S.L[g][idx[i]]; break;
+              case kOpSum: x = S.L[g][idx[i]] + S.L2[g][idx[i]]; break;
+              case kOpA: x = A[i]; break;
+              case kOpA0: x = A[i] - RA[i]; break;
+              default: x = RA[i]; break;
+            }
+          } else {
+            switch (kind) {
+              case kOpMem: x = S.R[g][idx[i]]; break;
+              case kOpSum: x = F[i]; break;
+              case kOpB: x = A[i]; break;
+              case kOpB0F: x = (A[i] - RA[i]) + F[i]; break;
+              case kOpBF: x = A[i] + F[i]; break;
+              case kOpNegSum: x = u64(0) - F[i]; break;
+              default: x = RA[i]; break;
+            }
+          }
+        }
+        lo[i] = u32(x);
+        hi[i] = u32(x >> 32);
+      }
+      char* base = out + img + u64(gp) * 8 * plane;
+#pragma unroll
+      for (int l = 0; l < 8; ++l) {
+        const u32* w = l < 4 ? lo : hi;
+        *reinterpret_cast<u32*>(base + l * pstride + off) = gather4(w[0], w[1], w[2], w[3], u32(l & 3));
+      }
+      ++gp;
     }
   }
 }
@@ -745,8 +795,8 @@ void launch_pack(Session& s, const GemmArgs& a, bool left, u32 rows, u32 nbatch,
     const int np = __builtin_popcount((i ? mask1 : mask0) & ((1u << a.sl[i].nseg) - 1));
     maxseg = np > maxseg ? np : maxseg;
   }
-  const u64 units = u64(nbatch) * tiles * nkb * maxseg * BR * 8;
-  if (units >= (u64(1) << 32)) throw Error(kShapeError, "tcgen05 pack: operand too large");
+  const u64 units = u64(nbatch) * tiles * nkb * BR * 8;  // a unit packs every segment of its slot
+  if (units * (maxseg > 0 ? 1 : 0) >= (u64(1) << 32)) throw Error(kShapeError, "tcgen05 pack: operand too large");
   cudaEvent_t pe;
   probe_begin(s.stream, &pe);
   launch_pdl(pack_limbs<BR>, dim3(ew_blocks(units), a.nslots), dim3(256), 0, s.stream, a, left ? 1 : 0, rows, nbatch,
@@ -898,6 +948,12 @@ bool ring_gemm_tc2_try(Session& s, const GemmArgs& a) {
     for (int g = 0; g < a.sl[i].nseg; ++g) {
       const GemmSlotArgs& S = a.sl[i];
       if (S.sL[g] != S.sL[0]) return false;  // the producer uses one row stride for every segment
+      if (S.sR[g] != S.sR[0]) return false;  // the pack shares draws across segments
+      const bool fk = S.rk[g] == kOpSum || S.rk[g] == kOpB0F || S.rk[g] == kOpBF || S.rk[g] == kOpNegSum;
+      for (int h = 0; h < g && fk; ++h) {
+        const bool fh = S.rk[h] == kOpSum || S.rk[h] == kOpB0F || S.rk[h] == kOpBF || S.rk[h] == kOpNegSum;
+        if (fh && (S.R[h] != S.R[g] || S.R2[h] != S.R2[g])) return false;  // ... and one opened F
+      }
     }
   // several N tiles: pack the left operand once (bulk-copied per tile) or regenerate it per
   // tile in the producers (CTAs of one M tile run side by side, so E re-reads hit L2).
