@@ -100,9 +100,9 @@ def main():
         ("mlp", "private", ["device", "nvlink"], True),
         ("lenet5", "private", ["device", "nvlink"], True),
         ("lenet5", "public", ["device"], True),
-        ("resnet18", "private", ["device", "nvlink"], False),
-        ("bert_base", "private", ["device", "nvlink"], False),
-        ("bert_base", "public", ["device"], False),
+        ("resnet18", "private", ["device", "nvlink"], True),
+        ("bert_base", "private", ["device", "nvlink"], True),
+        ("bert_base", "public", ["device"], True),
         ("vgg16", "private", ["device", "nvlink"], True),
     ]
     # inner-pipeline threshold per link: in-device opens never gain from chunking (the reference's
