@@ -568,6 +568,53 @@ __global__ void __launch_bounds__(256) eps_im2col_summed_kernel(MmTriple mm, Con
   }
 }
 
+// The same, tiled for input reuse: a block owns 8 consecutive output columns (ow) of one
+// output row (n, oh) — warp w the im2col row of ow0 + w — and stages, per chunk of cc input
+// channels, the summed input window x0 + x1 (cc x k x (7*stride + k) words, zero padded) in
+// shared memory once; every tap is then a shared-memory read instead of two gathers, so the
+// kernel is bound by its coalesced E stores.
+__global__ void __launch_bounds__(256) eps_im2col_tile_kernel(MmTriple mm, ConvGeom g, const u64* __restrict__ x0,
+                                                             const u64* __restrict__ x1, u64* __restrict__ out,
+                                                             u32 cc_max, FastDiv fkk, FastDiv fk, u64 a_off) {
+  extern __shared__ u64 sx[];
+  pdl_enter();
+  const u32 owt = (g.OW + 7) / 8;
+  const u32 bt = blockIdx.x % owt, rowid = blockIdx.x / owt;  // rowid = n*OH + oh
+  const u32 oh = rowid % g.OH, n = rowid / g.OH;
+  const u32 ow0 = bt * 8, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const u32 ow = ow0 + warp;
+  const u32 K = g.C * g.k * g.k, kk = g.k * g.k;
+  const u32 ww = 7 * g.stride + g.k;  // window width
+  const int ih0 = int(oh * g.stride) - int(g.pad), iw0 = int(ow0 * g.stride) - int(g.pad);
+  const u64 r = u64(rowid) * g.OW + ow;
+  const u64 key = tkey(mm.key, mm.kp) + mm.pA;
+  for (u32 c0 = 0; c0 < g.C; c0 += cc_max) {
+    const u32 cc = min(cc_max, g.C - c0);
+    __syncthreads();
+    const u32 wn = cc * g.k * ww;
+    for (u32 e = threadIdx.x; e < wn; e += blockDim.x) {
+      const u32 cl = e / (g.k * ww), rem = e - cl * (g.k * ww), ki = rem / ww, wx = rem - ki * ww;
+      const int ih = ih0 + int(ki), iw = iw0 + int(wx);
+      u64 v = 0;
+      if (unsigned(ih) < g.H && unsigned(iw) < g.W) {
+        const u64 src = ((u64(n) * g.C + c0 + cl) * g.H + u32(ih)) * g.W + u32(iw);
+        v = x0[src] + x1[src];
+      }
+      sx[e] = v;
+    }
+    __syncthreads();
+    if (ow >= g.OW) continue;
+    const u32 ncol = cc * kk;
+    const u64 jb = r * K + u64(c0) * kk;
+    u64 z = key + (a_off + jb + lane) * kPhi;
+    for (u32 cl = lane; cl < ncol; cl += 32, z += 32 * kPhi) {
+      const u32 ci = fkk.div(cl), t2 = cl - ci * kk, ki = fk.div(t2), kj = t2 - ki * g.k;
+      const u64 v = sx[(ci * g.k + ki) * ww + warp * g.stride + kj];
+      out[jb + cl] = v - mix64(z);  // eps0 + eps1 = x0 + x1 - (a0 + a1), a0 + a1 = A
+    }
+  }
+}
+
 template <class F>
 __global__ void __launch_bounds__(256) strip_kernel(u64 n, F f) {
   pdl_enter();
@@ -575,9 +622,31 @@ __global__ void __launch_bounds__(256) strip_kernel(u64 n, F f) {
 }
 }  // namespace
 
+static bool tile_eps_enabled() {  // MPCG_EPS_TILE=0: the warp-per-row gather kernel instead
+  static const bool on = [] {
+    const char* e = std::getenv("MPCG_EPS_TILE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const ConvGeom& gm, size_t a_off,
                       size_t na, Open& o, const DT* aops) {
   const u32 Kc = gm.C * gm.k * gm.k;
+  const u32 ww = 7 * gm.stride + gm.k;
+  const u32 cc_max = u32((48 * 1024) / (8 * gm.k * ww));
+  if (o.summed && s.n_local == 2 && !aops && a_off == 0 && na == u64(gm.N) * gm.OH * gm.OW * Kc && cc_max >= 1 &&
+      tile_eps_enabled()) {
+    const u32 cc = cc_max < gm.C ? cc_max : gm.C;
+    const size_t smem = size_t(cc) * gm.k * ww * 8;
+    const u64 blocks = u64(gm.N) * gm.OH * ((gm.OW + 7) / 8);
+    cudaEvent_t pe;
+    probe_begin(s.stream, &pe);
+    launch_pdl(eps_im2col_tile_kernel, dim3(unsigned(blocks)), dim3(256), smem, s.stream, t.mm, gm, x[0], x[1],
+               o.own(0), cc, FastDiv(gm.k * gm.k), FastDiv(gm.k), u64(a_off));
+    probe_end(s.stream, pe);
+    return;
+  }
   if (o.summed && s.n_local == 2 && !aops && a_off % Kc == 0 && na % Kc == 0 && Kc * sizeof(int2) <= 96 * 1024) {
     const u32 rows = u32(na / Kc);
     const size_t smem = Kc * sizeof(int2);
