@@ -812,8 +812,8 @@ bool beaver_combine_uses_tc(const Session& s, u32 nbatch, u32 M, u32 N, u32 K) {
 }
 
 // The eps build also emits the A-side operands (A, a0 / r_A) only for combines that read them
-// from memory (tiled SIMT and first-generation tcgen05); the small-M path and the
-// warp-specialised tcgen05 path draw them in place.
+// from memory (tiled SIMT and first-generation tcgen05); the small-M path, the skinny-N row
+// path and the warp-specialised tcgen05 path draw them in place.
 bool beaver_combine_wants_aops(const Session& s, u32 nbatch, u32 M, u32 N, u32 K) {
   GemmArgs a{};
   a.nslots = s.n_local;
@@ -823,6 +823,7 @@ bool beaver_combine_wants_aops(const Session& s, u32 nbatch, u32 M, u32 N, u32 K
   a.nbatch = nbatch;
   for (int i = 0; i < s.n_local; ++i) a.sl[i].nseg = s.party_of[i] == 0 ? 3 : 2;
   if (gemv_eligible_shape(M, nbatch, false, 0) && gemv_mode() != 0) return false;
+  if (rows_eligible(a) && gemv_mode() != 0) return false;  // the row kernel draws A / r_A itself
   return !ring_gemm_tc2_wants(a);
 }
 
