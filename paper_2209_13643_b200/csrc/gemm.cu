@@ -156,7 +156,7 @@ void launch_simt(Session& s, GemmArgs a) {
 // B / r_B draw and one F load — while the few L rows of a K-chunk are staged in shared
 // memory. Bound by reading F (2 x 8 B per (k, n) per party) and the dealer draws.
 constexpr int kGvMax = 16;  // the small-M path takes M <= kGvMax (M=64 x N=120 measured 6x slower than SIMT)
-constexpr int kGvKC = 64;   // K chunk staged in smem
+constexpr int kGvKC = 64;   // K chunk staged in smem (512 for M = 1 measured: -4% on VGG fc6, +20% on MLP)
 
 template <int MR>
 __global__ void __launch_bounds__(256) ring_gemv(GemmArgs a) {
@@ -244,9 +244,11 @@ void launch_gemv(Session& s, GemmArgs a) {
   cudaStream_t st = s.stream;
   const u32 ncol = (a.N + 31) / 32;
   const u32 mgrp = (a.M + MR - 1) / MR;
-  // split K until ~3 blocks per SM, >= one staged chunk per split
+  // split K until ~16 blocks per SM (two full waves of 8 resident 256-thread blocks: the
+  // per-(k, n) dealer draws are latency-bound chains, so the kernel needs every warp slot;
+  // VGG fc6 1 x 25088 x 4096: 1.61 ms at ~3 blocks per SM), >= one staged chunk per split
   const u64 base = u64(ncol) * a.nslots * mgrp;
-  u32 split = u32((3 * u64(kSms) + base - 1) / base);
+  u32 split = u32((16 * u64(kSms) + base - 1) / base);
   const u32 maxsplit = (a.K + kGvKC - 1) / kGvKC;
   split = split > maxsplit ? maxsplit : (split < 1 ? 1 : split);
   a.kchunk = ((a.K + split - 1) / split + kGvKC - 1) / kGvKC * kGvKC;
