@@ -1,21 +1,24 @@
 #!/usr/bin/env python
 """bench.py — 2PC private-inference latency/throughput on B200 (MPC-Pipe hot path).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--model lenet5]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--model resnet18]
 
-Workload (BASELINE.json configs[1]): LeNet-5 on a synthetic 28x28 batch of 64, 2PC,
-private weights, inter-linear-layer pipeline on (pipelined mode), seed 1 — the
-reference's seeded init_weights / demo_input. A step is one secure inference of the
-whole batch by both parties. N=1: both parties on cuda:0. N>=2: one party per GPU
-(rank 2k <-> 2k+1 over NCCL), N/2 data-parallel pairs each on its own 64-row shard
-of a 64*N/2 global batch (weak scaling; offset-aware PRG keeps every shard
-word-identical to the single-pair full-batch run).
+Workload (BASELINE.json configs[2], the largest config that fits one GPU): ResNet-18 on a
+synthetic CIFAR-10 batch of 128 (3x32x32), 2PC, private weights, pipelined (inter-linear
+delta prefetch + inner-layer chunked pipeline, n=4 lanes for operands >= the reference's 2 MiB
+threshold), seed 1 — the reference's seeded init_weights / demo_input. A step is one secure
+inference of the whole batch by both parties. N=1: both parties on cuda:0. N>=2: one party
+per GPU (rank 2k <-> 2k+1 over NCCL), N/2 data-parallel pairs each on its own 128-image shard
+of a 128*N/2 global batch (weak scaling; the offset-aware PRG keeps every shard word-identical
+to the single-pair full-batch run).
 
-`value` is whole-job inferences/s timed on device with CUDA events (inputs resident,
-L2 flushed between timed steps); `e2e` is the same metric through the public API with
-the input shares copied from pinned host memory and the logit shares read back every
-step. `--impl reference` times the UNMODIFIED reference (oracle/_ref/ref_driver, built
-from /root/reference by oracle/Makefile) on the host cores on the same workload.
+`value` is whole-job inferences/s timed on device with CUDA events (inputs resident, L2
+flushed between timed steps); `e2e` is the same metric through the public API with the input
+shares copied from pinned host memory and the logit shares read back every step.
+`--impl reference` times the UNMODIFIED reference (oracle/_ref/ref_driver, built from
+/root/reference by oracle/Makefile) on the host cores: end to end through its bench_party for
+the models it can run in seconds (MLP, LeNet-5), else an op-sum estimate from its own ops at
+every layer's shape (ResNet-18 / BERT-base are not expressible in it).
 """
 import argparse
 import json
@@ -39,18 +42,22 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--model", default="lenet5")
+    ap.add_argument("--model", default="resnet18")
     ap.add_argument("--batch", type=int, default=0, help="per-pair batch (default: the config's)")
     ap.add_argument("--mode", default="pipelined", choices=["pipelined", "blocking"])
     ap.add_argument("--weights", default="private", choices=["private", "public"])
     ap.add_argument("--no-blocking", action="store_true", help="skip the blocking comparison pass")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the per-slot and loopback one-party co-location measurements")
+    ap.add_argument("--chunks", type=int, default=4, help="inner-layer pipeline chunk count (ExecOptions::chunks)")
     ap.add_argument("--link", default="",
                     help="emulate a LAN/WAN link between the parties, e.g. 10gbps (1.25e9 B/s, 0.1 ms) or "
                          "'<latency_s>,<bytes_per_s>'; default: the real in-device / NVLink transport")
-    ap.add_argument("--threshold", default="auto",
-                    help="inner-pipeline chunk threshold: auto (calibrate_threshold on this link, like the "
-                         "reference CLI's --threshold auto), ref (the reference default 2 MiB) or bytes")
+    ap.add_argument("--threshold", default="ref",
+                    help="inner-pipeline chunk threshold: ref (the reference default 2 MiB: chunking on for "
+                         "operands >= 2 MiB), auto (calibrate_threshold on this link, like the reference CLI's "
+                         "--threshold auto) or bytes")
     return ap.parse_args()
 
 
@@ -135,6 +142,15 @@ def measure_int8_peak():
 
 
 # ----------------------------------------------------------------------------- reference
+# Models the reference can run end to end in seconds: timed through its own bench_party.
+# Everything else (ResNet-18 and BERT-base are not expressible in it; VGG-16 takes ~10 min
+# per inference) is an op-sum estimate: the reference's own ops timed at every layer's shape
+# on a row sample and scaled (oracle/ref_driver.cpp cmd_opsum).
+REF_E2E_MODELS = ("mlp", "lenet5", "toy_cnn", "toy_transformer")
+# 1/div of every layer's rows per sample: ~5 s of CPU per step per pair on this container
+OPSUM_DIV = {"resnet18": 128, "vgg16": 64, "bert_base": 48}
+
+
 def ref_bench(model_path, mode, iters, weights, seed=1, port=21000):
     env = dict(os.environ, MPCPIPE_PORT_BASE=str(port))
     out = subprocess.run([REF_DRIVER, "bench", model_path, mode, str(iters), weights, str(seed)],
@@ -144,25 +160,68 @@ def ref_bench(model_path, mode, iters, weights, seed=1, port=21000):
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
+def ref_opsum(model_path, weights, div, pairs, seed=1):
+    out = subprocess.run([REF_DRIVER, "opsum", model_path, weights, str(div), str(pairs), str(seed)],
+                         capture_output=True, text=True, timeout=1800)
+    if out.returncode != 0:
+        raise RuntimeError("reference driver failed: " + out.stderr.strip()[-400:])
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def ref_pairs():
+    """Concurrent 2PC pairs the host can run (the reference is single-threaded per party)."""
+    return max(1, (os.cpu_count() or 2) // 2)
+
+
+def reference_sample(model, model_path, g, mode, weights, iters, warmup=0, pairs=None):
+    """One timed reference measurement of the workload. Returns (inferences/s, ms per inference
+    batch, cpu_baseline-style description)."""
+    batch = g.input[0]
+    if model in REF_E2E_MODELS:
+        r = ref_bench(model_path, mode, warmup + iters, weights)
+        walls = r["iter_wall_s"][warmup:]
+        lat = sum(walls) / len(walls)
+        return batch / lat, lat * 1e3, {
+            "kind": "reference", "cores": 2, "logits_hash": r["logits_hash"],
+            "sample": f"{iters} timed iterations (+{warmup} warm-up) of the full workload through the reference's "
+                      f"bench_party over SocketComm, one thread per party (nproc={os.cpu_count()})"}
+    pairs = pairs or ref_pairs()
+    div = OPSUM_DIV.get(model, 32)
+    ests, walls, last = [], [], None
+    for _ in range(warmup + iters):
+        last = ref_opsum(model_path, weights, div, pairs)
+        ests.append(last["est_latency_s"])
+        walls.append(last["wall_s"])
+    ests, walls = ests[warmup:], walls[warmup:]
+    lat = sum(ests) / len(ests)
+    top = sorted(last["layers"], key=lambda l: -l["est_s"])[:4]
+    return pairs * batch / lat, lat * 1e3, {
+        "kind": "reference-op-sum-estimate", "cores": 2 * pairs,
+        "sample": f"{iters} samples (+{warmup} warm-up), each the reference's own ops (beaver_matmul + "
+                  f"truncate_shares, relu_shares, max_last_dim, softmax_shares, ...) run at every layer's shape on "
+                  f"1/{div} of its rows and scaled linearly, {pairs} concurrent 2PC pairs x 2 party threads over "
+                  f"the in-memory SimComm (compute only, no link cost); {sum(walls) / len(walls):.1f} s wall per sample; "
+                  f"throughput = pairs x batch / estimated latency",
+        "est_latency_ms_per_pair": lat * 1e3, "top_layers_s": {l["name"]: round(l["est_s"], 3) for l in top}}
+
+
 def run_reference(a, g, model_path):
     """The reference's own CPU implementation (oracle/_ref) on this host's cores."""
-    batch = g.input[0]
-    r = ref_bench(model_path, a.mode, a.warmup + a.steps, a.weights)
-    walls = r["iter_wall_s"][a.warmup:]
-    lat = sum(walls) / len(walls)
-    v = batch / lat
+    v, lat_ms, cpu = reference_sample(a.model, model_path, g, a.mode, a.weights, a.steps, a.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "inferences/s", "n_gpus": a.gpus,
-            "steps": a.steps, "warmup": a.warmup, "ms_per_step": lat * 1e3, "higher_is_better": True,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": lat_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded init_weights/demo_input)",
-            "config": {"workload": f"{g.name} b{batch} 2PC {a.weights} {a.mode}", "model": g.name,
-                       "global_batch": batch, "mode": a.mode, "weights": a.weights,
-                       "transport": "reference SocketComm over loopback, parties as threads",
-                       "logits_hash": r["logits_hash"], "bytes_sent_per_party": r["bytes_sent"]},
-            "cpu_baseline": {"value": v, "unit": "inferences/s", "cores": 2, "kind": "reference",
-                             "sample": f"{a.steps} timed iterations (+{a.warmup} warm-up) of the full workload, "
-                                       "one thread per party"},
+            "config": {"workload": workload_name(g, a), "model": g.name,
+                       "global_batch": g.input[0], "mode": a.mode, "weights": a.weights,
+                       "transport": "reference SocketComm / SimComm in-process, parties as threads"},
+            "cpu_baseline": dict(cpu, value=v, unit="inferences/s"),
             "e2e": {"value": v, "unit": "inferences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def workload_name(g, a):
+    chunked = f", inner-layer chunks {a.chunks}" if a.mode == "pipelined" and a.chunks > 1 else ""
+    return f"{g.name} b{g.input[0]} 2PC {a.weights} {a.mode}{chunked}"
 
 
 # ----------------------------------------------------------------------------- ours
@@ -227,7 +286,7 @@ def main():
     if a.threshold == "auto":
         if world == 1:
             from paper_2209_13643_b200 import tuning
-            calib = tuning.sweep_threshold("relu", chunks=4, link=link)
+            calib = tuning.sweep_threshold("relu", chunks=a.chunks, link=link)
             thr = calib["threshold_bytes"] or NEVER
         else:
             thr = 2 << 20  # NCCL link: keep the reference default (calibrating needs both ranks)
@@ -241,7 +300,7 @@ def main():
         if link:
             s.set_link(*link)
         ex = mp.SecureExecutor(s, g, public_weights=a.weights == "public", pipelined=mode == "pipelined",
-                               chunk_threshold=thr)
+                               chunks=a.chunks, chunk_threshold=thr)
         ex.deal_weights(weights, seed)
         x = s.deal_input(x_global, seed + 1, batch_offset=B * pair, local_batch=B)
         return s, ex, x
@@ -279,6 +338,18 @@ def main():
         ms = api.timer(s, "read")
         return maxall(ms) / steps, launches, clk.summary(), out
 
+    def graph_ms(mode, steps, warmup):
+        """A fresh session + executor in `mode`, one eager run (pipelined prologue), capture,
+        then timed graph replays. Returns (ms/step, per-layer ms of the last replay)."""
+        sb, exb, xb = setup(mode)
+        exb.run(xb)
+        exb.time_layers(True)
+        exb.capture(xb)
+        ms, _, _, _ = timed(sb, exb, xb, steps, warmup, graph=True)
+        lt = exb.layer_times()
+        del exb, sb
+        return ms, lt
+
     # ---- main arm: the requested mode
     s, ex, x = setup(a.mode)
     eager_ms, _, _, _ = timed(s, ex, x, max(3, a.steps // 4), 2, graph=False)
@@ -289,10 +360,11 @@ def main():
     for cls in ("adder_round", "beaver", "chain", "gemm"):
         barrier(s)
         api.probe_start(cls)
-        for _ in range(a.steps):
+        for _ in range(max(2, a.steps // 4)):
             ex.run(x)
         s.sync()
         probes[cls] = api.probe_stop()
+    probe_steps = max(2, a.steps // 4)
 
     ex.time_layers(True)   # per-layer CUDA events recorded inside the graph
     ex.capture(x)
@@ -300,8 +372,8 @@ def main():
     layer_ms = ex.layer_times()   # of the last timed replay
     z = out.numpy()
 
-    # ---- e2e through the public API: pinned H2D of the input shares, run, D2H of the logits
-    nloc = 2 if world == 1 else 1
+    # ---- e2e through the public API: pinned H2D of the input shares, one graph replay
+    # (mpcg_executor_replay), D2H of the logit shares — every step
     xin_host = x.numpy()
     pin_in = api.PinnedBuffer(xin_host.size)
     pin_in.array[:] = xin_host.reshape(-1)
@@ -318,40 +390,59 @@ def main():
     e2e_s = maxall(time.perf_counter() - t0) / a.steps
     h2d = xin_host.size * 8
     d2h = z.size * 8
+    ex.release_graph()
+    del ex, s
 
     # ---- blocking comparison (the paper's pipelined-vs-blocking reduction, per layer)
     blocking = None
     if not a.no_blocking and a.mode == "pipelined":
-        sb, exb, xb = setup("blocking")
-        exb.run(xb)
-        exb.time_layers(True)
-        exb.capture(xb)
-        b_ms, _, _, _ = timed(sb, exb, xb, a.steps, a.warmup, graph=True)
-        bl = exb.layer_times()
+        b_ms, bl = graph_ms("blocking", a.steps, a.warmup)
         blocking = {"ms_per_step": b_ms, "note": "graph replays; per-layer CUDA events inside the graph",
                     "reduction_pct": (b_ms - ms_step) / b_ms * 100.0,
                     "per_layer": [{"layer": l.name, "blocking_ms": round(bb, 4), "pipelined_ms": round(pp, 4),
                                    "reduction_pct": round((bb - pp) / bb * 100.0, 2) if bb > 0 else 0.0}
                                   for l, bb, pp in zip(g.layers, bl, layer_ms)]}
-        del exb, sb
+
+    # ---- co-location check (1 GPU): the pair-evaluated headline evaluates both parties of an
+    # element in one thread and writes each opened value once. Beside it: per-slot kernels (each
+    # party writes its own payload and reads the peer's, as two separate parties do) and two
+    # one-party sessions on two host threads over the in-process loopback link (the exact code
+    # a 2-GPU pair runs, with device copies in place of NCCL; eager launches).
+    colocation = None
+    if world == 1 and not a.no_variants:
+        api.set_pair_eval(False)
+        try:
+            ps_ms, _ = graph_ms(a.mode, a.steps, a.warmup)
+        finally:
+            api.set_pair_eval(True)
+        lb_ms = loopback_ms(mp, g, weights, x_global, a, thr, link, seed)
+        colocation = {
+            "pair_evaluated": {"ms_per_step": ms_step, "inferences_per_s": B / (ms_step / 1e3),
+                               "path": "one thread per element evaluates both local party slots; opened values "
+                                       "written once (headline `value`)"},
+            "per_slot": {"ms_per_step": ps_ms, "inferences_per_s": B / (ps_ms / 1e3),
+                         "path": "mpcg_set_pair_eval(0): per-slot kernels, two payloads written and both read "
+                                 "per open (MPCG_PAIR_EVAL=0 MPCG_EPS_FUSE=0); CUDA-graph replays"},
+            "loopback_one_party_sessions": {"ms_per_step": lb_ms, "inferences_per_s": B / (lb_ms / 1e3),
+                                            "path": "two n_local=1 sessions (party 0, party 1) on two host threads, "
+                                                    "loopback link (device copies in place of NCCL send/recv), eager "
+                                                    "launches; wall clock per step after a stream sync"}}
 
     if rank != 0:
+        if dist:
+            dist.destroy_process_group()
         return
     # ---- CPU baseline: the reference itself on this host (bounded sample)
     cpu = None
     if not a.no_cpu and os.path.exists(REF_DRIVER):
         try:
-            iters = 6 if a.model == "lenet5" else 3
-            r = ref_bench(model_path, a.mode, iters, a.weights)
-            lat = sum(r["iter_wall_s"]) / len(r["iter_wall_s"])
-            cpu = {"value": g.input[0] / lat, "unit": "inferences/s", "cores": 2, "kind": "reference",
-                   "sample": f"{iters} iterations of {g.name} b{g.input[0]} 2PC {a.weights} {a.mode} "
-                             f"(reference bench_party over SocketComm, 1 thread/party; nproc={os.cpu_count()})",
-                   "ms_per_inference_batch": lat * 1e3, "logits_hash": r["logits_hash"]}
+            v, lat_ms, desc = reference_sample(a.model, model_path, g, a.mode, a.weights, 1 if a.model not in
+                                               REF_E2E_MODELS else 4)
+            cpu = dict(desc, value=v, unit="inferences/s", ms_per_inference_batch=lat_ms)
         except Exception as e:  # reported, never fatal
-            cpu = {"value": None, "unit": "inferences/s", "cores": 2, "kind": "reference", "sample": str(e)[:200]}
+            cpu = {"value": None, "unit": "inferences/s", "cores": None, "kind": "reference", "sample": str(e)[:200]}
     elif not a.no_cpu:
-        cpu = {"value": None, "unit": "inferences/s", "cores": 2, "kind": "reference",
+        cpu = {"value": None, "unit": "inferences/s", "cores": None, "kind": "reference",
                "sample": "oracle/_ref/ref_driver not built (run make -C oracle where /root/reference exists)"}
 
     peaks = {}
@@ -369,13 +460,15 @@ def main():
     int8_peak, int8_src = measure_int8_peak()
     # algorithmic units per class: bytes for the HBM-bound protocol rounds, ring MACs
     # for the GEMM (x36 int8 MACs = 72 int8 ops each, the limb-pair products of the tcgen05 path)
-    notes = {"adder_round": "SPK level round (settle r, issue r+1), opened wire (pair evaluation): 64 B/elem/party = "
-                            "32 B opened value written + read once per element pair + 8x(2 in + 2 out) state "
-                            "(per-slot form: 96 B = 2x32 B wire + state)",
-             "beaver": "Beaver mul/square rounds incl. fused exp/Newton chains: 40 (opened wire) or 56 / 32 B/elem/party "
-                       "per op",
-             "chain": "persistent compare-and-select chain (ReLU/tournament): 512 B/elem/party",
-             "gemm": "ring GEMM main kernel: 72 int8 ops per ring MAC (36 limb-pair MACs), packing excluded"}
+    notes = {"adder_round": "SPK level round (settle r, issue r+1), SURVEY 8(d) bytes per element per party: "
+                            "2 x 32 B wire + 8 x (2 in + 2 out) state = 96 B (the per-slot form; the pair-evaluated "
+                            "kernel moves less, so frac can exceed its own traffic share)",
+             "beaver": "Beaver mul/square rounds incl. fused exp/Newton chains: 2 x 16 B wire + 8 x (2 in + 1 out) "
+                       "= 56 B/elem/party per mul, 32 B per square (SURVEY 8(d))",
+             "chain": "persistent compare-and-select chain (ReLU/tournament): 2 x 248 B wire + 16 B in/out = "
+                      "512 B/elem/party (SURVEY 8(d))",
+             "gemm": "ring GEMM main kernel: 72 int8 ops per ring MAC (36 limb-pair MACs); ring MACs = 3 MKN (party 0, "
+                     "dealer C online) + 2 MKN (party 1) per private linear layer; packing excluded"}
     rooflines = []
     for cls, (p_ms, p_launches, p_units) in probes.items():
         if p_launches == 0 or p_ms <= 0:
@@ -387,27 +480,27 @@ def main():
         else:
             ach = (p_units / 1e9) / (p_ms / 1e3)
             r = {"kernel": cls, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                 "frac": ach / hbm_peak, "peak_source": "measured" if hbm else "fallback"}
-        r.update({"launches": p_launches, "device_ms_per_step": p_ms / a.steps,
+                 "frac": ach / hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "fallback"}
+        r.update({"launches": p_launches, "device_ms_per_step": p_ms / probe_steps,
                   "avg_launch_us": p_ms * 1e3 / p_launches, "units_per_launch": p_units / p_launches,
-                  "traffic": (traffic.get(cls) or {}).get("dram_bytes_per_launch"), "note": notes[cls]})
+                  "traffic": (traffic.get(a.model, {}).get(cls) or {}).get("dram_bytes_per_launch"),
+                  "note": notes[cls]})
         rooflines.append(r)
     rooflines.sort(key=lambda r: -r["device_ms_per_step"])
     roof = dict(rooflines[0]) if rooflines else None  # the dominant class of the step
     if roof:
         roof["share_of_probed_ms"] = roof["device_ms_per_step"] / sum(r["device_ms_per_step"] for r in rooflines)
 
-    pipelined_ms = ms_step
     value = B * pairs / (ms_step / 1e3)
     dec = (z.sum(axis=0) if world == 1 else z[0]).reshape(-1)
     line = {
         "metric": METRIC, "value": value, "unit": "inferences/s", "n_gpus": a.gpus, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": pipelined_ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64",
         "data": "synthetic: the reference's seeded init_weights(seed 12) / demo_input(seed 13), shares dealt on host",
-        "config": {"workload": f"{g.name} b{B} 2PC {a.weights} {a.mode}", "model": g.name, "global_batch": B * pairs,
+        "config": {"workload": workload_name(g, a), "model": g.name, "global_batch": B * pairs,
                    "pairs": pairs, "parties_per_gpu": 2 if world == 1 else 1, "mode": a.mode, "weights": a.weights,
-                   "frac_bits": g.frac_bits, "chunks": 4,
+                   "frac_bits": g.frac_bits, "chunks": a.chunks,
                    "chunk_threshold_bytes": None if thr == NEVER else thr,
                    "chunk_threshold_source": a.threshold,
                    "calibration": calib,
@@ -418,19 +511,65 @@ def main():
                    "execution": "one CUDA-graph replay per step (whole 2PC inference, both parties)",
                    "eager_ms_per_step": eager_ms,
                    "logits_hash_slot0": mp.fnv1a_words(dec) if world == 1 else None,
-                   "blocking": blocking},
+                   "blocking": blocking,
+                   "colocation": colocation},
         "roofline": roof,
         "rooflines": rooflines,
         "cpu_baseline": cpu,
         "e2e": {"value": B * pairs / e2e_s, "unit": "inferences/s", "ms_per_step": e2e_s * 1e3,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "pinned host shares -> mpcg_tensor_copy_from_host -> mpcg_executor_run -> mpcg_tensor_download"},
+                "path": "pinned host input shares -> mpcg_tensor_copy_from_host -> mpcg_executor_replay (the "
+                        "captured inference) -> mpcg_tensor_download of the logit shares; wall clock"},
         "gpu_launches": launches,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def loopback_ms(mp, g, weights, x_global, a, thr, link, seed):
+    """Two single-party sessions on cuda:0 driven by two host threads, linked in-process."""
+    import threading
+    sess = [mp.Session(device=0, n_local=1, party=p, seed=seed, mask_seed=seed ^ PHI, frac_bits=g.frac_bits)
+            for p in (0, 1)]
+    sess[0].connect_loopback(sess[1])
+    if link:
+        for s in sess:
+            s.set_link(*link)
+    steps = max(2, min(a.steps, 8))
+    walls, err = [0.0, 0.0], []
+    go = threading.Barrier(2)
+
+    def party(p):
+        try:
+            s = sess[p]
+            ex = mp.SecureExecutor(s, g, public_weights=a.weights == "public", pipelined=a.mode == "pipelined",
+                                   chunks=a.chunks, chunk_threshold=thr)
+            ex.deal_weights(weights, seed)
+            x = s.deal_input(x_global, seed + 1)
+            for _ in range(2):
+                ex.run(x)
+            s.sync()
+            go.wait()
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                ex.run(x)
+            s.sync()
+            walls[p] = (time.perf_counter() - t0) / steps
+            del ex
+        except Exception as e:  # noqa: BLE001
+            err.append(repr(e))
+            go.abort()
+
+    th = [threading.Thread(target=party, args=(p,)) for p in (0, 1)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if err:
+        raise RuntimeError("loopback measurement failed: " + err[0])
+    return max(walls) * 1e3
 
 
 if __name__ == "__main__":

@@ -78,7 +78,21 @@ int mpcg_session_set_persistent(mpcg_session* s, int enable);
 /* CommStats of one local slot (transport/transport.hpp:39-45): bytes, collectives, p2p. */
 int mpcg_session_stats(mpcg_session* s, int slot, uint64_t out[3]);
 int mpcg_session_n_local(mpcg_session* s, int* out);
+/* Communicator::trace / clear_trace / now / add_delay (transport/transport.hpp:25-82).
+ * While enabled, one row per collective: seq, kind, tag, bytes and device timestamps in seconds
+ * since the trace was enabled — t[0] issue, t[1] sent (sender occupancy charged), t[2] wait
+ * begin, t[3] wait end (occupancy = t1 - t0, stall = t3 - t2; report.hpp:42-66 sums them into
+ * delta-wait / linear-comm). Reading synchronises the session. Opens recorded inside a graph
+ * capture or performed in-kernel carry no timestamps (0). */
 int mpcg_session_trace(mpcg_session* s, int enable);
+int mpcg_session_trace_count(mpcg_session* s, uint64_t* n);
+int mpcg_session_trace_get(mpcg_session* s, uint64_t i, uint32_t* seq, int* kind, uint64_t* bytes, double t[4],
+                           char* tag, int tag_cap);
+int mpcg_session_clear_trace(mpcg_session* s);
+/* Host wall seconds since the session was created. */
+int mpcg_session_now(mpcg_session* s, double* out);
+/* Fault injection: the session's compute stream idles `seconds` at this point. */
+int mpcg_session_add_delay(mpcg_session* s, double seconds);
 
 /* ---- tensors (device RingTensor shares; ring/tensor.hpp:36-76) ---- */
 int mpcg_tensor_create(mpcg_session* s, int ndim, const uint64_t* dims, int scale_bits,
@@ -158,7 +172,8 @@ int mpcg_executor_create(mpcg_session* s, const mpcg_model* m, int public_weight
                          uint64_t chunk_threshold, int merged_adder, mpcg_executor** out);
 /* deal_weight_shares / public_weight_set (engine/executor.hpp:49-68). */
 int mpcg_executor_deal_weights(mpcg_executor* e, int count, const char* const* names,
-                               const double* const* values, uint64_t seed);
+                               const double* const* values, const uint64_t* counts /* doubles per tensor */,
+                               uint64_t seed);
 int mpcg_executor_run(mpcg_executor* e, const mpcg_tensor* input, mpcg_tensor** out); /* executor.hpp:193 */
 /* CUDA-graph form of run(): capture one steady-state inference that reads `input` in place
  * (pipelined mode needs one mpcg_executor_run first), then each replay performs the next
@@ -166,6 +181,10 @@ int mpcg_executor_run(mpcg_executor* e, const mpcg_tensor* input, mpcg_tensor** 
  * replay output is valid until the next replay. */
 int mpcg_executor_capture(mpcg_executor* e, const mpcg_tensor* input);
 int mpcg_executor_replay(mpcg_executor* e, mpcg_tensor** out);
+/* While a graph is held, eager runs and the session's other triple-fetching ops fail with
+ * MPCG_ERR_USAGE (the graph owns the dealer streams). Releasing it hands them back: the next
+ * run() continues the iteration sequence where the last replay left it. */
+int mpcg_executor_release_graph(mpcg_executor* e);
 /* Per-layer device times (ms) of the next runs: enable=1 turns timing on. */
 int mpcg_executor_time_layers(mpcg_executor* e, int enable);
 int mpcg_executor_layer_times(mpcg_executor* e, int max, float* ms, int* count);
@@ -174,12 +193,14 @@ int mpcg_executor_destroy(mpcg_executor* e);
 /* Ring-GEMM engine: 0 = SIMT only, 1 = tcgen05 int8-limb path for every shape within its
  * exact-accumulation budget (K' <= 16384), 2 = auto (tcgen05 for large shapes; default). */
 int mpcg_set_gemm_mode(int mode);
+/* 1-GPU mode: pair evaluation (1, default: one thread evaluates both local party slots of an
+ * element and writes each open's opened value once; summed eps/delta opens) or per-slot
+ * kernels (0: each slot writes its own payload and reads the peer's, as two separate parties
+ * do). Values are identical. Process-wide; affects kernels launched or captured afterwards. */
+int mpcg_set_pair_eval(int on);
 /* Small-M combines (M <= 16, unbatched): fused-segment streaming kernel (1, default) or the
  * tiled SIMT/tcgen05 paths (0). */
 int mpcg_set_gemv(int on);
-/* tcgen05 generation: 1 = warp-specialised pipeline (operands generated in producer warps or
- * packed once, bulk-copied; default), 0 = first-generation kernel (materialised operands). */
-int mpcg_set_tc2(int on);
 /* Debug: stage timestamps (clock64) of the last tcgen05 GEMM's first CTA when MPCG_TC2_TRACE=1;
  * [stage][10] = MMA wait start/end/issue end, generated-producer and memory-producer
  * empty-wait start/end/arrive. */

@@ -58,6 +58,11 @@ SIGNATURES = {
     "mpcg_session_stats": [P, I32, U64P],
     "mpcg_session_n_local": [P, C.POINTER(I32)],
     "mpcg_session_trace": [P, I32],
+    "mpcg_session_trace_count": [P, U64P],
+    "mpcg_session_trace_get": [P, U64, C.POINTER(C.c_uint32), C.POINTER(I32), U64P, C.POINTER(DBL), C.c_char_p, I32],
+    "mpcg_session_clear_trace": [P],
+    "mpcg_session_now": [P, C.POINTER(DBL)],
+    "mpcg_session_add_delay": [P, DBL],
     "mpcg_tensor_create": [P, I32, U64P, I32, U64P, PP],
     "mpcg_tensor_download": [P, U64P],
     "mpcg_tensor_shape": [P, C.POINTER(I32), U64P, C.POINTER(I32)],
@@ -90,7 +95,9 @@ SIGNATURES = {
     "mpcg_global_avg_pool": [P, P, U64, U64, U64, PP],
     "mpcg_model_destroy": [P],
     "mpcg_executor_create": [P, P, I32, I32, I32, U64, I32, PP],
-    "mpcg_executor_deal_weights": [P, I32, C.POINTER(C.c_char_p), C.POINTER(C.POINTER(DBL)), U64],
+    "mpcg_executor_deal_weights": [P, I32, C.POINTER(C.c_char_p), C.POINTER(C.POINTER(DBL)), C.POINTER(U64), U64],
+    "mpcg_executor_release_graph": [P],
+    "mpcg_set_pair_eval": [I32],
     "mpcg_executor_run": [P, P, PP],
     "mpcg_executor_capture": [P, P],
     "mpcg_executor_replay": [P, PP],
@@ -99,7 +106,6 @@ SIGNATURES = {
     "mpcg_executor_destroy": [P],
     "mpcg_set_gemm_mode": [I32],
     "mpcg_set_gemv": [I32],
-    "mpcg_set_tc2": [I32],
     "mpcg_debug_tc2_trace": [U64P, I32],
     "mpcg_session_connect_loopback": [P, P],
     "mpcg_launch_count": [],

@@ -83,6 +83,40 @@ class Session:
         auto by size (2, the session default)."""
         N.call("mpcg_session_set_persistent", self._h, int(mode))
 
+    def trace(self, enable=True):
+        """Record one row per collective (Communicator::trace, H/transport/transport.hpp:25-37)
+        with device timestamps; see trace_rows()."""
+        N.call("mpcg_session_trace", self._h, int(enable))
+
+    def trace_rows(self):
+        """Synchronise and return the trace: dicts with seq, kind, tag, bytes, t_issue, t_sent,
+        t_wait_begin, t_wait_end (seconds since trace start), occupancy, stall."""
+        n = C.c_uint64()
+        N.call("mpcg_session_trace_count", self._h, C.byref(n))
+        rows = []
+        seq, kind, nb = C.c_uint32(), C.c_int32(), C.c_uint64()
+        t = (C.c_double * 4)()
+        buf = C.create_string_buffer(256)
+        for i in range(n.value):
+            N.call("mpcg_session_trace_get", self._h, i, C.byref(seq), C.byref(kind), C.byref(nb), t, buf, 256)
+            rows.append({"seq": seq.value, "kind": "xor" if kind.value else "sum", "tag": buf.value.decode(),
+                         "bytes": nb.value, "t_issue": t[0], "t_sent": t[1], "t_wait_begin": t[2],
+                         "t_wait_end": t[3], "occupancy": t[1] - t[0], "stall": t[3] - t[2]})
+        return rows
+
+    def clear_trace(self):
+        N.call("mpcg_session_clear_trace", self._h)
+
+    def now(self) -> float:
+        """Host wall seconds since the session was created (Communicator::now)."""
+        v = C.c_double()
+        N.call("mpcg_session_now", self._h, C.byref(v))
+        return v.value
+
+    def add_delay(self, seconds: float):
+        """Fault injection (Communicator::add_delay): this session's stream idles `seconds`."""
+        N.call("mpcg_session_add_delay", self._h, float(seconds))
+
     def stats(self, slot=0):
         out = (C.c_uint64 * 3)()
         N.call("mpcg_session_stats", self._h, slot, out)
@@ -252,14 +286,16 @@ def global_avg_pool(s, x, N_, C_, HW):
     return _op("mpcg_global_avg_pool", s, x.handle, N_, C_, HW)
 
 
+def set_pair_eval(on: bool = True):
+    """1-GPU mode: one thread evaluates both co-located party slots and writes each open's
+    opened value once (True, default), or per-slot kernels with two payloads per open, as two
+    separate parties compute (False). Values are identical; set before building executors."""
+    N.call("mpcg_set_pair_eval", int(on))
+
+
 def set_gemv(on: bool = True):
     """Small-M combines: fused-segment streaming kernel (True) or the tiled GEMM paths."""
     N.call("mpcg_set_gemv", int(on))
-
-
-def set_tc2(on: bool = True):
-    """tcgen05 kernel generation: warp-specialised pipeline (True) or the first-generation one."""
-    N.call("mpcg_set_tc2", int(on))
 
 
 def set_gemm_mode(mode: str = "auto"):
@@ -322,6 +358,38 @@ def timer(s: Session, op: str) -> float:
     return ms.value
 
 
+# ---- run report (H/engine/report.hpp:25-81) --------------------------------------
+def linear_tags(g: ModelGraph):
+    """SecureExecutor::linear_tags (H/engine/executor.hpp:208-218): one per weight op, in
+    build order; attention packs Wqkv and Wo as two ops."""
+    tags = []
+    for l in g.layers:
+        if l.type in ("dense", "conv2d"):
+            tags.append(l.name + ".mm")
+        elif l.type == "attention":
+            tags += [l.name + ".qkv", l.name + ".proj"]
+    return tags
+
+
+def _belongs(tag, prefixes):
+    return any(len(tag) > len(t) and tag.startswith(t) and tag[len(t)] == "." for t in prefixes)
+
+
+def party_report_fields(rows, g: ModelGraph):
+    """stall_s, occupancy_s, delta_wait_s, first_delta_wait_s, linear_comm_s, linear_bytes of
+    a PartyReport (H/engine/report.hpp:42-81, H/engine/bench.hpp:61-78) from trace rows."""
+    tags = linear_tags(g)
+    first = tags[0] if tags else ""
+    hideable = [t for t in tags if t != first]
+    return {"stall_s": sum(r["stall"] for r in rows),
+            "occupancy_s": sum(r["occupancy"] for r in rows),
+            "delta_wait_s": sum(r["stall"] for r in rows if r["tag"].endswith(".delta") and _belongs(r["tag"], hideable)),
+            "first_delta_wait_s": sum(r["stall"] for r in rows if r["tag"].endswith(".delta")
+                                      and _belongs(r["tag"], [first])) if first else 0.0,
+            "linear_comm_s": sum(r["occupancy"] for r in rows if _belongs(r["tag"], tags)),
+            "linear_bytes": sum(r["bytes"] for r in rows if _belongs(r["tag"], tags))}
+
+
 def fnv1a_words(words: np.ndarray) -> int:
     a = np.ascontiguousarray(words, dtype=np.uint64).reshape(-1)
     return int(N.lib().mpcg_fnv1a_words(_u64p(a), a.size))
@@ -357,11 +425,21 @@ class SecureExecutor:
             pass
 
     def deal_weights(self, weights: dict, seed: int):
+        """deal_weight_shares / public_weight_set (H/engine/executor.hpp:49-68), after the
+        reference's check_weights (H/engine/model.hpp:366-376); the C ABI re-checks every
+        tensor's element count before reading it."""
+        from .model import check_weights
+        check_weights(self.graph, weights)
         names = sorted(weights)
         arrs = [np.ascontiguousarray(weights[k], dtype=np.float64).reshape(-1) for k in names]
         cn = (C.c_char_p * len(names))(*[n.encode() for n in names])
         cv = (C.POINTER(C.c_double) * len(names))(*[a.ctypes.data_as(C.POINTER(C.c_double)) for a in arrs])
-        N.call("mpcg_executor_deal_weights", self._h, len(names), cn, cv, seed)
+        counts = np.array([a.size for a in arrs], dtype=np.uint64)
+        N.call("mpcg_executor_deal_weights", self._h, len(names), cn, cv, _u64p(counts), seed)
+
+    def release_graph(self):
+        """Drop the captured graph so run() and other session ops may fetch triples again."""
+        N.call("mpcg_executor_release_graph", self._h)
 
     def run(self, x: Tensor) -> Tensor:
         h = C.c_void_p()

@@ -108,6 +108,7 @@ def run_one_mode(g, w, x, a, mode, threshold):
     iters, layer_ms = [], np.zeros(len(g.layers))
     out = None
     st0 = s.stats(0)
+    s.trace(True)
     for _ in range(a.iterations):
         api.timer(s, "reset")
         api.timer(s, "start")
@@ -119,12 +120,15 @@ def run_one_mode(g, w, x, a, mode, threshold):
     z = out.numpy()
     opened = (z[0] + z[1]).reshape(-1)
     logits = opened.view(np.int64).astype(np.float64) * 2.0 ** -g.frac_bits
+    rows = s.trace_rows()
+    fields = api.party_report_fields(rows, g)
     parties = []
-    for p in (0, 1):
+    for p in (0, 1):  # both parties' collectives are the session's rows (same order, same bytes)
         st = s.stats(p)
-        parties.append({"party": p, "iter_wall_s": iters, "wall_s": float(sum(iters)),
-                        "bytes_sent": st["bytes_sent"], "collectives": st["collectives"],
-                        "p2p_sends": st["p2p_sends"]})
+        parties.append(dict({"party": p, "iter_wall_s": iters, "wall_s": float(sum(iters)),
+                             "bytes_sent": st["bytes_sent"] - st0["bytes_sent"],
+                             "collectives": st["collectives"] - st0["collectives"],
+                             "p2p_sends": st["p2p_sends"] - st0["p2p_sends"]}, **fields))
     rep = {"schema": 1, "model": g.name, "mode": mode, "weights": a.weights,
            "session": {"n_parties": 2, "backend": a.backend, "latency_s": link[0] if link else 0.0,
                        "bandwidth_bps": link[1] if link else None, "seed": a.seed, "device": a.device},

@@ -119,9 +119,15 @@ int mpcg_session_set_pipeline(mpcg_session* s, int chunks, uint64_t threshold, i
 int mpcg_session_set_link(mpcg_session* s, double latency_s, double bw, double msg) {
   return guard([&] {
     Session& ss = S(s);
+    // transport/config.hpp:34-38: latency >= 0, bandwidth > 0. (0, 0, 0) removes the emulated
+    // link (the real in-device / NVLink transport); a latency-only link is rejected like the
+    // reference rejects bandwidth <= 0, instead of silently running as an ideal link.
     if (latency_s < 0) throw Error(kConfigError, "latency must be >= 0");
+    if (msg < 0) throw Error(kConfigError, "sec_per_message must be >= 0");
+    const bool off = latency_s == 0 && bw == 0 && msg == 0;
+    if (!off && !(bw > 0)) throw Error(kConfigError, "bandwidth must be > 0");
     ss.cfg.link_latency_s = latency_s;
-    ss.cfg.link_bandwidth = bw > 0 ? bw : 0;
+    ss.cfg.link_bandwidth = off ? 0 : bw;
     ss.cfg.sec_per_message = msg;
   });
 }
@@ -168,7 +174,52 @@ int mpcg_session_n_local(mpcg_session* s, int* out) {
 }
 
 int mpcg_session_trace(mpcg_session* s, int enable) {
-  return guard([&] { S(s).trace_on = enable != 0; });
+  return guard([&] { S(s).set_trace(enable != 0); });
+}
+
+int mpcg_session_trace_count(mpcg_session* s, uint64_t* n) {
+  return guard([&] {
+    need(n, "n");
+    *n = S(s).trace_rows().size();
+  });
+}
+
+int mpcg_session_trace_get(mpcg_session* s, uint64_t i, uint32_t* seq, int* kind, uint64_t* bytes, double t[4],
+                           char* tag, int tag_cap) {
+  return guard([&] {
+    const auto& rows = S(s).trace_rows();
+    if (i >= rows.size()) throw Error(kRangeError, "trace row out of range");
+    const TraceEvent& r = rows[size_t(i)];
+    if (seq) *seq = r.seq;
+    if (kind) *kind = int(r.kind);
+    if (bytes) *bytes = r.bytes;
+    if (t) {
+      t[0] = r.t_issue;
+      t[1] = r.t_sent;
+      t[2] = r.t_wait_begin;
+      t[3] = r.t_wait_end;
+    }
+    if (tag && tag_cap > 0) {
+      const size_t n = std::min(r.tag.size(), size_t(tag_cap - 1));
+      std::memcpy(tag, r.tag.data(), n);
+      tag[n] = 0;
+    }
+  });
+}
+
+int mpcg_session_clear_trace(mpcg_session* s) {
+  return guard([&] { S(s).clear_trace(); });
+}
+
+int mpcg_session_now(mpcg_session* s, double* out) {
+  return guard([&] {
+    need(out, "out");
+    *out = S(s).now();
+  });
+}
+
+int mpcg_session_add_delay(mpcg_session* s, double seconds) {
+  return guard([&] { S(s).add_delay(seconds); });
 }
 
 int mpcg_tensor_create(mpcg_session* s, int ndim, const uint64_t* dims, int scale, const uint64_t* host,
@@ -394,16 +445,28 @@ int mpcg_executor_create(mpcg_session* s, const mpcg_model* m, int pub, int pipe
 }
 
 int mpcg_executor_deal_weights(mpcg_executor* e, int count, const char* const* names, const double* const* values,
-                               uint64_t seed) {
+                               const uint64_t* counts, uint64_t seed) {
   return guard([&] {
     need(e, "executor");
+    if (count < 0) throw Error(kConfigError, "negative weight count");
+    if (count > 0 && (!names || !values || !counts)) throw Error(kUsageError, "null weight arrays");
     std::vector<std::string> n;
     std::vector<const double*> v;
+    std::vector<size_t> k;
     for (int i = 0; i < count; ++i) {
+      if (!names[i]) throw Error(kUsageError, "null weight name");
       n.emplace_back(names[i]);
       v.push_back(values[i]);
+      k.push_back(size_t(counts[i]));
     }
-    e->e->deal_weights(n, v, seed);
+    e->e->deal_weights(n, v, k, seed);
+  });
+}
+
+int mpcg_executor_release_graph(mpcg_executor* e) {
+  return guard([&] {
+    need(e, "executor");
+    e->e->release_graph();
   });
 }
 
@@ -469,8 +532,11 @@ int mpcg_debug_tc2_trace(uint64_t* out, int n) {
   return guard([&] { tc2_trace_read(reinterpret_cast<unsigned long long*>(out), n); });
 }
 
-int mpcg_set_tc2(int on) {
-  return guard([&] { tc2_mode() = on ? 1 : 0; });
+int mpcg_set_pair_eval(int on) {
+  return guard([&] {
+    pair_eval_enabled() = on != 0;
+    eps_fuse_enabled() = on != 0;
+  });
 }
 
 int mpcg_set_gemv(int on) {

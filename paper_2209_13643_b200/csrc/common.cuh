@@ -223,7 +223,19 @@ __device__ __forceinline__ u64 mm_rC(const MmTriple& t, u64 k) {
 }
 
 // ------------------------------------------------------------------ launch helpers
-constexpr int kSms = 148;
+// SM count of the current device, queried once per device (148 on a full B200; fewer under
+// MIG / MPS partitions). Sizes persistent/cooperative grids and the split-K heuristics.
+inline int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev] = v;
+  }
+  return cache[dev];
+}
 
 // Instrumentation: count of kernels this library launched, and an optional probe that
 // brackets every launch of one kernel class with CUDA events (bench.py's live roofline).
@@ -311,7 +323,7 @@ __global__ void __launch_bounds__(256) ew_kernel(u64 n, F f) {
 
 inline unsigned ew_blocks(u64 n) {
   u64 b = (n + 255) / 256;
-  const u64 cap = u64(kSms) * 8;  // 8 resident 256-thread CTAs per SM
+  const u64 cap = u64(num_sms()) * 8;  // 8 resident 256-thread CTAs per SM
   return static_cast<unsigned>(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
@@ -327,6 +339,14 @@ struct has_both<F, std::void_t<decltype(std::declval<const F&>().both(u64(0)))>>
 inline bool& pair_eval_enabled() {
   static bool on = [] {
     const char* e = std::getenv("MPCG_PAIR_EVAL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+// Summed in-device opens of the matmul combine's eps / delta (MPCG_EPS_FUSE=0: both payloads).
+inline bool& eps_fuse_enabled() {
+  static bool on = [] {
+    const char* e = std::getenv("MPCG_EPS_FUSE");
     return !(e && e[0] == '0');
   }();
   return on;

@@ -2,6 +2,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -181,12 +182,19 @@ Session::Session(int dev, int nl, int party, u64 sd, u64 mask_seed, int frac_bit
   debug_sync = dbg && dbg[0] == '1';
   const char* per = std::getenv("MPCG_PERSISTENT");
   if (per && (per[0] == '0' || per[0] == '1')) persistent_mode = per[0] - '0';
+  created_ = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+double Session::now() const {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count() - created_;
 }
 
 Session::~Session() {
   cudaStreamSynchronize(stream);
   cudaStreamSynchronize(comm_stream);
   for (auto e : events_) cudaEventDestroy(e);
+  for (auto e : trace_events_) cudaEventDestroy(e);
+  if (trace_epoch_) cudaEventDestroy(trace_epoch_);
   for (auto& [a, b] : timer_ev) {
     cudaEventDestroy(a);
     if (b) cudaEventDestroy(b);
@@ -223,7 +231,28 @@ u64 Session::tag_stream(const std::string& tag) {
   return mix64(h + 0x51ed270bull * tag_counts[h]++);
 }
 
+void Session::require_eager_streams(const char* what) const {
+  // A captured graph replays fixed fetch/mask positions from host counters it advances per
+  // replay; an eager fetch in between would desynchronise the two and make the next replay
+  // reuse triples. Release the graph first.
+  if (cap.exec && !cap.active)
+    throw Error(kUsageError, std::string(what) + ": the session holds a captured graph that owns its dealer "
+                                                 "streams; release it (mpcg_executor_release_graph) first");
+}
+
+void Session::release_graph() {
+  if (cap.active) throw Error(kUsageError, "release_graph during a capture");
+  if (cap.exec) {
+    MPCG_CUDA(cudaStreamSynchronize(stream));
+    cudaGraphExecDestroy(cap.exec);
+    cudaGraphDestroy(cap.graph);
+    cap.exec = nullptr;
+    cap.graph = nullptr;
+  }
+}
+
 Triple Session::fetch(const TripleSpec& spec, const std::string& tag, bool batch_b) {
+  require_eager_streams("fetch");
   Triple t;
   t.spec = spec;
   const u64* kp = nullptr;
@@ -285,6 +314,7 @@ Triple Session::fetch(const TripleSpec& spec, const std::string& tag, bool batch
 }
 
 Session::MaskRef Session::take_mask(u64 numel_local) {
+  require_eager_streams("a2b mask");
   const u64 base = mask_ctr + dp_offset(numel_local);
   mask_ctr += dp_global(numel_local);
   MaskRef r{base, nullptr};
@@ -460,6 +490,73 @@ void Session::throttle(Open& o) {
   MPCG_CUDA(cudaGetLastError());
 }
 
+// ------------------------------------------------------------------ trace
+void Session::set_trace(bool on) {
+  if (on && !trace_epoch_) {
+    MPCG_CUDA(cudaEventCreate(&trace_epoch_));
+    MPCG_CUDA(cudaEventRecord(trace_epoch_, stream));
+  }
+  trace_on = on;
+}
+
+void Session::clear_trace() {
+  sync();
+  trace.clear();
+  trace_marks_.clear();
+  for (auto e : trace_events_) cudaEventDestroy(e);
+  trace_events_.clear();
+  trace_resolved_ = 0;
+  ++trace_gen_;
+  if (trace_epoch_) MPCG_CUDA(cudaEventRecord(trace_epoch_, stream));
+}
+
+cudaEvent_t Session::trace_event(cudaStream_t st) {
+  cudaEvent_t e;
+  MPCG_CUDA(cudaEventCreate(&e));
+  trace_events_.push_back(e);
+  MPCG_CUDA(cudaEventRecord(e, st));
+  return e;
+}
+
+const std::vector<TraceEvent>& Session::trace_rows() {
+  sync();
+  auto at = [&](cudaEvent_t e) {
+    float ms = 0;
+    MPCG_CUDA(cudaEventElapsedTime(&ms, trace_epoch_, e));
+    return double(ms) * 1e-3;
+  };
+  for (; trace_resolved_ < trace.size(); ++trace_resolved_) {
+    TraceEvent& r = trace[trace_resolved_];
+    const TraceMarks& m = trace_marks_[trace_resolved_];
+    if (!m.issue) continue;  // captured / in-kernel open: no timestamps
+    r.t_issue = at(m.issue);
+    r.t_sent = m.busy_s >= 0 ? r.t_issue + m.busy_s : (m.sent ? std::max(r.t_issue, at(m.sent)) : r.t_issue);
+    r.t_wait_begin = m.wait_begin ? at(m.wait_begin) : r.t_sent;
+    r.t_wait_end = m.wait_end ? std::max(r.t_wait_begin, at(m.wait_end)) : r.t_wait_begin;
+  }
+  return trace;
+}
+
+namespace {
+__global__ void delay_kernel(u64 ns) {
+  u64 t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 >= ns) break;
+    __nanosleep(1000);
+  }
+}
+}  // namespace
+
+void Session::add_delay(double seconds) {
+  if (!(seconds >= 0)) throw Error(kConfigError, "add_delay: seconds must be >= 0");
+  if (seconds == 0) return;
+  delay_kernel<<<1, 1, 0, stream>>>(u64(seconds * 1e9));
+  MPCG_CUDA(cudaGetLastError());
+}
+
 u32 Session::account(size_t nwords, Reduce kind, const std::string& tag, bool p2p) {
   const u32 seq = next_seq++;  // collective order = post order (what both parties must agree on)
   for (int i = 0; i < n_local; ++i) {
@@ -469,7 +566,10 @@ u32 Session::account(size_t nwords, Reduce kind, const std::string& tag, bool p2
     else
       stats[i].collectives++;
   }
-  if (trace_on) trace.push_back(TraceEvent{seq, kind, tag, nwords * 8});
+  if (trace_on) {
+    trace.push_back(TraceEvent{seq, kind, tag, nwords * 8});
+    trace_marks_.push_back(TraceMarks{});
+  }
   return seq;
 }
 
@@ -487,6 +587,14 @@ void Session::post(Open& o, const std::string& tag, bool p2p) {
   o.posted = true;
   o.seq = account(o.n, o.kind, tag, p2p);
   const bool throttled = cfg.link_bandwidth > 0;
+  TraceMarks* tm = nullptr;
+  if (trace_on && !cap.active) {
+    o.trace_idx = long(trace.size()) - 1;
+    o.trace_gen = trace_gen_;
+    tm = &trace_marks_.back();
+    tm->issue = trace_event(stream);
+    if (throttled) tm->busy_s = cfg.sec_per_message + double(o.n * 8) / cfg.link_bandwidth;
+  }
   if (n_local == 2 && !throttled) {
     check();
     return;  // zero-copy: the peer reads our outbox after the stream-ordered kernel boundary
@@ -527,6 +635,7 @@ void Session::post(Open& o, const std::string& tag, bool p2p) {
     nccl_check(api.Recv(o.in->ptr, o.n, ncclUint64, peer, nccl, comm_stream), "ncclRecv");
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
   }
+  if (tm && n_local == 1) tm->sent = trace_event(comm_stream);  // transfer done
   if (throttled) throttle(o);
   o.ready = pool_event();
   MPCG_CUDA(cudaEventRecord(o.ready, comm_stream));
@@ -537,7 +646,11 @@ void Session::wait(Open& o) {
   if (o.waited) throw Error(kUsageError, "wait() called twice on one handle");
   if (!o.posted) throw Error(kUsageError, "wait() on an open that was never posted");
   o.waited = true;
+  const bool timed = o.trace_idx >= 0 && o.trace_gen == trace_gen_ && size_t(o.trace_idx) < trace_marks_.size() &&
+                     !cap.active;
+  if (timed) trace_marks_[size_t(o.trace_idx)].wait_begin = trace_event(stream);
   if (o.ready) MPCG_CUDA(cudaStreamWaitEvent(stream, o.ready, 0));
+  if (timed) trace_marks_[size_t(o.trace_idx)].wait_end = o.ready ? trace_event(stream) : nullptr;
 }
 
 }  // namespace mpcg

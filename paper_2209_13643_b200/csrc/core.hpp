@@ -69,12 +69,23 @@ struct DT {
 
 enum class Reduce : int { Sum = 0, Xor = 1 };
 
-// Per-party communication counters (H/transport/transport.hpp:25-45).
+// One row per collective a party issued (H/transport/transport.hpp:25-37), with device
+// timestamps in seconds since the trace was enabled:
+//   t_issue      the compute stream reached the post (payload built, send issued)
+//   t_sent       sender occupancy charged: the emulated link's busy time (msg + bytes/bw, the
+//                sim model of H/transport/sim.hpp:90-92) or the NCCL / loopback transfer done
+//   t_wait_begin the compute stream reached wait() (all work before it done)
+//   t_wait_end   the stream resumed (the payload had arrived); == t_wait_begin when it was there
+// In-device zero-copy opens have no transfer: occupancy and stall are 0. Opens inside a CUDA
+// graph capture and in-kernel (persistent chain) opens carry no timestamps (all 0).
 struct TraceEvent {
   u32 seq;
   Reduce kind;
   std::string tag;
   u64 bytes;
+  double t_issue = 0, t_sent = 0, t_wait_begin = 0, t_wait_end = 0;
+  double occupancy() const { return t_sent - t_issue; }
+  double stall() const { return t_wait_end - t_wait_begin; }
 };
 struct CommStats {
   u64 bytes_sent = 0;
@@ -122,6 +133,8 @@ struct Open {
   u32 seq = 0;
   bool waited = false;
   bool posted = false;
+  long trace_idx = -1;           // row in Session::trace when its timestamps are recorded
+  u64 trace_gen = 0;             // Session::trace_gen_ when the row was made (clear_trace bumps it)
   cudaEvent_t ready = nullptr;   // arrival (throttled link or NCCL), or null
   // n_local == 2 only, set by the caller before the build: the build writes the opened value
   // (own0 + own1 — what both parties read after the zero-copy open) once into own(0) instead
@@ -231,6 +244,8 @@ class Session {
   void begin_capture();
   void end_capture();
   void replay();
+  void release_graph();
+  void require_eager_streams(const char* what) const;
 
   // ---- wire
   Open begin_open(size_t nwords, Reduce kind, std::shared_ptr<Block> out = nullptr,
@@ -252,6 +267,14 @@ class Session {
   CommStats stats[2];
   std::vector<TraceEvent> trace;
   bool trace_on = false;
+  void set_trace(bool on);
+  void clear_trace();
+  // Synchronises, resolves the device timestamps of every traced row and returns them.
+  const std::vector<TraceEvent>& trace_rows();
+  // Host wall seconds since the session was created (Communicator::now, socket backend).
+  double now() const;
+  // Fault injection (Communicator::add_delay): the compute stream idles `seconds` here.
+  void add_delay(double seconds);
 
   void sync();
   void check();  // debug: sync + error check when MPCG_DEBUG_SYNC=1
@@ -265,6 +288,19 @@ class Session {
  private:
   void throttle(Open& o);
   cudaEvent_t pool_event();
+  cudaEvent_t trace_event(cudaStream_t st);  // timing event recorded on `st`, owned by the trace
+  struct TraceMarks {
+    cudaEvent_t issue = nullptr, sent = nullptr, wait_begin = nullptr, wait_end = nullptr;
+    double busy_s = -1;  // emulated link: modelled sender occupancy
+  };
+  std::vector<TraceMarks> trace_marks_;
+  std::vector<cudaEvent_t> trace_events_;
+  cudaEvent_t trace_epoch_ = nullptr;
+  size_t trace_resolved_ = 0;
+ public:
+  u64 trace_gen_ = 0;
+ private:
+  double created_ = 0;
   std::vector<cudaEvent_t> events_;
   size_t event_next_ = 0;
   u64* link_state_ = nullptr;  // device: [next free ns]

@@ -176,11 +176,11 @@ void mul_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::stri
   chunks = clamp_chunks(chunks, m);
   std::vector<Open> opens(static_cast<size_t>(chunks));
   const Pid2 pid = pids(s);
-  // beaver_mul = 2 x 16 B wire + 8 x (2 in + 1 out) = 56 B/elem/party over build +
-  // combine; with the opened wire (pair evaluation) the 16 B opened pair is written and read once
-  // per element pair: 8 x 3 + 16 = 40 B/elem/party
+  // SURVEY 8(d) algorithmic bytes: beaver_mul = 2 x 16 B wire + 8 x (2 in + 1 out) = 56 B/elem/
+  // party over build + combine (28 per launch). The opened wire (pair evaluation) moves less — the
+  // 16 B opened pair is written and read once per element pair — but the roofline counts 8(d)'s.
   const bool opened = adder_opened_wire(s);
-  ClassScope cs(kClsBeaver, (opened ? 20.0 : 28.0) * double(m / chunks) * s.n_local);
+  ClassScope cs(kClsBeaver, 28.0 * double(m / chunks) * s.n_local);
   for (int k = 0; k < chunks; ++k) {
     const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
     opens[k] = s.begin_open(2 * (hi - lo), Reduce::Sum);
@@ -220,7 +220,7 @@ template <class VF, class OF>
 void row_reduce(Session& s, u64 rows, u32 L, VF vf, OF of) {
   if (rows == 0) return;
   u64 blocks = (rows * 32 + 255) / 256;
-  const u64 cap = u64(kSms) * 8;
+  const u64 cap = u64(num_sms()) * 8;
   blocks = blocks > cap ? cap : blocks;
   cudaEvent_t pe;
   probe_begin(s.stream, &pe);
@@ -316,9 +316,9 @@ void square_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::s
   std::vector<Open> opens(static_cast<size_t>(chunks));
   const Pid2 pid = pids(s);
   // beaver_square = 2 x 8 B wire + 8 x (1 in + 1 out) = 32 B/elem/party over build + combine
-  // (opened wire: 8 B written + read once per element pair = 24 B/elem/party)
+  // (the opened wire moves 24 B, the roofline counts 8(d)'s 32)
   const bool opened = adder_opened_wire(s);
-  ClassScope cs(kClsBeaver, (opened ? 12.0 : 16.0) * double(m / chunks) * s.n_local);
+  ClassScope cs(kClsBeaver, 16.0 * double(m / chunks) * s.n_local);
   for (int k = 0; k < chunks; ++k) {
     const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
     opens[k] = s.begin_open(hi - lo, Reduce::Sum);
@@ -1020,11 +1020,10 @@ void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& 
     }
     if (rn > c.levels) k.ff = ff_for_lane(lane, lo, hi - lo);
     // algorithmic bytes per element per party (2 x wire + 8 x (in + out)):
-    // level round = 2x32 wire + 8x(2 state in + 2 state out) = 96 B; with the opened wire
-    // (pair evaluation) the 32-byte opened value is written once and read once per element
-    // pair: 32 + 32 state = 64 B per element per party
-    ClassScope cs(rn >= 1 && rn <= c.levels ? kClsAdderRound : kClsOther,
-                  (adder_opened_wire(s) ? 64.0 : 96.0) * double(hi - lo) * s.n_local);
+    // level round = 2x32 wire + 8x(2 state in + 2 state out) = 96 B. With the opened wire (pair
+    // evaluation) the 32-byte opened value is written once and read once per element pair
+    // (64 B per element per party moved); the roofline counts 8(d)'s algorithmic 96 B.
+    ClassScope cs(rn >= 1 && rn <= c.levels ? kClsAdderRound : kClsOther, 96.0 * double(hi - lo) * s.n_local);
     launch_ew(s.stream, s.n_local, hi - lo, k);
   };
   fetch_round(0);
@@ -1149,7 +1148,7 @@ void persistent_beaver_chain(Session& s, u64 n, const B0& build, const std::vect
     MPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
     if (per_sm < 1) throw Error(kInternalError, "beaver chain kernel cannot be resident");
   }
-  const u64 cap = u64(per_sm) * kSms / gy;
+  const u64 cap = u64(per_sm) * num_sms() / gy;
   u64 blocks = (n + 255) / 256;
   blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);
   cudaLaunchConfig_t lc{};

@@ -145,6 +145,13 @@ SecureExecutor::SecureExecutor(Session& s, ModelGraph g, bool public_weights, Ex
 }
 
 SecureExecutor::~SecureExecutor() {
+  if (captured_) {  // the session's dealer streams return to eager use
+    try {
+      s_.sync();
+      s_.release_graph();
+    } catch (...) {
+    }
+  }
   for (auto e : ev_) cudaEventDestroy(e);
 }
 
@@ -195,14 +202,23 @@ void SecureExecutor::build_weight_ops() {
 }
 
 void SecureExecutor::deal_weights(const std::vector<std::string>& names, const std::vector<const double*>& values,
-                                  u64 seed) {
+                                  const std::vector<size_t>& counts, u64 seed) {
+  // check_weights (H/engine/model.hpp:366-376): same entries, same shapes, before any read
   const auto expected = model_weight_shapes(g_);
   if (names.size() != expected.size()) throw Error(kConfigError, "weights entry count mismatch for model " + g_.name);
+  if (values.size() != names.size() || counts.size() != names.size())
+    throw Error(kUsageError, "deal_weights: names, values and counts differ in length");
   std::map<std::string, const double*> byname;
-  for (size_t i = 0; i < names.size(); ++i) byname[names[i]] = values[i];
+  std::map<std::string, size_t> given;
+  for (size_t i = 0; i < names.size(); ++i) {
+    byname[names[i]] = values[i];
+    given[names[i]] = counts[i];
+  }
   std::map<std::string, Shape> shapes;
   for (auto& [k, sh] : expected) {
     if (!byname.count(k)) throw Error(kConfigError, "missing weight tensor: " + k);
+    if (given.at(k) != shape_numel(sh)) throw Error(kConfigError, "wrong shape for weight tensor: " + k);
+    if (!byname.at(k) && given.at(k)) throw Error(kUsageError, "null values for weight tensor: " + k);
     shapes[k] = sh;
   }
   HostRng rng(seed, 0x3e1f);  // one stream over sorted names (H/engine/executor.hpp:49-59)
@@ -495,7 +511,28 @@ DT SecureExecutor::replay() {
   return graph_out_;
 }
 
+// Hand the dealer streams back to eager calls. A triple prefetched inside the graph (the
+// pipelined wrap-around) reads its key from the device key table, which holds the key of the
+// last replay's prefetch; it is pinned to that key so the next eager run() consumes exactly
+// the triple whose delta the last replay left in the persistent payload buffer.
+void SecureExecutor::release_graph() {
+  if (!captured_) return;
+  s_.sync();
+  for (auto& op : wops_)
+    if (op.triple && (op.triple->ew.kp || op.triple->mm.kp)) {
+      const u64* kp = op.triple->mm.kp ? op.triple->mm.kp : op.triple->ew.kp;
+      u64 key = 0;
+      MPCG_CUDA(cudaMemcpy(&key, kp, sizeof key, cudaMemcpyDeviceToHost));
+      op.triple->key = op.triple->ew.key = op.triple->mm.key = key;
+      op.triple->ew.kp = op.triple->mm.kp = nullptr;
+    }
+  s_.release_graph();
+  captured_ = false;
+  graph_out_ = DT{};
+}
+
 DT SecureExecutor::run(const DT& input) {
+  if (!s_.cap.active) s_.require_eager_streams("run");  // before any prefetched state is consumed
   if (input.shape != g_.input) throw Error(kConfigError, "run: input shape mismatch");
   for (auto& [k, sh] : model_weight_shapes(g_))
     if (!w_.count(k)) throw Error(kConfigError, "missing weight tensor: " + k);

@@ -66,8 +66,10 @@ class SecureExecutor {
 
   // Weights: every party derives its share from the session seed, standing in for the
   // weight owner's dealer (H/engine/executor.hpp:49-68). `values` in sorted-name order.
+  // `counts[i]` = number of doubles behind values[i]; checked against the model's shapes
+  // (check_weights, H/engine/model.hpp:366-376) before anything is read.
   void deal_weights(const std::vector<std::string>& names, const std::vector<const double*>& values,
-                    u64 seed);
+                    const std::vector<size_t>& counts, u64 seed);
   void set_weight(const std::string& name, const u64* host_words);  // n_local*numel (or numel public)
 
   DT run(const DT& input);
@@ -78,6 +80,9 @@ class SecureExecutor {
   // iteration (device key table refreshed per replay).
   void capture(const DT& input);
   DT replay();
+  // Destroy the captured graph; run() and the session's other ops may fetch triples again
+  // (while a graph is held they throw UsageError: the graph owns the dealer streams).
+  void release_graph();
   DT graph_out_;
   bool captured_ = false;
 

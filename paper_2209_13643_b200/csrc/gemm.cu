@@ -122,8 +122,8 @@ void launch_simt(Session& s, GemmArgs a) {
   const u32 kp = u32(maxseg) * a.K;
   // split K' until ~2 waves of CTAs exist, keeping >= 2 k-steps of 16 per split
   u32 split = 1;
-  if (tiles < 2 * u64(kSms)) {
-    split = u32((2 * u64(kSms) + tiles - 1) / tiles);
+  if (tiles < 2 * u64(num_sms())) {
+    split = u32((2 * u64(num_sms()) + tiles - 1) / tiles);
     split = split > 16 ? 16 : split;  // the epilogue kernel sums the partials serially
     const u32 maxsplit = (kp + 31) / 32;
     split = split > maxsplit ? maxsplit : split;
@@ -248,7 +248,7 @@ void launch_gemv(Session& s, GemmArgs a) {
   // per-(k, n) dealer draws are latency-bound chains, so the kernel needs every warp slot;
   // VGG fc6 1 x 25088 x 4096: 1.61 ms at ~3 blocks per SM), >= one staged chunk per split
   const u64 base = u64(ncol) * a.nslots * mgrp;
-  u32 split = u32((16 * u64(kSms) + base - 1) / base);
+  u32 split = u32((16 * u64(num_sms()) + base - 1) / base);
   const u32 maxsplit = (a.K + kGvKC - 1) / kGvKC;
   split = split > maxsplit ? maxsplit : (split < 1 ? 1 : split);
   a.kchunk = ((a.K + split - 1) / split + kGvKC - 1) / kGvKC * kGvKC;
@@ -376,7 +376,6 @@ void ring_gemm_launch(Session& s, const GemmArgs& a) {
     return;
   }
   if (ring_gemm_tc2_try(s, a)) return;  // warp-specialised tcgen05 int8-limb path
-  if (ring_gemm_tc_try(s, a)) return;   // first-generation tcgen05 path (materialised operands)
   if (a.M <= 16) {
     if (a.N <= 16)
       launch_simt<16, 16, 1, 1>(s, a);
@@ -658,7 +657,7 @@ void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const 
       attr = smem;
     }
     u64 blocks = (u64(rows) + 7) / 8;
-    const u64 cap = u64(kSms) * 8;
+    const u64 cap = u64(num_sms()) * 8;
     blocks = blocks > cap ? cap : (blocks < 1 ? 1 : blocks);
     cudaEvent_t pe;
     probe_begin(s.stream, &pe);
@@ -701,118 +700,6 @@ void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const 
   });
 }
 
-// R operands per slot (3 x nb words): p0 {B, b0+F, F}, p1 {r_B, F}; F = own + peer delta.
-DT prepare_R(Session& s, const Triple& t, const Open& d, size_t nb) {
-  if (d.summed) throw Error(kUsageError, "prepare_R: summed delta");
-  DT r = s.alloc(Shape{3, nb});
-  const Pid2 pid = pids(s);
-  const CPtr2 ow = as_const(own_ptrs(d)), pe = peer_ptrs(d);
-  const Ptr2 rp = ptrs(r);
-  const MmTriple mm = t.mm;
-  launch_ew(s.stream, s.n_local, nb, [=] __device__(int slot, u64 j) {
-    const u64 F = ow.p[slot][j] + pe.p[slot][j];
-    const u64 rb = mm_rB(mm, j);
-    u64* o = rp.p[slot];
-    if (pid.v[slot] == 0) {
-      const u64 B = mm_B(mm, j);
-      o[j] = B;
-      o[nb + j] = (B - rb) + F;
-      o[2 * nb + j] = F;
-    } else {
-      o[j] = rb;
-      o[nb + j] = F;
-    }
-  });
-  return r;
-}
-
-// L operands per slot (3 x na words) for A elements [a_off, a_off+na):
-// p0 {A, E, a0 = A - r_A}, p1 {E, r_A}; E = own + peer eps.
-DT prepare_L(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na) {
-  DT l = s.alloc(Shape{3, na});
-  const Pid2 pid = pids(s);
-  const CPtr2 ow = as_const(own_ptrs(e)), pe = peer_ptrs(e);
-  const Ptr2 lp = ptrs(l);
-  const MmTriple mm = t.mm;
-  launch_ew(s.stream, s.n_local, na, [=] __device__(int slot, u64 j) {
-    const u64 E = ow.p[slot][j] + pe.p[slot][j];
-    const u64 ra = mm_rA(mm, a_off + j);
-    u64* o = lp.p[slot];
-    if (pid.v[slot] == 0) {
-      const u64 A = mm_A(mm, a_off + j);
-      o[j] = A;
-      o[na + j] = E;
-      o[2 * na + j] = A - ra;
-    } else {
-      o[j] = E;
-      o[na + j] = ra;
-    }
-  });
-  return l;
-}
-
-// z[out_off..] = combine for one chunk. L/R from prepare_L/prepare_R; batched when nbatch>1.
-void mm_combine(Session& s, const Triple& t, const DT& L, size_t na, const DT& R, size_t nb, u64* const out[2],
-                size_t out_off, u32 nbatch, u32 M, u32 N, u32 K, bool tb, bool batched_r, size_t r_batch0,
-                const Epi& ep) {
-  GemmArgs a{};
-  a.nslots = s.n_local;
-  a.M = M;
-  a.N = N;
-  a.K = K;
-  a.tb = tb;
-  a.nbatch = nbatch;
-  a.trunc_bits = ep.trunc_bits;
-  a.col2im = ep.col2im;
-  a.OHW = ep.OHW;
-  const u64 sL = u64(M) * K, sR = batched_r ? u64(K) * N : 0;
-  const u64 rboff = batched_r ? r_batch0 * u64(K) * N : 0;
-  for (int i = 0; i < s.n_local; ++i) {
-    GemmSlotArgs& S = a.sl[i];
-    const u64* Lp = L.s[i];
-    const u64* Rp = R.s[i];
-    S.out = out[i] + out_off;
-    S.bias = ep.bias[i];
-    S.ckey = t.mm.key;
-    S.ckp = t.mm.kp;
-    S.cbase = 1 + 2 * t.mm.na + 2 * t.mm.nb + t.mm.offC + out_off;
-    if (s.party_of[i] == 0) {
-      S.nseg = 3;
-      S.cterm = -1;
-      for (int g = 0; g < 3; ++g) {
-        S.L[g] = Lp + g * na;
-        S.R[g] = Rp + g * nb + rboff;
-      }
-    } else {
-      S.nseg = 2;
-      S.cterm = +1;
-      S.L[0] = Lp;          // E
-      S.R[0] = Rp + rboff;  // r_B
-      S.L[1] = Lp + na;     // r_A
-      S.R[1] = Rp + nb + rboff;  // F
-    }
-    for (int g = 0; g < 3; ++g) {
-      S.sL[g] = sL;
-      S.sR[g] = sR;
-    }
-  }
-  ring_gemm_launch(s, a);
-}
-
-// The Beaver combine of one chunk straight from the opened payloads (see the file header):
-// operands are generated in the SIMT tile loaders; only a tcgen05-bound GEMM materialises
-// them (prepare_L / prepare_R, R cached across chunks in *rcache).
-bool beaver_combine_uses_tc(const Session& s, u32 nbatch, u32 M, u32 N, u32 K) {
-  GemmArgs a{};
-  a.nslots = s.n_local;
-  a.M = M;
-  a.N = N;
-  a.K = K;
-  a.nbatch = nbatch;
-  for (int i = 0; i < s.n_local; ++i) a.sl[i].nseg = s.party_of[i] == 0 ? 3 : 2;
-  return ring_gemm_tc_wants(a);
-}
-
 // The eps build also emits the A-side operands (A, a0 / r_A) only for combines that read them
 // from memory (tiled SIMT and first-generation tcgen05); the small-M path, the skinny-N row
 // path and the warp-specialised tcgen05 path draw them in place.
@@ -830,21 +717,9 @@ bool beaver_combine_wants_aops(const Session& s, u32 nbatch, u32 M, u32 N, u32 K
 }
 
 // The eps open can be fused into its build (Open::summed) when both slots are local and the
-// combine reads E as a GEMM operand (not through prepare_L / the A-operand path).
+// combine reads E as a GEMM operand (not through the A-operand path).
 bool beaver_combine_fuses_eps(const Session& s, u32 nbatch, u32 M, u32 N, u32 K) {
-  static const bool enabled = [] {  // MPCG_EPS_FUSE=0: always materialise both payloads
-    const char* e = std::getenv("MPCG_EPS_FUSE");
-    return !(e && e[0] == '0');
-  }();
-  if (!enabled || s.n_local != 2 || beaver_combine_wants_aops(s, nbatch, M, N, K)) return false;
-  GemmArgs a{};
-  a.nslots = s.n_local;
-  a.M = M;
-  a.N = N;
-  a.K = K;
-  a.nbatch = nbatch;
-  for (int i = 0; i < s.n_local; ++i) a.sl[i].nseg = s.party_of[i] == 0 ? 3 : 2;
-  return ring_gemm_tc2_wants(a) || !ring_gemm_tc_wants(a);
+  return eps_fuse_enabled() && s.n_local == 2 && !beaver_combine_wants_aops(s, nbatch, M, N, K);
 }
 
 void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na, const Open& d, size_t nb,
@@ -861,48 +736,6 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
   a.col2im = ep.col2im;
   a.OHW = ep.OHW;
   for (int i = 0; i < s.n_local; ++i) a.sl[i].nseg = s.party_of[i] == 0 ? 3 : 2;
-  if (!ring_gemm_tc2_wants(a) && ring_gemm_tc_wants(a)) {
-    if (e.summed) throw Error(kUsageError, "beaver_combine: summed eps on the prepare_L path");
-    if (!*rcache) *rcache = prepare_R(s, t, d, nb);
-    if (!aops) {  // no A-side operands from the eps build: materialise L
-      DT L = prepare_L(s, t, e, a_off, na);
-      mm_combine(s, t, L, na, *rcache, nb, out, out_off, nbatch, M, N, K, tb, batched_r, r_batch0, ep);
-      return;
-    }
-    // L straight from the eps build's A-side operands and the two opened eps halves (E = own +
-    // peer, summed in the tcgen05 producer); R (weight side, small) materialised once per layer.
-    const u64 sL = u64(M) * K, sR = batched_r ? u64(K) * N : 0;
-    const u64 rboff = batched_r ? r_batch0 * u64(K) * N : 0;
-    for (int i = 0; i < s.n_local; ++i) {
-      GemmSlotArgs& S = a.sl[i];
-      const u64* Rp = rcache->s[i];
-      const u64* ao = aops->s[i];
-      S.out = out[i] + out_off;
-      S.bias = ep.bias[i];
-      S.ckey = t.mm.key;
-      S.ckp = t.mm.kp;
-      S.cbase = 1 + 2 * t.mm.na + 2 * t.mm.nb + t.mm.offC + out_off;
-      if (s.party_of[i] == 0) {  // -r_C + A*B + E*(b0 + F) + a0*F ; R = {B, b0+F, F}
-        S.cterm = -1;
-        S.L[0] = ao;
-        S.lk[1] = kOpSum, S.L[1] = e.own(i), S.L2[1] = e.peer(i);
-        S.L[2] = ao + na;
-        for (int g = 0; g < 3; ++g) S.R[g] = Rp + g * nb + rboff;
-      } else {  // +r_C + E*r_B + r_A*F ; R = {r_B, F}
-        S.cterm = +1;
-        S.lk[0] = kOpSum, S.L[0] = e.own(i), S.L2[0] = e.peer(i);
-        S.L[1] = ao;
-        S.R[0] = Rp + rboff;
-        S.R[1] = Rp + nb + rboff;
-      }
-      for (int g = 0; g < 3; ++g) {
-        S.sL[g] = sL;
-        S.sR[g] = sR;
-      }
-    }
-    ring_gemm_launch(s, a);
-    return;
-  }
   const u64 sL = u64(M) * K, sR = batched_r ? u64(K) * N : 0;
   const u64 rboff = batched_r ? r_batch0 * u64(K) * N : 0;
   const bool tc2 = !(gemv_eligible_shape(M, nbatch, tb, ep.col2im) && gemv_mode() != 0) && ring_gemm_tc2_wants(a);

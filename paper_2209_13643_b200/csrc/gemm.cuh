@@ -1,4 +1,4 @@
-// Ring GEMM interfaces (gemm.cu SIMT path, gemm_tc.cu tcgen05 int8-limb path).
+// Ring GEMM interfaces (gemm.cu SIMT / GEMV / row paths, gemm_tc2.cu tcgen05 int8-limb path).
 #pragma once
 
 #include "core.hpp"
@@ -122,21 +122,15 @@ inline int& gemv_mode() {
   }();
   return m;
 }
-bool ring_gemm_tc_try(Session& s, const GemmArgs& a);
 int& tc_gemm_mode();  // 0 = never tensor cores, 1 = whenever exact, 2 = auto by size
 // Warp-specialised tcgen05 path (gemm_tc2.cu): operands generated by producer warps or packed
-// once and bulk-copied; takes every operand kind. MPCG_TC2=0 / tc2_mode()=0 disables it.
-int& tc2_mode();
+// once and bulk-copied; takes every operand kind.
 bool ring_gemm_tc2_wants(const GemmArgs& a);
 bool ring_gemm_tc2_try(Session& s, const GemmArgs& a);
 void tc2_trace_read(unsigned long long* out, int n);  // debug: stage timestamps (MPCG_TC2_TRACE=1)
-bool ring_gemm_tc_wants(const GemmArgs& a);  // shape/budget test only (operands not inspected)
 void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na, const Open& d, size_t nb,
                     DT* rcache, u64* const out[2], size_t out_off, u32 nbatch, u32 M, u32 N, u32 K, bool tb,
                     bool batched_r, size_t r_batch0, const Epi& ep, const DT* aops = nullptr);
-// Whether the combine of this shape runs on the tensor cores (materialised operands) —
-// callers then skip emitting the A-side operands in the eps build.
-bool beaver_combine_uses_tc(const Session& s, u32 nbatch, u32 M, u32 N, u32 K);
 bool beaver_combine_fuses_eps(const Session& s, u32 nbatch, u32 M, u32 N, u32 K);
 bool beaver_combine_wants_aops(const Session& s, u32 nbatch, u32 M, u32 N, u32 K);
 
@@ -146,11 +140,6 @@ void eps_build_mem(Session& s, const Triple& t, const u64* const x[2], size_t a_
                    const DT* aops = nullptr);
 void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const ConvGeom& g, size_t a_off,
                       size_t na, Open& o, const DT* aops = nullptr);
-DT prepare_R(Session& s, const Triple& t, const Open& d, size_t nb);
-DT prepare_L(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na);
-void mm_combine(Session& s, const Triple& t, const DT& L, size_t na, const DT& R, size_t nb, u64* const out[2],
-                size_t out_off, u32 nbatch, u32 M, u32 N, u32 K, bool tb, bool batched_r, size_t r_batch0,
-                const Epi& ep);
 void public_gemm(Session& s, const u64* const x[2], const u64* W, u64* const out[2], u32 M, u32 N, u32 K,
                  const Epi& ep);
 

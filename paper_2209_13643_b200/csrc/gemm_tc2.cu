@@ -1,6 +1,6 @@
 // tcgen05 int8-limb ring GEMM over Z_2^64, warp-specialised (sm_100a).
 //
-// Same arithmetic as gemm_tc.cu (u64 operands split into 8 u8 limbs; the 36 limb pairs with
+// u64 operands split into 8 u8 limbs; the 36 limb pairs with
 // l+m <= 7 run as tcgen05.mma.kind::i8 into 8 s32 TMEM accumulators, one per diagonal
 // d = l+m; the epilogue recombines z = sum_d D_d << 8d mod 2^64 — the int8 form of
 // LimbPlan/limb_matmul, H/ring/limb.hpp:15-99), restructured as a Blackwell pipeline:
@@ -21,7 +21,7 @@
 // A 4-stage ring of 32-byte K slabs keeps HBM loads, PRG work and MMAs in flight together.
 // When N spans several BN tiles the left operand is also packed once (pack kernel) and both
 // sides arrive by cp.async.bulk, so the generation is not repeated per N tile.
-// Exactness: per-diagonal sums over K' = nseg*K <= 16384 (see gemm_tc.cu).
+// Exactness: per-diagonal sums over K' = nseg*K <= 16384 (see below).
 #include "gemm.cuh"
 
 namespace mpcg {
@@ -884,8 +884,8 @@ void launch_tc2(Session& s, const GemmArgs& a, int packL) {
   // split K when the tile grid cannot fill the SMs (small-M layers): >= 2 K blocks per split
   const u64 ctas = u64(ntiles) * mtiles * a.nslots * a.nbatch;
   u32 split = 1;
-  if (ctas < u64(kSms)) {
-    split = u32((kSms + ctas - 1) / ctas);
+  if (ctas < u64(num_sms())) {
+    split = u32((num_sms() + ctas - 1) / ctas);
     split = split > 16 ? 16 : split;
     const u32 maxs = P.nkb / 2 > 0 ? P.nkb / 2 : 1;
     split = split > maxs ? maxs : split;
@@ -922,16 +922,17 @@ void launch_tc2(Session& s, const GemmArgs& a, int packL) {
 
 }  // namespace
 
-int& tc2_mode() {  // 1 = warp-specialised tcgen05 path enabled (default), 0 = off (MPCG_TC2=0)
+// 0 = never, 1 = every shape within the exactness budget, 2 = auto (large shapes).
+int& tc_gemm_mode() {
   static int mode = [] {
-    const char* e = std::getenv("MPCG_TC2");
-    return (e && e[0] == '0') ? 0 : 1;
+    const char* e = std::getenv("MPCG_TC_GEMM");
+    return (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : 2;
   }();
   return mode;
 }
 
 bool ring_gemm_tc2_wants(const GemmArgs& a) {
-  if (tc2_mode() == 0 || tc_gemm_mode() == 0) return false;
+  if (tc_gemm_mode() == 0) return false;
   int maxseg = 0;
   for (int i = 0; i < a.nslots; ++i) maxseg = a.sl[i].nseg > maxseg ? a.sl[i].nseg : maxseg;
   if (u64(maxseg) * a.K > kMaxKPrime) return false;

@@ -511,7 +511,7 @@ void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const
     MPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
     if (per_sm < 1) throw Error(kInternalError, "chain kernel cannot be resident");
   }
-  const u64 cap = u64(per_sm) * kSms / gy;
+  const u64 cap = u64(per_sm) * num_sms() / gy;
   u64 blocks = (n + 255) / 256;  // one element per thread per round (the rounds are PRG-latency bound)
   blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);
   cudaLaunchConfig_t lc{};

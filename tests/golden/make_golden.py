@@ -8,6 +8,12 @@ and stores its dumps as compressed .npz fixtures in tests/golden/:
 * ops.npz            — per-op inputs and per-party output shares (see oracle/ref_driver.cpp cmd_golden)
 * model_<name>_<mode>_<weights>_it<k>.npz — per-party logits shares, opened logits, hash,
                        traffic counters and the double-precision reference_forward output.
+* scale.npz          — BASELINE-scale pins (``--scale``): the reference's ops and single-layer
+                       models at ResNet-18 / VGG-16 / BERT-base layer shapes, each party's output
+                       share pinned by FNV-1a word hash + head/tail words + traffic counters
+                       (oracle/ref_driver.cpp cmd_scale / model_pin). About 3 min on 8 cores.
+
+    python tests/golden/make_golden.py --scale [--from DIR]   # DIR: dumps made earlier
 """
 import os
 import struct
@@ -51,10 +57,36 @@ MODELS = [
     ("toy_transformer", "blocking", "private", 1),
     ("toy_transformer", "blocking", "public", 1),
     ("lenet5", "pipelined", "private", 1),
+    ("vgg16", "blocking", "private", 1),   # ~10 min: the reference's largest expressible config
 ]
 
 
+SCALE_OPS = ["relu_r18", "pool_vgg1", "softmax_bert", "qk_bert", "av_bert", "gemm_fc6", "gemm_r18l4"]
+SCALE_MODELS = ["r18_l1conv", "r18_l4conv", "vgg_fc6", "bert_ffn1", "bert_ffn2"]
+
+
+def main_scale(src=None):
+    """Pack (or first generate, 4 reference runs at a time) the BASELINE-scale pins."""
+    import concurrent.futures as cf
+    import tempfile
+    tmpd = src or tempfile.mkdtemp(prefix="mpcg_scale_")
+    if not src:
+        cmds = [[DRIVER, "scale", c, os.path.join(tmpd, c + ".bin")] for c in SCALE_OPS]
+        cmds += [[DRIVER, "model_pin", os.path.join(HERE, "scale", m + ".json"), "blocking", "1", "private", "1",
+                  os.path.join(tmpd, m + ".bin")] for m in SCALE_MODELS]
+        with cf.ThreadPoolExecutor(4) as ex:
+            list(ex.map(subprocess.check_call, cmds))
+    out = {}
+    for c in SCALE_OPS + SCALE_MODELS:
+        for k, v in read_dump(os.path.join(tmpd, c + ".bin")).items():
+            out[(c + "/" + k if c in SCALE_MODELS else k).replace("/", "__")] = v
+    np.savez_compressed(os.path.join(HERE, "scale.npz"), **out)
+
+
 def main():
+    if "--scale" in sys.argv:
+        src = sys.argv[sys.argv.index("--from") + 1] if "--from" in sys.argv else None
+        return main_scale(src)
     tmp = os.path.join(HERE, "_tmp.bin")
     subprocess.check_call([DRIVER, "golden", tmp])
     d = read_dump(tmp)

@@ -248,3 +248,68 @@ def test_empty_tensor_ops(mp):
     s = _sess(mp, 1, 16, 2)
     e = s.tensor(np.zeros((2, 0), dtype=np.uint64))
     assert mp.beaver_mul(s, e, e).numpy().shape == (2, 0)
+
+
+def test_graph_owns_dealer_streams_until_released(mp):
+    """an eager run between replays would advance the host dealer counters behind
+    the graph's back. While a graph is held, run() fails with UsageError; after
+    release_graph() the next run continues the iteration sequence (= eager iteration 4)."""
+    g = mp.ModelGraph.from_json(os.path.join(ROOT, "configs", "mlp.json"))
+
+    def make():
+        s = mp.Session(device=0, n_local=2, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
+        ex = mp.SecureExecutor(s, g, pipelined=True)
+        ex.deal_weights(mp.init_weights(g, 12), 1)
+        return s, ex, s.deal_input(mp.demo_input(g, 13), 2)
+
+    s, ex, x = make()
+    ex.run(x)                      # iteration 1
+    ex.capture(x)
+    ex.replay()                    # iteration 2
+    with pytest.raises(mp.UsageError):
+        ex.run(x)
+    with pytest.raises(mp.UsageError):
+        mp.relu_shares(s, x, "stray")
+    ex.replay()                    # iteration 3
+    ex.release_graph()
+    z = ex.run(x).numpy()          # iteration 4
+    s2, ex2, x2 = make()
+    for _ in range(4):
+        ze = ex2.run(x2)
+    assert np.array_equal(z, ze.numpy())
+    assert s.stats(0) == s2.stats(0)
+
+
+def test_deal_weights_checks_counts_through_the_abi(mp):
+    """the C ABI takes per-tensor element counts and rejects a wrongly shaped
+    tensor with ConfigError (the reference's check_weights) instead of over-reading."""
+    import ctypes as C
+    from paper_2209_13643_b200 import _native as N
+    g = mp.ModelGraph.from_json(os.path.join(ROOT, "configs", "mlp.json"))
+    s = mp.Session(device=0, n_local=2, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
+    ex = mp.SecureExecutor(s, g)
+    w = mp.init_weights(g, 12)
+    names = sorted(w)
+    arrs = [np.ascontiguousarray(w[k], dtype=np.float64).reshape(-1) for k in names]
+    arrs[0] = arrs[0][:-1]  # one value short
+    cn = (C.c_char_p * len(names))(*[n.encode() for n in names])
+    cv = (C.POINTER(C.c_double) * len(names))(*[a.ctypes.data_as(C.POINTER(C.c_double)) for a in arrs])
+    counts = np.array([a.size for a in arrs], dtype=np.uint64)
+    with pytest.raises(mp.ConfigError, match="wrong shape"):
+        N.call("mpcg_executor_deal_weights", ex._h, len(names), cn, cv,
+               counts.ctypes.data_as(C.POINTER(C.c_uint64)), 1)
+    with pytest.raises(ValueError):
+        w2 = dict(w)
+        w2[names[0]] = w2[names[0]].reshape(-1)[:-1]
+        ex.deal_weights(w2, 1)
+
+
+def test_set_link_rejects_latency_only(mp):
+    """ADVICE r1 / transport/config.hpp:34-38: bandwidth must be > 0 for an emulated link."""
+    s = mp.Session(device=0, n_local=2, seed=1, mask_seed=1, frac_bits=16)
+    with pytest.raises(mp.ConfigError):
+        s.set_link(1e-4, 0.0, 0.0)
+    with pytest.raises(mp.ConfigError):
+        s.set_link(-1.0, 1e9, 0.0)
+    s.set_link(1e-4, 1.25e9, 0.0)
+    s.set_link(0.0, 0.0, 0.0)  # back to the real transport

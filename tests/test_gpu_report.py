@@ -1,0 +1,79 @@
+"""GPU: trace timestamps and the run report's delta-wait attribution (AC6).
+
+Mirrors the reference's AC6 gate (P/tests/acceptance.cpp:353-381, H/engine/report.hpp:42-81):
+on a slow link the pipelined executor must be >= 5% faster than blocking, with bit-identical
+logits, and the weight openings it pre-transmits must cost < 5% of the linear layers' comm
+time in wait (delta_wait / linear_comm). Here the link is the emulated token bucket on the
+comm stream (H/transport/sim.hpp:90-92 model) and every timestamp is a CUDA event.
+"""
+import os
+import time
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PHI = 0x9E3779B97F4A7C15
+
+
+def _run(mp, api, g, mode, link, iters=2):
+    s = mp.Session(device=0, n_local=2, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
+    s.set_link(*link)
+    ex = mp.SecureExecutor(s, g, pipelined=mode == "pipelined", chunk_threshold=2 << 20)
+    ex.deal_weights(mp.init_weights(g, 12), 1)
+    x = s.deal_input(mp.demo_input(g, 13), 2)
+    s.trace(True)
+    api.timer(s, "reset")
+    for _ in range(iters):
+        api.timer(s, "start")
+        z = ex.run(x)
+        api.timer(s, "stop")
+    wall = api.timer(s, "read") / 1e3
+    rows = s.trace_rows()
+    return wall, rows, api.party_report_fields(rows, g), z.numpy()
+
+
+def test_ac6_directional_speedup_and_delta_attribution():
+    import paper_2209_13643_b200 as mp
+    from paper_2209_13643_b200 import api
+    g = mp.ModelGraph.from_json(os.path.join(ROOT, "configs", "toy_transformer.json"))
+    link = (1e-3, 1e9, 0.0)  # AC6's link: 1 ms, 1 GB/s
+    bw, brows, bf, zb = _run(mp, api, g, "blocking", link)
+    pw, prows, pf, zp = _run(mp, api, g, "pipelined", link)
+    assert np.array_equal(zb, zp), "blocking and pipelined logits differ"
+    speedup = (bw - pw) / bw
+    assert speedup >= 0.05, f"pipelined speedup {speedup:.3%} < 5%"
+    assert pf["linear_comm_s"] > 0
+    ratio = pf["delta_wait_s"] / pf["linear_comm_s"]
+    assert ratio < 0.05, f"delta-wait / linear-comm {ratio:.2%} >= 5%"
+    # blocking waits on every weight opening (the number pipelining drives to zero)
+    assert bf["delta_wait_s"] > pf["delta_wait_s"]
+    # the trace is the reference's: one row per collective, same tags and bytes in both modes
+    # (pipelined adds the wrap-around delta of the next run)
+    from collections import Counter
+    extra = Counter(r["tag"] for r in prows) - Counter(r["tag"] for r in brows)
+    assert extra == Counter({api.linear_tags(g)[0] + ".delta": 1})
+    for r in prows:
+        assert r["t_sent"] >= r["t_issue"] and r["t_wait_end"] >= r["t_wait_begin"]
+        assert r["occupancy"] == pytest.approx(r["bytes"] / 1e9, rel=1e-6, abs=1e-9)
+    assert sum(r["bytes"] for r in prows if r["tag"].endswith(".delta")) > 0
+
+
+def test_in_device_opens_have_no_stall_and_add_delay_idles_the_stream():
+    import paper_2209_13643_b200 as mp
+    s = mp.Session(device=0, n_local=2, seed=3, mask_seed=4, frac_bits=16)
+    s.trace(True)
+    x = s.tensor(np.arange(2 * 64, dtype=np.uint64).reshape(2, 64), 16)
+    mp.beaver_mul(s, x, x, "m")
+    rows = s.trace_rows()
+    assert [r["tag"] for r in rows] == ["m"] and rows[0]["stall"] == 0 and rows[0]["occupancy"] == 0
+    s.clear_trace()
+    assert s.trace_rows() == []
+    t0 = s.now()
+    s.add_delay(0.05)
+    s.sync()
+    assert s.now() - t0 >= 0.045
+    with pytest.raises(mp.ConfigError):
+        s.add_delay(-1.0)
+    time.sleep(0)

@@ -11,16 +11,14 @@ pytestmark = pytest.mark.gpu
 PHI = 0x9E3779B97F4A7C15
 
 
-@pytest.fixture(params=["tc2", "tc1"])
-def tc(request):
-    """Tensor cores forced on; tc2 = warp-specialised pipeline, tc1 = first-generation kernel."""
+@pytest.fixture
+def tc():
+    """Tensor cores forced on for every shape within the exactness budget."""
     import paper_2209_13643_b200 as mp
     from paper_2209_13643_b200 import api
     api.set_gemm_mode("tc")
-    api.set_tc2(request.param == "tc2")
     yield mp
     api.set_gemm_mode("auto")
-    api.set_tc2(True)
 
 
 def _run(mp, X, Y, tb, tag, chunks=1):
