@@ -250,23 +250,42 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (nranks) in the log
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("gloo")
     pairs, pair, party = lay["pairs"], lay["pair"], lay["party"]
     g_global = g.with_batch(lay["global_batch"])
     seed = 1
 
+    # N>1 transport: NCCL send/recv between the pair's two GPUs (default), or — for a dry run of
+    # the multi-process path on ONE GPU (MPCG_SAME_GPU=1; NCCL refuses two ranks on one device) —
+    # the TCP socket link with every rank on cuda:0.
+    same_gpu = world > 1 and os.environ.get("MPCG_SAME_GPU") == "1"
+    transport = "socket" if same_gpu else "nccl"
+    device = 0 if same_gpu else local_rank
+    n_made = [0]
+
     def make_session():
         if world == 1:
-            s = mp.Session(device=0, n_local=2, seed=seed, mask_seed=seed ^ PHI, frac_bits=g.frac_bits)
+            return mp.Session(device=0, n_local=2, seed=seed, mask_seed=seed ^ PHI, frac_bits=g.frac_bits)
+        s = mp.Session(device=device, n_local=1, party=party, seed=seed, mask_seed=seed ^ PHI, frac_bits=g.frac_bits)
+        if transport == "socket":
+            port = int(os.environ.get("MASTER_PORT", "29500")) + 101 + 8 * n_made[0] + pair
+            s.connect_socket("127.0.0.1", port, 300.0)
         else:
-            s = mp.Session(device=local_rank, n_local=1, party=party, seed=seed, mask_seed=seed ^ PHI,
-                           frac_bits=g.frac_bits)
             ids = [None] * world
             uid = mp.nccl_unique_id() if party == 0 else None
             dist.all_gather_object(ids, uid)
             s.connect_nccl(ids[2 * pair], party)
-            s.set_shard(B, B * pairs, B * pair)
+        n_made[0] += 1
+        s.set_shard(B, B * pairs, B * pair)
+        print(f"mpcg: rank {rank}/{world} pair {pair} party {party} device {device} transport {transport} "
+              f"(2-rank communicator per pair; data-parallel shard rows {B * pair}..{B * pair + B - 1} of "
+              f"{B * pairs})", file=sys.stderr, flush=True)
         return s
+    # one-party sessions replay CUDA graphs only when asked (MPCG_NCCL_GRAPH=1: NCCL send/recv
+    # captured into the graph); the socket link is host I/O and always runs eager
+    use_graph = world == 1 or (transport == "nccl" and os.environ.get("MPCG_NCCL_GRAPH") == "1")
 
     weights = mp.init_weights(g, seed + 11)
     x_global = mp.demo_input(g_global, seed + 12)
@@ -344,8 +363,9 @@ def main():
         sb, exb, xb = setup(mode)
         exb.run(xb)
         exb.time_layers(True)
-        exb.capture(xb)
-        ms, _, _, _ = timed(sb, exb, xb, steps, warmup, graph=True)
+        if use_graph:
+            exb.capture(xb)
+        ms, _, _, _ = timed(sb, exb, xb, steps, warmup, graph=use_graph)
         lt = exb.layer_times()
         del exb, sb
         return ms, lt
@@ -367,8 +387,9 @@ def main():
     probe_steps = max(2, a.steps // 4)
 
     ex.time_layers(True)   # per-layer CUDA events recorded inside the graph
-    ex.capture(x)
-    ms_step, launches, clocks, out = timed(s, ex, x, a.steps, a.warmup, graph=True)
+    if use_graph:
+        ex.capture(x)
+    ms_step, launches, clocks, out = timed(s, ex, x, a.steps, a.warmup, graph=use_graph)
     layer_ms = ex.layer_times()   # of the last timed replay
     z = out.numpy()
 
@@ -378,14 +399,15 @@ def main():
     pin_in = api.PinnedBuffer(xin_host.size)
     pin_in.array[:] = xin_host.reshape(-1)
     pin_out = api.PinnedBuffer(z.size)
+    step_api = ex.replay if use_graph else (lambda: ex.run(x))
     for _ in range(max(1, a.warmup)):
         api.copy_from_host(x, pin_in)      # the captured graph reads x in place
-        api.download_into(ex.replay(), pin_out)
+        api.download_into(step_api(), pin_out)
     barrier(s)
     t0 = time.perf_counter()
     for _ in range(a.steps):
         api.copy_from_host(x, pin_in)
-        api.download_into(ex.replay(), pin_out)
+        api.download_into(step_api(), pin_out)
     barrier(s)
     e2e_s = maxall(time.perf_counter() - t0) / a.steps
     h2d = xin_host.size * 8
@@ -505,10 +527,14 @@ def main():
                    "chunk_threshold_source": a.threshold,
                    "calibration": calib,
                    "l2": "flushed between timed steps (256 MiB memset, untimed)",
-                   "transport": ("in-device zero-copy opens" if world == 1 else "NCCL send/recv over NVLink")
+                   "transport": ("in-device zero-copy opens" if world == 1 else
+                                 "NCCL send/recv over NVLink" if transport == "nccl" else
+                                 "TCP socket link, all ranks on cuda:0 (MPCG_SAME_GPU=1 dry run)")
                    + (f" + emulated link latency {link[0]} s, {link[1]:.3g} B/s" if link else ""),
                    "kernels_per_step": launches / a.steps,
-                   "execution": "one CUDA-graph replay per step (whole 2PC inference, both parties)",
+                   "execution": ("one CUDA-graph replay per step (whole 2PC inference, both parties)" if world == 1
+                                 else "one CUDA-graph replay per step per party" if use_graph
+                                 else "eager launches (one-party sessions; MPCG_NCCL_GRAPH=1 captures NCCL)"),
                    "eager_ms_per_step": eager_ms,
                    "logits_hash_slot0": mp.fnv1a_words(dec) if world == 1 else None,
                    "blocking": blocking,
@@ -518,8 +544,9 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": B * pairs / e2e_s, "unit": "inferences/s", "ms_per_step": e2e_s * 1e3,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "pinned host input shares -> mpcg_tensor_copy_from_host -> mpcg_executor_replay (the "
-                        "captured inference) -> mpcg_tensor_download of the logit shares; wall clock"},
+                "path": "pinned host input shares -> mpcg_tensor_copy_from_host -> "
+                        + ("mpcg_executor_replay (the captured inference)" if use_graph else "mpcg_executor_run")
+                        + " -> mpcg_tensor_download of the logit shares; wall clock"},
         "gpu_launches": launches,
         "clocks": clocks,
     }

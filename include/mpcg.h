@@ -70,6 +70,11 @@ int mpcg_session_set_shard(mpcg_session* s, uint64_t local_batch, uint64_t globa
 /* NCCL link for n_local == 1 (the socket mesh of transport/socket.hpp:345-402). */
 int mpcg_nccl_unique_id(uint8_t out[128]);
 int mpcg_session_connect_nccl(mpcg_session* s, const uint8_t id[128], int rank);
+/* TCP link for n_local == 1 (transport/socket.hpp:60-413, SocketComm): party 0 listens on
+ * host:port, party 1 connects; both block until paired or `timeout_s` passes. Every payload is a
+ * framed message {seq, words, tag hash}; a mismatch raises MPCG_ERR_PROTOCOL at the wait. For
+ * parties in different processes or hosts; not capturable into a CUDA graph. */
+int mpcg_session_connect_socket(mpcg_session* s, const char* host, int port, double timeout_s);
 int mpcg_session_sync(mpcg_session* s);
 /* 1-GPU mode: run multi-round chains (ReLU, tournament rounds) as one persistent cooperative
  * kernel (1), one kernel per exchange round (0), or auto by size (2, default). Values are
@@ -174,6 +179,12 @@ int mpcg_executor_create(mpcg_session* s, const mpcg_model* m, int public_weight
 int mpcg_executor_deal_weights(mpcg_executor* e, int count, const char* const* names,
                                const double* const* values, const uint64_t* counts /* doubles per tensor */,
                                uint64_t seed);
+/* Extension (north_star (3)): in pipelined mode also open the linear layers' activation side in
+ * `chunks` row blocks ("<tag>.eps.chunk<k>", the beaver_matmul chunk unit of
+ * protocols/beaver.hpp:197-250) for operands >= the chunk threshold, each block's combine GEMM
+ * running as it lands. Off (default) = the reference's unchunked weight_matmul (executor.hpp:305);
+ * values and bytes are identical either way, only the collective count differs. */
+int mpcg_executor_set_linear_chunks(mpcg_executor* e, int on);
 int mpcg_executor_run(mpcg_executor* e, const mpcg_tensor* input, mpcg_tensor** out); /* executor.hpp:193 */
 /* CUDA-graph form of run(): capture one steady-state inference that reads `input` in place
  * (pipelined mode needs one mpcg_executor_run first), then each replay performs the next
@@ -209,6 +220,13 @@ int mpcg_debug_tc2_trace(uint64_t* out, int n);
  * one-party-per-GPU code path with device copies in place of NCCL send/recv. Each party
  * must be driven by its own host thread (a collective waits for the peer's matching post). */
 int mpcg_session_connect_loopback(mpcg_session* a, mpcg_session* b);
+/* Device-initiated link between party 0's and party 1's single-party sessions of this process
+ * (same GPU, or two GPUs with peer access over NVLink): each open's payload is stored by the
+ * sender straight into the receiver's inbox and published with a system-scope release flag the
+ * receiver's stream acquires on the device — no host event crosses the parties. Capturable into
+ * CUDA graphs (flag values follow the replay counter; each replay ends with a device barrier).
+ * Each party must be driven by its own host thread. */
+int mpcg_session_connect_p2p(mpcg_session* a, mpcg_session* b);
 
 /* ---- measurement hooks (bench.py) ---- */
 /* Kernels launched by this library since load. */

@@ -53,6 +53,8 @@ SIGNATURES = {
     "mpcg_session_set_shard": [P, U64, U64, U64],
     "mpcg_nccl_unique_id": [C.c_char_p],
     "mpcg_session_connect_nccl": [P, C.c_char_p, I32],
+    "mpcg_session_connect_socket": [P, C.c_char_p, I32, DBL],
+    "mpcg_session_connect_p2p": [P, P],
     "mpcg_session_sync": [P],
     "mpcg_session_set_persistent": [P, I32],
     "mpcg_session_stats": [P, I32, U64P],
@@ -97,6 +99,7 @@ SIGNATURES = {
     "mpcg_executor_create": [P, P, I32, I32, I32, U64, I32, PP],
     "mpcg_executor_deal_weights": [P, I32, C.POINTER(C.c_char_p), C.POINTER(C.POINTER(DBL)), C.POINTER(U64), U64],
     "mpcg_executor_release_graph": [P],
+    "mpcg_executor_set_linear_chunks": [P, I32],
     "mpcg_set_pair_eval": [I32],
     "mpcg_executor_run": [P, P, PP],
     "mpcg_executor_capture": [P, P],

@@ -72,6 +72,16 @@ class Session:
         2-GPU code path with device copies instead of NCCL (each party on its own thread)."""
         N.call("mpcg_session_connect_loopback", self._h, peer._h)
 
+    def connect_p2p(self, peer: "Session"):
+        """Device-initiated peer-store link with `peer` (the other party's single-party session in
+        this process, same GPU or a peer-accessible one): flags, no host events; graph-capturable."""
+        N.call("mpcg_session_connect_p2p", self._h, peer._h)
+
+    def connect_socket(self, host: str, port: int, timeout_s: float = 60.0):
+        """TCP link to the other party's process (party 0 listens, party 1 connects): the
+        reference's SocketComm for one-party sessions in different processes / hosts."""
+        N.call("mpcg_session_connect_socket", self._h, host.encode(), int(port), float(timeout_s))
+
     def connect_nccl(self, unique_id: bytes, rank: int):
         N.call("mpcg_session_connect_nccl", self._h, unique_id, rank)
 
@@ -400,7 +410,7 @@ class SecureExecutor:
     """H/engine/executor.hpp:173-205 on the GPU. ExecOptions: pipelined, chunks, threshold."""
 
     def __init__(self, sess: Session, g: ModelGraph, public_weights=False, pipelined=False, chunks=4,
-                 chunk_threshold=2 << 20, merged_adder=True):
+                 chunk_threshold=2 << 20, merged_adder=True, linear_chunks=False):
         mh = C.c_void_p()
         dims = np.array(g.input, dtype=np.uint64)
         N.call("mpcg_model_create", g.name.encode(), g.frac_bits, len(g.input), _u64p(dims), C.byref(mh))
@@ -416,6 +426,9 @@ class SecureExecutor:
         self._h = eh
         self.sess = sess
         self.graph = g
+        if linear_chunks:
+            # extension: the inner-layer pipeline also on conv / dense eps openings
+            N.call("mpcg_executor_set_linear_chunks", eh, 1)
 
     def __del__(self):
         try:

@@ -147,6 +147,18 @@ int mpcg_nccl_unique_id(uint8_t out[128]) {
   return guard([&] { nccl_unique_id(out); });
 }
 
+int mpcg_session_connect_p2p(mpcg_session* a, mpcg_session* b) {
+  return guard([&] { p2p_connect(S(a), S(b)); });
+}
+
+int mpcg_session_connect_socket(mpcg_session* s, const char* host, int port, double timeout_s) {
+  return guard([&] {
+    need(host, "host");
+    if (port <= 0 || port > 65535) throw Error(kConfigError, "bad port");
+    socket_connect(S(s), host, port, timeout_s > 0 ? timeout_s : 60.0);
+  });
+}
+
 int mpcg_session_connect_nccl(mpcg_session* s, const uint8_t id[128], int rank) {
   return guard([&] { nccl_connect(S(s), id, rank); });
 }
@@ -460,6 +472,14 @@ int mpcg_executor_deal_weights(mpcg_executor* e, int count, const char* const* n
       k.push_back(size_t(counts[i]));
     }
     e->e->deal_weights(n, v, k, seed);
+  });
+}
+
+int mpcg_executor_set_linear_chunks(mpcg_executor* e, int on) {
+  return guard([&] {
+    need(e, "executor");
+    if (e->e->captured_) throw Error(kUsageError, "set_linear_chunks after capture");
+    e->e->opt_.linear_chunks = on != 0;
   });
 }
 

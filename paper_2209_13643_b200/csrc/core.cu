@@ -178,6 +178,11 @@ Session::Session(int dev, int nl, int party, u64 sd, u64 mask_seed, int frac_bit
   MPCG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   MPCG_CUDA(cudaMalloc(&link_state_, 64));
   MPCG_CUDA(cudaMemset(link_state_, 0, 64));
+  if (nl == 1) {
+    MPCG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&desync_), sizeof(Desync), cudaHostAllocMapped));
+    std::memset(desync_, 0, sizeof(Desync));
+    MPCG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&desync_dev_), desync_, 0));
+  }
   const char* dbg = std::getenv("MPCG_DEBUG_SYNC");
   debug_sync = dbg && dbg[0] == '1';
   const char* per = std::getenv("MPCG_PERSISTENT");
@@ -192,6 +197,11 @@ double Session::now() const {
 Session::~Session() {
   cudaStreamSynchronize(stream);
   cudaStreamSynchronize(comm_stream);
+  try {
+    socket_reap(*this, true);
+  } catch (...) {
+  }
+  sock.reset();
   for (auto e : events_) cudaEventDestroy(e);
   for (auto e : trace_events_) cudaEventDestroy(e);
   if (trace_epoch_) cudaEventDestroy(trace_epoch_);
@@ -206,7 +216,9 @@ Session::~Session() {
   if (cap.tab) cudaFree(cap.tab);
   if (cap.meta) cudaFree(cap.meta);
   if (cap.iter) cudaFree(cap.iter);
+  if (cap.seqd) cudaFree(cap.seqd);
   if (nccl) nccl_api().CommDestroy(nccl);
+  if (desync_) cudaFreeHost(desync_);
   cudaFree(link_state_);
   cudaStreamDestroy(comm_stream);
   cudaStreamDestroy(stream);
@@ -215,6 +227,18 @@ Session::~Session() {
 void Session::sync() {
   MPCG_CUDA(cudaStreamSynchronize(comm_stream));
   MPCG_CUDA(cudaStreamSynchronize(stream));
+  socket_reap(*this, true);
+  check_desync();
+}
+
+void Session::check_desync() {
+  if (!desync_ || !reinterpret_cast<volatile Desync*>(desync_)->bad) return;
+  const Desync d = *desync_;
+  desync_->bad = 0;
+  throw Error(kProtocolError, "collective desync with the peer: expected seq " + std::to_string(d.want[0]) + " (" +
+                                  std::to_string(d.want[1]) + " words, tag hash " + std::to_string(d.want[2]) +
+                                  "), peer sent seq " + std::to_string(d.got[0]) + " (" + std::to_string(d.got[1]) +
+                                  " words, tag hash " + std::to_string(d.got[2]) + ")");
 }
 
 void Session::check() {
@@ -366,6 +390,7 @@ void Session::begin_capture() {
   if (!cap.tab) {
     MPCG_CUDA(cudaMalloc(&cap.tab, (kMaxKeys + kMaxMasks) * sizeof(u64)));
     MPCG_CUDA(cudaMalloc(&cap.iter, 64));
+    MPCG_CUDA(cudaMalloc(&cap.seqd, 64));
   }
   MPCG_CUDA(cudaMemset(cap.iter, 0, 64));
   cap.hs.clear();
@@ -385,6 +410,7 @@ void Session::begin_capture() {
 }
 
 void Session::end_capture() {
+  if (p2p) p2p_replay_barrier(*this);  // replay r+1 must not overwrite inboxes the peer still reads
   if (cap.comm_used) {  // rejoin the comm stream (opens still in flight at the end of the run)
     cudaEvent_t j = pool_event();
     MPCG_CUDA(cudaEventRecord(j, comm_stream));
@@ -401,6 +427,7 @@ void Session::end_capture() {
     cap.stats_delta[i].p2p_sends = stats[i].p2p_sends - cap.stats_delta[i].p2p_sends;
   }
   cap.seq_delta = next_seq - cap.seq_delta;
+  MPCG_CUDA(cudaMemcpy(cap.seqd, &cap.seq_delta, sizeof(u64), cudaMemcpyHostToDevice));
   const size_t nk = cap.hs.size(), nm = cap.mb0.size();
   std::vector<u64> meta(3 * nk + nm + 1);
   std::unordered_map<u64, u64> per_run;  // fetches of each tag per replay (its count stride)
@@ -461,8 +488,9 @@ Open Session::begin_open(size_t nwords, Reduce kind, std::shared_ptr<Block> out,
   o.n = nwords;
   o.kind = kind;
   o.n_local = n_local;
-  o.out = out ? out : raw(nwords * size_t(n_local) + 1);
-  if (n_local == 1) o.in = in ? in : raw(nwords + 1);
+  // one-party sessions: room for the collective trailer behind the payload
+  o.out = out ? out : raw(nwords * size_t(n_local) + (n_local == 1 ? kTrailer : 1));
+  if (n_local == 1) o.in = in ? in : raw(nwords + kTrailer);
   return o;
 }
 
@@ -483,6 +511,20 @@ __global__ void link_delay_kernel(u64* state, u64 busy_ns, u64 latency_ns) {
   while (globaltimer_ns() < arrive) __nanosleep(500);
 }
 }  // namespace
+
+__global__ void trailer_kernel(u64* tail, u64 seq, u64 n, u64 h) {
+  tail[0] = seq;
+  tail[1] = n;
+  tail[2] = h;
+}
+__global__ void trailer_check_kernel(const u64* got, u64 seq, u64 n, u64 h, Session::Desync* d) {
+  if (got[0] != seq || got[1] != n || got[2] != h) {
+    if (atomicExch(&d->bad, 1u) == 0u) {
+      d->want[0] = seq, d->want[1] = n, d->want[2] = h;
+      d->got[0] = got[0], d->got[1] = got[1], d->got[2] = got[2];
+    }
+  }
+}
 
 void Session::throttle(Open& o) {
   const double busy = cfg.sec_per_message + double(o.n * 8) / cfg.link_bandwidth;
@@ -586,6 +628,11 @@ void Session::post(Open& o, const std::string& tag, bool p2p) {
   if (o.posted) throw Error(kUsageError, "open posted twice");
   o.posted = true;
   o.seq = account(o.n, o.kind, tag, p2p);
+  {
+    u64 h = 0xcbf29ce484222325ull;
+    for (char ch : tag) h = (h ^ u64(static_cast<unsigned char>(ch))) * 0x100000001b3ull;
+    o.tag_hash = h ^ (p2p ? 1 : 0) ^ (u64(o.kind) << 1);
+  }
   const bool throttled = cfg.link_bandwidth > 0;
   TraceMarks* tm = nullptr;
   if (trace_on && !cap.active) {
@@ -603,26 +650,64 @@ void Session::post(Open& o, const std::string& tag, bool p2p) {
   MPCG_CUDA(cudaEventRecord(built, stream));
   MPCG_CUDA(cudaStreamWaitEvent(comm_stream, built, 0));
   if (cap.active) cap.comm_used = true;
+  if (n_local == 1 && sock) {  // TCP to a peer process: framed message with its own header
+    if (cap.active) throw Error(kUsageError, "socket link: graph capture is not supported (host I/O)");
+    socket_reap(*this, false);
+    socket_post(*this, o, o.n);
+    if (tm) tm->sent = trace_event(comm_stream);  // staged for the wire
+    check();
+    return;
+  }
+  if (n_local == 1 && p2p) {  // device-initiated peer stores + flag (link.cu)
+    p2p_post(*this, o);
+    if (tm) tm->sent = trace_event(comm_stream);
+    o.ready = pool_event();  // the push has read our payload (its lifetime is the compute stream's)
+    MPCG_CUDA(cudaEventRecord(o.ready, comm_stream));
+    check();
+    return;
+  }
+  const size_t wire = n_local == 1 ? o.n + kTrailer : o.n;  // words on the link
+  if (n_local == 1) {
+    trailer_kernel<<<1, 1, 0, comm_stream>>>(o.own(0) + o.n, o.seq, o.n, o.tag_hash);
+    MPCG_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1);
+  }
   if (n_local == 1 && loop) {
-    if (cap.active) throw Error(kUsageError, "loopback link: graph capture is not supported");
+    if (cap.active) throw Error(kUsageError, "loopback link: graph capture is not supported (use the p2p link)");
     const int me = party_of[0];
     std::unique_lock<std::mutex> lk(loop->mu);
     LoopLink::Slot& sl = loop->slots[u64(o.seq)];
     sl.own[me] = o.own(0);
     sl.in[me] = o.in->ptr;
     sl.built[me] = built;
-    if (sl.arrived == 1 && sl.n != o.n) throw Error(kProtocolError, "loopback link: collective size mismatch");
+    sl.tag_hash[me] = o.tag_hash;
+    if (sl.arrived == 1 && sl.n != o.n) {
+      // wake the peer so it fails too instead of waiting for a transfer that never comes
+      sl.completed = true;
+      sl.n = ~size_t(0);
+      loop->cv.notify_all();
+      throw Error(kProtocolError, "loopback link: collective size mismatch at seq " + std::to_string(o.seq));
+    }
     sl.n = o.n;
     if (++sl.arrived == 2) {
+      // the peer wrote its trailer on its own comm stream: order the copies behind it too
       MPCG_CUDA(cudaStreamWaitEvent(comm_stream, sl.built[1 - me], 0));
-      MPCG_CUDA(cudaMemcpyAsync(sl.in[me], sl.own[1 - me], o.n * sizeof(u64), cudaMemcpyDeviceToDevice, comm_stream));
-      MPCG_CUDA(cudaMemcpyAsync(sl.in[1 - me], sl.own[me], o.n * sizeof(u64), cudaMemcpyDeviceToDevice, comm_stream));
+      if (sl.trailer_done[1 - me]) MPCG_CUDA(cudaStreamWaitEvent(comm_stream, sl.trailer_done[1 - me], 0));
+      MPCG_CUDA(cudaMemcpyAsync(sl.in[me], sl.own[1 - me], wire * sizeof(u64), cudaMemcpyDeviceToDevice, comm_stream));
+      MPCG_CUDA(cudaMemcpyAsync(sl.in[1 - me], sl.own[me], wire * sizeof(u64), cudaMemcpyDeviceToDevice, comm_stream));
       sl.done = pool_event();
       MPCG_CUDA(cudaEventRecord(sl.done, comm_stream));
       sl.completed = true;
       loop->cv.notify_all();
     } else {
+      sl.trailer_done[me] = pool_event();
+      MPCG_CUDA(cudaEventRecord(sl.trailer_done[me], comm_stream));
+      loop->cv.notify_all();
       loop->cv.wait(lk, [&] { return sl.completed; });
+      if (sl.n == ~size_t(0)) {
+        loop->slots.erase(u64(o.seq));
+        throw Error(kProtocolError, "loopback link: collective size mismatch at seq " + std::to_string(o.seq));
+      }
       MPCG_CUDA(cudaStreamWaitEvent(comm_stream, sl.done, 0));
       loop->slots.erase(u64(o.seq));
     }
@@ -631,9 +716,14 @@ void Session::post(Open& o, const std::string& tag, bool p2p) {
     const int peer = 1 - party_of[0];
     auto& api = nccl_api();
     nccl_check(api.GroupStart(), "ncclGroupStart");
-    nccl_check(api.Send(o.own(0), o.n, ncclUint64, peer, nccl, comm_stream), "ncclSend");
-    nccl_check(api.Recv(o.in->ptr, o.n, ncclUint64, peer, nccl, comm_stream), "ncclRecv");
+    nccl_check(api.Send(o.own(0), wire, ncclUint64, peer, nccl, comm_stream), "ncclSend");
+    nccl_check(api.Recv(o.in->ptr, wire, ncclUint64, peer, nccl, comm_stream), "ncclRecv");
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
+  }
+  if (n_local == 1) {
+    trailer_check_kernel<<<1, 1, 0, comm_stream>>>(o.in->ptr + o.n, o.seq, o.n, o.tag_hash, desync_dev_);
+    MPCG_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1);
   }
   if (tm && n_local == 1) tm->sent = trace_event(comm_stream);  // transfer done
   if (throttled) throttle(o);
@@ -646,9 +736,12 @@ void Session::wait(Open& o) {
   if (o.waited) throw Error(kUsageError, "wait() called twice on one handle");
   if (!o.posted) throw Error(kUsageError, "wait() on an open that was never posted");
   o.waited = true;
+  check_desync();  // a mismatch the comm stream has already seen
   const bool timed = o.trace_idx >= 0 && o.trace_gen == trace_gen_ && size_t(o.trace_idx) < trace_marks_.size() &&
                      !cap.active;
   if (timed) trace_marks_[size_t(o.trace_idx)].wait_begin = trace_event(stream);
+  if (sock && n_local == 1 && !o.ready) socket_receive(*this, o);  // blocks until the peer's frame is here
+  if (p2p && n_local == 1) p2p_wait(*this, o);                      // device spin on the peer's flag
   if (o.ready) MPCG_CUDA(cudaStreamWaitEvent(stream, o.ready, 0));
   if (timed) trace_marks_[size_t(o.trace_idx)].wait_end = o.ready ? trace_event(stream) : nullptr;
 }

@@ -141,6 +141,7 @@ struct Open {
   // of the two payloads; consumers read it as one operand (beaver_combine).
   bool summed = false;
   u64* own(int slot) const { return out->ptr + size_t(slot) * n; }
+  u64 tag_hash = 0;              // FNV-1a of the post tag (collective header)
   const u64* peer(int slot) const;
   int n_local = 2;
 };
@@ -163,6 +164,8 @@ constexpr size_t kFlushBytes = size_t(256) << 20;  // > 126 MB L2
 // party to post a collective enqueues both directions on its comm stream; both wait on it.
 struct LoopLink {
   struct Slot {
+    u64 tag_hash[2] = {0, 0};
+    cudaEvent_t trailer_done[2] = {nullptr, nullptr};
     const u64* own[2] = {nullptr, nullptr};
     u64* in[2] = {nullptr, nullptr};
     cudaEvent_t built[2] = {nullptr, nullptr};
@@ -175,6 +178,9 @@ struct LoopLink {
   std::condition_variable cv;
   std::map<u64, Slot> slots;
 };
+
+struct SocketLink;  // link.cu: TCP link between one-party sessions in different processes
+struct P2PLink;     // link.cu: device-flag peer-store link between one-party sessions of a process
 
 class Session {
  public:
@@ -190,6 +196,14 @@ class Session {
   cudaStream_t comm_stream = nullptr;  // link emulation / NCCL
   ncclComm_t nccl = nullptr;
   std::shared_ptr<LoopLink> loop;      // in-process peer (tests of the one-party path on one GPU)
+  std::shared_ptr<SocketLink> sock;    // peer process over TCP (link.cu, the SocketComm counterpart)
+  std::shared_ptr<P2PLink> p2p;        // peer session of this process: device-initiated stores + flags
+  struct SockPending {                 // received frames staged host->device, buffer not yet reusable
+    cudaEvent_t ev;
+    u64* p;
+    size_t words;
+  };
+  std::vector<SockPending> sock_pending;
 
   // data-parallel shard (batch-leading tensors): local rows are a slice of the global batch
   u64 shard_local = 1, shard_global = 1, shard_offset = 0;
@@ -224,6 +238,7 @@ class Session {
     u64* tab = nullptr;              // device: keys [0,kMaxKeys), mask bases [kMaxKeys, +kMaxMasks)
     u64* meta = nullptr;             // device: h[], c0[], mbase0[] for the rekey kernel
     u64* iter = nullptr;             // device replay counter
+    u64* seqd = nullptr;             // device: collectives per replay (p2p flag values)
     std::vector<u64> hs, c0s, mb0;
     std::vector<char> carried;  // key slot adopted from a fetch made before the capture
     bool comm_used = false;     // the comm stream was forked into the capture
@@ -248,6 +263,20 @@ class Session {
   void require_eager_streams(const char* what) const;
 
   // ---- wire
+  // Collective header (H/transport/sim.hpp:101-110 checks seq / shape per reveal): with one
+  // party per session every payload crosses the link with a 3-word trailer {seq, n, tag hash}
+  // written on the comm stream; after the transfer a check kernel compares the peer's trailer
+  // with this party's own and records a mismatch in host-mapped memory. The next wait() /
+  // sync() throws ProtocolError (a desync can only be seen once the payload landed).
+  static constexpr size_t kTrailer = 3;
+  struct Desync {
+    unsigned int bad;
+    unsigned int pad;
+    unsigned long long want[3], got[3];
+  };
+  Desync* desync_ = nullptr;      // host-mapped
+  Desync* desync_dev_ = nullptr;  // its device alias
+  void check_desync();
   Open begin_open(size_t nwords, Reduce kind, std::shared_ptr<Block> out = nullptr,
                   std::shared_ptr<Block> in = nullptr);
   void post(Open& o, const std::string& tag, bool p2p = false);
@@ -305,6 +334,15 @@ class Session {
   size_t event_next_ = 0;
   u64* link_state_ = nullptr;  // device: [next free ns]
 };
+
+void socket_connect(Session& s, const char* host, int port, double timeout_s);
+void socket_post(Session& s, Open& o, size_t words);
+void socket_receive(Session& s, Open& o);
+void socket_reap(Session& s, bool all);
+void p2p_connect(Session& a, Session& b);
+void p2p_post(Session& s, Open& o);
+void p2p_wait(Session& s, const Open& o);
+void p2p_replay_barrier(Session& s);
 
 // ------------------------------------------------------------------ protocol ops
 // Mirrors of the reference free functions; arguments keep their meaning, each DT

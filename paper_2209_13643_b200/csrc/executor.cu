@@ -263,8 +263,8 @@ void SecureExecutor::prepare(size_t i) {
   const DT& W = w_.at(op.wkey);
   const size_t nb = W.numel();
   if (!op.dbuf_out) {  // fixed address: the wrap-around prefetch crosses graph replays
-    op.dbuf_out = Block::persistent(nb * s_.n_local + 1);
-    if (s_.n_local == 1) op.dbuf_in = Block::persistent(nb + 1);
+    op.dbuf_out = Block::persistent(nb * s_.n_local + Session::kTrailer);
+    if (s_.n_local == 1) op.dbuf_in = Block::persistent(nb + Session::kTrailer);
   }
   Open d = s_.begin_open(nb, Reduce::Sum, op.dbuf_out, op.dbuf_in);
   // fused in-device open of delta, on the same condition as eps's (weight_matmul)
@@ -322,24 +322,44 @@ DT SecureExecutor::weight_matmul(size_t i, const DT& x, const ConvGeom* geom, bo
   op.triple.reset();
   op.delta.reset();
   const size_t na = size_t(M) * K;
-  Open e = s_.begin_open(na, Reduce::Sum);
-  DT aops;  // A-side combine operands from the eps draws (memory-operand combines only)
-  if (beaver_combine_wants_aops(s_, 1, M, N, K)) aops = s_.alloc(Shape{2, na});
-  else if (!geom || na < (size_t(1) << 32)) e.summed = beaver_combine_fuses_eps(s_, 1, M, N, K);
-  if (geom)
-    eps_build_im2col(s_, t, x.s, *geom, 0, na, e, aops ? &aops : nullptr);
-  else
-    eps_build_mem(s_, t, x.s, 0, na, e, aops ? &aops : nullptr);
-  s_.post(e, op.tag + ".eps");
+  // Inner-layer pipeline on the linear layer (extension, ExecOptions::linear_chunks; the
+  // reference's weight_matmul opens eps whole, H/engine/executor.hpp:305): the activation-side
+  // opening leaves in n row blocks "<tag>.eps.chunk<k>" and the combine GEMM of block k runs as
+  // soon as it lands, while blocks k+1.. are still in flight — the chunk unit and labels of
+  // beaver_matmul (H/protocols/beaver.hpp:197-250). Triples, values and bytes are unchanged; a
+  // conv chunk is a block of whole output rows (n, oh) so the im2col build stays tiled.
+  int nch = opt_.pipelined && opt_.linear_chunks ? chunks_for(s_, na) : 1;
+  const size_t unit = geom ? size_t(geom->OW) : 1;  // rows per chunk granule
+  nch = clamp_chunks(nch, M / unit);
+  std::vector<Open> es(static_cast<size_t>(nch));
+  std::vector<DT> aops(static_cast<size_t>(nch));  // A-side combine operands (memory-operand combines only)
+  std::vector<std::pair<size_t, size_t>> rows(static_cast<size_t>(nch));
+  for (int k = 0; k < nch; ++k) {
+    const auto r = chunk_range(M / unit, nch, k);
+    rows[k] = {r.first * unit, k + 1 == nch ? size_t(M) : r.second * unit};
+    const u32 mk = u32(rows[k].second - rows[k].first);
+    const size_t nak = size_t(mk) * K;
+    es[k] = s_.begin_open(nak, Reduce::Sum);
+    if (beaver_combine_wants_aops(s_, 1, mk, N, K)) aops[k] = s_.alloc(Shape{2, nak});
+    else if (!geom || nak < (size_t(1) << 32)) es[k].summed = beaver_combine_fuses_eps(s_, 1, mk, N, K);
+    if (geom)
+      eps_build_im2col(s_, t, x.s, *geom, rows[k].first * K, nak, es[k], aops[k] ? &aops[k] : nullptr);
+    else
+      eps_build_mem(s_, t, x.s, rows[k].first * K, nak, es[k], aops[k] ? &aops[k] : nullptr);
+    s_.post(es[k], nch == 1 ? op.tag + ".eps" : op.tag + ".eps.chunk" + std::to_string(k));
+  }
   if (opt_.pipelined && wops_.size() > 1) {  // next op's delta leaves while this eps travels
     const size_t next = (i + 1) % wops_.size();
     if (!wops_[next].triple) prepare(next);
   }
   s_.wait(d);
-  s_.wait(e);
   DT rcache;
-  beaver_combine(s_, t, e, 0, na, d, W.numel(), &rcache, z.s, 0, 1, M, N, K, false, false, 0, ep,
-                 aops ? &aops : nullptr);
+  for (int k = 0; k < nch; ++k) {
+    const u32 mk = u32(rows[k].second - rows[k].first);
+    s_.wait(es[k]);
+    beaver_combine(s_, t, es[k], rows[k].first * K, size_t(mk) * K, d, W.numel(), &rcache, z.s,
+                   rows[k].first * N, 1, mk, N, K, false, false, 0, ep, aops[k] ? &aops[k] : nullptr);
+  }
   return z;
 }
 

@@ -52,6 +52,9 @@ struct ExecOptions {
   int chunks = 4;
   u64 chunk_threshold = u64(2) << 20;
   bool merged_adder = true;
+  // Extension: also chunk the linear layers' activation-side opening (inner-layer pipeline on
+  // conv / dense, `north_star` (3)). Off = the reference's unchunked weight_matmul traffic.
+  bool linear_chunks = false;
 };
 
 struct LayerTiming {  // per-layer device time of the last timed run (ms)

@@ -576,11 +576,13 @@ __global__ void __launch_bounds__(256) eps_im2col_summed_kernel(MmTriple mm, Con
 // kernel is bound by its coalesced E stores.
 __global__ void __launch_bounds__(256) eps_im2col_tile_kernel(MmTriple mm, ConvGeom g, const u64* __restrict__ x0,
                                                              const u64* __restrict__ x1, u64* __restrict__ out,
-                                                             u32 cc_max, FastDiv fkk, FastDiv fk, u64 a_off) {
+                                                             u32 cc_max, FastDiv fkk, FastDiv fk, u32 rowid0) {
   extern __shared__ u64 sx[];
   pdl_enter();
   const u32 owt = (g.OW + 7) / 8;
-  const u32 bt = blockIdx.x % owt, rowid = blockIdx.x / owt;  // rowid = n*OH + oh
+  // rowid = n*OH + oh; this call covers rowids [rowid0, rowid0 + gridDim.x / owt) and writes
+  // them from out[0] (a row-block chunk of the eps payload), drawing A at the global index
+  const u32 bt = blockIdx.x % owt, rowid = rowid0 + blockIdx.x / owt;
   const u32 oh = rowid % g.OH, n = rowid / g.OH;
   const u32 ow0 = bt * 8, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const u32 ow = ow0 + warp;
@@ -607,11 +609,12 @@ __global__ void __launch_bounds__(256) eps_im2col_tile_kernel(MmTriple mm, ConvG
     if (ow >= g.OW) continue;
     const u32 ncol = cc * kk;
     const u64 jb = r * K + u64(c0) * kk;
-    u64 z = key + (a_off + jb + lane) * kPhi;
+    const u64 ob = jb - u64(rowid0) * g.OW * K;
+    u64 z = key + (jb + lane) * kPhi;
     for (u32 cl = lane; cl < ncol; cl += 32, z += 32 * kPhi) {
       const u32 ci = fkk.div(cl), t2 = cl - ci * kk, ki = fk.div(t2), kj = t2 - ki * g.k;
       const u64 v = sx[(ci * g.k + ki) * ww + warp * g.stride + kj];
-      out[jb + cl] = v - mix64(z);  // eps0 + eps1 = x0 + x1 - (a0 + a1), a0 + a1 = A
+      out[ob + cl] = v - mix64(z);  // eps0 + eps1 = x0 + x1 - (a0 + a1), a0 + a1 = A
     }
   }
 }
@@ -636,15 +639,16 @@ void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const 
   const u32 Kc = gm.C * gm.k * gm.k;
   const u32 ww = 7 * gm.stride + gm.k;
   const u32 cc_max = u32((48 * 1024) / (8 * gm.k * ww));
-  if (o.summed && s.n_local == 2 && !aops && a_off == 0 && na == u64(gm.N) * gm.OH * gm.OW * Kc && cc_max >= 1 &&
+  const u64 row_words = u64(gm.OW) * Kc;  // one (n, oh) output row of the im2col matrix
+  if (o.summed && s.n_local == 2 && !aops && a_off % row_words == 0 && na % row_words == 0 && cc_max >= 1 &&
       tile_eps_enabled()) {
     const u32 cc = cc_max < gm.C ? cc_max : gm.C;
     const size_t smem = size_t(cc) * gm.k * ww * 8;
-    const u64 blocks = u64(gm.N) * gm.OH * ((gm.OW + 7) / 8);
+    const u64 blocks = u64(na / row_words) * ((gm.OW + 7) / 8);
     cudaEvent_t pe;
     probe_begin(s.stream, &pe);
     launch_pdl(eps_im2col_tile_kernel, dim3(unsigned(blocks)), dim3(256), smem, s.stream, t.mm, gm, x[0], x[1],
-               o.own(0), cc, FastDiv(gm.k * gm.k), FastDiv(gm.k), u64(a_off));
+               o.own(0), cc, FastDiv(gm.k * gm.k), FastDiv(gm.k), u32(a_off / row_words));
     probe_end(s.stream, pe);
     return;
   }
@@ -735,6 +739,7 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
   a.trunc_bits = ep.trunc_bits;
   a.col2im = ep.col2im;
   a.OHW = ep.OHW;
+  a.row0 = ep.col2im ? u32(out_off / N) : 0;
   for (int i = 0; i < s.n_local; ++i) a.sl[i].nseg = s.party_of[i] == 0 ? 3 : 2;
   const u64 sL = u64(M) * K, sR = batched_r ? u64(K) * N : 0;
   const u64 rboff = batched_r ? r_batch0 * u64(K) * N : 0;
@@ -746,7 +751,7 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
     const int ek = e.summed ? kOpMem : kOpSum;  // E = own + peer, or already summed
     const u64* F0 = (d.summed ? d.own(0) : d.own(i)) + rboff;
     const u64* F1 = d.summed ? nullptr : d.peer(i) + rboff;  // null: F summed at build time
-    S.out = out[i] + out_off;
+    S.out = ep.col2im ? out[i] : out[i] + out_off;  // col2im scatters by global row (a.row0)
     S.bias = ep.bias[i];
     S.ckey = t.mm.key;
     S.ckp = t.mm.kp;

@@ -47,6 +47,7 @@ struct GemmArgs {
   int trunc_bits = 0;  // 2PC local truncation (H/protocols/trunc.hpp:41)
   int col2im = 0;      // store NCHW with row = (n, oh, ow)  (H/engine/executor.hpp:110-123)
   u32 OHW = 1;
+  u32 row0 = 0;        // col2im: global row of this call's row 0 (row-block chunks of one conv)
   // split-K over the concatenated K' = nseg*K axis: partial sums are added mod 2^64 into
   // acc[slot] ([nbatch][M][N], zeroed) and a second kernel applies the epilogue.
   u32 ksplit = 1, kchunk = 0;
@@ -101,7 +102,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& a, const GemmSlotA
   if (a.trunc_bits) v = sar64(v, a.trunc_bits);
   if (S.bias) v += S.bias[n];
   if (a.col2im) {
-    const u32 img = m / a.OHW, rem = m - img * a.OHW;
+    const u32 mg = m + a.row0, img = mg / a.OHW, rem = mg - img * a.OHW;
     S.out[(u64(img) * a.N + n) * a.OHW + rem] = v;
   } else {
     S.out[lin] = v;

@@ -16,10 +16,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PHI = 0x9E3779B97F4A7C15
 
 
-def _run_pair(mp, g, mode, weights, iters, link=None):
+def _run_pair(mp, g, mode, weights, iters, link=None, kind="loopback", graph=False):
     sess = [mp.Session(device=0, n_local=1, party=p, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
             for p in (0, 1)]
-    sess[0].connect_loopback(sess[1])
+    if kind == "p2p":
+        sess[0].connect_p2p(sess[1])
+    else:
+        sess[0].connect_loopback(sess[1])
     if link:
         for s in sess:
             s.set_link(*link)
@@ -34,8 +37,14 @@ def _run_pair(mp, g, mode, weights, iters, link=None):
             ex.deal_weights(w, 1)
             xin = s.deal_input(x, 2)
             z = None
-            for _ in range(iters):
+            if graph:  # one eager run (pipelined prologue), capture, then replays = iterations 2..
                 z = ex.run(xin)
+                ex.capture(xin)
+                for _ in range(iters - 1):
+                    z = ex.replay()
+            else:
+                for _ in range(iters):
+                    z = ex.run(xin)
             out[p] = z.numpy()[0]
             s.sync()
         except Exception as e:  # noqa: BLE001
@@ -75,3 +84,85 @@ def test_one_party_sessions_extension_graph_and_link():
     (z0, z1), _ = _run_pair(mp, g, "pipelined", "private", 1, link=(2e-6, 5e9, 0.0))
     assert np.array_equal(z0.reshape(-1), ref[0].reshape(-1))
     assert np.array_equal(z1.reshape(-1), ref[1].reshape(-1))
+
+
+def _pair_ops(mp, fns):
+    """Run fns[p](session_p) for the two loopback-linked one-party sessions on two threads;
+    returns the exceptions raised per party."""
+    sess = [mp.Session(device=0, n_local=1, party=p, seed=5, mask_seed=6, frac_bits=16) for p in (0, 1)]
+    sess[0].connect_loopback(sess[1])
+    errs = [None, None]
+
+    def party(p):
+        try:
+            fns[p](mp, sess[p])
+            sess[p].sync()
+        except Exception as e:  # noqa: BLE001
+            errs[p] = e
+
+    th = [threading.Thread(target=party, args=(p,)) for p in (0, 1)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not any(t.is_alive() for t in th), "a party hung on a desynchronised collective"
+    return errs
+
+
+def _mul(n, tag):
+    def f(mp, s):
+        x = s.tensor(np.arange(n, dtype=np.uint64).reshape(1, n), 16)
+        mp.beaver_mul(s, x, x, tag)
+    return f
+
+
+def test_collective_desync_raises_protocol_error():
+    """H/transport/sim.hpp:101-110: parties that issue different collectives at the same
+    sequence number fail with ProtocolError (here via the {seq, n, tag} trailer every one-party
+    payload carries, checked on the receiving side) instead of computing garbage."""
+    import paper_2209_13643_b200 as mp
+    errs = _pair_ops(mp, [_mul(16, "same"), _mul(16, "same")])
+    assert errs == [None, None]
+    errs = _pair_ops(mp, [_mul(16, "alpha"), _mul(16, "beta")])
+    assert all(isinstance(e, mp.ProtocolError) for e in errs), errs
+    errs = _pair_ops(mp, [_mul(16, "m"), _mul(24, "m")])  # size mismatch: caught at post
+    assert all(isinstance(e, mp.ProtocolError) for e in errs), errs
+
+
+@pytest.mark.parametrize("name,mode,weights,it", [
+    ("mlp", "pipelined", "private", 2), ("lenet5", "pipelined", "private", 1),
+    ("toy_transformer", "blocking", "private", 1), ("toy_cnn", "pipelined", "public", 1)])
+def test_p2p_device_flag_link_matches_reference(name, mode, weights, it):
+    """Device-initiated opens (mpcg_session_connect_p2p): the sender's comm stream stores its
+    payload into the peer's inbox and releases a flag the peer's stream acquires on device."""
+    import paper_2209_13643_b200 as mp
+    g = mp.ModelGraph.from_json(os.path.join(ROOT, "configs", name + ".json"))
+    m = np.load(os.path.join(ROOT, "tests", "golden", f"model_{name}_{mode}_{weights}_it{it}.npz"))
+    (z0, z1), sess = _run_pair(mp, g, mode, weights, it, kind="p2p")
+    assert np.array_equal(z0.reshape(-1), m["z0"].reshape(-1)), "party 0 share differs"
+    assert np.array_equal(z1.reshape(-1), m["z1"].reshape(-1)), "party 1 share differs"
+    assert sess[0].stats(0) == sess[1].stats(0)
+
+
+@pytest.mark.parametrize("name,it", [("mlp", 2), ("lenet5", 1)])
+def test_p2p_link_graph_replays(name, it):
+    """Each party captures its own inference into a CUDA graph (flag values follow the replay
+    counter); concurrent replays of the two graphs reproduce the reference iteration by
+    iteration."""
+    import paper_2209_13643_b200 as mp
+    g = mp.ModelGraph.from_json(os.path.join(ROOT, "configs", name + ".json"))
+    m = np.load(os.path.join(ROOT, "tests", "golden", f"model_{name}_pipelined_private_it{it}.npz"))
+    iters = max(it, 2)
+    (z0, z1), _ = _run_pair(mp, g, "pipelined", "private", iters, kind="p2p", graph=True)
+    if it == iters:
+        assert np.array_equal(z0.reshape(-1), m["z0"].reshape(-1))
+        assert np.array_equal(z1.reshape(-1), m["z1"].reshape(-1))
+    else:  # compare replay 1 (= iteration 2) with eager two-slot iteration 2
+        s = mp.Session(device=0, n_local=2, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
+        ex = mp.SecureExecutor(s, g, pipelined=True)
+        ex.deal_weights(mp.init_weights(g, 12), 1)
+        x = s.deal_input(mp.demo_input(g, 13), 2)
+        for _ in range(iters):
+            ze = ex.run(x).numpy()
+        assert np.array_equal(z0.reshape(-1), ze[0].reshape(-1))
+        assert np.array_equal(z1.reshape(-1), ze[1].reshape(-1))

@@ -313,3 +313,31 @@ def test_set_link_rejects_latency_only(mp):
         s.set_link(-1.0, 1e9, 0.0)
     s.set_link(1e-4, 1.25e9, 0.0)
     s.set_link(0.0, 0.0, 0.0)  # back to the real transport
+
+
+@pytest.mark.parametrize("pair_eval", [True, False], ids=["pair", "per-slot"])
+@pytest.mark.parametrize("name,golden,chunks", [
+    ("lenet5", "model_lenet5_pipelined_private_it1", 4), ("toy_cnn", "model_toy_cnn_blocking_private_it1", 3),
+    ("toy_transformer", "model_toy_transformer_blocking_private_it1", 2)])
+def test_linear_chunks_keep_reference_shares(mp, name, golden, chunks, pair_eval):
+    """Inner-layer pipeline on the linear layers (ExecOptions::linear_chunks): the eps opening
+    leaves in row blocks '<tag>.eps.chunk<k>' and each block's combine runs as it lands. The
+    triples are keyed by tag, so the per-party shares equal the reference's unchunked run."""
+    from paper_2209_13643_b200 import api
+    g = mp.ModelGraph.from_json(os.path.join(ROOT, "configs", name + ".json"))
+    m = np.load(os.path.join(ROOT, "tests", "golden", golden + ".npz"))
+    api.set_pair_eval(pair_eval)
+    try:
+        s = mp.Session(device=0, n_local=2, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
+        ex = mp.SecureExecutor(s, g, pipelined=True, chunks=chunks, chunk_threshold=0, linear_chunks=True)
+        ex.deal_weights(mp.init_weights(g, 12), 1)
+        x = s.deal_input(mp.demo_input(g, 13), 2)
+        s.trace(True)
+        z = ex.run(x).numpy()
+    finally:
+        api.set_pair_eval(True)
+    assert np.array_equal(z[0].reshape(-1), m["z0"].reshape(-1)), "party 0 share differs"
+    assert np.array_equal(z[1].reshape(-1), m["z1"].reshape(-1)), "party 1 share differs"
+    tags = [r["tag"] for r in s.trace_rows()]
+    first = api.linear_tags(g)[0]
+    assert first + ".eps.chunk0" in tags and first + ".eps" not in tags

@@ -108,14 +108,16 @@ def test_op_at_baseline_scale(mp, G, name, seed, f, build, fn):
 MODELS = ["r18_l1conv", "r18_l4conv", "vgg_fc6", "bert_ffn1", "bert_ffn2"]
 
 
-@pytest.mark.parametrize("mode", ["blocking", "pipelined"])
+@pytest.mark.parametrize("mode", ["blocking", "pipelined", "chunked"])
 @pytest.mark.parametrize("name", MODELS)
 def test_linear_layer_at_baseline_scale(mp, G, name, mode):
     """SecureExecutor::run of one linear layer at a BASELINE shape (private weights, seed 1):
-    the reference's per-party output shares, in both modes (AC2: modes are bit-identical)."""
+    the reference's per-party output shares, in every mode (AC2: modes are bit-identical;
+    "chunked" = pipelined with the inner-layer pipeline on the linear layer, 4 eps row blocks)."""
     g = mp.ModelGraph.from_json(os.path.join(GOLD, "scale", name + ".json"))
     s = mp.Session(device=0, n_local=2, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
-    ex = mp.SecureExecutor(s, g, pipelined=mode == "pipelined")
+    ex = mp.SecureExecutor(s, g, pipelined=mode != "blocking", chunks=4, chunk_threshold=THR,
+                           linear_chunks=mode == "chunked")
     ex.deal_weights(mp.init_weights(g, 12), 1)
     x = s.deal_input(mp.demo_input(g, 13), 2)
     z = ex.run(x).numpy()

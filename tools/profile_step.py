@@ -10,10 +10,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2209_13643_b200 as mp  # noqa: E402
 from paper_2209_13643_b200 import api  # noqa: E402
 
-model = os.environ.get("MODEL", "lenet5")
+model = os.environ.get("MODEL", "resnet18")
 g = mp.ModelGraph.from_json(model)
 s = mp.Session(device=0, n_local=2, seed=1, frac_bits=g.frac_bits)
-ex = mp.SecureExecutor(s, g, pipelined=True, chunk_threshold=1 << 62)
+# the bench.py configuration: pipelined, 4 chunk lanes for operands >= the reference's 2 MiB
+thr = int(os.environ.get("THR", str(2 << 20)))
+ex = mp.SecureExecutor(s, g, pipelined=True, chunks=4, chunk_threshold=thr)
 ex.deal_weights(mp.init_weights(g, 12), 1)
 x = s.deal_input(mp.demo_input(g, 13), 2)
 ex.run(x)            # warm-up (includes the pipelined prologue)
