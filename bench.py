@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-variants", action="store_true",
                     help="skip the per-slot and loopback one-party co-location measurements")
     ap.add_argument("--chunks", type=int, default=4, help="inner-layer pipeline chunk count (ExecOptions::chunks)")
+    ap.add_argument("--linear-chunks", action="store_true",
+                    help="inner-layer pipeline on the conv / dense layers too (eps opened in row blocks; "
+                         "extension: the reference's weight_matmul is unchunked)")
     ap.add_argument("--link", default="",
                     help="emulate a LAN/WAN link between the parties, e.g. 10gbps (1.25e9 B/s, 0.1 ms) or "
                          "'<latency_s>,<bytes_per_s>'; default: the real in-device / NVLink transport")
@@ -319,7 +322,7 @@ def main():
         if link:
             s.set_link(*link)
         ex = mp.SecureExecutor(s, g, public_weights=a.weights == "public", pipelined=mode == "pipelined",
-                               chunks=a.chunks, chunk_threshold=thr)
+                               chunks=a.chunks, chunk_threshold=thr, linear_chunks=a.linear_chunks)
         ex.deal_weights(weights, seed)
         x = s.deal_input(x_global, seed + 1, batch_offset=B * pair, local_batch=B)
         return s, ex, x
@@ -522,7 +525,7 @@ def main():
         "data": "synthetic: the reference's seeded init_weights(seed 12) / demo_input(seed 13), shares dealt on host",
         "config": {"workload": workload_name(g, a), "model": g.name, "global_batch": B * pairs,
                    "pairs": pairs, "parties_per_gpu": 2 if world == 1 else 1, "mode": a.mode, "weights": a.weights,
-                   "frac_bits": g.frac_bits, "chunks": a.chunks,
+                   "frac_bits": g.frac_bits, "chunks": a.chunks, "linear_chunks": a.linear_chunks,
                    "chunk_threshold_bytes": None if thr == NEVER else thr,
                    "chunk_threshold_source": a.threshold,
                    "calibration": calib,
@@ -572,7 +575,7 @@ def loopback_ms(mp, g, weights, x_global, a, thr, link, seed):
         try:
             s = sess[p]
             ex = mp.SecureExecutor(s, g, public_weights=a.weights == "public", pipelined=a.mode == "pipelined",
-                                   chunks=a.chunks, chunk_threshold=thr)
+                                   chunks=a.chunks, chunk_threshold=thr, linear_chunks=a.linear_chunks)
             ex.deal_weights(weights, seed)
             x = s.deal_input(x_global, seed + 1)
             for _ in range(2):

@@ -48,6 +48,7 @@ typedef struct mpcg_session mpcg_session;
 typedef struct mpcg_tensor mpcg_tensor;
 typedef struct mpcg_model mpcg_model;
 typedef struct mpcg_executor mpcg_executor;
+typedef struct mpcg_triple_queue mpcg_triple_queue;
 
 /* Thread-local message of the last failing call. */
 const char* mpcg_last_error(void);
@@ -147,6 +148,30 @@ int mpcg_layernorm(mpcg_session* s, const mpcg_tensor* x, uint64_t d, const mpcg
                    const mpcg_tensor* beta, int public_weights, const char* tag, mpcg_tensor** out);
 int mpcg_global_avg_pool(mpcg_session* s, const mpcg_tensor* x, uint64_t N, uint64_t C, uint64_t HW,
                          mpcg_tensor** out);
+
+/* ---- TripleSource plugin (sharing/triple.hpp:126-179): offline/online split ----
+ * A queue holds materialised 2PC triples, consumed in fetch order with the reference's
+ * QueueTripleSource semantics (spec checked -> MPCG_ERR_PROTOCOL "triple queue spec mismatch at
+ * record i" / "triple queue exhausted"; tags ignored). Offline: a session in record mode
+ * materialises every triple it fetches from its seeded dealer into the queue, or a queue is
+ * loaded from a reference triple file (save_triples format, triple.hpp:181-307; records must be
+ * valid Beaver triples). Online: a session using the queue reads triples from HBM instead of
+ * regenerating them. Queues are device-resident on the session's GPU; not for graph capture or
+ * data-parallel shards. */
+int mpcg_triple_queue_create(mpcg_triple_queue** out);
+int mpcg_triple_queue_destroy(mpcg_triple_queue* q);
+int mpcg_triple_queue_size(mpcg_triple_queue* q, uint64_t* records, uint64_t* consumed);
+int mpcg_triple_queue_rewind(mpcg_triple_queue* q);
+int mpcg_triple_queue_save(mpcg_triple_queue* q, const char* path);   /* save_triples */
+int mpcg_triple_queue_load(mpcg_triple_queue* q, const char* path);   /* load_triples (appends) */
+int mpcg_session_record_triples(mpcg_session* s, mpcg_triple_queue* q /* NULL stops */);
+int mpcg_session_use_triple_queue(mpcg_session* s, mpcg_triple_queue* q /* NULL = seeded dealer */);
+/* TripleSource::fetch (triple.hpp:126-130): this session's local party shares of the next triple
+ * for the spec (kind 0 arith / 1 binary; matmul; square; transpose_b), from the seeded dealer or
+ * the queue in use. Returns three tensors (a, b, c), one share per local slot. */
+int mpcg_dealer_fetch(mpcg_session* s, int kind, int matmul, int square, int transpose_b, int nda,
+                      const uint64_t* dims_a, int ndb, const uint64_t* dims_b, const char* tag, mpcg_tensor** a,
+                      mpcg_tensor** b, mpcg_tensor** c);
 
 /* ---- model + executor (engine/model.hpp, engine/executor.hpp:173-205) ---- */
 #define MPCG_LAYER_DENSE 0

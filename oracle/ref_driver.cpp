@@ -21,6 +21,9 @@
 //       Reference ops at BASELINE shapes (ResNet-18 ReLU, VGG-16 pool1, BERT-base softmax /
 //       QK^T / AV, full-word GEMMs at ResNet-18 layer4 and VGG-16 fc6), pinned the same way.
 //
+//   ref_driver triples <out.bin>
+//       Two dealer triples written by the reference's save_triples (triple-file pin).
+//
 //   ref_driver opsum <model.json> <private|public> <div> <pairs> <seed>
 //       Op-sum CPU estimate of one inference (configs the reference cannot express): the
 //       reference's ops timed at every layer's shape on 1/div of its rows, scaled; `pairs`
@@ -669,6 +672,28 @@ int cmd_opsum(const char* model_path, const char* weights, std::size_t div, int 
   return 0;
 }
 
+// Triple-file pin: the triples SeededDealer(5, *, 2) hands out for "t.mul" [3,4] and "t.qk"
+// [2,3,4]x[2,5,4]^T (first fetch of each tag, H/sharing/triple.hpp:138-151), written with the
+// reference's save_triples (:181-218) — the format the GPU queue loader must read.
+int cmd_triples(const char* path) {
+  auto stream_of = [](const std::string& tag) {
+    u64 h = 0xcbf29ce484222325ull;
+    for (char c : tag) h = (h ^ u64(static_cast<unsigned char>(c))) * 0x100000001b3ull;
+    return CounterRng::mix(h + 0x51ed270b * 0);
+  };
+  std::vector<TripleSet> sets;
+  {
+    CounterRng rng(5, stream_of("t.mul"));
+    sets.push_back(dealer_gen_triple(TripleSpec::elementwise(TripleKind::Arith, {3, 4}), 2, rng));
+  }
+  {
+    CounterRng rng(5, stream_of("t.qk"));
+    sets.push_back(dealer_gen_triple(TripleSpec::matmul_of({2, 3, 4}, {2, 5, 4}, true), 2, rng));
+  }
+  save_triples(path, sets);
+  return 0;
+}
+
 // MPCW interchange check: the reference's own init_weights(model, seed) written by its
 // save_weights (H/engine/model.hpp:257-275,277-313), and a file read back by its
 // load_weights + check_weights (:315-376) and re-saved, so the package's MPCW reader/writer
@@ -698,6 +723,7 @@ int main(int argc, char** argv) {
       return cmd_model_golden(argv[2], argv[3], std::atoi(argv[4]), argv[5],
                               std::strtoull(argv[6], nullptr, 10), argv[7], true);
     if (argc >= 4 && std::string(argv[1]) == "scale") return cmd_scale(argv[2], argv[3]);
+    if (argc >= 3 && std::string(argv[1]) == "triples") return cmd_triples(argv[2]);
     if (argc >= 7 && std::string(argv[1]) == "opsum")
       return cmd_opsum(argv[2], argv[3], std::strtoull(argv[4], nullptr, 10), std::atoi(argv[5]),
                        std::strtoull(argv[6], nullptr, 10));
@@ -713,6 +739,7 @@ int main(int argc, char** argv) {
                "       ref_driver model <model.json> <mode> <iters> <private|public> <seed> <out.bin>\n"
                "       ref_driver model_pin <model.json> <mode> <iters> <private|public> <seed> <out.bin>\n"
                "       ref_driver scale <case|all> <out.bin>\n"
+               "       ref_driver triples <out.bin>\n"
                "       ref_driver opsum <model.json> <private|public> <div> <pairs> <seed>\n"
                "       ref_driver bench <model.json> <mode> <iters> <private|public> <seed> [chunks thr]\n"
                "       ref_driver mpcw <model.json> <seed> <out.mpcw> [<in.mpcw>]\n");

@@ -55,6 +55,15 @@ SIGNATURES = {
     "mpcg_session_connect_nccl": [P, C.c_char_p, I32],
     "mpcg_session_connect_socket": [P, C.c_char_p, I32, DBL],
     "mpcg_session_connect_p2p": [P, P],
+    "mpcg_triple_queue_create": [PP],
+    "mpcg_triple_queue_destroy": [P],
+    "mpcg_triple_queue_size": [P, U64P, U64P],
+    "mpcg_triple_queue_rewind": [P],
+    "mpcg_triple_queue_save": [P, STR],
+    "mpcg_triple_queue_load": [P, STR],
+    "mpcg_session_record_triples": [P, P],
+    "mpcg_session_use_triple_queue": [P, P],
+    "mpcg_dealer_fetch": [P, I32, I32, I32, I32, I32, U64P, I32, U64P, STR, PP, PP, PP],
     "mpcg_session_sync": [P],
     "mpcg_session_set_persistent": [P, I32],
     "mpcg_session_stats": [P, I32, U64P],

@@ -368,6 +368,59 @@ def timer(s: Session, op: str) -> float:
     return ms.value
 
 
+# ---- TripleSource plugin (H/sharing/triple.hpp:126-307) ---------------------------
+class TripleQueue:
+    """Materialised 2PC triples consumed in fetch order (QueueTripleSource): recorded by a
+    session's seeded dealer (offline phase) or loaded from a reference triple file."""
+
+    def __init__(self):
+        h = C.c_void_p()
+        N.call("mpcg_triple_queue_create", C.byref(h))
+        self._h = h
+
+    def __del__(self):
+        try:
+            if self._h:
+                N.lib().mpcg_triple_queue_destroy(self._h)
+        except Exception:
+            pass
+
+    def size(self):
+        r, c = C.c_uint64(), C.c_uint64()
+        N.call("mpcg_triple_queue_size", self._h, C.byref(r), C.byref(c))
+        return {"records": r.value, "consumed": c.value}
+
+    def rewind(self):
+        N.call("mpcg_triple_queue_rewind", self._h)
+
+    def save(self, path):
+        N.call("mpcg_triple_queue_save", self._h, path.encode())
+
+    def load(self, path):
+        N.call("mpcg_triple_queue_load", self._h, path.encode())
+
+
+def record_triples(s: Session, q):
+    """Offline dealer: every triple `s` fetches is also materialised into `q` (None stops)."""
+    N.call("mpcg_session_record_triples", s.handle, q._h if q is not None else None)
+
+
+def use_triple_queue(s: Session, q):
+    """Online phase: `s` consumes triples from `q` in order (None = back to the seeded dealer)."""
+    N.call("mpcg_session_use_triple_queue", s.handle, q._h if q is not None else None)
+
+
+def dealer_fetch(s: Session, shape_a, shape_b=None, kind="arith", matmul=False, square=False, transpose_b=False,
+                 tag=""):
+    """TripleSource::fetch: (a, b, c) tensors holding this session's party shares."""
+    sa = np.array(shape_a, dtype=np.uint64)
+    sb = np.array(shape_b if shape_b is not None else shape_a, dtype=np.uint64)
+    ha, hb, hc = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    N.call("mpcg_dealer_fetch", s.handle, int(kind == "bin"), int(matmul), int(square), int(transpose_b), sa.size,
+           _u64p(sa), sb.size, _u64p(sb), _tag(tag), C.byref(ha), C.byref(hb), C.byref(hc))
+    return Tensor(s, ha), Tensor(s, hb), Tensor(s, hc)
+
+
 # ---- run report (H/engine/report.hpp:25-81) --------------------------------------
 def linear_tags(g: ModelGraph):
     """SecureExecutor::linear_tags (H/engine/executor.hpp:208-218): one per weight op, in

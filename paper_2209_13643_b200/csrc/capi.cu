@@ -147,6 +147,96 @@ int mpcg_nccl_unique_id(uint8_t out[128]) {
   return guard([&] { nccl_unique_id(out); });
 }
 
+// ---- triple queues (TripleSource / QueueTripleSource, H/sharing/triple.hpp:126-307)
+struct mpcg_triple_queue {
+  std::shared_ptr<TripleQueue> q;
+};
+
+int mpcg_triple_queue_create(mpcg_triple_queue** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = new mpcg_triple_queue{std::make_shared<TripleQueue>()};
+  });
+}
+
+int mpcg_triple_queue_destroy(mpcg_triple_queue* q) {
+  delete q;
+  return 0;
+}
+
+int mpcg_triple_queue_size(mpcg_triple_queue* q, uint64_t* records, uint64_t* consumed) {
+  return guard([&] {
+    need(q, "queue");
+    if (records) *records = q->q->items.size();
+    if (consumed) *consumed = q->q->next;
+  });
+}
+
+int mpcg_triple_queue_rewind(mpcg_triple_queue* q) {
+  return guard([&] {
+    need(q, "queue");
+    q->q->next = 0;
+  });
+}
+
+int mpcg_triple_queue_save(mpcg_triple_queue* q, const char* path) {
+  return guard([&] {
+    need(q, "queue");
+    need(path, "path");
+    queue_save(*q->q, path);
+  });
+}
+
+int mpcg_triple_queue_load(mpcg_triple_queue* q, const char* path) {
+  return guard([&] {
+    need(q, "queue");
+    need(path, "path");
+    queue_load(*q->q, path);
+  });
+}
+
+int mpcg_session_record_triples(mpcg_session* s, mpcg_triple_queue* q) {
+  return guard([&] {
+    Session& ss = S(s);
+    if (q && ss.source_q) throw Error(kUsageError, "record and consume modes are exclusive");
+    ss.record_q = q ? q->q : nullptr;
+  });
+}
+
+int mpcg_session_use_triple_queue(mpcg_session* s, mpcg_triple_queue* q) {
+  return guard([&] {
+    Session& ss = S(s);
+    if (q && ss.record_q) throw Error(kUsageError, "record and consume modes are exclusive");
+    ss.source_q = q ? q->q : nullptr;
+  });
+}
+
+int mpcg_dealer_fetch(mpcg_session* s, int kind, int matmul, int square, int transpose_b, int nda,
+                      const uint64_t* dims_a, int ndb, const uint64_t* dims_b, const char* tag, mpcg_tensor** a,
+                      mpcg_tensor** b, mpcg_tensor** c) {
+  return guard([&] {
+    need(a, "a");
+    need(b, "b");
+    need(c, "c");
+    if (nda < 1 || ndb < 1 || nda > 8 || ndb > 8) throw Error(kShapeError, "dealer_fetch: bad rank");
+    TripleSpec sp;
+    sp.kind = kind ? TripleKind::Bin : TripleKind::Arith;
+    sp.matmul = matmul != 0;
+    sp.square = square != 0;
+    sp.transpose_b = transpose_b != 0;
+    sp.shape_a.assign(dims_a, dims_a + nda);
+    sp.shape_b.assign(dims_b, dims_b + ndb);
+    if (sp.matmul && (sp.square || sp.kind == TripleKind::Bin))
+      throw Error(kConfigError, "dealer_fetch: matmul triples are arithmetic and not square");
+    if (!sp.matmul && sp.shape_a != sp.shape_b) throw Error(kConfigError, "dealer_gen_triple: elementwise shapes differ");
+    DT x, y, z;
+    dealer_fetch(S(s), sp, tag ? tag : "", x, y, z);
+    *a = wrap(SP(s), x);
+    *b = wrap(SP(s), y);
+    *c = wrap(SP(s), z);
+  });
+}
+
 int mpcg_session_connect_p2p(mpcg_session* a, mpcg_session* b) {
   return guard([&] { p2p_connect(S(a), S(b)); });
 }

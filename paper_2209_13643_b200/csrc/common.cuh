@@ -75,6 +75,15 @@ __host__ __device__ __forceinline__ u64 mix64(u64 z) {
 // draw #c (c >= 1) of the stream keyed `key` (already key ^ stream*phi).
 __host__ __device__ __forceinline__ u64 drw(u64 key, u64 c) { return mix64(key + c * kPhi); }
 
+// Dealer draw at counter position z = key + c*phi of a triple stream. With a materialised triple
+// (queue / pool source, TripleSource plugin: H/sharing/triple.hpp:126-179) the stream's draws
+// live in device memory, draw c at pool[c - 1] (c = (z - key) * phi^-1 mod 2^64), laid out as
+// the seeded dealer's counters: [A | B | r_A | r_B | r_C] for 2 parties.
+constexpr u64 kPhiInv = 0xF1DE83E19937733Dull;  // phi * kPhiInv == 1 (mod 2^64)
+__device__ __forceinline__ u64 dmix(u64 z, u64 key, const u64* pool) {
+  return pool ? __ldg(pool + ((z - key) * kPhiInv - 1)) : mix64(z);
+}
+
 // ------------------------------------------------------------------ dealer
 // Triple stream keys are either immediates (eager launches) or read from a device key
 // table that a rekey kernel refreshes at the head of every CUDA-graph replay, so a
@@ -88,6 +97,7 @@ __host__ __device__ __forceinline__ u64 drw(u64 key, u64 c) { return mix64(key +
 struct EwTriple {
   u64 key;        // seed ^ (stream * phi)
   const u64* kp;  // device key slot (graph replay), or null
+  const u64* pool = nullptr;  // materialised draws (queue source), or null = seeded dealer
   u64 mg;         // global numel of A (== of B, C)
   u64 ghalf;      // global elements per stacked half (== mg when unstacked)
   u64 off;        // global offset of this shard inside each half
@@ -122,13 +132,13 @@ __device__ __forceinline__ Dw ew_draw(const EwTriple& t, u64 g, bool p0) {
   const u64 key = tkey(t.key, t.kp);
   const u64 gp = g * kPhi;
   Dw d;
-  d.ra = mix64(key + t.pra + gp);
-  d.rb = mix64(key + t.prb + gp);
-  d.rc = WithC ? mix64(key + t.prc + gp) : 0;
+  d.ra = dmix(key + t.pra + gp, key, t.pool);
+  d.rb = dmix(key + t.prb + gp, key, t.pool);
+  d.rc = WithC ? dmix(key + t.prc + gp, key, t.pool) : 0;
   d.A = d.B = 0;
   if (p0) {
-    d.A = mix64(key + t.pA + gp);
-    d.B = t.square ? d.A : mix64(key + t.pB + gp);
+    d.A = dmix(key + t.pA + gp, key, t.pool);
+    d.B = t.square ? d.A : dmix(key + t.pB + gp, key, t.pool);
   }
   return d;
 }
@@ -139,8 +149,8 @@ __device__ __forceinline__ Dw ew_secrets(const EwTriple& t, u64 g) {
   const u64 gp = g * kPhi;
   Dw d;
   d.ra = d.rb = d.rc = 0;
-  d.A = mix64(key + t.pA + gp);
-  d.B = t.square ? d.A : mix64(key + t.pB + gp);
+  d.A = dmix(key + t.pA + gp, key, t.pool);
+  d.B = t.square ? d.A : dmix(key + t.pB + gp, key, t.pool);
   return d;
 }
 // `party`'s shares of a drawn element (0 absorbs the secret).
@@ -177,13 +187,13 @@ __device__ __forceinline__ void ew_abc(const EwTriple& t, int party, u64 g, u64&
 __device__ __forceinline__ void sq_ac(const EwTriple& t, int party, u64 g, u64& a, u64& c) {
   const u64 key = tkey(t.key, t.kp);
   const u64 gp = g * kPhi;
-  const u64 ra = mix64(key + t.pra + gp), rc = mix64(key + t.prc + gp);
+  const u64 ra = dmix(key + t.pra + gp, key, t.pool), rc = dmix(key + t.prc + gp, key, t.pool);
   if (party != 0) {
     a = ra;
     c = rc;
     return;
   }
-  const u64 A = mix64(key + t.pA + gp);
+  const u64 A = dmix(key + t.pA + gp, key, t.pool);
   a = A - ra;
   c = A * A - rc;
 }
@@ -191,14 +201,15 @@ __device__ __forceinline__ void sq_ac(const EwTriple& t, int party, u64 g, u64& 
 __device__ __forceinline__ u64 sq_a(const EwTriple& t, int party, u64 g) {
   const u64 key = tkey(t.key, t.kp);
   const u64 gp = g * kPhi;
-  const u64 ra = mix64(key + t.pra + gp);
-  return party != 0 ? ra : mix64(key + t.pA + gp) - ra;
+  const u64 ra = dmix(key + t.pra + gp, key, t.pool);
+  return party != 0 ? ra : dmix(key + t.pA + gp, key, t.pool) - ra;
 }
 
 // Matmul triple (H/sharing/triple.hpp:96-114): draws A (na), B (nb), then r_A, r_B, r_C.
 struct MmTriple {
   u64 key;
   const u64* kp;
+  const u64* pool = nullptr;  // materialised draws (queue source), or null = seeded dealer
   u64 na, nb, nc;     // global numels
   u64 offA, offB, offC;
   u64 pA, pB, prA, prB, prC;  // (stream base + shard offset) * phi, see EwTriple::set_phis
@@ -210,17 +221,15 @@ struct MmTriple {
     prC = (1 + 2 * na + 2 * nb + offC) * kPhi;
   }
 };
-__device__ __forceinline__ u64 mm_A(const MmTriple& t, u64 i) { return mix64(tkey(t.key, t.kp) + t.pA + i * kPhi); }
-__device__ __forceinline__ u64 mm_B(const MmTriple& t, u64 j) { return mix64(tkey(t.key, t.kp) + t.pB + j * kPhi); }
-__device__ __forceinline__ u64 mm_rA(const MmTriple& t, u64 i) {
-  return mix64(tkey(t.key, t.kp) + t.prA + i * kPhi);
+__device__ __forceinline__ u64 mm_draw(const MmTriple& t, u64 base_phi, u64 i) {
+  const u64 key = tkey(t.key, t.kp);
+  return dmix(key + base_phi + i * kPhi, key, t.pool);
 }
-__device__ __forceinline__ u64 mm_rB(const MmTriple& t, u64 j) {
-  return mix64(tkey(t.key, t.kp) + t.prB + j * kPhi);
-}
-__device__ __forceinline__ u64 mm_rC(const MmTriple& t, u64 k) {
-  return mix64(tkey(t.key, t.kp) + t.prC + k * kPhi);
-}
+__device__ __forceinline__ u64 mm_A(const MmTriple& t, u64 i) { return mm_draw(t, t.pA, i); }
+__device__ __forceinline__ u64 mm_B(const MmTriple& t, u64 j) { return mm_draw(t, t.pB, j); }
+__device__ __forceinline__ u64 mm_rA(const MmTriple& t, u64 i) { return mm_draw(t, t.prA, i); }
+__device__ __forceinline__ u64 mm_rB(const MmTriple& t, u64 j) { return mm_draw(t, t.prB, j); }
+__device__ __forceinline__ u64 mm_rC(const MmTriple& t, u64 k) { return mm_draw(t, t.prC, k); }
 
 // ------------------------------------------------------------------ launch helpers
 // SM count of the current device, queried once per device (148 on a full B200; fewer under

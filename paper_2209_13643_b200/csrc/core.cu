@@ -334,6 +334,7 @@ Triple Session::fetch(const TripleSpec& spec, const std::string& tag, bool batch
     t.mm.offC = dp_offset(nc);
     t.mm.set_phis();
   }
+  pool_on_fetch(*this, t);
   return t;
 }
 
@@ -410,7 +411,7 @@ void Session::begin_capture() {
 }
 
 void Session::end_capture() {
-  if (p2p) p2p_replay_barrier(*this);  // replay r+1 must not overwrite inboxes the peer still reads
+  if (p2p_link) p2p_replay_barrier(*this);  // replay r+1 must not overwrite inboxes the peer still reads
   if (cap.comm_used) {  // rejoin the comm stream (opens still in flight at the end of the run)
     cudaEvent_t j = pool_event();
     MPCG_CUDA(cudaEventRecord(j, comm_stream));
@@ -658,7 +659,7 @@ void Session::post(Open& o, const std::string& tag, bool p2p) {
     check();
     return;
   }
-  if (n_local == 1 && p2p) {  // device-initiated peer stores + flag (link.cu)
+  if (n_local == 1 && p2p_link) {  // device-initiated peer stores + flag (link.cu)
     p2p_post(*this, o);
     if (tm) tm->sent = trace_event(comm_stream);
     o.ready = pool_event();  // the push has read our payload (its lifetime is the compute stream's)
@@ -741,7 +742,7 @@ void Session::wait(Open& o) {
                      !cap.active;
   if (timed) trace_marks_[size_t(o.trace_idx)].wait_begin = trace_event(stream);
   if (sock && n_local == 1 && !o.ready) socket_receive(*this, o);  // blocks until the peer's frame is here
-  if (p2p && n_local == 1) p2p_wait(*this, o);                      // device spin on the peer's flag
+  if (p2p_link && n_local == 1) p2p_wait(*this, o);                      // device spin on the peer's flag
   if (o.ready) MPCG_CUDA(cudaStreamWaitEvent(stream, o.ready, 0));
   if (timed) trace_marks_[size_t(o.trace_idx)].wait_end = o.ready ? trace_event(stream) : nullptr;
 }

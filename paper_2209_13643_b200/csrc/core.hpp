@@ -122,6 +122,23 @@ struct Triple {
   }
 };
 
+// ------------------------------------------------------------------ triple queues (pool.cu)
+// One materialised triple: the seeded dealer's draw sequence [A | B | r_A | r_B | r_C] (2PC).
+struct PoolTriple {
+  TripleSpec spec;
+  std::shared_ptr<Block> draws;
+  u64 words = 0;
+};
+// QueueTripleSource (H/sharing/triple.hpp:161-179): consumed in order, specs checked.
+struct TripleQueue {
+  std::vector<PoolTriple> items;
+  size_t next = 0;
+};
+u64 triple_draw_count(const TripleSpec& sp);
+bool spec_equal(const TripleSpec& a, const TripleSpec& b);
+void queue_save(const TripleQueue& q, const std::string& path);
+void queue_load(TripleQueue& q, const std::string& path);
+
 // ------------------------------------------------------------------ the wire
 // One collective: each local slot's build kernel writes its payload into own(slot);
 // after wait() the peer's payload for the same slot is readable at peer(slot).
@@ -197,7 +214,7 @@ class Session {
   ncclComm_t nccl = nullptr;
   std::shared_ptr<LoopLink> loop;      // in-process peer (tests of the one-party path on one GPU)
   std::shared_ptr<SocketLink> sock;    // peer process over TCP (link.cu, the SocketComm counterpart)
-  std::shared_ptr<P2PLink> p2p;        // peer session of this process: device-initiated stores + flags
+  std::shared_ptr<P2PLink> p2p_link;        // peer session of this process: device-initiated stores + flags
   struct SockPending {                 // received frames staged host->device, buffer not yet reusable
     cudaEvent_t ev;
     u64* p;
@@ -221,6 +238,9 @@ class Session {
   u64 tag_stream(const std::string& tag);
   std::unordered_map<u64, u64> tag_counts;
   u64 untagged_index = 0;
+  // TripleSource plugin (H/sharing/triple.hpp:126-179): record every fetched triple into a
+  // queue (offline dealer) and/or consume triples from a queue instead of the seeded dealer.
+  std::shared_ptr<TripleQueue> record_q, source_q;
 
   // ---- party mask rng (CounterRng(mask_seed, party)): sequential counters per slot
   u64 mask_key[2] = {0, 0};
@@ -335,6 +355,8 @@ class Session {
   u64* link_state_ = nullptr;  // device: [next free ns]
 };
 
+void pool_on_fetch(Session& s, Triple& t);
+void dealer_fetch(Session& s, const TripleSpec& spec, const std::string& tag, DT& a, DT& b, DT& c);
 void socket_connect(Session& s, const char* host, int port, double timeout_s);
 void socket_post(Session& s, Open& o, size_t words);
 void socket_receive(Session& s, Open& o);

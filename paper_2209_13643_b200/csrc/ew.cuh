@@ -238,15 +238,16 @@ __device__ __forceinline__ Sw sq_draw(const EwTriple& t, u64 g, bool p0, bool wi
   const u64 key = tkey(t.key, t.kp);
   const u64 gp = g * kPhi;
   Sw d;
-  d.ra = mix64(key + t.pra + gp);
-  d.rc = with_c ? mix64(key + t.prc + gp) : 0;
-  d.A = p0 ? mix64(key + t.pA + gp) : 0;
+  d.ra = dmix(key + t.pra + gp, key, t.pool);
+  d.rc = with_c ? dmix(key + t.prc + gp, key, t.pool) : 0;
+  d.A = p0 ? dmix(key + t.pA + gp, key, t.pool) : 0;
   return d;
 }
 __device__ __forceinline__ u64 sq_share_a(int party, const Sw& d) { return party ? d.ra : d.A - d.ra; }
 // the square triple's secret A alone (a0 + a1 = A: all an opened-wire build needs)
 __device__ __forceinline__ u64 sq_secret(const EwTriple& t, u64 g) {
-  return mix64(tkey(t.key, t.kp) + t.pA + g * kPhi);
+  const u64 key = tkey(t.key, t.kp);
+  return dmix(key + t.pA + g * kPhi, key, t.pool);
 }
 __device__ __forceinline__ u64 sq_share_c(int party, const Sw& d) { return party ? d.rc : d.A * d.A - d.rc; }
 
@@ -266,7 +267,7 @@ struct SqBuild {
   __device__ void both(u64 j) const {
     const u64 g = lo + j;
     if (opened) {  // eps0 + eps1 = x0 + x1 - A
-      own.p[0][j] = xf(0, g) + xf(1, g) - mix64(tkey(T.key, T.kp) + T.pA + (T.off + g) * kPhi);
+      own.p[0][j] = xf(0, g) + xf(1, g) - sq_secret(T, T.off + g);
       return;
     }
     (*this)(0, j);
@@ -778,7 +779,8 @@ __device__ __forceinline__ Dw dw_load(const u64* c, u64 n, u64 g, int half, cons
   d.B = b[n];
   d.ra = b[2 * n];
   d.rb = b[3 * n];
-  d.rc = mix64(tkey(t.key, t.kp) + t.prc + gidx * kPhi);
+  const u64 key = tkey(t.key, t.kp);
+  d.rc = dmix(key + t.prc + gidx * kPhi, key, t.pool);
   return d;
 }
 

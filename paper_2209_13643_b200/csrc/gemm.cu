@@ -317,8 +317,8 @@ __global__ void __launch_bounds__(256) ring_gemm_rows(GemmArgs a) {
         const u64 e0 = S.aoff + rowbase + kk;
         u64 z = key + (kind == kOpRA ? S.mm.prA : S.mm.pA) + e0 * kPhi, z2 = key + S.mm.prA + e0 * kPhi;
         for (; kk < kc; ++kk, z += kPhi, z2 += kPhi) {
-          u64 v = mix64(z);
-          if (kind == kOpA0) v -= mix64(z2);
+          u64 v = dmix(z, key, S.mm.pool);
+          if (kind == kOpA0) v -= dmix(z2, key, S.mm.pool);
 #pragma unroll
           for (int n = 0; n < NR; ++n) acc[n] += v * Rs[g][kk][n];
         }
@@ -427,12 +427,12 @@ void delta_build_mem(Session& s, const Triple& t, const u64* const y[2], size_t 
 // the eps payload needs anyway, so the combine GEMM reads them instead of redrawing.
 __device__ __forceinline__ u64 a_share_out(const MmTriple& t, int party, u64 i, u64* aop, u64 j, u64 na) {
   const u64 key = tkey(t.key, t.kp), ip = i * kPhi;
-  const u64 ra = mix64(key + t.prA + ip);
+  const u64 ra = dmix(key + t.prA + ip, key, t.pool);
   if (party) {
     if (aop) aop[j] = ra;
     return ra;
   }
-  const u64 A = mix64(key + t.pA + ip), a0 = A - ra;
+  const u64 A = dmix(key + t.pA + ip, key, t.pool), a0 = A - ra;
   if (aop) {
     aop[j] = A;
     aop[na + j] = a0;
@@ -451,7 +451,7 @@ void eps_build_mem(Session& s, const Triple& t, const u64* const x[2], size_t a_
     if (s.n_local != 2 || aops) throw Error(kUsageError, "summed eps open needs both slots and no A operands");
     launch_ew(s.stream, 1, na, [=] __device__(int, u64 j) {  // eps0 + eps1 = x0 + x1 - A
       const u64 key = tkey(mm.key, mm.kp);
-      own.p[0][j] = xp.p[0][a_off + j] + xp.p[1][a_off + j] - mix64(key + mm.pA + (a_off + j) * kPhi);
+      own.p[0][j] = xp.p[0][a_off + j] + xp.p[1][a_off + j] - dmix(key + mm.pA + (a_off + j) * kPhi, key, mm.pool);
     });
     return;
   }
@@ -501,10 +501,10 @@ struct EpsIm2colPair {
     const u64 ip = (a_off + j) * kPhi;
     if (summed) {  // eps0 + eps1 = (x0 + x1) - (a0 + a1), a0 + a1 = A: the r_A masks cancel
       const u64 v = in ? xp.p[0][src] + xp.p[1][src] : 0;
-      own.p[0][j] = v - mix64(key + mm.pA + ip);
+      own.p[0][j] = v - dmix(key + mm.pA + ip, key, mm.pool);
       return;
     }
-    const u64 ra = mix64(key + mm.prA + ip);
+    const u64 ra = dmix(key + mm.prA + ip, key, mm.pool);
     u64 A = 0;
     bool haveA = false;
 #pragma unroll
@@ -514,7 +514,7 @@ struct EpsIm2colPair {
       u64 a;
       if (pid.v[sl] == 0) {
         if (!haveA) {
-          A = mix64(key + mm.pA + ip);
+          A = dmix(key + mm.pA + ip, key, mm.pool);
           haveA = true;
         }
         a = A - ra;
@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(256) eps_im2col_summed_kernel(MmTriple mm, Con
         const long long src = xb + e.x;
         v = x0[src] + x1[src];
       }
-      out[j0 + c] = v - mix64(z);  // eps0 + eps1 = x0 + x1 - (a0 + a1), a0 + a1 = A
+      out[j0 + c] = v - dmix(z, key - mm.pA, mm.pool);  // eps0 + eps1 = x0 + x1 - (a0 + a1), a0 + a1 = A
     }
   }
 }
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(256) eps_im2col_tile_kernel(MmTriple mm, ConvG
     for (u32 cl = lane; cl < ncol; cl += 32, z += 32 * kPhi) {
       const u32 ci = fkk.div(cl), t2 = cl - ci * kk, ki = fk.div(t2), kj = t2 - ki * g.k;
       const u64 v = sx[(ci * g.k + ki) * ww + warp * g.stride + kj];
-      out[ob + cl] = v - mix64(z);  // eps0 + eps1 = x0 + x1 - (a0 + a1), a0 + a1 = A
+      out[ob + cl] = v - dmix(z, key - mm.pA, mm.pool);  // eps0 + eps1 = x0 + x1 - (a0 + a1), a0 + a1 = A
     }
   }
 }

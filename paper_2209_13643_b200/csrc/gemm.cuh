@@ -96,7 +96,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& a, const GemmSlotA
                                               u64 v) {
   const u64 lin = (u64(b) * a.M + m) * a.N + n;
   if (S.cterm) {
-    const u64 rc = drw(tkey(S.ckey, S.ckp), S.cbase + lin);
+    const u64 rc = S.mm.pool ? __ldg(S.mm.pool + S.cbase + lin - 1) : drw(tkey(S.ckey, S.ckp), S.cbase + lin);
     v = S.cterm > 0 ? v + rc : v - rc;
   }
   if (a.trunc_bits) v = sar64(v, a.trunc_bits);

@@ -109,7 +109,12 @@ __device__ __forceinline__ u32 gather4(u32 a, u32 b, u32 c, u32 d, u32 l) {
 }
 
 
-__device__ __forceinline__ void draws16(u64 key, u64 c0, u64 (&v)[16]) {
+__device__ __forceinline__ void draws16(u64 key, u64 c0, u64 (&v)[16], const u64* pool) {
+  if (pool) {  // materialised triple (queue source): draw c at pool[c - 1]
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __ldg(pool + c0 - 1 + i);
+    return;
+  }
   u64 z = key + c0 * kPhi;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
@@ -168,7 +173,12 @@ __device__ __forceinline__ void transpose16_tmem(const u64 (&v)[16], u32 taddr) 
 }
 
 // kVW dealer draws c0, c0+1, ... of one stream (key + c*phi advances by phi).
-__device__ __forceinline__ void draws_vec(u64 key, u64 c0, u64 (&v)[kVW]) {
+__device__ __forceinline__ void draws_vec(u64 key, u64 c0, u64 (&v)[kVW], const u64* pool) {
+  if (pool) {
+#pragma unroll
+    for (int i = 0; i < kVW; ++i) v[i] = __ldg(pool + c0 - 1 + i);
+    return;
+  }
   u64 z = key + c0 * kPhi;
 #pragma unroll
   for (int i = 0; i < kVW; ++i) {
@@ -428,10 +438,10 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = 0;
           } else {
-            draws16(key, (kind == kOpRA ? iRA : iA) + e0, v);
+            draws16(key, (kind == kOpRA ? iRA : iA) + e0, v, S.mm.pool);
             if (kind == kOpA0) {
               u64 w[16];
-              draws16(key, iRA + e0, w);
+              draws16(key, iRA + e0, w, S.mm.pool);
 #pragma unroll
               for (int i = 0; i < 16; ++i) v[i] -= w[i];
             }
@@ -532,10 +542,10 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
             }
           } else {  // dealer draws: A, r_A (party 0 splits a0*F as A*F - r_A*F), or a0 = A - r_A
             const u64 e0 = rowoff + k0;
-            draws_vec(key, (kind == kOpRA ? iRA : iA) + e0, v);
+            draws_vec(key, (kind == kOpRA ? iRA : iA) + e0, v, S.mm.pool);
             if (kind == kOpA0) {
               u64 w[kVW];
-              draws_vec(key, iRA + e0, w);
+              draws_vec(key, iRA + e0, w, S.mm.pool);
 #pragma unroll
               for (int i = 0; i < kVW; ++i) v[i] -= w[i];
             }

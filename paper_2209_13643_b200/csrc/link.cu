@@ -174,7 +174,7 @@ struct SocketLink {
 
 void socket_connect(Session& s, const char* host, int port, double timeout_s) {
   if (s.n_local != 1) throw Error(kUsageError, "socket link needs a single-party session");
-  if (s.sock || s.nccl || s.loop || s.p2p) throw Error(kUsageError, "session already has a peer link");
+  if (s.sock || s.nccl || s.loop || s.p2p_link) throw Error(kUsageError, "session already has a peer link");
   auto L = std::make_shared<SocketLink>();
   L->device = s.device;
   const auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(timeout_s);
@@ -361,7 +361,7 @@ void p2p_connect(Session& a, Session& b) {
   if (a.n_local != 1 || b.n_local != 1 || a.party_of[0] == b.party_of[0])
     throw Error(kUsageError, "p2p link joins party 0's and party 1's single-party sessions");
   for (Session* s : {&a, &b})
-    if (s->sock || s->nccl || s->loop || s->p2p) throw Error(kUsageError, "session already has a peer link");
+    if (s->sock || s->nccl || s->loop || s->p2p_link) throw Error(kUsageError, "session already has a peer link");
   if (a.seed != b.seed) throw Error(kProtocolError, "p2p link: the parties' session seeds differ");
   auto L = std::make_shared<P2PLink>();
   for (Session* s : {&a, &b}) {
@@ -384,12 +384,12 @@ void p2p_connect(Session& a, Session& b) {
   }
   MPCG_CUDA(cudaDeviceSynchronize());
   MPCG_CUDA(cudaSetDevice(a.device));
-  a.p2p = L;
-  b.p2p = L;
+  a.p2p_link = L;
+  b.p2p_link = L;
 }
 
 void p2p_post(Session& s, Open& o) {
-  P2PLink& L = *s.p2p;
+  P2PLink& L = *s.p2p_link;
   const int me = s.party_of[0];
   u64* peer_inbox = nullptr;
   {
@@ -430,7 +430,7 @@ void p2p_post(Session& s, Open& o) {
 }
 
 void p2p_wait(Session& s, const Open& o) {
-  P2PLink& L = *s.p2p;
+  P2PLink& L = *s.p2p_link;
   const int me = s.party_of[0];
   const u64* it = s.cap.active ? s.cap.iter : nullptr;
   const u64* dl = s.cap.active ? s.cap.seqd : nullptr;
@@ -442,7 +442,7 @@ void p2p_wait(Session& s, const Open& o) {
 // End of a captured inference: each party tells the other it is done with this replay and waits
 // for the peer's word, so replay r+1 never pushes into an inbox the peer still reads in replay r.
 void p2p_replay_barrier(Session& s) {
-  P2PLink& L = *s.p2p;
+  P2PLink& L = *s.p2p_link;
   const int me = s.party_of[0];
   // value = replay index + 1 on both sides: base 0, delta 1 -> (*iter - 1) * 1 + 1 = *iter
   static u64* one = nullptr;

@@ -100,6 +100,8 @@ def main():
         d = read_dump(tmp)
         np.savez_compressed(os.path.join(HERE, f"model_{name}_{mode}_{weights}_it{iters}.npz"), **d)
     os.remove(tmp)
+    # triple-file pin: two dealer triples written by the reference's save_triples
+    subprocess.check_call([DRIVER, "triples", os.path.join(HERE, "triples_ref.bin")])
     # MPCW interchange pin: the reference's init_weights(toy_cnn, 12) written by its save_weights
     subprocess.check_call([DRIVER, "mpcw", os.path.join(ROOT, "configs", "toy_cnn.json"), "12",
                            os.path.join(HERE, "toy_cnn_seed12.mpcw")])
