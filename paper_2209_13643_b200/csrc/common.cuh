@@ -80,8 +80,12 @@ __host__ __device__ __forceinline__ u64 drw(u64 key, u64 c) { return mix64(key +
 // live in device memory, draw c at pool[c - 1] (c = (z - key) * phi^-1 mod 2^64), laid out as
 // the seeded dealer's counters: [A | B | r_A | r_B | r_C] for 2 parties.
 constexpr u64 kPhiInv = 0xF1DE83E19937733Dull;  // phi * kPhiInv == 1 (mod 2^64)
+__device__ __forceinline__ u64 pool_at(const u64* pool, u64 z, u64 key) {
+  return __ldg(pool + ((z - key) * kPhiInv - 1));
+}
 __device__ __forceinline__ u64 dmix(u64 z, u64 key, const u64* pool) {
-  return pool ? __ldg(pool + ((z - key) * kPhiInv - 1)) : mix64(z);
+  if (pool) return pool_at(pool, z, key);
+  return mix64(z);
 }
 
 // ------------------------------------------------------------------ dealer
@@ -127,31 +131,46 @@ __device__ __forceinline__ u64 tkey(u64 key, const u64* kp) { return kp ? __ldg(
 struct Dw {
   u64 A, B, ra, rb, rc;
 };
-template <bool WithC>
-__device__ __forceinline__ Dw ew_draw(const EwTriple& t, u64 g, bool p0) {
+// Pool = true: the triple is materialised (queue source) and its draws are read from HBM;
+// false: the seeded dealer's straight-line splitmix64 code. Hot kernels (the SPK adder rounds)
+// are instantiated per mode; others take the runtime-checked ew_draw / ew_secrets.
+template <bool WithC, bool Pool>
+__device__ __forceinline__ Dw ew_draw_t(const EwTriple& t, u64 g, bool p0) {
   const u64 key = tkey(t.key, t.kp);
   const u64 gp = g * kPhi;
   Dw d;
-  d.ra = dmix(key + t.pra + gp, key, t.pool);
-  d.rb = dmix(key + t.prb + gp, key, t.pool);
-  d.rc = WithC ? dmix(key + t.prc + gp, key, t.pool) : 0;
+  auto dr = [&](u64 z) { return Pool ? pool_at(t.pool, z, key) : mix64(z); };
+  d.ra = dr(key + t.pra + gp);
+  d.rb = dr(key + t.prb + gp);
+  d.rc = WithC ? dr(key + t.prc + gp) : 0;
   d.A = d.B = 0;
   if (p0) {
-    d.A = dmix(key + t.pA + gp, key, t.pool);
-    d.B = t.square ? d.A : dmix(key + t.pB + gp, key, t.pool);
+    d.A = dr(key + t.pA + gp);
+    d.B = t.square ? d.A : dr(key + t.pB + gp);
   }
   return d;
 }
+template <bool WithC>
+__device__ __forceinline__ Dw ew_draw(const EwTriple& t, u64 g, bool p0) {
+  if (t.pool) return ew_draw_t<WithC, true>(t, g, p0);
+  return ew_draw_t<WithC, false>(t, g, p0);
+}
 // Only the dealer's secrets A, B of element g: what the two parties' shares reconstruct to
 // (a0 ^ a1 or a0 + a1), all an opened-wire issue needs — the masks cancel in the open.
-__device__ __forceinline__ Dw ew_secrets(const EwTriple& t, u64 g) {
+template <bool Pool>
+__device__ __forceinline__ Dw ew_secrets_t(const EwTriple& t, u64 g) {
   const u64 key = tkey(t.key, t.kp);
   const u64 gp = g * kPhi;
+  auto dr = [&](u64 z) { return Pool ? pool_at(t.pool, z, key) : mix64(z); };
   Dw d;
   d.ra = d.rb = d.rc = 0;
-  d.A = dmix(key + t.pA + gp, key, t.pool);
-  d.B = t.square ? d.A : dmix(key + t.pB + gp, key, t.pool);
+  d.A = dr(key + t.pA + gp);
+  d.B = t.square ? d.A : dr(key + t.pB + gp);
   return d;
+}
+__device__ __forceinline__ Dw ew_secrets(const EwTriple& t, u64 g) {
+  if (t.pool) return ew_secrets_t<true>(t, g);
+  return ew_secrets_t<false>(t, g);
 }
 // `party`'s shares of a drawn element (0 absorbs the secret).
 template <bool WithC>

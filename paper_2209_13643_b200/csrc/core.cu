@@ -617,7 +617,8 @@ u32 Session::account(size_t nwords, Reduce kind, const std::string& tag, bool p2
 }
 
 bool Session::persistent_ok(size_t n) const {
-  if (n_local != 2 || cfg.link_bandwidth > 0 || persistent_mode == 0) return false;
+  // (queue-sourced triples run the per-round kernels: the persistent chains draw in place)
+  if (n_local != 2 || cfg.link_bandwidth > 0 || persistent_mode == 0 || source_q) return false;
   static const size_t max_elems = [] {  // MPCG_PERSIST_MAX overrides the measured default
     const char* e = std::getenv("MPCG_PERSIST_MAX");
     return e ? size_t(std::strtoull(e, nullptr, 10)) : kPersistentMaxElems;

@@ -784,7 +784,7 @@ __device__ __forceinline__ Dw dw_load(const u64* c, u64 n, u64 g, int half, cons
   return d;
 }
 
-template <class XF, class YF, class FF>
+template <class XF, class YF, class FF, bool Pool = false>
 struct AdderRound {
   int rp, rn, levels;
   EwTriple Tp, Tn;
@@ -817,7 +817,7 @@ struct AdderRound {
     if (rn == 0) {  // issue the generate AND: payload [x^a | y^b]
       // opened wire: payload0 ^ payload1 = (x0 ^ x1) ^ (a0 ^ a1) with a0 ^ a1 = A (the masks
       // r_A cancel), so only the dealer's A, B are drawn
-      const Dw dn = op && !cwn ? ew_secrets(Tn, Tn.off + g) : ew_draw<false>(Tn, Tn.off + g, p0);
+      const Dw dn = op && !cwn ? ew_secrets_t<Pool>(Tn, Tn.off + g) : ew_draw_t<false, Pool>(Tn, Tn.off + g, p0);
       if (cwn) dw_store(cwn, cwN, g, 0, dn);
       u64 o0 = 0, o1 = 0;
 #pragma unroll
@@ -843,7 +843,7 @@ struct AdderRound {
     }
     u64 s[NS], p[NS];
     if (rp == 0) {  // settle the generate AND (H/protocols/adder.hpp:209-223)
-      const Dw dp = cwp ? dw_load(cwp, cwN, g, 0, Tp, Tp.off + g) : ew_draw<true>(Tp, Tp.off + g, p0);
+      const Dw dp = cwp ? dw_load(cwp, cwN, g, 0, Tp, Tp.off + g) : ew_draw_t<true, Pool>(Tp, Tp.off + g, p0);
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
         const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
@@ -859,9 +859,9 @@ struct AdderRound {
     } else {  // settle a prefix level (H/protocols/adder.hpp:142-165)
       // Own payload is recomputed from the pre-round state instead of re-read from HBM:
       // it is a function of (s, p) and the triple, all of which this thread holds.
-      const Dw d0 = cwp ? dw_load(cwp, cwN, g, 0, Tp, Tp.off + g) : ew_draw<true>(Tp, Tp.off + g, p0);
+      const Dw d0 = cwp ? dw_load(cwp, cwN, g, 0, Tp, Tp.off + g) : ew_draw_t<true, Pool>(Tp, Tp.off + g, p0);
       const Dw d1 = cwp ? dw_load(cwp, cwN, g, 1, Tp, Tp.ghalf + Tp.off + g)
-                        : ew_draw<true>(Tp, Tp.ghalf + Tp.off + g, p0);
+                        : ew_draw_t<true, Pool>(Tp, Tp.ghalf + Tp.off + g, p0);
       u64 oe0 = 0, oe1 = 0, od0 = 0, od1 = 0;  // the opened wire (pair evaluation)
       if (op) {
         const u64* o = ownp.p[0];
@@ -892,8 +892,9 @@ struct AdderRound {
     if (rn <= levels) {  // issue level rn-1 (H/protocols/adder.hpp:122-140)
       // opened wire: the masks r_A, r_B cancel between the two payloads (see rn == 0)
       const bool sec = op && !cwn;
-      const Dw d0 = sec ? ew_secrets(Tn, Tn.off + g) : ew_draw<false>(Tn, Tn.off + g, p0);
-      const Dw d1 = sec ? ew_secrets(Tn, Tn.ghalf + Tn.off + g) : ew_draw<false>(Tn, Tn.ghalf + Tn.off + g, p0);
+      const Dw d0 = sec ? ew_secrets_t<Pool>(Tn, Tn.off + g) : ew_draw_t<false, Pool>(Tn, Tn.off + g, p0);
+      const Dw d1 = sec ? ew_secrets_t<Pool>(Tn, Tn.ghalf + Tn.off + g)
+                        : ew_draw_t<false, Pool>(Tn, Tn.ghalf + Tn.off + g, p0);
       if (cwn) {
         dw_store(cwn, cwN, g, 0, d0);
         dw_store(cwn, cwN, g, 1, d1);
@@ -966,9 +967,9 @@ inline bool adder_draw_cache_ok(const Session& s, size_t n) {
 // lane hands the sum to ff_for_lane(lane, lo, w) — a functor (slot, party, g, j, sum) that
 // may already build the next protocol's payload for the same lane — and post_lane(lane)
 // runs right after it (to post that payload), so a protocol tail costs no extra kernel.
-template <class XF, class YF, class FFL, class POST = NoPost>
-void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& tag, XF xf, YF yf,
-              FFL ff_for_lane, POST post_lane = NoPost{}) {
+template <bool Pool, class XF, class YF, class FFL, class POST>
+void adder_op_t(Session& s, size_t n, const AdderOptions& opt, const std::string& tag, XF xf, YF yf,
+                FFL ff_for_lane, POST post_lane) {
   using FF = decltype(ff_for_lane(0, size_t(0), size_t(0)));
   const SpkConsts c = make_spk_constants(opt.width);
   const int chunks = clamp_chunks(opt.chunks, n);
@@ -993,7 +994,7 @@ void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& 
   auto kernel = [&](int rp, int rn, int lane, Open* prev, Open* next) {
     const auto rng_ = chunk_range(n, chunks, lane);
     const size_t lo = rng_.first, hi = rng_.second;
-    AdderRound<XF, YF, FF> k{};
+    AdderRound<XF, YF, FF, Pool> k{};
     k.rp = rp;
     k.rn = rn;
     k.levels = c.levels;
@@ -1052,6 +1053,17 @@ void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& 
     post_lane(lane);
   }
   s.check();
+}
+
+// The SPK adder rounds are the hottest kernels: they are instantiated per triple source so the
+// seeded-dealer build keeps its straight-line code (queue mode: triples read from HBM).
+template <class XF, class YF, class FFL, class POST = NoPost>
+void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& tag, XF xf, YF yf,
+              FFL ff_for_lane, POST post_lane = NoPost{}) {
+  if (s.source_q)
+    adder_op_t<true>(s, n, opt, tag, xf, yf, ff_for_lane, post_lane);
+  else
+    adder_op_t<false>(s, n, opt, tag, xf, yf, ff_for_lane, post_lane);
 }
 
 // ---------------------------------------------------------------- persistent round chain

@@ -316,9 +316,10 @@ __global__ void __launch_bounds__(256) ring_gemm_rows(GemmArgs a) {
         const u64 key = tkey(S.mm.key, S.mm.kp);
         const u64 e0 = S.aoff + rowbase + kk;
         u64 z = key + (kind == kOpRA ? S.mm.prA : S.mm.pA) + e0 * kPhi, z2 = key + S.mm.prA + e0 * kPhi;
+        const u64* pool = S.mm.pool;
         for (; kk < kc; ++kk, z += kPhi, z2 += kPhi) {
-          u64 v = dmix(z, key, S.mm.pool);
-          if (kind == kOpA0) v -= dmix(z2, key, S.mm.pool);
+          u64 v = pool ? pool_at(pool, z, key) : mix64(z);
+          if (kind == kOpA0) v -= pool ? pool_at(pool, z2, key) : mix64(z2);
 #pragma unroll
           for (int n = 0; n < NR; ++n) acc[n] += v * Rs[g][kk][n];
         }
