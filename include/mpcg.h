@@ -227,7 +227,8 @@ int mpcg_executor_layer_times(mpcg_executor* e, int max, float* ms, int* count);
 int mpcg_executor_destroy(mpcg_executor* e);
 
 /* Ring-GEMM engine: 0 = SIMT only, 1 = tcgen05 int8-limb path for every shape within its
- * exact-accumulation budget (K' <= 16384), 2 = auto (tcgen05 for large shapes; default). */
+ * exact-accumulation budget (K' <= 16384), 2 = auto (tcgen05 for large shapes; default),
+ * 3 = as 1 but one CTA per party slot only (the both-slots combine kernel off). */
 int mpcg_set_gemm_mode(int mode);
 /* 1-GPU mode: pair evaluation (1, default: one thread evaluates both local party slots of an
  * element and writes each open's opened value once; summed eps/delta opens) or per-slot

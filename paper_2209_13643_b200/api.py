@@ -309,8 +309,9 @@ def set_gemv(on: bool = True):
 
 
 def set_gemm_mode(mode: str = "auto"):
-    """Ring-GEMM engine: "simt", "tc" (tcgen05 int8 limbs wherever exact) or "auto"."""
-    N.call("mpcg_set_gemm_mode", {"simt": 0, "tc": 1, "auto": 2}[mode])
+    """Ring-GEMM engine: "simt", "tc" (tcgen05 int8 limbs wherever exact), "tc2" (as "tc" with
+    one CTA per party slot only: the both-slots combine kernel off) or "auto"."""
+    N.call("mpcg_set_gemm_mode", {"simt": 0, "tc": 1, "auto": 2, "tc2": 3}[mode])
 
 
 def launch_count() -> int:

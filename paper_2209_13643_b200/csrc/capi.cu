@@ -655,8 +655,9 @@ int mpcg_set_gemv(int on) {
 
 int mpcg_set_gemm_mode(int mode) {
   return guard([&] {
-    if (mode < 0 || mode > 2) throw Error(kConfigError, "gemm mode must be 0, 1 or 2");
-    tc_gemm_mode() = mode;
+    if (mode < 0 || mode > 3) throw Error(kConfigError, "gemm mode must be 0, 1, 2 or 3");
+    tc_gemm_mode() = mode == 3 ? 1 : mode;
+    tc3_mode() = mode == 3 ? 0 : tc3_default();
   });
 }
 

@@ -376,6 +376,7 @@ void ring_gemm_launch(Session& s, const GemmArgs& a) {
     s.check();
     return;
   }
+  if (ring_gemm_tc2_wants(a) && ring_gemm_tc3_try(s, a)) return;  // both slots per CTA (tcgen05)
   if (ring_gemm_tc2_try(s, a)) return;  // warp-specialised tcgen05 int8-limb path
   if (a.M <= 16) {
     if (a.N <= 16)

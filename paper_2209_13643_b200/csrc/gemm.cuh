@@ -128,6 +128,10 @@ int& tc_gemm_mode();  // 0 = never tensor cores, 1 = whenever exact, 2 = auto by
 // once and bulk-copied; takes every operand kind.
 bool ring_gemm_tc2_wants(const GemmArgs& a);
 bool ring_gemm_tc2_try(Session& s, const GemmArgs& a);
+// Both party slots of a pair-evaluated Beaver combine in one CTA (gemm_tc3.cu); false = not taken.
+bool ring_gemm_tc3_try(Session& s, const GemmArgs& a);
+int& tc3_mode();    // 1 = both-slots kernel where it applies (default), 0 = tc2 only
+int tc3_default();  // MPCG_TC3 (0 = off)
 void tc2_trace_read(unsigned long long* out, int n);  // debug: stage timestamps (MPCG_TC2_TRACE=1)
 void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na, const Open& d, size_t nb,
                     DT* rcache, u64* const out[2], size_t out_off, u32 nbatch, u32 M, u32 N, u32 K, bool tb,

@@ -11,12 +11,14 @@ pytestmark = pytest.mark.gpu
 PHI = 0x9E3779B97F4A7C15
 
 
-@pytest.fixture
-def tc():
-    """Tensor cores forced on for every shape within the exactness budget."""
+@pytest.fixture(params=["tc", "tc2"])
+def tc(request):
+    """Tensor cores forced on for every shape within the exactness budget: "tc" takes the
+    both-slots combine kernel (gemm_tc3.cu) wherever its operand pattern applies, "tc2" the
+    one-CTA-per-slot kernel only."""
     import paper_2209_13643_b200 as mp
     from paper_2209_13643_b200 import api
-    api.set_gemm_mode("tc")
+    api.set_gemm_mode(request.param)
     yield mp
     api.set_gemm_mode("auto")
 
@@ -91,3 +93,25 @@ def test_tc_public_gemm_model_path(tc):
         z = ex.run(s.deal_input(tc.demo_input(g, 13), 2)).numpy()
         assert np.array_equal(z[0].reshape(-1), m["z0"].reshape(-1))
         assert np.array_equal(z[1].reshape(-1), m["z1"].reshape(-1))
+
+
+@pytest.mark.parametrize("M,K,N", [(16384, 576, 64), (4096, 1152, 128), (2048, 2304, 256), (9000, 27, 64)])
+def test_tc3_matches_tc2_at_conv_shapes(M, K, N):
+    """Both-slots kernel vs one-CTA-per-slot kernel at ResNet-18 conv shapes (row counts cut):
+    word-identical per-party shares (each is pinned to the reference separately)."""
+    import paper_2209_13643_b200 as mp
+    from paper_2209_13643_b200 import api
+    rng = np.random.default_rng(M + K + N)
+    X = rng.integers(0, 2**64, size=(2, M, K), dtype=np.uint64)
+    Y = rng.integers(0, 2**64, size=(2, K, N), dtype=np.uint64)
+    out = {}
+    try:
+        for mode in ("auto", "tc2"):
+            api.set_gemm_mode(mode)
+            s = mp.Session(device=0, n_local=2, seed=5, mask_seed=5 ^ PHI, frac_bits=16)
+            out[mode] = mp.beaver_matmul(s, s.tensor(X), s.tensor(Y), False, "conv").numpy()
+    finally:
+        api.set_gemm_mode("auto")
+    assert np.array_equal(out["auto"], out["tc2"])
+    z = out["auto"][0][:64] + out["auto"][1][:64]
+    assert np.array_equal(z, (X[0][:64] + X[1][:64]) @ (Y[0] + Y[1]))  # opened product, mod 2^64
