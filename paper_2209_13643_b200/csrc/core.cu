@@ -626,6 +626,14 @@ bool Session::persistent_ok(size_t n) const {
   return persistent_mode == 1 || n <= max_elems;
 }
 
+bool Session::fuse_lanes() const {
+  static const bool on = [] {
+    const char* e = std::getenv("MPCG_FUSE_LANES");
+    return !(e && e[0] == '0');
+  }();
+  return on && n_local == 2 && !(cfg.link_bandwidth > 0) && !trace_on;
+}
+
 void Session::post(Open& o, const std::string& tag, bool p2p) {
   if (o.posted) throw Error(kUsageError, "open posted twice");
   o.posted = true;

@@ -309,6 +309,26 @@ class Session {
   // kernel per round at full occupancy. 0 = never, 1 = always (MPCG_PERSISTENT / set_persistent).
   bool persistent_ok(size_t n) const;
   int persistent_mode = 2;
+  // In-device opens without an emulated link and without tracing (two local slots): a chunked
+  // op runs the lanes of each round as ONE launch over the whole tensor, and accounts the
+  // collectives per lane in the reference's order (round-major, lanes in order), so tags,
+  // counts and bytes are those of the lane-by-lane schedule. There is no transfer for the
+  // lanes to overlap; splitting the launches only adds ramp and tail per round.
+  // MPCG_FUSE_LANES=0 keeps one launch per lane.
+  bool fuse_lanes() const;
+  // Post `o` (the whole tensor's payload, already built) as `ch` lane collectives: lane k
+  // carries words_per_elem x |chunk_range(n, ch, k)| words under tag_of(k).
+  template <class TagOf>
+  void post_lanes(Open& o, size_t n, int ch, size_t words_per_elem, TagOf tag_of) {
+    if (o.posted) throw Error(kUsageError, "open posted twice");
+    o.posted = true;
+    for (int k = 0; k < ch; ++k) {
+      const size_t lo = n * size_t(k) / size_t(ch), hi = n * size_t(k + 1) / size_t(ch);
+      const u32 seq = account(words_per_elem * (hi - lo), o.kind, tag_of(k));
+      if (k == 0) o.seq = seq;
+    }
+    check();
+  }
   // measured with whole-inference graph replay: 16384 beats 32768 / 65536 on LeNet-5 (0.604 vs
   // 0.626 ms) and is level on BERT-base (46.5 vs 46.6 ms)
   static constexpr size_t kPersistentMaxElems = 16384;

@@ -972,7 +972,8 @@ void adder_op_t(Session& s, size_t n, const AdderOptions& opt, const std::string
                 FFL ff_for_lane, POST post_lane) {
   using FF = decltype(ff_for_lane(0, size_t(0), size_t(0)));
   const SpkConsts c = make_spk_constants(opt.width);
-  const int chunks = clamp_chunks(opt.chunks, n);
+  const int chunks = clamp_chunks(opt.chunks, n);  // lanes as the reference accounts them
+  const int xl = chunks > 1 && s.fuse_lanes() ? 1 : chunks;  // lanes launched (Session::fuse_lanes)
   const Pid2 pid = pids(s);
   DT S = s.alloc(Shape{n}), P = s.alloc(Shape{n}), P0 = s.alloc(Shape{n});
   const int rounds = 1 + c.levels;
@@ -990,9 +991,13 @@ void adder_op_t(Session& s, size_t n, const AdderOptions& opt, const std::string
     std::string t = r == 0 ? tag + ".g" : tag + ".l" + std::to_string(r - 1);
     return chunks > 1 && !opt.merged ? t + ".chunk" + std::to_string(lane) : t;
   };
-  std::vector<Open> hs(static_cast<size_t>(chunks));
+  std::vector<Open> hs(static_cast<size_t>(xl));
+  auto post_round = [&](int r, int lane) {
+    if (xl == chunks) s.post(hs[lane], round_tag(r, lane));
+    else s.post_lanes(hs[lane], n, chunks, r == 0 ? 2 : 4, [&](int k) { return round_tag(r, k); });
+  };
   auto kernel = [&](int rp, int rn, int lane, Open* prev, Open* next) {
-    const auto rng_ = chunk_range(n, chunks, lane);
+    const auto rng_ = chunk_range(n, xl, lane);
     const size_t lo = rng_.first, hi = rng_.second;
     AdderRound<XF, YF, FF, Pool> k{};
     k.rp = rp;
@@ -1030,24 +1035,24 @@ void adder_op_t(Session& s, size_t n, const AdderOptions& opt, const std::string
     launch_ew(s.stream, s.n_local, hi - lo, k);
   };
   fetch_round(0);
-  for (int lane = 0; lane < chunks; ++lane) {
-    const auto rng_ = chunk_range(n, chunks, lane);
+  for (int lane = 0; lane < xl; ++lane) {
+    const auto rng_ = chunk_range(n, xl, lane);
     hs[lane] = s.begin_open(2 * (rng_.second - rng_.first), Reduce::Xor);
     kernel(-1, 0, lane, nullptr, &hs[lane]);
-    s.post(hs[lane], round_tag(0, lane));
+    post_round(0, lane);
   }
   for (int r = 1; r < rounds; ++r) {
     fetch_round(r);
-    for (int lane = 0; lane < chunks; ++lane) {
-      const auto rng_ = chunk_range(n, chunks, lane);
+    for (int lane = 0; lane < xl; ++lane) {
+      const auto rng_ = chunk_range(n, xl, lane);
       Open next = s.begin_open(4 * (rng_.second - rng_.first), Reduce::Xor);
       s.wait(hs[lane]);
       kernel(r - 1, r, lane, &hs[lane], &next);
       hs[lane] = std::move(next);
-      s.post(hs[lane], round_tag(r, lane));
+      post_round(r, lane);
     }
   }
-  for (int lane = 0; lane < chunks; ++lane) {
+  for (int lane = 0; lane < xl; ++lane) {
     s.wait(hs[lane]);
     kernel(rounds - 1, rounds, lane, &hs[lane], nullptr);
     post_lane(lane);

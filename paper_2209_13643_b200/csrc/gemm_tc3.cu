@@ -344,7 +344,11 @@ bool ring_gemm_tc3_try(Session& s, const GemmArgs& a) {
   // Several N tiles regenerate the left operand per tile; beyond 4 the tc2 hybrid (dealer-drawn
   // planes packed once per layer) is cheaper. A grid below one wave leaves SMs idle where tc2
   // splits K.
-  if (ntiles > 4) return false;
+  static const u32 maxn = [] {  // N tiles regenerating the left operand (MPCG_TC3_MAXN)
+    const char* e = std::getenv("MPCG_TC3_MAXN");
+    return e ? u32(std::atoi(e)) : 8u;  // 8 measured faster than the tc2 hybrid at N = 512
+  }();
+  if (ntiles > maxn) return false;
   if (tc_gemm_mode() != 1 && u64(ntiles) * mtiles < u64(num_sms())) return false;  // forced: any grid
   static bool attr = false;
   if (!attr) {

@@ -566,14 +566,19 @@ void compare_mul(Session& s, size_t n, const AdderOptions& opt, const std::strin
     return;
   }
   const Pid2 pid = pids(s);
+  const int xl = ch > 1 && s.fuse_lanes() ? 1 : ch;  // lanes launched (Session::fuse_lanes)
   DT bits = s.alloc(Shape{n});
-  std::vector<Open> ob(static_cast<size_t>(ch)), og(static_cast<size_t>(ch));
-  for (int k = 0; k < ch; ++k) {
-    const auto r = chunk_range(n, ch, k);
+  std::vector<Open> ob(static_cast<size_t>(xl)), og(static_cast<size_t>(xl));
+  for (int k = 0; k < xl; ++k) {
+    const auto r = chunk_range(n, xl, k);
     ob[k] = s.begin_open(2 * (r.second - r.first), Reduce::Sum);
     og[k] = s.begin_open(2 * (r.second - r.first), Reduce::Sum);
   }
   auto ctag = [&](const std::string& t, int k) { return ch == 1 ? t : t + ".chunk" + std::to_string(k); };
+  auto post_lane = [&](Open& o, const std::string& t, int k) {
+    if (xl == ch) s.post(o, ctag(t, k));
+    else s.post_lanes(o, n, ch, 2, [&](int kk) { return ctag(t, kk); });
+  };
   Triple t1, t2;
   bool fetched = false;
   auto fetch_tail = [&] {  // after the adder's fetches, in reference order
@@ -592,9 +597,9 @@ void compare_mul(Session& s, size_t n, const AdderOptions& opt, const std::strin
         f.opened = opened;
         return f;
       },
-      [&](int lane) { s.post(ob[lane], ctag(tag_b2a + ".m1", lane)); });
-  for (int k = 0; k < ch; ++k) {
-    const auto r = chunk_range(n, ch, k);
+      [&](int lane) { post_lane(ob[lane], tag_b2a + ".m1", lane); });
+  for (int k = 0; k < xl; ++k) {
+    const auto r = chunk_range(n, xl, k);
     const size_t lo = r.first, w = r.second - r.first;
     s.wait(ob[k]);
     MulByBitBuild<UF> gb{t2.ew, own_ptrs(og[k]), cptrs(bits), lo, w, uf, cout};
@@ -602,10 +607,10 @@ void compare_mul(Session& s, size_t n, const AdderOptions& opt, const std::strin
     MulCombine<MulByBitBuild<UF>> bc{t1.ew, pid, as_const(own_ptrs(ob[k])), peer_ptrs(ob[k]), lo, w, gb};
     bc.opened = opened;
     launch_ew(s.stream, s.n_local, w, bc);
-    s.post(og[k], ctag(tag_mul, k));
+    post_lane(og[k], tag_mul, k);
   }
-  for (int k = 0; k < ch; ++k) {
-    const auto r = chunk_range(n, ch, k);
+  for (int k = 0; k < xl; ++k) {
+    const auto r = chunk_range(n, xl, k);
     s.wait(og[k]);
     MulCombine<PF> fc{t2.ew, pid, as_const(own_ptrs(og[k])), peer_ptrs(og[k]), r.first, r.second - r.first, pf};
     fc.opened = opened;
