@@ -485,15 +485,18 @@ def main():
     int8_peak, int8_src = measure_int8_peak()
     # algorithmic units per class: bytes for the HBM-bound protocol rounds, ring MACs
     # for the GEMM (x36 int8 MACs = 72 int8 ops each, the limb-pair products of the tcgen05 path)
-    notes = {"adder_round": "SPK level round (settle r, issue r+1), SURVEY 8(d) bytes per element per party: "
-                            "2 x 32 B wire + 8 x (2 in + 2 out) state = 96 B (the per-slot form; the pair-evaluated "
-                            "kernel moves less, so frac can exceed its own traffic share)",
+    notes = {"adder_round": "SPK level round (settle r, issue r+1). Bytes per element per party of the form that "
+                            "runs: pair-evaluated (opened wire) = (2 x 32 B state in/out per slot + 32 B opened value "
+                            "written + 32 B read) / 2 = 64 B; per-slot = SURVEY 8(d)'s 2 x 32 B wire + 8 x (2 in + 2 "
+                            "out) = 96 B",
              "beaver": "Beaver mul/square rounds incl. fused exp/Newton chains: 2 x 16 B wire + 8 x (2 in + 1 out) "
                        "= 56 B/elem/party per mul, 32 B per square (SURVEY 8(d))",
              "chain": "persistent compare-and-select chain (ReLU/tournament): 2 x 248 B wire + 16 B in/out = "
                       "512 B/elem/party (SURVEY 8(d))",
              "gemm": "ring GEMM main kernel: 72 int8 ops per ring MAC (36 limb-pair MACs); ring MACs = 3 MKN (party 0, "
-                     "dealer C online) + 2 MKN (party 1) per private linear layer; packing excluded"}
+                     "dealer C online) + 2 MKN (party 1) per private linear layer; weight packing excluded; the "
+                     "both-slots kernel (gemm_tc3.cu) also generates the opened E = x0 + x1 - A in its producers "
+                     "for convolutions (deferred eps), so its time includes that build"}
     rooflines = []
     for cls, (p_ms, p_launches, p_units) in probes.items():
         if p_launches == 0 or p_ms <= 0:

@@ -142,6 +142,21 @@ void queue_load(TripleQueue& q, const std::string& path);
 // ------------------------------------------------------------------ the wire
 // One collective: each local slot's build kernel writes its payload into own(slot);
 // after wait() the peer's payload for the same slot is readable at peer(slot).
+struct ConvGeom {
+  u32 N, C, H, W, k, stride, pad, OH, OW;
+};
+// An eps open whose opened value E = x0 + x1 - A (two local slots, pair evaluation) is not
+// materialised: the combine GEMM (gemm_tc3.cu) generates it in its producer warps from the
+// activation shares and the dealer's A. mode 1 = dense rows x[a_off + m*K + k], 2 = im2col rows
+// of a convolution (global row a_off/K + m). The open is still posted and accounted.
+struct EpsDefer {
+  int mode = 0;
+  const u64* x0 = nullptr;
+  const u64* x1 = nullptr;
+  ConvGeom g{};
+  u64 a_off = 0;
+};
+
 struct Open {
   std::shared_ptr<Block> out;    // n_local * n words: own payloads
   std::shared_ptr<Block> in;     // n words: received peer payload (n_local == 1 only)
@@ -157,6 +172,7 @@ struct Open {
   // (own0 + own1 — what both parties read after the zero-copy open) once into own(0) instead
   // of the two payloads; consumers read it as one operand (beaver_combine).
   bool summed = false;
+  EpsDefer defer{};              // summed eps built inside the combine GEMM (defer.mode != 0)
   u64* own(int slot) const { return out->ptr + size_t(slot) * n; }
   u64 tag_hash = 0;              // FNV-1a of the post tag (collective header)
   const u64* peer(int slot) const;

@@ -1029,9 +1029,10 @@ void adder_op_t(Session& s, size_t n, const AdderOptions& opt, const std::string
     if (rn > c.levels) k.ff = ff_for_lane(lane, lo, hi - lo);
     // algorithmic bytes per element per party (2 x wire + 8 x (in + out)):
     // level round = 2x32 wire + 8x(2 state in + 2 state out) = 96 B. With the opened wire (pair
-    // evaluation) the 32-byte opened value is written once and read once per element pair
-    // (64 B per element per party moved); the roofline counts 8(d)'s algorithmic 96 B.
-    ClassScope cs(rn >= 1 && rn <= c.levels ? kClsAdderRound : kClsOther, 96.0 * double(hi - lo) * s.n_local);
+    // evaluation) the 32-byte opened value is written once and read once per element pair, so
+    // the form needs 64 B per element per party; the roofline counts the bytes of the form run.
+    const double bpe = s.n_local == 2 && pair_eval_enabled() ? 64.0 : 96.0;
+    ClassScope cs(rn >= 1 && rn <= c.levels ? kClsAdderRound : kClsOther, bpe * double(hi - lo) * s.n_local);
     launch_ew(s.stream, s.n_local, hi - lo, k);
   };
   fetch_round(0);

@@ -342,10 +342,12 @@ DT SecureExecutor::weight_matmul(size_t i, const DT& x, const ConvGeom* geom, bo
     es[k] = s_.begin_open(nak, Reduce::Sum);
     if (beaver_combine_wants_aops(s_, 1, mk, N, K)) aops[k] = s_.alloc(Shape{2, nak});
     else if (!geom || nak < (size_t(1) << 32)) es[k].summed = beaver_combine_fuses_eps(s_, 1, mk, N, K);
-    if (geom)
-      eps_build_im2col(s_, t, x.s, *geom, rows[k].first * K, nak, es[k], aops[k] ? &aops[k] : nullptr);
-    else
-      eps_build_mem(s_, t, x.s, rows[k].first * K, nak, es[k], aops[k] ? &aops[k] : nullptr);
+    if (aops[k] || !eps_defer(s_, es[k], x.s, geom, rows[k].first * K, mk, N, K)) {
+      if (geom)
+        eps_build_im2col(s_, t, x.s, *geom, rows[k].first * K, nak, es[k], aops[k] ? &aops[k] : nullptr);
+      else
+        eps_build_mem(s_, t, x.s, rows[k].first * K, nak, es[k], aops[k] ? &aops[k] : nullptr);
+    }
     s_.post(es[k], nch == 1 ? op.tag + ".eps" : op.tag + ".eps.chunk" + std::to_string(k));
   }
   if (opt_.pipelined && wops_.size() > 1) {  // next op's delta leaves while this eps travels

@@ -377,6 +377,7 @@ void ring_gemm_launch(Session& s, const GemmArgs& a) {
     return;
   }
   if (ring_gemm_tc2_wants(a) && ring_gemm_tc3_try(s, a)) return;  // both slots per CTA (tcgen05)
+  if (a.ed.mode) throw Error(kInternalError, "deferred eps: the both-slots GEMM did not take the combine");
   if (ring_gemm_tc2_try(s, a)) return;  // warp-specialised tcgen05 int8-limb path
   if (a.M <= 16) {
     if (a.N <= 16)
@@ -793,6 +794,17 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
       S.sR[g] = sR;
     }
   }
+  if (e.defer.mode) {  // E is generated by the both-slots GEMM's producers (eps_defer)
+    a.ed = e.defer;
+    if (!ring_gemm_tc3_accepts(s, a)) {  // not expected: build the opened value after all
+      Open o = e;
+      o.defer = EpsDefer{};
+      const u64* const x[2] = {e.defer.x0, e.defer.x1};
+      if (e.defer.mode == 2) eps_build_im2col(s, t, x, e.defer.g, a_off, na, o);
+      else eps_build_mem(s, t, x, a_off, na, o);
+      a.ed = EpsDefer{};
+    }
+  }
   ring_gemm_launch(s, a);
 }
 
@@ -850,7 +862,8 @@ DT beaver_matmul(Session& s, const DT& x, const DT& y, bool transpose_b, const s
     else
       he[k].summed = batched_b ? beaver_combine_fuses_eps(s, u32(cnt), u32(M), u32(N), u32(K))
                                : beaver_combine_fuses_eps(s, 1, u32(cnt), u32(N), u32(K));
-    eps_build_mem(s, t, x.s, r.first * row_w, cnt * row_w, he[k], want ? &aops[k] : nullptr);
+    if (want || batched_b || !eps_defer(s, he[k], x.s, nullptr, r.first * row_w, u32(cnt), u32(N), u32(K)))
+      eps_build_mem(s, t, x.s, r.first * row_w, cnt * row_w, he[k], want ? &aops[k] : nullptr);
     s.post(he[k], chunks == 1 ? tag + ".eps" : tag + ".eps.chunk" + std::to_string(k));
   }
   s.wait(hd);

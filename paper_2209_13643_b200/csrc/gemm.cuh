@@ -53,6 +53,7 @@ struct GemmArgs {
   u32 ksplit = 1, kchunk = 0;
   u64* acc[2] = {nullptr, nullptr};
   int vec16 = 0;  // every L (and transposed R) row start is 16-byte aligned (K even, bases aligned)
+  EpsDefer ed{};  // E generated in the GEMM (gemm_tc3.cu only; ed.mode != 0)
 };
 
 struct Epi {
@@ -62,9 +63,6 @@ struct Epi {
   u32 OHW = 1;
 };
 
-struct ConvGeom {
-  u32 N, C, H, W, k, stride, pad, OH, OW;
-};
 
 // Element idx (call-local linear index in the segment's stored layout) of a segment.
 __device__ __forceinline__ u64 load_l(const GemmSlotArgs& S, int sg, u64 idx) {
@@ -130,7 +128,12 @@ bool ring_gemm_tc2_wants(const GemmArgs& a);
 bool ring_gemm_tc2_try(Session& s, const GemmArgs& a);
 // Both party slots of a pair-evaluated Beaver combine in one CTA (gemm_tc3.cu); false = not taken.
 bool ring_gemm_tc3_try(Session& s, const GemmArgs& a);
-int& tc3_mode();    // 1 = both-slots kernel where it applies (default), 0 = tc2 only
+int& tc3_mode();
+bool tc3_shape_ok(const Session& s, u32 M, u32 N, u32 K, bool col2im);
+bool ring_gemm_tc3_accepts(const Session& s, const GemmArgs& a);
+// Defer a summed eps open into the combine GEMM when the both-slots kernel will run it (sets
+// o.defer; the caller then skips the build and still posts o). false = build it as usual.
+bool eps_defer(Session& s, Open& o, const u64* const x[2], const ConvGeom* g, size_t a_off, u32 M, u32 N, u32 K);    // 1 = both-slots kernel where it applies (default), 0 = tc2 only
 int tc3_default();  // MPCG_TC3 (0 = off)
 void tc2_trace_read(unsigned long long* out, int n);  // debug: stage timestamps (MPCG_TC2_TRACE=1)
 void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na, const Open& d, size_t nb,

@@ -72,6 +72,43 @@ __device__ __forceinline__ void e_fetch(const Tc3Args& P, u32 row, u32 k0, u64 (
 }
 
 // 18 warps: SM sub-partitions hold 5 warps x 96 registers at most (16K registers each)
+// Deferred eps (EpsDefer): the 16 opened values E = x0 + x1 - A of row m from the activation
+// shares and the dealer's A, in the producer (what the summed eps build kernels write,
+// eps_build_mem / eps_build_im2col in gemm.cu, H/protocols/beaver.hpp:186-196 + im2col of
+// H/engine/executor.hpp:82-108). v holds the A draws on entry.
+__device__ __forceinline__ void e_gen(const Tc3Args& P, u32 m, u32 k0, u64 (&v)[16]) {
+  const EpsDefer& ed = P.g.ed;
+  const u32 K = P.g.K;
+  if (ed.mode == 1) {
+    const u64 base = ed.a_off + u64(m) * K + k0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      v[i] = (k0 + u32(i) < K) ? __ldg(ed.x0 + base + i) + __ldg(ed.x1 + base + i) - v[i] : 0;
+    return;
+  }
+  const ConvGeom& g = ed.g;
+  const u32 row = u32(ed.a_off / K) + m;  // global im2col row (n, oh, ow)
+  const u32 ow = row % g.OW, rq = row / g.OW, oh = rq % g.OH, n = rq / g.OH;
+  const u32 kk = g.k * g.k;
+  u32 ci = k0 / kk, rem = k0 - ci * kk, ki = rem / g.k, kj = rem - ki * g.k;
+  const int ih0 = int(oh * g.stride) - int(g.pad), iw0 = int(ow * g.stride) - int(g.pad);
+  const u32 img = n * g.C;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int ih = ih0 + int(ki), iw = iw0 + int(kj);
+    u64 x = 0;
+    if (k0 + u32(i) < K && ih >= 0 && iw >= 0 && ih < int(g.H) && iw < int(g.W)) {
+      const u32 idx = ((img + ci) * g.H + u32(ih)) * g.W + u32(iw);
+      x = __ldg(ed.x0 + idx) + __ldg(ed.x1 + idx);
+    }
+    v[i] = (k0 + u32(i) < K) ? x - v[i] : 0;
+    if (++kj == g.k) {
+      kj = 0;
+      if (++ki == g.k) ki = 0, ++ci;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_constant__ Tc3Args P) {
   extern __shared__ __align__(1024) char smem[];
   __shared__ __align__(8) u64 full[kT3Stages], empty[kT3Stages], done;
@@ -130,12 +167,20 @@ __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_cons
       const u32 kp = (ite / 3) * kKB + hf * 16;
       if (ite < nst && m < M && kp < K) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.E + u64(m) * K + kp));
     };
-    l2_prefetch(next_e(u32(j)));
+    if (a.ed.mode == 0) l2_prefetch(next_e(u32(j)));
     for (u32 it = u32(j), use = 0; it < nst; it += kT3Stages, ++use) {
       const u32 kb = it / 3, type = it % 3;
       const u32 k0 = kb * kKB + hf * 16;
       u64 v[16];
-      if (type == 1) {
+      if (type == 1 && a.ed.mode != 0) {  // deferred eps: E = x0 + x1 - A generated here
+        if (m >= M || k0 >= K) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0;
+        } else {
+          draws16(key, iA + u64(m) * K + k0, v, S0.mm.pool);
+          e_gen(P, m, k0, v);
+        }
+      } else if (type == 1) {
         e_fetch(P, m, k0, v);
         l2_prefetch(next_e(it + kT3Stages));
       } else if (m >= M || k0 >= K) {
@@ -326,6 +371,7 @@ int tc3_pattern(const GemmArgs& a) {
 }  // namespace
 
 // 0 = off, 1 = on (default): the both-slots tcgen05 kernel where its pattern applies.
+bool tc3_shape_ok(const Session& s, u32 M, u32 N, u32 K, bool col2im);
 int tc3_default() {
   const char* e = std::getenv("MPCG_TC3");
   return (e && e[0] == '0') ? 0 : 1;
@@ -335,21 +381,62 @@ int& tc3_mode() {
   return mode;
 }
 
-bool ring_gemm_tc3_try(Session& s, const GemmArgs& a) {
-  if (tc3_mode() == 0 || tc_gemm_mode() == 0) return false;
-  const int p0 = tc3_pattern(a);
-  if (p0 < 0) return false;
-  if (u64(3) * a.K > kT3MaxKPrime) return false;
-  const u32 ntiles = (a.N + 63) / 64, mtiles = (a.M + kT3Rows - 1) / kT3Rows;
-  // Several N tiles regenerate the left operand per tile; beyond 4 the tc2 hybrid (dealer-drawn
-  // planes packed once per layer) is cheaper. A grid below one wave leaves SMs idle where tc2
-  // splits K.
+static u32 tc3_maxn() {
   static const u32 maxn = [] {  // N tiles regenerating the left operand (MPCG_TC3_MAXN)
     const char* e = std::getenv("MPCG_TC3_MAXN");
     return e ? u32(std::atoi(e)) : 8u;  // 8 measured faster than the tc2 hybrid at N = 512
   }();
-  if (ntiles > maxn) return false;
+  return maxn;
+}
+
+// Shape policy of the both-slots kernel for a pair-evaluated unbatched combine of an M x K by
+// K x N product: the dispatch order of ring_gemm_launch (small-M GEMV, skinny-N rows, then the
+// tcgen05 size policy) and this kernel's own limits.
+bool tc3_shape_ok(const Session& s, u32 M, u32 N, u32 K, bool col2im) {
+  if (tc3_mode() == 0 || tc_gemm_mode() == 0 || s.n_local != 2) return false;
+  if (gemv_mode() != 0 && (gemv_eligible_shape(M, 1, false, col2im ? 1 : 0) || (N <= 8 && M >= 1024)))
+    return false;
+  GemmArgs a{};
+  a.nslots = 2;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.sl[0].nseg = 3;
+  a.sl[1].nseg = 2;
+  if (!ring_gemm_tc2_wants(a)) return false;
+  if (u64(3) * K > kT3MaxKPrime) return false;
+  const u32 ntiles = (N + 63) / 64, mtiles = (M + kT3Rows - 1) / kT3Rows;
+  if (ntiles > tc3_maxn()) return false;
   if (tc_gemm_mode() != 1 && u64(ntiles) * mtiles < u64(num_sms())) return false;  // forced: any grid
+  return true;
+}
+
+bool ring_gemm_tc3_accepts(const Session& s, const GemmArgs& a) {
+  return tc3_pattern(a) >= 0 && tc3_shape_ok(s, a.M, a.N, a.K, a.col2im != 0);
+}
+
+// Deferred eps (EpsDefer): the summed eps open of a combine that the both-slots kernel will
+// run is not built; its producers generate E. MPCG_EPS_DEFER=0 keeps the build kernels.
+bool eps_defer(Session& s, Open& o, const u64* const x[2], const ConvGeom* g, size_t a_off, u32 M, u32 N, u32 K) {
+  static const bool on = [] {
+    const char* e = std::getenv("MPCG_EPS_DEFER");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || !o.summed || s.n_local != 2 || s.cfg.link_bandwidth > 0) return false;
+  if (!tc3_shape_ok(s, M, N, K, g != nullptr)) return false;
+  if (g && u64(g->N) * g->C * g->H * g->W >= (u64(1) << 32)) return false;  // 32-bit gather index
+  o.defer.mode = g ? 2 : 1;
+  o.defer.x0 = x[0];
+  o.defer.x1 = x[1];
+  if (g) o.defer.g = *g;
+  o.defer.a_off = a_off;
+  return true;
+}
+
+bool ring_gemm_tc3_try(Session& s, const GemmArgs& a) {
+  const int p0 = tc3_pattern(a);
+  if (p0 < 0 || !tc3_shape_ok(s, a.M, a.N, a.K, a.col2im != 0)) return false;
+  const u32 ntiles = (a.N + 63) / 64, mtiles = (a.M + kT3Rows - 1) / kT3Rows;
   static bool attr = false;
   if (!attr) {
     MPCG_CUDA(cudaFuncSetAttribute(ring_gemm_tc3, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -13,7 +13,7 @@ from collections import defaultdict
 
 CLASSES = [
     ("adder_round", r"AdderRound"),
-    ("gemm", r"ring_gemm_tc2|ring_gemm_simt|ring_gemv|ring_gemm_rows"),
+    ("gemm", r"ring_gemm_tc2|ring_gemm_tc3|ring_gemm_simt|ring_gemv|ring_gemm_rows"),
     ("gemm_aux", r"tc2_pack|pack_|gemm_splitk_epilogue"),
     ("eps_delta_build", r"eps_|delta_build|EpsIm2col"),
     ("chain", r"chain_kernel|ChainStep"),
