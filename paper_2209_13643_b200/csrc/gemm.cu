@@ -470,16 +470,6 @@ void eps_build_mem(Session& s, const Triple& t, const u64* const x[2], size_t a_
 // hardware-less 32-bit division, and, when both party slots are local, one r_A draw per element
 // for both slots (party 0 also draws A), as the dealer does.
 namespace {
-struct FastDiv {  // q = n / d for any 32-bit n (Granlund-Montgomery, round-up multiplier)
-  u32 d, m, l;
-  FastDiv() = default;
-  explicit FastDiv(u32 dv) : d(dv) {
-    l = 0;
-    while ((u64(1) << l) < dv) ++l;
-    m = u32(((u64(1) << 32) * ((u64(1) << l) - dv)) / dv + 1);
-  }
-  __device__ __forceinline__ u32 div(u32 n) const { return u32((u64(__umulhi(m, n)) + n) >> l); }
-};
 struct EpsIm2colPair {
   MmTriple mm;
   Pid2 pid;

@@ -64,6 +64,17 @@ struct Epi {
 };
 
 
+struct FastDiv {  // q = n / d for any 32-bit n (Granlund-Montgomery, round-up multiplier)
+  u32 d, m, l;
+  FastDiv() = default;
+  explicit FastDiv(u32 dv) : d(dv) {
+    l = 0;
+    while ((u64(1) << l) < dv) ++l;
+    m = u32(((u64(1) << 32) * ((u64(1) << l) - dv)) / dv + 1);
+  }
+  __device__ __forceinline__ u32 div(u32 n) const { return u32((u64(__umulhi(m, n)) + n) >> l); }
+};
+
 // Element idx (call-local linear index in the segment's stored layout) of a segment.
 __device__ __forceinline__ u64 load_l(const GemmSlotArgs& S, int sg, u64 idx) {
   switch (S.lk[sg]) {

@@ -50,6 +50,7 @@ struct Tc3Args {
   const char* Wpk = nullptr;  // packed weights: [ntile][kb][3][8 planes][128 rows x 32 B]
   u32 nkb = 0;
   int vec = 0;                // 2 = E rows 32-byte aligned (LDG.256), 1 = 16-byte, 0 = scalar
+  FastDiv fkk, fk;            // deferred conv eps: k*k and k
 };
 
 // 16 K-consecutive values of E row `row` starting at k0 (zero past M / K).
@@ -75,8 +76,27 @@ __device__ __forceinline__ void e_fetch(const Tc3Args& P, u32 row, u32 k0, u64 (
 // Deferred eps (EpsDefer): the 16 opened values E = x0 + x1 - A of row m from the activation
 // shares and the dealer's A, in the producer (what the summed eps build kernels write,
 // eps_build_mem / eps_build_im2col in gemm.cu, H/protocols/beaver.hpp:186-196 + im2col of
-// H/engine/executor.hpp:82-108). v holds the A draws on entry.
-__device__ __forceinline__ void e_gen(const Tc3Args& P, u32 m, u32 k0, u64 (&v)[16]) {
+// H/engine/executor.hpp:82-108). v holds the A draws on entry. Conv rows: the thread's output
+// pixel is decoded once (GatherRow); per stage the (ci, ki, kj) of k0 by two multiply-shift
+// divisions, then the input index advances incrementally; rows whose 3x3 (k x k) window lies
+// inside the image skip the bounds tests.
+struct GatherRow {
+  u32 img;       // n * C
+  int ih0, iw0;  // top-left input coordinate of the window
+  bool inside;
+};
+__device__ __forceinline__ GatherRow gather_row(const EpsDefer& ed, u32 K, u32 m) {
+  const ConvGeom& g = ed.g;
+  GatherRow gr{};
+  const u32 row = u32(ed.a_off / K) + m;  // global im2col row (n, oh, ow)
+  const u32 ow = row % g.OW, rq = row / g.OW, oh = rq % g.OH, n = rq / g.OH;
+  gr.img = n * g.C;
+  gr.ih0 = int(oh * g.stride) - int(g.pad);
+  gr.iw0 = int(ow * g.stride) - int(g.pad);
+  gr.inside = gr.ih0 >= 0 && gr.iw0 >= 0 && gr.ih0 + int(g.k) <= int(g.H) && gr.iw0 + int(g.k) <= int(g.W);
+  return gr;
+}
+__device__ __forceinline__ void e_gen(const Tc3Args& P, const GatherRow& gr, u32 m, u32 k0, u64 (&v)[16]) {
   const EpsDefer& ed = P.g.ed;
   const u32 K = P.g.K;
   if (ed.mode == 1) {
@@ -86,25 +106,35 @@ __device__ __forceinline__ void e_gen(const Tc3Args& P, u32 m, u32 k0, u64 (&v)[
       v[i] = (k0 + u32(i) < K) ? __ldg(ed.x0 + base + i) + __ldg(ed.x1 + base + i) - v[i] : 0;
     return;
   }
-  const ConvGeom& g = ed.g;
-  const u32 row = u32(ed.a_off / K) + m;  // global im2col row (n, oh, ow)
-  const u32 ow = row % g.OW, rq = row / g.OW, oh = rq % g.OH, n = rq / g.OH;
-  const u32 kk = g.k * g.k;
-  u32 ci = k0 / kk, rem = k0 - ci * kk, ki = rem / g.k, kj = rem - ki * g.k;
-  const int ih0 = int(oh * g.stride) - int(g.pad), iw0 = int(ow * g.stride) - int(g.pad);
-  const u32 img = n * g.C;
+  const u32 ks = ed.g.k, H = ed.g.H, W = ed.g.W;
+  const u32 ci = P.fkk.div(k0), rem = k0 - ci * P.fkk.d, ki0 = P.fk.div(rem), kj0 = rem - ki0 * ks;
+  int ki = int(ki0), kj = int(kj0);
+  int idx = int(((gr.img + ci) * H) * W) + (gr.ih0 + ki) * int(W) + gr.iw0 + kj;
+  const int wstep = int(W) - int(ks), cstep = int(H - ks) * int(W);
+  if (gr.inside && k0 + 16 <= K) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      v[i] = __ldg(ed.x0 + idx) + __ldg(ed.x1 + idx) - v[i];
+      ++idx;
+      if (++kj == int(ks)) {
+        kj = 0;
+        idx += wstep;
+        if (++ki == int(ks)) ki = 0, idx += cstep;
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
-    const int ih = ih0 + int(ki), iw = iw0 + int(kj);
+    const int ih = gr.ih0 + ki, iw = gr.iw0 + kj;
     u64 x = 0;
-    if (k0 + u32(i) < K && ih >= 0 && iw >= 0 && ih < int(g.H) && iw < int(g.W)) {
-      const u32 idx = ((img + ci) * g.H + u32(ih)) * g.W + u32(iw);
-      x = __ldg(ed.x0 + idx) + __ldg(ed.x1 + idx);
-    }
+    if (k0 + u32(i) < K && ih >= 0 && iw >= 0 && ih < int(H) && iw < int(W)) x = __ldg(ed.x0 + idx) + __ldg(ed.x1 + idx);
     v[i] = (k0 + u32(i) < K) ? x - v[i] : 0;
-    if (++kj == g.k) {
+    ++idx;
+    if (++kj == int(ks)) {
       kj = 0;
-      if (++ki == g.k) ki = 0, ++ci;
+      idx += wstep;
+      if (++ki == int(ks)) ki = 0, idx += cstep;
     }
   }
 }
@@ -168,6 +198,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_cons
       if (ite < nst && m < M && kp < K) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.E + u64(m) * K + kp));
     };
     if (a.ed.mode == 0) l2_prefetch(next_e(u32(j)));
+    const GatherRow gr = a.ed.mode == 2 ? gather_row(a.ed, K, m) : GatherRow{};
     for (u32 it = u32(j), use = 0; it < nst; it += kT3Stages, ++use) {
       const u32 kb = it / 3, type = it % 3;
       const u32 k0 = kb * kKB + hf * 16;
@@ -178,7 +209,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_cons
           for (int i = 0; i < 16; ++i) v[i] = 0;
         } else {
           draws16(key, iA + u64(m) * K + k0, v, S0.mm.pool);
-          e_gen(P, m, k0, v);
+          e_gen(P, gr, m, k0, v);
         }
       } else if (type == 1) {
         e_fetch(P, m, k0, v);
@@ -448,6 +479,10 @@ bool ring_gemm_tc3_try(Session& s, const GemmArgs& a) {
   P.p0slot = p0;
   P.E = a.sl[p0].L[1];
   P.nkb = (a.K + kKB - 1) / kKB;
+  if (a.ed.mode == 2) {
+    P.fkk = FastDiv(a.ed.g.k * a.ed.g.k);
+    P.fk = FastDiv(a.ed.g.k);
+  }
   const uintptr_t ea = reinterpret_cast<uintptr_t>(P.E);
   P.vec = (a.K % 4 == 0 && ea % 32 == 0) ? 2 : (a.K % 2 == 0 && ea % 16 == 0) ? 1 : 0;
   const u64 wbytes = u64(ntiles) * P.nkb * 3 * 8 * kT3A;
