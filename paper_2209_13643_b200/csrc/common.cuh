@@ -84,8 +84,23 @@ __device__ __forceinline__ u64 pool_at(const u64* pool, u64 z, u64 key) {
   return __ldg(pool + ((z - key) * kPhiInv - 1));
 }
 __device__ __forceinline__ u64 dmix(u64 z, u64 key, const u64* pool) {
-  if (pool) return pool_at(pool, z, key);
+#ifndef MPCG_SEEDED_ONLY  // (A/B measurement build: seeded dealer only, no queue source)
+  if (__builtin_expect(pool != nullptr, 0)) return pool_at(pool, z, key);
+#endif
   return mix64(z);
+}
+
+// The triple source is decided once per call site, not per draw: f(std::true_type) reads the
+// materialised draws, f(std::false_type) runs the seeded dealer's splitmix64 straight-line (a
+// branch per draw would split the independent draws of an element into separate blocks).
+template <class F>
+__device__ __forceinline__ auto by_source(const u64* pool, F f) {
+  if (__builtin_expect(pool != nullptr, 0)) return f(std::true_type{});  // cold: queue source
+  return f(std::false_type{});
+}
+template <bool P>
+__device__ __forceinline__ u64 drawp(u64 z, u64 key, const u64* pool) {
+  return P ? pool_at(pool, z, key) : mix64(z);
 }
 
 // ------------------------------------------------------------------ dealer
@@ -152,9 +167,35 @@ __device__ __forceinline__ Dw ew_draw_t(const EwTriple& t, u64 g, bool p0) {
 }
 template <bool WithC>
 __device__ __forceinline__ Dw ew_draw(const EwTriple& t, u64 g, bool p0) {
-  if (t.pool) return ew_draw_t<WithC, true>(t, g, p0);
+  if (__builtin_expect(t.pool != nullptr, 0)) return ew_draw_t<WithC, true>(t, g, p0);  // cold: queue source
   return ew_draw_t<WithC, false>(t, g, p0);
 }
+// The same draws with the stream key and (global index)*phi supplied by the caller: hot loops
+// resolve the key once per thread and share one 64-bit multiply between an element's triples.
+template <bool WithC, bool Pool>
+__device__ __forceinline__ Dw ew_draw_kg(const EwTriple& t, u64 key, u64 gp, bool p0) {
+  Dw d;
+  auto dr = [&](u64 z) { return Pool ? pool_at(t.pool, z, key) : mix64(z); };
+  d.ra = dr(key + t.pra + gp);
+  d.rb = dr(key + t.prb + gp);
+  d.rc = WithC ? dr(key + t.prc + gp) : 0;
+  d.A = d.B = 0;
+  if (p0) {
+    d.A = dr(key + t.pA + gp);
+    d.B = t.square ? d.A : dr(key + t.pB + gp);
+  }
+  return d;
+}
+template <bool Pool>
+__device__ __forceinline__ Dw ew_secrets_kg(const EwTriple& t, u64 key, u64 gp) {
+  auto dr = [&](u64 z) { return Pool ? pool_at(t.pool, z, key) : mix64(z); };
+  Dw d;
+  d.ra = d.rb = d.rc = 0;
+  d.A = dr(key + t.pA + gp);
+  d.B = t.square ? d.A : dr(key + t.pB + gp);
+  return d;
+}
+
 // Only the dealer's secrets A, B of element g: what the two parties' shares reconstruct to
 // (a0 ^ a1 or a0 + a1), all an opened-wire issue needs — the masks cancel in the open.
 template <bool Pool>
@@ -169,7 +210,7 @@ __device__ __forceinline__ Dw ew_secrets_t(const EwTriple& t, u64 g) {
   return d;
 }
 __device__ __forceinline__ Dw ew_secrets(const EwTriple& t, u64 g) {
-  if (t.pool) return ew_secrets_t<true>(t, g);
+  if (__builtin_expect(t.pool != nullptr, 0)) return ew_secrets_t<true>(t, g);  // cold: queue source
   return ew_secrets_t<false>(t, g);
 }
 // `party`'s shares of a drawn element (0 absorbs the secret).
@@ -206,22 +247,29 @@ __device__ __forceinline__ void ew_abc(const EwTriple& t, int party, u64 g, u64&
 __device__ __forceinline__ void sq_ac(const EwTriple& t, int party, u64 g, u64& a, u64& c) {
   const u64 key = tkey(t.key, t.kp);
   const u64 gp = g * kPhi;
-  const u64 ra = dmix(key + t.pra + gp, key, t.pool), rc = dmix(key + t.prc + gp, key, t.pool);
-  if (party != 0) {
-    a = ra;
-    c = rc;
-    return;
-  }
-  const u64 A = dmix(key + t.pA + gp, key, t.pool);
-  a = A - ra;
-  c = A * A - rc;
+  by_source(t.pool, [&](auto src) {
+    constexpr bool P = decltype(src)::value;
+    const u64 ra = drawp<P>(key + t.pra + gp, key, t.pool), rc = drawp<P>(key + t.prc + gp, key, t.pool);
+    if (party != 0) {
+      a = ra;
+      c = rc;
+      return 0;
+    }
+    const u64 A = drawp<P>(key + t.pA + gp, key, t.pool);
+    a = A - ra;
+    c = A * A - rc;
+    return 0;
+  });
 }
 
 __device__ __forceinline__ u64 sq_a(const EwTriple& t, int party, u64 g) {
   const u64 key = tkey(t.key, t.kp);
   const u64 gp = g * kPhi;
-  const u64 ra = dmix(key + t.pra + gp, key, t.pool);
-  return party != 0 ? ra : dmix(key + t.pA + gp, key, t.pool) - ra;
+  return by_source(t.pool, [&](auto src) {
+    constexpr bool P = decltype(src)::value;
+    const u64 ra = drawp<P>(key + t.pra + gp, key, t.pool);
+    return party != 0 ? ra : drawp<P>(key + t.pA + gp, key, t.pool) - ra;
+  });
 }
 
 // Matmul triple (H/sharing/triple.hpp:96-114): draws A (na), B (nb), then r_A, r_B, r_C.
@@ -393,10 +441,23 @@ __device__ __forceinline__ void eval_slots(const F& f, bool pair, int slot, u64 
   }
 }
 
+// Functors may define prep() -> P (per-thread values computed once before the grid-stride
+// loop, e.g. the dealer keys of graph replay) and both_p(i, P); the functor itself stays in
+// the kernel's parameter space (a local copy of a large functor lands in local memory).
+template <class F, class = void>
+struct has_prep : std::false_type {};
+template <class F>
+struct has_prep<F, std::void_t<decltype(std::declval<const F&>().prep())>> : std::true_type {};
+
 template <class F>
 __global__ void __launch_bounds__(256, 4) ew_pair_kernel(u64 n, F f) {
   pdl_enter();
-  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) f.both(i);
+  if constexpr (has_prep<F>::value) {
+    const auto p = f.prep();
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) f.both_p(i, p);
+  } else {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) f.both(i);
+  }
 }
 
 // Launch f(slot, i) for i in [0, n) and every local party slot, on `stream`.

@@ -237,11 +237,14 @@ struct Sw {
 __device__ __forceinline__ Sw sq_draw(const EwTriple& t, u64 g, bool p0, bool with_c) {
   const u64 key = tkey(t.key, t.kp);
   const u64 gp = g * kPhi;
-  Sw d;
-  d.ra = dmix(key + t.pra + gp, key, t.pool);
-  d.rc = with_c ? dmix(key + t.prc + gp, key, t.pool) : 0;
-  d.A = p0 ? dmix(key + t.pA + gp, key, t.pool) : 0;
-  return d;
+  return by_source(t.pool, [&](auto src) {
+    constexpr bool P = decltype(src)::value;
+    Sw d;
+    d.ra = drawp<P>(key + t.pra + gp, key, t.pool);
+    d.rc = with_c ? drawp<P>(key + t.prc + gp, key, t.pool) : 0;
+    d.A = p0 ? drawp<P>(key + t.pA + gp, key, t.pool) : 0;
+    return d;
+  });
 }
 __device__ __forceinline__ u64 sq_share_a(int party, const Sw& d) { return party ? d.ra : d.A - d.ra; }
 // the square triple's secret A alone (a0 + a1 = A: all an opened-wire build needs)
@@ -800,12 +803,19 @@ struct AdderRound {
   const u64* cwp = nullptr;  // draw cache written by the previous round's issue (or null)
   u64* cwn = nullptr;        // draw cache for the next round's settle (or null)
   u64 cwN = 0;               // elements per cache plane
-  __device__ void operator()(int slot, u64 j) const { step<1>(slot, j); }
-  __device__ void both(u64 j) const { step<2>(0, j); }
+  struct Keys {
+    u64 p, n;
+  };
+  __device__ Keys keys() const { return {tkey(Tp.key, Tp.kp), tkey(Tn.key, Tn.kp)}; }
+  __device__ void operator()(int slot, u64 j) const { step<1>(slot, j, keys()); }
+  __device__ void both(u64 j) const { step<2>(0, j, keys()); }
+  // ew_pair_kernel: the two triples' keys (device key slots under graph replay) read once
+  __device__ Keys prep() const { return keys(); }
+  __device__ void both_p(u64 j, const Keys& k) const { step<2>(0, j, k); }
 
   // NS party slots (slot0, slot0+1, ...) of element j; dealer draws are shared by the slots.
   template <int NS>
-  __device__ __forceinline__ void step(int slot0, u64 j) const {
+  __device__ __forceinline__ void step(int slot0, u64 j, const Keys& ks) const {
     const u64 g = lo + j;
     const bool p0 = NS == 2 || pid.v[slot0] == 0;  // does any evaluated slot play party 0
     u64 dummy;
@@ -859,9 +869,10 @@ struct AdderRound {
     } else {  // settle a prefix level (H/protocols/adder.hpp:142-165)
       // Own payload is recomputed from the pre-round state instead of re-read from HBM:
       // it is a function of (s, p) and the triple, all of which this thread holds.
-      const Dw d0 = cwp ? dw_load(cwp, cwN, g, 0, Tp, Tp.off + g) : ew_draw_t<true, Pool>(Tp, Tp.off + g, p0);
+      const u64 kp = ks.p, gp0 = (Tp.off + g) * kPhi;  // one multiply for both triples
+      const Dw d0 = cwp ? dw_load(cwp, cwN, g, 0, Tp, Tp.off + g) : ew_draw_kg<true, Pool>(Tp, kp, gp0, p0);
       const Dw d1 = cwp ? dw_load(cwp, cwN, g, 1, Tp, Tp.ghalf + Tp.off + g)
-                        : ew_draw_t<true, Pool>(Tp, Tp.ghalf + Tp.off + g, p0);
+                        : ew_draw_kg<true, Pool>(Tp, kp, gp0 + Tp.ghalf * kPhi, p0);
       u64 oe0 = 0, oe1 = 0, od0 = 0, od1 = 0;  // the opened wire (pair evaluation)
       if (op) {
         const u64* o = ownp.p[0];
@@ -892,9 +903,9 @@ struct AdderRound {
     if (rn <= levels) {  // issue level rn-1 (H/protocols/adder.hpp:122-140)
       // opened wire: the masks r_A, r_B cancel between the two payloads (see rn == 0)
       const bool sec = op && !cwn;
-      const Dw d0 = sec ? ew_secrets_t<Pool>(Tn, Tn.off + g) : ew_draw_t<false, Pool>(Tn, Tn.off + g, p0);
-      const Dw d1 = sec ? ew_secrets_t<Pool>(Tn, Tn.ghalf + Tn.off + g)
-                        : ew_draw_t<false, Pool>(Tn, Tn.ghalf + Tn.off + g, p0);
+      const u64 kn = ks.n, gn0 = (Tn.off + g) * kPhi, gn1 = gn0 + Tn.ghalf * kPhi;
+      const Dw d0 = sec ? ew_secrets_kg<Pool>(Tn, kn, gn0) : ew_draw_kg<false, Pool>(Tn, kn, gn0, p0);
+      const Dw d1 = sec ? ew_secrets_kg<Pool>(Tn, kn, gn1) : ew_draw_kg<false, Pool>(Tn, kn, gn1, p0);
       if (cwn) {
         dw_store(cwn, cwN, g, 0, d0);
         dw_store(cwn, cwN, g, 1, d1);
