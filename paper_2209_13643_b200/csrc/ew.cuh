@@ -1084,10 +1084,27 @@ void adder_op(Session& s, size_t n, const AdderOptions& opt, const std::string& 
 }
 
 // ---------------------------------------------------------------- persistent round chain
+// Launch geometry of a persistent chain over n elements: one element per thread per round, in
+// CTAs of 256 threads, or smaller CTAs when n is small so the chain spreads over more SMs (a
+// round's cost is one element's dealer-draw latency on a lightly loaded sub-partition, plus the
+// grid barrier). MPCG_CHAIN_TPB forces a CTA size.
+inline unsigned chain_tpb(u64 n) {
+  static const int forced = [] {
+    const char* e = std::getenv("MPCG_CHAIN_TPB");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 64 || forced == 128 || forced == 256) return unsigned(forced);
+  const u64 sms = u64(num_sms());
+  return n <= sms * 64 ? 64u : n <= sms * 128 ? 128u : 256u;
+}
 // In 1-GPU mode an open is only an ordering point between the two party slots, so a whole
 // chain of secure rounds can run as ONE cooperative kernel: each round is a grid-stride
 // pass over the elements, and a grid-wide barrier (release/acquire at gpu scope) takes the
 // place of the kernel boundary. Round logic is the same functors as the multi-kernel path.
+#ifndef MPCG_BARRIER_SLEEP
+#define MPCG_BARRIER_SLEEP 20
+#endif
+constexpr unsigned kBarrierSleep = MPCG_BARRIER_SLEEP;  // ns between polls of the grid barrier
 __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1096,7 +1113,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
     while (true) {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
       if (v >= target) break;
-      __nanosleep(20);
+      if (kBarrierSleep) __nanosleep(kBarrierSleep);
     }
   }
   __syncthreads();
@@ -1179,12 +1196,13 @@ void persistent_beaver_chain(Session& s, u64 n, const B0& build, const std::vect
     MPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
     if (per_sm < 1) throw Error(kInternalError, "beaver chain kernel cannot be resident");
   }
-  const u64 cap = u64(per_sm) * num_sms() / gy;
-  u64 blocks = (n + 255) / 256;
+  const unsigned tpb = chain_tpb(n);
+  const u64 cap = u64(per_sm) * (256 / tpb) * num_sms() / gy;  // residency measured at 256 threads
+  u64 blocks = (n + tpb - 1) / tpb;
   blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(unsigned(blocks), gy);
-  lc.blockDim = dim3(256);
+  lc.blockDim = dim3(tpb);
   lc.stream = s.stream;
   cudaLaunchAttribute attr{};
   attr.id = cudaLaunchAttributeCooperative;

@@ -511,12 +511,13 @@ void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const
     MPCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
     if (per_sm < 1) throw Error(kInternalError, "chain kernel cannot be resident");
   }
-  const u64 cap = u64(per_sm) * num_sms() / gy;
-  u64 blocks = (n + 255) / 256;  // one element per thread per round (the rounds are PRG-latency bound)
+  const unsigned tpb = chain_tpb(n);  // one element per thread per round (PRG-latency bound)
+  const u64 cap = u64(per_sm) * (256 / tpb) * num_sms() / gy;  // residency measured at 256 threads
+  u64 blocks = (n + tpb - 1) / tpb;
   blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(unsigned(blocks), gy);
-  lc.blockDim = dim3(256);
+  lc.blockDim = dim3(tpb);
   lc.stream = s.stream;
   cudaLaunchAttribute attr{};
   attr.id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barrier)
