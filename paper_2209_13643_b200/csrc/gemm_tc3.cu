@@ -51,7 +51,20 @@ struct Tc3Args {
   u32 nkb = 0;
   int vec = 0;                // 2 = E rows 32-byte aligned (LDG.256), 1 = 16-byte, 0 = scalar
   FastDiv fkk, fk;            // deferred conv eps: k*k and k
+  FastDiv fohw;               // col2im epilogue: OH*OW
 };
+
+// gemm_epilogue's value (+-r_C, truncation, bias) without the store.
+__device__ __forceinline__ u64 epi_value(const GemmArgs& a, const GemmSlotArgs& S, u32 m, u32 n, u64 v) {
+  const u64 lin = u64(m) * a.N + n;
+  if (S.cterm) {
+    const u64 rc = S.mm.pool ? __ldg(S.mm.pool + S.cbase + lin - 1) : drw(tkey(S.ckey, S.ckp), S.cbase + lin);
+    v = S.cterm > 0 ? v + rc : v - rc;
+  }
+  if (a.trunc_bits) v = sar64(v, a.trunc_bits);
+  if (S.bias) v += S.bias[n];
+  return v;
+}
 
 // 16 K-consecutive values of E row `row` starting at k0 (zero past M / K).
 __device__ __forceinline__ void e_fetch(const Tc3Args& P, u32 row, u32 k0, u64 (&v)[16]) {
@@ -288,12 +301,34 @@ __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_cons
 #pragma unroll
         for (int c = 0; c < 8; ++c) acc[c] += u64(rr[c]) << (8 * d);
       }
-      if (n < N) {
+      if (a.col2im) {  // staged in shared memory, stored below with lanes along the rows
+        u64* tile = reinterpret_cast<u64*>(smem) + (u32(q >> 1) * 64 + u32(q & 1) * 32 + u32(lane)) * kT3Rows;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const u32 mloc = u32(cg) * 16 + u32(h) * 8 + u32(c);
+          tile[mloc] = (n < N && m0 + mloc < M) ? epi_value(a, S, m0 + mloc, n, acc[c]) : 0;
+        }
+      } else if (n < N) {
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const u32 mm = m0 + u32(cg) * 16 + u32(h) * 8 + u32(c);
           if (mm < M) gemm_epilogue(a, S, 0, mm, n, acc[c]);
         }
+      }
+    }
+    if (a.col2im) {
+      // col2im (H/engine/executor.hpp:110-123): out[(img*N + n)*OHW + rem] for global row
+      // m0 + row0 + mloc = img*OHW + rem. Lanes run along the rows, so a warp writes up to 32
+      // consecutive words of one output plane instead of 32 planes one word each.
+      asm volatile("bar.sync 1, %0;" ::"r"(4 * kT3Groups * 32) : "memory");
+      const u64* tile = reinterpret_cast<const u64*>(smem);
+      for (u32 e = u32(tid); e < 2u * 64u * kT3Rows; e += 4 * kT3Groups * 32) {
+        const u32 mloc = e % kT3Rows, nq = e / kT3Rows;  // nq = party*64 + column
+        const u32 party = nq / 64, n = n0 + nq % 64, mm = m0 + mloc;
+        if (n >= N || mm >= M) continue;
+        const int sl = party == 0 ? P.p0slot : 1 - P.p0slot;
+        const u32 mg = mm + a.row0, img = P.fohw.div(mg), rem = mg - img * a.OHW;
+        a.sl[sl].out[(u64(img) * N + n) * a.OHW + rem] = tile[nq * kT3Rows + mloc];
       }
     }
   }
@@ -483,6 +518,7 @@ bool ring_gemm_tc3_try(Session& s, const GemmArgs& a) {
     P.fkk = FastDiv(a.ed.g.k * a.ed.g.k);
     P.fk = FastDiv(a.ed.g.k);
   }
+  if (a.col2im) P.fohw = FastDiv(a.OHW);
   const uintptr_t ea = reinterpret_cast<uintptr_t>(P.E);
   P.vec = (a.K % 4 == 0 && ea % 32 == 0) ? 2 : (a.K % 2 == 0 && ea % 16 == 0) ? 1 : 0;
   const u64 wbytes = u64(ntiles) * P.nkb * 3 * 8 * kT3A;
