@@ -119,6 +119,7 @@ SIGNATURES = {
     "mpcg_set_gemm_mode": [I32],
     "mpcg_set_gemv": [I32],
     "mpcg_debug_tc2_trace": [U64P, I32],
+    "mpcg_debug_tc3_trace": [U64P, I32],
     "mpcg_session_connect_loopback": [P, P],
     "mpcg_launch_count": [],
     "mpcg_probe_start": [I32],

@@ -638,6 +638,10 @@ int mpcg_session_connect_loopback(mpcg_session* a, mpcg_session* b) {
   });
 }
 
+int mpcg_debug_tc3_trace(uint64_t* out, int n) {
+  return guard([&] { tc3_trace_read(reinterpret_cast<unsigned long long*>(out), n); });
+}
+
 int mpcg_debug_tc2_trace(uint64_t* out, int n) {
   return guard([&] { tc2_trace_read(reinterpret_cast<unsigned long long*>(out), n); });
 }

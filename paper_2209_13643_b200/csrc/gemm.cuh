@@ -146,7 +146,8 @@ bool ring_gemm_tc3_accepts(const Session& s, const GemmArgs& a);
 // o.defer; the caller then skips the build and still posts o). false = build it as usual.
 bool eps_defer(Session& s, Open& o, const u64* const x[2], const ConvGeom* g, size_t a_off, u32 M, u32 N, u32 K);    // 1 = both-slots kernel where it applies (default), 0 = tc2 only
 int tc3_default();  // MPCG_TC3 (0 = off)
-void tc2_trace_read(unsigned long long* out, int n);  // debug: stage timestamps (MPCG_TC2_TRACE=1)
+void tc2_trace_read(unsigned long long* out, int n);
+void tc3_trace_read(unsigned long long* out, int n);  // debug: MPCG_TC3_TRACE=1 stage stamps  // debug: stage timestamps (MPCG_TC2_TRACE=1)
 void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, size_t na, const Open& d, size_t nb,
                     DT* rcache, u64* const out[2], size_t out_off, u32 nbatch, u32 M, u32 N, u32 K, bool tb,
                     bool batched_r, size_t r_batch0, const Epi& ep, const DT* aops = nullptr);

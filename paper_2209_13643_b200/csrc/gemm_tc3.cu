@@ -43,6 +43,13 @@ constexpr u32 kT3B = kT3Rows * kKB;            // bytes per generated limb plane
 constexpr u32 kT3Stage = 8 * (kT3A + kT3B);    // 48 KB
 constexpr u32 kT3MaxKPrime = 16384;
 
+// Debug trace (MPCG_TC3_TRACE=1): per-stage clock64 stamps of CTA (0,0,0) — MMA thread: wait
+// start, stage full, MMAs issued; the producing group's first warp: generation start, empty
+// wait start, empty acquired, arrived — plus the epilogue start/end (row kT3TraceRows - 1).
+// Read back with mpcg_debug_tc3_trace; off by default, no effect on values.
+constexpr int kT3TraceRows = 256;
+__device__ unsigned long long g_tc3_trace[kT3TraceRows][8];
+
 struct Tc3Args {
   GemmArgs g;
   int p0slot = 0;             // slot index of party 0 (image rows 0-63)
@@ -52,6 +59,7 @@ struct Tc3Args {
   int vec = 0;                // 2 = E rows 32-byte aligned (LDG.256), 1 = 16-byte, 0 = scalar
   FastDiv fkk, fk;            // deferred conv eps: k*k and k
   FastDiv fohw;               // col2im epilogue: OH*OW
+  int trace = 0;
 };
 
 // gemm_epilogue's value (+-r_C, truncation, bias) without the store.
@@ -212,9 +220,11 @@ __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_cons
     };
     if (a.ed.mode == 0) l2_prefetch(next_e(u32(j)));
     const GatherRow gr = a.ed.mode == 2 ? gather_row(a.ed, K, m) : GatherRow{};
+    const bool tr = P.trace && blockIdx.x == 0 && blockIdx.y == 0 && (tid & 127) == 0;
     for (u32 it = u32(j), use = 0; it < nst; it += kT3Stages, ++use) {
       const u32 kb = it / 3, type = it % 3;
       const u32 k0 = kb * kKB + hf * 16;
+      if (tr && it < kT3TraceRows - 1) g_tc3_trace[it][3] = clock64();
       u64 v[16];
       if (type == 1 && a.ed.mode != 0) {  // deferred eps: E = x0 + x1 - A generated here
         if (m >= M || k0 >= K) {
@@ -238,11 +248,14 @@ __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_cons
             if (k0 + u32(i) >= K) v[i] = 0;
         }
       }
+      if (tr && it < kT3TraceRows - 1) g_tc3_trace[it][4] = clock64();
       if (use > 0) mbar_wait(&empty[j], (use - 1) & 1);
+      if (tr && it < kT3TraceRows - 1) g_tc3_trace[it][5] = clock64();
       limb_store16(v, sB + off, 8 * 128);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[j]);
+      if (tr && it < kT3TraceRows - 1) g_tc3_trace[it][6] = clock64();
     }
   } else if (warp == 4 * kT3Groups) {
     if (lane == 0) {  // ---- bulk loader: the packed weight image of each stage
@@ -256,9 +269,12 @@ __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_cons
     }
   } else {
     if (lane == 0) {  // ---- MMA issuer
+      const bool tr = P.trace && blockIdx.x == 0 && blockIdx.y == 0;
       for (u32 it = 0; it < nst; ++it) {
         const int stg = int(it % kT3Stages);
+        if (tr && it < kT3TraceRows - 1) g_tc3_trace[it][0] = clock64();
         mbar_wait(&full[stg], (it / kT3Stages) & 1);
+        if (tr && it < kT3TraceRows - 1) g_tc3_trace[it][1] = clock64();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const u32 aBase = smem_u32(smem + stg * kT3Stage), bBase = aBase + 8 * kT3A;
         // weight plane l x generated planes 0..7-l stacked along N -> diagonals l..7
@@ -274,6 +290,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_cons
           }
         }
         mma_commit(&empty[stg]);
+        if (tr && it < kT3TraceRows - 1) g_tc3_trace[it][2] = clock64();
       }
       mma_commit(&done);
     }
@@ -284,6 +301,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_cons
   if (warp < 4 * kT3Groups) {
     mbar_wait(&done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const bool tre = P.trace && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0;
+    if (tre) g_tc3_trace[kT3TraceRows - 1][0] = clock64();
     const int q = warp & 3, cg = warp >> 2;
     const int slot = (q >> 1) == 0 ? P.p0slot : 1 - P.p0slot;
     const u32 n = n0 + u32(q & 1) * 32 + u32(lane);
@@ -295,18 +314,37 @@ __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_cons
 #pragma unroll
       for (int c = 0; c < 8; ++c) acc[c] = 0;
 #pragma unroll
-      for (int d = 0; d < 8; ++d) {
-        u32 rr[8];
-        tmem_ld<8>(lane_addr + u32(d) * kT3Rows, rr);
+      for (int d0 = 0; d0 < 8; d0 += 4) {  // 4 diagonals in flight per wait
+        u32 rr[32];
+        tmem_ld4x8(lane_addr + u32(d0) * kT3Rows, lane_addr + u32(d0 + 1) * kT3Rows,
+                   lane_addr + u32(d0 + 2) * kT3Rows, lane_addr + u32(d0 + 3) * kT3Rows, rr);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) acc[c] += u64(rr[c]) << (8 * d);
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[c] += u64(rr[8 * i + c]) << (8 * (d0 + i));
       }
       if (a.col2im) {  // staged in shared memory, stored below with lanes along the rows
         u64* tile = reinterpret_cast<u64*>(smem) + (u32(q >> 1) * 64 + u32(q & 1) * 32 + u32(lane)) * kT3Rows;
+        // Beaver epilogue per value (gemm_epilogue's +-r_C, truncation, bias), with the r_C
+        // stream position advanced by N*phi per row instead of recomputed, and the key, bias
+        // and slot fields read once
+        const u32 mb = m0 + u32(cg) * 16 + u32(h) * 8;
+        const u64 ck = S.cterm ? (S.mm.pool ? 0 : tkey(S.ckey, S.ckp)) : 0;
+        u64 z = ck + (S.cbase + u64(mb) * N + n) * kPhi;
+        const u64 dz = u64(N) * kPhi;
+        const u64 bias = (S.bias && n < N) ? S.bias[n] : 0;
+        const int cterm = S.cterm, tb = a.trunc_bits;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const u32 mloc = u32(cg) * 16 + u32(h) * 8 + u32(c);
-          tile[mloc] = (n < N && m0 + mloc < M) ? epi_value(a, S, m0 + mloc, n, acc[c]) : 0;
+          u64 v = acc[c];
+          if (cterm) {
+            const u64 rc = S.mm.pool ? __ldg(S.mm.pool + S.cbase + (u64(mb + c) * N + n) - 1) : mix64(z);
+            v = cterm > 0 ? v + rc : v - rc;
+          }
+          if (tb) v = sar64(v, tb);
+          tile[mloc] = (n < N && m0 + mloc < M) ? v + bias : 0;
+          z += dz;
         }
       } else if (n < N) {
 #pragma unroll
@@ -331,6 +369,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_cons
         a.sl[sl].out[(u64(img) * N + n) * a.OHW + rem] = tile[nq * kT3Rows + mloc];
       }
     }
+    if (tre) g_tc3_trace[kT3TraceRows - 1][1] = clock64();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -519,6 +558,11 @@ bool ring_gemm_tc3_try(Session& s, const GemmArgs& a) {
     P.fk = FastDiv(a.ed.g.k);
   }
   if (a.col2im) P.fohw = FastDiv(a.OHW);
+  static const int trace = [] {
+    const char* e = std::getenv("MPCG_TC3_TRACE");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  P.trace = trace;
   const uintptr_t ea = reinterpret_cast<uintptr_t>(P.E);
   P.vec = (a.K % 4 == 0 && ea % 32 == 0) ? 2 : (a.K % 2 == 0 && ea % 16 == 0) ? 1 : 0;
   const u64 wbytes = u64(ntiles) * P.nkb * 3 * 8 * kT3A;
@@ -538,6 +582,11 @@ bool ring_gemm_tc3_try(Session& s, const GemmArgs& a) {
   probe_end(s.stream, pe);
   s.check();
   return true;
+}
+
+void tc3_trace_read(unsigned long long* out, int n) {
+  const int m = n < kT3TraceRows * 8 ? n : kT3TraceRows * 8;
+  MPCG_CUDA(cudaMemcpyFromSymbol(out, g_tc3_trace, sizeof(unsigned long long) * size_t(m)));
 }
 
 }  // namespace mpcg

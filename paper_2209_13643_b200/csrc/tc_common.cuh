@@ -248,6 +248,25 @@ __device__ __forceinline__ void transpose8_store(const u64 (&v)[kVW], char* base
     *reinterpret_cast<uint2*>(base + (p + 4) * plane + off) = make_uint2(hi[0][p], hi[1][p]);
   }
 }
+// Four 8-column TMEM loads in flight, one wait: the wait names the 32 destination registers so
+// the compiler cannot consume them before the loads have landed.
+__device__ __forceinline__ void tmem_ld4x8(u32 a0, u32 a1, u32 a2, u32 a3, u32 (&r)[32]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const u32 ad = i == 0 ? a0 : i == 1 ? a1 : i == 2 ? a2 : a3;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[8 * i]), "=r"(r[8 * i + 1]), "=r"(r[8 * i + 2]), "=r"(r[8 * i + 3]), "=r"(r[8 * i + 4]),
+                   "=r"(r[8 * i + 5]), "=r"(r[8 * i + 6]), "=r"(r[8 * i + 7])
+                 : "r"(ad));
+  }
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+                 "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+                 "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
 
 }  // namespace
 }  // namespace mpcg
