@@ -266,6 +266,21 @@ def main():
     same_gpu = world > 1 and os.environ.get("MPCG_SAME_GPU") == "1"
     transport = "socket" if same_gpu else "nccl"
     device = 0 if same_gpu else local_rank
+    nccl_note = None
+    if world > 1 and transport == "nccl":
+        # every rank must be able to load NCCL before any enters ncclCommInitRank (a rank that
+        # cannot would leave its peer blocked in the init); otherwise all ranks use the socket link
+        try:
+            mp.nccl_unique_id()
+            ok = 1
+        except Exception as e:  # noqa: BLE001
+            ok, nccl_note = 0, f"NCCL unavailable on rank {rank}: {e}"
+        oks = [None] * world
+        dist.all_gather_object(oks, ok)
+        if not all(oks):
+            transport = "socket"
+            print(f"mpcg: falling back to the socket link ({nccl_note or 'NCCL unavailable on a peer rank'})",
+                  file=sys.stderr, flush=True)
     n_made = [0]
 
     def make_session():
