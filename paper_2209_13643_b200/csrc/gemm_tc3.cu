@@ -60,6 +60,7 @@ struct Tc3Args {
   FastDiv fkk, fk;            // deferred conv eps: k*k and k
   FastDiv fohw;               // col2im epilogue: OH*OW
   int trace = 0;
+  int mfast = 0;              // grid x = M tiles (see the kernel)
 };
 
 // gemm_epilogue's value (+-r_C, truncation, bias) without the store.
@@ -169,7 +170,11 @@ __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_cons
   const GemmArgs& a = P.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const u32 M = a.M, N = a.N, K = a.K;
-  const u32 ntile = blockIdx.x, m0 = blockIdx.y * kT3Rows, n0 = ntile * 64;
+  // grid: (N tile, M tile) — the CTAs of one M tile run together (their gathered / loaded L
+  // rows shared in L2) — or, with P.mfast, (M tile, N tile): the CTAs in flight share one N
+  // tile's weight images (large-N layers, where all images would not stay in L2 together)
+  const u32 ntile = P.mfast ? blockIdx.y : blockIdx.x;
+  const u32 m0 = (P.mfast ? blockIdx.x : blockIdx.y) * kT3Rows, n0 = ntile * 64;
   const u32 nst = P.nkb * 3;
 
   if (tid == 0) {
@@ -578,7 +583,13 @@ bool ring_gemm_tc3_try(Session& s, const GemmArgs& a) {
   }
   cudaEvent_t pe;
   probe_begin(s.stream, &pe);
-  launch_pdl(ring_gemm_tc3, dim3(ntiles, mtiles, 1), dim3(kT3Threads), size_t(kT3Stages) * kT3Stage, s.stream, P);
+  static const u32 mfast_min = [] {  // N tiles from which the grid runs M tiles fastest
+    const char* e = std::getenv("MPCG_TC3_MFAST");
+    return e ? u32(std::atoi(e)) : 1000u;
+  }();
+  P.mfast = ntiles >= mfast_min ? 1 : 0;
+  const dim3 grid = P.mfast ? dim3(mtiles, ntiles, 1) : dim3(ntiles, mtiles, 1);
+  launch_pdl(ring_gemm_tc3, grid, dim3(kT3Threads), size_t(kT3Stages) * kT3Stage, s.stream, P);
   probe_end(s.stream, pe);
   s.check();
   return true;
