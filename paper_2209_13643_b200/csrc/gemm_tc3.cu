@@ -365,13 +365,21 @@ __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_cons
       // consecutive words of one output plane instead of 32 planes one word each.
       asm volatile("bar.sync 1, %0;" ::"r"(4 * kT3Groups * 32) : "memory");
       const u64* tile = reinterpret_cast<const u64*>(smem);
-      for (u32 e = u32(tid); e < 2u * 64u * kT3Rows; e += 4 * kT3Groups * 32) {
-        const u32 mloc = e % kT3Rows, nq = e / kT3Rows;  // nq = party*64 + column
-        const u32 party = nq / 64, n = n0 + nq % 64, mm = m0 + mloc;
-        if (n >= N || mm >= M) continue;
-        const int sl = party == 0 ? P.p0slot : 1 - P.p0slot;
+      // element e = tid + 512 i: row mloc = tid % 64 is fixed per thread (512 % 64 == 0), so the
+      // image / position decode is done once; the (party, column) index advances by 8 per step
+      constexpr u32 kEpiThreads = 4 * kT3Groups * 32;
+      static_assert(kEpiThreads % kT3Rows == 0, "epilogue row mapping");
+      const u32 mloc = u32(tid) % kT3Rows, mm = m0 + mloc;
+      if (mm < M) {
         const u32 mg = mm + a.row0, img = P.fohw.div(mg), rem = mg - img * a.OHW;
-        a.sl[sl].out[(u64(img) * N + n) * a.OHW + rem] = tile[nq * kT3Rows + mloc];
+        u64* const out0 = a.sl[P.p0slot].out;
+        u64* const out1 = a.sl[1 - P.p0slot].out;
+        const u64 ibase = u64(img) * N;
+#pragma unroll 4
+        for (u32 nq = u32(tid) / kT3Rows; nq < 128; nq += kEpiThreads / kT3Rows) {
+          const u32 n = n0 + (nq & 63u);
+          if (n < N) (nq < 64 ? out0 : out1)[(ibase + n) * a.OHW + rem] = tile[nq * kT3Rows + mloc];
+        }
       }
     }
     if (tre) g_tc3_trace[kT3TraceRows - 1][1] = clock64();
