@@ -304,8 +304,12 @@ void socket_reap(Session& s, bool all) {
 namespace {
 constexpr u32 kFlagRing = 1u << 16;
 
-__device__ __forceinline__ u64 flag_value(u64 base, const u64* iter, const u64* delta) {
-  return base + 1 + (iter ? (*iter - 1) * *delta : 0);
+// The sequence number of a collective in this run: the baked capture-time number plus one run's
+// worth of collectives per replay after the first. Both the flag SLOT and its value derive from
+// it, so a collective posted in replay r and waited in replay r+1 (the pipelined executor's
+// wrap-around weight-side opening) meets in the same slot.
+__device__ __forceinline__ u64 run_seq(u64 base, const u64* iter, const u64* delta) {
+  return base + (iter ? (*iter - 1) * *delta : 0);
 }
 __global__ void p2p_push_kernel(const u64* __restrict__ src, u64* __restrict__ dst, u64 n) {
   const u64 stride = u64(gridDim.x) * blockDim.x;
@@ -319,19 +323,31 @@ __global__ void p2p_push_kernel(const u64* __restrict__ src, u64* __restrict__ d
     for (u64 j = i; j < n; j += stride) dst[j] = src[j];
   }
 }
-__global__ void p2p_signal_kernel(u64* flag, u64 base, const u64* iter, const u64* delta) {
-  const u64 v = flag_value(base, iter, delta);
+__device__ __forceinline__ void flag_release(u64* flag, u64 v) {
   __threadfence_system();
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(v) : "memory");
 }
-__global__ void p2p_wait_kernel(const u64* flag, u64 base, const u64* iter, const u64* delta) {
-  const u64 v = flag_value(base, iter, delta);
+__device__ __forceinline__ void flag_acquire(const u64* flag, u64 v) {
   for (;;) {
     u64 f;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(flag) : "memory");
     if (f >= v) break;
     __nanosleep(256);
   }
+}
+// collective flags: ring[run_seq % kFlagRing] = run_seq + 1 (monotonic, never reset)
+__global__ void p2p_signal_kernel(u64* ring, u64 base, const u64* iter, const u64* delta) {
+  const u64 s = run_seq(base, iter, delta);
+  flag_release(ring + s % kFlagRing, s + 1);
+}
+__global__ void p2p_wait_kernel(const u64* ring, u64 base, const u64* iter, const u64* delta) {
+  const u64 s = run_seq(base, iter, delta);
+  flag_acquire(ring + s % kFlagRing, s + 1);
+}
+// end-of-replay barrier word (after the ring): value = replay index (*iter)
+__global__ void p2p_barrier_kernel(u64* peer_word, const u64* own_word, const u64* iter) {
+  flag_release(peer_word, *iter);
+  flag_acquire(own_word, *iter);
 }
 }  // namespace
 
@@ -424,7 +440,7 @@ void p2p_post(Session& s, Open& o) {
     p2p_push_kernel<<<unsigned(blocks), 256, 0, s.comm_stream>>>(o.own(0), peer_inbox, o.n);
     MPCG_CUDA(cudaGetLastError());
   }
-  p2p_signal_kernel<<<1, 1, 0, s.comm_stream>>>(L.flags[1 - me] + o.seq % kFlagRing, o.seq, it, dl);
+  p2p_signal_kernel<<<1, 1, 0, s.comm_stream>>>(L.flags[1 - me], o.seq, it, dl);
   MPCG_CUDA(cudaGetLastError());
   g_launches.fetch_add(o.n ? 2 : 1);
 }
@@ -434,7 +450,7 @@ void p2p_wait(Session& s, const Open& o) {
   const int me = s.party_of[0];
   const u64* it = s.cap.active ? s.cap.iter : nullptr;
   const u64* dl = s.cap.active ? s.cap.seqd : nullptr;
-  p2p_wait_kernel<<<1, 1, 0, s.stream>>>(L.flags[me] + o.seq % kFlagRing, o.seq, it, dl);
+  p2p_wait_kernel<<<1, 1, 0, s.stream>>>(L.flags[me], o.seq, it, dl);
   MPCG_CUDA(cudaGetLastError());
   g_launches.fetch_add(1);
 }
@@ -444,18 +460,11 @@ void p2p_wait(Session& s, const Open& o) {
 void p2p_replay_barrier(Session& s) {
   P2PLink& L = *s.p2p_link;
   const int me = s.party_of[0];
-  // value = replay index + 1 on both sides: base 0, delta 1 -> (*iter - 1) * 1 + 1 = *iter
-  static u64* one = nullptr;
-  if (!one) {
-    MPCG_CUDA(cudaMallocManaged(&one, sizeof(u64)));
-    *one = 1;
-  }
   // both parties' comm streams are joined into the capture at end_capture: order the signal
   // behind everything this party enqueued in the replay (the compute stream)
-  p2p_signal_kernel<<<1, 1, 0, s.stream>>>(L.flags[1 - me] + kFlagRing, 0, s.cap.iter, one);
-  p2p_wait_kernel<<<1, 1, 0, s.stream>>>(L.flags[me] + kFlagRing, 0, s.cap.iter, one);
+  p2p_barrier_kernel<<<1, 1, 0, s.stream>>>(L.flags[1 - me] + kFlagRing, L.flags[me] + kFlagRing, s.cap.iter);
   MPCG_CUDA(cudaGetLastError());
-  g_launches.fetch_add(2);
+  g_launches.fetch_add(1);
 }
 
 }  // namespace mpcg

@@ -144,25 +144,21 @@ def test_p2p_device_flag_link_matches_reference(name, mode, weights, it):
     assert sess[0].stats(0) == sess[1].stats(0)
 
 
-@pytest.mark.parametrize("name,it", [("mlp", 2), ("lenet5", 1)])
-def test_p2p_link_graph_replays(name, it):
-    """Each party captures its own inference into a CUDA graph (flag values follow the replay
-    counter); concurrent replays of the two graphs reproduce the reference iteration by
-    iteration."""
+@pytest.mark.parametrize("name,mode", [("mlp", "pipelined"), ("lenet5", "pipelined"), ("lenet5", "blocking")])
+def test_p2p_link_graph_replays(name, mode):
+    """Each party captures its own inference into a CUDA graph (flag slots and values follow the
+    replay counter); three concurrent replays of the two graphs reproduce iteration 4 of the
+    two-slot session word for word — including the pipelined executor's weight-side opening
+    that one replay posts and the next one waits for."""
     import paper_2209_13643_b200 as mp
     g = mp.ModelGraph.from_json(os.path.join(ROOT, "configs", name + ".json"))
-    m = np.load(os.path.join(ROOT, "tests", "golden", f"model_{name}_pipelined_private_it{it}.npz"))
-    iters = max(it, 2)
-    (z0, z1), _ = _run_pair(mp, g, "pipelined", "private", iters, kind="p2p", graph=True)
-    if it == iters:
-        assert np.array_equal(z0.reshape(-1), m["z0"].reshape(-1))
-        assert np.array_equal(z1.reshape(-1), m["z1"].reshape(-1))
-    else:  # compare replay 1 (= iteration 2) with eager two-slot iteration 2
-        s = mp.Session(device=0, n_local=2, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
-        ex = mp.SecureExecutor(s, g, pipelined=True)
-        ex.deal_weights(mp.init_weights(g, 12), 1)
-        x = s.deal_input(mp.demo_input(g, 13), 2)
-        for _ in range(iters):
-            ze = ex.run(x).numpy()
-        assert np.array_equal(z0.reshape(-1), ze[0].reshape(-1))
-        assert np.array_equal(z1.reshape(-1), ze[1].reshape(-1))
+    iters = 4
+    (z0, z1), _ = _run_pair(mp, g, mode, "private", iters, kind="p2p", graph=True)
+    s = mp.Session(device=0, n_local=2, seed=1, mask_seed=1 ^ PHI, frac_bits=g.frac_bits)
+    ex = mp.SecureExecutor(s, g, pipelined=mode == "pipelined")
+    ex.deal_weights(mp.init_weights(g, 12), 1)
+    x = s.deal_input(mp.demo_input(g, 13), 2)
+    for _ in range(iters):
+        ze = ex.run(x).numpy()
+    assert np.array_equal(z0.reshape(-1), ze[0].reshape(-1))
+    assert np.array_equal(z1.reshape(-1), ze[1].reshape(-1))
