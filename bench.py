@@ -456,6 +456,7 @@ def main():
         finally:
             api.set_pair_eval(True)
         lb_ms = loopback_ms(mp, g, weights, x_global, a, thr, link, seed)
+        p2p_ms = loopback_ms(mp, g, weights, x_global, a, thr, link, seed, kind="p2p")
         colocation = {
             "pair_evaluated": {"ms_per_step": ms_step, "inferences_per_s": B / (ms_step / 1e3),
                                "path": "one thread per element evaluates both local party slots; opened values "
@@ -466,7 +467,11 @@ def main():
             "loopback_one_party_sessions": {"ms_per_step": lb_ms, "inferences_per_s": B / (lb_ms / 1e3),
                                             "path": "two n_local=1 sessions (party 0, party 1) on two host threads, "
                                                     "loopback link (device copies in place of NCCL send/recv), eager "
-                                                    "launches; wall clock per step after a stream sync"}}
+                                                    "launches; wall clock per step after a stream sync"},
+            "p2p_one_party_sessions": {"ms_per_step": p2p_ms, "inferences_per_s": B / (p2p_ms / 1e3),
+                                       "path": "two n_local=1 sessions on two host threads over the device-flag P2P "
+                                               "link (peer stores + flags), each party's inference one CUDA-graph "
+                                               "replay, both parties sharing cuda:0; wall clock per step"}}
 
     if rank != 0:
         if dist:
@@ -576,12 +581,16 @@ def main():
         dist.destroy_process_group()
 
 
-def loopback_ms(mp, g, weights, x_global, a, thr, link, seed):
-    """Two single-party sessions on cuda:0 driven by two host threads, linked in-process."""
+def loopback_ms(mp, g, weights, x_global, a, thr, link, seed, kind="loopback"):
+    """Two single-party sessions on cuda:0 driven by two host threads, linked in-process: the
+    loopback link (eager launches) or the device-flag P2P link (each party one graph replay)."""
     import threading
     sess = [mp.Session(device=0, n_local=1, party=p, seed=seed, mask_seed=seed ^ PHI, frac_bits=g.frac_bits)
             for p in (0, 1)]
-    sess[0].connect_loopback(sess[1])
+    if kind == "p2p":
+        sess[0].connect_p2p(sess[1])
+    else:
+        sess[0].connect_loopback(sess[1])
     if link:
         for s in sess:
             s.set_link(*link)
@@ -596,13 +605,19 @@ def loopback_ms(mp, g, weights, x_global, a, thr, link, seed):
                                    chunks=a.chunks, chunk_threshold=thr, linear_chunks=a.linear_chunks)
             ex.deal_weights(weights, seed)
             x = s.deal_input(x_global, seed + 1)
-            for _ in range(2):
+            if kind == "p2p":
                 ex.run(x)
+                ex.capture(x)
+                step = ex.replay
+            else:
+                step = lambda: ex.run(x)  # noqa: E731
+            for _ in range(2):
+                step()
             s.sync()
             go.wait()
             t0 = time.perf_counter()
             for _ in range(steps):
-                ex.run(x)
+                step()
             s.sync()
             walls[p] = (time.perf_counter() - t0) / steps
             del ex
@@ -616,7 +631,7 @@ def loopback_ms(mp, g, weights, x_global, a, thr, link, seed):
     for t in th:
         t.join()
     if err:
-        raise RuntimeError("loopback measurement failed: " + err[0])
+        raise RuntimeError(kind + " measurement failed: " + err[0])
     return max(walls) * 1e3
 
 
