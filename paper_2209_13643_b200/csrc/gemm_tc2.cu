@@ -54,6 +54,9 @@ struct Tc2Args {
   const char* Lpk[2] = {nullptr, nullptr};  // packed left operand (multi-N-tile shapes) or null
   u64 Lpk_b[2] = {0, 0};
   u32 lmask[2] = {0, 0};  // segments whose left operand is in Lpk (all: fully packed; else hybrid)
+  // packed-left image layout per slot: segments per K block in the image and this slot's first
+  // segment in it (party 1 may read E and r_A from party 0's image: lnpk 3, lseg0 1)
+  u32 lnpk[2] = {0, 0}, lseg0[2] = {0, 0};
   u32 nkb = 0;                              // K blocks of 32
   int vec = 0;                              // L row loads: 2 = 32-byte, 1 = 16-byte, 0 = scalar
   u32 ksplit = 1, kbper = 0;                // split-K over K blocks (partials summed by the epilogue kernel)
@@ -363,7 +366,8 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
       const char* Rb = P.Rpk[slot] + u64(b) * P.Rpk_b[slot] +
                        (u64(ntile) * P.nkb + kb0) * u64(nseg) * 8 * kB;
       const char* Lb =
-          lm ? P.Lpk[slot] + u64(b) * P.Lpk_b[slot] + (u64(blockIdx.y) * P.nkb + kb0) * u64(npk) * 8 * kA : nullptr;
+          lm ? P.Lpk[slot] + u64(b) * P.Lpk_b[slot] + (u64(blockIdx.y) * P.nkb + kb0) * u64(P.lnpk[slot]) * 8 * kA
+             : nullptr;
       for (u32 it = 0; it < nst; ++it) {
         const int stg = int(it % kStages);
         if (it >= kStages) mbar_wait(&empty[stg], ((it / kStages) & 1) ^ 1);
@@ -372,7 +376,9 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
         const bool pl = (lm >> g) & 1u;
         mbar_arrive_tx(&full[stg], 8 * kB + (pl ? 8 * kA : 0));
         bulk_g2s(sA + 8 * kA, Rb + u64(it) * 8 * kB, 8 * kB, &full[stg]);
-        if (pl) bulk_g2s(sA, Lb + (u64(kr) * npk + __popc(lm & ((1u << g) - 1))) * 8 * kA, 8 * kA, &full[stg]);
+        if (pl)
+          bulk_g2s(sA, Lb + (u64(kr) * P.lnpk[slot] + P.lseg0[slot] + __popc(lm & ((1u << g) - 1))) * 8 * kA, 8 * kA,
+                   &full[stg]);
       }
     }
   } else {
@@ -584,6 +590,24 @@ __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows
   }
 }
 
+// The pair-evaluated Beaver combine's tensor-core operand pattern (beaver_combine): party 0's
+// slot [A, E, r_A] and party 1's [E, r_A] on one dealer stream; returns party 0's slot or -1.
+int pair_combine_p0(const GemmArgs& a) {
+  if (a.nslots != 2) return -1;
+  int p0 = -1;
+  for (int i = 0; i < 2; ++i)
+    if (a.sl[i].nseg == 3) p0 = i;
+  if (p0 < 0 || a.sl[1 - p0].nseg != 2) return -1;
+  const GemmSlotArgs& S0 = a.sl[p0];
+  const GemmSlotArgs& S1 = a.sl[1 - p0];
+  const bool e0 = S0.lk[1] == kOpMem || S0.lk[1] == kOpSum, e1 = S1.lk[0] == kOpMem || S1.lk[0] == kOpSum;
+  if (S0.lk[0] != kOpA || !e0 || S0.lk[2] != kOpRA || !e1 || S1.lk[1] != kOpRA) return -1;
+  if (S0.aoff != S1.aoff || S0.sL[0] != S1.sL[0] || S0.mm.key != S1.mm.key || S0.mm.kp != S1.mm.kp ||
+      S0.mm.pool != S1.mm.pool || S0.mm.prA != S1.mm.prA)
+    return -1;
+  return p0;
+}
+
 template <int BR>
 void launch_pack(Session& s, const GemmArgs& a, bool left, u32 rows, u32 nbatch, u32 nkb, char* out0, char* out1,
                  u32 mask0 = ~0u, u32 mask1 = ~0u) {
@@ -636,11 +660,25 @@ void launch_tc2(Session& s, const GemmArgs& a, int packL) {
     for (int g = 0; g < a.sl[i].nseg; ++g) rbatched |= a.sl[i].sR[g] != 0;
   const u32 rb = rbatched ? a.nbatch : 1;
   std::vector<std::shared_ptr<Block>> keep;
+  // Fully packed pair combine: party 1's left segments (E, r_A) are party 0's segments 1 and 2
+  // (the opened E and the dealer's r_A are the same values for both slots), so party 1 reads
+  // party 0's image and only one image is packed (MPCG_TC2_SHAREL=0: one per slot).
+  int share_slot = -1;
+  {
+    static const bool share_on = [] {
+      const char* e = std::getenv("MPCG_TC2_SHAREL");
+      return !(e && e[0] == '0');
+    }();
+    const int p0 = packL == 1 && share_on ? pair_combine_p0(a) : -1;
+    if (p0 >= 0) share_slot = 1 - p0;
+  }
+  // the shared slot must come after party 0's image is allocated
   {
     ClassScope pack_scope(kClsOther, 0);  // the roofline probe times the GEMM kernel itself
     char* rp[2] = {nullptr, nullptr};
     char* lp[2] = {nullptr, nullptr};
-    for (int i = 0; i < a.nslots; ++i) {
+    for (int ii = 0; ii < a.nslots; ++ii) {
+      const int i = share_slot == 0 ? 1 - ii : ii;  // the image owner (party 0) first
       const u64 rbytes = u64(ntiles) * P.nkb * a.sl[i].nseg * 8 * BN * kKB;
       auto blk = s.raw((rbytes * rb + 7) / 8);
       keep.push_back(blk);
@@ -653,6 +691,16 @@ void launch_tc2(Session& s, const GemmArgs& a, int packL) {
         if (packL == 1 || (packL == 2 && k != kOpMem && k != kOpSum)) lmask |= 1u << g;
       }
       P.lmask[i] = lmask;
+      P.lnpk[i] = u32(__builtin_popcount(lmask));
+      P.lseg0[i] = 0;
+      if (lmask && i == share_slot) {  // reads party 0's image (E, r_A are the same values)
+        P.lnpk[i] = P.lnpk[1 - i];
+        P.lseg0[i] = 1;
+        P.Lpk[i] = P.Lpk[1 - i];
+        P.Lpk_b[i] = P.Lpk_b[1 - i];
+        lp[i] = nullptr;
+        continue;
+      }
       if (lmask) {
         const u64 lbytes = u64(mtiles) * P.nkb * __builtin_popcount(lmask) * 8 * kM * kKB;
         auto lb = s.raw((lbytes * a.nbatch + 7) / 8);
@@ -664,7 +712,8 @@ void launch_tc2(Session& s, const GemmArgs& a, int packL) {
     }
     launch_pack<BN>(s, a, false, a.N, rb, P.nkb, rp[0], rp[1]);
     if (P.lmask[0] | P.lmask[1])
-      launch_pack<kM>(s, a, true, a.M, a.nbatch, P.nkb, lp[0], lp[1], P.lmask[0], P.lmask[1]);
+      launch_pack<kM>(s, a, true, a.M, a.nbatch, P.nkb, lp[0], lp[1], share_slot == 0 ? 0u : P.lmask[0],
+                      share_slot == 1 ? 0u : P.lmask[1]);
   }
   // vector width of the L row loads: 2 = 32-byte (LDG.256), 1 = 16-byte, 0 = scalar
   auto aligned = [&](u32 vals) {

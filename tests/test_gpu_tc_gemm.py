@@ -37,7 +37,8 @@ def _run(mp, X, Y, tb, tag, chunks=1):
 @pytest.mark.parametrize("M,K,N", [(128, 32, 32), (256, 64, 64), (300, 100, 48), (128, 576, 64),
                                    (1000, 150, 16), (257, 1000, 130), (300, 25, 6), (129, 33, 7),
                                    (6400, 150, 16), (4000, 25, 6), (640, 96, 256), (512, 1152, 128),
-                                   (384, 64, 200), (260, 200, 320), (640, 96, 512)])  # N > 256: hybrid pack
+                                   (384, 64, 200), (260, 200, 320), (640, 96, 512),  # N > 256: hybrid pack
+                                   (300, 64, 640), (1024, 96, 768)])  # N > 512: fully packed, shared left image
 def test_tc_gemm_random(tc, M, K, N):
     from oracle import mpc_oracle as O
     r = O.CounterRng(M * 7 + K * 3 + N)
