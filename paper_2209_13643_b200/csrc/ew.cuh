@@ -174,23 +174,27 @@ template <class XF, class YF, class PF>
 void mul_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::string& tag, XF xf, YF yf,
             PF pf) {
   chunks = clamp_chunks(chunks, m);
-  std::vector<Open> opens(static_cast<size_t>(chunks));
+  const int acct = chunks;                                // lanes as the reference accounts them
+  const int xl = acct > 1 && s.fuse_lanes() ? 1 : acct;  // lanes launched (Session::fuse_lanes)
+  auto ltag = [&](int k) { return acct == 1 ? tag : tag + ".chunk" + std::to_string(k); };
+  std::vector<Open> opens(static_cast<size_t>(xl));
   const Pid2 pid = pids(s);
   // SURVEY 8(d) algorithmic bytes: beaver_mul = 2 x 16 B wire + 8 x (2 in + 1 out) = 56 B/elem/
   // party over build + combine (28 per launch). The opened wire (pair evaluation) moves less — the
   // 16 B opened pair is written and read once per element pair — but the roofline counts 8(d)'s.
   const bool opened = adder_opened_wire(s);
-  ClassScope cs(kClsBeaver, 28.0 * double(m / chunks) * s.n_local);
-  for (int k = 0; k < chunks; ++k) {
-    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
+  ClassScope cs(kClsBeaver, 28.0 * double(m / xl) * s.n_local);
+  for (int k = 0; k < xl; ++k) {
+    const auto rng_ = chunk_range(m, xl, k); const size_t lo = rng_.first, hi = rng_.second;
     opens[k] = s.begin_open(2 * (hi - lo), Reduce::Sum);
     MulBuild<XF, YF> mb{T, pid, own_ptrs(opens[k]), lo, hi - lo, xf, yf};
     mb.opened = opened;
     launch_ew(s.stream, s.n_local, hi - lo, mb);
-    s.post(opens[k], chunks == 1 ? tag : tag + ".chunk" + std::to_string(k));
+    if (xl == acct) s.post(opens[k], ltag(k));
+    else s.post_lanes(opens[k], m, acct, 2, ltag);
   }
-  for (int k = 0; k < chunks; ++k) {
-    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
+  for (int k = 0; k < xl; ++k) {
+    const auto rng_ = chunk_range(m, xl, k); const size_t lo = rng_.first, hi = rng_.second;
     s.wait(opens[k]);
     MulCombine<PF> mc{T, pid, as_const(own_ptrs(opens[k])), peer_ptrs(opens[k]), lo, hi - lo, pf};
     mc.opened = opened;
@@ -317,22 +321,26 @@ struct SqCombine {
 template <class XF, class PF>
 void square_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::string& tag, XF xf, PF pf) {
   chunks = clamp_chunks(chunks, m);
-  std::vector<Open> opens(static_cast<size_t>(chunks));
+  const int acct = chunks;
+  const int xl = acct > 1 && s.fuse_lanes() ? 1 : acct;  // lanes launched (Session::fuse_lanes)
+  auto ltag = [&](int k) { return acct == 1 ? tag : tag + ".chunk" + std::to_string(k); };
+  std::vector<Open> opens(static_cast<size_t>(xl));
   const Pid2 pid = pids(s);
   // beaver_square = 2 x 8 B wire + 8 x (1 in + 1 out) = 32 B/elem/party over build + combine
   // (the opened wire moves 24 B, the roofline counts 8(d)'s 32)
   const bool opened = adder_opened_wire(s);
-  ClassScope cs(kClsBeaver, 16.0 * double(m / chunks) * s.n_local);
-  for (int k = 0; k < chunks; ++k) {
-    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
+  ClassScope cs(kClsBeaver, 16.0 * double(m / xl) * s.n_local);
+  for (int k = 0; k < xl; ++k) {
+    const auto rng_ = chunk_range(m, xl, k); const size_t lo = rng_.first, hi = rng_.second;
     opens[k] = s.begin_open(hi - lo, Reduce::Sum);
     SqBuild<XF> b{T, pid, own_ptrs(opens[k]), lo, xf};
     b.opened = opened;
     launch_ew(s.stream, s.n_local, hi - lo, b);
-    s.post(opens[k], chunks == 1 ? tag : tag + ".chunk" + std::to_string(k));
+    if (xl == acct) s.post(opens[k], ltag(k));
+    else s.post_lanes(opens[k], m, acct, 1, ltag);
   }
-  for (int k = 0; k < chunks; ++k) {
-    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
+  for (int k = 0; k < xl; ++k) {
+    const auto rng_ = chunk_range(m, xl, k); const size_t lo = rng_.first, hi = rng_.second;
     s.wait(opens[k]);
     SqCombine<PF> c{T, pid, as_const(own_ptrs(opens[k])), peer_ptrs(opens[k]), lo, pf};
     c.opened = opened;
@@ -427,7 +435,8 @@ void square_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& t
   chunks = clamp_chunks(chunks, n);
   const int R = int(tr.size());
   const Pid2 pid = pids(s);
-  auto ctag = [&](int r, int k) { return chunks == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
+  const int acct_ = chunks;  // lanes as the reference accounts them (tags)
+  auto ctag = [&](int r, int k) { return acct_ == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
   using YF0 = decltype(yf_for(0));
   if (chunks == 1 && R <= 24 && n > 0 && s.persistent_ok(n)) {
     std::vector<Open> op(static_cast<size_t>(R));
@@ -445,6 +454,12 @@ void square_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& t
     s.check();
     return;
   }
+  const int acct = acct_;
+  if (chunks > 1 && s.fuse_lanes()) chunks = 1;  // lanes launched (Session::fuse_lanes)
+  auto post_r = [&](Open& o, int r, int k) {
+    if (chunks == acct) s.post(o, ctag(r, k));
+    else s.post_lanes(o, n, acct, 1, [&](int kk) { return ctag(r, kk); });
+  };
   std::vector<Open> hs(static_cast<size_t>(chunks));
   // R squares x 32 B/elem/party spread over the R+1 fused launches of a lane
   ClassScope cs(kClsBeaver, 32.0 * R / (R + 1) * double(n / chunks) * s.n_local);
@@ -454,7 +469,7 @@ void square_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& t
     SqBuild2<XF> b0{tr[0].ew, pid, own_ptrs(hs[k]), rg.first, x0};
     b0.opened = opened;
     launch_ew(s.stream, s.n_local, rg.second - rg.first, b0);
-    s.post(hs[k], ctag(0, k));
+    post_r(hs[k], 0, k);
   }
   using YF = decltype(yf_for(0));
   for (int r = 1; r <= R; ++r) {
@@ -471,7 +486,7 @@ void square_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& t
       launch_ew(s.stream, s.n_local, w, st);
       if (r < R) {
         hs[k] = std::move(next);
-        s.post(hs[k], ctag(r, k));
+        post_r(hs[k], r, k);
       }
     }
   }
@@ -543,7 +558,8 @@ void mul_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, 
   chunks = clamp_chunks(chunks, n);
   const int R = int(tr.size());
   const Pid2 pid = pids(s);
-  auto ctag = [&](int r, int k) { return chunks == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
+  const int acct_ = chunks;  // lanes as the reference accounts them (tags)
+  auto ctag = [&](int r, int k) { return acct_ == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
   using PV0 = decltype(pv_for(0));
   if (chunks == 1 && R <= 24 && n > 0 && s.persistent_ok(n)) {
     std::vector<Open> op(static_cast<size_t>(R));
@@ -562,6 +578,12 @@ void mul_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, 
     s.check();
     return;
   }
+  const int acct = acct_;
+  if (chunks > 1 && s.fuse_lanes()) chunks = 1;  // lanes launched (Session::fuse_lanes)
+  auto post_r = [&](Open& o, int r, int k) {
+    if (chunks == acct) s.post(o, ctag(r, k));
+    else s.post_lanes(o, n, acct, 2, [&](int kk) { return ctag(r, kk); });
+  };
   std::vector<Open> hs(static_cast<size_t>(chunks));
   // R multiplies x 56 B/elem/party spread over the R+1 fused launches of a lane
   ClassScope cs(kClsBeaver, 56.0 * R / (R + 1) * double(n / chunks) * s.n_local);
@@ -572,7 +594,7 @@ void mul_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, 
     MulBuild<XF, YF> b0{tr[0].ew, pid, own_ptrs(hs[k]), rg.first, w, x0, y0};
     b0.opened = opened;
     launch_ew(s.stream, s.n_local, w, b0);
-    s.post(hs[k], ctag(0, k));
+    post_r(hs[k], 0, k);
   }
   using PV = decltype(pv_for(0));
   for (int r = 1; r <= R; ++r) {
@@ -589,7 +611,7 @@ void mul_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, 
       launch_ew(s.stream, s.n_local, w, st);
       if (r < R) {
         hs[k] = std::move(next);
-        s.post(hs[k], ctag(r, k));
+        post_r(hs[k], r, k);
       }
     }
   }
@@ -689,7 +711,8 @@ void mixed_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr
   chunks = clamp_chunks(chunks, n);
   const int R = int(tr.size());
   const Pid2 pid = pids(s);
-  auto ctag = [&](int r, int k) { return chunks == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
+  const int acct_ = chunks;  // lanes as the reference accounts them (tags)
+  auto ctag = [&](int r, int k) { return acct_ == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
   auto words = [&](int r, size_t w) { return sq[r] ? w : 2 * w; };
   using PV0 = decltype(pv_for(0));
   if (chunks == 1 && R <= 24 && n > 0 && s.persistent_ok(n)) {  // one cooperative kernel
@@ -715,6 +738,12 @@ void mixed_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr
     s.check();
     return;
   }
+  const int acct = acct_;
+  if (chunks > 1 && s.fuse_lanes()) chunks = 1;  // lanes launched (Session::fuse_lanes)
+  auto post_r = [&](Open& o, int r, int k) {
+    if (chunks == acct) s.post(o, ctag(r, k));
+    else s.post_lanes(o, n, acct, words(r, 1), [&](int kk) { return ctag(r, kk); });
+  };
   std::vector<Open> hs(static_cast<size_t>(chunks));
   for (int k = 0; k < chunks; ++k) {
     const auto rg = chunk_range(n, chunks, k);
@@ -729,7 +758,7 @@ void mixed_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr
       b0.opened = opened;
       launch_ew(s.stream, s.n_local, w, b0);
     }
-    s.post(hs[k], ctag(0, k));
+    post_r(hs[k], 0, k);
   }
   using PV = decltype(pv_for(0));
   for (int r = 1; r <= R; ++r) {
@@ -747,7 +776,7 @@ void mixed_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr
       launch_ew(s.stream, s.n_local, w, st);
       if (r < R) {
         hs[k] = std::move(next);
-        s.post(hs[k], ctag(r, k));
+        post_r(hs[k], r, k);
       }
     }
   }

@@ -193,18 +193,22 @@ DT beaver_and(Session& s, const DT& x, const DT& y, const std::string& tag, int 
   t.mark_consumed();
   const size_t m = x.numel();
   chunks = clamp_chunks(chunks, m);
+  const int acct = chunks;
+  const int xl = acct > 1 && s.fuse_lanes() ? 1 : acct;  // lanes launched (Session::fuse_lanes)
+  auto ltag = [&](int k) { return acct == 1 ? tag : tag + ".chunk" + std::to_string(k); };
   DT z = s.alloc(x.shape, x.scale);
   const Pid2 pid = pids(s);
-  std::vector<Open> opens(static_cast<size_t>(chunks));
-  for (int k = 0; k < chunks; ++k) {
-    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
+  std::vector<Open> opens(static_cast<size_t>(xl));
+  for (int k = 0; k < xl; ++k) {
+    const auto rng_ = chunk_range(m, xl, k); const size_t lo = rng_.first, hi = rng_.second;
     opens[k] = s.begin_open(2 * (hi - lo), Reduce::Xor);
     launch_ew(s.stream, s.n_local, hi - lo,
               AndBuild<SrcMem, SrcMem>{t.ew, pid, own_ptrs(opens[k]), lo, hi - lo, SrcMem{cptrs(x)}, SrcMem{cptrs(y)}});
-    s.post(opens[k], chunks == 1 ? tag : tag + ".chunk" + std::to_string(k));
+    if (xl == acct) s.post(opens[k], ltag(k));
+    else s.post_lanes(opens[k], m, acct, 2, ltag);
   }
-  for (int k = 0; k < chunks; ++k) {
-    const auto rng_ = chunk_range(m, chunks, k); const size_t lo = rng_.first, hi = rng_.second;
+  for (int k = 0; k < xl; ++k) {
+    const auto rng_ = chunk_range(m, xl, k); const size_t lo = rng_.first, hi = rng_.second;
     s.wait(opens[k]);
     launch_ew(s.stream, s.n_local, hi - lo,
               AndCombine{t.ew, pid, as_const(own_ptrs(opens[k])), peer_ptrs(opens[k]), ptrs(z), lo, hi - lo});
