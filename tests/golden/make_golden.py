@@ -62,7 +62,7 @@ MODELS = [
 
 
 SCALE_OPS = ["relu_r18", "pool_vgg1", "softmax_bert", "qk_bert", "av_bert", "gemm_fc6", "gemm_r18l4"]
-SCALE_MODELS = ["r18_l1conv", "r18_l2conv_s2", "r18_l3conv", "r18_l4conv", "vgg_fc6", "bert_ffn1", "bert_ffn2"]
+SCALE_MODELS = ["r18_conv1", "r18_l1conv", "r18_l2sc", "r18_l2conv_s2", "r18_l3conv", "r18_l4conv", "vgg_fc6", "bert_ffn1", "bert_ffn2"]
 
 
 def main_scale(src=None):

@@ -105,7 +105,7 @@ def test_op_at_baseline_scale(mp, G, name, seed, f, build, fn):
     _check(mp, G, name, z, s.stats(0))
 
 
-MODELS = ["r18_l1conv", "r18_l2conv_s2", "r18_l3conv", "r18_l4conv", "vgg_fc6", "bert_ffn1", "bert_ffn2"]
+MODELS = ["r18_conv1", "r18_l1conv", "r18_l2sc", "r18_l2conv_s2", "r18_l3conv", "r18_l4conv", "vgg_fc6", "bert_ffn1", "bert_ffn2"]
 
 
 @pytest.mark.parametrize("mode", ["blocking", "pipelined", "chunked"])
