@@ -728,6 +728,10 @@ void launch_tc2(Session& s, const GemmArgs& a, int packL) {
     return ok;
   };
   P.vec = aligned(4) ? 2 : aligned(2) ? 1 : 0;
+  static const bool wave_split = [] {
+    const char* e = std::getenv("MPCG_TC2_WAVESPLIT");
+    return !(e && e[0] == '0');
+  }();
   // split K when the tile grid cannot fill the SMs (small-M layers): >= 2 K blocks per split
   const u64 ctas = u64(ntiles) * mtiles * a.nslots * a.nbatch;
   u32 split = 1;
@@ -736,6 +740,22 @@ void launch_tc2(Session& s, const GemmArgs& a, int packL) {
     split = split > 16 ? 16 : split;
     const u32 maxs = P.nkb / 2 > 0 ? P.nkb / 2 : 1;
     split = split > maxs ? maxs : split;
+  } else if (wave_split) {
+    // wave quantisation (one resident CTA per SM): a grid of 1.3 waves idles a third of the
+    // last wave (BERT-base ffn2, 192 CTAs). Split K when it fills the waves >= 15% better and
+    // each split keeps >= 48 pipeline stages (shorter splits pay the CTA fill and the partials
+    // pass: BERT-base attention out, 24-36 stages per split, measured slower).
+    // MPCG_TC2_WAVESPLIT=0 disables.
+    const u64 sms = num_sms();
+    u32 maxseg = 1;
+    for (int i = 0; i < a.nslots; ++i) maxseg = u32(a.sl[i].nseg) > maxseg ? u32(a.sl[i].nseg) : maxseg;
+    auto eff = [&](u64 sp) { const u64 c = ctas * sp; return double(c) / double((c + sms - 1) / sms * sms); };
+    double best = eff(1);
+    for (u32 sp = 2; sp <= 4; ++sp)
+      if (P.nkb * maxseg / sp >= 48 && eff(sp) >= 1.15 * eff(1) && eff(sp) > best + 1e-9) {
+        best = eff(sp);
+        split = sp;
+      }
   }
   P.kbper = (P.nkb + split - 1) / split;
   P.ksplit = (P.nkb + P.kbper - 1) / P.kbper;
