@@ -533,6 +533,13 @@ def main():
                   "avg_launch_us": p_ms * 1e3 / p_launches, "units_per_launch": p_units / p_launches,
                   "traffic": (traffic.get(a.model, {}).get(cls) or {}).get("dram_bytes_per_launch"),
                   "note": notes[cls]})
+        # the ncu-captured launches are specific ones (e.g. conv1's ReLU at 8.4M elements), not the
+        # step's average launch: their own algorithmic bytes give the comparable ratio
+        t = traffic.get(a.model, {}).get(cls) or {}
+        if t.get("algorithmic_bytes_per_launch"):
+            r["traffic_captured"] = {k: t[k] for k in ("dram_bytes_per_launch", "algorithmic_bytes_per_launch",
+                                                      "launches") if k in t}
+            r["traffic_captured"]["ratio"] = t["dram_bytes_per_launch"] / t["algorithmic_bytes_per_launch"]
         rooflines.append(r)
     rooflines.sort(key=lambda r: -r["device_ms_per_step"])
     roof = dict(rooflines[0]) if rooflines else None  # the dominant class of the step
