@@ -276,7 +276,8 @@ void SecureExecutor::prepare(size_t i) {
   op.delta = std::move(d);
 }
 
-DT SecureExecutor::weight_matmul(size_t i, const DT& x, const ConvGeom* geom, bool col2im_out, Shape out_shape) {
+DT SecureExecutor::weight_matmul(size_t i, const DT& x, const ConvGeom* geom, bool col2im_out, Shape out_shape,
+                                 const DT* addend) {
   WeightOp& op = wops_[i];
   const u32 M = u32(op.x_shape[0]), K = u32(op.x_shape[1]);
   const DT& W = w_.at(op.wkey);
@@ -293,6 +294,8 @@ DT SecureExecutor::weight_matmul(size_t i, const DT& x, const ConvGeom* geom, bo
     ep.col2im = 1;
     ep.OHW = geom->OH * geom->OW;
   }
+  if (addend)  // a following residual add fused into the epilogue (run())
+    for (int sl = 0; sl < s_.n_local; ++sl) ep.addend[sl] = addend->s[sl];
   DT z = s_.alloc(out_shape, g_.frac_bits);
   if (public_) {  // local product, no triple, no opening (H/engine/executor.hpp:294-298)
     DT cols = x;
@@ -441,14 +444,14 @@ DT SecureExecutor::attention(const LayerSpec& l, const DT& x, const Shape& in_sh
   return reshape(out, Shape{B, T, d});
 }
 
-DT SecureExecutor::run_layer(const LayerSpec& l, const DT& x, const Shape& in_shape) {
+DT SecureExecutor::run_layer(const LayerSpec& l, const DT& x, const Shape& in_shape, const DT* addend) {
   switch (l.kind) {
     case LayerKind::Dense: {
       const size_t op = wop_index_.at(l.name + ".mm");
       Shape out_shape = in_shape;
       out_shape.back() = l.out;
       DT x2 = reshape(x, wops_[op].x_shape);
-      return reshape(weight_matmul(op, x2, nullptr, false, Shape{wops_[op].x_shape[0], l.out}), out_shape);
+      return reshape(weight_matmul(op, x2, nullptr, false, Shape{wops_[op].x_shape[0], l.out}, addend), out_shape);
     }
     case LayerKind::Conv2d: {
       const size_t N = in_shape[0], C = in_shape[1], H = in_shape[2], W = in_shape[3];
@@ -456,7 +459,7 @@ DT SecureExecutor::run_layer(const LayerSpec& l, const DT& x, const Shape& in_sh
       const size_t OW = (W + 2 * l.pad - l.kernel) / l.stride + 1;
       const size_t op = wop_index_.at(l.name + ".mm");
       ConvGeom g{u32(N), u32(C), u32(H), u32(W), u32(l.kernel), u32(l.stride), u32(l.pad), u32(OH), u32(OW)};
-      return weight_matmul(op, x, &g, true, Shape{N, l.out, OH, OW});
+      return weight_matmul(op, x, &g, true, Shape{N, l.out, OH, OW}, addend);
     }
     case LayerKind::Relu:
       return relu_shares(s_, x, l.name);
@@ -576,13 +579,39 @@ DT SecureExecutor::run(const DT& input) {
     if (wr.src[i] >= 0) last[size_t(wr.src[i])] = std::max(last[size_t(wr.src[i])], i);
     if (wr.other[i] >= 0) last[size_t(wr.other[i])] = std::max(last[size_t(wr.other[i])], i);
   }
+  // A conv / dense layer whose only reader is the residual add right after it takes the add's
+  // other operand as an epilogue addend (one pass over the output instead of a separate add
+  // kernel re-reading it; values identical, the add has no collective). MPCG_FUSE_RESIDUAL=0
+  // keeps the separate add.
+  static const bool fuse_res = [] {
+    const char* e = std::getenv("MPCG_FUSE_RESIDUAL");
+    return !(e && e[0] == '0');
+  }();
+  std::vector<int> fused_into(nl, -1);  // add layer j -> the linear layer that produced it
+  if (fuse_res)
+    for (size_t j = 1; j < nl; ++j) {
+      const LayerSpec& l = g_.layers[j];
+      const size_t i = j - 1;
+      const LayerKind k = g_.layers[i].kind;
+      if (l.kind != LayerKind::Add || (k != LayerKind::Conv2d && k != LayerKind::Dense)) continue;
+      if (!(wr.src[j] == int(i)) == !(wr.other[j] == int(i))) continue;  // exactly one operand is layer i
+      bool only = true;
+      for (size_t q = 0; q < nl; ++q)
+        if (q != j && (wr.src[q] == int(i) || wr.other[q] == int(i))) only = false;
+      if (only && shape_numel(shapes_[i]) == shape_numel(shapes_[j])) fused_into[j] = int(i);
+    }
   std::vector<DT> outs(nl);
   for (size_t i = 0; i < nl; ++i) {
     const LayerSpec& l = g_.layers[i];
     const DT& x = wr.src[i] < 0 ? input : outs[size_t(wr.src[i])];
     const Shape& xs = wr.src[i] < 0 ? g_.input : shapes_[size_t(wr.src[i])];
-    if (l.kind == LayerKind::Add) {  // residual: local share addition
+    if (l.kind == LayerKind::Add && fused_into[i] >= 0) {  // already added in the GEMM epilogue
+      outs[i] = outs[size_t(fused_into[i])];
+    } else if (l.kind == LayerKind::Add) {  // residual: local share addition
       outs[i] = add_t(s_, x, wr.other[i] < 0 ? input : outs[size_t(wr.other[i])]);
+    } else if (i + 1 < nl && fused_into[i + 1] == int(i)) {
+      const long o = wr.src[i + 1] == long(i) ? wr.other[i + 1] : wr.src[i + 1];
+      outs[i] = run_layer(l, x, xs, o < 0 ? &input : &outs[size_t(o)]);
     } else {
       outs[i] = run_layer(l, x, xs);
     }

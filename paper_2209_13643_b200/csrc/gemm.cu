@@ -745,6 +745,7 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
     const u64* F0 = (d.summed ? d.own(0) : d.own(i)) + rboff;
     const u64* F1 = d.summed ? nullptr : d.peer(i) + rboff;  // null: F summed at build time
     S.out = ep.col2im ? out[i] : out[i] + out_off;  // col2im scatters by global row (a.row0)
+    S.addend = ep.addend[i] ? (ep.col2im ? ep.addend[i] : ep.addend[i] + out_off) : nullptr;
     S.bias = ep.bias[i];
     S.ckey = t.mm.key;
     S.ckp = t.mm.kp;
@@ -816,6 +817,7 @@ void public_gemm(Session& s, const u64* const x[2], const u64* W, u64* const out
     S.L[0] = x[i];
     S.R[0] = W;
     S.out = out[i];
+    S.addend = ep.addend[i];
     S.bias = ep.bias[i];
   }
   ring_gemm_launch(s, a);

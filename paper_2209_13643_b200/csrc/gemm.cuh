@@ -34,6 +34,7 @@ struct GemmSlotArgs {
   u64 aoff = 0, boff = 0; // element offset of this call inside A / B (PRG index base)
   u64* out = nullptr;
   const u64* bias = nullptr;  // [N], added after truncation
+  const u64* addend = nullptr;  // fused residual add: same layout as out, added last (or null)
   int cterm = 0;              // +1 / -1: add / subtract the triple's r_C
   u64 ckey = 0, cbase = 0;    // r_C(idx) = drw(ckey, cbase + idx)
   const u64* ckp = nullptr;   // device key slot (graph replay)
@@ -59,6 +60,7 @@ struct GemmArgs {
 struct Epi {
   int trunc_bits = 0;
   const u64* bias[2] = {nullptr, nullptr};
+  const u64* addend[2] = {nullptr, nullptr};  // fused residual add (the layer's full output layout)
   int col2im = 0;
   u32 OHW = 1;
 };
@@ -112,9 +114,10 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& a, const GemmSlotA
   if (S.bias) v += S.bias[n];
   if (a.col2im) {
     const u32 mg = m + a.row0, img = mg / a.OHW, rem = mg - img * a.OHW;
-    S.out[(u64(img) * a.N + n) * a.OHW + rem] = v;
+    const u64 o = (u64(img) * a.N + n) * a.OHW + rem;
+    S.out[o] = S.addend ? v + __ldg(S.addend + o) : v;
   } else {
-    S.out[lin] = v;
+    S.out[lin] = S.addend ? v + __ldg(S.addend + lin) : v;
   }
 }
 

@@ -374,11 +374,29 @@ __global__ void __launch_bounds__(kT3Threads, 1) ring_gemm_tc3(const __grid_cons
         const u32 mg = mm + a.row0, img = P.fohw.div(mg), rem = mg - img * a.OHW;
         u64* const out0 = a.sl[P.p0slot].out;
         u64* const out1 = a.sl[1 - P.p0slot].out;
+        const u64* const add0 = a.sl[P.p0slot].addend;  // fused residual add (or null)
+        const u64* const add1 = a.sl[1 - P.p0slot].addend;
         const u64 ibase = u64(img) * N;
+        constexpr u32 kStep = kEpiThreads / kT3Rows, kIt = 128 / kStep;
+        if (add0 || add1) {  // fused residual add: every addend load in flight before the stores
+          u64 adv[kIt];
+#pragma unroll
+          for (u32 it = 0; it < kIt; ++it) {
+            const u32 nq = u32(tid) / kT3Rows + it * kStep, n = n0 + (nq & 63u);
+            const u64* const ad = nq < 64 ? add0 : add1;
+            adv[it] = (ad && n < N) ? __ldg(ad + (ibase + n) * a.OHW + rem) : 0;
+          }
+#pragma unroll
+          for (u32 it = 0; it < kIt; ++it) {
+            const u32 nq = u32(tid) / kT3Rows + it * kStep, n = n0 + (nq & 63u);
+            if (n < N) (nq < 64 ? out0 : out1)[(ibase + n) * a.OHW + rem] = tile[nq * kT3Rows + mloc] + adv[it];
+          }
+        } else {
 #pragma unroll 4
-        for (u32 nq = u32(tid) / kT3Rows; nq < 128; nq += kEpiThreads / kT3Rows) {
-          const u32 n = n0 + (nq & 63u);
-          if (n < N) (nq < 64 ? out0 : out1)[(ibase + n) * a.OHW + rem] = tile[nq * kT3Rows + mloc];
+          for (u32 nq = u32(tid) / kT3Rows; nq < 128; nq += kStep) {
+            const u32 n = n0 + (nq & 63u);
+            if (n < N) (nq < 64 ? out0 : out1)[(ibase + n) * a.OHW + rem] = tile[nq * kT3Rows + mloc];
+          }
         }
       }
     }
