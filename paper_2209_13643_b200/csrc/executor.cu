@@ -380,7 +380,7 @@ DT SecureExecutor::scale_and_rescale(const DT& x, double c) {
   return z;
 }
 
-DT SecureExecutor::attention(const LayerSpec& l, const DT& x, const Shape& in_shape) {
+DT SecureExecutor::attention(const LayerSpec& l, const DT& x, const Shape& in_shape, const DT* addend) {
   // H/engine/executor.hpp:332-362
   const size_t B = in_shape[0], T = in_shape[1], d = in_shape[2];
   const size_t heads = l.heads, dh = d / heads;
@@ -440,7 +440,7 @@ DT SecureExecutor::attention(const LayerSpec& l, const DT& x, const Shape& in_sh
       dst.p[slot][i] = sar64(src.p[slot][((u64(b) * H + h) * Tt + t) * DH + j], f);
     });
   }
-  DT out = weight_matmul(proj_op, merged, nullptr, false, Shape{B * T, d});
+  DT out = weight_matmul(proj_op, merged, nullptr, false, Shape{B * T, d}, addend);
   return reshape(out, Shape{B, T, d});
 }
 
@@ -471,7 +471,7 @@ DT SecureExecutor::run_layer(const LayerSpec& l, const DT& x, const Shape& in_sh
       return reshape(x, Shape{in_shape[0], rest});
     }
     case LayerKind::Attention:
-      return attention(l, x, in_shape);
+      return attention(l, x, in_shape, addend);
     case LayerKind::Softmax:
       return softmax_shares(s_, x, in_shape.back(), l.name);
     case LayerKind::MeanPool: {
@@ -579,7 +579,7 @@ DT SecureExecutor::run(const DT& input) {
     if (wr.src[i] >= 0) last[size_t(wr.src[i])] = std::max(last[size_t(wr.src[i])], i);
     if (wr.other[i] >= 0) last[size_t(wr.other[i])] = std::max(last[size_t(wr.other[i])], i);
   }
-  // A conv / dense layer whose only reader is the residual add right after it takes the add's
+  // A conv / dense / attention layer (its output projection) whose only reader is the residual add right after it takes the add's
   // other operand as an epilogue addend (one pass over the output instead of a separate add
   // kernel re-reading it; values identical, the add has no collective). MPCG_FUSE_RESIDUAL=0
   // keeps the separate add.
@@ -593,7 +593,8 @@ DT SecureExecutor::run(const DT& input) {
       const LayerSpec& l = g_.layers[j];
       const size_t i = j - 1;
       const LayerKind k = g_.layers[i].kind;
-      if (l.kind != LayerKind::Add || (k != LayerKind::Conv2d && k != LayerKind::Dense)) continue;
+      if (l.kind != LayerKind::Add || (k != LayerKind::Conv2d && k != LayerKind::Dense && k != LayerKind::Attention))
+        continue;
       if (!(wr.src[j] == int(i)) == !(wr.other[j] == int(i))) continue;  // exactly one operand is layer i
       bool only = true;
       for (size_t q = 0; q < nl; ++q)

@@ -112,7 +112,7 @@ class SecureExecutor {
   // x source: plain 2-D shares, or an NCHW tensor gathered by im2col when geom != null
   DT weight_matmul(size_t i, const DT& x, const struct ConvGeom* geom, bool col2im_out, Shape out_shape,
                    const DT* addend = nullptr);
-  DT attention(const LayerSpec& l, const DT& x, const Shape& in_shape);
+  DT attention(const LayerSpec& l, const DT& x, const Shape& in_shape, const DT* addend = nullptr);
   DT run_layer(const LayerSpec& l, const DT& x, const Shape& in_shape, const DT* addend = nullptr);
   DT scale_and_rescale(const DT& x, double c);
 
