@@ -150,7 +150,7 @@ struct ConvGeom {
 // activation shares and the dealer's A. mode 1 = dense rows x[a_off + m*K + k], 2 = im2col rows
 // of a convolution (global row a_off/K + m). The open is still posted and accounted.
 struct EpsDefer {
-  int mode = 0;
+  int mode = 0;  // 1 dense eps, 2 im2col eps (gemm_tc3.cu), 3 weight-side delta F = x0 + x1 - B (ring_gemv_pair)
   const u64* x0 = nullptr;
   const u64* x1 = nullptr;
   ConvGeom g{};

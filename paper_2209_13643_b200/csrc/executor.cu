@@ -270,7 +270,7 @@ void SecureExecutor::prepare(size_t i) {
   // fused in-device open of delta, on the same condition as eps's (weight_matmul)
   const size_t M = op.x_shape[0], K = op.x_shape[1];
   d.summed = beaver_combine_fuses_eps(s_, 1, u32(M), u32(nb / K), u32(K));
-  delta_build_mem(s_, t, W.s, nb, d);
+  if (!delta_defer(s_, d, W.s, u32(M), u32(nb / K), u32(K))) delta_build_mem(s_, t, W.s, nb, d);
   s_.post(d, op.tag + ".delta");
   op.triple = t;
   op.delta = std::move(d);

@@ -239,6 +239,118 @@ __global__ void __launch_bounds__(256) ring_gemv(GemmArgs a) {
   }
 }
 
+// Pair-evaluated form (both party slots on this device, one dealer stream): one thread per
+// column n evaluates BOTH slots' combines, so B and r_B are drawn and F is loaded once per
+// (k, n) instead of per slot (2 draws + 8 B instead of 3 + 16 B; the per-slot blocks also ran
+// a whole slot apart, so the second F read missed L2). Segment forms (beaver_combine):
+//   party 0: A*B + E*((B - r_B) + F) + (A - r_A)*F,   party 1: E*r_B + r_A*F
+// with the left values A, E, A - r_A, r_A of the staged K chunk in shared memory.
+template <int MR>
+__global__ void __launch_bounds__(256) ring_gemv_pair(GemmArgs a, int p0) {
+  __shared__ u64 Ls[4][MR][kGvKC];  // A, E, A - r_A, r_A
+  constexpr int kRG = MR < 4 ? MR : 4;
+  __shared__ u64 red[8][kRG][32];
+  pdl_enter();
+  const GemmSlotArgs& S0 = a.sl[p0];
+  const GemmSlotArgs& S1 = a.sl[1 - p0];
+  const u32 m0 = blockIdx.z * MR;
+  const u32 M = a.M, N = a.N, K = a.K;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u32 n = blockIdx.x * 32 + lane;
+  const u32 kb = blockIdx.y * a.kchunk, ke = min(K, kb + a.kchunk);
+  const u64* const Fo = S0.R[1];
+  const u64* const Fp = S0.R2[1];
+  u64 acc0[MR], acc1[MR];
+#pragma unroll
+  for (int m = 0; m < MR; ++m) acc0[m] = acc1[m] = 0;
+  for (u32 k0 = kb; k0 < ke; k0 += kGvKC) {
+    const u32 kc = min(u32(kGvKC), ke - k0);
+    __syncthreads();
+    for (u32 e = threadIdx.x; e < 4u * MR * kGvKC; e += 256) {
+      const u32 kk = e % kGvKC, m = (e / kGvKC) % MR, g = e / (kGvKC * MR);
+      u64 v = 0;
+      if (m0 + m < M && kk < kc) {
+        const u64 idx = u64(m0 + m) * K + k0 + kk;
+        v = g == 3 ? load_l(S1, 1, idx) : load_l(S0, int(g), idx);
+      }
+      Ls[g][m][kk] = v;
+    }
+    __syncthreads();
+    if (n >= N) continue;
+    for (u32 kk = u32(warp); kk < kc; kk += 8) {
+      const u64 idx = u64(k0 + kk) * N + n;
+      const u64 B = mm_B(S0.mm, S0.boff + idx), rB = mm_rB(S0.mm, S0.boff + idx);
+      const u64 F = Fp ? __ldg(Fo + idx) + __ldg(Fp + idx) - (a.fdefer ? B : 0) : __ldg(Fo + idx);
+      const u64 b0F = (B - rB) + F;
+#pragma unroll
+      for (int m = 0; m < MR; ++m) {
+        const u64 e = Ls[1][m][kk];
+        acc0[m] += Ls[0][m][kk] * B + e * b0F + Ls[2][m][kk] * F;
+        acc1[m] += e * rB + Ls[3][m][kk] * F;
+      }
+    }
+  }
+  const u64 per = u64(M) * N;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const u64* acc = q == 0 ? acc0 : acc1;
+    u64* const dst = a.acc[q == 0 ? p0 : 1 - p0];
+#pragma unroll
+    for (int mb = 0; mb < MR; mb += kRG) {
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < kRG; ++j) red[warp][j][lane] = acc[mb + j];
+      __syncthreads();
+      if (warp == 0 && n < N) {
+#pragma unroll
+        for (int j = 0; j < kRG; ++j) {
+          u64 v = 0;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) v += red[w][j][lane];
+          if (m0 + u32(mb + j) < M) dst[u64(blockIdx.y) * per + u64(m0 + mb + j) * N + n] = v;
+        }
+      }
+    }
+  }
+}
+
+// The pair-evaluated combine pattern of beaver_combine's non-tensor-core form on one dealer
+// stream: party 0's slot [A*B, E*(b0+F), a0*F], party 1's [E*r_B, r_A*F]; returns party 0's
+// slot or -1 (then the per-slot kernel runs).
+bool gemv_pair_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("MPCG_GEMV_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+int gemv_pair_pattern(const GemmArgs& a) {
+  if (!gemv_pair_on() || !pair_eval_enabled() || a.nslots != 2 || a.nbatch != 1) return -1;
+  int p0 = -1;
+  for (int i = 0; i < 2; ++i)
+    if (a.sl[i].nseg == 3) p0 = i;
+  if (p0 < 0 || a.sl[1 - p0].nseg != 2) return -1;
+  const GemmSlotArgs& S0 = a.sl[p0];
+  const GemmSlotArgs& S1 = a.sl[1 - p0];
+  const int ek = S0.lk[1];
+  if ((ek != kOpMem && ek != kOpSum) || S1.lk[0] != ek) return -1;
+  if (S0.lk[0] != kOpA || S0.lk[2] != kOpA0 || S1.lk[1] != kOpRA) return -1;
+  if (S0.rk[0] != kOpB || S0.rk[1] != kOpB0F || S0.rk[2] != kOpSum || S1.rk[0] != kOpRB || S1.rk[1] != kOpSum)
+    return -1;
+  // one opened E and one opened F for both slots (as (own, peer) of either slot)
+  auto same = [](const u64* x0, const u64* x1, const u64* y0, const u64* y1) {
+    return (x0 == y0 && x1 == y1) || (x1 && x0 == y1 && x1 == y0);
+  };
+  if (!same(S0.L[1], S0.L2[1], S1.L[0], S1.L2[0])) return -1;
+  if (S0.R[1] != S0.R[2] || S0.R2[1] != S0.R2[2] || !same(S0.R[1], S0.R2[1], S1.R[1], S1.R2[1])) return -1;
+  if (S0.aoff != S1.aoff || S0.boff != S1.boff || S0.sL[0] != S1.sL[0]) return -1;
+  if (S0.mm.key != S1.mm.key || S0.mm.kp != S1.mm.kp || S0.mm.pool != S1.mm.pool || S0.mm.pA != S1.mm.pA ||
+      S0.mm.prA != S1.mm.prA || S0.mm.pB != S1.mm.pB || S0.mm.prB != S1.mm.prB)
+    return -1;
+  return p0;
+}
+
 template <int MR>
 void launch_gemv(Session& s, GemmArgs a) {
   cudaStream_t st = s.stream;
@@ -247,7 +359,8 @@ void launch_gemv(Session& s, GemmArgs a) {
   // split K until ~16 blocks per SM (two full waves of 8 resident 256-thread blocks: the
   // per-(k, n) dealer draws are latency-bound chains, so the kernel needs every warp slot;
   // VGG fc6 1 x 25088 x 4096: 1.61 ms at ~3 blocks per SM), >= one staged chunk per split
-  const u64 base = u64(ncol) * a.nslots * mgrp;
+  const int p0 = gemv_pair_pattern(a);
+  const u64 base = u64(ncol) * (p0 >= 0 ? 1 : a.nslots) * mgrp;
   u32 split = u32((16 * u64(num_sms()) + base - 1) / base);
   const u32 maxsplit = (a.K + kGvKC - 1) / kGvKC;
   split = split > maxsplit ? maxsplit : (split < 1 ? 1 : split);
@@ -258,7 +371,10 @@ void launch_gemv(Session& s, GemmArgs a) {
   for (int i = 0; i < a.nslots; ++i) a.acc[i] = ws->ptr + i * per * a.ksplit;
   cudaEvent_t pe;
   probe_begin(st, &pe);
-  launch_pdl(ring_gemv<MR>, dim3(ncol, a.ksplit, a.nslots * mgrp), dim3(256), 0, st, a);
+  if (p0 >= 0)
+    launch_pdl(ring_gemv_pair<MR>, dim3(ncol, a.ksplit, mgrp), dim3(256), 0, st, a, p0);
+  else
+    launch_pdl(ring_gemv<MR>, dim3(ncol, a.ksplit, a.nslots * mgrp), dim3(256), 0, st, a);
   launch_pdl(gemm_splitk_epilogue, dim3(ew_blocks(per * a.nslots)), dim3(256), 0, st, a);
   probe_end(st, pe);
 }
@@ -353,6 +469,8 @@ void ring_gemm_launch(Session& s, const GemmArgs& a) {
   double macs = 0;
   for (int i = 0; i < a.nslots; ++i) macs += double(a.sl[i].nseg) * a.M * a.N * a.K * a.nbatch;
   ClassScope cs(kClsGemm, macs);
+  if (a.fdefer && !(gemv_eligible(a) && gemv_mode() != 0 && gemv_pair_pattern(a) >= 0))
+    throw Error(kInternalError, "deferred delta: the pair-evaluated GEMV did not take the combine");
   if (gemv_eligible(a) && gemv_mode() != 0) {
     if (a.M <= 1) launch_gemv<1>(s, a);
     else if (a.M <= 4) launch_gemv<4>(s, a);
@@ -715,6 +833,21 @@ bool beaver_combine_wants_aops(const Session& s, u32 nbatch, u32 M, u32 N, u32 K
 
 // The eps open can be fused into its build (Open::summed) when both slots are local and the
 // combine reads E as a GEMM operand (not through the A-operand path).
+bool delta_defer(Session& s, Open& o, const u64* const w[2], u32 M, u32 N, u32 K) {
+  static const bool on = [] {
+    const char* e = std::getenv("MPCG_DELTA_DEFER");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || !o.summed || s.n_local != 2 || s.cfg.link_bandwidth > 0 || !gemv_pair_on() || !pair_eval_enabled())
+    return false;
+  if (!(gemv_eligible_shape(M, 1, false, 0) && gemv_mode() != 0) || beaver_combine_wants_aops(s, 1, M, N, K))
+    return false;
+  o.defer.mode = 3;
+  o.defer.x0 = w[0];
+  o.defer.x1 = w[1];
+  return true;
+}
+
 bool beaver_combine_fuses_eps(const Session& s, u32 nbatch, u32 M, u32 N, u32 K) {
   return eps_fuse_enabled() && s.n_local == 2 && !beaver_combine_wants_aops(s, nbatch, M, N, K);
 }
@@ -742,8 +875,9 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
     const u64* E0 = e.summed ? e.own(0) : e.own(i);
     const u64* E1 = e.summed ? nullptr : e.peer(i);
     const int ek = e.summed ? kOpMem : kOpSum;  // E = own + peer, or already summed
-    const u64* F0 = (d.summed ? d.own(0) : d.own(i)) + rboff;
-    const u64* F1 = d.summed ? nullptr : d.peer(i) + rboff;  // null: F summed at build time
+    const u64* F0 = (d.defer.mode == 3 ? d.defer.x0 : d.summed ? d.own(0) : d.own(i)) + rboff;
+    const u64* F1 = d.defer.mode == 3 ? d.defer.x1 + rboff  // deferred: F = W0 + W1 - B in the GEMV
+                    : d.summed ? nullptr : d.peer(i) + rboff;  // null: F summed at build time
     S.out = ep.col2im ? out[i] : out[i] + out_off;  // col2im scatters by global row (a.row0)
     S.addend = ep.addend[i] ? (ep.col2im ? ep.addend[i] : ep.addend[i] + out_off) : nullptr;
     S.bias = ep.bias[i];
@@ -783,6 +917,22 @@ void beaver_combine(Session& s, const Triple& t, const Open& e, size_t a_off, si
     for (int g = 0; g < 3; ++g) {
       S.sL[g] = sL;
       S.sR[g] = sR;
+    }
+  }
+  if (d.defer.mode == 3) {  // F formed by the pair-evaluated GEMV (delta_defer)
+    a.fdefer = 1;
+    if (!(gemv_eligible(a) && gemv_mode() != 0 && gemv_pair_pattern(a) >= 0)) {  // not expected: build it
+      Open o = d;
+      o.defer = EpsDefer{};
+      const u64* const w[2] = {d.defer.x0, d.defer.x1};
+      delta_build_mem(s, t, w, nb, o);
+      a.fdefer = 0;
+      for (int i = 0; i < s.n_local; ++i)
+        for (int g = 0; g < a.sl[i].nseg; ++g)
+          if (a.sl[i].R2[g] == d.defer.x1 + rboff || a.sl[i].R2[g] == d.defer.x0 + rboff) {
+            a.sl[i].R[g] = d.own(0) + rboff;
+            a.sl[i].R2[g] = nullptr;
+          }
     }
   }
   if (e.defer.mode) {  // E is generated by the both-slots GEMM's producers (eps_defer)

@@ -55,6 +55,7 @@ struct GemmArgs {
   u64* acc[2] = {nullptr, nullptr};
   int vec16 = 0;  // every L (and transposed R) row start is 16-byte aligned (K even, bases aligned)
   EpsDefer ed{};  // E generated in the GEMM (gemm_tc3.cu only; ed.mode != 0)
+  int fdefer = 0;  // F = R + R2 - B: the weight-side delta open not built (ring_gemv_pair only)
 };
 
 struct Epi {
@@ -127,6 +128,9 @@ __global__ void gemm_splitk_epilogue(GemmArgs a);
 using splitk_epilogue_t = void (*)(GemmArgs);
 splitk_epilogue_t gemm_splitk_epilogue_fn();
 bool gemv_eligible_shape(u32 M, u32 nbatch, bool tb, int col2im);  // the small-M path takes it
+// Deferred weight-side delta: the summed delta open of a combine the pair-evaluated GEMV will
+// run is not built (o.defer.mode = 3); the GEMV forms F = W0 + W1 - B from the weight shares.
+bool delta_defer(Session& s, Open& o, const u64* const w[2], u32 M, u32 N, u32 K);
 // Small-M fused-segment path (ring_gemv): 1 = on (default), 0 = off (MPCG_GEMV=0).
 inline int& gemv_mode() {
   static int m = [] {
