@@ -1,8 +1,9 @@
 """The fused in-device opens must leave every output share word-identical to the two-payload
 forms: the eps open summed at build time (Open::summed, off with MPCG_EPS_FUSE=0) and the
 opened-value wire of pair-evaluated adder rounds (off with MPCG_PAIR_EVAL=0, which evaluates
-each party slot separately with its own payload). Runs each form in a subprocess (the knobs
-are read once)."""
+each party slot separately with its own payload), and the round-2 fusions (pair GEMV, deferred
+delta, fused residual adds, wave-fill split-K) against their unfused forms. Runs each form in a
+subprocess (the knobs are read once)."""
 import json
 import os
 import subprocess
@@ -40,8 +41,8 @@ print(json.dumps(out))
 ''' % ROOT
 
 
-def run(fuse, pair="1"):
-    env = dict(os.environ, MPCG_EPS_FUSE=fuse, MPCG_PAIR_EVAL=pair)
+def run(fuse, pair="1", **extra):
+    env = dict(os.environ, MPCG_EPS_FUSE=fuse, MPCG_PAIR_EVAL=pair, **extra)
     r = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     return json.loads(r.stdout.strip().splitlines()[-1])
@@ -52,6 +53,10 @@ def test_fused_opens_match_two_payloads():
     a, b, c = run("1"), run("0"), run("0", pair="0")
     assert a == b
     assert a == c
+    # the pair-evaluated GEMV with the deferred weight-side delta, the residual adds fused into
+    # the GEMM epilogues and the wave-fill split-K against their separate / per-slot forms
+    d = run("1", MPCG_GEMV_PAIR="0", MPCG_DELTA_DEFER="0", MPCG_FUSE_RESIDUAL="0", MPCG_TC2_WAVESPLIT="0")
+    assert a == d
 
 
 SCRIPT_LANES = r'''
