@@ -395,7 +395,7 @@ def main():
     # ---- roofline probes: device time of every launch of each kernel class (eager steps, CUDA
     # events on the session stream around each launch of the class)
     probes = {}
-    for cls in ("adder_round", "beaver", "chain", "gemm"):
+    for cls in ("adder_round", "beaver", "chain", "chain_reg", "gemm"):
         barrier(s)
         api.probe_start(cls)
         for _ in range(max(2, a.steps // 4)):
@@ -503,6 +503,10 @@ def main():
     hbm = peaks.get("hbm_gbs")
     hbm_peak = hbm or 6650.0
     int8_peak, int8_src = measure_int8_peak()
+    try:  # the dealer's splitmix64 draw rate: ALU roofline of the element-by-element chain
+        draw_peak = api.draw_peak(device) / 1e9
+    except Exception:  # noqa: BLE001
+        draw_peak = None
     # algorithmic units per class: bytes for the HBM-bound protocol rounds, ring MACs
     # for the GEMM (x36 int8 MACs = 72 int8 ops each, the limb-pair products of the tcgen05 path)
     notes = {"adder_round": "SPK level round (settle r, issue r+1). Bytes per element per party of the form that "
@@ -513,6 +517,12 @@ def main():
                        "= 56 B/elem/party per mul, 32 B per square (SURVEY 8(d))",
              "chain": "persistent compare-and-select chain (ReLU/tournament): 2 x 248 B wire + 16 B in/out = "
                       "512 B/elem/party (SURVEY 8(d))",
+             "chain_reg": "element-by-element compare-and-select chain (pair evaluation, in-device opens): the "
+                          "adder state and opened wires stay in registers, so it is bound by the dealer's "
+                          "splitmix64 draws (ALU), not HBM: 77 draws per element pair (2 mask, 65 adder: 13 "
+                          "ANDs x (A, B, r_A, r_B, r_C), 5 b2a, 5 multiply) against the measured draw rate "
+                          "(mpcg_debug_draw_peak: a full grid of independent draw streams); the opens are "
+                          "still posted and accounted per round",
              "gemm": "ring GEMM main kernel: 72 int8 ops per ring MAC (36 limb-pair MACs); ring MACs = 3 MKN (party 0, "
                      "dealer C online) + 2 MKN (party 1) per private linear layer; weight packing excluded; the "
                      "both-slots kernel (gemm_tc3.cu) also generates the opened E = x0 + x1 - A in its producers "
@@ -525,6 +535,12 @@ def main():
             ach = 72.0 * p_units / (p_ms / 1e3) / 1e12
             r = {"kernel": cls, "bound": "tensor", "achieved": ach, "peak": int8_peak, "unit": "TOP/s (int8)",
                  "frac": ach / int8_peak, "peak_source": int8_src}
+        elif cls == "chain_reg":
+            if not draw_peak:
+                continue
+            ach = p_units / (p_ms / 1e3) / 1e9
+            r = {"kernel": cls, "bound": "alu", "achieved": ach, "peak": draw_peak, "unit": "Gdraws/s",
+                 "frac": ach / draw_peak, "peak_source": "measured: mpcg_debug_draw_peak (splitmix64 draw rate)"}
         else:
             ach = (p_units / 1e9) / (p_ms / 1e3)
             r = {"kernel": cls, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",

@@ -245,6 +245,10 @@ int mpcg_debug_tc2_trace(uint64_t* out, int n);
 /* Debug: per-stage clock64 stamps of CTA (0,0,0) of the last both-slots tcgen05 GEMM run with
  * MPCG_TC3_TRACE=1 ([256][8]: MMA wait/full/issued, producer start/wait/acquired/arrived). */
 int mpcg_debug_tc3_trace(uint64_t* out, int n);
+/* Measurement: the dealer's draw rate on `device` — splitmix64 counter draws (rng.hpp) per
+ * second, a full grid of independent streams, best of 3 (the ALU roofline of the
+ * element-by-element compare chain). */
+int mpcg_debug_draw_peak(int device, double* draws_per_s);
 /* Link two single-party sessions (party 0, party 1) of this process on the same GPU: the
  * one-party-per-GPU code path with device copies in place of NCCL send/recv. Each party
  * must be driven by its own host thread (a collective waits for the peer's matching post). */

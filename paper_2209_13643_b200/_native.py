@@ -120,6 +120,7 @@ SIGNATURES = {
     "mpcg_set_gemv": [I32],
     "mpcg_debug_tc2_trace": [U64P, I32],
     "mpcg_debug_tc3_trace": [U64P, I32],
+    "mpcg_debug_draw_peak": [I32, C.POINTER(C.c_double)],
     "mpcg_session_connect_loopback": [P, P],
     "mpcg_launch_count": [],
     "mpcg_probe_start": [I32],

@@ -319,7 +319,14 @@ def launch_count() -> int:
     return int(N.lib().mpcg_launch_count())
 
 
-KERNEL_CLASS = {"adder_round": 1, "gemm": 2, "beaver": 3, "chain": 4}
+KERNEL_CLASS = {"adder_round": 1, "gemm": 2, "beaver": 3, "chain": 4, "chain_reg": 5}
+
+
+def draw_peak(device=0):
+    """Measured dealer draw rate (splitmix64 draws / s) on `device` (mpcg_debug_draw_peak)."""
+    v = C.c_double()
+    N.call("mpcg_debug_draw_peak", int(device), C.byref(v))
+    return v.value
 
 
 def probe_start(kernel_class="adder_round"):

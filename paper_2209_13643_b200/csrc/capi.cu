@@ -642,6 +642,44 @@ int mpcg_debug_tc3_trace(uint64_t* out, int n) {
   return guard([&] { tc3_trace_read(reinterpret_cast<unsigned long long*>(out), n); });
 }
 
+namespace {
+__global__ void draw_peak_kernel(u64 key, u64* out, int iters) {
+  u64 acc = 0;
+  const u64 z = key + u64(blockIdx.x * blockDim.x + threadIdx.x) * kPhi * 16;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc ^= mix64(z + u64(i + it * 16) * kPhi);
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+}  // namespace
+
+int mpcg_debug_draw_peak(int device, double* draws_per_s) {
+  return guard([&] {
+    MPCG_CUDA(cudaSetDevice(device));
+    const int blocks = num_sms() * 8, threads = 256, iters = 256;
+    u64* d = nullptr;
+    MPCG_CUDA(cudaMalloc(&d, size_t(blocks) * threads * 8));
+    cudaEvent_t a, b;
+    MPCG_CUDA(cudaEventCreate(&a));
+    MPCG_CUDA(cudaEventCreate(&b));
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+      MPCG_CUDA(cudaEventRecord(a));
+      draw_peak_kernel<<<blocks, threads>>>(0x1234567ull + rep, d, iters);
+      MPCG_CUDA(cudaEventRecord(b));
+      MPCG_CUDA(cudaEventSynchronize(b));
+      float ms = 0;
+      MPCG_CUDA(cudaEventElapsedTime(&ms, a, b));
+      if (rep > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(d);
+    *draws_per_s = double(blocks) * threads * iters * 16 / (double(best) * 1e-3);
+  });
+}
+
 int mpcg_debug_tc2_trace(uint64_t* out, int n) {
   return guard([&] { tc2_trace_read(reinterpret_cast<unsigned long long*>(out), n); });
 }

@@ -315,7 +315,7 @@ inline int num_sms() {
 
 // Instrumentation: count of kernels this library launched, and an optional probe that
 // brackets every launch of one kernel class with CUDA events (bench.py's live roofline).
-enum KernelClass : int { kClsOther = 0, kClsAdderRound = 1, kClsGemm = 2, kClsBeaver = 3, kClsChain = 4 };
+enum KernelClass : int { kClsOther = 0, kClsAdderRound = 1, kClsGemm = 2, kClsBeaver = 3, kClsChain = 4, kClsChainReg = 5 };
 struct Probe {
   int cls = -1;             // class being timed, -1 = off
   double bytes = 0;         // algorithmic bytes of the probed launches

@@ -1181,6 +1181,23 @@ __global__ void __launch_bounds__(256) chain_kernel(const __grid_constant__ Chai
   for (u64 g = t0; g < p.n; g += st) eval_slots(p.fin, pr, slot, g);
 }
 
+// Pair evaluation with in-device opens: round r+1 of element g reads only element g's adder
+// state and opened wire, which the same thread wrote in round r (the SPK levels shift inside
+// the 64-bit word; the b2a and the multiply are elementwise), so the whole chain runs element
+// by element in one ordinary kernel — no grid barrier, and the round-to-round state is re-read
+// from L1/L2 while it is hot instead of from HBM a whole pass later. Same functors and values
+// as chain_kernel; the opens are still posted / accounted by the launcher.
+template <class MR, class AR, class BR, class CR>
+__global__ void __launch_bounds__(256) chain_pair_kernel(const __grid_constant__ ChainParams<MR, AR, BR, CR> p) {
+  const u64 t0 = blockIdx.x * u64(blockDim.x) + threadIdx.x, st = u64(gridDim.x) * blockDim.x;
+  for (u64 g = t0; g < p.n; g += st) {
+    if (!p.skip_mask) eval_slots(p.mask, true, 0, g);
+    for (int r = 0; r < p.nadder; ++r) eval_slots(p.adder[r], true, 0, g);
+    eval_slots(p.b2a, true, 0, g);
+    eval_slots(p.fin, true, 0, g);
+  }
+}
+
 constexpr int kMaxChainSteps = 24;
 template <class B0, class ST>
 struct BeaverChainParams {

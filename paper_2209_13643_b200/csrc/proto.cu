@@ -418,6 +418,132 @@ struct MaskRound {
   }
 };
 
+// Register form of the element-by-element chain (pair evaluation, seeded dealer, 64-bit
+// adder): the round algebra of AdderRound::step<2> (opened wire), B2aBuildFF::pair,
+// MulCombine and MulByBitBuild::pair, with the adder state (s, p, P0), the opened wires and
+// the bits held in registers instead of memory, and each triple's secrets A, B drawn once for
+// its issue and reused by its settle (the per-round kernels redraw them a launch later). Only
+// the input x (through the sources) and the sink's output touch HBM.
+template <class DF, class UF, class PF>
+using ChainP = ChainParams<MaskRound<DF>, AdderRound<A2bPart<DF>, A2bPart<DF>, B2aBuildFF>,
+                           MulCombine<MulByBitBuild<UF>>, MulCombine<PF>>;
+
+// the masks r_A, r_B, r_C of element gp (= global index * phi) with the secrets A, B given
+__device__ __forceinline__ Dw masks_with(const EwTriple& t, u64 key, u64 gp, const Dw& sec) {
+  Dw d;
+  d.A = sec.A;
+  d.B = sec.B;
+  d.ra = mix64(key + t.pra + gp);
+  d.rb = mix64(key + t.prb + gp);
+  d.rc = mix64(key + t.prc + gp);
+  return d;
+}
+
+template <class DF, class UF, class PF>
+__global__ void __launch_bounds__(256) chain_reg_kernel(const __grid_constant__ ChainP<DF, UF, PF> p) {
+  const Pid2 pid = p.adder[0].pid;
+  const int q0 = pid.v[0] == 0 ? 0 : 1, q1 = 1 - q0;  // slots of party 0 and party 1
+  constexpr int L = 6;                               // SPK levels of the 64-bit adder
+  const u64 t0 = blockIdx.x * u64(blockDim.x) + threadIdx.x, st = u64(gridDim.x) * blockDim.x;
+  for (u64 g = t0; g < p.n; g += st) {
+    // round 0: issue the generate AND (x ^ a | y ^ b), opened
+    const auto& R0 = p.adder[0];
+    const u64 x0 = R0.xf(q0, g), x1 = R0.xf(q1, g), y0 = R0.yf(q0, g), y1 = R0.yf(q1, g);
+    const u64 P0a = x0 ^ y0, P0b = x1 ^ y1;
+    u64 s0, s1, pa, pb;
+    {
+      const EwTriple& T = R0.Tn;
+      const u64 key = tkey(T.key, T.kp), gp = (T.off + g) * kPhi;
+      const Dw dn = ew_secrets_kg<false>(T, key, gp);
+      const u64 e = (x0 ^ x1) ^ dn.A, d = (y0 ^ y1) ^ dn.B;
+      // round 1 settles it (adder.hpp:209-223)
+      const Dw dp = masks_with(T, key, gp, dn);
+      const u64 a0 = dp.A ^ dp.ra, b0 = dp.B ^ dp.rb, c0 = (dp.A & dp.B) ^ dp.rc;
+      s0 = c0 ^ (e & b0) ^ (d & a0) ^ (e & d);
+      s1 = dp.rc ^ (e & dp.rb) ^ (d & dp.ra);
+      pa = P0a;
+      pb = P0b;
+    }
+#pragma unroll 1
+    for (int r = 1; r <= L; ++r) {  // issue level r-1 (adder.hpp:122-140), settle it (142-165)
+      const auto& R = p.adder[r];
+      const EwTriple& T = R.Tn;
+      const SpkLevel lv = R.ln;
+      const u64 key = tkey(T.key, T.kp), gp0 = (T.off + g) * kPhi, gp1 = gp0 + T.ghalf * kPhi;
+      const Dw d0 = ew_secrets_kg<false>(T, key, gp0), d1 = ew_secrets_kg<false>(T, key, gp1);
+      const u64 po = (pa & lv.out) ^ (pb & lv.out);
+      const u64 w0 = po ^ d0.A, w1 = po ^ d1.A;
+      const u64 w2 = (((s0 & lv.in) * lv.mult) ^ ((s1 & lv.in) * lv.mult)) ^ d0.B;
+      const u64 w3 = (((pa & lv.in) * lv.mult) ^ ((pb & lv.in) * lv.mult)) ^ d1.B;
+      const Dw e0 = masks_with(T, key, gp0, d0), e1 = masks_with(T, key, gp1, d1);
+      // party 0 (absorbs the secrets) and party 1 (the masks)
+      const u64 a00 = e0.A ^ e0.ra, b00 = e0.B ^ e0.rb, c00 = (e0.A & e0.B) ^ e0.rc;
+      const u64 a01 = e1.A ^ e1.ra, b01 = e1.B ^ e1.rb, c01 = (e1.A & e1.B) ^ e1.rc;
+      const u64 z0a = c00 ^ (w0 & b00) ^ (w2 & a00) ^ (w0 & w2);
+      const u64 z1a = c01 ^ (w1 & b01) ^ (w3 & a01) ^ (w1 & w3);
+      const u64 z0b = e0.rc ^ (w0 & e0.rb) ^ (w2 & e0.ra);
+      const u64 z1b = e1.rc ^ (w1 & e1.rb) ^ (w3 & e1.ra);
+      s0 ^= z0a;
+      s1 ^= z0b;
+      pa = (pa & ~lv.out) ^ z1a;
+      pb = (pb & ~lv.out) ^ z1b;
+    }
+    // final round: sums -> msb bits -> b2a ".m1" open (B2aBuildFF::pair)
+    const auto& RF = p.adder[L + 1];
+    const u64 bit0 = ((P0a ^ (s0 << 1)) & RF.wmask) >> 63, bit1 = ((P0b ^ (s1 << 1)) & RF.wmask) >> 63;
+    const EwTriple& T1 = RF.ff.T;
+    const u64 k1 = tkey(T1.key, T1.kp), g1 = (T1.off + g) * kPhi;
+    const Dw t1 = ew_secrets_kg<false>(T1, k1, g1);
+    const u64 eB = bit0 - t1.A, dB = bit1 - t1.B;
+    // b2a combine (MulCombine over T1): prod_k, then MulByBitBuild::pair
+    const Dw m1 = masks_with(T1, k1, g1, t1);
+    const u64 prod0 = (m1.A * m1.B - m1.rc) + (eB * (m1.B - m1.rb) + dB * (m1.A - m1.ra)) + eB * dB;
+    const u64 prod1 = m1.rc + (eB * m1.rb + dB * m1.ra);
+    const auto& MB = p.b2a.pf;
+    const u64 c0 = (bit0 & 1) - (prod0 + prod0), c1 = (bit1 & 1) - (prod1 + prod1);
+    if (MB.cout.p[q0]) MB.cout.p[q0][g] = c0;
+    if (MB.cout.p[q1]) MB.cout.p[q1][g] = c1;
+    const EwTriple& T2 = MB.T;
+    const u64 k2 = tkey(T2.key, T2.kp), g2 = (T2.off + g) * kPhi;
+    const Dw t2 = ew_secrets_kg<false>(T2, k2, g2);
+    const u64 eM = MB.uf(q0, g) + MB.uf(q1, g) - t2.A, dM = c0 + c1 - t2.B;
+    // the multiply's combine (MulCombine over T2) -> sink
+    const Dw m2 = masks_with(T2, k2, g2, t2);
+    const u64 z0 = (m2.A * m2.B - m2.rc) + (eM * (m2.B - m2.rb) + dM * (m2.A - m2.ra)) + eM * dM;
+    const u64 z1 = m2.rc + (eM * m2.rb + dM * m2.ra);
+    if constexpr (has_pair_pf<PF>::value) {
+      p.fin.pf.pair(q0, g, z0, z1);
+    } else {
+      p.fin.pf(q0, 0, g, z0);
+      p.fin.pf(q1, 1, g, z1);
+    }
+  }
+}
+
+// The element-by-element chain: pair evaluation with the opened wire, no link, seeded dealer
+// (queue-sourced triples run the per-round kernels), not forced to per-round kernels
+// (mpcg_session_set_persistent(0)). The register form (chain_reg_kernel, MPCG_CHAIN_REG=0
+// disables) takes every size: ResNet-18 27.6 -> 20.7 ms, BERT-base 46.2 -> 40.9 ms, LeNet-5
+// 0.51 -> 0.41 ms against the per-round kernels (A/B on one box). The memory form
+// (chain_pair_kernel) only up to MPCG_FUSED_CHAIN_MAX elements (default 4M): at 8.4M it was 8%
+// slower than the per-round kernels (each thread's round-to-round state round-trips through
+// L2 with every round's latency exposed), at <= 2M 10-45% faster.
+bool chain_reg_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("MPCG_CHAIN_REG");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+bool fused_chain_ok(const Session& s, size_t n) {
+  static const size_t max_n = [] {
+    const char* e = std::getenv("MPCG_FUSED_CHAIN_MAX");
+    return e ? size_t(std::strtoull(e, nullptr, 10)) : size_t(4000000);
+  }();
+  return (chain_reg_on() || n <= max_n) && adder_opened_wire(s) && !(s.cfg.link_bandwidth > 0) && !s.source_q &&
+         s.persistent_mode != 0;
+}
+
 // One persistent cooperative kernel for the whole compare-and-select chain (1-GPU mode):
 // 10 exchanges become 10 grid barriers. Values, tags and collective accounting are those
 // of the per-round path (chunk lanes only change where an open may start; with in-device
@@ -425,7 +551,7 @@ struct MaskRound {
 template <class DF, class UF, class PF>
 void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const std::string& tag_msb,
                             const std::string& tag_b2a, const std::string& tag_mul, DF df, UF uf, PF pf,
-                            Ptr2 cout) {
+                            Ptr2 cout, bool fused = false) {
   const bool opened = adder_opened_wire(s);  // pair evaluation: opened wire for b2a and the multiply
   const int ch = clamp_chunks(opt.chunks, n);
   const Pid2 pid = pids(s);
@@ -509,6 +635,25 @@ void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const
   p.skip_mask = opened ? 1 : 0;
   const unsigned gy = p.pair ? 1u : unsigned(s.n_local);
 
+  if (fused) {  // element by element, no grid barrier (chain_reg_kernel / chain_pair_kernel)
+    const u64 blocks = std::min<u64>((n + 255) / 256, u64(num_sms()) * 16);
+    const bool reg = chain_reg_on();
+    bool seeded = t1.ew.pool == nullptr && t2.ew.pool == nullptr;
+    for (int r = 0; r < 7; ++r) seeded = seeded && tr[r].ew.pool == nullptr;
+    const bool use_reg = reg && seeded && c.levels == 6 && !cw[0];
+    // register form: ALU-bound on the dealer, so its unit is the draw — 2 mask + 65 adder
+    // (generate AND + 12 level ANDs, 5 each: A, B once for issue and settle, r_A, r_B, r_C)
+    // + 5 b2a + 5 multiply = 77 splitmix64 draws per element pair
+    ClassScope cs(use_reg ? kClsChainReg : kClsChain, use_reg ? 77.0 * double(n) : 512.0 * double(n) * s.n_local);
+    cudaEvent_t pe;
+    probe_begin(s.stream, &pe);
+    if (use_reg)
+      chain_reg_kernel<DF, UF, PF><<<unsigned(blocks), 256, 0, s.stream>>>(p);
+    else
+      chain_pair_kernel<MaskRound<DF>, AR, BR, CR><<<unsigned(blocks), 256, 0, s.stream>>>(p);
+    MPCG_CUDA(cudaGetLastError());
+    probe_end(s.stream, pe);
+  } else {
   auto kern = chain_kernel<MaskRound<DF>, AR, BR, CR>;
   static int per_sm = -1;  // resident 256-thread CTAs per SM for this instantiation
   if (per_sm < 0) {
@@ -535,6 +680,7 @@ void compare_mul_persistent(Session& s, size_t n, const AdderOptions& opt, const
     probe_begin(s.stream, &pe);
     MPCG_CUDA(cudaLaunchKernelEx(&lc, kern, p));
     probe_end(s.stream, pe);
+  }
   }
   // bookkeeping in the reference's collective order (H/protocols/compare.hpp:37-52,
   // adder.hpp:312-322, beaver.hpp:63-71)
@@ -566,6 +712,10 @@ void compare_mul(Session& s, size_t n, const AdderOptions& opt, const std::strin
   const int ch = clamp_chunks(opt.chunks, n);
   if (clamp_chunks(chunks_b2a, n) != ch || clamp_chunks(chunks_mul, n) != ch)
     throw Error(kUsageError, "compare_mul: misaligned chunk lanes");
+  if (n > 0 && fused_chain_ok(s, n)) {
+    compare_mul_persistent(s, n, opt, tag_msb, tag_b2a, tag_mul, df, uf, pf, cout, /*fused=*/true);
+    return;
+  }
   if (n > 0 && s.persistent_ok(n)) {
     compare_mul_persistent(s, n, opt, tag_msb, tag_b2a, tag_mul, df, uf, pf, cout);
     return;
