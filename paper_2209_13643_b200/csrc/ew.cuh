@@ -425,6 +425,26 @@ struct SqChainStep {
 // boundaries, as the compare chains do); defined after grid_barrier below.
 template <class B0, class ST>
 void persistent_beaver_chain(Session& s, u64 n, const B0& build, const std::vector<ST>& steps);
+// Element-by-element Beaver chains (beaver_chain_pair_kernel): pair evaluation with the opened
+// wire, no link, seeded dealer, not forced to per-round kernels. MPCG_FUSED_BCHAIN=0 disables.
+inline bool pair_chain_ok(const Session& s) {
+  static const bool on = [] {
+    const char* e = std::getenv("MPCG_FUSED_BCHAIN");
+    return !(e && e[0] == '0');
+  }();
+  return on && adder_opened_wire(s) && !(s.cfg.link_bandwidth > 0) && !s.source_q && s.persistent_mode != 0;
+}
+// the reference's collective order of a chain of R lane-chunked rounds: round by round, lanes
+// in order within a round (what post_lanes accounts)
+template <class TagOf>
+void account_chain(Session& s, size_t n, int R, int lanes, TagOf words_tag) {
+  for (int r = 0; r < R; ++r)
+    for (int k = 0; k < lanes; ++k) {
+      const size_t lo = n * size_t(k) / size_t(lanes), hi = n * size_t(k + 1) / size_t(lanes);
+      const auto wt = words_tag(r, k);
+      s.account(wt.first * (hi - lo), Reduce::Sum, wt.second);
+    }
+}
 
 // Rounds tr[0..R) of squares: round 0 squares x0(slot, g); round r squares the value
 // yf_for(r-1) produced from round r-1's product; yf_for(R-1) sees the chain's last product.
@@ -438,7 +458,7 @@ void square_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& t
   const int acct_ = chunks;  // lanes as the reference accounts them (tags)
   auto ctag = [&](int r, int k) { return acct_ == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
   using YF0 = decltype(yf_for(0));
-  if (chunks == 1 && R <= 24 && n > 0 && s.persistent_ok(n)) {
+  if (R <= 24 && n > 0 && ((chunks == 1 && s.persistent_ok(n)) || pair_chain_ok(s))) {
     std::vector<Open> op(static_cast<size_t>(R));
     for (int r = 0; r < R; ++r) op[r] = s.begin_open(n, Reduce::Sum);
     std::vector<SqChainStep<YF0>> st;
@@ -450,7 +470,7 @@ void square_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& t
     b0.opened = opened;
     for (auto& x : st) x.opened = opened;
     persistent_beaver_chain(s, n, b0, st);
-    for (int r = 0; r < R; ++r) s.account(n, Reduce::Sum, tags[r]);  // the reference's collective order
+    account_chain(s, n, R, chunks, [&](int r, int k) { return std::make_pair(size_t(1), ctag(r, k)); });
     s.check();
     return;
   }
@@ -561,7 +581,7 @@ void mul_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, 
   const int acct_ = chunks;  // lanes as the reference accounts them (tags)
   auto ctag = [&](int r, int k) { return acct_ == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
   using PV0 = decltype(pv_for(0));
-  if (chunks == 1 && R <= 24 && n > 0 && s.persistent_ok(n)) {
+  if (R <= 24 && n > 0 && ((chunks == 1 && s.persistent_ok(n)) || pair_chain_ok(s))) {
     std::vector<Open> op(static_cast<size_t>(R));
     for (int r = 0; r < R; ++r) op[r] = s.begin_open(2 * n, Reduce::Sum);
     std::vector<MulChainStep<PV0>> st;
@@ -574,7 +594,7 @@ void mul_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr, 
     b0.opened = opened;
     for (auto& x : st) x.opened = opened;
     persistent_beaver_chain(s, n, b0, st);
-    for (int r = 0; r < R; ++r) s.account(2 * n, Reduce::Sum, tags[r]);
+    account_chain(s, n, R, chunks, [&](int r, int k) { return std::make_pair(size_t(2), ctag(r, k)); });
     s.check();
     return;
   }
@@ -715,7 +735,7 @@ void mixed_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr
   auto ctag = [&](int r, int k) { return acct_ == 1 ? tags[r] : tags[r] + ".chunk" + std::to_string(k); };
   auto words = [&](int r, size_t w) { return sq[r] ? w : 2 * w; };
   using PV0 = decltype(pv_for(0));
-  if (chunks == 1 && R <= 24 && n > 0 && s.persistent_ok(n)) {  // one cooperative kernel
+  if (R <= 24 && n > 0 && ((chunks == 1 && s.persistent_ok(n)) || pair_chain_ok(s))) {  // one kernel
     std::vector<Open> op(static_cast<size_t>(R));
     for (int r = 0; r < R; ++r) op[r] = s.begin_open(words(r, n), Reduce::Sum);
     std::vector<MixedChainStep<PV0>> st;
@@ -734,7 +754,7 @@ void mixed_chain(Session& s, size_t n, int chunks, const std::vector<Triple>& tr
       b0.opened = opened;
       persistent_beaver_chain(s, n, b0, st);
     }
-    for (int r = 0; r < R; ++r) s.account(words(r, n), Reduce::Sum, tags[r]);
+    account_chain(s, n, R, chunks, [&](int r, int k) { return std::make_pair(words(r, 1), ctag(r, k)); });
     s.check();
     return;
   }
@@ -1223,9 +1243,37 @@ __global__ void __launch_bounds__(256) beaver_chain_kernel(const __grid_constant
   }
 }
 
+// Pair evaluation with in-device opens: each round of a Beaver chain (exp squares, Newton
+// steps) is elementwise and its opened wire for element g is written and read by the same
+// thread, so the chain runs element by element with no grid barrier (as chain_pair_kernel).
+template <class B0, class ST>
+__global__ void __launch_bounds__(256) beaver_chain_pair_kernel(const __grid_constant__ BeaverChainParams<B0, ST> p) {
+  const u64 t0 = blockIdx.x * u64(blockDim.x) + threadIdx.x, stride = u64(gridDim.x) * blockDim.x;
+  for (u64 g = t0; g < p.n; g += stride) {
+    eval_slots(p.build, true, 0, g);
+    for (int r = 0; r < p.nsteps; ++r) eval_slots(p.steps[r], true, 0, g);
+  }
+}
+
 template <class B0, class ST>
 void persistent_beaver_chain(Session& s, u64 n, const B0& build, const std::vector<ST>& steps) {
   if (steps.size() > size_t(kMaxChainSteps)) throw Error(kInternalError, "beaver chain too long");
+  if (pair_chain_ok(s)) {  // element by element (beaver_chain_pair_kernel), any size
+    BeaverChainParams<B0, ST> p{};
+    p.build = build;
+    for (size_t i = 0; i < steps.size(); ++i) p.steps[i] = steps[i];
+    p.nsteps = int(steps.size());
+    p.n = n;
+    p.pair = 1;
+    ClassScope cs(kClsOther, 0);
+    cudaEvent_t pe;
+    probe_begin(s.stream, &pe);
+    const u64 blocks = std::min<u64>((n + 255) / 256, u64(num_sms()) * 16);
+    beaver_chain_pair_kernel<B0, ST><<<unsigned(blocks), 256, 0, s.stream>>>(p);
+    MPCG_CUDA(cudaGetLastError());
+    probe_end(s.stream, pe);
+    return;
+  }
   BeaverChainParams<B0, ST> p{};
   p.build = build;
   for (size_t i = 0; i < steps.size(); ++i) p.steps[i] = steps[i];
