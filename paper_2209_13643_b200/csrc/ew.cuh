@@ -40,6 +40,18 @@ inline Pid2 pids(const Session& s) { return Pid2{{s.party_of[0], s.party_of[1]}}
 // when the pair kernel evaluates every kernel of the exchange (both slots local, pair
 // evaluation on); MPCG_PAIR_EVAL=0 = per-slot evaluation with two payloads.
 inline bool adder_opened_wire(const Session& s) { return s.n_local == 2 && pair_eval_enabled(); }
+// Element-by-element Beaver chains (beaver_chain_pair_kernel) and one-pass multiplies
+// (MulFused): pair evaluation with the opened wire, no link, seeded dealer (queue-sourced
+// triples keep the per-round kernels), not forced to per-round kernels. MPCG_FUSED_BCHAIN=0
+// disables.
+inline bool pair_chain_ok(const Session& s) {
+  static const bool on = [] {
+    const char* e = std::getenv("MPCG_FUSED_BCHAIN");
+    return !(e && e[0] == '0');
+  }();
+  return on && adder_opened_wire(s) && !(s.cfg.link_bandwidth > 0) && !s.source_q && s.persistent_mode != 0;
+}
+
 inline Ptr2 ptrs(const DT& t) { return Ptr2{{t.s[0], t.s[1]}}; }
 inline CPtr2 cptrs(const DT& t) { return CPtr2{{t.s[0], t.s[1]}}; }
 inline Ptr2 own_ptrs(const Open& o) {
@@ -169,6 +181,32 @@ struct MulCombine {
 
 inline CPtr2 as_const(Ptr2 p) { return CPtr2{{p.p[0], p.p[1]}}; }
 
+// Pair evaluation with in-device opens (pair_chain_ok): the Beaver multiply of element g in one
+// pass — the opened (eps, delta) of MulBuild's opened wire kept in registers and combined at
+// once (MulCombine's algebra), A and B drawn once for both. Arithmetic triples only.
+template <class XF, class YF, class PF>
+struct MulFused {
+  EwTriple T;
+  Pid2 pid;
+  XF xf;
+  YF yf;
+  PF pf;
+  __device__ void operator()(int, u64) const {}  // pair evaluation only (launch_ew's both())
+  __device__ void both(u64 g) const {
+    const int q0 = pid.v[0] == 0 ? 0 : 1, q1 = 1 - q0;
+    const Dw d = ew_draw<true>(T, T.off + g, true);
+    const u64 e = xf(q0, g) + xf(q1, g) - d.A, dd = yf(q0, g) + yf(q1, g) - d.B;
+    const u64 z0 = (d.A * d.B - d.rc) + (e * (d.B - d.rb) + dd * (d.A - d.ra)) + e * dd;
+    const u64 z1 = d.rc + (e * d.rb + dd * d.ra);
+    if constexpr (has_pair_pf<PF>::value) {
+      pf.pair(q0, g, z0, z1);
+    } else {
+      pf(q0, 0, g, z0);
+      pf(q1, 1, g, z1);
+    }
+  }
+};
+
 // z = x*y with sources/sink functors; `chunks` reveals as in beaver_mul.
 template <class XF, class YF, class PF>
 void mul_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::string& tag, XF xf, YF yf,
@@ -177,6 +215,18 @@ void mul_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::stri
   const int acct = chunks;                                // lanes as the reference accounts them
   const int xl = acct > 1 && s.fuse_lanes() ? 1 : acct;  // lanes launched (Session::fuse_lanes)
   auto ltag = [&](int k) { return acct == 1 ? tag : tag + ".chunk" + std::to_string(k); };
+  if (m > 0 && !T.bin && pair_chain_ok(s)) {  // build + open + combine in one pass (MulFused)
+    {
+      ClassScope cs(kClsOther, 0);
+      launch_ew(s.stream, s.n_local, m, MulFused<XF, YF, PF>{T, pids(s), xf, yf, pf});
+    }
+    for (int k = 0; k < acct; ++k) {  // the opens, as post / post_lanes account them
+      const auto r = chunk_range(m, acct, k);
+      s.account(2 * (r.second - r.first), Reduce::Sum, ltag(k));
+    }
+    s.check();
+    return;
+  }
   std::vector<Open> opens(static_cast<size_t>(xl));
   const Pid2 pid = pids(s);
   // SURVEY 8(d) algorithmic bytes: beaver_mul = 2 x 16 B wire + 8 x (2 in + 1 out) = 56 B/elem/
@@ -425,15 +475,6 @@ struct SqChainStep {
 // boundaries, as the compare chains do); defined after grid_barrier below.
 template <class B0, class ST>
 void persistent_beaver_chain(Session& s, u64 n, const B0& build, const std::vector<ST>& steps);
-// Element-by-element Beaver chains (beaver_chain_pair_kernel): pair evaluation with the opened
-// wire, no link, seeded dealer, not forced to per-round kernels. MPCG_FUSED_BCHAIN=0 disables.
-inline bool pair_chain_ok(const Session& s) {
-  static const bool on = [] {
-    const char* e = std::getenv("MPCG_FUSED_BCHAIN");
-    return !(e && e[0] == '0');
-  }();
-  return on && adder_opened_wire(s) && !(s.cfg.link_bandwidth > 0) && !s.source_q && s.persistent_mode != 0;
-}
 // the reference's collective order of a chain of R lane-chunked rounds: round by round, lanes
 // in order within a round (what post_lanes accounts)
 template <class TagOf>
