@@ -12,6 +12,7 @@ import sys
 from collections import defaultdict
 
 CLASSES = [
+    ("chain_fused", r"chain_reg_kernel|chain_pair_kernel|beaver_chain_pair_kernel|MulFused"),
     ("adder_round", r"AdderRound"),
     ("gemm", r"ring_gemm_tc2|ring_gemm_tc3|ring_gemm_simt|ring_gemv|ring_gemm_rows"),
     ("gemm_aux", r"tc2_pack|pack_|gemm_splitk_epilogue"),

@@ -12,6 +12,8 @@ import subprocess
 import sys
 
 CLASSES = [
+    ("chain_reg", r"chain_reg_kernel"),
+    ("chain_fused", r"chain_pair_kernel|beaver_chain_pair_kernel|MulFused"),
     ("adder_round", r"AdderRound"),
     ("beaver_mul_build", r"MulBuild"),
     ("beaver_mul_combine", r"MulCombine"),
