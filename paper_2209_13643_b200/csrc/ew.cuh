@@ -64,7 +64,8 @@ inline CPtr2 peer_ptrs(const Open& o) {
 // ---------------------------------------------------------------- value sources
 struct SrcMem {  // x[g]
   CPtr2 x;
-  __device__ u64 operator()(int slot, u64 g) const { return x.p[slot][g]; }
+  // select, not index: a runtime slot index into the parameter array spills it to local memory
+  __device__ u64 operator()(int slot, u64 g) const { return (slot ? x.p[1] : x.p[0])[g]; }
 };
 struct SrcZero {
   __device__ u64 operator()(int, u64) const { return 0; }

@@ -273,7 +273,8 @@ struct MaskedPart {
   int y;
   __device__ u64 operator()(int slot, u64 g) const {
     const u64 c = tkey(mr.base, mr.bp) + 1 + g;
-    if ((pid.v[slot] == 0) == (y == 0)) return xf(slot, g) ^ drw(slot == 0 ? k0 : k1, c);  // keep
+    const int party = slot ? pid.v[1] : pid.v[0];  // select: no local copy of pid
+    if ((party == 0) == (y == 0)) return xf(slot, g) ^ drw(slot == 0 ? k0 : k1, c);  // keep
     return drw(slot == 0 ? k1 : k0, c);  // the peer slot's mask r
   }
 };
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(256) chain_reg_kernel(const __grid_constant__ 
       pa = P0a;
       pb = P0b;
     }
-#pragma unroll 1
+#pragma unroll  // constant parameter offsets: the triples' fields fold into the instructions
     for (int r = 1; r <= L; ++r) {  // issue level r-1 (adder.hpp:122-140), settle it (142-165)
       const auto& R = p.adder[r];
       const EwTriple& T = R.Tn;
@@ -501,8 +502,10 @@ __global__ void __launch_bounds__(256) chain_reg_kernel(const __grid_constant__ 
     const u64 prod1 = m1.rc + (eB * m1.rb + dB * m1.ra);
     const auto& MB = p.b2a.pf;
     const u64 c0 = (bit0 & 1) - (prod0 + prod0), c1 = (bit1 & 1) - (prod1 + prod1);
-    if (MB.cout.p[q0]) MB.cout.p[q0][g] = c0;
-    if (MB.cout.p[q1]) MB.cout.p[q1][g] = c1;
+    u64* const co0 = q0 ? MB.cout.p[1] : MB.cout.p[0];
+    u64* const co1 = q0 ? MB.cout.p[0] : MB.cout.p[1];
+    if (co0) co0[g] = c0;
+    if (co1) co1[g] = c1;
     const EwTriple& T2 = MB.T;
     const u64 k2 = tkey(T2.key, T2.kp), g2 = (T2.off + g) * kPhi;
     const Dw t2 = ew_secrets_kg<false>(T2, k2, g2);
@@ -809,7 +812,9 @@ namespace {
 struct SinkXMinus {  // out = x - z  (relu gate, H/nonlinear/activations.hpp:46)
   CPtr2 x;
   Ptr2 out;
-  __device__ void operator()(int slot, int, u64 g, u64 z) const { out.p[slot][g] = x.p[slot][g] - z; }
+  __device__ void operator()(int slot, int, u64 g, u64 z) const {
+    (slot ? out.p[1] : out.p[0])[g] = (slot ? x.p[1] : x.p[0])[g] - z;
+  }
 };
 }  // namespace
 
@@ -832,7 +837,7 @@ struct SrcHalfDiff {
   int sign;
   __device__ u64 operator()(int slot, u64 g) const {
     const u32 o = u32(g) / h, j = u32(g) - o * h;
-    const u64* row = cur.p[slot] + u64(o) * len;
+    const u64* row = (slot ? cur.p[1] : cur.p[0]) + u64(o) * len;
     return sign > 0 ? row[j] - row[h + j] : row[h + j] - row[j];
   }
 };
@@ -842,7 +847,7 @@ struct SinkPick {  // m = a + step, written into the next [outer, nw] row layout
   u32 h, len, nw;
   __device__ void operator()(int slot, int, u64 g, u64 z) const {
     const u32 o = u32(g) / h, j = u32(g) - o * h;
-    next.p[slot][u64(o) * nw + j] = cur.p[slot][u64(o) * len + j] + z;
+    (slot ? next.p[1] : next.p[0])[u64(o) * nw + j] = (slot ? cur.p[1] : cur.p[0])[u64(o) * len + j] + z;
   }
 };
 }  // namespace
@@ -1080,7 +1085,9 @@ namespace {
 struct SinkNegAbs {  // -|x| = 2 x b - x
   CPtr2 x;
   Ptr2 out;
-  __device__ void operator()(int slot, int, u64 g, u64 z) const { out.p[slot][g] = (z + z) - x.p[slot][g]; }
+  __device__ void operator()(int slot, int, u64 g, u64 z) const {
+    (slot ? out.p[1] : out.p[0])[g] = (z + z) - (slot ? x.p[1] : x.p[0])[g];
+  }
 };
 struct SrcOneMinus2 {  // [p0] 2^f - 2 r
   Pid2 pid;

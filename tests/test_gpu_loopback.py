@@ -6,6 +6,7 @@ then runs with one local slot, reads the peer payload from the receive buffer, a
 pipelined wrap-around delta crosses the link — and the per-party output shares must equal
 the reference's own (tests/golden) word for word, exactly like the two-slot session's."""
 import os
+import sys
 import threading
 
 import numpy as np
@@ -48,6 +49,8 @@ def _run_pair(mp, g, mode, weights, iters, link=None, kind="loopback", graph=Fal
             out[p] = z.numpy()[0]
             s.sync()
         except Exception as e:  # noqa: BLE001
+            # reported at once: the peer party may now wait on the link until the join timeout
+            print(f"party {p} failed: {e!r}", file=sys.stderr, flush=True)
             err.append(e)
 
     th = [threading.Thread(target=party, args=(p,)) for p in (0, 1)]
