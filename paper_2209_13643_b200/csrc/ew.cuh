@@ -34,6 +34,10 @@ struct Ptr2 {
 struct CPtr2 {
   const u64* p[2];
 };
+// Slot pointer / party of a runtime slot by selection: indexing a kernel-parameter array with a
+// runtime index makes the compiler copy the array to local memory (STL/LDL in the hot loops).
+__host__ __device__ __forceinline__ u64* sel(const Ptr2& x, int slot) { return slot ? x.p[1] : x.p[0]; }
+__host__ __device__ __forceinline__ const u64* sel(const CPtr2& x, int slot) { return slot ? x.p[1] : x.p[0]; }
 
 inline Pid2 pids(const Session& s) { return Pid2{{s.party_of[0], s.party_of[1]}}; }
 // Opened wire (AdderRound, MulBuild/MulCombine, the compare chain's b2a and multiply): exactly
@@ -72,23 +76,23 @@ struct SrcZero {
 };
 struct SrcSub {  // x[g] - y[g]
   CPtr2 x, y;
-  __device__ u64 operator()(int slot, u64 g) const { return x.p[slot][g] - y.p[slot][g]; }
+  __device__ u64 operator()(int slot, u64 g) const { return sel(x, slot)[g] - sel(y, slot)[g]; }
 };
 struct SrcSar {  // sar(x[g], k)
   CPtr2 x;
   int k;
-  __device__ u64 operator()(int slot, u64 g) const { return sar64(x.p[slot][g], k); }
+  __device__ u64 operator()(int slot, u64 g) const { return sar64(sel(x, slot)[g], k); }
 };
 
 // ---------------------------------------------------------------- sinks (post-combine)
 struct SinkStore {  // out[g] = z
   Ptr2 out;
-  __device__ void operator()(int slot, int, u64 g, u64 z) const { out.p[slot][g] = z; }
+  __device__ void operator()(int slot, int, u64 g, u64 z) const { sel(out, slot)[g] = z; }
 };
 struct SinkTrunc {  // out[g] = sar(z, k)
   Ptr2 out;
   int k;
-  __device__ void operator()(int slot, int, u64 g, u64 z) const { out.p[slot][g] = sar64(z, k); }
+  __device__ void operator()(int slot, int, u64 g, u64 z) const { sel(out, slot)[g] = sar64(z, k); }
 };
 
 // ---------------------------------------------------------------- Beaver multiply
@@ -119,8 +123,8 @@ struct MulBuild {
       const int slot = pair_slot<NS>(pid, slot0, k);
       u64 a, b, c;
       ew_share<false>(T, pid.v[slot], d, a, b, c);
-      own.p[slot][j] = xf(slot, g) - a;
-      own.p[slot][w + j] = yf(slot, g) - b;
+      sel(own, slot)[j] = xf(slot, g) - a;
+      sel(own, slot)[w + j] = yf(slot, g) - b;
     }
   }
 };
@@ -164,8 +168,8 @@ struct MulCombine {
       const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
       u64 e = oe, d = od;
       if (!op) {
-        const u64* o = own.p[slot];
-        const u64* q = peer.p[slot];
+        const u64* o = sel(own, slot);
+        const u64* q = sel(peer, slot);
         e = o[j] + q[j];
         d = o[w + j] + q[w + j];
       }
@@ -320,7 +324,7 @@ struct SqBuild {
   bool opened = false;  // pair evaluation: the opened eps once (slot 0's outbox)
   __device__ void operator()(int slot, u64 j) const {
     const u64 g = lo + j;
-    own.p[slot][j] = xf(slot, g) - sq_a(T, pid.v[slot], T.off + g);
+    sel(own, slot)[j] = xf(slot, g) - sq_a(T, pid.v[slot], T.off + g);
   }
   __device__ void both(u64 j) const {
     const u64 g = lo + j;
@@ -343,7 +347,7 @@ struct SqCombine {
   __device__ void operator()(int slot, u64 j) const {
     const int party = pid.v[slot];
     const u64 g = lo + j;
-    const u64 e = own.p[slot][j] + peer.p[slot][j];
+    const u64 e = sel(own, slot)[j] + sel(peer, slot)[j];
     u64 a, c;
     sq_ac(T, party, T.off + g, a, c);
     u64 z = c + (e * a) * 2;
@@ -430,7 +434,7 @@ struct SqBuild2 {
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       const int slot = pair_slot<NS>(pid, slot0, k);
-      own.p[slot][j] = xf(slot, g) - sq_share_a(pid.v[slot], d);
+      sel(own, slot)[j] = xf(slot, g) - sq_share_a(pid.v[slot], d);
     }
   }
 };
@@ -461,12 +465,12 @@ struct SqChainStep {
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
-      const u64 e = op ? oe : ownp.p[slot][j] + peerp.p[slot][j];
+      const u64 e = op ? oe : sel(ownp, slot)[j] + sel(peerp, slot)[j];
       u64 z = sq_share_c(party, dp) + (e * sq_share_a(party, dp)) * 2;
       if (party == 0) z += e * e;
       const u64 y = yf(slot, party, g, z);
       if (op) ysum += y;
-      else if (!last) ownn.p[slot][j] = y - sq_share_a(party, dn);
+      else if (!last) sel(ownn, slot)[j] = y - sq_share_a(party, dn);
     }
     if (op && !last) ownn.p[0][j] = ysum - sq_secret(Tn, Tn.off + g);  // masks cancel in the open
   }
@@ -584,8 +588,8 @@ struct MulChainStep {
       const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
       u64 e = oe, d = od;
       if (!op) {
-        const u64* o = ownp.p[slot];
-        const u64* q = peerp.p[slot];
+        const u64* o = sel(ownp, slot);
+        const u64* q = sel(peerp, slot);
         e = o[j] + q[j], d = o[w + j] + q[w + j];
       }
       u64 a, b, c;
@@ -599,8 +603,8 @@ struct MulChainStep {
         } else {
           u64 an, bn, cn;
           ew_share<false>(Tn, party, dn, an, bn, cn);
-          ownn.p[slot][j] = pv.nx(slot, g, v) - an;
-          ownn.p[slot][w + j] = pv.ny(slot, g, v) - bn;
+          sel(ownn, slot)[j] = pv.nx(slot, g, v) - an;
+          sel(ownn, slot)[w + j] = pv.ny(slot, g, v) - bn;
         }
       }
     }
@@ -724,8 +728,8 @@ struct MixedChainStep {
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
-      const u64* o = ownp.p[slot];
-      const u64* q = peerp.p[slot];
+      const u64* o = sel(ownp, slot);
+      const u64* q = sel(peerp, slot);
       u64 z;
       if (psq) {
         const u64 e = op ? oe : o[j] + q[j];
@@ -744,12 +748,12 @@ struct MixedChainStep {
           sx += pv.nx(slot, g, v);
           if (!nsq) sy += pv.ny(slot, g, v);
         } else if (nsq) {
-          ownn.p[slot][j] = pv.nx(slot, g, v) - sq_share_a(party, sn);
+          sel(ownn, slot)[j] = pv.nx(slot, g, v) - sq_share_a(party, sn);
         } else {
           u64 an, bn, cn;
           ew_share<false>(Tn, party, dn, an, bn, cn);
-          ownn.p[slot][j] = pv.nx(slot, g, v) - an;
-          ownn.p[slot][w + j] = pv.ny(slot, g, v) - bn;
+          sel(ownn, slot)[j] = pv.nx(slot, g, v) - an;
+          sel(ownn, slot)[w + j] = pv.ny(slot, g, v) - bn;
         }
       }
     }
@@ -925,15 +929,15 @@ struct AdderRound {
       for (int k = 0; k < NS; ++k) {
         const int slot = pair_slot<NS>(pid, slot0, k);
         const u64 x = xf(slot, g), y = yf(slot, g);
-        P0.p[slot][g] = x ^ y;
+        sel(P0, slot)[g] = x ^ y;
         u64 a, b;
         ew_share<false>(Tn, pid.v[slot], dn, a, b, dummy);
         if (op) {
           o0 ^= x;
           o1 ^= y;
         } else {
-          ownn.p[slot][j] = x ^ a;
-          ownn.p[slot][w + j] = y ^ b;
+          sel(ownn, slot)[j] = x ^ a;
+          sel(ownn, slot)[w + j] = y ^ b;
         }
       }
       if (op) {
@@ -949,13 +953,13 @@ struct AdderRound {
       for (int k = 0; k < NS; ++k) {
         const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
         const u64* o = ownp.p[op ? 0 : slot];
-        const u64* q = peerp.p[slot];
+        const u64* q = sel(peerp, slot);
         const u64 e = op ? o[j] : o[j] ^ q[j], d = op ? o[w + j] : o[w + j] ^ q[w + j];
         u64 a, b, c;
         ew_share<true>(Tp, party, dp, a, b, c);
         s[k] = c ^ (e & b) ^ (d & a);
         if (party == 0) s[k] ^= e & d;
-        p[k] = P0.p[slot][g];
+        p[k] = sel(P0, slot)[g];
       }
     } else {  // settle a prefix level (H/protocols/adder.hpp:142-165)
       // Own payload is recomputed from the pre-round state instead of re-read from HBM:
@@ -972,11 +976,11 @@ struct AdderRound {
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
         const int slot = pair_slot<NS>(pid, slot0, k), party = pair_party<NS>(pid, slot, k);
-        const u64* q = peerp.p[slot];
+        const u64* q = sel(peerp, slot);
         u64 a0, b0, c0, a1, b1, c1;
         ew_share<true>(Tp, party, d0, a0, b0, c0);
         ew_share<true>(Tp, party, d1, a1, b1, c1);
-        const u64 s0 = S.p[slot][g], p0s = P.p[slot][g];
+        const u64 s0 = sel(S, slot)[g], p0s = sel(P, slot)[g];
         const u64 po = p0s & lp.out;
         const u64 e0 = op ? oe0 : (po ^ a0) ^ q[j], e1 = op ? oe1 : (po ^ a1) ^ q[w + j];
         const u64 dd0 = op ? od0 : (((s0 & lp.in) * lp.mult) ^ b0) ^ q[2 * w + j];
@@ -1013,14 +1017,14 @@ struct AdderRound {
           o[0] ^= po, o[2] ^= ms, o[3] ^= mp;
         } else {
           const u64 v0 = po ^ a0, v1 = po ^ a1, v2 = ms ^ b0, v3 = mp ^ b1;
-          u64* nn = ownn.p[slot];
+          u64* nn = sel(ownn, slot);
           nn[j] = v0;
           nn[w + j] = v1;
           nn[2 * w + j] = v2;
           nn[3 * w + j] = v3;
         }
-        S.p[slot][g] = s[k];
-        P.p[slot][g] = p[k];
+        sel(S, slot)[g] = s[k];
+        sel(P, slot)[g] = p[k];
       }
       if (op) {  // a0 ^ a1 = A, b0 ^ b1 = B for each of the two triples
         u64* nn = ownn.p[0];
@@ -1031,12 +1035,12 @@ struct AdderRound {
       }
     } else if constexpr (NS == 2 && has_pair_ff<FF>::value) {
       const int q0 = pair_slot<2>(pid, 0, 0);
-      ff.pair(q0, g, j, (P0.p[q0][g] ^ (s[0] << 1)) & wmask, (P0.p[1 - q0][g] ^ (s[1] << 1)) & wmask);
+      ff.pair(q0, g, j, (sel(P0, q0)[g] ^ (s[0] << 1)) & wmask, (sel(P0, 1 - q0)[g] ^ (s[1] << 1)) & wmask);
     } else {
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
         const int slot = pair_slot<NS>(pid, slot0, k);
-        ff(slot, pid.v[slot], g, j, (P0.p[slot][g] ^ (s[k] << 1)) & wmask);
+        ff(slot, pid.v[slot], g, j, (sel(P0, slot)[g] ^ (s[k] << 1)) & wmask);
       }
     }
   }
@@ -1354,11 +1358,11 @@ void persistent_beaver_chain(Session& s, u64 n, const B0& build, const std::vect
 // Plain final sinks for adder_op (same functor for every lane).
 struct SumSink {  // binary share of the sum
   Ptr2 out;
-  __device__ void operator()(int slot, int, u64 g, u64, u64 sum) const { out.p[slot][g] = sum; }
+  __device__ void operator()(int slot, int, u64 g, u64, u64 sum) const { sel(out, slot)[g] = sum; }
 };
 struct MsbSink {  // sign bit in position 0 (H/protocols/compare.hpp:57-62)
   Ptr2 out;
-  __device__ void operator()(int slot, int, u64 g, u64, u64 sum) const { out.p[slot][g] = sum >> 63; }
+  __device__ void operator()(int slot, int, u64 g, u64, u64 sum) const { sel(out, slot)[g] = sum >> 63; }
 };
 template <class FF>
 struct SameFF {

@@ -312,8 +312,8 @@ DT SecureExecutor::weight_matmul(size_t i, const DT& x, const ConvGeom* geom, bo
         const int ih = int(oh * g.stride + ki) - int(g.pad), iw = int(ow * g.stride + kj) - int(g.pad);
         u64 v = 0;
         if (ih >= 0 && iw >= 0 && ih < int(g.H) && iw < int(g.W))
-          v = xp.p[slot][((u64(n) * g.C + ci) * g.H + u32(ih)) * g.W + u32(iw)];
-        cp.p[slot][idx] = v;
+          v = sel(xp, slot)[((u64(n) * g.C + ci) * g.H + u32(ih)) * g.W + u32(iw)];
+        sel(cp, slot)[idx] = v;
       });
     }
     public_gemm(s_, cols.s, W.s[0], z.s, M, N, K, ep);
@@ -376,7 +376,7 @@ DT SecureExecutor::scale_and_rescale(const DT& x, double c) {
   const CPtr2 xp = cptrs(x);
   const Ptr2 zp = ptrs(z);
   launch_ew(s_.stream, s_.n_local, x.numel(),
-            [=] __device__(int slot, u64 i) { zp.p[slot][i] = sar64(xp.p[slot][i] * k, f); });
+            [=] __device__(int slot, u64 i) { sel(zp, slot)[i] = sar64(sel(xp, slot)[i] * k, f); });
   return z;
 }
 
@@ -399,7 +399,7 @@ DT SecureExecutor::attention(const LayerSpec& l, const DT& x, const Shape& in_sh
     launch_ew(s_.stream, s_.n_local, 3 * per, [=] __device__(int slot, u64 i64) {  // 32-bit index math
       const u32 i = u32(i64), part = i / per32, r = i - part * per32;
       const u32 rj = r / DH, j = r - rj * DH, rt = rj / Tt, t = rj - rt * Tt, b = rt / H, h = rt - b * H;
-      dst.p[slot][i] = src.p[slot][(u64(b) * Tt + t) * 3 * D + part * D + h * DH + j];
+      sel(dst, slot)[i] = sel(src, slot)[(u64(b) * Tt + t) * 3 * D + part * D + h * DH + j];
     });
   }
   const size_t per = B * heads * T * dh;
@@ -423,7 +423,7 @@ DT SecureExecutor::attention(const LayerSpec& l, const DT& x, const Shape& in_sh
     const CPtr2 xp = cptrs(scores);
     const Ptr2 zp = ptrs(z);
     launch_ew(s_.stream, s_.n_local, scores.numel(),
-              [=] __device__(int slot, u64 i) { zp.p[slot][i] = sar64(sar64(xp.p[slot][i], f) * kc, f); });
+              [=] __device__(int slot, u64 i) { sel(zp, slot)[i] = sar64(sar64(sel(xp, slot)[i], f) * kc, f); });
     scores = z;
   }
   DT probs = softmax_shares(s_, scores, T, l.name + ".softmax");
@@ -437,7 +437,7 @@ DT SecureExecutor::attention(const LayerSpec& l, const DT& x, const Shape& in_sh
     if (B * T * d >= (u64(1) << 32)) throw Error(kShapeError, "attention: activation too large");
     launch_ew(s_.stream, s_.n_local, B * T * d, [=] __device__(int slot, u64 i64) {
       const u32 i = u32(i64), q1 = i / DH, j = i - q1 * DH, q2 = q1 / H, h = q1 - q2 * H, b = q2 / Tt, t = q2 - b * Tt;
-      dst.p[slot][i] = sar64(src.p[slot][((u64(b) * H + h) * Tt + t) * DH + j], f);
+      sel(dst, slot)[i] = sar64(sel(src, slot)[((u64(b) * H + h) * Tt + t) * DH + j], f);
     });
   }
   DT out = weight_matmul(proj_op, merged, nullptr, false, Shape{B * T, d}, addend);
@@ -485,8 +485,8 @@ DT SecureExecutor::run_layer(const LayerSpec& l, const DT& x, const Shape& in_sh
       launch_ew(s_.stream, s_.n_local, B * d, [=] __device__(int slot, u64 i) {
         const u64 b = i / D, j = i - b * D;
         u64 acc = 0;
-        for (u64 t = 0; t < Tt; ++t) acc += xp.p[slot][(b * Tt + t) * D + j];
-        op.p[slot][i] = sar64(acc * k, f);
+        for (u64 t = 0; t < Tt; ++t) acc += sel(xp, slot)[(b * Tt + t) * D + j];
+        sel(op, slot)[i] = sar64(acc * k, f);
       });
       return out;
     }

@@ -16,17 +16,17 @@ namespace {
 struct SrcSubRow {  // x[g] - mu[g / d]
   CPtr2 x, mu;
   u32 d;
-  __device__ u64 operator()(int slot, u64 g) const { return x.p[slot][g] - mu.p[slot][g / d]; }
+  __device__ u64 operator()(int slot, u64 g) const { return sel(x, slot)[g] - sel(mu, slot)[g / d]; }
 };
 struct SrcRowB {  // y[g / d]
   CPtr2 y;
   u32 d;
-  __device__ u64 operator()(int slot, u64 g) const { return y.p[slot][g / d]; }
+  __device__ u64 operator()(int slot, u64 g) const { return sel(y, slot)[g / d]; }
 };
 struct SrcColB {  // v[g % d]
   CPtr2 v;
   u32 d;
-  __device__ u64 operator()(int slot, u64 g) const { return v.p[slot][g % d]; }
+  __device__ u64 operator()(int slot, u64 g) const { return sel(v, slot)[g % d]; }
 };
 struct OutScaleRescale {  // out[r] = sar(acc * k, f) (+ [p0] add)
   Pid2 pid;
@@ -34,7 +34,7 @@ struct OutScaleRescale {  // out[r] = sar(acc * k, f) (+ [p0] add)
   u64 k, add;
   int f;
   __device__ void operator()(int slot, u64 r, u64 acc) const {
-    out.p[slot][r] = sar64(acc * k, f) + (pid.v[slot] == 0 ? add : 0);
+    sel(out, slot)[r] = sar64(acc * k, f) + (pid.v[slot] == 0 ? add : 0);
   }
 };
 // Round policy of the fused inverse-sqrt Newton chain (oracle inv_sqrt_shares):
@@ -52,11 +52,11 @@ struct IsqrtPV {
     if (phase == 0) return sar64(z, f);
     if (phase == 1) return (party == 0 ? three : 0) - sar64(z, f);
     const u64 yy = sar64(z, f + 1);
-    y.p[slot][g] = yy;
+    sel(y, slot)[g] = yy;
     return yy;
   }
   __device__ u64 nx(int slot, u64 g, u64 val) const {
-    return phase == 0 ? v.p[slot][g] : (phase == 1 ? y.p[slot][g] : val);
+    return phase == 0 ? sel(v, slot)[g] : (phase == 1 ? sel(y, slot)[g] : val);
   }
   __device__ u64 ny(int, u64, u64 val) const { return val; }
 };
@@ -66,7 +66,7 @@ struct SinkTruncAddCol {  // out = sar(z, f) + beta[g % d]
   int f;
   u32 d;
   __device__ void operator()(int slot, int, u64 g, u64 z) const {
-    out.p[slot][g] = sar64(z, f) + beta.p[slot][g % d];
+    sel(out, slot)[g] = sar64(z, f) + sel(beta, slot)[g % d];
   }
 };
 
@@ -82,7 +82,7 @@ DT gelu_shares(Session& s, const DT& x, const std::string& tag) {
   {
     const CPtr2 xp = cptrs(x);
     const Ptr2 zp = ptrs(z);
-    launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) { zp.p[slot][i] = sar64(xp.p[slot][i] * k, f); });
+    launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) { sel(zp, slot)[i] = sar64(sel(xp, slot)[i] * k, f); });
   }
   DT sg = sigmoid_shares(s, z, tag + ".sig");
   Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Arith, x.shape), tag + ".out");
@@ -104,7 +104,7 @@ DT inv_sqrt_shares(Session& s, const DT& v, const std::string& tag, int newton_i
     const CPtr2 vp = cptrs(v);
     const Ptr2 tp = ptrs(t0);
     launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) {
-      tp.p[slot][i] = (pid.v[slot] == 0 ? u64(0) - c02 : 0) - sar64(vp.p[slot][i], 1);
+      sel(tp, slot)[i] = (pid.v[slot] == 0 ? u64(0) - c02 : 0) - sar64(sel(vp, slot)[i], 1);
     });
   }
   DT e = exp_shares(s, t0, tag + ".seed");
@@ -113,7 +113,7 @@ DT inv_sqrt_shares(Session& s, const DT& v, const std::string& tag, int newton_i
     const CPtr2 ep = cptrs(e), vp = cptrs(v);
     const Ptr2 yp = ptrs(y);
     launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) {
-      yp.p[slot][i] = (sar64(ep.p[slot][i] * c22, f) - sar64(vp.p[slot][i], 10)) + (pid.v[slot] == 0 ? c02 : 0);
+      sel(yp, slot)[i] = (sar64(sel(ep, slot)[i] * c22, f) - sar64(sel(vp, slot)[i], 10)) + (pid.v[slot] == 0 ? c02 : 0);
     });
   }
   if (newton_iters <= 0) return y;
@@ -176,7 +176,7 @@ DT layernorm_shares(Session& s, const DT& x, size_t d, const DT& gamma, const DT
     const Ptr2 op = ptrs(out);
     launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) {
       const u32 c = u32(i % D);
-      op.p[slot][i] = sar64(np.p[slot][i] * gp.p[slot][c], f) + (pid.v[slot] == 0 ? bp.p[slot][c] : 0);
+      sel(op, slot)[i] = sar64(sel(np, slot)[i] * sel(gp, slot)[c], f) + (pid.v[slot] == 0 ? sel(bp, slot)[c] : 0);
     });
   } else {
     Triple t = s.fetch(TripleSpec::elementwise(TripleKind::Arith, Shape{rows, d}), tag + ".gamma");

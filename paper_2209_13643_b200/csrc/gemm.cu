@@ -534,7 +534,7 @@ static void delta_build(Session& s, const Triple& t, size_t nb, Open& o, YF yf) 
     return;
   }
   launch_ew(s.stream, s.n_local, nb, [=] __device__(int slot, u64 j) {
-    own.p[slot][j] = yf(slot, j) - mm_b_share(mm, pid.v[slot], j);
+    sel(own, slot)[j] = yf(slot, j) - mm_b_share(mm, pid.v[slot], j);
   });
 }
 
@@ -577,7 +577,7 @@ void eps_build_mem(Session& s, const Triple& t, const u64* const x[2], size_t a_
     return;
   }
   launch_ew(s.stream, s.n_local, na, [=] __device__(int slot, u64 j) {
-    own.p[slot][j] = xp.p[slot][a_off + j] - a_share_out(mm, pid.v[slot], a_off + j, ap.p[slot], j, na);
+    sel(own, slot)[j] = sel(xp, slot)[a_off + j] - a_share_out(mm, pid.v[slot], a_off + j, sel(ap, slot), j, na);
   });
 }
 
@@ -810,8 +810,8 @@ void eps_build_im2col(Session& s, const Triple& t, const u64* const x[2], const 
     const int ih = int(oh * g.stride + ki) - int(g.pad), iw = int(ow * g.stride + kj) - int(g.pad);
     u64 v = 0;
     if (ih >= 0 && iw >= 0 && ih < int(g.H) && iw < int(g.W))
-      v = xp.p[slot][((u64(n) * g.C + ci) * g.H + u32(ih)) * g.W + u32(iw)];
-    own.p[slot][j] = v - a_share_out(mm, pid.v[slot], idx, ap.p[slot], j, na);
+      v = sel(xp, slot)[((u64(n) * g.C + ci) * g.H + u32(ih)) * g.W + u32(iw)];
+    sel(own, slot)[j] = v - a_share_out(mm, pid.v[slot], idx, sel(ap, slot), j, na);
   });
 }
 

@@ -303,6 +303,10 @@ void socket_reap(Session& s, bool all) {
 // device barrier so a replay never overwrites an inbox the peer is still reading.
 namespace {
 constexpr u32 kFlagRing = 1u << 16;
+// per party: [0, kFlagRing) collective flags, [kFlagRing] replay-barrier word, then from
+// kReadyOff a second ring: "my inbox for collective s is free to overwrite" (see p2p_post)
+constexpr u32 kReadyOff = kFlagRing + 8;
+constexpr u32 kFlagWords = kReadyOff + kFlagRing;
 
 // The sequence number of a collective in this run: the baked capture-time number plus one run's
 // worth of collectives per replay after the first. Both the flag SLOT and its value derive from
@@ -384,8 +388,8 @@ void p2p_connect(Session& a, Session& b) {
     const int p = s->party_of[0];
     L->device[p] = s->device;
     MPCG_CUDA(cudaSetDevice(s->device));
-    MPCG_CUDA(cudaMalloc(&L->flags[p], (kFlagRing + 1) * sizeof(u64)));
-    MPCG_CUDA(cudaMemset(L->flags[p], 0, (kFlagRing + 1) * sizeof(u64)));
+    MPCG_CUDA(cudaMalloc(&L->flags[p], kFlagWords * sizeof(u64)));
+    MPCG_CUDA(cudaMemset(L->flags[p], 0, kFlagWords * sizeof(u64)));
   }
   if (a.device != b.device) {  // peer stores over NVLink both ways
     for (auto [x, y] : {std::pair<int, int>{a.device, b.device}, {b.device, a.device}}) {
@@ -434,6 +438,16 @@ void p2p_post(Session& s, Open& o) {
   const u64* it = s.cap.active ? s.cap.iter : nullptr;
   const u64* dl = s.cap.active ? s.cap.seqd : nullptr;
   if (o.n) {
+    // Inbox reuse: this party's inbox for seq may be pool memory whose previous reader (the
+    // consumer of an earlier collective) is queued on this party's compute stream but has not
+    // run yet; the peer pushes from ITS comm stream, which nothing orders behind that reader.
+    // So publish "inbox free" from the compute stream (after everything queued so far) and
+    // let the push wait for the peer's.
+    p2p_signal_kernel<<<1, 1, 0, s.stream>>>(L.flags[1 - me] + kReadyOff, o.seq, it, dl);
+    MPCG_CUDA(cudaGetLastError());
+    p2p_wait_kernel<<<1, 1, 0, s.comm_stream>>>(L.flags[me] + kReadyOff, o.seq, it, dl);
+    MPCG_CUDA(cudaGetLastError());
+    g_launches.fetch_add(2);
     u64 blocks = (o.n / 2 + 255) / 256;
     const u64 cap = u64(num_sms()) * 2;
     blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);

@@ -276,20 +276,20 @@ void dealer_fetch(Session& s, const TripleSpec& spec, const std::string& tag, DT
     launch_ew(s.stream, s.n_local, z.na, [=] __device__(int slot, u64 i) {
       u64 x, y, w;
       ew_abc(T, pid.v[slot], T.off + i, x, y, w);
-      ap.p[slot][i] = x;
-      bp.p[slot][i] = y;
-      cp.p[slot][i] = w;
+      sel(ap, slot)[i] = x;
+      sel(bp, slot)[i] = y;
+      sel(cp, slot)[i] = w;
     });
     return;
   }
   const MmTriple mm = t.mm;
   launch_ew(s.stream, s.n_local, z.na, [=] __device__(int slot, u64 i) {
     const u64 ra = mm_rA(mm, i);
-    ap.p[slot][i] = pid.v[slot] ? ra : mm_A(mm, i) - ra;
+    sel(ap, slot)[i] = pid.v[slot] ? ra : mm_A(mm, i) - ra;
   });
   launch_ew(s.stream, s.n_local, z.nb, [=] __device__(int slot, u64 j) {
     const u64 rb = mm_rB(mm, j);
-    bp.p[slot][j] = pid.v[slot] ? rb : mm_B(mm, j) - rb;
+    sel(bp, slot)[j] = pid.v[slot] ? rb : mm_B(mm, j) - rb;
   });
   // c: party 1 = r_C; party 0 = A*B - r_C (one-segment ring GEMM with dealer-drawn operands)
   const u64 K = spec.shape_a.back(), M = spec.shape_a[spec.shape_a.size() - 2];
@@ -323,7 +323,7 @@ void dealer_fetch(Session& s, const TripleSpec& spec, const std::string& tag, DT
   const bool all_p1 = s.n_local == 1 && s.party_of[0] == 1;
   if (all_p1) {
     const u64 nc = z.nc;
-    launch_ew(s.stream, 1, nc, [=] __device__(int slot, u64 k) { cp.p[slot][k] = mm_rC(mm, k); });
+    launch_ew(s.stream, 1, nc, [=] __device__(int slot, u64 k) { sel(cp, slot)[k] = mm_rC(mm, k); });
     return;
   }
   if (s.n_local == 2) {  // party 1's slot: r_C directly; the GEMM runs party 0's slot only

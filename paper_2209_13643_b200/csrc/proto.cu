@@ -68,7 +68,7 @@ DT add_public(Session& s, const DT& x, u64 v) {
   const CPtr2 xp = cptrs(x);
   const Ptr2 zp = ptrs(z);
   launch_ew(s.stream, s.n_local, x.numel(), [=] __device__(int slot, u64 i) {
-    zp.p[slot][i] = xp.p[slot][i] + (pid.v[slot] == 0 ? v : 0);
+    sel(zp, slot)[i] = sel(xp, slot)[i] + (pid.v[slot] == 0 ? v : 0);
   });
   return z;
 }
@@ -77,7 +77,7 @@ DT scale_public(Session& s, const DT& x, u64 k) {
   DT z = s.alloc(x.shape, x.scale);
   const CPtr2 xp = cptrs(x);
   const Ptr2 zp = ptrs(z);
-  launch_ew(s.stream, s.n_local, x.numel(), [=] __device__(int slot, u64 i) { zp.p[slot][i] = xp.p[slot][i] * k; });
+  launch_ew(s.stream, s.n_local, x.numel(), [=] __device__(int slot, u64 i) { sel(zp, slot)[i] = sel(xp, slot)[i] * k; });
   return z;
 }
 
@@ -87,7 +87,7 @@ DT sub_t(Session& s, const DT& a, const DT& b) {
   const CPtr2 ap = cptrs(a), bp = cptrs(b);
   const Ptr2 zp = ptrs(z);
   launch_ew(s.stream, s.n_local, a.numel(),
-            [=] __device__(int slot, u64 i) { zp.p[slot][i] = ap.p[slot][i] - bp.p[slot][i]; });
+            [=] __device__(int slot, u64 i) { sel(zp, slot)[i] = sel(ap, slot)[i] - sel(bp, slot)[i]; });
   return z;
 }
 
@@ -97,7 +97,7 @@ DT add_t(Session& s, const DT& a, const DT& b) {
   const CPtr2 ap = cptrs(a), bp = cptrs(b);
   const Ptr2 zp = ptrs(z);
   launch_ew(s.stream, s.n_local, a.numel(),
-            [=] __device__(int slot, u64 i) { zp.p[slot][i] = ap.p[slot][i] + bp.p[slot][i]; });
+            [=] __device__(int slot, u64 i) { sel(zp, slot)[i] = sel(ap, slot)[i] + sel(bp, slot)[i]; });
   return z;
 }
 
@@ -107,7 +107,7 @@ DT truncate_shares(Session& s, const DT& x, int bits) {
   const CPtr2 xp = cptrs(x);
   const Ptr2 zp = ptrs(z);
   launch_ew(s.stream, s.n_local, x.numel(),
-            [=] __device__(int slot, u64 i) { zp.p[slot][i] = sar64(xp.p[slot][i], bits); });
+            [=] __device__(int slot, u64 i) { sel(zp, slot)[i] = sar64(sel(xp, slot)[i], bits); });
   return z;
 }
 
@@ -118,15 +118,15 @@ DT open_value(Session& s, const DT& x, Reduce kind, const std::string& tag) {
   Open o = s.begin_open(n, kind);
   const Ptr2 own = own_ptrs(o);
   const CPtr2 xp = cptrs(x);
-  launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) { own.p[slot][i] = xp.p[slot][i]; });
+  launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) { sel(own, slot)[i] = sel(xp, slot)[i]; });
   s.post(o, tag);
   s.wait(o);
   const CPtr2 ow = as_const(own_ptrs(o)), pe = peer_ptrs(o);
   const Ptr2 zp = ptrs(z);
   const int xr = kind == Reduce::Xor;
   launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) {
-    const u64 a = ow.p[slot][i], b = pe.p[slot][i];
-    zp.p[slot][i] = xr ? (a ^ b) : (a + b);
+    const u64 a = sel(ow, slot)[i], b = sel(pe, slot)[i];
+    sel(zp, slot)[i] = xr ? (a ^ b) : (a + b);
   });
   s.check();
   return z;
@@ -163,8 +163,8 @@ struct AndBuild {
     const u64 g = lo + j;
     u64 a, b;
     ew_ab(T, pid.v[slot], T.off + g, a, b);
-    own.p[slot][j] = xf(slot, g) ^ a;
-    own.p[slot][w + j] = yf(slot, g) ^ b;
+    sel(own, slot)[j] = xf(slot, g) ^ a;
+    sel(own, slot)[w + j] = yf(slot, g) ^ b;
   }
 };
 struct AndCombine {
@@ -176,13 +176,13 @@ struct AndCombine {
   __device__ void operator()(int slot, u64 j) const {
     const int party = pid.v[slot];
     const u64 g = lo + j;
-    const u64 e = own.p[slot][j] ^ peer.p[slot][j];
-    const u64 d = own.p[slot][w + j] ^ peer.p[slot][w + j];
+    const u64 e = sel(own, slot)[j] ^ sel(peer, slot)[j];
+    const u64 d = sel(own, slot)[w + j] ^ sel(peer, slot)[w + j];
     u64 a, b, c;
     ew_abc(T, party, T.off + g, a, b, c);
     u64 z = c ^ (e & b) ^ (d & a);
     if (party == 0) z ^= e & d;
-    out.p[slot][g] = z;
+    sel(out, slot)[g] = z;
   }
 };
 }  // namespace
@@ -231,14 +231,14 @@ struct PartX {
   Pid2 pid;
   CPtr2 keep, peer;
   __device__ u64 operator()(int slot, u64 g) const {
-    return pid.v[slot] == 0 ? keep.p[slot][g] : peer.p[slot][g];
+    return pid.v[slot] == 0 ? sel(keep, slot)[g] : sel(peer, slot)[g];
   }
 };
 struct PartY {
   Pid2 pid;
   CPtr2 keep, peer;
   __device__ u64 operator()(int slot, u64 g) const {
-    return pid.v[slot] == 0 ? peer.p[slot][g] : keep.p[slot][g];
+    return pid.v[slot] == 0 ? sel(peer, slot)[g] : sel(keep, slot)[g];
   }
 };
 
@@ -252,8 +252,8 @@ DT a2b_mask(Session& s, size_t n, XF xf, Open& o) {
   const u64 k0 = s.mask_key[0], k1 = s.mask_key[1];
   launch_ew(s.stream, s.n_local, n, [=] __device__(int slot, u64 i) {
     const u64 r = drw(slot == 0 ? k0 : k1, tkey(mr.base, mr.bp) + 1 + i);
-    own.p[slot][i] = r;
-    kp.p[slot][i] = xf(slot, i) ^ r;
+    sel(own, slot)[i] = r;
+    sel(kp, slot)[i] = xf(slot, i) ^ r;
   });
   s.post(o, "", /*p2p=*/true);
   s.wait(o);
@@ -292,7 +292,7 @@ struct A2bPart {
   int fused;
   __device__ u64 operator()(int slot, u64 g) const {
     if (fused) return MaskedPart<XF>{pid, k0, k1, mr, xf, y}(slot, g);
-    return (pid.v[slot] == 0) == (y == 0) ? keep.p[slot][g] : peer.p[slot][g];
+    return (pid.v[slot] == 0) == (y == 0) ? sel(keep, slot)[g] : sel(peer, slot)[g];
   }
 };
 
@@ -320,18 +320,18 @@ void a2b_op(Session& s, size_t n, const AdderOptions& opt, const std::string& ta
 struct BitAcc {
   Pid2 pid;
   CPtr2 b;
-  __device__ u64 operator()(int slot, u64 g) const { return pid.v[slot] == 0 ? (b.p[slot][g] & 1) : 0; }
+  __device__ u64 operator()(int slot, u64 g) const { return pid.v[slot] == 0 ? (sel(b, slot)[g] & 1) : 0; }
 };
 struct BitBq {
   Pid2 pid;
   CPtr2 b;
-  __device__ u64 operator()(int slot, u64 g) const { return pid.v[slot] == 1 ? (b.p[slot][g] & 1) : 0; }
+  __device__ u64 operator()(int slot, u64 g) const { return pid.v[slot] == 1 ? (sel(b, slot)[g] & 1) : 0; }
 };
 struct B2aSink {
   CPtr2 b;
   Ptr2 out;
   __device__ void operator()(int slot, int, u64 g, u64 prod) const {
-    out.p[slot][g] = (b.p[slot][g] & 1) - (prod + prod);
+    sel(out, slot)[g] = (sel(b, slot)[g] & 1) - (prod + prod);
   }
 };
 
@@ -344,11 +344,11 @@ struct B2aBuildFF {
   bool opened = false;  // pair evaluation: the opened (eps, delta) once in slot 0's outbox
   __device__ void operator()(int slot, int party, u64 g, u64 j, u64 sum) const {
     const u64 bit = sum >> 63;
-    bits.p[slot][g] = bit;
+    sel(bits, slot)[g] = bit;
     u64 a, b;
     ew_ab(T, party, T.off + g, a, b);
-    own.p[slot][j] = (party == 0 ? bit : 0) - a;      // eps = acc - a
-    own.p[slot][w + j] = (party == 1 ? bit : 0) - b;  // delta = bq - b
+    sel(own, slot)[j] = (party == 0 ? bit : 0) - a;      // eps = acc - a
+    sel(own, slot)[w + j] = (party == 1 ? bit : 0) - b;  // delta = bq - b
   }
   // both parties (sum_k = party k's, q0 = slot of party 0)
   __device__ void pair(int q0, u64 g, u64 j, u64 sum0, u64 sum1) const {
@@ -358,8 +358,8 @@ struct B2aBuildFF {
       return;
     }
     const u64 bit0 = sum0 >> 63, bit1 = sum1 >> 63;
-    bits.p[q0][g] = bit0;
-    bits.p[1 - q0][g] = bit1;
+    sel(bits, q0)[g] = bit0;
+    sel(bits, 1 - q0)[g] = bit1;
     const Dw d = ew_secrets(T, T.off + g);  // eps0 + eps1 = bit0 - A, delta0 + delta1 = bit1 - B
     own.p[0][j] = bit0 - d.A;
     own.p[0][w + j] = bit1 - d.B;
@@ -376,13 +376,13 @@ struct MulByBitBuild {
   Ptr2 cout;  // optional: keep the arithmetic bit c (sigmoid's select reuses it)
   bool opened = false;  // pair evaluation: the opened (eps, delta) once in slot 0's outbox
   __device__ void operator()(int slot, int party, u64 g, u64 prod) const {
-    const u64 c = (bits.p[slot][g] & 1) - (prod + prod);
-    if (cout.p[slot]) cout.p[slot][g] = c;
+    const u64 c = (sel(bits, slot)[g] & 1) - (prod + prod);
+    if (sel(cout, slot)) sel(cout, slot)[g] = c;
     const u64 j = g - lo;
     u64 a, b;
     ew_ab(T, party, T.off + g, a, b);
-    own.p[slot][j] = uf(slot, g) - a;
-    own.p[slot][w + j] = c - b;
+    sel(own, slot)[j] = uf(slot, g) - a;
+    sel(own, slot)[w + j] = c - b;
   }
   __device__ void pair(int q0, u64 g, u64 prod0, u64 prod1) const {
     if (!opened) {
@@ -391,9 +391,9 @@ struct MulByBitBuild {
       return;
     }
     const int q1 = 1 - q0;
-    const u64 c0 = (bits.p[q0][g] & 1) - (prod0 + prod0), c1 = (bits.p[q1][g] & 1) - (prod1 + prod1);
-    if (cout.p[q0]) cout.p[q0][g] = c0;
-    if (cout.p[q1]) cout.p[q1][g] = c1;
+    const u64 c0 = (sel(bits, q0)[g] & 1) - (prod0 + prod0), c1 = (sel(bits, q1)[g] & 1) - (prod1 + prod1);
+    if (sel(cout, q0)) sel(cout, q0)[g] = c0;
+    if (sel(cout, q1)) sel(cout, q1)[g] = c1;
     const u64 j = g - lo;
     const Dw d = ew_secrets(T, T.off + g);  // the masks cancel in the open
     own.p[0][j] = uf(q0, g) + uf(q1, g) - d.A;
@@ -414,8 +414,8 @@ struct MaskRound {
   XF xf;
   __device__ void operator()(int slot, u64 i) const {
     const u64 r = drw(slot == 0 ? k0 : k1, tkey(mr.base, mr.bp) + 1 + i);
-    own.p[slot][i] = r;
-    keep.p[slot][i] = xf(slot, i) ^ r;
+    sel(own, slot)[i] = r;
+    sel(keep, slot)[i] = xf(slot, i) ^ r;
   }
 };
 
@@ -871,7 +871,7 @@ DT max_last_dim(Session& s, const DT& x, size_t L, const std::string& tag) {
       const Ptr2 np = ptrs(next);
       const u32 LEN = u32(len), NW = u32(nw), HH = u32(h);
       launch_ew(s.stream, s.n_local, outer, [=] __device__(int slot, u64 o) {
-        np.p[slot][o * NW + HH] = cp.p[slot][o * LEN + LEN - 1];
+        sel(np, slot)[o * NW + HH] = sel(cp, slot)[o * LEN + LEN - 1];
       });
     }
     // gate = less_than(a, b) (tags rt.msb.add1.*, rt.b2a.m1); pick = (b - a) * gate (rt.pick)
@@ -909,13 +909,13 @@ struct SarOf {  // w = trunc(x, it), the first squared value
 };
 struct OutStore {  // out[g] = y
   Ptr2 out;
-  __device__ void operator()(int slot, int, u64 g, u64 y) const { out.p[slot][g] = y; }
+  __device__ void operator()(int slot, int, u64 g, u64 y) const { sel(out, slot)[g] = y; }
 };
 struct OutAffine {  // out[g] = k*y + [p0] c   (reciprocal seed 3 exp + 0.003; sigmoid's 1 + exp)
   Ptr2 out;
   u64 k, c;
   __device__ void operator()(int slot, int party, u64 g, u64 y) const {
-    out.p[slot][g] = y * k + (party == 0 ? c : 0);
+    sel(out, slot)[g] = y * k + (party == 0 ? c : 0);
   }
 };
 struct OutRecipSeed {  // d = y + [p0] 1; seed = [p0] c0 - trunc(d * c1, f)
@@ -924,15 +924,15 @@ struct OutRecipSeed {  // d = y + [p0] 1; seed = [p0] c0 - trunc(d * c1, f)
   int f;
   __device__ void operator()(int slot, int party, u64 g, u64 y) const {
     const u64 dv = y + (party == 0 ? one : 0);
-    d.p[slot][g] = dv;
-    seed.p[slot][g] = (party == 0 ? c0 : 0) - sar64(dv * c1, f);
+    sel(d, slot)[g] = dv;
+    sel(seed, slot)[g] = (party == 0 ? c0 : 0) - sar64(dv * c1, f);
   }
 };
 struct SrcConstMinus {  // [p0] c - x[g]   (reciprocal seed argument 0.5 - x)
   Pid2 pid;
   CPtr2 x;
   u64 c;
-  __device__ u64 operator()(int slot, u64 g) const { return (pid.v[slot] == 0 ? c : 0) - x.p[slot][g]; }
+  __device__ u64 operator()(int slot, u64 g) const { return (pid.v[slot] == 0 ? c : 0) - sel(x, slot)[g]; }
 };
 
 template <class XF, class OF>
@@ -971,10 +971,10 @@ struct RecipPV {
   __device__ u64 val(int slot, int party, u64 g, u64 z) const {
     if (!odd) return (party == 0 ? (u64(2) << f) : 0) - sar64(z, f);
     const u64 v = sar64(z, f);
-    y.p[slot][g] = v;
+    sel(y, slot)[g] = v;
     return v;
   }
-  __device__ u64 nx(int slot, u64 g, u64) const { return odd ? x.p[slot][g] : y.p[slot][g]; }
+  __device__ u64 nx(int slot, u64 g, u64) const { return odd ? sel(x, slot)[g] : sel(y, slot)[g]; }
   __device__ u64 ny(int, u64, u64 v) const { return v; }
 };
 }  // namespace
@@ -1020,18 +1020,18 @@ namespace {
 struct SrcSubRowMax {  // x[g] - m[g / L]
   CPtr2 x, m;
   u32 L;
-  __device__ u64 operator()(int slot, u64 g) const { return x.p[slot][g] - m.p[slot][u32(g) / L]; }
+  __device__ u64 operator()(int slot, u64 g) const { return sel(x, slot)[g] - sel(m, slot)[u32(g) / L]; }
 };
 struct SrcBcast {  // r[g / L]
   CPtr2 r;
   u32 L;
-  __device__ u64 operator()(int slot, u64 g) const { return r.p[slot][u32(g) / L]; }
+  __device__ u64 operator()(int slot, u64 g) const { return sel(r, slot)[u32(g) / L]; }
 };
 }  // namespace
 
 struct OutRowStore {  // out[r] = acc
   Ptr2 out;
-  __device__ void operator()(int slot, u64 r, u64 acc) const { out.p[slot][r] = acc; }
+  __device__ void operator()(int slot, u64 r, u64 acc) const { sel(out, slot)[r] = acc; }
 };
 
 DT softmax_shares(Session& s, const DT& x, size_t L, const std::string& tag) {
@@ -1068,7 +1068,7 @@ DT maxpool2d_shares(Session& s, const DT& x, size_t N, size_t C, size_t H, size_
       const u32 ki = t / K, kj = t - ki * K;
       const u32 ow = r % OWw, oh = (r / OWw) % OHh, nc = r / (OWw * OHh);
       const u64 src = (u64(nc) * HH + oh * S + ki) * WW + ow * S + kj;
-      wp.p[slot][i] = xp.p[slot][src];
+      sel(wp, slot)[i] = sel(xp, slot)[src];
     });
   }
   DT mx = max_last_dim(s, win, k * k, tag);
@@ -1094,13 +1094,13 @@ struct SrcOneMinus2 {  // [p0] 2^f - 2 r
   CPtr2 r;
   u64 one;
   __device__ u64 operator()(int slot, u64 g) const {
-    return (pid.v[slot] == 0 ? one : 0) - (r.p[slot][g] + r.p[slot][g]);
+    return (pid.v[slot] == 0 ? one : 0) - (sel(r, slot)[g] + sel(r, slot)[g]);
   }
 };
 struct SinkAddTo {  // out = r + z
   CPtr2 r;
   Ptr2 out;
-  __device__ void operator()(int slot, int, u64 g, u64 z) const { out.p[slot][g] = r.p[slot][g] + z; }
+  __device__ void operator()(int slot, int, u64 g, u64 z) const { sel(out, slot)[g] = sel(r, slot)[g] + z; }
 };
 }  // namespace
 
