@@ -464,14 +464,13 @@ __global__ void __launch_bounds__(kThreads, 1) ring_gemm_tc2(const __grid_consta
 // transposed, (b*sR + row*K + k).
 template <int BR>
 __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows, u32 nbatch, u32 nkb, char* out0,
-                                                  char* out1, u32 mask0, u32 mask1) {
+                                                  char* out1, u32 mask0, u32 mask1, int both) {
   pdl_enter();
-  const int slot = blockIdx.y;  // every local slot in one launch
-  char* out = slot ? out1 : out0;
+  // every local slot in one launch: one slot per grid row, or (both: the pair combine's right
+  // operand, one dealer stream and one F) both slots per thread, B / r_B drawn and F read once
+  const int slot = both ? 0 : int(blockIdx.y);
   const GemmSlotArgs& S = a.sl[slot];
-  // packed segments: all (right operand, full left pack) or the masked ones (hybrid left)
-  const u32 smask = (slot ? mask1 : mask0) & ((1u << S.nseg) - 1);
-  const u32 K = a.K, N = a.N, nseg = u32(__popc(smask));
+  const u32 K = a.K, N = a.N;
   const u32 tiles = (rows + BR - 1) / BR;
   // unit = 4 K-consecutive values of one row for EVERY packed segment of the slot: one 4-byte
   // word in each limb plane of each segment. The dealer draws (A, r_A / B, r_B) and the
@@ -480,17 +479,18 @@ __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows
   const u32 units = nbatch * tiles * nkb * BR * 8;
   constexpr u32 plane = BR * kKB;
   bool dA = false, dRA = false, dB = false, dRB = false, dF = false;
-  int fseg = 0;
-  for (u32 g = 0; g < u32(S.nseg); ++g) {
-    if (!((smask >> g) & 1u)) continue;
-    const int k = left ? S.lk[g] : S.rk[g];
+  int fseg = 0, fslot = slot;
+  for (int sl = slot; sl < slot + (both ? 2 : 1); ++sl)
+  for (u32 g = 0; g < u32(a.sl[sl].nseg); ++g) {
+    if (!(((sl ? mask1 : mask0) >> g) & 1u)) continue;
+    const int k = left ? a.sl[sl].lk[g] : a.sl[sl].rk[g];
     if (left) {
       dA |= k == kOpA || k == kOpA0;
       dRA |= k == kOpRA || k == kOpA0;
     } else {
       dB |= k == kOpB || k == kOpB0F || k == kOpBF;
       dRB |= k == kOpRB || k == kOpB0F;
-      if (k == kOpSum || k == kOpB0F || k == kOpBF || k == kOpNegSum) dF = true, fseg = int(g);
+      if (k == kOpSum || k == kOpB0F || k == kOpBF || k == kOpNegSum) dF = true, fseg = int(g), fslot = sl;
     }
   }
   // Unit order: when the source rows are K-contiguous (left operand, transposed right operand)
@@ -536,17 +536,23 @@ __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows
         } else {
           if (dB) A[i] = mm_B(S.mm, S.boff + idx[i]);
           if (dRB) RA[i] = mm_rB(S.mm, S.boff + idx[i]);
-          if (dF) F[i] = load_f(S, fseg, idx[i]);
+          if (dF) F[i] = load_f(a.sl[fslot], fseg, idx[i]);
         }
       }
     }
-    const u64 img = (((u64(bb) * tiles + tile) * nkb + kb) * nseg) * 8 * plane;
     const u32 kc = kq / 4;  // which 16-byte K chunk of the core matrix
     // left: plane-major (one MMA A operand per plane); right: the 8 planes stacked along N
     // inside each K chunk, so planes 0..7-l form one B operand of N = (8-l)*BR rows
     const u32 off = left ? (kc * (BR / 8) + r / 8) * 128 + (r % 8) * 16 + (kq % 4) * 4
                          : kc * (BR * 128) + (r / 8) * 128 + (r % 8) * 16 + (kq % 4) * 4;
     const u32 pstride = left ? plane : BR * 16;
+    for (int sl = slot; sl < slot + (both ? 2 : 1); ++sl) {
+    const GemmSlotArgs& S = a.sl[sl];
+    char* out = sl ? out1 : out0;
+    // packed segments: all (right operand, full left pack) or the masked ones (hybrid left)
+    const u32 smask = (sl ? mask1 : mask0) & ((1u << S.nseg) - 1);
+    const u32 nseg = u32(__popc(smask));
+    const u64 img = (((u64(bb) * tiles + tile) * nkb + kb) * nseg) * 8 * plane;
     u32 gp = 0;
     for (int g = 0; g < S.nseg; ++g) {
       if (!((smask >> g) & 1u)) continue;
@@ -587,6 +593,7 @@ __global__ void __launch_bounds__(256) pack_limbs(GemmArgs a, int left, u32 rows
       }
       ++gp;
     }
+    }
   }
 }
 
@@ -608,6 +615,41 @@ int pair_combine_p0(const GemmArgs& a) {
   return p0;
 }
 
+bool pack_pair_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("MPCG_PACK_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+// both slots' right operands come from one dealer stream (B, r_B at the same offset and
+// stride) and one opened F (as (own, peer) of either slot)
+bool pair_same_right(const GemmArgs& a) {
+  const GemmSlotArgs& S0 = a.sl[0];
+  const GemmSlotArgs& S1 = a.sl[1];
+  if (S0.boff != S1.boff || S0.sR[0] != S1.sR[0] || S0.mm.key != S1.mm.key || S0.mm.kp != S1.mm.kp ||
+      S0.mm.pool != S1.mm.pool || S0.mm.pB != S1.mm.pB || S0.mm.prB != S1.mm.prB)
+    return false;
+  const u64* f0 = nullptr;
+  const u64* f1 = nullptr;
+  bool any = false;
+  for (int i = 0; i < 2; ++i)
+    for (int g = 0; g < a.sl[i].nseg; ++g) {
+      const int k = a.sl[i].rk[g];
+      if (k == kOpMem) return false;
+      if (k == kOpSum || k == kOpB0F || k == kOpBF || k == kOpNegSum) {
+        const u64* x0 = a.sl[i].R[g];
+        const u64* x1 = a.sl[i].R2[g];
+        if (!any) {
+          f0 = x0, f1 = x1, any = true;
+        } else if (!((x0 == f0 && x1 == f1) || (x1 && x0 == f1 && x1 == f0))) {
+          return false;
+        }
+      }
+    }
+  return true;
+}
+
 template <int BR>
 void launch_pack(Session& s, const GemmArgs& a, bool left, u32 rows, u32 nbatch, u32 nkb, char* out0, char* out1,
                  u32 mask0 = ~0u, u32 mask1 = ~0u) {
@@ -621,8 +663,10 @@ void launch_pack(Session& s, const GemmArgs& a, bool left, u32 rows, u32 nbatch,
   if (units * (maxseg > 0 ? 1 : 0) >= (u64(1) << 32)) throw Error(kShapeError, "tcgen05 pack: operand too large");
   cudaEvent_t pe;
   probe_begin(s.stream, &pe);
-  launch_pdl(pack_limbs<BR>, dim3(ew_blocks(units), a.nslots), dim3(256), 0, s.stream, a, left ? 1 : 0, rows, nbatch,
-             nkb, out0, out1, mask0, mask1);
+  // the pair combine's right operand: both slots per thread (one B / r_B draw and F load)
+  const int both = !left && pack_pair_on() && pair_combine_p0(a) >= 0 && pair_same_right(a) ? 1 : 0;
+  launch_pdl(pack_limbs<BR>, dim3(ew_blocks(units), both ? 1 : a.nslots), dim3(256), 0, s.stream, a, left ? 1 : 0,
+             rows, nbatch, nkb, out0, out1, mask0, mask1, both);
   probe_end(s.stream, pe);
 }
 
