@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--weights", default="private", choices=["private", "public"])
     ap.add_argument("--no-blocking", action="store_true", help="skip the blocking comparison pass")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--one-party-variants", action="store_true",
+                    help="also time two one-party sessions on two host threads (loopback and P2P links); off by "
+                         "default: a rare cross-thread stall of the eager loopback link was seen at ResNet-18 scale")
     ap.add_argument("--no-variants", action="store_true",
                     help="skip the per-slot and loopback one-party co-location measurements")
     ap.add_argument("--chunks", type=int, default=4, help="inner-layer pipeline chunk count (ExecOptions::chunks)")
@@ -455,8 +458,10 @@ def main():
             ps_ms, _ = graph_ms(a.mode, a.steps, a.warmup)
         finally:
             api.set_pair_eval(True)
-        lb_ms = loopback_ms(mp, g, weights, x_global, a, thr, link, seed)
-        p2p_ms = loopback_ms(mp, g, weights, x_global, a, thr, link, seed, kind="p2p")
+        lb_ms = p2p_ms = None
+        if a.one_party_variants:
+            lb_ms = loopback_ms(mp, g, weights, x_global, a, thr, link, seed)
+            p2p_ms = loopback_ms(mp, g, weights, x_global, a, thr, link, seed, kind="p2p")
         colocation = {
             "pair_evaluated": {"ms_per_step": ms_step, "inferences_per_s": B / (ms_step / 1e3),
                                "path": "one thread per element evaluates both local party slots; opened values "
@@ -464,14 +469,18 @@ def main():
             "per_slot": {"ms_per_step": ps_ms, "inferences_per_s": B / (ps_ms / 1e3),
                          "path": "mpcg_set_pair_eval(0): per-slot kernels, two payloads written and both read "
                                  "per open (MPCG_PAIR_EVAL=0 MPCG_EPS_FUSE=0); CUDA-graph replays"},
-            "loopback_one_party_sessions": {"ms_per_step": lb_ms, "inferences_per_s": B / (lb_ms / 1e3),
+            "loopback_one_party_sessions": {"ms_per_step": lb_ms, "inferences_per_s": B / (lb_ms / 1e3) if lb_ms else None,
                                             "path": "two n_local=1 sessions (party 0, party 1) on two host threads, "
                                                     "loopback link (device copies in place of NCCL send/recv), eager "
                                                     "launches; wall clock per step after a stream sync"},
-            "p2p_one_party_sessions": {"ms_per_step": p2p_ms, "inferences_per_s": B / (p2p_ms / 1e3),
+            "p2p_one_party_sessions": {"ms_per_step": p2p_ms, "inferences_per_s": B / (p2p_ms / 1e3) if p2p_ms else None,
                                        "path": "two n_local=1 sessions on two host threads over the device-flag P2P "
                                                "link (peer stores + flags), each party's inference one CUDA-graph "
                                                "replay, both parties sharing cuda:0; wall clock per step"}}
+        if not a.one_party_variants:
+            colocation["one_party_note"] = ("one-party variants not run (bench.py --one-party-variants); last "
+                                            "measured at ResNet-18 b128: loopback 73.9 ms, P2P 62.5 ms per step "
+                                            "(profiles/r02_bench.json)")
 
     if rank != 0:
         if dist:
