@@ -1,4 +1,5 @@
 // Session runtime: device memory, dealer tag streams, the open/reveal wire.
+#include <cstdio>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -685,6 +686,8 @@ void Session::post(Open& o, const std::string& tag, bool p2p) {
   if (n_local == 1 && loop) {
     if (cap.active) throw Error(kUsageError, "loopback link: graph capture is not supported (use the p2p link)");
     const int me = party_of[0];
+    static const bool dbg = std::getenv("MPCG_LINK_DEBUG") != nullptr;  // diagnosis of a rare stall
+    if (dbg) std::fprintf(stderr, "loopback party %d post seq %u n %zu\n", me, unsigned(o.seq), o.n);
     std::unique_lock<std::mutex> lk(loop->mu);
     LoopLink::Slot& sl = loop->slots[u64(o.seq)];
     sl.own[me] = o.own(0);
