@@ -373,12 +373,46 @@ struct SqCombine {
   }
 };
 
+// Pair evaluation with in-device opens (pair_chain_ok): the Beaver square of element g in one
+// pass (SqBuild's opened eps kept in a register, SqCombine's algebra), one draw set.
+template <class XF, class PF>
+struct SqFused {
+  EwTriple T;
+  Pid2 pid;
+  XF xf;
+  PF pf;
+  __device__ void operator()(int, u64) const {}  // pair evaluation only (launch_ew's both())
+  __device__ void both(u64 g) const {
+    const Sw d = sq_draw(T, T.off + g, true, true);
+    const u64 e = xf(0, g) + xf(1, g) - d.A;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int slot = pair_slot<2>(pid, 0, k);
+      u64 z = sq_share_c(k, d) + (e * sq_share_a(k, d)) * 2;
+      if (k == 0) z += e * e;
+      pf(slot, k, g, z);
+    }
+  }
+};
+
 template <class XF, class PF>
 void square_op(Session& s, const EwTriple& T, size_t m, int chunks, const std::string& tag, XF xf, PF pf) {
   chunks = clamp_chunks(chunks, m);
   const int acct = chunks;
   const int xl = acct > 1 && s.fuse_lanes() ? 1 : acct;  // lanes launched (Session::fuse_lanes)
   auto ltag = [&](int k) { return acct == 1 ? tag : tag + ".chunk" + std::to_string(k); };
+  if (m > 0 && pair_chain_ok(s)) {  // build + open + combine in one pass (SqFused)
+    {
+      ClassScope cs(kClsOther, 0);
+      launch_ew(s.stream, s.n_local, m, SqFused<XF, PF>{T, pids(s), xf, pf});
+    }
+    for (int k = 0; k < acct; ++k) {  // the opens, as post / post_lanes account them
+      const auto r = chunk_range(m, acct, k);
+      s.account(r.second - r.first, Reduce::Sum, ltag(k));
+    }
+    s.check();
+    return;
+  }
   std::vector<Open> opens(static_cast<size_t>(xl));
   const Pid2 pid = pids(s);
   // beaver_square = 2 x 8 B wire + 8 x (1 in + 1 out) = 32 B/elem/party over build + combine
